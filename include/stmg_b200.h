@@ -1,0 +1,197 @@
+/* stmg_b200 — B200-native space-time multigrid (STMG) solve, C ABI.
+ *
+ * This is the drop-in boundary for the reference's solver path
+ * (/root/reference/proj, namespace stmg).  Each entry point names the
+ * reference interface it replaces.  Plain pointers and sizes only; no C++ or
+ * torch types cross this boundary.  All arithmetic is IEEE fp64.
+ *
+ * Errors: every int-returning function returns STMG_OK (0) or one of the
+ * codes below; stmg_last_error() (thread-local) describes the last failure.
+ * The three exception classes the reference throws map to
+ *   std::invalid_argument -> STMG_EINVAL, std::runtime_error -> STMG_ERUNTIME,
+ *   std::out_of_range -> STMG_ERANGE.
+ * Non-convergence is data, not an error (stmg_solve_report.status), exactly
+ * as SolveStatus in proj/include/stmg/multigrid.hpp:79.
+ *
+ * Threading: one hierarchy handle must not be used from two threads at once;
+ * distinct handles are independent (proj/src/multigrid.cpp:228-239).
+ *
+ * Memory: b/u arguments of stmg_mg_solve may be host (pageable or pinned) or
+ * device pointers; the kind is detected.  Level-kernel entry points take
+ * device pointers to full level vectors in the reference's time-major layout
+ * flat = n * (n_el + 1) + i (proj/include/stmg/mesh.hpp:46-48).
+ */
+#ifndef STMG_B200_H
+#define STMG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STMG_ABI_VERSION 1
+
+enum stmg_status_code {
+  STMG_OK = 0,
+  STMG_EINVAL = 1,   /* std::invalid_argument */
+  STMG_ERUNTIME = 2, /* std::runtime_error */
+  STMG_ERANGE = 3,   /* std::out_of_range */
+  STMG_ECUDA = 4,    /* CUDA runtime / driver failure */
+  STMG_ENOMEM = 5    /* host or device allocation failure */
+};
+
+/* CoarseningDirection, proj/include/stmg/mesh.hpp:23 */
+enum stmg_direction { STMG_DIR_X = 0, STMG_DIR_T = 1, STMG_DIR_XT = 2 };
+/* ReassemblyMethod, proj/include/stmg/rediscretisation.hpp:36 */
+enum stmg_reassembly { STMG_REASM_K = 0, STMG_REASM_D = 1, STMG_REASM_R = 2, STMG_REASM_P = 3 };
+/* PlanStrategy, proj/include/stmg/strategy.hpp:74 */
+enum stmg_strategy {
+  STMG_PLAN_UNIFORM = 0,
+  STMG_PLAN_CONTRAST = 1,
+  STMG_PLAN_RESOLUTION = 2,
+  STMG_PLAN_DESIGN_INDEPENDENT = 3
+};
+/* SolveStatus, proj/include/stmg/multigrid.hpp:79 */
+enum stmg_solve_status { STMG_CONVERGED = 0, STMG_MAX_CYCLES = 1, STMG_DIVERGED = 2 };
+
+/* SpaceTimeGrid geometry, proj/include/stmg/mesh.hpp:27-37 (dx, dt derived). */
+typedef struct stmg_grid {
+  double L;
+  double t_T;
+  int64_t n_el;
+  int64_t n_t;
+} stmg_grid;
+
+/* MaterialPair, proj/include/stmg/materials.hpp:16-23 */
+typedef struct stmg_material_pair {
+  double k_ins, k_con, c_ins, c_con, p_k, p_c;
+} stmg_material_pair;
+
+/* PlanRequest, proj/include/stmg/strategy.hpp:76-86 (chi/mat passed separately). */
+typedef struct stmg_plan_request {
+  int32_t n_levels;
+  double lambda_crit;
+  int32_t strategy;   /* stmg_strategy */
+  int32_t reassembly; /* stmg_reassembly */
+  int64_t min_elements;
+} stmg_plan_request;
+
+/* SolveOptions, proj/include/stmg/multigrid.hpp:83-89 */
+typedef struct stmg_solve_options {
+  int32_t nu;
+  double omega;
+  double tol;
+  double div_tol;
+  int32_t max_cycles;
+} stmg_solve_options;
+
+/* SolveReport, proj/include/stmg/multigrid.hpp:91-102 (history is caller-allocated). */
+typedef struct stmg_solve_report {
+  int32_t status; /* stmg_solve_status */
+  int32_t cycles;
+  double factor;
+  int32_t absolute_norms;
+  int32_t n_history;           /* entries written to history (cycles + 1) */
+  double seconds;              /* wall time of the solve, as SolveReport.seconds */
+  double device_seconds;       /* device time between the first and last kernel (CUDA events) */
+  double smoother_dof_updates; /* sum over levels and cycles of Jacobi DOF updates */
+  int64_t kernel_launches;     /* kernels this solve launched (graph nodes counted) */
+} stmg_solve_report;
+
+typedef struct stmg_hierarchy stmg_hierarchy;
+
+const char* stmg_last_error(void);
+int stmg_abi_version(void);
+
+/* ---- host-side setup (proj/src/{materials,assembly,strategy}.cpp) ---------------- */
+
+/* apply_design, proj/include/stmg/materials.hpp:48-49 */
+int stmg_apply_design(const double* chi, int64_t n, const stmg_material_pair* mat, double* k_out,
+                      double* c_out);
+
+/* load_vector(g, q), proj/include/stmg/assembly.hpp:54-56, for the preset sources
+ * (kind 0 uniform, 1 mirrored box, 2 modulated mirrored box, 3 heat_load_value; see
+ * paper_2505_10168_b200/configs.py); masked != 0 zeroes fixed DOFs as
+ * assemble_system does (proj/src/assembly.cpp:128-130).  b is a host array of
+ * (n_t+1)(n_el+1) doubles. */
+int stmg_load_vector(const stmg_grid* g, int32_t kind, const double* params, int32_t masked,
+                     double* b);
+
+/* load_vector with a caller callback q(x, t, ctx) (the std::function overload). */
+typedef double (*stmg_source_fn)(double x, double t, void* ctx);
+int stmg_load_vector_cb(const stmg_grid* g, stmg_source_fn q, void* ctx, int32_t masked,
+                        double* b);
+
+/* plan_coarsening, proj/include/stmg/strategy.hpp:104-105.  k/c (n_el each) may be
+ * NULL only for DesignIndependent; chi/mat are needed by D reassembly and
+ * DesignIndependent.  dirs_out/indicator_out hold n_levels-1 entries. */
+int stmg_plan_coarsening(const stmg_grid* g, const double* k, const double* c, const double* chi,
+                         const stmg_material_pair* mat, const stmg_plan_request* req,
+                         int32_t* dirs_out, double* indicator_out);
+
+/* ---- hierarchy (proj/src/multigrid.cpp:86-160) ------------------------------------- */
+
+/* build_hierarchy, proj/include/stmg/multigrid.hpp:70-74.  method is the reference's
+ * two-letter name (parse_method, proj/include/stmg/rediscretisation.hpp:45); this
+ * build supports causal transfers with K, D or R reassembly ("CK", "CD", "CR").
+ * dirs: n_dirs coarsening directions (STMG_DIR_X / STMG_DIR_T).  device: CUDA
+ * ordinal.  Level operators, transfers and the coarsest exact solver all live on
+ * the device; no CSR matrix is formed. */
+int stmg_hierarchy_create(const stmg_grid* g, const double* k, const double* c,
+                          const double* chi, const stmg_material_pair* mat, const char* method,
+                          int32_t n_dirs, const int32_t* dirs, int32_t device,
+                          stmg_hierarchy** out);
+
+/* transposed_hierarchy, proj/include/stmg/multigrid.hpp:77: same levels/transfers,
+ * every operator transposed (the adjoint solve). */
+int stmg_hierarchy_transposed(const stmg_hierarchy* h, stmg_hierarchy** out);
+
+void stmg_hierarchy_destroy(stmg_hierarchy* h);
+
+int stmg_hierarchy_n_levels(const stmg_hierarchy* h, int32_t* n_levels);
+int stmg_hierarchy_level_info(const stmg_hierarchy* h, int32_t level, int64_t* n_el,
+                              int64_t* n_t, double* w_diri);
+/* Per-node stencil coefficients of a level (host arrays of n_el+1): the row's
+ * same-time (i-1, i, i+1) and other-time (i-1, i, i+1) entries and 1/diag, in the
+ * hierarchy's orientation (J for primal, J^T for transposed). */
+int stmg_hierarchy_level_coeffs(const stmg_hierarchy* h, int32_t level, double* cur_m,
+                                double* cur_0, double* cur_p, double* oth_m, double* oth_0,
+                                double* oth_p, double* inv_diag);
+/* Bytes of device memory the hierarchy holds. */
+int stmg_hierarchy_device_bytes(const stmg_hierarchy* h, int64_t* bytes);
+
+/* ---- solve (proj/src/multigrid.cpp:212-279) ---------------------------------------- */
+
+/* mg_solve, proj/include/stmg/multigrid.hpp:107-108.  u is in/out (warm start).
+ * history must hold history_cap >= opts->max_cycles + 1 doubles. */
+int stmg_mg_solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_options* opts,
+                  stmg_solve_report* report, double* history, int32_t history_cap);
+
+/* ---- level kernels on device vectors (parity tests, profiling) ------------------- */
+/* `sweeps` damped-Jacobi sweeps in place (csr_residual + jacobi_update). */
+int stmg_level_sweeps(stmg_hierarchy* h, int32_t level, const double* f, double* x,
+                      int32_t sweeps, double omega);
+/* r = f - J_l x  (csr_residual) */
+int stmg_level_residual(stmg_hierarchy* h, int32_t level, const double* f, const double* x,
+                        double* r);
+/* f_{l+1} = R (f - J_l x), residual recomputed on the fly (csr_residual + csr_spmv) */
+int stmg_level_restrict_residual(stmg_hierarchy* h, int32_t level, const double* f,
+                                 const double* x, double* f_coarse);
+/* f_{l+1} = R r  (csr_spmv with R = s P^T) */
+int stmg_level_restrict(stmg_hierarchy* h, int32_t level, const double* r, double* f_coarse);
+/* x_l += P x_{l+1}  (csr_spmv_add) */
+int stmg_level_prolong_add(stmg_hierarchy* h, int32_t level, const double* x_coarse, double* x);
+/* exact solve of the coarsest level (DirectSolver::solve) */
+int stmg_coarsest_solve(stmg_hierarchy* h, const double* f, double* x);
+/* ||f - J_0 x||_2 on level 0 (device reduction, fixed order) */
+int stmg_residual_norm(stmg_hierarchy* h, const double* f, const double* x, double* norm);
+/* ||x||_2 over n doubles on the hierarchy's device */
+int stmg_norm2(stmg_hierarchy* h, const double* x, int64_t n, double* norm);
+int stmg_synchronize(stmg_hierarchy* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STMG_B200_H */

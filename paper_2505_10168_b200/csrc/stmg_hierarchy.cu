@@ -1,0 +1,1108 @@
+// Host side of stmg_b200: grids, materials, planner, level build, device
+// hierarchy, V-cycle orchestration (CUDA graphs) and the C ABI of
+// include/stmg_b200.h.  Semantics follow the reference module by module;
+// each function cites the reference code it restates.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <tuple>
+#include <vector>
+
+#include "../../include/stmg_b200.h"
+#include "stmg_internal.h"
+
+namespace stmgb {
+namespace {
+
+thread_local std::string g_error;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NoMem : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    if (e == cudaErrorMemoryAllocation) {
+      cudaGetLastError();
+      throw NoMem(std::string(what) + ": " + cudaGetErrorString(e));
+    }
+    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+void launch_check(int rc, const char* what) {
+  if (rc != 0) cuda_check(static_cast<cudaError_t>(rc), what);
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return STMG_OK;
+  } catch (const std::invalid_argument& e) {
+    g_error = e.what();
+    return STMG_EINVAL;
+  } catch (const std::out_of_range& e) {
+    g_error = e.what();
+    return STMG_ERANGE;
+  } catch (const NoMem& e) {
+    g_error = e.what();
+    return STMG_ENOMEM;
+  } catch (const CudaError& e) {
+    g_error = e.what();
+    return STMG_ECUDA;
+  } catch (const std::bad_alloc&) {
+    g_error = "host allocation failed";
+    return STMG_ENOMEM;
+  } catch (const std::runtime_error& e) {
+    g_error = e.what();
+    return STMG_ERUNTIME;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return STMG_ERUNTIME;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host model (proj/src/{mesh,materials,assembly,rediscretisation,strategy}.cpp)
+// ---------------------------------------------------------------------------
+
+struct HostGrid {
+  double L = 0, t_T = 0, dx = 0, dt = 0;
+  int64_t n_el = 0, n_t = 0;
+};
+
+// build_fine_grid, proj/src/mesh.cpp:16-29
+HostGrid make_grid(double L, double t_T, int64_t n_el, int64_t n_t) {
+  if (L <= 0.0 || t_T <= 0.0) throw std::invalid_argument("build_fine_grid: non-positive extent");
+  if (n_el <= 0 || n_t <= 0) throw std::invalid_argument("build_fine_grid: non-positive count");
+  HostGrid g;
+  g.L = L;
+  g.t_T = t_T;
+  g.n_el = n_el;
+  g.n_t = n_t;
+  g.dx = L / static_cast<double>(n_el);
+  g.dt = t_T / static_cast<double>(n_t);
+  return g;
+}
+
+// coarsen_grid, proj/src/mesh.cpp:31-42
+HostGrid coarsen(const HostGrid& g, int dir) {
+  const bool hx = dir != STMG_DIR_T, ht = dir != STMG_DIR_X;
+  if ((hx && g.n_el % 2 != 0)) throw std::invalid_argument("coarsen_grid: odd element count");
+  if ((ht && g.n_t % 2 != 0)) throw std::invalid_argument("coarsen_grid: odd step count");
+  if ((hx && g.n_el < 2) || (ht && g.n_t < 2))
+    throw std::invalid_argument("coarsen_grid: grid too small to coarsen");
+  return make_grid(g.L, g.t_T, hx ? g.n_el / 2 : g.n_el, ht ? g.n_t / 2 : g.n_t);
+}
+
+void check_material(const stmg_material_pair& m) {
+  if (m.k_ins <= 0.0 || m.k_con <= 0.0 || m.c_ins <= 0.0 || m.c_con <= 0.0)
+    throw std::invalid_argument("material properties must be positive");
+  if (m.p_k <= 0.0 || m.p_c <= 0.0)
+    throw std::invalid_argument("penalisation exponents must be positive");
+}
+
+// simp_eval / apply_design, proj/src/materials.cpp:27-32, 44-50
+void simp(const double* chi, int64_t n, const stmg_material_pair& m, double* k, double* c) {
+  check_material(m);
+  for (int64_t e = 0; e < n; ++e) {
+    if (!(chi[e] >= 0.0 && chi[e] <= 1.0)) throw std::invalid_argument("volume fraction outside [0, 1]");
+    k[e] = m.k_ins + (m.k_con - m.k_ins) * std::pow(chi[e], m.p_k);
+    c[e] = m.c_ins + (m.c_con - m.c_ins) * std::pow(chi[e], m.p_c);
+  }
+}
+
+// coarsen_materials, proj/src/rediscretisation.cpp:53-110 (x step; t copies)
+void coarsen_materials_x(const std::vector<double>& k, const std::vector<double>& c,
+                         const std::vector<double>* chi, const stmg_material_pair* mat, int reasm,
+                         std::vector<double>& kc, std::vector<double>& cc, std::vector<double>* chic) {
+  const size_t nc = k.size() / 2;
+  kc.resize(nc);
+  cc.resize(nc);
+  if (reasm == STMG_REASM_D) {
+    if (!chi || !mat)
+      throw std::invalid_argument("coarsen_materials: D method needs the design field and materials");
+    chic->resize(nc);
+    for (size_t e = 0; e < nc; ++e) (*chic)[e] = 0.5 * ((*chi)[2 * e] + (*chi)[2 * e + 1]);
+    simp(chic->data(), static_cast<int64_t>(nc), *mat, kc.data(), cc.data());
+    return;
+  }
+  for (size_t e = 0; e < nc; ++e) {
+    const double a = k[2 * e], b = k[2 * e + 1];
+    kc[e] = reasm == STMG_REASM_R ? 2.0 * a * b / (a + b) : 0.5 * (a + b);
+    cc[e] = 0.5 * (c[2 * e] + c[2 * e + 1]);
+  }
+}
+
+// design_independent_diffusivity, proj/src/strategy.cpp:85-106
+double design_independent_d(const stmg_material_pair& m) {
+  const double d0 = m.k_ins / m.c_ins, d1 = m.k_con / m.c_con;
+  const double lo = std::min(d0, d1), hi = std::max(d0, d1);
+  for (int i = 0; i < 1001; ++i) {
+    const double chi = static_cast<double>(i) / (1001 - 1);
+    double k, c;
+    simp(&chi, 1, m, &k, &c);
+    const double d = k / c;
+    if (d < lo * (1.0 - 1e-9) || d > hi * (1.0 + 1e-9))
+      throw std::invalid_argument(
+          "design_independent_diffusivity: interpolated diffusivity has an interior extremum; "
+          "the design-independent indicator is invalid for this material pair");
+  }
+  return std::sqrt(d0 * d1);
+}
+
+// anisotropy / effective_lambda, proj/src/strategy.cpp:9-28
+double lambda_eff(const std::vector<double>& k, const std::vector<double>& c, double dx, double dt) {
+  const double scale = dt / (dx * dx);
+  double lo = 0, hi = 0;
+  for (size_t e = 0; e < k.size(); ++e) {
+    const double le = (k[e] / c[e]) * scale;
+    if (e == 0 || le < lo) lo = le;
+    if (e == 0 || le > hi) hi = le;
+  }
+  return std::sqrt(lo * hi);
+}
+
+// plan_coarsening, proj/src/strategy.cpp:127-234
+void plan(const HostGrid& fine, const double* k, const double* c, const double* chi,
+          const stmg_material_pair* mat, const stmg_plan_request& req, int32_t* dirs,
+          double* ind) {
+  if (req.n_levels < 1) throw std::invalid_argument("plan_coarsening: need at least one level");
+  if (req.lambda_crit <= 0.0)
+    throw std::invalid_argument("plan_coarsening: lambda_crit must be positive");
+  double fixed_d = 0.0;
+  if (req.strategy == STMG_PLAN_DESIGN_INDEPENDENT) {
+    if (!mat)
+      throw std::invalid_argument("plan_coarsening: design-independent planning needs the material pair");
+    fixed_d = design_independent_d(*mat);
+  } else if (!k || !c) {
+    throw std::invalid_argument("plan_coarsening: grid has no materials");
+  }
+  if (req.strategy < 0 || req.strategy > 3) throw std::invalid_argument("plan_coarsening: bad strategy");
+  const bool track_chi = req.reassembly == STMG_REASM_D && req.strategy != STMG_PLAN_DESIGN_INDEPENDENT;
+  if (track_chi && (!chi || !mat))
+    throw std::invalid_argument("plan_coarsening: D reassembly needs the design field and materials");
+  HostGrid lev = fine;
+  std::vector<double> lk, lc, lchi;
+  if (req.strategy != STMG_PLAN_DESIGN_INDEPENDENT) {
+    lk.assign(k, k + fine.n_el);
+    lc.assign(c, c + fine.n_el);
+    if (track_chi) lchi.assign(chi, chi + fine.n_el);
+  }
+  for (int l = 1; l < req.n_levels; ++l) {
+    double lambda = 0.0;
+    if (req.strategy == STMG_PLAN_UNIFORM) {
+      for (size_t e = 1; e < lk.size(); ++e)
+        if (lk[e] != lk[0] || lc[e] != lc[0])
+          throw std::invalid_argument("plan_coarsening: uniform strategy on non-uniform materials");
+      lambda = (lk[0] / lc[0]) * lev.dt / (lev.dx * lev.dx);
+    } else if (req.strategy == STMG_PLAN_DESIGN_INDEPENDENT) {
+      lambda = fixed_d * lev.dt / (lev.dx * lev.dx);
+    } else {
+      lambda = lambda_eff(lk, lc, lev.dx, lev.dt);
+    }
+    const bool guard = req.strategy == STMG_PLAN_RESOLUTION && lev.n_el / 2 < req.min_elements;
+    const bool want_time = lambda < req.lambda_crit || guard;
+    const bool x_ok = lev.n_el % 2 == 0 && lev.n_el >= 2;
+    const bool t_ok = lev.n_t % 2 == 0 && lev.n_t >= 2;
+    int dir;
+    if (want_time) {
+      if (t_ok) dir = STMG_DIR_T;
+      else if (guard)
+        throw std::runtime_error(
+            "plan_coarsening: forced time-coarsening impossible and the element floor forbids "
+            "space-coarsening");
+      else if (x_ok) dir = STMG_DIR_X;
+      else throw std::runtime_error("plan_coarsening: no legal coarsening step");
+    } else {
+      if (x_ok) dir = STMG_DIR_X;
+      else if (t_ok) dir = STMG_DIR_T;
+      else throw std::runtime_error("plan_coarsening: no legal coarsening step");
+    }
+    dirs[l - 1] = dir;
+    if (ind) ind[l - 1] = lambda;
+    HostGrid next = coarsen(lev, dir);
+    if (req.strategy != STMG_PLAN_DESIGN_INDEPENDENT && dir == STMG_DIR_X) {
+      std::vector<double> kc, cc, chic;
+      coarsen_materials_x(lk, lc, track_chi ? &lchi : nullptr, mat, req.reassembly, kc, cc,
+                          track_chi ? &chic : nullptr);
+      lk.swap(kc);
+      lc.swap(cc);
+      if (track_chi) lchi.swap(chic);
+    }
+    lev = next;
+  }
+}
+
+// One level's stencil in the reference's exact arithmetic:
+// element terms proj/src/assembly.cpp:17-32, per-row triplets :99-121, masked
+// weight :52-57, 1/diag proj/src/multigrid.cpp:73-82.  Duplicate (row, col)
+// entries are pairs, so from_triplets' summation order does not matter.
+struct HostLevel {
+  HostGrid g;
+  std::vector<double> k, c, chi;
+  double w = 0, inv_w = 0;
+  std::vector<double> W, D, E, SW, S, SE, invD;  // primal, per node i (0 unused)
+
+  void build() {
+    const int64_t ne = g.n_el, nn = ne + 1;
+    for (int64_t e = 0; e < ne; ++e)
+      if (!(k[e] > 0.0) || !(c[e] > 0.0) || !(g.dx > 0.0))
+        throw std::invalid_argument("element_matrices: non-positive input");
+    const double kmax = *std::max_element(k.begin(), k.end());
+    const double cmax = *std::max_element(c.begin(), c.end());
+    w = cmax * g.dx / g.dt + kmax / g.dx;
+    inv_w = 1.0 / w;
+    for (auto* v : {&W, &D, &E, &SW, &S, &SE, &invD}) v->assign(static_cast<size_t>(nn), 0.0);
+    for (int64_t i = 1; i <= ne; ++i) {
+      const double kdl = k[i - 1] / g.dx;
+      const double cdl = c[i - 1] * g.dx / 6.0;
+      const double c11 = (2.0 * cdl) / g.dt, c10 = cdl / g.dt;
+      double d = c11 + kdl;
+      double s = -c11;
+      W[i] = c10 + (-kdl);
+      SW[i] = -c10;
+      if (i <= ne - 1) {
+        const double kdr = k[i] / g.dx;
+        const double cdr = c[i] * g.dx / 6.0;
+        const double c00 = (2.0 * cdr) / g.dt, c01 = cdr / g.dt;
+        d = d + (c00 + kdr);
+        s = s + (-c00);
+        E[i] = c01 + (-kdr);
+        SE[i] = -c01;
+      }
+      D[i] = d;
+      S[i] = s;
+      if (d == 0.0)
+        throw std::runtime_error("build_hierarchy: level operator has a zero diagonal entry");
+      invD[i] = 1.0 / d;
+    }
+    invD[0] = inv_w;
+  }
+
+  // Coefficient table in a row orientation (see LevelView).  The transposed
+  // operator's row (n, i) is J's column (n, i) (proj/src/sparse.cpp:74-96).
+  std::vector<double> table(bool adjoint) const {
+    const int64_t nn = g.n_el + 1, ne = g.n_el;
+    std::vector<double> t(static_cast<size_t>(kNumCoef * nn), 0.0);
+    auto at = [&](int k, int64_t i) -> double& { return t[static_cast<size_t>(k * nn + i)]; };
+    for (int64_t i = 0; i < nn; ++i) {
+      if (!adjoint) {
+        at(kCm, i) = W[i];
+        at(kCp, i) = E[i];
+        at(kOm, i) = SW[i];
+        at(kOp, i) = SE[i];
+      } else {
+        at(kCm, i) = i >= 2 ? E[i - 1] : 0.0;
+        at(kCp, i) = i <= ne - 1 ? W[i + 1] : 0.0;
+        at(kOm, i) = i >= 2 ? SE[i - 1] : 0.0;
+        at(kOp, i) = i <= ne - 1 ? SW[i + 1] : 0.0;
+      }
+      at(kC0, i) = D[i];
+      at(kO0, i) = S[i];
+      at(kInvD, i) = invD[i];
+    }
+    return t;
+  }
+};
+
+int parse_method(const char* name) {
+  if (!name || std::strlen(name) != 2) throw std::invalid_argument("parse_method: expected two letters");
+  if (name[0] != 'C' && name[0] != 'B')
+    throw std::invalid_argument("parse_method: unknown interpolation letter");
+  int re;
+  switch (name[1]) {
+    case 'K': re = STMG_REASM_K; break;
+    case 'D': re = STMG_REASM_D; break;
+    case 'R': re = STMG_REASM_R; break;
+    case 'P': re = STMG_REASM_P; break;
+    default: throw std::invalid_argument("parse_method: unknown reassembly letter");
+  }
+  if (name[0] == 'B')
+    throw std::invalid_argument("stmg_b200: bilinear temporal transfers are not supported (causal only)");
+  if (re == STMG_REASM_P)
+    throw std::invalid_argument("stmg_b200: Galerkin (P) coarse operators are not supported");
+  return re;
+}
+
+// ---------------------------------------------------------------------------
+// Device hierarchy
+// ---------------------------------------------------------------------------
+
+struct DeviceBuf {
+  double* p = nullptr;
+  int64_t n = 0;
+  DeviceBuf() = default;
+  explicit DeviceBuf(int64_t count) : n(count) {
+    if (count > 0) cuda_check(cudaMalloc(&p, sizeof(double) * static_cast<size_t>(count)), "cudaMalloc");
+  }
+  DeviceBuf(const DeviceBuf&) = delete;
+  DeviceBuf& operator=(const DeviceBuf&) = delete;
+  ~DeviceBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+// Vector workspaces (f, x, y per level; level 0: b, u, u').  A hierarchy and
+// its transpose share one Workspace (they are never solved concurrently),
+// which halves the footprint for 1e9-DOF grids.
+struct Workspace {
+  std::vector<std::unique_ptr<DeviceBuf>> f, xa, xb;
+  std::unique_ptr<DeviceBuf> partials, scalars, coarse_scratch;
+  double* pinned = nullptr;  // 4 host doubles
+  ~Workspace() {
+    if (pinned) cudaFreeHost(pinned);
+  }
+};
+
+struct GraphKey {
+  int nu;
+  double omega;
+  bool operator<(const GraphKey& o) const { return std::tie(nu, omega) < std::tie(o.nu, o.omega); }
+};
+
+struct GraphEntry {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int64_t kernels = 0;
+  int final_buf = 0;
+};
+
+}  // namespace
+}  // namespace stmgb
+
+struct stmg_hierarchy {
+  int device = 0;
+  bool adjoint = false;
+  int reassembly = STMG_REASM_K;
+  std::vector<int32_t> dirs;
+  std::vector<stmgb::HostLevel> host;
+  std::vector<std::unique_ptr<stmgb::DeviceBuf>> coef;  // per level
+  std::vector<stmgb::LevelView> views;
+  stmgb::CoarsestView coarsest{};
+  std::unique_ptr<stmgb::DeviceBuf> pcr_alpha, pcr_gamma, pcr_bfin;
+  std::shared_ptr<stmgb::Workspace> ws;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::map<stmgb::GraphKey, stmgb::GraphEntry> graphs;
+  int64_t device_bytes = 0;
+
+  ~stmg_hierarchy() {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    for (auto& kv : graphs) {
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+      if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+    }
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+    coef.clear();
+    pcr_alpha.reset();
+    pcr_gamma.reset();
+    pcr_bfin.reset();
+    ws.reset();
+    cudaSetDevice(prev);
+  }
+  int n_levels() const { return static_cast<int>(host.size()); }
+  int64_t ndofs(int l) const { return (host[l].g.n_el + 1) * (host[l].g.n_t + 1); }
+};
+
+namespace stmgb {
+namespace {
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+// Parallel-cyclic-reduction factors of the coarsest step matrix (rows 1..n_el:
+// sub cm, diag c0, super cp), shared by every time level.
+void build_pcr(stmg_hierarchy* h) {
+  const HostLevel& hl = h->host.back();
+  const int64_t nn = hl.g.n_el + 1;
+  const int m = static_cast<int>(hl.g.n_el);
+  const std::vector<double> t = hl.table(h->adjoint);
+  std::vector<double> a(m), b(m), c(m);
+  for (int j = 0; j < m; ++j) {
+    const int64_t i = j + 1;
+    a[j] = i >= 2 ? t[kCm * nn + i] : 0.0;
+    b[j] = t[kC0 * nn + i];
+    c[j] = i <= m - 1 ? t[kCp * nn + i] : 0.0;
+  }
+  int steps = 0;
+  while ((1 << steps) < m) ++steps;
+  std::vector<double> alpha(static_cast<size_t>(std::max(steps, 1)) * m, 0.0), gamma(alpha.size(), 0.0);
+  for (int k = 0; k < steps; ++k) {
+    const int s = 1 << k;
+    std::vector<double> a2(m, 0.0), b2(m), c2(m, 0.0);
+    for (int j = 0; j < m; ++j) {
+      double al = 0.0, ga = 0.0;
+      double bb = b[j];
+      if (j - s >= 0) {
+        al = -a[j] / b[j - s];
+        a2[j] = al * a[j - s];
+        bb += al * c[j - s];
+      }
+      if (j + s < m) {
+        ga = -c[j] / b[j + s];
+        c2[j] = ga * c[j + s];
+        bb += ga * a[j + s];
+      }
+      b2[j] = bb;
+      alpha[static_cast<size_t>(k) * m + j] = al;
+      gamma[static_cast<size_t>(k) * m + j] = ga;
+    }
+    a.swap(a2);
+    b.swap(b2);
+    c.swap(c2);
+  }
+  h->pcr_alpha = std::make_unique<DeviceBuf>(static_cast<int64_t>(alpha.size()));
+  h->pcr_gamma = std::make_unique<DeviceBuf>(static_cast<int64_t>(gamma.size()));
+  h->pcr_bfin = std::make_unique<DeviceBuf>(std::max(m, 1));
+  cuda_check(cudaMemcpy(h->pcr_alpha->p, alpha.data(), alpha.size() * 8, cudaMemcpyHostToDevice), "pcr");
+  cuda_check(cudaMemcpy(h->pcr_gamma->p, gamma.data(), gamma.size() * 8, cudaMemcpyHostToDevice), "pcr");
+  if (m > 0) cuda_check(cudaMemcpy(h->pcr_bfin->p, b.data(), b.size() * 8, cudaMemcpyHostToDevice), "pcr");
+  h->coarsest.lv = h->views.back();
+  h->coarsest.m = m;
+  h->coarsest.n_steps = steps;
+  h->coarsest.alpha = h->pcr_alpha->p;
+  h->coarsest.gamma = h->pcr_gamma->p;
+  h->coarsest.bfin = h->pcr_bfin->p;
+  h->device_bytes += static_cast<int64_t>((alpha.size() * 2 + b.size()) * 8);
+}
+
+void upload_levels(stmg_hierarchy* h) {
+  h->coef.clear();
+  h->views.clear();
+  for (const HostLevel& hl : h->host) {
+    const std::vector<double> t = hl.table(h->adjoint);
+    auto buf = std::make_unique<DeviceBuf>(static_cast<int64_t>(t.size()));
+    cuda_check(cudaMemcpy(buf->p, t.data(), t.size() * 8, cudaMemcpyHostToDevice), "coef upload");
+    LevelView v;
+    v.n_el = hl.g.n_el;
+    v.n_t = hl.g.n_t;
+    v.nn = hl.g.n_el + 1;
+    v.w = hl.w;
+    v.inv_w = hl.inv_w;
+    v.coef = buf->p;
+    h->views.push_back(v);
+    h->device_bytes += static_cast<int64_t>(t.size() * 8);
+    h->coef.push_back(std::move(buf));
+  }
+  build_pcr(h);
+}
+
+std::shared_ptr<Workspace> make_workspace(const stmg_hierarchy* h, int64_t* bytes) {
+  auto ws = std::make_shared<Workspace>();
+  const int nl = h->n_levels();
+  int64_t max_partials = sumsq_partials_needed(0);
+  for (int l = 0; l < nl; ++l) {
+    const int64_t nd = h->ndofs(l);
+    ws->f.push_back(std::make_unique<DeviceBuf>(nd));
+    ws->xa.push_back(std::make_unique<DeviceBuf>(nd));
+    // the coarsest level never ping-pongs unless it is also level 0
+    ws->xb.push_back(std::make_unique<DeviceBuf>(l < nl - 1 || nl == 1 ? nd : 0));
+    *bytes += 8 * (3 * nd);
+    max_partials = std::max(max_partials, sweep_partials_needed(h->views[l]));
+  }
+  ws->partials = std::make_unique<DeviceBuf>(max_partials);
+  ws->scalars = std::make_unique<DeviceBuf>(8);
+  const int m = h->coarsest.m;
+  ws->coarse_scratch = std::make_unique<DeviceBuf>(std::max<int64_t>(2 * static_cast<int64_t>(m), 2));
+  *bytes += 8 * (max_partials + 8 + 2 * m);
+  cuda_check(cudaMallocHost(&ws->pinned, 8 * sizeof(double)), "cudaMallocHost");
+  return ws;
+}
+
+void finish_create(stmg_hierarchy* h, bool share_ws_from_other, const stmg_hierarchy* other) {
+  DeviceGuard dg(h->device);
+  launch_check(kernels_init(), "kernels_init");
+  upload_levels(h);
+  if (share_ws_from_other) {
+    h->ws = other->ws;
+  } else {
+    int64_t bytes = 0;
+    h->ws = make_workspace(h, &bytes);
+    h->device_bytes += bytes;
+  }
+  cuda_check(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  cuda_check(cudaEventCreate(&h->ev0), "cudaEventCreate");
+  cuda_check(cudaEventCreate(&h->ev1), "cudaEventCreate");
+}
+
+// ---------------------------------------------------------------------------
+// V-cycle emission (proj/src/multigrid.cpp:184-208), recorded into a graph
+// ---------------------------------------------------------------------------
+
+struct Emitter {
+  stmg_hierarchy* h;
+  int nu;
+  double omega;
+  cudaStream_t s;
+  int64_t kernels = 0;
+
+  double* buf(int l, int which) {
+    return which == 0 ? h->ws->xa[l]->p : h->ws->xb[l]->p;
+  }
+
+  // Returns the buffer index (0 = xa, 1 = xb) holding the level's result.
+  // start: buffer holding the current iterate; pre_done: sweeps already done;
+  // from_zero: the iterate is identically zero (coarse levels).
+  int level(int l, int start, int pre_done, bool from_zero) {
+    const int nl = h->n_levels();
+    const LevelView& L = h->views[l];
+    double* f = h->ws->f[l]->p;
+    if (l == nl - 1) {
+      launch_check(launch_coarsest(h->adjoint, h->coarsest, f, buf(l, 0), h->ws->coarse_scratch->p, s),
+                   "coarsest");
+      ++kernels;
+      return 0;
+    }
+    int cur = start;
+    int pre = nu - pre_done;
+    if (from_zero) {
+      cur = 0;
+      if (nu >= 1) {
+        launch_check(launch_sweep_from_zero(L, f, buf(l, 0), omega, s), "sweep0");
+        ++kernels;
+        pre = nu - 1;
+      } else {
+        cuda_check(cudaMemsetAsync(buf(l, 0), 0, sizeof(double) * h->ndofs(l), s), "memset");
+        pre = 0;
+      }
+    }
+    for (int k = 0; k < pre; ++k) {
+      launch_check(launch_sweep(h->adjoint, L, f, buf(l, cur), buf(l, 1 - cur), omega, nullptr,
+                                nullptr, s),
+                   "sweep");
+      ++kernels;
+      cur = 1 - cur;
+    }
+    const LevelView& C = h->views[l + 1];
+    launch_check(launch_restrict_residual(h->adjoint, L, C, h->dirs[l], f, buf(l, cur),
+                                          h->ws->f[l + 1]->p, s),
+                 "restrict");
+    ++kernels;
+    const int child = level(l + 1, 0, 0, true);
+    const double* xc = buf(l + 1, child);
+    int post = nu;
+    if (nu >= 1) {
+      launch_check(launch_sweep_prolong(h->adjoint, L, C, h->dirs[l], f, buf(l, cur), xc,
+                                        buf(l, 1 - cur), omega, s),
+                   "sweep_prolong");
+      ++kernels;
+      cur = 1 - cur;
+      post = nu - 1;
+    } else {
+      launch_check(launch_prolong_add(L, C, h->dirs[l], xc, buf(l, cur), s), "prolong");
+      ++kernels;
+    }
+    for (int k = 0; k < post; ++k) {
+      launch_check(launch_sweep(h->adjoint, L, f, buf(l, cur), buf(l, 1 - cur), omega, nullptr,
+                                nullptr, s),
+                   "sweep");
+      ++kernels;
+      cur = 1 - cur;
+    }
+    return cur;
+  }
+};
+
+bool speculative(const stmg_hierarchy* h, int nu) { return h->n_levels() > 1 && nu >= 1; }
+
+GraphEntry& get_graph(stmg_hierarchy* h, int nu, double omega) {
+  const GraphKey key{nu, omega};
+  auto it = h->graphs.find(key);
+  if (it != h->graphs.end()) return it->second;
+  GraphEntry e;
+  Emitter em{h, nu, omega, h->stream};
+  cuda_check(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal), "capture");
+  const bool spec = speculative(h, nu);
+  e.final_buf = em.level(0, spec ? 1 : 0, spec ? 1 : 0, false);
+  cuda_check(cudaStreamEndCapture(h->stream, &e.graph), "end capture");
+  cuda_check(cudaGraphInstantiate(&e.exec, e.graph, 0), "graph instantiate");
+  e.kernels = em.kernels;
+  return h->graphs.emplace(key, e).first->second;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// sum of squares of the level-0 residual (and optionally a speculative sweep
+// into xb) -> scalars[slot]
+int64_t emit_norm(stmg_hierarchy* h, const double* f, const double* x, double* y, double omega,
+                  int slot) {
+  int64_t np = 0;
+  launch_check(launch_sweep(h->adjoint, h->views[0], f, x, y, omega, h->ws->partials->p, &np,
+                            h->stream),
+               "norm sweep");
+  launch_check(launch_finalize_sum(h->ws->partials->p, np, h->ws->scalars->p + slot, h->stream),
+               "finalize");
+  return 2;
+}
+
+double fetch_scalars(stmg_hierarchy* h, int count, double* out) {
+  cuda_check(cudaMemcpyAsync(h->ws->pinned, h->ws->scalars->p, sizeof(double) * count,
+                             cudaMemcpyDeviceToHost, h->stream),
+             "scalar d2h");
+  cuda_check(cudaStreamSynchronize(h->stream), "stream sync");
+  for (int i = 0; i < count; ++i) out[i] = h->ws->pinned[i];
+  return out[0];
+}
+
+// mg_solve, proj/src/multigrid.cpp:212-279
+void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_options& o,
+           stmg_solve_report* rep, double* history, int32_t cap) {
+  if (!b || !u) throw std::invalid_argument("mg_solve: vector size mismatch");
+  if (o.nu < 0 || o.omega <= 0.0 || o.tol <= 0.0 || o.div_tol <= o.tol || o.max_cycles < 0)
+    throw std::invalid_argument("mg_solve: invalid options");
+  if (!history || cap < o.max_cycles + 1)
+    throw std::invalid_argument("mg_solve: history buffer smaller than max_cycles + 1");
+  DeviceGuard dg(h->device);
+  const auto t0 = std::chrono::steady_clock::now();
+  const int64_t n = h->ndofs(0);
+  const size_t bytes = sizeof(double) * static_cast<size_t>(n);
+  Workspace& ws = *h->ws;
+  double* B = ws.f[0]->p;
+  double* X = ws.xa[0]->p;
+  double* Y = ws.xb[0]->p;
+  const bool b_dev = is_device_ptr(b), u_dev = is_device_ptr(u);
+  cuda_check(cudaEventRecord(h->ev0, h->stream), "event");
+  cuda_check(cudaMemcpyAsync(B, b, bytes, b_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream), "b copy");
+  cuda_check(cudaMemcpyAsync(X, u, bytes, u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream), "u copy");
+  int64_t launches = 0;
+  int64_t np = 0;
+  launch_check(launch_sumsq(B, n, ws.partials->p, &np, h->stream), "sumsq");
+  launch_check(launch_finalize_sum(ws.partials->p, np, ws.scalars->p + 0, h->stream), "finalize");
+  launches += 2;
+  const bool spec = speculative(h, o.nu);
+  GraphEntry* g = nullptr;
+  if (o.max_cycles > 0) g = &get_graph(h, o.nu, o.omega);
+  launches += emit_norm(h, B, X, spec && o.max_cycles > 0 ? Y : nullptr, o.omega, 1);
+  double sc[2];
+  fetch_scalars(h, 2, sc);
+  const double norm_b = std::sqrt(sc[0]);
+  rep->absolute_norms = norm_b == 0.0 ? 1 : 0;
+  const double denom = rep->absolute_norms ? 1.0 : norm_b;
+  const double r0 = std::sqrt(sc[1]) / denom;
+  int nh = 0;
+  history[nh++] = r0;
+  rep->cycles = 0;
+  rep->factor = 1.0;
+  rep->smoother_dof_updates = 0.0;
+  double per_cycle_updates = 0.0;
+  for (int l = 0; l + 1 < h->n_levels(); ++l) per_cycle_updates += 2.0 * o.nu * static_cast<double>(h->ndofs(l));
+  if (r0 < o.tol) {
+    rep->status = STMG_CONVERGED;
+  } else {
+    rep->status = STMG_MAX_CYCLES;
+    for (int cycle = 1; cycle <= o.max_cycles; ++cycle) {
+      cuda_check(cudaGraphLaunch(g->exec, h->stream), "graph launch");
+      launches += g->kernels;
+      if (g->final_buf != 0) throw std::logic_error("level-0 iterate left the primary buffer");
+      const bool more = cycle < o.max_cycles;
+      launches += emit_norm(h, B, X, spec && more ? Y : nullptr, o.omega, 1);
+      fetch_scalars(h, 2, sc);
+      const double rn = std::sqrt(sc[1]) / denom;
+      history[nh++] = rn;
+      rep->cycles = cycle;
+      rep->smoother_dof_updates += per_cycle_updates;
+      if (rn < o.tol) {
+        rep->status = STMG_CONVERGED;
+        break;
+      }
+      if (!std::isfinite(rn) || rn > o.div_tol) {
+        rep->status = STMG_DIVERGED;
+        break;
+      }
+    }
+  }
+  if (rep->cycles > 0) rep->factor = std::pow(history[nh - 1] / r0, 1.0 / rep->cycles);
+  cuda_check(cudaEventRecord(h->ev1, h->stream), "event");
+  cuda_check(cudaMemcpyAsync(u, X, bytes, u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream), "u copy back");
+  cuda_check(cudaStreamSynchronize(h->stream), "stream sync");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->ev0, h->ev1);
+  rep->device_seconds = ms * 1e-3;
+  rep->n_history = nh;
+  rep->kernel_launches = launches;
+  rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+stmg_hierarchy* checked(stmg_hierarchy* h) {
+  if (!h) throw std::invalid_argument("null hierarchy handle");
+  return h;
+}
+void check_level(const stmg_hierarchy* h, int l) {
+  if (l < 0 || l >= h->n_levels()) throw std::out_of_range("level index outside hierarchy");
+}
+
+// source kinds shared with paper_2505_10168_b200/configs.py
+double source_value(int kind, const double* p, double x, double t, double L, double t_T) {
+  switch (kind) {
+    case 0: return p[0];
+    case 1: return (L - x < p[1]) ? p[0] : 0.0;
+    case 2: return (L - x < p[2]) ? 1.0 + p[0] * std::sin(2.0 * M_PI * p[1] * t) : 0.0;
+    case 3: {  // heat_load_value, proj/src/assembly.cpp:59-63
+      const double xs = x / L - 0.5, ts = t / t_T - 0.5;
+      return (1.0 + std::cos(200.0 * (xs * xs + ts * ts))) * 1.0e6;
+    }
+  }
+  throw std::invalid_argument("load_vector: unknown source kind");
+}
+
+// load_vector, proj/src/assembly.cpp:65-83; time levels are independent, so
+// they are filled by several host threads with identical per-entry arithmetic.
+template <class Q>
+void load_vector_impl(const HostGrid& g, Q&& q, bool masked, double* b) {
+  const int64_t nn = g.n_el + 1;
+  const int64_t levels = g.n_t + 1;
+  auto work = [&](int64_t lo, int64_t hi) {
+    for (int64_t n = lo; n < hi; ++n) {
+      double* row = b + n * nn;
+      std::fill(row, row + nn, 0.0);
+      if (n == 0) continue;
+      const double t = static_cast<double>(n) * g.dt;
+      for (int64_t e = 0; e < g.n_el; ++e) {
+        const double qe = q((static_cast<double>(e) + 0.5) * g.dx, t) * g.dx / 2.0;
+        row[e] += qe;
+        row[e + 1] += qe;
+      }
+      if (masked) row[0] = 0.0;
+    }
+    if (masked && lo == 0)
+      for (int64_t i = 0; i < nn; ++i) b[i] = 0.0;
+  };
+  const int64_t total = levels * nn;
+  unsigned nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  if (total < (1 << 20)) nth = 1;
+  std::vector<std::thread> th;
+  const int64_t chunk = (levels + nth - 1) / nth;
+  for (unsigned k = 0; k < nth; ++k) {
+    const int64_t lo = k * chunk, hi = std::min(levels, lo + chunk);
+    if (lo >= hi) break;
+    th.emplace_back(work, lo, hi);
+  }
+  for (auto& t : th) t.join();
+}
+
+}  // namespace
+}  // namespace stmgb
+
+using namespace stmgb;
+
+extern "C" {
+
+const char* stmg_last_error(void) { return g_error.c_str(); }
+int stmg_abi_version(void) { return STMG_ABI_VERSION; }
+
+int stmg_apply_design(const double* chi, int64_t n, const stmg_material_pair* mat, double* k,
+                      double* c) {
+  return guarded([&] {
+    if (!chi || !mat || !k || !c || n < 0) throw std::invalid_argument("apply_design: null argument");
+    simp(chi, n, *mat, k, c);
+  });
+}
+
+int stmg_load_vector(const stmg_grid* g, int32_t kind, const double* params, int32_t masked,
+                     double* b) {
+  return guarded([&] {
+    if (!g || !b) throw std::invalid_argument("load_vector: null argument");
+    const HostGrid hg = make_grid(g->L, g->t_T, g->n_el, g->n_t);
+    double p[4] = {0, 0, 0, 0};
+    const int np = kind == 0 ? 1 : kind == 1 ? 2 : kind == 2 ? 3 : 0;
+    if (kind < 0 || kind > 3) throw std::invalid_argument("load_vector: unknown source kind");
+    if (np > 0 && !params) throw std::invalid_argument("load_vector: missing source parameters");
+    for (int i = 0; i < np; ++i) p[i] = params[i];
+    load_vector_impl(hg, [&](double x, double t) { return source_value(kind, p, x, t, hg.L, hg.t_T); },
+                     masked != 0, b);
+  });
+}
+
+int stmg_load_vector_cb(const stmg_grid* g, stmg_source_fn q, void* ctx, int32_t masked, double* b) {
+  return guarded([&] {
+    if (!g || !b || !q) throw std::invalid_argument("load_vector: null argument");
+    const HostGrid hg = make_grid(g->L, g->t_T, g->n_el, g->n_t);
+    const int64_t nn = hg.n_el + 1;
+    // callbacks may not be thread-safe: sequential, same per-entry arithmetic
+    std::fill(b, b + (hg.n_t + 1) * nn, 0.0);
+    for (int64_t n = 1; n <= hg.n_t; ++n) {
+      const double t = static_cast<double>(n) * hg.dt;
+      for (int64_t e = 0; e < hg.n_el; ++e) {
+        const double qe = q((static_cast<double>(e) + 0.5) * hg.dx, t, ctx) * hg.dx / 2.0;
+        b[n * nn + e] += qe;
+        b[n * nn + e + 1] += qe;
+      }
+    }
+    if (masked) {
+      for (int64_t i = 0; i < nn; ++i) b[i] = 0.0;
+      for (int64_t n = 1; n <= hg.n_t; ++n) b[n * nn] = 0.0;
+    }
+  });
+}
+
+int stmg_plan_coarsening(const stmg_grid* g, const double* k, const double* c, const double* chi,
+                         const stmg_material_pair* mat, const stmg_plan_request* req,
+                         int32_t* dirs_out, double* indicator_out) {
+  return guarded([&] {
+    if (!g || !req || (!dirs_out && req->n_levels > 1))
+      throw std::invalid_argument("plan_coarsening: null argument");
+    const HostGrid hg = make_grid(g->L, g->t_T, g->n_el, g->n_t);
+    plan(hg, k, c, chi, mat, *req, dirs_out, indicator_out);
+  });
+}
+
+int stmg_hierarchy_create(const stmg_grid* g, const double* k, const double* c, const double* chi,
+                          const stmg_material_pair* mat, const char* method, int32_t n_dirs,
+                          const int32_t* dirs, int32_t device, stmg_hierarchy** out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("build_hierarchy: null output handle");
+    *out = nullptr;
+    if (!g) throw std::invalid_argument("build_hierarchy: null grid");
+    const HostGrid fine = make_grid(g->L, g->t_T, g->n_el, g->n_t);
+    if (!k || !c) throw std::invalid_argument("build_hierarchy: fine grid has no materials");
+    const int reasm = parse_method(method);
+    if (reasm == STMG_REASM_D && (!chi || !mat))
+      throw std::invalid_argument("build_hierarchy: D reassembly needs the design field and materials");
+    if (n_dirs < 0 || (n_dirs > 0 && !dirs)) throw std::invalid_argument("build_hierarchy: bad path");
+    int n_dev = 0;
+    cuda_check(cudaGetDeviceCount(&n_dev), "cudaGetDeviceCount");
+    if (device < 0 || device >= n_dev) throw std::invalid_argument("build_hierarchy: bad device ordinal");
+    auto h = std::make_unique<stmg_hierarchy>();
+    h->device = device;
+    h->reassembly = reasm;
+    h->dirs.assign(dirs, dirs + n_dirs);
+    HostLevel l0;
+    l0.g = fine;
+    l0.k.assign(k, k + fine.n_el);
+    l0.c.assign(c, c + fine.n_el);
+    if (chi) l0.chi.assign(chi, chi + fine.n_el);
+    l0.build();
+    h->host.push_back(std::move(l0));
+    for (int32_t s = 0; s < n_dirs; ++s) {
+      const int dir = dirs[s];
+      if (dir == STMG_DIR_XT)
+        throw std::invalid_argument("stmg_b200: combined space-time (FullST) coarsening is not supported");
+      if (dir != STMG_DIR_X && dir != STMG_DIR_T) throw std::invalid_argument("build_hierarchy: bad direction");
+      const HostLevel& p = h->host.back();
+      HostLevel lc;
+      lc.g = coarsen(p.g, dir);
+      if (dir == STMG_DIR_T) {
+        lc.k = p.k;
+        lc.c = p.c;
+        lc.chi = p.chi;
+      } else {
+        coarsen_materials_x(p.k, p.c, p.chi.empty() ? nullptr : &p.chi, mat, reasm, lc.k, lc.c,
+                            &lc.chi);
+        if (reasm != STMG_REASM_D) lc.chi.clear();
+      }
+      lc.build();
+      h->host.push_back(std::move(lc));
+    }
+    finish_create(h.get(), false, nullptr);
+    *out = h.release();
+  });
+}
+
+int stmg_hierarchy_transposed(const stmg_hierarchy* src, stmg_hierarchy** out) {
+  return guarded([&] {
+    if (!src || !out) throw std::invalid_argument("transposed_hierarchy: null argument");
+    auto h = std::make_unique<stmg_hierarchy>();
+    h->device = src->device;
+    h->adjoint = !src->adjoint;
+    h->reassembly = src->reassembly;
+    h->dirs = src->dirs;
+    h->host = src->host;
+    finish_create(h.get(), true, src);
+    *out = h.release();
+  });
+}
+
+void stmg_hierarchy_destroy(stmg_hierarchy* h) { delete h; }
+
+int stmg_hierarchy_n_levels(const stmg_hierarchy* h, int32_t* n) {
+  return guarded([&] {
+    if (!h || !n) throw std::invalid_argument("null argument");
+    *n = h->n_levels();
+  });
+}
+
+int stmg_hierarchy_level_info(const stmg_hierarchy* h, int32_t l, int64_t* n_el, int64_t* n_t,
+                              double* w) {
+  return guarded([&] {
+    if (!h) throw std::invalid_argument("null hierarchy handle");
+    check_level(h, l);
+    if (n_el) *n_el = h->host[l].g.n_el;
+    if (n_t) *n_t = h->host[l].g.n_t;
+    if (w) *w = h->host[l].w;
+  });
+}
+
+int stmg_hierarchy_level_coeffs(const stmg_hierarchy* h, int32_t l, double* cm, double* c0,
+                                double* cp, double* om, double* o0, double* op, double* invd) {
+  return guarded([&] {
+    if (!h) throw std::invalid_argument("null hierarchy handle");
+    check_level(h, l);
+    const std::vector<double> t = h->host[l].table(h->adjoint);
+    const size_t nn = static_cast<size_t>(h->host[l].g.n_el + 1);
+    double* outs[7] = {cm, c0, cp, om, o0, op, invd};
+    for (int k = 0; k < 7; ++k)
+      if (outs[k]) std::memcpy(outs[k], t.data() + k * nn, nn * sizeof(double));
+  });
+}
+
+int stmg_hierarchy_device_bytes(const stmg_hierarchy* h, int64_t* bytes) {
+  return guarded([&] {
+    if (!h || !bytes) throw std::invalid_argument("null argument");
+    *bytes = h->device_bytes;
+  });
+}
+
+int stmg_mg_solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_options* opts,
+                  stmg_solve_report* report, double* history, int32_t cap) {
+  return guarded([&] {
+    checked(h);
+    if (!opts || !report) throw std::invalid_argument("mg_solve: null argument");
+    solve(h, b, u, *opts, report, history, cap);
+  });
+}
+
+int stmg_level_sweeps(stmg_hierarchy* h, int32_t l, const double* f, double* x, int32_t sweeps,
+                      double omega) {
+  return guarded([&] {
+    checked(h);
+    check_level(h, l);
+    DeviceGuard dg(h->device);
+    double* tmp = h->ws->xb[l]->p;
+    std::unique_ptr<DeviceBuf> own;
+    if (!tmp) {
+      own = std::make_unique<DeviceBuf>(h->ndofs(l));
+      tmp = own->p;
+    }
+    double* a = x;
+    double* b = tmp;
+    for (int s = 0; s < sweeps; ++s) {
+      launch_check(launch_sweep(h->adjoint, h->views[l], f, a, b, omega, nullptr, nullptr, h->stream), "sweep");
+      std::swap(a, b);
+    }
+    if (a != x)
+      cuda_check(cudaMemcpyAsync(x, a, sizeof(double) * h->ndofs(l), cudaMemcpyDeviceToDevice, h->stream), "copy");
+    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+  });
+}
+
+int stmg_level_residual(stmg_hierarchy* h, int32_t l, const double* f, const double* x, double* r) {
+  return guarded([&] {
+    checked(h);
+    check_level(h, l);
+    DeviceGuard dg(h->device);
+    launch_check(launch_residual(h->adjoint, h->views[l], f, x, r, h->stream), "residual");
+    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+  });
+}
+
+int stmg_level_restrict_residual(stmg_hierarchy* h, int32_t l, const double* f, const double* x,
+                                 double* fc) {
+  return guarded([&] {
+    checked(h);
+    check_level(h, l);
+    if (l + 1 >= h->n_levels()) throw std::out_of_range("no coarser level");
+    DeviceGuard dg(h->device);
+    launch_check(launch_restrict_residual(h->adjoint, h->views[l], h->views[l + 1], h->dirs[l], f, x,
+                                          fc, h->stream),
+                 "restrict");
+    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+  });
+}
+
+int stmg_level_restrict(stmg_hierarchy* h, int32_t l, const double* r, double* fc) {
+  return guarded([&] {
+    checked(h);
+    check_level(h, l);
+    if (l + 1 >= h->n_levels()) throw std::out_of_range("no coarser level");
+    DeviceGuard dg(h->device);
+    launch_check(launch_restrict(h->views[l], h->views[l + 1], h->dirs[l], r, fc, h->stream), "restrict");
+    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+  });
+}
+
+int stmg_level_prolong_add(stmg_hierarchy* h, int32_t l, const double* xc, double* x) {
+  return guarded([&] {
+    checked(h);
+    check_level(h, l);
+    if (l + 1 >= h->n_levels()) throw std::out_of_range("no coarser level");
+    DeviceGuard dg(h->device);
+    launch_check(launch_prolong_add(h->views[l], h->views[l + 1], h->dirs[l], xc, x, h->stream), "prolong");
+    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+  });
+}
+
+int stmg_coarsest_solve(stmg_hierarchy* h, const double* f, double* x) {
+  return guarded([&] {
+    checked(h);
+    DeviceGuard dg(h->device);
+    launch_check(launch_coarsest(h->adjoint, h->coarsest, f, x, h->ws->coarse_scratch->p, h->stream),
+                 "coarsest");
+    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+  });
+}
+
+int stmg_residual_norm(stmg_hierarchy* h, const double* f, const double* x, double* norm) {
+  return guarded([&] {
+    checked(h);
+    if (!norm) throw std::invalid_argument("null argument");
+    DeviceGuard dg(h->device);
+    emit_norm(h, f, x, nullptr, 0.5, 1);
+    double sc[2];
+    fetch_scalars(h, 2, sc);
+    *norm = std::sqrt(sc[1]);
+  });
+}
+
+int stmg_norm2(stmg_hierarchy* h, const double* x, int64_t n, double* norm) {
+  return guarded([&] {
+    checked(h);
+    if (!norm || n < 0) throw std::invalid_argument("bad argument");
+    DeviceGuard dg(h->device);
+    int64_t np = 0;
+    launch_check(launch_sumsq(x, n, h->ws->partials->p, &np, h->stream), "sumsq");
+    launch_check(launch_finalize_sum(h->ws->partials->p, np, h->ws->scalars->p, h->stream), "finalize");
+    double sc[1];
+    fetch_scalars(h, 1, sc);
+    *norm = std::sqrt(sc[0]);
+  });
+}
+
+int stmg_synchronize(stmg_hierarchy* h) {
+  return guarded([&] {
+    checked(h);
+    DeviceGuard dg(h->device);
+    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,72 @@
+// Internal definitions shared by the sm_100a kernels and the host orchestration.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace stmgb {
+
+// Device view of one level's operator.  The stencil of row (n, i) is stored
+// per node i in the row's own orientation (J for a primal hierarchy, J^T for a
+// transposed one), so kernels never index i-1/i+1 coefficient arrays:
+//   cm, c0, cp : same-time-level entries at columns i-1, i, i+1
+//   om, o0, op : other-time-level entries (n-1 for J, n+1 for J^T) at i-1, i, i+1
+// Masked rows (n == 0 || i == 0) have the single diagonal w
+// (proj/src/assembly.cpp:85-88, 122-123).
+struct LevelView {
+  int64_t n_el;
+  int64_t n_t;
+  int64_t nn;  // n_el + 1 nodes per time level
+  double w;
+  double inv_w;
+  const double* coef;  // 7 * nn: cm, c0, cp, om, o0, op, inv_diag
+};
+
+enum Coef { kCm = 0, kC0 = 1, kCp = 2, kOm = 3, kO0 = 4, kOp = 5, kInvD = 6, kNumCoef = 7 };
+
+// PCR tables for the exact coarsest solve (per tridiagonal step system of the
+// unmasked nodes 1..n_el, identical on every time level).
+struct CoarsestView {
+  LevelView lv;
+  int32_t m;            // n_el unmasked nodes per time level
+  int32_t n_steps;      // ceil(log2(m))
+  const double* alpha;  // n_steps * m
+  const double* gamma;  // n_steps * m
+  const double* bfin;   // m, final diagonal after reduction
+};
+
+// ---- kernel launchers (stmg_kernels.cu); all asynchronous on `s` ------------------
+// One damped-Jacobi sweep y = x + omega (f - J x) / diag.  If partials != nullptr,
+// the block partial sums of r^2 are written too (deterministic order).  If y ==
+// nullptr only the residual norm partials are produced.
+int launch_sweep(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
+                 double omega, double* partials, int64_t* n_partials, cudaStream_t s);
+// First sweep from a zero iterate: y = 0 + omega * (f * inv_diag), bitwise equal
+// to the general sweep applied to x = +0.
+int launch_sweep_from_zero(const LevelView& L, const double* f, double* y, double omega,
+                           cudaStream_t s);
+// Jacobi sweep applied to (x + P xc), i.e. prolong-add fused into the first
+// post-smoothing sweep.  dir: 0 = x, 1 = t.
+int launch_sweep_prolong(bool adjoint, const LevelView& L, const LevelView& C, int dir,
+                         const double* f, const double* x, const double* xc, double* y,
+                         double omega, cudaStream_t s);
+int launch_residual(bool adjoint, const LevelView& L, const double* f, const double* x, double* r,
+                    cudaStream_t s);
+int launch_restrict_residual(bool adjoint, const LevelView& F, const LevelView& C, int dir,
+                             const double* f, const double* x, double* fc, cudaStream_t s);
+int launch_restrict(const LevelView& F, const LevelView& C, int dir, const double* r, double* fc,
+                    cudaStream_t s);
+int launch_prolong_add(const LevelView& F, const LevelView& C, int dir, const double* xc, double* x,
+                       cudaStream_t s);
+int launch_coarsest(bool adjoint, const CoarsestView& cv, const double* f, double* x,
+                    double* scratch, cudaStream_t s);
+// Sum of n_partials doubles in a fixed order into *out (device scalar).
+int launch_finalize_sum(const double* partials, int64_t n, double* out, cudaStream_t s);
+// Sum of squares of x[0..n) into partials (fixed grid) then *out.
+int launch_sumsq(const double* x, int64_t n, double* partials, int64_t* n_partials, cudaStream_t s);
+int64_t sweep_partials_needed(const LevelView& L);
+int kernels_init();  // once per device
+int64_t sumsq_partials_needed(int64_t n);
+
+}  // namespace stmgb

@@ -1,0 +1,523 @@
+"""Python mirror of the reference's solver API over the stmg_b200 C ABI.
+
+Names, argument meaning and error behaviour follow the reference's C++ API
+(namespace ``stmg``; proj/include/stmg/*.hpp) so a caller of the reference
+can switch to the B200 path:
+
+    reference (C++)                         here
+    build_fine_grid (mesh.hpp:62)           build_fine_grid
+    apply_design (materials.hpp:48-49)      apply_design
+    load_vector (assembly.hpp:54-56)        load_vector
+    dof_is_masked (assembly.hpp:68)         dof_is_masked
+    plan_coarsening (strategy.hpp:104-105)  plan_coarsening
+    path_to_string (strategy.hpp:99)        path_to_string
+    parse_method (rediscretisation.hpp:45)  (method strings "CK", "CD", "CR")
+    build_hierarchy (multigrid.hpp:70-74)   build_hierarchy
+    transposed_hierarchy (multigrid.hpp:77) transposed_hierarchy
+    mg_solve (multigrid.hpp:107-108)        mg_solve
+    SolveOptions / SolveReport / SolveStatus
+
+Exceptions: std::invalid_argument -> ValueError, std::runtime_error ->
+RuntimeError, std::out_of_range -> IndexError (STMG_EINVAL / ERUNTIME / ERANGE).
+
+All compute runs in libstmg_b200.so on the GPU.  There is no CPU fallback:
+importing this module without the built extension raises ImportError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import os
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libstmg_b200.so")
+
+
+class StmgCudaError(RuntimeError):
+    pass
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"stmg_b200 CUDA extension not built ({LIB_PATH} missing); run "
+            "`python -c 'import __graft_entry__ as g; g.build()'` or paper_2505_10168_b200/build.py")
+    lib = C.CDLL(LIB_PATH)
+    i32, i64, f64, vp = C.c_int32, C.c_int64, C.c_double, C.c_void_p
+    lib.stmg_last_error.restype = C.c_char_p
+    lib.stmg_abi_version.restype = C.c_int
+    sig = {
+        "stmg_apply_design": [vp, i64, vp, vp, vp],
+        "stmg_load_vector": [vp, i32, vp, i32, vp],
+        "stmg_load_vector_cb": [vp, vp, vp, i32, vp],
+        "stmg_plan_coarsening": [vp, vp, vp, vp, vp, vp, vp, vp],
+        "stmg_hierarchy_create": [vp, vp, vp, vp, vp, C.c_char_p, i32, vp, i32, C.POINTER(vp)],
+        "stmg_hierarchy_transposed": [vp, C.POINTER(vp)],
+        "stmg_hierarchy_n_levels": [vp, C.POINTER(i32)],
+        "stmg_hierarchy_level_info": [vp, i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(f64)],
+        "stmg_hierarchy_level_coeffs": [vp, i32, vp, vp, vp, vp, vp, vp, vp],
+        "stmg_hierarchy_device_bytes": [vp, C.POINTER(i64)],
+        "stmg_mg_solve": [vp, vp, vp, vp, vp, vp, i32],
+        "stmg_level_sweeps": [vp, i32, vp, vp, i32, f64],
+        "stmg_level_residual": [vp, i32, vp, vp, vp],
+        "stmg_level_restrict_residual": [vp, i32, vp, vp, vp],
+        "stmg_level_restrict": [vp, i32, vp, vp],
+        "stmg_level_prolong_add": [vp, i32, vp, vp],
+        "stmg_coarsest_solve": [vp, vp, vp],
+        "stmg_residual_norm": [vp, vp, vp, C.POINTER(f64)],
+        "stmg_norm2": [vp, vp, i64, C.POINTER(f64)],
+        "stmg_synchronize": [vp],
+    }
+    for name, args in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = C.c_int
+    lib.stmg_hierarchy_destroy.argtypes = [vp]
+    lib.stmg_hierarchy_destroy.restype = None
+    return lib
+
+
+_lib = _load()
+
+STMG_OK, STMG_EINVAL, STMG_ERUNTIME, STMG_ERANGE, STMG_ECUDA, STMG_ENOMEM = range(6)
+
+
+def _check(rc: int):
+    if rc == STMG_OK:
+        return
+    msg = _lib.stmg_last_error().decode(errors="replace")
+    if rc == STMG_EINVAL:
+        raise ValueError(msg)
+    if rc == STMG_ERANGE:
+        raise IndexError(msg)
+    if rc == STMG_ENOMEM:
+        raise MemoryError(msg)
+    if rc == STMG_ECUDA:
+        raise StmgCudaError(msg)
+    raise RuntimeError(msg)
+
+
+# ---- C structs (include/stmg_b200.h) -------------------------------------------------
+class _Grid(C.Structure):
+    _fields_ = [("L", C.c_double), ("t_T", C.c_double), ("n_el", C.c_int64), ("n_t", C.c_int64)]
+
+
+class _Mat(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("k_ins", "k_con", "c_ins", "c_con", "p_k", "p_c")]
+
+
+class _PlanReq(C.Structure):
+    _fields_ = [("n_levels", C.c_int32), ("lambda_crit", C.c_double), ("strategy", C.c_int32),
+                ("reassembly", C.c_int32), ("min_elements", C.c_int64)]
+
+
+class _SolveOpts(C.Structure):
+    _fields_ = [("nu", C.c_int32), ("omega", C.c_double), ("tol", C.c_double),
+                ("div_tol", C.c_double), ("max_cycles", C.c_int32)]
+
+
+class _SolveRep(C.Structure):
+    _fields_ = [("status", C.c_int32), ("cycles", C.c_int32), ("factor", C.c_double),
+                ("absolute_norms", C.c_int32), ("n_history", C.c_int32), ("seconds", C.c_double),
+                ("device_seconds", C.c_double), ("smoother_dof_updates", C.c_double),
+                ("kernel_launches", C.c_int64)]
+
+
+# ---- enums ---------------------------------------------------------------------------
+class CoarseningDirection(enum.IntEnum):
+    SpaceX = 0
+    TimeT = 1
+    FullST = 2
+
+
+class ReassemblyMethod(enum.IntEnum):
+    K = 0
+    D = 1
+    R = 2
+    P = 3
+
+
+class PlanStrategy(enum.IntEnum):
+    Uniform = 0
+    Contrast = 1
+    Resolution = 2
+    DesignIndependent = 3
+
+
+class SolveStatus(enum.IntEnum):
+    Converged = 0
+    MaxCycles = 1
+    Diverged = 2
+
+
+def direction_name(d) -> str:
+    return {0: "x", 1: "t", 2: "xt"}[int(d)]
+
+
+def status_name(s) -> str:
+    return {0: "converged", 1: "max-cycles", 2: "diverged"}[int(s)]
+
+
+# ---- value types -----------------------------------------------------------------------
+@dataclass
+class MaterialPair:
+    k_ins: float = 0.0
+    k_con: float = 0.0
+    c_ins: float = 0.0
+    c_con: float = 0.0
+    p_k: float = 3.0
+    p_c: float = 2.0
+
+    def _c(self) -> _Mat:
+        return _Mat(self.k_ins, self.k_con, self.c_ins, self.c_con, self.p_k, self.p_c)
+
+    @classmethod
+    def of(cls, m) -> "MaterialPair":
+        return m if isinstance(m, MaterialPair) else cls(*m)
+
+
+@dataclass
+class SpaceTimeGrid:
+    """proj/include/stmg/mesh.hpp:27-59"""
+    L: float
+    t_T: float
+    n_el: int
+    n_t: int
+    k: Optional[np.ndarray] = None
+    c: Optional[np.ndarray] = None
+
+    @property
+    def dx(self) -> float:
+        return self.L / self.n_el
+
+    @property
+    def dt(self) -> float:
+        return self.t_T / self.n_t
+
+    def n_nodes(self) -> int:
+        return self.n_el + 1
+
+    def n_times(self) -> int:
+        return self.n_t + 1
+
+    def n_dofs(self) -> int:
+        return self.n_times() * self.n_nodes()
+
+    def flatten(self, n: int, i: int) -> int:
+        return n * self.n_nodes() + i
+
+    def unflatten(self, flat: int):
+        return divmod(flat, self.n_nodes())
+
+    def element_centre(self, e: int) -> float:
+        return (e + 0.5) * self.dx
+
+    def has_materials(self) -> bool:
+        return self.k is not None and self.c is not None and len(self.k) == self.n_el == len(self.c)
+
+    def _c(self) -> _Grid:
+        return _Grid(float(self.L), float(self.t_T), int(self.n_el), int(self.n_t))
+
+
+def build_fine_grid(L: float, t_T: float, n_el: int, n_t: int) -> SpaceTimeGrid:
+    if L <= 0.0 or t_T <= 0.0:
+        raise ValueError("build_fine_grid: non-positive extent")
+    if n_el <= 0 or n_t <= 0:
+        raise ValueError("build_fine_grid: non-positive count")
+    return SpaceTimeGrid(float(L), float(t_T), int(n_el), int(n_t))
+
+
+def _f64(a, n: Optional[int] = None) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if n is not None and a.size != n:
+        raise ValueError("size mismatch")
+    return a
+
+
+def _ptr(a) -> int:
+    """Data pointer of a float64 contiguous numpy array or torch tensor."""
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("expected a C-contiguous float64 array")
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        import torch
+
+        if a.dtype != torch.float64 or not a.is_contiguous():
+            raise ValueError("expected a contiguous float64 tensor")
+        return a.data_ptr()
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+def _numel(a) -> int:
+    return a.size if isinstance(a, np.ndarray) else a.numel()
+
+
+def apply_design(chi, mat) -> tuple[np.ndarray, np.ndarray]:
+    """k(chi), c(chi) per element (proj/src/materials.cpp:27-50)."""
+    chi = _f64(chi)
+    k = np.empty_like(chi)
+    c = np.empty_like(chi)
+    m = MaterialPair.of(mat)._c()
+    _check(_lib.stmg_apply_design(chi.ctypes.data, chi.size, C.byref(m), k.ctypes.data, c.ctypes.data))
+    return k, c
+
+
+_SOURCE_FN = C.CFUNCTYPE(C.c_double, C.c_double, C.c_double, C.c_void_p)
+
+
+def load_vector(g: SpaceTimeGrid, q: Optional[Callable[[float, float], float]] = None, *,
+                kind: Optional[int] = None, params: Sequence[float] = (), masked: bool = False,
+                out: Optional[np.ndarray] = None) -> np.ndarray:
+    """All-at-once load vector (proj/src/assembly.cpp:65-83).
+
+    Either a Python callable q(x, t) (the std::function overload; slow, for
+    small grids) or a preset source ``kind`` (configs.py) evaluated natively.
+    With kind=None and q=None the reference's heat_load_value is used
+    (proj/src/assembly.cpp:80-83).  masked=True zeroes the fixed DOFs as
+    assemble_system does (proj/src/assembly.cpp:128-130).
+    """
+    b = out if out is not None else np.empty(g.n_dofs(), np.float64)
+    if b.size != g.n_dofs() or b.dtype != np.float64:
+        raise ValueError("load_vector: output size mismatch")
+    gc = g._c()
+    if q is not None:
+        cb = _SOURCE_FN(lambda x, t, _ctx: float(q(x, t)))
+        _check(_lib.stmg_load_vector_cb(C.byref(gc), cb, None, 1 if masked else 0, b.ctypes.data))
+        return b
+    if kind is None:
+        kind = 3
+    p = (C.c_double * 4)(*list(params)[:4])
+    _check(_lib.stmg_load_vector(C.byref(gc), int(kind), p, 1 if masked else 0, b.ctypes.data))
+    return b
+
+
+def dof_is_masked(g: SpaceTimeGrid, flat: int) -> bool:
+    n, i = g.unflatten(flat)
+    return n == 0 or i == 0
+
+
+@dataclass
+class PlanRequest:
+    """proj/include/stmg/strategy.hpp:76-86"""
+    n_levels: int = 2
+    lambda_crit: float = 0.25
+    strategy: PlanStrategy = PlanStrategy.Contrast
+    reassembly: ReassemblyMethod = ReassemblyMethod.K
+    min_elements: int = 0
+    chi: Optional[np.ndarray] = None
+    mat: Optional[MaterialPair] = None
+
+
+@dataclass
+class CoarseningPath:
+    """proj/include/stmg/strategy.hpp:88-96"""
+    dirs: list = field(default_factory=list)
+    indicator_at_decision: list = field(default_factory=list)
+    strategy: PlanStrategy = PlanStrategy.Contrast
+    lambda_crit: float = 0.25
+    min_elements: int = 0
+
+    def n_levels(self) -> int:
+        return len(self.dirs) + 1
+
+
+def path_to_string(path: CoarseningPath) -> str:
+    return ",".join(direction_name(d) for d in path.dirs)
+
+
+def plan_coarsening(fine: SpaceTimeGrid, req: PlanRequest) -> CoarseningPath:
+    n = max(req.n_levels - 1, 0)
+    dirs = np.zeros(max(n, 1), np.int32)
+    ind = np.zeros(max(n, 1), np.float64)
+    k = None if fine.k is None else _f64(fine.k, fine.n_el)
+    c = None if fine.c is None else _f64(fine.c, fine.n_el)
+    chi = None if req.chi is None else _f64(req.chi, fine.n_el)
+    mat = None if req.mat is None else MaterialPair.of(req.mat)._c()
+    pr = _PlanReq(int(req.n_levels), float(req.lambda_crit), int(req.strategy), int(req.reassembly),
+                  int(req.min_elements))
+    gc = fine._c()
+    _check(_lib.stmg_plan_coarsening(C.byref(gc), None if k is None else k.ctypes.data,
+                                     None if c is None else c.ctypes.data,
+                                     None if chi is None else chi.ctypes.data,
+                                     None if mat is None else C.byref(mat), C.byref(pr),
+                                     dirs.ctypes.data, ind.ctypes.data))
+    return CoarseningPath([CoarseningDirection(int(d)) for d in dirs[:n]], [float(v) for v in ind[:n]],
+                          PlanStrategy(req.strategy), float(req.lambda_crit), int(req.min_elements))
+
+
+@dataclass
+class SolveOptions:
+    """proj/include/stmg/multigrid.hpp:83-89"""
+    nu: int = 5
+    omega: float = 0.5
+    tol: float = 1e-9
+    div_tol: float = 1e9
+    max_cycles: int = 100
+
+
+@dataclass
+class SolveReport:
+    """proj/include/stmg/multigrid.hpp:91-102 (+ device timing and work counters)"""
+    status: SolveStatus = SolveStatus.MaxCycles
+    cycles: int = 0
+    factor: float = 1.0
+    history: list = field(default_factory=list)
+    absolute_norms: bool = False
+    seconds: float = 0.0
+    device_seconds: float = 0.0
+    smoother_dof_updates: float = 0.0
+    kernel_launches: int = 0
+
+
+@dataclass
+class LevelInfo:
+    n_el: int
+    n_t: int
+    w_diri: float
+
+    @property
+    def n_dofs(self) -> int:
+        return (self.n_el + 1) * (self.n_t + 1)
+
+
+class LevelHierarchy:
+    """Device-resident hierarchy (proj/include/stmg/multigrid.hpp:51-65).
+
+    Owns the C handle; level operators, transfers and the coarsest exact solver
+    live on the GPU.  A hierarchy and its transpose share vector workspaces and
+    must not be solved concurrently (the reference never does,
+    proj/src/optimisation.cpp:132-139).
+    """
+
+    def __init__(self, handle: C.c_void_p, path: Optional[CoarseningPath], method: str, device: int,
+                 adjoint: bool = False, parent: Optional["LevelHierarchy"] = None):
+        self._h = handle
+        self.path = path
+        self.method = method
+        self.device = device
+        self.adjoint = adjoint
+        self._parent = parent  # keeps the shared workspace owner alive
+        n = C.c_int32()
+        _check(_lib.stmg_hierarchy_n_levels(self._h, C.byref(n)))
+        self._n_levels = n.value
+        self.levels = []
+        for l in range(self._n_levels):
+            ne, nt, w = C.c_int64(), C.c_int64(), C.c_double()
+            _check(_lib.stmg_hierarchy_level_info(self._h, l, C.byref(ne), C.byref(nt), C.byref(w)))
+            self.levels.append(LevelInfo(ne.value, nt.value, w.value))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.stmg_hierarchy_destroy(h)
+            self._h = None
+
+    def close(self):
+        self.__del__()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def n_levels(self) -> int:
+        return self._n_levels
+
+    def device_bytes(self) -> int:
+        b = C.c_int64()
+        _check(_lib.stmg_hierarchy_device_bytes(self._h, C.byref(b)))
+        return b.value
+
+    def level_coeffs(self, l: int) -> dict:
+        nn = self.levels[l].n_el + 1
+        arrs = [np.zeros(nn) for _ in range(7)]
+        _check(_lib.stmg_hierarchy_level_coeffs(self._h, l, *[a.ctypes.data for a in arrs]))
+        return dict(zip(["cur_m", "cur_0", "cur_p", "oth_m", "oth_0", "oth_p", "inv_diag"], arrs))
+
+    # -- level kernels on device vectors (torch tensors on this hierarchy's device) --
+    def sweeps(self, l, f, x, n, omega=0.5):
+        _check(_lib.stmg_level_sweeps(self._h, l, _ptr(f), _ptr(x), int(n), float(omega)))
+
+    def residual(self, l, f, x, r):
+        _check(_lib.stmg_level_residual(self._h, l, _ptr(f), _ptr(x), _ptr(r)))
+
+    def restrict_residual(self, l, f, x, fc):
+        _check(_lib.stmg_level_restrict_residual(self._h, l, _ptr(f), _ptr(x), _ptr(fc)))
+
+    def restrict(self, l, r, fc):
+        _check(_lib.stmg_level_restrict(self._h, l, _ptr(r), _ptr(fc)))
+
+    def prolong_add(self, l, xc, x):
+        _check(_lib.stmg_level_prolong_add(self._h, l, _ptr(xc), _ptr(x)))
+
+    def coarsest_solve(self, f, x):
+        _check(_lib.stmg_coarsest_solve(self._h, _ptr(f), _ptr(x)))
+
+    def residual_norm(self, f, x) -> float:
+        v = C.c_double()
+        _check(_lib.stmg_residual_norm(self._h, _ptr(f), _ptr(x), C.byref(v)))
+        return v.value
+
+    def norm2(self, x) -> float:
+        v = C.c_double()
+        _check(_lib.stmg_norm2(self._h, _ptr(x), _numel(x), C.byref(v)))
+        return v.value
+
+    def synchronize(self):
+        _check(_lib.stmg_synchronize(self._h))
+
+
+def build_hierarchy(fine: SpaceTimeGrid, method, path: CoarseningPath, chi=None, mat=None,
+                    device: int = 0) -> LevelHierarchy:
+    """proj/src/multigrid.cpp:86-143 (causal transfers; K, D or R coarse operators)."""
+    if not fine.has_materials():
+        raise ValueError("build_hierarchy: fine grid has no materials")
+    name = method if isinstance(method, str) else str(method)
+    k = _f64(fine.k, fine.n_el)
+    c = _f64(fine.c, fine.n_el)
+    chi_a = None if chi is None else _f64(chi.chi if hasattr(chi, "chi") else chi, fine.n_el)
+    m = None if mat is None else MaterialPair.of(mat)._c()
+    dirs = np.array([int(d) for d in path.dirs], np.int32)
+    h = C.c_void_p()
+    gc = fine._c()
+    _check(_lib.stmg_hierarchy_create(C.byref(gc), k.ctypes.data, c.ctypes.data,
+                                      None if chi_a is None else chi_a.ctypes.data,
+                                      None if m is None else C.byref(m), name.encode(), dirs.size,
+                                      dirs.ctypes.data if dirs.size else None, int(device),
+                                      C.byref(h)))
+    return LevelHierarchy(h, path, name, device)
+
+
+def transposed_hierarchy(h: LevelHierarchy) -> LevelHierarchy:
+    """proj/src/multigrid.cpp:145-160"""
+    out = C.c_void_p()
+    _check(_lib.stmg_hierarchy_transposed(h.handle, C.byref(out)))
+    return LevelHierarchy(out, h.path, h.method, h.device, adjoint=not h.adjoint, parent=h)
+
+
+def mg_solve(h: LevelHierarchy, b, u, opts: Optional[SolveOptions] = None) -> SolveReport:
+    """V-cycle solve of J u = b from the caller's u (warm start), u updated in place.
+
+    b and u may be numpy arrays (host) or torch tensors (host, pinned or on the
+    hierarchy's GPU); proj/src/multigrid.cpp:212-279.
+    """
+    o = opts or SolveOptions()
+    n = h.levels[0].n_dofs
+    if _numel(b) != n or _numel(u) != n:
+        raise ValueError("mg_solve: vector size mismatch")
+    hist = np.zeros(max(o.max_cycles, 0) + 1, np.float64)
+    rep = _SolveRep()
+    co = _SolveOpts(int(o.nu), float(o.omega), float(o.tol), float(o.div_tol), int(o.max_cycles))
+    _check(_lib.stmg_mg_solve(h.handle, _ptr(b), _ptr(u), C.byref(co), C.byref(rep), hist.ctypes.data,
+                              hist.size))
+    return SolveReport(SolveStatus(rep.status), rep.cycles, rep.factor,
+                       [float(v) for v in hist[: rep.n_history]], bool(rep.absolute_norms),
+                       rep.seconds, rep.device_seconds, rep.smoother_dof_updates, rep.kernel_launches)
+
+
+def abi_version() -> int:
+    return _lib.stmg_abi_version()

@@ -1,0 +1,118 @@
+"""Problem cases shared by the CPU (oracle vs reference) and GPU parity tests.
+
+Each case is a small seeded instance of one BASELINE config family (or of a
+reference unit-test situation) that the CPU checkers finish in seconds.
+Planning uses the C oracle's restatement of plan_coarsening; the test suite
+separately pins that planner to the reference's.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from paper_2505_10168_b200 import configs as C
+
+
+@dataclass
+class Case:
+    name: str
+    L: float
+    tT: float
+    n_el: int
+    n_t: int
+    k: np.ndarray
+    c: np.ndarray
+    chi: np.ndarray | None
+    mat: tuple | None
+    method: str
+    strategy: int
+    n_levels: int
+    min_elements: int = 0
+    adjoint: bool = False
+    nu: int = 1
+    tol: float = 1e-10
+    max_cycles: int = 100
+    source_kind: int = 0
+    source_params: tuple = (1.0,)
+    rhs: str = "load"
+    dirs: np.ndarray | None = None
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def reassembly(self) -> int:
+        return {"K": 0, "D": 1, "R": 2, "P": 3}[self.method[1]]
+
+    @property
+    def n_dofs(self) -> int:
+        return (self.n_el + 1) * (self.n_t + 1)
+
+    def plan(self, port):
+        if self.dirs is None:
+            self.dirs, _ = port.plan(self.L, self.tT, self.n_el, self.n_t, self.k, self.c, self.n_levels,
+                                     strategy=self.strategy, reassembly=self.reassembly,
+                                     min_elements=self.min_elements, chi=self.chi, mat=self.mat)
+        return self.dirs
+
+    def rhs_vector(self, port):
+        if self.rhs == "adjoint_uniform":
+            return C.adjoint_uniform_rhs(self.n_el, self.n_t, self.L, self.tT)
+        return port.load_vector(self.L, self.tT, self.n_el, self.n_t, self.source_kind,
+                                self.source_params)
+
+
+def _from_cfg(name, cfg, **kw) -> Case:
+    c = Case(name, cfg.L, cfg.t_T, cfg.n_el, cfg.n_t, cfg.k, cfg.c, cfg.chi, cfg.mat, cfg.method,
+             cfg.strategy, cfg.n_levels, cfg.min_elements, cfg.adjoint, cfg.nu, cfg.tol,
+             cfg.max_cycles, cfg.source_kind, cfg.source_params, cfg.rhs)
+    for k_, v in kw.items():
+        setattr(c, k_, v)
+    return c
+
+
+def _uniform(name, n_el, n_t, nl, strategy=C.PLAN_UNIFORM, method="CK", **kw) -> Case:
+    return Case(name, 1.0, 1.0, n_el, n_t, np.ones(n_el), np.ones(n_el), None, None, method,
+                strategy, nl, source_kind=3, source_params=(), **kw)
+
+
+def case(name: str) -> Case:
+    if name == "cfg0":  # BASELINE config 0 exactly: reference-default two-grid, V(1,1)
+        return _from_cfg(name, C.cfg0(), n_levels=2)
+    if name == "cfg0_deep":
+        return _from_cfg(name, C.cfg0(), n_levels=10, nu=2)
+    if name == "cfg1_mini":
+        return _from_cfg(name, C.cfg1(n_el=128, n_t=256), n_levels=8, nu=5)
+    if name == "cfg2_mini":
+        return _from_cfg(name, C.cfg2(n_el=256, n_t=512, min_elements=16), n_levels=9, nu=5)
+    if name == "cfg3_mini":
+        return _from_cfg(name, C.cfg3(n_el=256, n_t=512, min_elements=16), n_levels=9, nu=5)
+    if name == "cfg1_mini_adj":
+        return _from_cfg(name, C.cfg1(n_el=128, n_t=256), n_levels=8, nu=5, adjoint=True)
+    if name == "cfgD":  # design-averaging reassembly
+        cfg = C.cfg1(n_el=128, n_t=256)
+        cc = _from_cfg(name, cfg, n_levels=6, nu=5)
+        cc.method = "CD"
+        return cc
+    if name == "cfgK_contrast":
+        return _from_cfg(name, C.cfg1(n_el=128, n_t=256), n_levels=6, nu=5, method="CK")
+    if name == "time_first":  # proj/tests/test_multigrid.cpp:77-94 situation
+        return _uniform(name, 4, 256, 4, nu=5)
+    if name == "space_first":  # proj/tests/test_multigrid.cpp:55-75 situation
+        return _uniform(name, 32, 32, 4, nu=5)
+    if name == "single_level":  # proj/tests/test_multigrid.cpp:96-107
+        return _uniform(name, 8, 8, 1, nu=5)
+    if name == "tiny":  # one element, the hand-computed march (test_assembly.cpp:133-144)
+        return Case(name, 1.0, 3.0, 1, 3, np.ones(1), np.ones(1), None, None, "CK", C.PLAN_UNIFORM,
+                    1, source_kind=0, source_params=(1.0,), nu=1)
+    if name == "wide_short":  # n_el > 256 exercises multi-tile node blocks; n_t not a tile multiple
+        cc = _from_cfg(name, C.cfg2(n_el=1024, n_t=30, min_elements=0), n_levels=4, nu=2)
+        cc.strategy = C.PLAN_CONTRAST
+        return cc
+    if name == "cfg4_mini":
+        return _from_cfg(name, C.cfg4(n_el=256, n_t=1024), n_levels=8, nu=5)
+    raise KeyError(name)
+
+
+SMALL_CASES = ["cfg0", "cfg0_deep", "cfg1_mini", "cfg1_mini_adj", "cfg2_mini", "cfg3_mini", "cfgD",
+               "cfgK_contrast", "time_first", "space_first", "single_level", "tiny", "wide_short",
+               "cfg4_mini"]
