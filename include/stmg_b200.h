@@ -98,6 +98,14 @@ typedef struct stmg_solve_report {
   double device_seconds;       /* device time between the first and last kernel (CUDA events) */
   double smoother_dof_updates; /* sum over levels and cycles of Jacobi DOF updates */
   int64_t kernel_launches;     /* kernels this solve launched (graph nodes counted) */
+  /* Filled only when profiling is on (stmg_hierarchy_set_profiling): device time
+   * of the finest level's kernels, measured by CUDA events inside the graph. */
+  int64_t fine_sweeps;         /* plain fine-level Jacobi sweep launches timed */
+  double fine_sweep_seconds;   /* their summed device time */
+  int64_t fine_restricts;      /* fine-level residual+restriction launches timed */
+  double fine_restrict_seconds;
+  int64_t fine_prolong_sweeps; /* fused prolongation + first post-sweep launches */
+  double fine_prolong_sweep_seconds;
 } stmg_solve_report;
 
 typedef struct stmg_hierarchy stmg_hierarchy;
@@ -159,6 +167,13 @@ int stmg_hierarchy_level_info(const stmg_hierarchy* h, int32_t level, int64_t* n
 int stmg_hierarchy_level_coeffs(const stmg_hierarchy* h, int32_t level, double* cur_m,
                                 double* cur_0, double* cur_p, double* oth_m, double* oth_0,
                                 double* oth_p, double* inv_diag);
+/* Run this hierarchy's work on a caller stream (cudaStream_t, NULL restores the
+ * hierarchy's own stream).  Graphs are captured on a private stream and launched
+ * on this one. */
+int stmg_hierarchy_set_stream(stmg_hierarchy* h, void* cuda_stream);
+/* Record CUDA events around the finest level's kernels inside the V-cycle graph
+ * (on != 0); the timings appear in stmg_solve_report.  Off by default. */
+int stmg_hierarchy_set_profiling(stmg_hierarchy* h, int32_t on);
 /* Bytes of device memory the hierarchy holds. */
 int stmg_hierarchy_device_bytes(const stmg_hierarchy* h, int64_t* bytes);
 
@@ -190,6 +205,10 @@ int stmg_residual_norm(stmg_hierarchy* h, const double* f, const double* x, doub
 /* ||x||_2 over n doubles on the hierarchy's device */
 int stmg_norm2(stmg_hierarchy* h, const double* x, int64_t n, double* norm);
 int stmg_synchronize(stmg_hierarchy* h);
+
+/* Benchmarking knob, not part of the reference-facing surface: stencil kernel
+ * design (0 tiled NT=8 default, 1 tiled NT=4, 2 tiled NT=16, 3 warp streaming). */
+int stmg_debug_set_kernel_variant(int32_t variant);
 
 #ifdef __cplusplus
 }

@@ -132,11 +132,12 @@ def _mirror(a: np.ndarray) -> np.ndarray:
 def cfg0(n_el=128, n_t=128) -> Config:
     k = np.ones(n_el)
     c = np.ones(n_el)
+    # "default coarsening": the reference's PlanRequest default, two levels (strategy.hpp:77)
     return Config("cfg0", 1.0, 1.0, n_el, n_t, None, None, k, c, 0, (1.0,), "CK", PLAN_CONTRAST,
-                  n_levels=10, nu=1)
+                  n_levels=2, nu=1)
 
 
-def cfg1(n_el=1024, n_t=4096, seed=1, n_levels=14, nu=1) -> Config:
+def cfg1(n_el=1024, n_t=4096, seed=1, n_levels=10, nu=5) -> Config:
     rng = MT19937_64(seed)
     n_blocks = n_el // 16
     bits = [bernoulli_half(rng) for _ in range(n_blocks)]

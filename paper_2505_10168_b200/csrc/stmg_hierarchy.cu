@@ -370,7 +370,17 @@ struct Workspace {
 struct GraphKey {
   int nu;
   double omega;
-  bool operator<(const GraphKey& o) const { return std::tie(nu, omega) < std::tie(o.nu, o.omega); }
+  bool profiling;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(nu, omega, profiling) < std::tie(o.nu, o.omega, o.profiling);
+  }
+};
+
+enum TimedKind { kTimedSweep = 0, kTimedRestrict = 1, kTimedProlongSweep = 2 };
+
+struct TimedKernel {
+  int kind;
+  cudaEvent_t start, stop;
 };
 
 struct GraphEntry {
@@ -378,6 +388,7 @@ struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
   int64_t kernels = 0;
   int final_buf = 0;
+  std::vector<TimedKernel> timed;  // event pairs recorded inside the graph (profiling)
 };
 
 }  // namespace
@@ -394,7 +405,10 @@ struct stmg_hierarchy {
   stmgb::CoarsestView coarsest{};
   std::unique_ptr<stmgb::DeviceBuf> pcr_alpha, pcr_gamma, pcr_bfin;
   std::shared_ptr<stmgb::Workspace> ws;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;      // where work runs (own_stream or a caller's)
+  cudaStream_t own_stream = nullptr;  // created with the hierarchy
+  cudaStream_t cap_stream = nullptr;  // private stream for graph capture
+  bool profiling = false;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::map<stmgb::GraphKey, stmgb::GraphEntry> graphs;
   int64_t device_bytes = 0;
@@ -403,13 +417,19 @@ struct stmg_hierarchy {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
     for (auto& kv : graphs) {
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
       if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+      for (auto& t : kv.second.timed) {
+        cudaEventDestroy(t.start);
+        cudaEventDestroy(t.stop);
+      }
     }
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
-    if (stream) cudaStreamDestroy(stream);
+    if (own_stream) cudaStreamDestroy(own_stream);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
     coef.clear();
     pcr_alpha.reset();
     pcr_gamma.reset();
@@ -543,7 +563,9 @@ void finish_create(stmg_hierarchy* h, bool share_ws_from_other, const stmg_hiera
     h->ws = make_workspace(h, &bytes);
     h->device_bytes += bytes;
   }
-  cuda_check(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  cuda_check(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  cuda_check(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  h->stream = h->own_stream;
   cuda_check(cudaEventCreate(&h->ev0), "cudaEventCreate");
   cuda_check(cudaEventCreate(&h->ev1), "cudaEventCreate");
 }
@@ -558,6 +580,22 @@ struct Emitter {
   double omega;
   cudaStream_t s;
   int64_t kernels = 0;
+  std::vector<TimedKernel>* timed = nullptr;  // non-null: profile the finest level
+
+  template <class F>
+  void timed_launch(int l, int kind, F&& launch) {
+    if (timed && l == 0) {
+      TimedKernel t{kind, nullptr, nullptr};
+      cuda_check(cudaEventCreate(&t.start), "cudaEventCreate");
+      cuda_check(cudaEventCreate(&t.stop), "cudaEventCreate");
+      cuda_check(cudaEventRecordWithFlags(t.start, s, cudaEventRecordExternal), "event record");
+      launch();
+      cuda_check(cudaEventRecordWithFlags(t.stop, s, cudaEventRecordExternal), "event record");
+      timed->push_back(t);
+    } else {
+      launch();
+    }
+  }
 
   double* buf(int l, int which) {
     return which == 0 ? h->ws->xa[l]->p : h->ws->xb[l]->p;
@@ -590,24 +628,30 @@ struct Emitter {
       }
     }
     for (int k = 0; k < pre; ++k) {
-      launch_check(launch_sweep(h->adjoint, L, f, buf(l, cur), buf(l, 1 - cur), omega, nullptr,
-                                nullptr, s),
-                   "sweep");
+      timed_launch(l, kTimedSweep, [&] {
+        launch_check(launch_sweep(h->adjoint, L, f, buf(l, cur), buf(l, 1 - cur), omega, nullptr,
+                                  nullptr, s),
+                     "sweep");
+      });
       ++kernels;
       cur = 1 - cur;
     }
     const LevelView& C = h->views[l + 1];
-    launch_check(launch_restrict_residual(h->adjoint, L, C, h->dirs[l], f, buf(l, cur),
-                                          h->ws->f[l + 1]->p, s),
-                 "restrict");
+    timed_launch(l, kTimedRestrict, [&] {
+      launch_check(launch_restrict_residual(h->adjoint, L, C, h->dirs[l], f, buf(l, cur),
+                                            h->ws->f[l + 1]->p, s),
+                   "restrict");
+    });
     ++kernels;
     const int child = level(l + 1, 0, 0, true);
     const double* xc = buf(l + 1, child);
     int post = nu;
     if (nu >= 1) {
-      launch_check(launch_sweep_prolong(h->adjoint, L, C, h->dirs[l], f, buf(l, cur), xc,
-                                        buf(l, 1 - cur), omega, s),
-                   "sweep_prolong");
+      timed_launch(l, kTimedProlongSweep, [&] {
+        launch_check(launch_sweep_prolong(h->adjoint, L, C, h->dirs[l], f, buf(l, cur), xc,
+                                          buf(l, 1 - cur), omega, s),
+                     "sweep_prolong");
+      });
       ++kernels;
       cur = 1 - cur;
       post = nu - 1;
@@ -616,9 +660,11 @@ struct Emitter {
       ++kernels;
     }
     for (int k = 0; k < post; ++k) {
-      launch_check(launch_sweep(h->adjoint, L, f, buf(l, cur), buf(l, 1 - cur), omega, nullptr,
-                                nullptr, s),
-                   "sweep");
+      timed_launch(l, kTimedSweep, [&] {
+        launch_check(launch_sweep(h->adjoint, L, f, buf(l, cur), buf(l, 1 - cur), omega, nullptr,
+                                  nullptr, s),
+                     "sweep");
+      });
       ++kernels;
       cur = 1 - cur;
     }
@@ -629,15 +675,16 @@ struct Emitter {
 bool speculative(const stmg_hierarchy* h, int nu) { return h->n_levels() > 1 && nu >= 1; }
 
 GraphEntry& get_graph(stmg_hierarchy* h, int nu, double omega) {
-  const GraphKey key{nu, omega};
+  const GraphKey key{nu, omega, h->profiling};
   auto it = h->graphs.find(key);
   if (it != h->graphs.end()) return it->second;
   GraphEntry e;
-  Emitter em{h, nu, omega, h->stream};
-  cuda_check(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal), "capture");
+  Emitter em{h, nu, omega, h->cap_stream};
+  if (h->profiling) em.timed = &e.timed;
+  cuda_check(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal), "capture");
   const bool spec = speculative(h, nu);
   e.final_buf = em.level(0, spec ? 1 : 0, spec ? 1 : 0, false);
-  cuda_check(cudaStreamEndCapture(h->stream, &e.graph), "end capture");
+  cuda_check(cudaStreamEndCapture(h->cap_stream, &e.graph), "end capture");
   cuda_check(cudaGraphInstantiate(&e.exec, e.graph, 0), "graph instantiate");
   e.kernels = em.kernels;
   return h->graphs.emplace(key, e).first->second;
@@ -714,6 +761,8 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
   rep->cycles = 0;
   rep->factor = 1.0;
   rep->smoother_dof_updates = 0.0;
+  rep->fine_sweeps = rep->fine_restricts = rep->fine_prolong_sweeps = 0;
+  rep->fine_sweep_seconds = rep->fine_restrict_seconds = rep->fine_prolong_sweep_seconds = 0.0;
   double per_cycle_updates = 0.0;
   for (int l = 0; l + 1 < h->n_levels(); ++l) per_cycle_updates += 2.0 * o.nu * static_cast<double>(h->ndofs(l));
   if (r0 < o.tol) {
@@ -727,6 +776,20 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
       const bool more = cycle < o.max_cycles;
       launches += emit_norm(h, B, X, spec && more ? Y : nullptr, o.omega, 1);
       fetch_scalars(h, 2, sc);
+      for (const TimedKernel& t : g->timed) {
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, t.start, t.stop), "event elapsed");
+        if (t.kind == kTimedSweep) {
+          rep->fine_sweeps += 1;
+          rep->fine_sweep_seconds += ms * 1e-3;
+        } else if (t.kind == kTimedRestrict) {
+          rep->fine_restricts += 1;
+          rep->fine_restrict_seconds += ms * 1e-3;
+        } else {
+          rep->fine_prolong_sweeps += 1;
+          rep->fine_prolong_sweep_seconds += ms * 1e-3;
+        }
+      }
       const double rn = std::sqrt(sc[1]) / denom;
       history[nh++] = rn;
       rep->cycles = cycle;
@@ -975,6 +1038,22 @@ int stmg_hierarchy_level_coeffs(const stmg_hierarchy* h, int32_t l, double* cm, 
   });
 }
 
+int stmg_hierarchy_set_stream(stmg_hierarchy* h, void* cuda_stream) {
+  return guarded([&] {
+    checked(h);
+    DeviceGuard dg(h->device);
+    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+    h->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : h->own_stream;
+  });
+}
+
+int stmg_hierarchy_set_profiling(stmg_hierarchy* h, int32_t on) {
+  return guarded([&] {
+    checked(h);
+    h->profiling = on != 0;
+  });
+}
+
 int stmg_hierarchy_device_bytes(const stmg_hierarchy* h, int64_t* bytes) {
   return guarded([&] {
     if (!h || !bytes) throw std::invalid_argument("null argument");
@@ -1095,6 +1174,13 @@ int stmg_norm2(stmg_hierarchy* h, const double* x, int64_t n, double* norm) {
     fetch_scalars(h, 1, sc);
     *norm = std::sqrt(sc[0]);
   });
+}
+
+// Benchmarking knob (not part of the reference-facing API): select the stencil
+// kernel design (0 tiled NT=8 default, 1 tiled NT=4, 2 tiled NT=16, 3 warp
+// streaming).  Existing graphs keep the design they were captured with.
+int stmg_debug_set_kernel_variant(int32_t v) {
+  return guarded([&] { set_kernel_variant(v); });
 }
 
 int stmg_synchronize(stmg_hierarchy* h) {

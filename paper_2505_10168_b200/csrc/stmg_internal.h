@@ -67,6 +67,9 @@ int launch_finalize_sum(const double* partials, int64_t n, double* out, cudaStre
 int launch_sumsq(const double* x, int64_t n, double* partials, int64_t* n_partials, cudaStream_t s);
 int64_t sweep_partials_needed(const LevelView& L);
 int kernels_init();  // once per device
+// Kernel design selection for benchmarking (0 = production default).
+void set_kernel_variant(int v);
+int kernel_variant();
 int64_t sumsq_partials_needed(int64_t n);
 
 }  // namespace stmgb

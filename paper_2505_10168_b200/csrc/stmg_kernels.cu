@@ -170,54 +170,345 @@ __device__ __forceinline__ double block_sum(double v) {
 
 enum Mode { kSweep = 0, kResidual = 1, kNormOnly = 2 };
 
-// Thread column march: blockIdx.x = time tile (kNT levels), blockIdx.y = node
-// tile (blockDim.x nodes).  Same-level neighbours come from warp shuffles
-// (warp-edge lanes load them), the other time level is carried in registers.
-template <bool ADJ, int MODE, bool NORM, class Ld>
-__global__ void __launch_bounds__(kMaxTW) k_march(LevelView L, Ld ld, const double* __restrict__ f,
-                                                  double* __restrict__ y, double omega,
-                                                  double* __restrict__ partials) {
+// ---------------------------------------------------------------------------
+// Lean stencil kernels (production): blockIdx.x = time tile of NT levels,
+// blockIdx.y = node tile of blockDim.x nodes, one node column per thread.  No
+// shared memory and no block barrier: every global load of the tile (x on the
+// NT + 1 staged levels, f on the NT rows, and the strip-edge halo node of
+// lanes 0 / 31) is issued up front, same-level neighbours then come from warp
+// shuffles.  Tiles whose rows and nodes are all interior (the overwhelming
+// majority) take a branch-free path with the fixed interior lane order; the
+// rest use the general row evaluation.
+// ---------------------------------------------------------------------------
+template <bool ADJ, int MODE, bool NORM, int NT, int MINB, class Ld>
+__global__ void __launch_bounds__(kMaxTW, MINB) k_lean(LevelView L, Ld ld,
+                                                       const double* __restrict__ f,
+                                                       double* __restrict__ y, double omega,
+                                                       double* __restrict__ partials) {
   const int lane = threadIdx.x & 31;
   const int64_t nn = L.nn, nt = L.n_t;
   const int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
-  const int64_t n0 = (int64_t)blockIdx.x * kNT;
+  const int64_t n0 = (int64_t)blockIdx.x * NT;
+  const int64_t nbase = ADJ ? n0 : n0 - 1;  // level of staged row 0
+  const int64_t wfirst = i - lane;          // first node of this warp
   const bool valid = i < nn;
+  // rows n0..n0+NT-1 all have their coupled level and are unmasked in time
+  const bool rows_in = ADJ ? (n0 >= 1 && n0 + NT - 1 <= nt - 1) : (n0 >= 2 && n0 + NT - 1 <= nt);
+  const bool nodes_in = wfirst >= 2 && wfirst + 31 <= L.n_el - 1;
+  const int64_t ih = lane == 0 ? i - 1 : i + 1;  // halo node of the edge lanes
+  const bool edge = lane == 0 || lane == 31;
+  double xr[NT + 1], hr[NT + 1], fv[NT];
   Coefs c{};
-  if (valid) c = load_coefs(L, i);
-
-  auto fetch = [&](int64_t n, double& xm, double& x0, double& xp) {
-    x0 = valid ? ld(n, i) : 0.0;
-    xm = __shfl_up_sync(kFull, x0, 1);
-    xp = __shfl_down_sync(kFull, x0, 1);
-    if (lane == 0) xm = (valid && i >= 1) ? ld(n, i - 1) : 0.0;
-    if (lane == 31) xp = (i + 1 < nn) ? ld(n, i + 1) : 0.0;
-  };
-
   double acc = 0.0;
-  double xm = 0.0, x0 = 0.0, xp = 0.0, ym = 0.0, y0 = 0.0, yp = 0.0;
-  if (!ADJ) {
-    if (n0 >= 1) fetch(n0 - 1, ym, y0, yp);
+  if (rows_in && nodes_in) {
+    // ---- interior fast path: no bounds checks, fixed canonical lane order ----
+    const double* fp = f + n0 * nn + i;
+#pragma unroll
+    for (int k = 0; k < NT; ++k) fv[k] = fp[k * nn];
+#pragma unroll
+    for (int r = 0; r <= NT; ++r) {
+      xr[r] = ld(nbase + r, i);
+      hr[r] = edge ? ld(nbase + r, ih) : 0.0;
+    }
+    c = load_coefs(L, i);
+    double pm = 0.0, pp = 0.0;  // neighbours of staged row 0 / the previous row
+    {
+      pm = __shfl_up_sync(kFull, xr[0], 1);
+      pp = __shfl_down_sync(kFull, xr[0], 1);
+      if (lane == 0) pm = hr[0];
+      if (lane == 31) pp = hr[0];
+    }
+    double* yp = y + n0 * nn + i;
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const double x1 = xr[k + 1];
+      double qm = __shfl_up_sync(kFull, x1, 1);
+      double qp = __shfl_down_sync(kFull, x1, 1);
+      if (lane == 0) qm = hr[k + 1];
+      if (lane == 31) qp = hr[k + 1];
+      double s0, s1, s2, s3, x0;
+      if (!ADJ) {  // row n0+k: level = staged k+1 (q), coupled = staged k (p)
+        x0 = x1;
+        s0 = (0.0 + c.om * pm) + c.c0 * x1;
+        s1 = (0.0 + c.o0 * xr[k]) + c.cp * qp;
+        s2 = 0.0 + c.op * pp;
+        s3 = 0.0 + c.cm * qm;
+      } else {  // row n0+k: level = staged k (p), coupled = staged k+1 (q)
+        x0 = xr[k];
+        s0 = (0.0 + c.cm * pm) + c.o0 * x1;
+        s1 = (0.0 + c.c0 * x0) + c.op * qp;
+        s2 = 0.0 + c.cp * pp;
+        s3 = 0.0 + c.om * qm;
+      }
+      const double r = fv[k] - ((s0 + s1) + (s2 + s3));
+      if (NORM) acc = acc + r * r;
+      if (MODE == kSweep) yp[k * nn] = x0 + omega * (r * c.invd);
+      else if (MODE == kResidual) yp[k * nn] = r;
+      pm = qm;
+      pp = qp;
+    }
   } else {
-    fetch(n0, xm, x0, xp);
+    // ---- general path (time-boundary tiles, boundary nodes, partial tiles) ----
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const int64_t n = n0 + k;
+      fv[k] = (valid && n <= nt) ? f[n * nn + i] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r <= NT; ++r) {
+      const int64_t n = nbase + r;
+      const bool nok = n >= 0 && n <= nt;
+      xr[r] = (nok && valid) ? ld(n, i) : 0.0;
+      hr[r] = (nok && edge && ih >= 0 && ih < nn) ? ld(n, ih) : 0.0;
+    }
+    if (valid) c = load_coefs(L, i);
+    double pm = __shfl_up_sync(kFull, xr[0], 1);
+    double pp = __shfl_down_sync(kFull, xr[0], 1);
+    if (lane == 0) pm = hr[0];
+    if (lane == 31) pp = hr[0];
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const int64_t n = n0 + k;
+      if (n > nt) break;
+      const double x1 = xr[k + 1];
+      double qm = __shfl_up_sync(kFull, x1, 1);
+      double qp = __shfl_down_sync(kFull, x1, 1);
+      if (lane == 0) qm = hr[k + 1];
+      if (lane == 31) qp = hr[k + 1];
+      if (valid) {
+        // J: level = staged k+1 (q), coupled = staged k (p); J^T: the reverse
+        const double row = ADJ ? row_sum<true>(L, n, i, c, pm, xr[k], pp, qm, x1, qp)
+                               : row_sum<false>(L, n, i, c, qm, x1, qp, pm, xr[k], pp);
+        const double x0 = ADJ ? xr[k] : x1;
+        const double r = fv[k] - row;
+        if (NORM) acc = acc + r * r;
+        if (MODE == kSweep) {
+          const double id = (n == 0 || i == 0) ? L.inv_w : c.invd;
+          y[n * nn + i] = x0 + omega * (r * id);
+        } else if (MODE == kResidual) {
+          y[n * nn + i] = r;
+        }
+      }
+      pm = qm;
+      pp = qp;
+    }
+  }
+  if (NORM) {
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) partials[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+// f_c = R (f - J x) over one lean tile, R = s P^T (proj/src/transfer.cpp:95-104);
+// the fine residual never reaches memory.  x step (DIR 0): lane l computes the
+// residual at its node (lane 0 also at the node before its strip, from an
+// extra halo), lanes 0..15 gather nodes 2I-1, 2I, 2I+1 of coarse node
+// I = wfirst/2 + l by shuffles.  Causal t step (DIR 1): coarse level N takes
+// fine levels 2N, 2N+1 at the same node (NT is even, tiles start even).
+template <bool ADJ, int DIR, int NT>
+__global__ void __launch_bounds__(kMaxTW, 2) k_lean_restrict(LevelView F, LevelView C,
+                                                             const double* __restrict__ f,
+                                                             const double* __restrict__ x,
+                                                             double* __restrict__ fc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nn = F.nn, nt = F.n_t, nnc = C.nn;
+  const int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
+  const int64_t n0 = (int64_t)blockIdx.x * NT;
+  const int64_t nbase = ADJ ? n0 : n0 - 1;
+  const int64_t wfirst = i - lane;
+  const bool valid = i < nn;
+  const int64_t ih = lane == 0 ? i - 1 : i + 1;
+  const bool edge = lane == 0 || lane == 31;
+  const bool x2 = DIR == 0 && lane == 0 && i >= 2;   // node i - 2 for the extra residual
+  const bool xr1 = DIR == 0 && lane == 0 && i >= 1;  // extra residual at node i - 1
+  double xr[NT + 1], hr[NT + 1], h2[NT + 1], fv[NT], f1[NT];
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    const int64_t n = n0 + k;
+    fv[k] = (valid && n <= nt) ? f[n * nn + i] : 0.0;
+    f1[k] = (xr1 && n <= nt) ? f[n * nn + i - 1] : 0.0;
   }
 #pragma unroll
-  for (int t = 0; t < kNT; ++t) {
-    const int64_t n = n0 + t;
+  for (int r = 0; r <= NT; ++r) {
+    const int64_t n = nbase + r;
+    const bool nok = n >= 0 && n <= nt;
+    xr[r] = (nok && valid) ? x[n * nn + i] : 0.0;
+    hr[r] = (nok && edge && ih >= 0 && ih < nn) ? x[n * nn + ih] : 0.0;
+    h2[r] = (nok && x2) ? x[n * nn + i - 2] : 0.0;
+  }
+  Coefs c{}, ch{};
+  if (valid) c = load_coefs(F, i);
+  if (xr1) ch = load_coefs(F, i - 1);
+  double pm = __shfl_up_sync(kFull, xr[0], 1);
+  double pp = __shfl_down_sync(kFull, xr[0], 1);
+  if (lane == 0) pm = hr[0];
+  if (lane == 31) pp = hr[0];
+  double r_even = 0.0;
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    const int64_t n = n0 + k;
     if (n > nt) break;
-    if (!ADJ) {
-      fetch(n, xm, x0, xp);
-    } else {
-      if (n + 1 <= nt) {
-        fetch(n + 1, ym, y0, yp);
+    const double x1 = xr[k + 1];
+    double qm = __shfl_up_sync(kFull, x1, 1);
+    double qp = __shfl_down_sync(kFull, x1, 1);
+    if (lane == 0) qm = hr[k + 1];
+    if (lane == 31) qp = hr[k + 1];
+    // (cur, oth) triples at nodes (i-1, i, i+1): J uses staged k+1 / k, J^T k / k+1
+    double r = 0.0;
+    if (valid)
+      r = fv[k] - (ADJ ? row_sum<true>(F, n, i, c, pm, xr[k], pp, qm, x1, qp)
+                       : row_sum<false>(F, n, i, c, qm, x1, qp, pm, xr[k], pp));
+    if (DIR == 0) {
+      double r1 = 0.0;  // residual at node i - 1 (lane 0): triples at nodes i-2, i-1, i
+      if (xr1)
+        r1 = f1[k] - (ADJ ? row_sum<true>(F, n, i - 1, ch, h2[k], hr[k], xr[k], h2[k + 1], hr[k + 1], x1)
+                          : row_sum<false>(F, n, i - 1, ch, h2[k + 1], hr[k + 1], x1, h2[k], hr[k], xr[k]));
+      const int src = 2 * lane;
+      const double ra = __shfl_sync(kFull, r, (src - 1) & 31);
+      const double rb = __shfl_sync(kFull, r, src & 31);
+      const double rc = __shfl_sync(kFull, r, (src + 1) & 31);
+      if (lane < 16) {
+        const int64_t I = wfirst / 2 + lane;
+        if (I < nnc) {
+          Acc a;
+          if (I >= 1) a.add(0.5 * (lane == 0 ? r1 : ra));
+          a.add(1.0 * rb);
+          if (2 * I + 1 <= F.n_el) a.add(0.5 * rc);
+          fc[n * nnc + I] = a.result();
+        }
+      }
+    } else if (valid) {
+      if ((k & 1) == 0) {
+        r_even = r;
+        if (n == nt) {  // last coarse level: truncated row, 0.5 * r(2N) only
+          Acc a;
+          a.add(0.5 * r);
+          fc[(n >> 1) * nnc + i] = a.result();
+        }
       } else {
-        ym = 0.0;
-        y0 = 0.0;
-        yp = 0.0;
+        Acc a;
+        a.add(0.5 * r_even);
+        a.add(0.5 * r);
+        fc[(n >> 1) * nnc + i] = a.result();
       }
     }
-    if (valid) {
-      const double row = row_sum<ADJ>(L, n, i, c, xm, x0, xp, ym, y0, yp);
-      const double r = f[n * nn + i] - row;
+    pm = qm;
+    pp = qp;
+  }
+}
+
+// Elementwise kernels on a level, 2-D grid (no 64-bit division): blockIdx.x =
+// time tile of kFlatNT levels, blockIdx.y = node tile of blockDim.x nodes.
+constexpr int kFlatNT = 8;
+
+__global__ void k_sweep_from_zero2(LevelView L, const double* __restrict__ f, double* __restrict__ y,
+                                   double omega) {
+  const int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
+  if (i >= L.nn) return;
+  const int64_t n0 = (int64_t)blockIdx.x * kFlatNT;
+  const double idv = __ldg(L.coef + kInvD * L.nn + i);
+#pragma unroll
+  for (int k = 0; k < kFlatNT; ++k) {
+    const int64_t n = n0 + k;
+    if (n > L.n_t) break;
+    const double id = (n == 0 || i == 0) ? L.inv_w : idv;
+    y[n * L.nn + i] = 0.0 + omega * (f[n * L.nn + i] * id);
+  }
+}
+
+template <int DIR>
+__global__ void k_prolong_add2(LevelView F, LevelView C, const double* __restrict__ xc,
+                               double* __restrict__ x) {
+  const int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
+  if (i >= F.nn) return;
+  const int64_t n0 = (int64_t)blockIdx.x * kFlatNT;
+#pragma unroll
+  for (int k = 0; k < kFlatNT; ++k) {
+    const int64_t n = n0 + k;
+    if (n > F.n_t) break;
+    x[n * F.nn + i] = x[n * F.nn + i] + prolong_row<DIR>(xc, C.nn, n, i);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Tiled stencil kernels: blockIdx.x = time tile of NT levels, blockIdx.y =
+// node tile of TW = blockDim.x nodes.  Tile row r holds time level nbase + r
+// (nbase = n0 - 1 for J, n0 for J^T), so row pairs (r, r + 1) are a level and
+// its coupled level.  Every global load of the tile is issued before the
+// shared-memory stores, so each thread has ~2 NT + 1 independent loads in
+// flight; then one barrier, then the rows are evaluated from shared memory.
+// ---------------------------------------------------------------------------
+struct TileGeom {
+  int64_t i0, n0, nbase;
+};
+
+template <bool ADJ, int NT>
+__device__ __forceinline__ TileGeom tile_geom() {
+  TileGeom g;
+  g.i0 = (int64_t)blockIdx.y * blockDim.x;
+  g.n0 = (int64_t)blockIdx.x * NT;
+  g.nbase = ADJ ? g.n0 : g.n0 - 1;
+  return g;
+}
+
+template <int NT, int HL, int HR, class Ld>
+__device__ __forceinline__ void stage_x(const LevelView& L, const Ld& ld, const TileGeom& g,
+                                        double* tile, double (&own)[NT + 1]) {
+  const int t = threadIdx.x, tw = blockDim.x, W = tw + HL + HR;
+  const int64_t i = g.i0 + t;
+  double halo[NT + 1];
+  const bool is_halo = t < HL + HR;
+  const int64_t ih = t < HL ? g.i0 - HL + t : g.i0 + tw + (t - HL);
+  const int hcol = t < HL ? t : HL + tw + (t - HL);
+#pragma unroll
+  for (int r = 0; r <= NT; ++r) {
+    const int64_t n = g.nbase + r;
+    const bool nok = n >= 0 && n <= L.n_t;
+    own[r] = (nok && i < L.nn) ? ld(n, i) : 0.0;
+    halo[r] = (is_halo && nok && ih >= 0 && ih < L.nn) ? ld(n, ih) : 0.0;
+  }
+#pragma unroll
+  for (int r = 0; r <= NT; ++r) {
+    tile[r * W + HL + t] = own[r];
+    if (is_halo) tile[r * W + hcol] = halo[r];
+  }
+}
+
+template <bool ADJ, int MODE, bool NORM, int NT, int MINB, class Ld>
+__global__ void __launch_bounds__(kMaxTW, MINB) k_tile(LevelView L, Ld ld,
+                                                       const double* __restrict__ f,
+                                                       double* __restrict__ y, double omega,
+                                                       double* __restrict__ partials) {
+  extern __shared__ double tile[];
+  const TileGeom g = tile_geom<ADJ, NT>();
+  const int t = threadIdx.x, W = blockDim.x + 2;
+  const int64_t nn = L.nn, nt = L.n_t;
+  const int64_t i = g.i0 + t;
+  const bool valid = i < nn;
+  double own[NT + 1];
+  double fv[NT];
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    const int64_t n = g.n0 + k;
+    fv[k] = (valid && n <= nt) ? f[n * nn + i] : 0.0;
+  }
+  Coefs c{};
+  if (valid) c = load_coefs(L, i);
+  stage_x<NT, 1, 1>(L, ld, g, tile, own);
+  __syncthreads();
+  double acc = 0.0;
+  if (valid) {
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const int64_t n = g.n0 + k;
+      if (n > nt) break;
+      const int rc = ADJ ? k : k + 1;
+      const int ro = ADJ ? k + 1 : k;
+      const double* cur = tile + rc * W + t;
+      const double* oth = tile + ro * W + t;
+      const double x0 = own[rc];
+      const double row = row_sum<ADJ>(L, n, i, c, cur[0], x0, cur[2], oth[0], oth[1], oth[2]);
+      const double r = fv[k] - row;
       if (NORM) acc = acc + r * r;
       if (MODE == kSweep) {
         const double id = (n == 0 || i == 0) ? L.inv_w : c.invd;
@@ -226,20 +517,278 @@ __global__ void __launch_bounds__(kMaxTW) k_march(LevelView L, Ld ld, const doub
         y[n * nn + i] = r;
       }
     }
-    if (!ADJ) {
-      ym = xm;
-      y0 = x0;
-      yp = xp;
-    } else {
-      xm = ym;
-      x0 = y0;
-      xp = yp;
-    }
   }
   if (NORM) {
     const double s = block_sum(acc);
     if (threadIdx.x == 0) partials[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
   }
+}
+
+template <bool ADJ, int DIR, int NT>
+__global__ void __launch_bounds__(kMaxTW) k_restrict_tile(LevelView F, LevelView C,
+                                                          const double* __restrict__ f,
+                                                          const double* __restrict__ x,
+                                                          double* __restrict__ fc) {
+  extern __shared__ double smem[];
+  const TileGeom g = tile_geom<ADJ, NT>();
+  const int t = threadIdx.x, tw = blockDim.x;
+  const int64_t nn = F.nn, nt = F.n_t, nnc = C.nn;
+  const PlainLoad ld{x, nn};
+  constexpr int HL = DIR == 0 ? 2 : 1;
+  const int W = tw + HL + 1;
+  double* tile = smem;
+  double own[NT + 1];
+  const int64_t i = g.i0 + t;
+  double fv[NT], fh[NT];
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    const int64_t n = g.n0 + k;
+    fv[k] = (i < nn && n <= nt) ? f[n * nn + i] : 0.0;
+    fh[k] = (DIR == 0 && t == 0 && g.i0 >= 1 && n <= nt) ? f[n * nn + g.i0 - 1] : 0.0;
+  }
+  Coefs c{}, ch{};
+  if (i < nn) c = load_coefs(F, i);
+  if (DIR == 0 && t == 0 && g.i0 >= 1) ch = load_coefs(F, g.i0 - 1);
+  stage_x<NT, HL, 1>(F, ld, g, tile, own);
+  __syncthreads();
+  auto resid = [&](int k, int col, int64_t node, const Coefs& cc, double fval) -> double {
+    const int64_t n = g.n0 + k;
+    const int rc = ADJ ? k : k + 1;
+    const int ro = ADJ ? k + 1 : k;
+    const double* cur = tile + rc * W + col;
+    const double* oth = tile + ro * W + col;
+    return fval - row_sum<ADJ>(F, n, node, cc, cur[-1], cur[0], cur[1], oth[-1], oth[0], oth[1]);
+  };
+  if (DIR == 0) {
+    double* R = smem + (NT + 1) * W;  // NT rows x (tw + 1): column j <-> node i0 - 1 + j
+    const int RW = tw + 1;
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      if (g.n0 + k > nt) break;
+      if (i < nn) R[k * RW + t + 1] = resid(k, HL + t, i, c, fv[k]);
+      if (t == 0) R[k * RW] = g.i0 >= 1 ? resid(k, HL - 1, g.i0 - 1, ch, fh[k]) : 0.0;
+    }
+    __syncthreads();
+    if (t < tw / 2) {
+      const int64_t I = g.i0 / 2 + t;
+      if (I < nnc) {
+#pragma unroll
+        for (int k = 0; k < NT; ++k) {
+          const int64_t n = g.n0 + k;
+          if (n > nt) break;
+          const double* rr = R + k * RW + 2 * t;  // nodes 2I-1, 2I, 2I+1
+          Acc a;
+          if (I >= 1) a.add(0.5 * rr[0]);
+          a.add(1.0 * rr[1]);
+          if (2 * I + 1 <= F.n_el) a.add(0.5 * rr[2]);
+          fc[n * nnc + I] = a.result();
+        }
+      }
+    }
+  } else {
+    if (i >= nn) return;
+    double rv[NT];
+#pragma unroll
+    for (int k = 0; k < NT; ++k) rv[k] = (g.n0 + k <= nt) ? resid(k, HL + t, i, c, fv[k]) : 0.0;
+#pragma unroll
+    for (int s2 = 0; s2 < NT / 2; ++s2) {
+      const int64_t n2 = g.n0 + 2 * s2;  // fine level 2N
+      if (n2 > nt) break;
+      Acc a;
+      a.add(0.5 * rv[2 * s2]);
+      if (n2 + 1 <= nt) a.add(0.5 * rv[2 * s2 + 1]);
+      fc[(n2 / 2) * nnc + i] = a.result();
+    }
+  }
+}
+
+// Streaming stencil kernels.  Block (blockIdx.x, blockIdx.y) covers node tile
+// [i0, i0 + TW) (TW = blockDim.x) for rows n in [nA, nB), a long chunk of time
+// levels; each warp streams its own 32-node strip through the chunk with no
+// block barrier (a barrier would wait on the prefetched loads).  A rolling
+// register queue keeps the next kQ levels' loads in flight (x, f, and the
+// strip-edge halo nodes loaded by lanes 0 and 31), so every vector element is
+// read from HBM once per pass with ~2 kQ independent loads per thread
+// outstanding.  Same-level neighbours come from warp shuffles.
+//   J   (ADJ = false): step j stages level m = nA - 1 + j, computes row m.
+//   J^T (ADJ = true) : step j stages level m = nA + j,     computes row m - 1.
+constexpr int kQ = 8;  // prefetch depth (levels)
+
+struct StreamGeom {
+  int64_t i0, nA, nB, first, count;
+};
+
+template <bool ADJ>
+__device__ __forceinline__ StreamGeom stream_geom(const LevelView& L, int64_t chunk) {
+  StreamGeom g;
+  g.i0 = (int64_t)blockIdx.y * blockDim.x;
+  g.nA = (int64_t)blockIdx.x * chunk;
+  g.nB = g.nA + chunk < L.n_t + 1 ? g.nA + chunk : L.n_t + 1;
+  g.first = ADJ ? g.nA : g.nA - 1;
+  g.count = g.nB - g.nA + 1;  // levels staged; rows computed at steps 1 .. count-1
+  return g;
+}
+
+// One staged level as seen by a lane: x at i-1, i, i+1, and (X2, lane 0 of a
+// strip only) x at i-2 plus f at i-1 for the extra residual of restriction.
+struct Staged {
+  double xm, x0, xp, x2, f, f1;
+};
+
+// Drives the per-level pipeline of a warp strip and calls
+// body(m, cur, prev) for every staged level m after the first, where cur is
+// level m and prev level m - 1.
+template <bool X2, class Ld, class Body>
+__device__ __forceinline__ void warp_stream(const LevelView& L, const Ld& ld,
+                                            const double* __restrict__ f, const StreamGeom& g,
+                                            Body&& body) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nn = L.nn;
+  const int64_t i = g.i0 + threadIdx.x;
+  const bool own_ok = i < nn;
+  // lane 0 loads i-1 (and i-2), lane 31 loads i+1
+  const int64_t ih = lane == 0 ? i - 1 : i + 1;
+  const bool has_h = (lane == 0 || lane == 31) && ih >= 0 && ih < nn;
+  const bool has_h2 = X2 && lane == 0 && i - 2 >= 0 && i - 2 < nn;
+  const bool has_f1 = X2 && lane == 0 && i - 1 >= 0 && i - 1 < nn;
+  double qx[kQ], qh[kQ], qf[kQ], qx2[kQ], qf1[kQ];
+  auto load = [&](int64_t m, int k) {
+    const bool mok = m >= 0 && m <= L.n_t;
+    qx[k] = (mok && own_ok) ? ld(m, i) : 0.0;
+    qh[k] = (mok && has_h) ? ld(m, ih) : 0.0;
+    qf[k] = (mok && own_ok) ? f[m * nn + i] : 0.0;
+    if (X2) {
+      qx2[k] = (mok && has_h2) ? ld(m, i - 2) : 0.0;
+      qf1[k] = (mok && has_f1) ? f[m * nn + i - 1] : 0.0;
+    }
+  };
+#pragma unroll
+  for (int k = 0; k < kQ; ++k)
+    if (k < g.count) load(g.first + k, k);
+  Staged prev{0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int64_t base = 0; base < g.count; base += kQ) {
+#pragma unroll
+    for (int k = 0; k < kQ; ++k) {
+      const int64_t j = base + k;
+      if (j >= g.count) break;
+      Staged cur;
+      cur.x0 = qx[k];
+      const double h = qh[k];
+      cur.f = qf[k];
+      cur.x2 = X2 ? qx2[k] : 0.0;
+      cur.f1 = X2 ? qf1[k] : 0.0;
+      if (j + kQ < g.count) load(g.first + j + kQ, k);
+      cur.xm = __shfl_up_sync(kFull, cur.x0, 1);
+      cur.xp = __shfl_down_sync(kFull, cur.x0, 1);
+      if (lane == 0) cur.xm = h;
+      if (lane == 31) cur.xp = h;
+      if (j >= 1) body(g.first + j, cur, prev);
+      prev = cur;
+    }
+  }
+}
+
+// Damped-Jacobi sweep / residual / residual-norm pass over a level.
+template <bool ADJ, int MODE, bool NORM, class Ld>
+__global__ void __launch_bounds__(kMaxTW, 2) k_stream(LevelView L, Ld ld, const double* __restrict__ f,
+                                                      double* __restrict__ y, double omega,
+                                                      double* __restrict__ partials, int64_t chunk) {
+  const StreamGeom g = stream_geom<ADJ>(L, chunk);
+  const int64_t nn = L.nn;
+  const int64_t i = g.i0 + threadIdx.x;
+  const bool valid = i < nn;
+  Coefs c{};
+  if (valid) c = load_coefs(L, i);
+  double acc = 0.0;
+  warp_stream<false>(L, ld, f, g, [&](int64_t m, const Staged& cu, const Staged& pv) {
+    if (!valid) return;
+    const int64_t n = ADJ ? m - 1 : m;  // row
+    const Staged& rowl = ADJ ? pv : cu;  // level n
+    const Staged& oth = ADJ ? cu : pv;   // coupled level
+    const double row = row_sum<ADJ>(L, n, i, c, rowl.xm, rowl.x0, rowl.xp, oth.xm, oth.x0, oth.xp);
+    const double r = rowl.f - row;
+    if (NORM) acc = acc + r * r;
+    if (MODE == kSweep) {
+      const double id = (n == 0 || i == 0) ? L.inv_w : c.invd;
+      y[n * nn + i] = rowl.x0 + omega * (r * id);
+    } else if (MODE == kResidual) {
+      y[n * nn + i] = r;
+    }
+  });
+  if (NORM) {
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) partials[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+// f_c = R (f - J x), R = s P^T (proj/src/transfer.cpp:95-104); the fine
+// residual never reaches memory.  x step (DIR 0): lane l of a strip computes
+// the residual at node i0 + l (lane 0 also at i0 - 1), lanes 0..15 then gather
+// nodes 2I-1, 2I, 2I+1 of coarse node I = (i0 + 2l) / 2 by shuffles.  Causal t
+// step (DIR 1): coarse level N = (fine 2N, fine 2N+1) at the same node; time
+// chunks are even so pairs never straddle blocks.
+template <bool ADJ, int DIR>
+__global__ void __launch_bounds__(kMaxTW, 2) k_restrict_stream(LevelView F, LevelView C,
+                                                               const double* __restrict__ f,
+                                                               const double* __restrict__ x,
+                                                               double* __restrict__ fc,
+                                                               int64_t chunk) {
+  const StreamGeom g = stream_geom<ADJ>(F, chunk);
+  const int lane = threadIdx.x & 31;
+  const int64_t nn = F.nn, nnc = C.nn;
+  const int64_t i = g.i0 + threadIdx.x;
+  const int64_t istrip = i - lane;  // first node of this warp's strip (even)
+  const bool valid = i < nn;
+  const PlainLoad ld{x, nn};
+  Coefs c{}, ch{};
+  if (valid) c = load_coefs(F, i);
+  if (DIR == 0 && lane == 0 && i >= 1 && i - 1 < nn) ch = load_coefs(F, i - 1);
+  double r_even = 0.0;
+  warp_stream<DIR == 0>(F, ld, f, g, [&](int64_t m, const Staged& cu, const Staged& pv) {
+    const int64_t n = ADJ ? m - 1 : m;
+    const Staged& rowl = ADJ ? pv : cu;
+    const Staged& oth = ADJ ? cu : pv;
+    double r = 0.0;
+    if (valid)
+      r = rowl.f - row_sum<ADJ>(F, n, i, c, rowl.xm, rowl.x0, rowl.xp, oth.xm, oth.x0, oth.xp);
+    if (DIR == 0) {
+      double r1 = 0.0;  // residual at node i - 1 (lane 0 only)
+      if (lane == 0 && i >= 1 && i - 1 < nn)
+        r1 = rowl.f1 - row_sum<ADJ>(F, n, i - 1, ch, rowl.x2, rowl.xm, rowl.x0, oth.x2, oth.xm,
+                                    oth.x0);
+      // lane l < 16: coarse node I = istrip/2 + l needs r at fine lanes 2l-1, 2l, 2l+1
+      const int src = 2 * lane;
+      const double ra = __shfl_sync(kFull, r, (src - 1) & 31);
+      const double rb = __shfl_sync(kFull, r, src & 31);
+      const double rc = __shfl_sync(kFull, r, (src + 1) & 31);
+      if (lane < 16) {
+        const int64_t I = istrip / 2 + lane;
+        if (I < nnc && 2 * I <= F.n_el) {
+          const double rm1 = lane == 0 ? r1 : ra;
+          Acc a;
+          if (I >= 1) a.add(0.5 * rm1);
+          a.add(1.0 * rb);
+          if (2 * I + 1 <= F.n_el) a.add(0.5 * rc);
+          fc[n * nnc + I] = a.result();
+        }
+      }
+    } else {
+      if (!valid) return;
+      if ((n & 1) == 0) {
+        r_even = r;
+        if (n == F.n_t) {  // last coarse level: truncated row (0.5 * r(2N) only)
+          Acc a;
+          a.add(0.5 * r);
+          fc[(n >> 1) * nnc + i] = a.result();
+        }
+      } else {
+        Acc a;
+        a.add(0.5 * r_even);
+        a.add(0.5 * r);
+        fc[(n >> 1) * nnc + i] = a.result();
+      }
+    }
+  });
 }
 
 __global__ void k_sweep_from_zero(LevelView L, const double* __restrict__ f, double* __restrict__ y,
@@ -349,6 +898,85 @@ __global__ void __launch_bounds__(1024) k_coarsest(CoarsestView cv, const double
   }
 }
 
+// Coarsest exact solve for n_el <= 32: one warp, lane j owns unmasked node
+// j + 1.  Per time level: right-hand side with the coupled level's values
+// (shuffles), then PCR by shuffles with the same precomputed factors and the
+// same operation order as k_coarsest, so both give identical results; f is
+// prefetched kPF levels ahead because the march itself is sequential.
+constexpr int kPF = 8;
+
+template <bool ADJ>
+__global__ void __launch_bounds__(32) k_coarsest_warp(CoarsestView cv, const double* __restrict__ f,
+                                                      double* __restrict__ x) {
+  const LevelView& L = cv.lv;
+  const int m = cv.m;
+  const int64_t nn = L.nn, nt = L.n_t;
+  const int j = threadIdx.x;
+  const int64_t i = j + 1;
+  const bool active = j < m;
+  for (int64_t k = j; k < nn; k += 32) x[k] = f[k] / L.w;
+  for (int64_t n = 1 + j; n <= nt; n += 32) x[n * nn] = f[n * nn] / L.w;
+  double al[5] = {0, 0, 0, 0, 0}, ga[5] = {0, 0, 0, 0, 0};
+  double om = 0, o0 = 0, op = 0, bf = 1.0;
+  if (active) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k)
+      if (k < cv.n_steps) {
+        al[k] = cv.alpha[(int64_t)k * m + j];
+        ga[k] = cv.gamma[(int64_t)k * m + j];
+      }
+    om = L.coef[kOm * nn + i];
+    o0 = L.coef[kO0 * nn + i];
+    op = L.coef[kOp * nn + i];
+    bf = cv.bfin[j];
+  }
+  double q[kPF];
+#pragma unroll
+  for (int k = 0; k < kPF; ++k) {
+    const int64_t s = 1 + k;
+    const int64_t n = ADJ ? nt + 1 - s : s;
+    q[k] = (active && s <= nt) ? f[n * nn + i] : 0.0;
+  }
+  double xprev = 0.0;
+  for (int64_t base = 1; base <= nt; base += kPF) {
+#pragma unroll
+    for (int k = 0; k < kPF; ++k) {
+      const int64_t s = base + k;
+      if (s > nt) break;
+      const int64_t n = ADJ ? nt + 1 - s : s;
+      const bool coupled = ADJ ? (n + 1 <= nt) : (n - 1 >= 1);
+      double acc = q[k];
+      const int64_t s2 = s + kPF;
+      if (s2 <= nt) {
+        const int64_t n2 = ADJ ? nt + 1 - s2 : s2;
+        q[k] = active ? f[n2 * nn + i] : 0.0;
+      }
+      const double xm = __shfl_up_sync(kFull, xprev, 1);
+      const double xp = __shfl_down_sync(kFull, xprev, 1);
+      if (coupled) {
+        if (i >= 2) acc = acc - om * xm;
+        acc = acc - o0 * xprev;
+        if (i <= m - 1) acc = acc - op * xp;
+      }
+      double d = acc;
+#pragma unroll
+      for (int st = 0; st < 5; ++st) {
+        if (st >= cv.n_steps) break;
+        const int sh = 1 << st;
+        const double dm = __shfl_up_sync(kFull, d, sh);
+        const double dp = __shfl_down_sync(kFull, d, sh);
+        double v = d;
+        if (j - sh >= 0) v = v + al[st] * dm;
+        if (j + sh < m) v = v + ga[st] * dp;
+        d = v;
+      }
+      const double xv = active ? d / bf : 0.0;
+      if (active) x[n * nn + i] = xv;
+      xprev = xv;
+    }
+  }
+}
+
 __global__ void k_sumsq(const double* __restrict__ x, int64_t n, double* __restrict__ partials) {
   double acc = 0.0;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
@@ -370,58 +998,133 @@ __global__ void k_finalize_sum(const double* __restrict__ partials, int64_t n, d
 // Launchers return the cudaError_t of the launch (0 on success).
 inline int check_launch() { return static_cast<int>(cudaGetLastError()); }
 
+constexpr int kBlocksPerSM = 2;  // stream kernels: __launch_bounds__(kMaxTW, 2)
+constexpr int kNumSMs = 148;
+
+// Kernel design selection (benchmarking knob; 0 is the production default):
+//   0: lean NT=8   1: lean NT=4   2: tile NT=4   3: warp streaming   4: tile NT=8
+int g_variant = 0;
+
 inline dim3 march_block(const LevelView& L) {
   int tw = L.nn >= kMaxTW ? kMaxTW : (int)((L.nn + 31) / 32 * 32);
   return dim3(tw);
 }
-inline dim3 march_grid(const LevelView& L, dim3 blk) {
-  return dim3((unsigned)((L.n_t + 1 + kNT - 1) / kNT), (unsigned)((L.nn + blk.x - 1) / blk.x));
+inline int64_t stream_chunk(const LevelView& L, dim3 blk) {
+  const int64_t tiles = (L.nn + blk.x - 1) / blk.x;
+  int64_t chunks = (kNumSMs * kBlocksPerSM) / tiles;
+  if (chunks < 1) chunks = 1;
+  int64_t chunk = (L.n_t + 1 + chunks - 1) / chunks;
+  if (chunk < 16) chunk = 16;
+  chunk = (chunk + 1) & ~int64_t(1);
+  return chunk;
 }
+inline int variant_nt(int v) { return (v == 1 || v == 2) ? 4 : 8; }
+inline dim3 grid_for(const LevelView& L, dim3 blk, int v) {
+  const unsigned tiles = (unsigned)((L.nn + blk.x - 1) / blk.x);
+  if (v == 3) {
+    const int64_t chunk = stream_chunk(L, blk);
+    return dim3((unsigned)((L.n_t + 1 + chunk - 1) / chunk), tiles);
+  }
+  const int nt = variant_nt(v);
+  return dim3((unsigned)((L.n_t + 1 + nt - 1) / nt), tiles);
+}
+inline size_t tile_smem(dim3 blk, int nt, int halo) { return sizeof(double) * (nt + 1) * (blk.x + halo); }
 inline unsigned flat_grid(int64_t total) { return (unsigned)((total + kFlatBlock - 1) / kFlatBlock); }
+
+template <bool ADJ, int MODE, bool NORM, class Ld>
+void launch_pass(const LevelView& L, const Ld& ld, const double* f, double* y, double omega,
+                 double* partials, cudaStream_t s) {
+  const dim3 blk = march_block(L), grd = grid_for(L, blk, g_variant);
+  switch (g_variant) {
+    case 1:
+      k_lean<ADJ, MODE, NORM, 4, 3><<<grd, blk, 0, s>>>(L, ld, f, y, omega, partials);
+      break;
+    case 2:
+      k_tile<ADJ, MODE, NORM, 4, 4><<<grd, blk, tile_smem(blk, 4, 2), s>>>(L, ld, f, y, omega, partials);
+      break;
+    case 3:
+      k_stream<ADJ, MODE, NORM><<<grd, blk, 0, s>>>(L, ld, f, y, omega, partials, stream_chunk(L, blk));
+      break;
+    case 4:
+      k_tile<ADJ, MODE, NORM, 8, 2><<<grd, blk, tile_smem(blk, 8, 2), s>>>(L, ld, f, y, omega, partials);
+      break;
+    default:
+      k_lean<ADJ, MODE, NORM, 8, 2><<<grd, blk, 0, s>>>(L, ld, f, y, omega, partials);
+  }
+}
 
 template <bool ADJ>
 int sweep_impl(const LevelView& L, const double* f, const double* x, double* y, double omega,
                double* partials, cudaStream_t s) {
-  const dim3 blk = march_block(L), grd = march_grid(L, blk);
   const PlainLoad ld{x, L.nn};
   if (y != nullptr && partials != nullptr)
-    k_march<ADJ, kSweep, true><<<grd, blk, 0, s>>>(L, ld, f, y, omega, partials);
+    launch_pass<ADJ, kSweep, true>(L, ld, f, y, omega, partials, s);
   else if (y != nullptr)
-    k_march<ADJ, kSweep, false><<<grd, blk, 0, s>>>(L, ld, f, y, omega, partials);
+    launch_pass<ADJ, kSweep, false>(L, ld, f, y, omega, partials, s);
   else
-    k_march<ADJ, kNormOnly, true><<<grd, blk, 0, s>>>(L, ld, f, y, omega, partials);
+    launch_pass<ADJ, kNormOnly, true>(L, ld, f, y, omega, partials, s);
   return check_launch();
 }
 
 template <bool ADJ, int DIR>
 int sweep_prolong_impl(const LevelView& L, const LevelView& C, const double* f, const double* x,
                        const double* xc, double* y, double omega, cudaStream_t s) {
-  const dim3 blk = march_block(L), grd = march_grid(L, blk);
   const ProlongLoad<DIR> ld{x, xc, L.nn, C.nn};
-  k_march<ADJ, kSweep, false><<<grd, blk, 0, s>>>(L, ld, f, y, omega, nullptr);
+  launch_pass<ADJ, kSweep, false>(L, ld, f, y, omega, nullptr, s);
+  return check_launch();
+}
+
+template <bool ADJ, int DIR>
+int restrict_tile_impl(const LevelView& F, const LevelView& C, const double* f, const double* x,
+                       double* fc, cudaStream_t s) {
+  const dim3 blk = march_block(F);
+  if (g_variant == 0 || g_variant == 1) {
+    constexpr int NT = DIR == 0 ? 4 : 8;
+    const dim3 grd((unsigned)((F.n_t + 1 + NT - 1) / NT), (unsigned)((F.nn + blk.x - 1) / blk.x));
+    k_lean_restrict<ADJ, DIR, NT><<<grd, blk, 0, s>>>(F, C, f, x, fc);
+    return check_launch();
+  }
+  if (g_variant == 3) {
+    const dim3 grd = grid_for(F, blk, 3);
+    k_restrict_stream<ADJ, DIR><<<grd, blk, 0, s>>>(F, C, f, x, fc, stream_chunk(F, blk));
+    return check_launch();
+  }
+  constexpr int NT = 8;
+  const dim3 grd = grid_for(F, blk, 4);  // NT = 8 tiles
+  size_t sm = tile_smem(blk, NT, DIR == 0 ? 3 : 2);
+  if (DIR == 0) sm += sizeof(double) * NT * (blk.x + 1);
+  k_restrict_tile<ADJ, DIR, NT><<<grd, blk, sm, s>>>(F, C, f, x, fc);
   return check_launch();
 }
 
 }  // namespace
 
 int64_t sweep_partials_needed(const LevelView& L) {
-  const dim3 blk = march_block(L), grd = march_grid(L, blk);
+  // the largest grid any variant launches for this level (NT = 4 variants)
+  const dim3 blk = march_block(L), grd = grid_for(L, blk, 1);
   return (int64_t)grd.x * grd.y;
 }
+
+void set_kernel_variant(int v) { g_variant = (v >= 0 && v <= 4) ? v : 0; }
+int kernel_variant() { return g_variant; }
 
 int64_t sumsq_partials_needed(int64_t) { return kSumGrid; }
 
 int launch_sweep(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
                  double omega, double* partials, int64_t* n_partials, cudaStream_t s) {
-  if (n_partials) *n_partials = sweep_partials_needed(L);
+  if (n_partials) {
+    const dim3 blk = march_block(L), grd = grid_for(L, blk, g_variant);
+    *n_partials = (int64_t)grd.x * grd.y;
+  }
   return adjoint ? sweep_impl<true>(L, f, x, y, omega, partials, s)
                  : sweep_impl<false>(L, f, x, y, omega, partials, s);
 }
 
 int launch_sweep_from_zero(const LevelView& L, const double* f, double* y, double omega,
                            cudaStream_t s) {
-  const int64_t total = L.nn * (L.n_t + 1);
-  k_sweep_from_zero<<<flat_grid(total), kFlatBlock, 0, s>>>(L, f, y, omega, total);
+  const dim3 blk = march_block(L);
+  const dim3 grd((unsigned)((L.n_t + 1 + kFlatNT - 1) / kFlatNT), (unsigned)((L.nn + blk.x - 1) / blk.x));
+  k_sweep_from_zero2<<<grd, blk, 0, s>>>(L, f, y, omega);
   return check_launch();
 }
 
@@ -437,27 +1140,21 @@ int launch_sweep_prolong(bool adjoint, const LevelView& L, const LevelView& C, i
 
 int launch_residual(bool adjoint, const LevelView& L, const double* f, const double* x, double* r,
                     cudaStream_t s) {
-  const dim3 blk = march_block(L), grd = march_grid(L, blk);
   const PlainLoad ld{x, L.nn};
   if (adjoint)
-    k_march<true, kResidual, false><<<grd, blk, 0, s>>>(L, ld, f, r, 0.0, nullptr);
+    launch_pass<true, kResidual, false>(L, ld, f, r, 0.0, nullptr, s);
   else
-    k_march<false, kResidual, false><<<grd, blk, 0, s>>>(L, ld, f, r, 0.0, nullptr);
+    launch_pass<false, kResidual, false>(L, ld, f, r, 0.0, nullptr, s);
   return check_launch();
 }
 
 int launch_restrict_residual(bool adjoint, const LevelView& F, const LevelView& C, int dir,
                              const double* f, const double* x, double* fc, cudaStream_t s) {
-  const int64_t total = C.nn * (C.n_t + 1);
-  const unsigned g = flat_grid(total);
-  if (adjoint) {
-    if (dir == 0) k_restrict<true, 0, false><<<g, kFlatBlock, 0, s>>>(F, C, f, x, fc, total);
-    else k_restrict<true, 1, false><<<g, kFlatBlock, 0, s>>>(F, C, f, x, fc, total);
-  } else {
-    if (dir == 0) k_restrict<false, 0, false><<<g, kFlatBlock, 0, s>>>(F, C, f, x, fc, total);
-    else k_restrict<false, 1, false><<<g, kFlatBlock, 0, s>>>(F, C, f, x, fc, total);
-  }
-  return check_launch();
+  if (adjoint)
+    return dir == 0 ? restrict_tile_impl<true, 0>(F, C, f, x, fc, s)
+                    : restrict_tile_impl<true, 1>(F, C, f, x, fc, s);
+  return dir == 0 ? restrict_tile_impl<false, 0>(F, C, f, x, fc, s)
+                  : restrict_tile_impl<false, 1>(F, C, f, x, fc, s);
 }
 
 int launch_restrict(const LevelView& F, const LevelView& C, int dir, const double* r, double* fc,
@@ -471,14 +1168,20 @@ int launch_restrict(const LevelView& F, const LevelView& C, int dir, const doubl
 
 int launch_prolong_add(const LevelView& F, const LevelView& C, int dir, const double* xc, double* x,
                        cudaStream_t s) {
-  const int64_t total = F.nn * (F.n_t + 1);
-  if (dir == 0) k_prolong_add<0><<<flat_grid(total), kFlatBlock, 0, s>>>(F, C, xc, x, total);
-  else k_prolong_add<1><<<flat_grid(total), kFlatBlock, 0, s>>>(F, C, xc, x, total);
+  const dim3 blk = march_block(F);
+  const dim3 grd((unsigned)((F.n_t + 1 + kFlatNT - 1) / kFlatNT), (unsigned)((F.nn + blk.x - 1) / blk.x));
+  if (dir == 0) k_prolong_add2<0><<<grd, blk, 0, s>>>(F, C, xc, x);
+  else k_prolong_add2<1><<<grd, blk, 0, s>>>(F, C, xc, x);
   return check_launch();
 }
 
 int launch_coarsest(bool adjoint, const CoarsestView& cv, const double* f, double* x,
                     double* scratch, cudaStream_t s) {
+  if (cv.m <= 32) {
+    if (adjoint) k_coarsest_warp<true><<<1, 32, 0, s>>>(cv, f, x);
+    else k_coarsest_warp<false><<<1, 32, 0, s>>>(cv, f, x);
+    return check_launch();
+  }
   const size_t smem = sizeof(double) * 2 * (size_t)cv.m;
   const int use_smem = smem <= 160 * 1024 ? 1 : 0;
   int threads = cv.m >= 1024 ? 1024 : (int)((cv.m + 31) / 32 * 32);

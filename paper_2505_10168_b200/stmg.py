@@ -61,6 +61,8 @@ def _load():
         "stmg_hierarchy_level_info": [vp, i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(f64)],
         "stmg_hierarchy_level_coeffs": [vp, i32, vp, vp, vp, vp, vp, vp, vp],
         "stmg_hierarchy_device_bytes": [vp, C.POINTER(i64)],
+        "stmg_hierarchy_set_stream": [vp, vp],
+        "stmg_hierarchy_set_profiling": [vp, i32],
         "stmg_mg_solve": [vp, vp, vp, vp, vp, vp, i32],
         "stmg_level_sweeps": [vp, i32, vp, vp, i32, f64],
         "stmg_level_residual": [vp, i32, vp, vp, vp],
@@ -71,6 +73,7 @@ def _load():
         "stmg_residual_norm": [vp, vp, vp, C.POINTER(f64)],
         "stmg_norm2": [vp, vp, i64, C.POINTER(f64)],
         "stmg_synchronize": [vp],
+        "stmg_debug_set_kernel_variant": [i32],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -124,7 +127,10 @@ class _SolveRep(C.Structure):
     _fields_ = [("status", C.c_int32), ("cycles", C.c_int32), ("factor", C.c_double),
                 ("absolute_norms", C.c_int32), ("n_history", C.c_int32), ("seconds", C.c_double),
                 ("device_seconds", C.c_double), ("smoother_dof_updates", C.c_double),
-                ("kernel_launches", C.c_int64)]
+                ("kernel_launches", C.c_int64), ("fine_sweeps", C.c_int64),
+                ("fine_sweep_seconds", C.c_double), ("fine_restricts", C.c_int64),
+                ("fine_restrict_seconds", C.c_double), ("fine_prolong_sweeps", C.c_int64),
+                ("fine_prolong_sweep_seconds", C.c_double)]
 
 
 # ---- enums ---------------------------------------------------------------------------
@@ -372,6 +378,7 @@ class SolveReport:
     device_seconds: float = 0.0
     smoother_dof_updates: float = 0.0
     kernel_launches: int = 0
+    kernel_times: dict = field(default_factory=dict)  # profiling: kind -> (launches, seconds)
 
 
 @dataclass
@@ -470,6 +477,14 @@ class LevelHierarchy:
     def synchronize(self):
         _check(_lib.stmg_synchronize(self._h))
 
+    def set_stream(self, stream):
+        """Run on a caller stream (a torch.cuda.Stream, a raw cudaStream_t int, or None)."""
+        raw = getattr(stream, "cuda_stream", stream)
+        _check(_lib.stmg_hierarchy_set_stream(self._h, C.c_void_p(raw) if raw else None))
+
+    def set_profiling(self, on: bool = True):
+        _check(_lib.stmg_hierarchy_set_profiling(self._h, 1 if on else 0))
+
 
 def build_hierarchy(fine: SpaceTimeGrid, method, path: CoarseningPath, chi=None, mat=None,
                     device: int = 0) -> LevelHierarchy:
@@ -514,9 +529,20 @@ def mg_solve(h: LevelHierarchy, b, u, opts: Optional[SolveOptions] = None) -> So
     co = _SolveOpts(int(o.nu), float(o.omega), float(o.tol), float(o.div_tol), int(o.max_cycles))
     _check(_lib.stmg_mg_solve(h.handle, _ptr(b), _ptr(u), C.byref(co), C.byref(rep), hist.ctypes.data,
                               hist.size))
+    kt = {}
+    if rep.fine_sweeps or rep.fine_restricts or rep.fine_prolong_sweeps:
+        kt = {"fine_sweep": (rep.fine_sweeps, rep.fine_sweep_seconds),
+              "fine_restrict": (rep.fine_restricts, rep.fine_restrict_seconds),
+              "fine_prolong_sweep": (rep.fine_prolong_sweeps, rep.fine_prolong_sweep_seconds)}
     return SolveReport(SolveStatus(rep.status), rep.cycles, rep.factor,
                        [float(v) for v in hist[: rep.n_history]], bool(rep.absolute_norms),
-                       rep.seconds, rep.device_seconds, rep.smoother_dof_updates, rep.kernel_launches)
+                       rep.seconds, rep.device_seconds, rep.smoother_dof_updates, rep.kernel_launches,
+                       kt)
+
+
+def set_kernel_variant(v: int) -> None:
+    """Benchmarking knob: stencil kernel design (0 is the production default)."""
+    _check(_lib.stmg_debug_set_kernel_variant(int(v)))
 
 
 def abi_version() -> int:

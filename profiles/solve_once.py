@@ -1,0 +1,45 @@
+"""One STMG solve of a BASELINE config through the public API (target for
+ncu launch lists): python profiles/solve_once.py --config cfg1 [--solves 1]"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cfg1")
+    ap.add_argument("--solves", type=int, default=1)
+    ap.add_argument("--n-levels", type=int, default=None)
+    ap.add_argument("--nu", type=int, default=None)
+    a = ap.parse_args()
+    import torch
+
+    from paper_2505_10168_b200 import configs as C
+    from paper_2505_10168_b200 import stmg as S
+
+    cfg = C.CONFIGS[a.config]()
+    if a.n_levels:
+        cfg.n_levels = a.n_levels
+    if a.nu is not None:
+        cfg.nu = a.nu
+    g = S.build_fine_grid(cfg.L, cfg.t_T, cfg.n_el, cfg.n_t)
+    g.k, g.c = cfg.k, cfg.c
+    path = S.plan_coarsening(g, S.PlanRequest(n_levels=cfg.n_levels, strategy=S.PlanStrategy(cfg.strategy),
+                                              reassembly=S.ReassemblyMethod(cfg.reassembly),
+                                              min_elements=cfg.min_elements, chi=cfg.chi, mat=cfg.mat))
+    h = S.build_hierarchy(g, cfg.method, path, chi=cfg.chi, mat=cfg.mat)
+    b = torch.from_numpy(S.load_vector(g, kind=cfg.source_kind, params=cfg.source_params, masked=True)).cuda()
+    for _ in range(a.solves):
+        u = torch.zeros_like(b)
+        rep = S.mg_solve(h, b, u, S.SolveOptions(nu=cfg.nu, tol=cfg.tol, max_cycles=cfg.max_cycles))
+    print(f"{cfg.name} path={S.path_to_string(path)} cycles={rep.cycles} seconds={rep.seconds:.4f} "
+          f"device_seconds={rep.device_seconds:.4f} launches={rep.kernel_launches}")
+    for l, lv in enumerate(h.levels):
+        print(f"level {l}: {lv.n_el}x{lv.n_t} dofs={lv.n_dofs}")
+
+
+if __name__ == "__main__":
+    main()
