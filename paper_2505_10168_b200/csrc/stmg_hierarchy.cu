@@ -563,7 +563,10 @@ void finish_create(stmg_hierarchy* h, bool share_ws_from_other, const stmg_hiera
     h->ws = make_workspace(h, &bytes);
     h->device_bytes += bytes;
   }
-  cuda_check(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  // A blocking stream: ordered with the legacy default stream, so device inputs
+  // produced by a caller on the default stream (e.g. PyTorch) are complete
+  // before the solve reads them, and results are visible to it afterwards.
+  cuda_check(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamDefault), "cudaStreamCreate");
   cuda_check(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking), "cudaStreamCreate");
   h->stream = h->own_stream;
   cuda_check(cudaEventCreate(&h->ev0), "cudaEventCreate");
