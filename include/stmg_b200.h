@@ -207,7 +207,8 @@ int stmg_norm2(stmg_hierarchy* h, const double* x, int64_t n, double* norm);
 int stmg_synchronize(stmg_hierarchy* h);
 
 /* Benchmarking knob, not part of the reference-facing surface: stencil kernel
- * design (0 tiled NT=8 default, 1 tiled NT=4, 2 tiled NT=16, 3 warp streaming). */
+ * design (5 = production default; see csrc/stmg_kernels.cu for the list).  The
+ * environment variable STMG_KERNEL_VARIANT sets it at load time. */
 int stmg_debug_set_kernel_variant(int32_t variant);
 
 #ifdef __cplusplus

@@ -1180,8 +1180,8 @@ int stmg_norm2(stmg_hierarchy* h, const double* x, int64_t n, double* norm) {
 }
 
 // Benchmarking knob (not part of the reference-facing API): select the stencil
-// kernel design (0 tiled NT=8 default, 1 tiled NT=4, 2 tiled NT=16, 3 warp
-// streaming).  Existing graphs keep the design they were captured with.
+// kernel design (see stmg_kernels.cu).  Existing graphs keep the design they
+// were captured with.
 int stmg_debug_set_kernel_variant(int32_t v) {
   return guarded([&] { set_kernel_variant(v); });
 }

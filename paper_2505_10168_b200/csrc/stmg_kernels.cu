@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "stmg_internal.h"
 
@@ -299,6 +300,113 @@ __global__ void __launch_bounds__(kMaxTW, MINB) k_lean(LevelView L, Ld ld,
   }
 }
 
+// Lean variant with overlapping warps: each warp covers 32 consecutive nodes
+// but only lanes 1..30 compute and store; lanes 0 and 31 load the strip-edge
+// nodes, so no separate halo registers are needed (lower register pressure,
+// higher occupancy).  Blocks are ordered node-tile fastest (1-D grid) so that
+// the staged coupled level of a time tile is usually still in L2.
+template <bool ADJ, int MODE, bool NORM, int NT, int MINB, class Ld>
+__global__ void __launch_bounds__(kMaxTW, MINB) k_lean2(LevelView L, Ld ld,
+                                                        const double* __restrict__ f,
+                                                        double* __restrict__ y, double omega,
+                                                        double* __restrict__ partials,
+                                                        int64_t node_tiles) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nn = L.nn, nt = L.n_t;
+  const int64_t bid = blockIdx.x;
+  const int64_t tile = bid % node_tiles, ttile = bid / node_tiles;
+  const int64_t per_block = (int64_t)(blockDim.x >> 5) * 30;
+  const int64_t i = tile * per_block + warp * 30 + lane - 1;  // node of this lane
+  const int64_t n0 = ttile * NT;
+  const int64_t nbase = ADJ ? n0 : n0 - 1;
+  const bool in_grid = i >= 0 && i < nn;
+  const bool computes = lane >= 1 && lane <= 30 && in_grid;
+  const int64_t wfirst = tile * per_block + warp * 30;  // first computing node
+  const bool rows_in = ADJ ? (n0 >= 1 && n0 + NT - 1 <= nt - 1) : (n0 >= 2 && n0 + NT - 1 <= nt);
+  const bool nodes_in = wfirst >= 2 && wfirst + 29 <= L.n_el - 1;
+  double xr[NT + 1], fv[NT];
+  Coefs c{};
+  double acc = 0.0;
+  if (rows_in && nodes_in) {
+#pragma unroll
+    for (int k = 0; k < NT; ++k) fv[k] = computes ? f[(n0 + k) * nn + i] : 0.0;
+#pragma unroll
+    for (int r = 0; r <= NT; ++r) xr[r] = ld(nbase + r, i);
+    if (computes) c = load_coefs(L, i);
+    double pm = __shfl_up_sync(kFull, xr[0], 1);
+    double pp = __shfl_down_sync(kFull, xr[0], 1);
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const double x1 = xr[k + 1];
+      const double qm = __shfl_up_sync(kFull, x1, 1);
+      const double qp = __shfl_down_sync(kFull, x1, 1);
+      double s0, s1, s2, s3, x0;
+      if (!ADJ) {
+        x0 = x1;
+        s0 = (0.0 + c.om * pm) + c.c0 * x1;
+        s1 = (0.0 + c.o0 * xr[k]) + c.cp * qp;
+        s2 = 0.0 + c.op * pp;
+        s3 = 0.0 + c.cm * qm;
+      } else {
+        x0 = xr[k];
+        s0 = (0.0 + c.cm * pm) + c.o0 * x1;
+        s1 = (0.0 + c.c0 * x0) + c.op * qp;
+        s2 = 0.0 + c.cp * pp;
+        s3 = 0.0 + c.om * qm;
+      }
+      const double r = fv[k] - ((s0 + s1) + (s2 + s3));
+      if (computes) {
+        if (NORM) acc = acc + r * r;
+        if (MODE == kSweep) y[(n0 + k) * nn + i] = x0 + omega * (r * c.invd);
+        else if (MODE == kResidual) y[(n0 + k) * nn + i] = r;
+      }
+      pm = qm;
+      pp = qp;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const int64_t n = n0 + k;
+      fv[k] = (computes && n <= nt) ? f[n * nn + i] : 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r <= NT; ++r) {
+      const int64_t n = nbase + r;
+      xr[r] = (n >= 0 && n <= nt && in_grid) ? ld(n, i) : 0.0;
+    }
+    if (computes) c = load_coefs(L, i);
+    double pm = __shfl_up_sync(kFull, xr[0], 1);
+    double pp = __shfl_down_sync(kFull, xr[0], 1);
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const int64_t n = n0 + k;
+      if (n > nt) break;
+      const double x1 = xr[k + 1];
+      const double qm = __shfl_up_sync(kFull, x1, 1);
+      const double qp = __shfl_down_sync(kFull, x1, 1);
+      if (computes) {
+        const double row = ADJ ? row_sum<true>(L, n, i, c, pm, xr[k], pp, qm, x1, qp)
+                               : row_sum<false>(L, n, i, c, qm, x1, qp, pm, xr[k], pp);
+        const double x0 = ADJ ? xr[k] : x1;
+        const double r = fv[k] - row;
+        if (NORM) acc = acc + r * r;
+        if (MODE == kSweep) {
+          const double id = (n == 0 || i == 0) ? L.inv_w : c.invd;
+          y[n * nn + i] = x0 + omega * (r * id);
+        } else if (MODE == kResidual) {
+          y[n * nn + i] = r;
+        }
+      }
+      pm = qm;
+      pp = qp;
+    }
+  }
+  if (NORM) {
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) partials[bid] = s;
+  }
+}
+
 // f_c = R (f - J x) over one lean tile, R = s P^T (proj/src/transfer.cpp:95-104);
 // the fine residual never reaches memory.  x step (DIR 0): lane l computes the
 // residual at its node (lane 0 also at the node before its strip, from an
@@ -339,11 +447,81 @@ __global__ void __launch_bounds__(kMaxTW, 2) k_lean_restrict(LevelView F, LevelV
   Coefs c{}, ch{};
   if (valid) c = load_coefs(F, i);
   if (xr1) ch = load_coefs(F, i - 1);
+  // interior tile: every row has its coupled level, every node (incl. lane 0's
+  // extra node i - 1) has both same-level neighbours, every coarse node has
+  // all three fine contributions -> fixed canonical orders, no branches.
+  const bool rows_in = ADJ ? (n0 >= 1 && n0 + NT - 1 <= nt - 1) : (n0 >= 2 && n0 + NT - 1 <= nt);
+  const bool nodes_in = wfirst >= 32 && wfirst + 31 <= F.n_el - 1;
   double pm = __shfl_up_sync(kFull, xr[0], 1);
   double pp = __shfl_down_sync(kFull, xr[0], 1);
   if (lane == 0) pm = hr[0];
   if (lane == 31) pp = hr[0];
   double r_even = 0.0;
+  if (rows_in && nodes_in) {
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const int64_t n = n0 + k;
+      const double x1 = xr[k + 1];
+      double qm = __shfl_up_sync(kFull, x1, 1);
+      double qp = __shfl_down_sync(kFull, x1, 1);
+      if (lane == 0) qm = hr[k + 1];
+      if (lane == 31) qp = hr[k + 1];
+      double r;
+      if (!ADJ) {
+        const double s0 = (0.0 + c.om * pm) + c.c0 * x1;
+        const double s1 = (0.0 + c.o0 * xr[k]) + c.cp * qp;
+        const double s2 = 0.0 + c.op * pp;
+        const double s3 = 0.0 + c.cm * qm;
+        r = fv[k] - ((s0 + s1) + (s2 + s3));
+      } else {
+        const double s0 = (0.0 + c.cm * pm) + c.o0 * x1;
+        const double s1 = (0.0 + c.c0 * xr[k]) + c.op * qp;
+        const double s2 = 0.0 + c.cp * pp;
+        const double s3 = 0.0 + c.om * qm;
+        r = fv[k] - ((s0 + s1) + (s2 + s3));
+      }
+      if (DIR == 0) {
+        double r1 = 0.0;
+        if (lane == 0) {  // node i - 1: same-level (h2, hr, x) and coupled-level triples
+          double t0, t1, t2, t3;
+          if (!ADJ) {
+            t0 = (0.0 + ch.om * h2[k]) + ch.c0 * hr[k + 1];
+            t1 = (0.0 + ch.o0 * hr[k]) + ch.cp * x1;
+            t2 = 0.0 + ch.op * xr[k];
+            t3 = 0.0 + ch.cm * h2[k + 1];
+          } else {
+            t0 = (0.0 + ch.cm * h2[k]) + ch.o0 * hr[k + 1];
+            t1 = (0.0 + ch.c0 * hr[k]) + ch.op * x1;
+            t2 = 0.0 + ch.cp * xr[k];
+            t3 = 0.0 + ch.om * h2[k + 1];
+          }
+          r1 = f1[k] - ((t0 + t1) + (t2 + t3));
+        }
+        const int src = 2 * lane;
+        const double ra = __shfl_sync(kFull, r, (src - 1) & 31);
+        const double rb = __shfl_sync(kFull, r, src & 31);
+        const double rc = __shfl_sync(kFull, r, (src + 1) & 31);
+        if (lane < 16) {
+          const int64_t I = wfirst / 2 + lane;
+          const double a0 = 0.0 + 0.5 * (lane == 0 ? r1 : ra);
+          const double a1 = 0.0 + 1.0 * rb;
+          const double a2 = 0.0 + 0.5 * rc;
+          fc[n * nnc + I] = (a0 + a1) + (a2 + 0.0);
+        }
+      } else {
+        if ((k & 1) == 0) {
+          r_even = r;
+        } else {
+          const double a0 = 0.0 + 0.5 * r_even;
+          const double a1 = 0.0 + 0.5 * r;
+          fc[(n >> 1) * nnc + i] = (a0 + a1) + (0.0 + 0.0);
+        }
+      }
+      pm = qm;
+      pp = qp;
+    }
+    return;
+  }
 #pragma unroll
   for (int k = 0; k < NT; ++k) {
     const int64_t n = n0 + k;
@@ -1001,9 +1179,11 @@ inline int check_launch() { return static_cast<int>(cudaGetLastError()); }
 constexpr int kBlocksPerSM = 2;  // stream kernels: __launch_bounds__(kMaxTW, 2)
 constexpr int kNumSMs = 148;
 
-// Kernel design selection (benchmarking knob; 0 is the production default):
+// Kernel design selection (benchmarking knob; 5 is the production default):
 //   0: lean NT=8   1: lean NT=4   2: tile NT=4   3: warp streaming   4: tile NT=8
-int g_variant = 0;
+//   5: lean2 (overlapping warps, node-fastest order) NT=8   6: lean2 NT=16
+constexpr int kDefaultVariant = 5;
+int g_variant = kDefaultVariant;
 
 inline dim3 march_block(const LevelView& L) {
   int tw = L.nn >= kMaxTW ? kMaxTW : (int)((L.nn + 31) / 32 * 32);
@@ -1018,8 +1198,16 @@ inline int64_t stream_chunk(const LevelView& L, dim3 blk) {
   chunk = (chunk + 1) & ~int64_t(1);
   return chunk;
 }
-inline int variant_nt(int v) { return (v == 1 || v == 2) ? 4 : 8; }
+inline int variant_nt(int v) { return (v == 1 || v == 2) ? 4 : v == 6 ? 16 : 8; }
+inline int64_t lean2_tiles(const LevelView& L, dim3 blk) {
+  const int64_t per = (int64_t)(blk.x / 32) * 30;
+  return (L.nn + per - 1) / per;
+}
 inline dim3 grid_for(const LevelView& L, dim3 blk, int v) {
+  if (v == 5 || v == 6) {
+    const int nt = variant_nt(v);
+    return dim3((unsigned)(lean2_tiles(L, blk) * ((L.n_t + 1 + nt - 1) / nt)));
+  }
   const unsigned tiles = (unsigned)((L.nn + blk.x - 1) / blk.x);
   if (v == 3) {
     const int64_t chunk = stream_chunk(L, blk);
@@ -1047,6 +1235,12 @@ void launch_pass(const LevelView& L, const Ld& ld, const double* f, double* y, d
       break;
     case 4:
       k_tile<ADJ, MODE, NORM, 8, 2><<<grd, blk, tile_smem(blk, 8, 2), s>>>(L, ld, f, y, omega, partials);
+      break;
+    case 5:
+      k_lean2<ADJ, MODE, NORM, 8, 3><<<grd, blk, 0, s>>>(L, ld, f, y, omega, partials, lean2_tiles(L, blk));
+      break;
+    case 6:
+      k_lean2<ADJ, MODE, NORM, 16, 2><<<grd, blk, 0, s>>>(L, ld, f, y, omega, partials, lean2_tiles(L, blk));
       break;
     default:
       k_lean<ADJ, MODE, NORM, 8, 2><<<grd, blk, 0, s>>>(L, ld, f, y, omega, partials);
@@ -1078,7 +1272,7 @@ template <bool ADJ, int DIR>
 int restrict_tile_impl(const LevelView& F, const LevelView& C, const double* f, const double* x,
                        double* fc, cudaStream_t s) {
   const dim3 blk = march_block(F);
-  if (g_variant == 0 || g_variant == 1) {
+  if (g_variant == 0 || g_variant == 1 || g_variant == 5 || g_variant == 6) {
     constexpr int NT = DIR == 0 ? 4 : 8;
     const dim3 grd((unsigned)((F.n_t + 1 + NT - 1) / NT), (unsigned)((F.nn + blk.x - 1) / blk.x));
     k_lean_restrict<ADJ, DIR, NT><<<grd, blk, 0, s>>>(F, C, f, x, fc);
@@ -1100,12 +1294,14 @@ int restrict_tile_impl(const LevelView& F, const LevelView& C, const double* f, 
 }  // namespace
 
 int64_t sweep_partials_needed(const LevelView& L) {
-  // the largest grid any variant launches for this level (NT = 4 variants)
-  const dim3 blk = march_block(L), grd = grid_for(L, blk, 1);
-  return (int64_t)grd.x * grd.y;
+  // the largest grid any variant launches for this level
+  const dim3 blk = march_block(L);
+  const dim3 g1 = grid_for(L, blk, 1), g5 = grid_for(L, blk, 5);
+  const int64_t a = (int64_t)g1.x * g1.y, b = (int64_t)g5.x * g5.y;
+  return a > b ? a : b;
 }
 
-void set_kernel_variant(int v) { g_variant = (v >= 0 && v <= 4) ? v : 0; }
+void set_kernel_variant(int v) { g_variant = (v >= 0 && v <= 6) ? v : kDefaultVariant; }
 int kernel_variant() { return g_variant; }
 
 int64_t sumsq_partials_needed(int64_t) { return kSumGrid; }
@@ -1193,6 +1389,11 @@ int launch_coarsest(bool adjoint, const CoarsestView& cv, const double* f, doubl
 }
 
 int kernels_init() {
+  static bool env_read = false;
+  if (!env_read) {  // STMG_KERNEL_VARIANT lets the test suite exercise every design
+    env_read = true;
+    if (const char* v = std::getenv("STMG_KERNEL_VARIANT")) set_kernel_variant(std::atoi(v));
+  }
   // The coarsest march keeps its two PCR work vectors in shared memory up to 160 KB.
   cudaError_t e = cudaFuncSetAttribute(k_coarsest<true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);

@@ -22,7 +22,7 @@ def main():
     ap.add_argument("--sweeps", type=int, default=20)
     ap.add_argument("--adjoint", action="store_true")
     ap.add_argument("--reps", type=int, default=3)
-    ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--variant", type=int, default=5)
     args = ap.parse_args()
     import numpy as np
     import torch
