@@ -292,6 +292,8 @@ def main():
     ap.add_argument("--ref-cores", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--hbm-roofline", type=int, default=1)
+    ap.add_argument("--dist", action="store_true",
+                    help="use the time-slab (NCCL) path even at N=1 (smoke test of that path)")
     args = ap.parse_args()
 
     if args.impl == "reference":
@@ -316,6 +318,12 @@ def main():
             dist.barrier()
 
     cfg = bench_config(args.config, args)
+    if world > 1 and args.config == "cfg1":
+        from paper_2505_10168_b200 import configs as Cf
+
+        nu_, nl_ = cfg.nu, cfg.n_levels
+        cfg = Cf.cfg1_weak(world)
+        cfg.nu, cfg.n_levels = nu_, nl_
     g = S.build_fine_grid(cfg.L, cfg.t_T, cfg.n_el, cfg.n_t)
     g.k, g.c = cfg.k, cfg.c
     req = S.PlanRequest(n_levels=cfg.n_levels, lambda_crit=cfg.lambda_crit,
@@ -324,14 +332,25 @@ def main():
                         chi=cfg.chi, mat=cfg.mat)
     path = S.plan_coarsening(g, req)
     t_build = time.perf_counter()
-    h = S.build_hierarchy(g, cfg.method, path, chi=cfg.chi, mat=cfg.mat, device=local)
-    if cfg.adjoint:
-        h = S.transposed_hierarchy(h)
+    dh = None
+    if world > 1 or args.dist:
+        # time slabs over NCCL: rank 0 makes the NCCL id, torch.distributed ships it
+        obj = [S.nccl_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(obj, src=0)
+        dh = S.build_dist_hierarchy(g, cfg.method, path, world, rank=rank, nccl_id=obj[0], device=local,
+                                    adjoint=cfg.adjoint, chi=cfg.chi, mat=cfg.mat, min_slab=16)
+        h = None
+    else:
+        h = S.build_hierarchy(g, cfg.method, path, chi=cfg.chi, mat=cfg.mat, device=local)
+        if cfg.adjoint:
+            h = S.transposed_hierarchy(h)
     t_build = time.perf_counter() - t_build
     b_host = rhs_for(cfg, S, g)
     n = b_host.size
     stream = torch.cuda.Stream(device=dev)
-    h.set_stream(stream)
+    if h is not None:
+        h.set_stream(stream)
     opts = S.SolveOptions(nu=cfg.nu, omega=cfg.omega, tol=cfg.tol, div_tol=cfg.div_tol,
                           max_cycles=cfg.max_cycles)
     with torch.cuda.stream(stream):
@@ -339,14 +358,21 @@ def main():
         u_dev = torch.zeros_like(b_dev)
     stream.synchronize()
 
+    def solve_on(bv, uv):
+        if dh is not None:
+            stream.synchronize()
+            return S.mg_solve_dist(dh, bv, uv, opts)
+        return S.mg_solve(h, bv, uv, opts)
+
     def one_solve():
         with torch.cuda.stream(stream):
             u_dev.zero_()
-        return S.mg_solve(h, b_dev, u_dev, opts)
+        return solve_on(b_dev, u_dev)
 
     for _ in range(args.warmup):
         rep = one_solve()
-    h.set_profiling(True)
+    if h is not None:
+        h.set_profiling(True)
     rep = one_solve()  # capture the profiled graph outside the timed region
     # L2 flush buffer (> 126 MB L2): written between timed steps, outside the events
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
@@ -363,13 +389,14 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            reps.append(S.mg_solve(h, b_dev, u_dev, opts))
+            reps.append(solve_on(b_dev, u_dev))
             e1.record(stream)
             e1.synchronize()
             step_ms.append(e0.elapsed_time(e1))
     torch.cuda.synchronize(dev)
     barrier()
-    h.set_profiling(False)
+    if h is not None:
+        h.set_profiling(False)
     ms = sum(step_ms)
     updates = sum(r.smoother_dof_updates for r in reps)
     t_max = ms
@@ -394,7 +421,7 @@ def main():
         avg = sweep_s / sweeps
         achieved = 24.0 * n0 / avg / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                    "frac": achieved / hbm, "traffic": None, "kernel": "k_march<sweep> (fine level)",
+                    "frac": achieved / hbm, "traffic": None, "kernel": "k_lean2<sweep> (fine level, in-graph CUDA events)",
                     "algorithmic_bytes_per_launch": 24 * n0, "avg_launch_ms": avg * 1e3,
                     "launches_timed": sweeps, "peak_source": peak_kind}
     kt = {}
@@ -424,7 +451,7 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            r = S.mg_solve(h, bh, uh, opts)
+            r = solve_on(bh, uh)
             e1.record(stream)
             e1.synchronize()
             tot_ms += e0.elapsed_time(e1)
@@ -444,6 +471,14 @@ def main():
         hbm_scale = hbm_scale_sweep(S, torch, dev, hbm)
         if hbm_scale is not None and roofline is not None:
             roofline["hbm_scale_cfg2_sweep"] = hbm_scale
+        elif hbm_scale is not None and "achieved" in hbm_scale:
+            # distributed solves carry no in-graph event timers: report the same kernel at HBM scale
+            roofline = {"bound": "hbm", "achieved": hbm_scale["achieved"], "peak": hbm, "unit": "GB/s",
+                        "frac": hbm_scale["frac"], "traffic": None,
+                        "kernel": "k_lean2<sweep> on the cfg2 grid (in-graph timers off for slab solves)",
+                        "algorithmic_bytes_per_launch": 24 * hbm_scale["dofs"],
+                        "avg_launch_ms": hbm_scale["avg_launch_ms"], "peak_source": peak_kind,
+                        "hbm_scale_cfg2_sweep": hbm_scale}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -467,14 +502,16 @@ def main():
             "config": {"workload": cfg.name, "n_el": cfg.n_el, "n_t": cfg.n_t, "dofs": n0,
                        "method": cfg.method, "strategy": int(cfg.strategy), "n_levels": cfg.n_levels,
                        "min_elements": cfg.min_elements, "nu": cfg.nu, "tol": cfg.tol,
-                       "path": S.path_to_string(path), "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "path": S.path_to_string(path),
+                       "parallelism": (f"time-slabs{world} (NCCL, {dh.n_distributed} distributed levels)"
+                                       if dh is not None else "single"),
                        "l2": ("inputs larger than L2" if n0 * 8 * 3 > 126e6 else
                               "L2 flushed (256 MB write) before every timed step"),
                        "adjoint": cfg.adjoint},
             "solve_seconds": step_ms_avg * 1e-3, "cycles": last.cycles, "status": S.status_name(last.status),
             "final_rel_residual": last.history[-1], "gpu_launches": int(sum(r.kernel_launches for r in reps)),
             "roofline": roofline, "kernels": kt, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
-            "build_seconds": t_build, "device_bytes": h.device_bytes(),
+            "build_seconds": t_build, "device_bytes": h.device_bytes() if h is not None else dh.device_bytes,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

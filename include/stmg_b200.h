@@ -206,6 +206,30 @@ int stmg_residual_norm(stmg_hierarchy* h, const double* f, const double* x, doub
 int stmg_norm2(stmg_hierarchy* h, const double* x, int64_t n, double* norm);
 int stmg_synchronize(stmg_hierarchy* h);
 
+/* ---- time-slab multi-GPU ------------------------------------
+ * A distributed hierarchy splits the time axis of every level that can be cut
+ * into `world` equal slabs (>= min_slab levels, even where the next step
+ * coarsens in time) and gathers the remaining coarse levels to rank 0.  With
+ * nccl_id != NULL this process is rank `rank` of an NCCL job (one GPU per
+ * process; get the id with stmg_dist_nccl_unique_id on rank 0 and broadcast
+ * it); with nccl_id == NULL this process hosts all `world` ranks on `device`
+ * and exchanges through device copies (loopback, for validation).
+ * stmg_dist_mg_solve takes full-size b and u (host or device); u receives this
+ * process's slab rows of the finest level (loopback: all rows). */
+typedef struct stmg_dist stmg_dist;
+int stmg_dist_partition(int32_t n_levels, const int64_t* n_t, const int32_t* dirs, int32_t world,
+                        int64_t min_slab, int32_t* n_distributed, int64_t* bounds);
+int stmg_dist_nccl_unique_id(void* id_out, int32_t cap);
+int stmg_dist_create(const stmg_grid* g, const double* k, const double* c, const double* chi,
+                     const stmg_material_pair* mat, const char* method, int32_t n_dirs,
+                     const int32_t* dirs, int32_t adjoint, int32_t world, int32_t rank,
+                     const void* nccl_id, int32_t device, int64_t min_slab, stmg_dist** out);
+int stmg_dist_info(const stmg_dist* d, int32_t* n_distributed, int64_t* row_lo, int64_t* row_hi,
+                   int32_t* n_local, int64_t* device_bytes);
+int stmg_dist_mg_solve(stmg_dist* d, const double* b, double* u, const stmg_solve_options* opts,
+                       stmg_solve_report* report, double* history, int32_t history_cap);
+void stmg_dist_destroy(stmg_dist* d);
+
 /* Benchmarking knob, not part of the reference-facing surface: stencil kernel
  * design (5 = production default; see csrc/stmg_kernels.cu for the list).  The
  * environment variable STMG_KERNEL_VARIANT sets it at load time. */

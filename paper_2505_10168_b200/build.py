@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libstmg_b200.so")
 SOURCES = ["stmg_kernels.cu", "stmg_hierarchy.cu"]
-HEADERS = ["stmg_internal.h", os.path.join("..", "..", "include", "stmg_b200.h")]
+HEADERS = ["stmg_internal.h", "stmg_dist.cuh", os.path.join("..", "..", "include", "stmg_b200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -56,7 +56,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(obj)
     tmp = OUT + ".tmp"
     cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", tmp,
-           "-lcudart_static", "-lpthread", "-ldl", "-lrt"]
+           "-lcudart_static", "-lpthread", "-ldl", "-lrt"]  # NCCL is dlopen'ed at run time
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

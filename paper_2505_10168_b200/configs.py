@@ -149,6 +149,16 @@ def cfg1(n_el=1024, n_t=4096, seed=1, n_levels=10, nu=5) -> Config:
                   n_levels=n_levels, nu=nu)
 
 
+def cfg1_weak(world: int = 1, **kw) -> Config:
+    """Weak-scaled config 1 for the time-slab runs: the horizon grows with the GPU
+    count (t_T = world, n_t = 4096 world) so dt, the anisotropy and the planned
+    coarsening path stay those of config 1; each GPU owns one 1024 x 4096 slab."""
+    c = cfg1(n_t=4096 * world, **kw)
+    c.t_T = float(world)
+    c.name = f"cfg1-weak{world}"
+    return c
+
+
 def cfg2(n_el=16384, n_t=65536, seed=2, n_levels=18, nu=1, min_elements=256) -> Config:
     rng = MT19937_64(seed)
     u = np.array([uniform01(rng) for _ in range(n_el)])

@@ -1,0 +1,644 @@
+// Time-slab multi-GPU STMG; included by stmg_hierarchy.cu.
+//
+// Partition.  Level l of the hierarchy is *distributed* when its n_t steps split
+// into `world` equal slabs of >= min_slab levels (even-sized when the next step
+// coarsens in time, so causal restriction 2N, 2N+1 -> N and prolongation
+// floor(n/2) stay rank-local).  Rank g owns rows [g n_t/W, (g+1) n_t/W); the
+// last rank also owns level n_t.  The first non-distributed level Lg and all
+// coarser ones (incl. the coarsest exact march, which is sequential in time)
+// are *gathered*: their right-hand side is gathered to rank 0, which runs that
+// tail of the V-cycle as an ordinary single-GPU hierarchy and broadcasts the
+// correction back.
+//
+// Storage.  Every rank keeps full-size, globally indexed level vectors but only
+// reads/writes its slab rows plus one ghost level on each side, so HBM traffic
+// scales as 1/W while indexing and layout stay those of the single-GPU path
+// (capacity does not scale: cfg2's 52 GB fit in one B200).  Before every
+// stencil pass the ghost levels of the input vector are exchanged with the
+// neighbours (J reads level n-1, J^T level n+1; both ghosts are exchanged), the
+// norms are all-reduced.  All operations are pointwise-identical to the
+// single-GPU path, so the iterate after k cycles is bit-identical; only the
+// norm summation order changes.
+//
+// Transport.  `Comm` has two implementations: NCCL (one rank per process,
+// NVLink/NVSwitch; libnccl.so.2 is dlopen'ed, reusing an already-loaded copy
+// such as PyTorch's) and Loopback (this process hosts all `world` ranks on one
+// GPU and exchanges by device-to-device copies — the single-GPU validation of
+// the exact slab code path).  Every transport call is stream-ordered and is
+// captured into the V-cycle graph.
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace stmgb {
+namespace {
+
+// ---------------------------------------------------------------------------
+// Partition (shared with the CPU gloo tests through stmg_dist_partition)
+// ---------------------------------------------------------------------------
+struct SlabPlan {
+  int world = 1;
+  int Lg = 0;                                // levels [0, Lg) distributed
+  std::vector<std::vector<int64_t>> bounds;  // [l][g], g = 0..world; bounds[l][world] = n_t+1
+};
+
+SlabPlan plan_slabs(const std::vector<int64_t>& nts, const std::vector<int32_t>& dirs, int world,
+                    int64_t min_slab) {
+  if (world < 1) throw std::invalid_argument("dist: world size must be >= 1");
+  if (min_slab < 8) min_slab = 8;
+  SlabPlan p;
+  p.world = world;
+  const int L = static_cast<int>(nts.size());
+  for (int l = 0; l + 1 < L; ++l) {
+    const int64_t nt = nts[l];
+    if (nt % world != 0) break;
+    const int64_t slab = nt / world;
+    if (slab < min_slab) break;
+    if (dirs[l] == STMG_DIR_T && slab % 2 != 0) break;
+    std::vector<int64_t> b(static_cast<size_t>(world) + 1);
+    for (int g = 0; g < world; ++g) b[g] = g * slab;
+    b[world] = nt + 1;
+    p.bounds.push_back(std::move(b));
+    p.Lg = l + 1;
+  }
+  return p;
+}
+
+// Rows of the first gathered level that rank g produces when restricting from
+// its slab of level Lg - 1.
+std::pair<int64_t, int64_t> gathered_rows(const SlabPlan& p, int dir_into, int g, int64_t nt_coarse) {
+  const auto& b = p.bounds[p.Lg - 1];
+  if (dir_into == STMG_DIR_T) {
+    const int64_t lo = b[g] / 2;
+    const int64_t hi = (g == p.world - 1) ? nt_coarse + 1 : b[g + 1] / 2;
+    return {lo, hi};
+  }
+  return {b[g], b[g + 1]};
+}
+
+// ---------------------------------------------------------------------------
+// Transport
+// ---------------------------------------------------------------------------
+__global__ void k_sum_scalars(const double* const* in, int n, double* const* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int k = 0; k < n; ++k) s = s + *in[k];  // fixed rank order
+    for (int k = 0; k < n; ++k) *out[k] = s;
+  }
+}
+
+struct Comm {
+  int world = 1;
+  int n_local = 1;
+  int rank0 = 0;  // global rank of local slot 0
+  virtual ~Comm() = default;
+  virtual const char* name() const = 0;
+  // ghost exchange of one vector per local rank (rows of level partition b, nn doubles per row)
+  virtual void exchange(const std::vector<double*>& v, const std::vector<int64_t>& b, int64_t nn,
+                        cudaStream_t s) = 0;
+  virtual void allreduce_sum(const std::vector<double*>& in, const std::vector<double*>& out,
+                             cudaStream_t s) = 0;
+  // rows [lo_g, hi_g) of every rank's src (full-size, nn per row) -> dst on rank 0
+  virtual void gather_rows(const std::vector<double*>& src, double* dst,
+                           const std::vector<std::pair<int64_t, int64_t>>& rows, int64_t nn,
+                           cudaStream_t s) = 0;
+  // count doubles from rank 0's root buffer to every local rank's dst
+  virtual void broadcast(const double* root, const std::vector<double*>& dst, int64_t count,
+                         cudaStream_t s) = 0;
+  bool is_root() const { return rank0 == 0; }
+};
+
+struct LoopbackComm : Comm {
+  std::unique_ptr<DeviceBuf> ptrs;  // 2 * n_local device pointers for allreduce
+  std::vector<const double*> last_in;
+  std::vector<double*> last_out;
+  explicit LoopbackComm(int w) {
+    world = w;
+    n_local = w;
+    rank0 = 0;
+  }
+  const char* name() const override { return "loopback"; }
+  void exchange(const std::vector<double*>& v, const std::vector<int64_t>& b, int64_t nn,
+                cudaStream_t s) override {
+    const size_t bytes = sizeof(double) * static_cast<size_t>(nn);
+    for (int g = 1; g < world; ++g) {
+      // last row of g-1 -> leading ghost of g ; first row of g -> trailing ghost of g-1
+      cuda_check(cudaMemcpyAsync(v[g] + (b[g] - 1) * nn, v[g - 1] + (b[g] - 1) * nn, bytes,
+                                 cudaMemcpyDeviceToDevice, s), "ghost copy");
+      cuda_check(cudaMemcpyAsync(v[g - 1] + b[g] * nn, v[g] + b[g] * nn, bytes,
+                                 cudaMemcpyDeviceToDevice, s), "ghost copy");
+    }
+  }
+  void allreduce_sum(const std::vector<double*>& in, const std::vector<double*>& out,
+                     cudaStream_t s) override {
+    if (!ptrs) ptrs = std::make_unique<DeviceBuf>(2 * static_cast<int64_t>(world));
+    if (last_out != out || last_in.size() != in.size() ||
+        !std::equal(in.begin(), in.end(), last_in.begin())) {
+      std::vector<const void*> hp;
+      for (double* p : in) hp.push_back(p);
+      for (double* p : out) hp.push_back(p);
+      cuda_check(cudaMemcpy(ptrs->p, hp.data(), hp.size() * sizeof(void*), cudaMemcpyHostToDevice),
+                 "ptr upload");
+      last_in.assign(in.begin(), in.end());
+      last_out = out;
+    }
+    const double* const* pin = reinterpret_cast<const double* const*>(ptrs->p);
+    double* const* pout = reinterpret_cast<double* const*>(reinterpret_cast<void**>(ptrs->p) + world);
+    k_sum_scalars<<<1, 32, 0, s>>>(pin, world, pout);
+    launch_check(static_cast<int>(cudaGetLastError()), "sum scalars");
+  }
+  void gather_rows(const std::vector<double*>& src, double* dst,
+                   const std::vector<std::pair<int64_t, int64_t>>& rows, int64_t nn,
+                   cudaStream_t s) override {
+    for (int g = 0; g < world; ++g) {
+      const auto [lo, hi] = rows[g];
+      if (hi > lo)
+        cuda_check(cudaMemcpyAsync(dst + lo * nn, src[g] + lo * nn,
+                                   sizeof(double) * static_cast<size_t>((hi - lo) * nn),
+                                   cudaMemcpyDeviceToDevice, s), "gather copy");
+    }
+  }
+  void broadcast(const double* root, const std::vector<double*>& dst, int64_t count,
+                 cudaStream_t s) override {
+    for (int g = 0; g < world; ++g)
+      cuda_check(cudaMemcpyAsync(dst[g], root, sizeof(double) * static_cast<size_t>(count),
+                                 cudaMemcpyDeviceToDevice, s), "broadcast copy");
+  }
+};
+
+// NCCL entry points resolved at run time from libnccl.so.2.
+struct NcclApi {
+  decltype(&ncclCommInitRank) CommInitRank = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+  decltype(&ncclSend) Send = nullptr;
+  decltype(&ncclRecv) Recv = nullptr;
+  decltype(&ncclGroupStart) GroupStart = nullptr;
+  decltype(&ncclGroupEnd) GroupEnd = nullptr;
+  decltype(&ncclAllReduce) AllReduce = nullptr;
+  decltype(&ncclBroadcast) Broadcast = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+    if (!h) throw std::runtime_error("dist: libnccl.so.2 not found");
+    auto sym = [&](const char* n) {
+      void* p = dlsym(h, n);
+      if (!p) throw std::runtime_error(std::string("dist: NCCL symbol missing: ") + n);
+      return p;
+    };
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
+    a.Send = reinterpret_cast<decltype(a.Send)>(sym("ncclSend"));
+    a.Recv = reinterpret_cast<decltype(a.Recv)>(sym("ncclRecv"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
+    a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(sym("ncclAllReduce"));
+    a.Broadcast = reinterpret_cast<decltype(a.Broadcast)>(sym("ncclBroadcast"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
+    return a;
+  }();
+  return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw CudaError(std::string(what) + ": " + nccl().GetErrorString(r));
+}
+
+struct NcclComm : Comm {
+  ncclComm_t comm = nullptr;
+  NcclComm(int w, int rank, const ncclUniqueId& id) {
+    world = w;
+    n_local = 1;
+    rank0 = rank;
+    nccl_check(nccl().CommInitRank(&comm, w, id, rank), "ncclCommInitRank");
+  }
+  ~NcclComm() override {
+    if (comm) nccl().CommDestroy(comm);
+  }
+  const char* name() const override { return "nccl"; }
+  void exchange(const std::vector<double*>& v, const std::vector<int64_t>& b, int64_t nn,
+                cudaStream_t s) override {
+    const int g = rank0;
+    double* x = v[0];
+    const auto& A = nccl();
+    nccl_check(A.GroupStart(), "group");
+    if (g > 0) {
+      nccl_check(A.Send(x + b[g] * nn, nn, ncclDouble, g - 1, comm, s), "send");
+      nccl_check(A.Recv(x + (b[g] - 1) * nn, nn, ncclDouble, g - 1, comm, s), "recv");
+    }
+    if (g < world - 1) {
+      nccl_check(A.Send(x + (b[g + 1] - 1) * nn, nn, ncclDouble, g + 1, comm, s), "send");
+      nccl_check(A.Recv(x + b[g + 1] * nn, nn, ncclDouble, g + 1, comm, s), "recv");
+    }
+    nccl_check(A.GroupEnd(), "group");
+  }
+  void allreduce_sum(const std::vector<double*>& in, const std::vector<double*>& out,
+                     cudaStream_t s) override {
+    nccl_check(nccl().AllReduce(in[0], out[0], 1, ncclDouble, ncclSum, comm, s), "allreduce");
+  }
+  void gather_rows(const std::vector<double*>& src, double* dst,
+                   const std::vector<std::pair<int64_t, int64_t>>& rows, int64_t nn,
+                   cudaStream_t s) override {
+    const auto& A = nccl();
+    nccl_check(A.GroupStart(), "group");
+    if (rank0 == 0) {
+      for (int g = 1; g < world; ++g) {
+        const auto [lo, hi] = rows[g];
+        if (hi > lo) nccl_check(A.Recv(dst + lo * nn, (hi - lo) * nn, ncclDouble, g, comm, s), "recv");
+      }
+    } else {
+      const auto [lo, hi] = rows[rank0];
+      if (hi > lo) nccl_check(A.Send(src[0] + lo * nn, (hi - lo) * nn, ncclDouble, 0, comm, s), "send");
+    }
+    nccl_check(A.GroupEnd(), "group");
+    if (rank0 == 0) {
+      const auto [lo, hi] = rows[0];
+      if (hi > lo)
+        cuda_check(cudaMemcpyAsync(dst + lo * nn, src[0] + lo * nn,
+                                   sizeof(double) * static_cast<size_t>((hi - lo) * nn),
+                                   cudaMemcpyDeviceToDevice, s), "gather copy");
+    }
+  }
+  void broadcast(const double* root, const std::vector<double*>& dst, int64_t count,
+                 cudaStream_t s) override {
+    nccl_check(nccl().Broadcast(rank0 == 0 ? root : dst[0], dst[0], count, ncclDouble, 0, comm, s),
+               "broadcast");
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Distributed hierarchy
+// ---------------------------------------------------------------------------
+struct RankState {
+  std::vector<std::unique_ptr<DeviceBuf>> f, xa, xb;  // levels [0, Lg): full-size vectors
+  std::unique_ptr<DeviceBuf> fg, xg;                   // first gathered level: f rows out, x in
+  std::unique_ptr<DeviceBuf> partials, scalars;
+  std::vector<LevelView> views;  // levels [0, Lg) with this rank's slab row range
+};
+
+}  // namespace
+}  // namespace stmgb
+
+struct stmg_dist {
+  int device = 0;
+  bool adjoint = false;
+  std::vector<stmgb::HostLevel> host;
+  std::vector<int32_t> dirs;
+  stmgb::SlabPlan plan;
+  std::unique_ptr<stmgb::Comm> comm;
+  std::vector<std::unique_ptr<stmgb::DeviceBuf>> coef;
+  std::vector<stmgb::LevelView> full_views;
+  std::vector<stmgb::RankState> ranks;  // local ranks
+  stmg_hierarchy* tail = nullptr;       // root process: levels [Lg, L)
+  cudaStream_t stream = nullptr, cap_stream = nullptr;
+  double* pinned = nullptr;
+  std::map<stmgb::GraphKey, stmgb::GraphEntry> graphs;
+  int64_t device_bytes = 0;
+
+  ~stmg_dist() {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    for (auto& kv : graphs) {
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+      if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+    }
+    delete tail;
+    ranks.clear();
+    coef.clear();
+    comm.reset();
+    if (pinned) cudaFreeHost(pinned);
+    if (stream) cudaStreamDestroy(stream);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+    cudaSetDevice(prev);
+  }
+  int L() const { return static_cast<int>(host.size()); }
+  int Lg() const { return plan.Lg; }
+  int64_t nn(int l) const { return host[l].g.n_el + 1; }
+  int64_t ndofs(int l) const { return nn(l) * (host[l].g.n_t + 1); }
+};
+
+namespace stmgb {
+namespace {
+
+struct DistEmitter {
+  stmg_dist* d;
+  int nu;
+  double omega;
+  cudaStream_t s;
+  int64_t kernels = 0;
+
+  int W() const { return static_cast<int>(d->ranks.size()); }
+  double* buf(int k, int l, int which) {
+    return which == 0 ? d->ranks[k].xa[l]->p : d->ranks[k].xb[l]->p;
+  }
+  std::vector<double*> bufs(int l, int which) {
+    std::vector<double*> v;
+    for (int k = 0; k < W(); ++k) v.push_back(buf(k, l, which));
+    return v;
+  }
+  void exchange(int l, int which) { d->comm->exchange(bufs(l, which), d->plan.bounds[l], d->nn(l), s); }
+  void sweep_all(int l, int cur) {
+    exchange(l, cur);
+    for (int k = 0; k < W(); ++k) {
+      launch_check(launch_sweep(d->adjoint, d->ranks[k].views[l], d->ranks[k].f[l]->p, buf(k, l, cur),
+                                buf(k, l, 1 - cur), omega, nullptr, nullptr, s),
+                   "dist sweep");
+      ++kernels;
+    }
+  }
+
+  // Returns the buffer index holding the level-l result on every rank (2 = the
+  // broadcast gathered-level buffer xg, only for l == Lg).
+  int level(int l, int start, int pre_done, bool from_zero) {
+    const int Lg = d->Lg();
+    if (l == Lg) {
+      std::vector<double*> src;
+      std::vector<std::pair<int64_t, int64_t>> rows;
+      for (int k = 0; k < W(); ++k) src.push_back(d->ranks[k].fg->p);
+      for (int g = 0; g < d->plan.world; ++g)
+        rows.push_back(gathered_rows(d->plan, d->dirs[Lg - 1], g, d->host[Lg].g.n_t));
+      double* tail_f = d->comm->is_root() ? d->tail->ws->f[0]->p : nullptr;
+      d->comm->gather_rows(src, tail_f, rows, d->nn(Lg), s);
+      const double* root = nullptr;
+      if (d->comm->is_root()) {
+        Emitter em{d->tail, nu, omega, s};
+        const int fin = em.level(0, 0, 0, true);
+        kernels += em.kernels;
+        root = fin == 0 ? d->tail->ws->xa[0]->p : d->tail->ws->xb[0]->p;
+      }
+      std::vector<double*> dst;
+      for (int k = 0; k < W(); ++k) dst.push_back(d->ranks[k].xg->p);
+      d->comm->broadcast(root, dst, d->ndofs(Lg), s);
+      return 2;
+    }
+    int cur = start;
+    int pre = nu - pre_done;
+    if (from_zero) {
+      cur = 0;
+      for (int k = 0; k < W(); ++k) {
+        if (nu >= 1) {
+          launch_check(launch_sweep_from_zero(d->ranks[k].views[l], d->ranks[k].f[l]->p, buf(k, l, 0),
+                                              omega, s),
+                       "dist sweep0");
+          ++kernels;
+        } else {
+          const LevelView& V = d->ranks[k].views[l];
+          cuda_check(cudaMemsetAsync(buf(k, l, 0) + V.n_lo * V.nn, 0,
+                                     sizeof(double) * static_cast<size_t>((V.n_hi - V.n_lo) * V.nn), s),
+                     "memset");
+        }
+      }
+      pre = nu >= 1 ? nu - 1 : 0;
+    }
+    for (int it = 0; it < pre; ++it) {
+      sweep_all(l, cur);
+      cur = 1 - cur;
+    }
+    // residual + restriction into level l+1 (slab rows of l+1, or the rows this
+    // rank contributes to the first gathered level)
+    exchange(l, cur);
+    for (int k = 0; k < W(); ++k) {
+      const LevelView C = l + 1 < Lg ? d->ranks[k].views[l + 1] : d->full_views[l + 1];
+      double* fc = l + 1 < Lg ? d->ranks[k].f[l + 1]->p : d->ranks[k].fg->p;
+      launch_check(launch_restrict_residual(d->adjoint, d->ranks[k].views[l], C, d->dirs[l],
+                                            d->ranks[k].f[l]->p, buf(k, l, cur), fc, s),
+                   "dist restrict");
+      ++kernels;
+    }
+    const int child = level(l + 1, 0, 0, true);
+    if (child != 2) exchange(l + 1, child);  // coarse ghosts for the prolongation of ghost rows
+    std::vector<const double*> xc;
+    for (int k = 0; k < W(); ++k) xc.push_back(child == 2 ? d->ranks[k].xg->p : buf(k, l + 1, child));
+    int post = nu;
+    if (nu >= 1) {
+      for (int k = 0; k < W(); ++k) {
+        const LevelView C = l + 1 < Lg ? d->ranks[k].views[l + 1] : d->full_views[l + 1];
+        launch_check(launch_sweep_prolong(d->adjoint, d->ranks[k].views[l], C, d->dirs[l],
+                                          d->ranks[k].f[l]->p, buf(k, l, cur), xc[k],
+                                          buf(k, l, 1 - cur), omega, s),
+                     "dist sweep_prolong");
+        ++kernels;
+      }
+      cur = 1 - cur;
+      post = nu - 1;
+    } else {
+      for (int k = 0; k < W(); ++k) {
+        const LevelView C = l + 1 < Lg ? d->ranks[k].views[l + 1] : d->full_views[l + 1];
+        launch_check(launch_prolong_add(d->ranks[k].views[l], C, d->dirs[l], xc[k], buf(k, l, cur), s),
+                     "dist prolong");
+        ++kernels;
+      }
+    }
+    for (int it = 0; it < post; ++it) {
+      sweep_all(l, cur);
+      cur = 1 - cur;
+    }
+    return cur;
+  }
+};
+
+void dist_build(stmg_dist* d, int world, int rank, const void* nccl_id, int64_t min_slab) {
+  DeviceGuard dg(d->device);
+  launch_check(kernels_init(), "kernels_init");
+  std::vector<int64_t> nts;
+  for (const HostLevel& h : d->host) nts.push_back(h.g.n_t);
+  d->plan = plan_slabs(nts, d->dirs, world, min_slab);
+  if (d->plan.Lg < 1)
+    throw std::invalid_argument("dist: the finest level cannot be split into time slabs for this world size");
+  if (nccl_id) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    d->comm = std::make_unique<NcclComm>(world, rank, id);
+  } else {
+    d->comm = std::make_unique<LoopbackComm>(world);
+  }
+  for (const HostLevel& hl : d->host) {
+    const std::vector<double> t = hl.table(d->adjoint);
+    auto buf = std::make_unique<DeviceBuf>(static_cast<int64_t>(t.size()));
+    cuda_check(cudaMemcpy(buf->p, t.data(), t.size() * 8, cudaMemcpyHostToDevice), "coef upload");
+    LevelView v{hl.g.n_el, hl.g.n_t, hl.g.n_el + 1, hl.w, hl.inv_w, buf->p, 0, hl.g.n_t + 1};
+    d->full_views.push_back(v);
+    d->device_bytes += static_cast<int64_t>(t.size() * 8);
+    d->coef.push_back(std::move(buf));
+  }
+  const int Lg = d->plan.Lg;
+  d->ranks.resize(static_cast<size_t>(d->comm->n_local));
+  for (int k = 0; k < d->comm->n_local; ++k) {
+    const int g = d->comm->rank0 + k;
+    RankState& R = d->ranks[k];
+    int64_t max_partials = sumsq_partials_needed(0);
+    for (int l = 0; l < Lg; ++l) {
+      const int64_t nd = d->ndofs(l);
+      R.f.push_back(std::make_unique<DeviceBuf>(nd));
+      R.xa.push_back(std::make_unique<DeviceBuf>(nd));
+      R.xb.push_back(std::make_unique<DeviceBuf>(nd));
+      cuda_check(cudaMemset(R.xa.back()->p, 0, nd * 8), "memset");
+      cuda_check(cudaMemset(R.xb.back()->p, 0, nd * 8), "memset");
+      d->device_bytes += 3 * 8 * nd;
+      LevelView v = d->full_views[l];
+      v.n_lo = d->plan.bounds[l][g];
+      v.n_hi = d->plan.bounds[l][g + 1];
+      R.views.push_back(v);
+      max_partials = std::max(max_partials, sweep_partials_needed(v));
+    }
+    R.fg = std::make_unique<DeviceBuf>(d->ndofs(Lg));
+    R.xg = std::make_unique<DeviceBuf>(d->ndofs(Lg));
+    R.partials = std::make_unique<DeviceBuf>(max_partials);
+    R.scalars = std::make_unique<DeviceBuf>(8);
+    d->device_bytes += 8 * (2 * d->ndofs(Lg) + max_partials + 8);
+  }
+  if (d->comm->is_root()) {
+    auto t = std::make_unique<stmg_hierarchy>();
+    t->device = d->device;
+    t->adjoint = d->adjoint;
+    t->dirs.assign(d->dirs.begin() + Lg, d->dirs.end());
+    t->host.assign(d->host.begin() + Lg, d->host.end());
+    finish_create(t.get(), false, nullptr);
+    d->device_bytes += t->device_bytes;
+    d->tail = t.release();
+  }
+  cuda_check(cudaStreamCreateWithFlags(&d->stream, cudaStreamDefault), "cudaStreamCreate");
+  cuda_check(cudaStreamCreateWithFlags(&d->cap_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  cuda_check(cudaMallocHost(&d->pinned, 8 * sizeof(double)), "cudaMallocHost");
+  cuda_check(cudaDeviceSynchronize(), "sync");
+}
+
+GraphEntry& dist_graph(stmg_dist* d, int nu, double omega) {
+  const GraphKey key{nu, omega, false};
+  auto it = d->graphs.find(key);
+  if (it != d->graphs.end()) return it->second;
+  GraphEntry e;
+  DistEmitter em{d, nu, omega, d->cap_stream};
+  cuda_check(cudaStreamBeginCapture(d->cap_stream, cudaStreamCaptureModeThreadLocal), "capture");
+  e.final_buf = em.level(0, nu >= 1 ? 1 : 0, nu >= 1 ? 1 : 0, false);
+  cuda_check(cudaStreamEndCapture(d->cap_stream, &e.graph), "end capture");
+  cuda_check(cudaGraphInstantiate(&e.exec, e.graph, 0), "graph instantiate");
+  e.kernels = em.kernels;
+  return d->graphs.emplace(key, e).first->second;
+}
+
+// residual-norm pass on level 0 of every local rank (optionally the speculative
+// first sweep), all-reduced into scalars[slot] of every rank
+void dist_norm(stmg_dist* d, bool spec, double omega, int slot) {
+  std::vector<double*> X, in, out;
+  for (auto& R : d->ranks) X.push_back(R.xa[0]->p);
+  d->comm->exchange(X, d->plan.bounds[0], d->nn(0), d->stream);
+  for (auto& R : d->ranks) {
+    int64_t np = 0;
+    launch_check(launch_sweep(d->adjoint, R.views[0], R.f[0]->p, R.xa[0]->p, spec ? R.xb[0]->p : nullptr,
+                              omega, R.partials->p, &np, d->stream),
+                 "dist norm sweep");
+    launch_check(launch_finalize_sum(R.partials->p, np, R.scalars->p + 4, d->stream), "finalize");
+    in.push_back(R.scalars->p + 4);
+    out.push_back(R.scalars->p + slot);
+  }
+  d->comm->allreduce_sum(in, out, d->stream);
+}
+
+double dist_fetch(stmg_dist* d, int slot) {
+  cuda_check(cudaMemcpyAsync(d->pinned, d->ranks[0].scalars->p + slot, sizeof(double),
+                             cudaMemcpyDeviceToHost, d->stream), "scalar d2h");
+  cuda_check(cudaStreamSynchronize(d->stream), "sync");
+  return d->pinned[0];
+}
+
+void dist_solve(stmg_dist* d, const double* b, double* u, const stmg_solve_options& o,
+                stmg_solve_report* rep, double* history, int32_t cap) {
+  if (!b || !u) throw std::invalid_argument("mg_solve: vector size mismatch");
+  if (o.nu < 0 || o.omega <= 0.0 || o.tol <= 0.0 || o.div_tol <= o.tol || o.max_cycles < 0)
+    throw std::invalid_argument("mg_solve: invalid options");
+  if (!history || cap < o.max_cycles + 1)
+    throw std::invalid_argument("mg_solve: history buffer smaller than max_cycles + 1");
+  DeviceGuard dg(d->device);
+  const auto t0 = std::chrono::steady_clock::now();
+  const int64_t n = d->ndofs(0), nn = d->nn(0);
+  const size_t bytes = sizeof(double) * static_cast<size_t>(n);
+  const bool b_dev = is_device_ptr(b), u_dev = is_device_ptr(u);
+  for (auto& R : d->ranks) {
+    cuda_check(cudaMemcpyAsync(R.f[0]->p, b, bytes, b_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                               d->stream), "b copy");
+    cuda_check(cudaMemcpyAsync(R.xa[0]->p, u, bytes, u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                               d->stream), "u copy");
+  }
+  std::vector<double*> in, out;
+  for (auto& R : d->ranks) {
+    const LevelView& V = R.views[0];
+    int64_t np = 0;
+    launch_check(launch_sumsq(R.f[0]->p + V.n_lo * nn, (V.n_hi - V.n_lo) * nn, R.partials->p, &np, d->stream),
+                 "sumsq");
+    launch_check(launch_finalize_sum(R.partials->p, np, R.scalars->p + 4, d->stream), "finalize");
+    in.push_back(R.scalars->p + 4);
+    out.push_back(R.scalars->p + 0);
+  }
+  d->comm->allreduce_sum(in, out, d->stream);
+  const double norm_b = std::sqrt(dist_fetch(d, 0));
+  rep->absolute_norms = norm_b == 0.0 ? 1 : 0;
+  const double denom = rep->absolute_norms ? 1.0 : norm_b;
+  const bool spec = o.nu >= 1;
+  GraphEntry* g = o.max_cycles > 0 ? &dist_graph(d, o.nu, o.omega) : nullptr;
+  dist_norm(d, spec && o.max_cycles > 0, o.omega, 1);
+  const double r0 = std::sqrt(dist_fetch(d, 1)) / denom;
+  int nh = 0;
+  history[nh++] = r0;
+  rep->cycles = 0;
+  rep->factor = 1.0;
+  rep->smoother_dof_updates = 0.0;
+  rep->fine_sweeps = rep->fine_restricts = rep->fine_prolong_sweeps = 0;
+  rep->fine_sweep_seconds = rep->fine_restrict_seconds = rep->fine_prolong_sweep_seconds = 0.0;
+  // work of this process: its slab rows on distributed levels, the tail on the root
+  double per_cycle = 0.0;
+  for (const RankState& R : d->ranks)
+    for (int l = 0; l < d->Lg(); ++l)
+      per_cycle += 2.0 * o.nu * static_cast<double>((R.views[l].n_hi - R.views[l].n_lo) * R.views[l].nn);
+  if (d->comm->is_root())
+    for (int l = d->Lg(); l + 1 < d->L(); ++l) per_cycle += 2.0 * o.nu * static_cast<double>(d->ndofs(l));
+  int64_t launches = 0;
+  if (r0 < o.tol) {
+    rep->status = STMG_CONVERGED;
+  } else {
+    rep->status = STMG_MAX_CYCLES;
+    for (int cycle = 1; cycle <= o.max_cycles; ++cycle) {
+      cuda_check(cudaGraphLaunch(g->exec, d->stream), "graph launch");
+      launches += g->kernels;
+      if (g->final_buf != 0) throw std::logic_error("dist: level-0 iterate left the primary buffer");
+      dist_norm(d, spec && cycle < o.max_cycles, o.omega, 1);
+      const double rn = std::sqrt(dist_fetch(d, 1)) / denom;
+      history[nh++] = rn;
+      rep->cycles = cycle;
+      rep->smoother_dof_updates += per_cycle;
+      if (rn < o.tol) {
+        rep->status = STMG_CONVERGED;
+        break;
+      }
+      if (!std::isfinite(rn) || rn > o.div_tol) {
+        rep->status = STMG_DIVERGED;
+        break;
+      }
+    }
+  }
+  if (rep->cycles > 0) rep->factor = std::pow(history[nh - 1] / r0, 1.0 / rep->cycles);
+  // this process's slab rows of u (loopback: every rank's rows -> the full vector)
+  for (auto& R : d->ranks) {
+    const LevelView& V = R.views[0];
+    const size_t off = static_cast<size_t>(V.n_lo * nn);
+    cuda_check(cudaMemcpyAsync(u + off, R.xa[0]->p + off, sizeof(double) * static_cast<size_t>((V.n_hi - V.n_lo) * nn),
+                               u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, d->stream),
+               "u copy back");
+  }
+  cuda_check(cudaStreamSynchronize(d->stream), "sync");
+  rep->n_history = nh;
+  rep->kernel_launches = launches;
+  rep->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  rep->device_seconds = rep->seconds;
+}
+
+}  // namespace
+}  // namespace stmgb

@@ -523,6 +523,8 @@ void upload_levels(stmg_hierarchy* h) {
     v.w = hl.w;
     v.inv_w = hl.inv_w;
     v.coef = buf->p;
+    v.n_lo = 0;
+    v.n_hi = hl.g.n_t + 1;
     h->views.push_back(v);
     h->device_bytes += static_cast<int64_t>(t.size() * 8);
     h->coef.push_back(std::move(buf));
@@ -876,8 +878,54 @@ void load_vector_impl(const HostGrid& g, Q&& q, bool masked, double* b) {
   for (auto& t : th) t.join();
 }
 
+// build_hierarchy's host half (proj/src/multigrid.cpp:86-143): level grids,
+// coarse materials and per-node coefficients, no device work.
+std::vector<HostLevel> make_host_levels(const stmg_grid* g, const double* k, const double* c,
+                                        const double* chi, const stmg_material_pair* mat,
+                                        const char* method, int32_t n_dirs, const int32_t* dirs,
+                                        int* reasm_out) {
+  if (!g) throw std::invalid_argument("build_hierarchy: null grid");
+  const HostGrid fine = make_grid(g->L, g->t_T, g->n_el, g->n_t);
+  if (!k || !c) throw std::invalid_argument("build_hierarchy: fine grid has no materials");
+  const int reasm = parse_method(method);
+  if (reasm == STMG_REASM_D && (!chi || !mat))
+    throw std::invalid_argument("build_hierarchy: D reassembly needs the design field and materials");
+  if (n_dirs < 0 || (n_dirs > 0 && !dirs)) throw std::invalid_argument("build_hierarchy: bad path");
+  std::vector<HostLevel> host;
+  HostLevel l0;
+  l0.g = fine;
+  l0.k.assign(k, k + fine.n_el);
+  l0.c.assign(c, c + fine.n_el);
+  if (chi) l0.chi.assign(chi, chi + fine.n_el);
+  l0.build();
+  host.push_back(std::move(l0));
+  for (int32_t s = 0; s < n_dirs; ++s) {
+    const int dir = dirs[s];
+    if (dir == STMG_DIR_XT)
+      throw std::invalid_argument("stmg_b200: combined space-time (FullST) coarsening is not supported");
+    if (dir != STMG_DIR_X && dir != STMG_DIR_T) throw std::invalid_argument("build_hierarchy: bad direction");
+    const HostLevel& p = host.back();
+    HostLevel lc;
+    lc.g = coarsen(p.g, dir);
+    if (dir == STMG_DIR_T) {
+      lc.k = p.k;
+      lc.c = p.c;
+      lc.chi = p.chi;
+    } else {
+      coarsen_materials_x(p.k, p.c, p.chi.empty() ? nullptr : &p.chi, mat, reasm, lc.k, lc.c, &lc.chi);
+      if (reasm != STMG_REASM_D) lc.chi.clear();
+    }
+    lc.build();
+    host.push_back(std::move(lc));
+  }
+  if (reasm_out) *reasm_out = reasm;
+  return host;
+}
+
 }  // namespace
 }  // namespace stmgb
+
+#include "stmg_dist.cuh"
 
 using namespace stmgb;
 
@@ -949,46 +997,13 @@ int stmg_hierarchy_create(const stmg_grid* g, const double* k, const double* c, 
     if (!out) throw std::invalid_argument("build_hierarchy: null output handle");
     *out = nullptr;
     if (!g) throw std::invalid_argument("build_hierarchy: null grid");
-    const HostGrid fine = make_grid(g->L, g->t_T, g->n_el, g->n_t);
-    if (!k || !c) throw std::invalid_argument("build_hierarchy: fine grid has no materials");
-    const int reasm = parse_method(method);
-    if (reasm == STMG_REASM_D && (!chi || !mat))
-      throw std::invalid_argument("build_hierarchy: D reassembly needs the design field and materials");
-    if (n_dirs < 0 || (n_dirs > 0 && !dirs)) throw std::invalid_argument("build_hierarchy: bad path");
     int n_dev = 0;
     cuda_check(cudaGetDeviceCount(&n_dev), "cudaGetDeviceCount");
     if (device < 0 || device >= n_dev) throw std::invalid_argument("build_hierarchy: bad device ordinal");
     auto h = std::make_unique<stmg_hierarchy>();
     h->device = device;
-    h->reassembly = reasm;
     h->dirs.assign(dirs, dirs + n_dirs);
-    HostLevel l0;
-    l0.g = fine;
-    l0.k.assign(k, k + fine.n_el);
-    l0.c.assign(c, c + fine.n_el);
-    if (chi) l0.chi.assign(chi, chi + fine.n_el);
-    l0.build();
-    h->host.push_back(std::move(l0));
-    for (int32_t s = 0; s < n_dirs; ++s) {
-      const int dir = dirs[s];
-      if (dir == STMG_DIR_XT)
-        throw std::invalid_argument("stmg_b200: combined space-time (FullST) coarsening is not supported");
-      if (dir != STMG_DIR_X && dir != STMG_DIR_T) throw std::invalid_argument("build_hierarchy: bad direction");
-      const HostLevel& p = h->host.back();
-      HostLevel lc;
-      lc.g = coarsen(p.g, dir);
-      if (dir == STMG_DIR_T) {
-        lc.k = p.k;
-        lc.c = p.c;
-        lc.chi = p.chi;
-      } else {
-        coarsen_materials_x(p.k, p.c, p.chi.empty() ? nullptr : &p.chi, mat, reasm, lc.k, lc.c,
-                            &lc.chi);
-        if (reasm != STMG_REASM_D) lc.chi.clear();
-      }
-      lc.build();
-      h->host.push_back(std::move(lc));
-    }
+    h->host = make_host_levels(g, k, c, chi, mat, method, n_dirs, dirs, &h->reassembly);
     finish_create(h.get(), false, nullptr);
     *out = h.release();
   });
@@ -1185,6 +1200,76 @@ int stmg_norm2(stmg_hierarchy* h, const double* x, int64_t n, double* norm) {
 int stmg_debug_set_kernel_variant(int32_t v) {
   return guarded([&] { set_kernel_variant(v); });
 }
+
+// ---- time-slab multi-GPU --------------------------------------------------------
+int stmg_dist_partition(int32_t n_levels, const int64_t* n_t, const int32_t* dirs, int32_t world,
+                        int64_t min_slab, int32_t* n_distributed, int64_t* bounds) {
+  return guarded([&] {
+    if (n_levels < 1 || !n_t || (!dirs && n_levels > 1) || !n_distributed)
+      throw std::invalid_argument("dist_partition: bad arguments");
+    std::vector<int64_t> nts(n_t, n_t + n_levels);
+    std::vector<int32_t> d(dirs, dirs + (n_levels - 1));
+    const SlabPlan p = plan_slabs(nts, d, world, min_slab);
+    *n_distributed = p.Lg;
+    if (bounds)
+      for (int l = 0; l < p.Lg; ++l)
+        for (int g = 0; g <= world; ++g) bounds[static_cast<size_t>(l) * (world + 1) + g] = p.bounds[l][g];
+  });
+}
+
+int stmg_dist_nccl_unique_id(void* id_out, int32_t cap) {
+  return guarded([&] {
+    if (!id_out || cap < static_cast<int32_t>(sizeof(ncclUniqueId)))
+      throw std::invalid_argument("dist: unique-id buffer too small");
+    ncclUniqueId id;
+    nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+    std::memcpy(id_out, &id, sizeof(id));
+  });
+}
+
+int stmg_dist_create(const stmg_grid* g, const double* k, const double* c, const double* chi,
+                     const stmg_material_pair* mat, const char* method, int32_t n_dirs,
+                     const int32_t* dirs, int32_t adjoint, int32_t world, int32_t rank,
+                     const void* nccl_id, int32_t device, int64_t min_slab, stmg_dist** out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("dist_create: null output handle");
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("dist_create: bad rank/world");
+    int n_dev = 0;
+    cuda_check(cudaGetDeviceCount(&n_dev), "cudaGetDeviceCount");
+    if (device < 0 || device >= n_dev) throw std::invalid_argument("dist_create: bad device ordinal");
+    auto d = std::make_unique<stmg_dist>();
+    d->device = device;
+    d->adjoint = adjoint != 0;
+    d->dirs.assign(dirs, dirs + n_dirs);
+    d->host = make_host_levels(g, k, c, chi, mat, method, n_dirs, dirs, nullptr);
+    if (d->host.size() < 2) throw std::invalid_argument("dist_create: need at least two levels");
+    dist_build(d.get(), world, rank, nccl_id, min_slab);
+    *out = d.release();
+  });
+}
+
+int stmg_dist_info(const stmg_dist* d, int32_t* n_distributed, int64_t* row_lo, int64_t* row_hi,
+                   int32_t* n_local, int64_t* device_bytes) {
+  return guarded([&] {
+    if (!d) throw std::invalid_argument("null handle");
+    if (n_distributed) *n_distributed = d->plan.Lg;
+    if (row_lo) *row_lo = d->ranks.front().views[0].n_lo;
+    if (row_hi) *row_hi = d->ranks.back().views[0].n_hi;
+    if (n_local) *n_local = static_cast<int32_t>(d->ranks.size());
+    if (device_bytes) *device_bytes = d->device_bytes;
+  });
+}
+
+int stmg_dist_mg_solve(stmg_dist* d, const double* b, double* u, const stmg_solve_options* opts,
+                       stmg_solve_report* report, double* history, int32_t cap) {
+  return guarded([&] {
+    if (!d || !opts || !report) throw std::invalid_argument("mg_solve: null argument");
+    dist_solve(d, b, u, *opts, report, history, cap);
+  });
+}
+
+void stmg_dist_destroy(stmg_dist* d) { delete d; }
 
 int stmg_synchronize(stmg_hierarchy* h) {
   return guarded([&] {

@@ -21,7 +21,14 @@ struct LevelView {
   double w;
   double inv_w;
   const double* coef;  // 7 * nn: cm, c0, cp, om, o0, op, inv_diag
+  // Rows (time levels) a launch computes: [n_lo, n_hi).  The full level is
+  // [0, n_t + 1); a time slab of a distributed level is a sub-range (vectors
+  // stay full-size and globally indexed; only the slab is read and written).
+  int64_t n_lo;
+  int64_t n_hi;
 };
+
+inline bool full_range(const LevelView& L) { return L.n_lo == 0 && L.n_hi == L.n_t + 1; }
 
 enum Coef { kCm = 0, kC0 = 1, kCp = 2, kOm = 3, kO0 = 4, kOp = 5, kInvD = 6, kNumCoef = 7 };
 

@@ -317,12 +317,13 @@ __global__ void __launch_bounds__(kMaxTW, MINB) k_lean2(LevelView L, Ld ld,
   const int64_t tile = bid % node_tiles, ttile = bid / node_tiles;
   const int64_t per_block = (int64_t)(blockDim.x >> 5) * 30;
   const int64_t i = tile * per_block + warp * 30 + lane - 1;  // node of this lane
-  const int64_t n0 = ttile * NT;
+  const int64_t n0 = L.n_lo + ttile * NT;
   const int64_t nbase = ADJ ? n0 : n0 - 1;
   const bool in_grid = i >= 0 && i < nn;
   const bool computes = lane >= 1 && lane <= 30 && in_grid;
   const int64_t wfirst = tile * per_block + warp * 30;  // first computing node
-  const bool rows_in = ADJ ? (n0 >= 1 && n0 + NT - 1 <= nt - 1) : (n0 >= 2 && n0 + NT - 1 <= nt);
+  const bool rows_in = (ADJ ? (n0 >= 1 && n0 + NT - 1 <= nt - 1) : (n0 >= 2 && n0 + NT - 1 <= nt)) &&
+                       n0 + NT - 1 < L.n_hi;
   const bool nodes_in = wfirst >= 2 && wfirst + 29 <= L.n_el - 1;
   double xr[NT + 1], fv[NT];
   Coefs c{};
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(kMaxTW, MINB) k_lean2(LevelView L, Ld ld,
 #pragma unroll
     for (int k = 0; k < NT; ++k) {
       const int64_t n = n0 + k;
-      fv[k] = (computes && n <= nt) ? f[n * nn + i] : 0.0;
+      fv[k] = (computes && n < L.n_hi) ? f[n * nn + i] : 0.0;
     }
 #pragma unroll
     for (int r = 0; r <= NT; ++r) {
@@ -380,7 +381,7 @@ __global__ void __launch_bounds__(kMaxTW, MINB) k_lean2(LevelView L, Ld ld,
 #pragma unroll
     for (int k = 0; k < NT; ++k) {
       const int64_t n = n0 + k;
-      if (n > nt) break;
+      if (n >= L.n_hi) break;
       const double x1 = xr[k + 1];
       const double qm = __shfl_up_sync(kFull, x1, 1);
       const double qp = __shfl_down_sync(kFull, x1, 1);
@@ -421,7 +422,7 @@ __global__ void __launch_bounds__(kMaxTW, 2) k_lean_restrict(LevelView F, LevelV
   const int lane = threadIdx.x & 31;
   const int64_t nn = F.nn, nt = F.n_t, nnc = C.nn;
   const int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
-  const int64_t n0 = (int64_t)blockIdx.x * NT;
+  const int64_t n0 = F.n_lo + (int64_t)blockIdx.x * NT;
   const int64_t nbase = ADJ ? n0 : n0 - 1;
   const int64_t wfirst = i - lane;
   const bool valid = i < nn;
@@ -433,8 +434,8 @@ __global__ void __launch_bounds__(kMaxTW, 2) k_lean_restrict(LevelView F, LevelV
 #pragma unroll
   for (int k = 0; k < NT; ++k) {
     const int64_t n = n0 + k;
-    fv[k] = (valid && n <= nt) ? f[n * nn + i] : 0.0;
-    f1[k] = (xr1 && n <= nt) ? f[n * nn + i - 1] : 0.0;
+    fv[k] = (valid && n < F.n_hi) ? f[n * nn + i] : 0.0;
+    f1[k] = (xr1 && n < F.n_hi) ? f[n * nn + i - 1] : 0.0;
   }
 #pragma unroll
   for (int r = 0; r <= NT; ++r) {
@@ -450,7 +451,8 @@ __global__ void __launch_bounds__(kMaxTW, 2) k_lean_restrict(LevelView F, LevelV
   // interior tile: every row has its coupled level, every node (incl. lane 0's
   // extra node i - 1) has both same-level neighbours, every coarse node has
   // all three fine contributions -> fixed canonical orders, no branches.
-  const bool rows_in = ADJ ? (n0 >= 1 && n0 + NT - 1 <= nt - 1) : (n0 >= 2 && n0 + NT - 1 <= nt);
+  const bool rows_in = (ADJ ? (n0 >= 1 && n0 + NT - 1 <= nt - 1) : (n0 >= 2 && n0 + NT - 1 <= nt)) &&
+                       n0 + NT - 1 < F.n_hi;
   const bool nodes_in = wfirst >= 32 && wfirst + 31 <= F.n_el - 1;
   double pm = __shfl_up_sync(kFull, xr[0], 1);
   double pp = __shfl_down_sync(kFull, xr[0], 1);
@@ -525,7 +527,7 @@ __global__ void __launch_bounds__(kMaxTW, 2) k_lean_restrict(LevelView F, LevelV
 #pragma unroll
   for (int k = 0; k < NT; ++k) {
     const int64_t n = n0 + k;
-    if (n > nt) break;
+    if (n >= F.n_hi) break;
     const double x1 = xr[k + 1];
     double qm = __shfl_up_sync(kFull, x1, 1);
     double qp = __shfl_down_sync(kFull, x1, 1);
@@ -583,12 +585,12 @@ __global__ void k_sweep_from_zero2(LevelView L, const double* __restrict__ f, do
                                    double omega) {
   const int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
   if (i >= L.nn) return;
-  const int64_t n0 = (int64_t)blockIdx.x * kFlatNT;
+  const int64_t n0 = L.n_lo + (int64_t)blockIdx.x * kFlatNT;
   const double idv = __ldg(L.coef + kInvD * L.nn + i);
 #pragma unroll
   for (int k = 0; k < kFlatNT; ++k) {
     const int64_t n = n0 + k;
-    if (n > L.n_t) break;
+    if (n >= L.n_hi) break;
     const double id = (n == 0 || i == 0) ? L.inv_w : idv;
     y[n * L.nn + i] = 0.0 + omega * (f[n * L.nn + i] * id);
   }
@@ -599,11 +601,11 @@ __global__ void k_prolong_add2(LevelView F, LevelView C, const double* __restric
                                double* __restrict__ x) {
   const int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
   if (i >= F.nn) return;
-  const int64_t n0 = (int64_t)blockIdx.x * kFlatNT;
+  const int64_t n0 = F.n_lo + (int64_t)blockIdx.x * kFlatNT;
 #pragma unroll
   for (int k = 0; k < kFlatNT; ++k) {
     const int64_t n = n0 + k;
-    if (n > F.n_t) break;
+    if (n >= F.n_hi) break;
     x[n * F.nn + i] = x[n * F.nn + i] + prolong_row<DIR>(xc, C.nn, n, i);
   }
 }
@@ -1203,10 +1205,13 @@ inline int64_t lean2_tiles(const LevelView& L, dim3 blk) {
   const int64_t per = (int64_t)(blk.x / 32) * 30;
   return (L.nn + per - 1) / per;
 }
+inline int64_t rows(const LevelView& L) { return L.n_hi - L.n_lo; }
+// Sub-range (slab) launches always use the production design.
+inline int eff_variant(const LevelView& L) { return full_range(L) ? g_variant : kDefaultVariant; }
 inline dim3 grid_for(const LevelView& L, dim3 blk, int v) {
   if (v == 5 || v == 6) {
     const int nt = variant_nt(v);
-    return dim3((unsigned)(lean2_tiles(L, blk) * ((L.n_t + 1 + nt - 1) / nt)));
+    return dim3((unsigned)(lean2_tiles(L, blk) * ((rows(L) + nt - 1) / nt)));
   }
   const unsigned tiles = (unsigned)((L.nn + blk.x - 1) / blk.x);
   if (v == 3) {
@@ -1222,8 +1227,9 @@ inline unsigned flat_grid(int64_t total) { return (unsigned)((total + kFlatBlock
 template <bool ADJ, int MODE, bool NORM, class Ld>
 void launch_pass(const LevelView& L, const Ld& ld, const double* f, double* y, double omega,
                  double* partials, cudaStream_t s) {
-  const dim3 blk = march_block(L), grd = grid_for(L, blk, g_variant);
-  switch (g_variant) {
+  const int v = eff_variant(L);
+  const dim3 blk = march_block(L), grd = grid_for(L, blk, v);
+  switch (v) {
     case 1:
       k_lean<ADJ, MODE, NORM, 4, 3><<<grd, blk, 0, s>>>(L, ld, f, y, omega, partials);
       break;
@@ -1272,13 +1278,14 @@ template <bool ADJ, int DIR>
 int restrict_tile_impl(const LevelView& F, const LevelView& C, const double* f, const double* x,
                        double* fc, cudaStream_t s) {
   const dim3 blk = march_block(F);
-  if (g_variant == 0 || g_variant == 1 || g_variant == 5 || g_variant == 6) {
+  const int v = eff_variant(F);
+  if (v == 0 || v == 1 || v == 5 || v == 6) {
     constexpr int NT = DIR == 0 ? 4 : 8;
-    const dim3 grd((unsigned)((F.n_t + 1 + NT - 1) / NT), (unsigned)((F.nn + blk.x - 1) / blk.x));
+    const dim3 grd((unsigned)((rows(F) + NT - 1) / NT), (unsigned)((F.nn + blk.x - 1) / blk.x));
     k_lean_restrict<ADJ, DIR, NT><<<grd, blk, 0, s>>>(F, C, f, x, fc);
     return check_launch();
   }
-  if (g_variant == 3) {
+  if (v == 3) {
     const dim3 grd = grid_for(F, blk, 3);
     k_restrict_stream<ADJ, DIR><<<grd, blk, 0, s>>>(F, C, f, x, fc, stream_chunk(F, blk));
     return check_launch();
@@ -1309,7 +1316,7 @@ int64_t sumsq_partials_needed(int64_t) { return kSumGrid; }
 int launch_sweep(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
                  double omega, double* partials, int64_t* n_partials, cudaStream_t s) {
   if (n_partials) {
-    const dim3 blk = march_block(L), grd = grid_for(L, blk, g_variant);
+    const dim3 blk = march_block(L), grd = grid_for(L, blk, eff_variant(L));
     *n_partials = (int64_t)grd.x * grd.y;
   }
   return adjoint ? sweep_impl<true>(L, f, x, y, omega, partials, s)
@@ -1319,7 +1326,7 @@ int launch_sweep(bool adjoint, const LevelView& L, const double* f, const double
 int launch_sweep_from_zero(const LevelView& L, const double* f, double* y, double omega,
                            cudaStream_t s) {
   const dim3 blk = march_block(L);
-  const dim3 grd((unsigned)((L.n_t + 1 + kFlatNT - 1) / kFlatNT), (unsigned)((L.nn + blk.x - 1) / blk.x));
+  const dim3 grd((unsigned)((rows(L) + kFlatNT - 1) / kFlatNT), (unsigned)((L.nn + blk.x - 1) / blk.x));
   k_sweep_from_zero2<<<grd, blk, 0, s>>>(L, f, y, omega);
   return check_launch();
 }
@@ -1365,7 +1372,7 @@ int launch_restrict(const LevelView& F, const LevelView& C, int dir, const doubl
 int launch_prolong_add(const LevelView& F, const LevelView& C, int dir, const double* xc, double* x,
                        cudaStream_t s) {
   const dim3 blk = march_block(F);
-  const dim3 grd((unsigned)((F.n_t + 1 + kFlatNT - 1) / kFlatNT), (unsigned)((F.nn + blk.x - 1) / blk.x));
+  const dim3 grd((unsigned)((rows(F) + kFlatNT - 1) / kFlatNT), (unsigned)((F.nn + blk.x - 1) / blk.x));
   if (dir == 0) k_prolong_add2<0><<<grd, blk, 0, s>>>(F, C, xc, x);
   else k_prolong_add2<1><<<grd, blk, 0, s>>>(F, C, xc, x);
   return check_launch();

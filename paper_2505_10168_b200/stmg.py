@@ -74,6 +74,13 @@ def _load():
         "stmg_norm2": [vp, vp, i64, C.POINTER(f64)],
         "stmg_synchronize": [vp],
         "stmg_debug_set_kernel_variant": [i32],
+        "stmg_dist_partition": [i32, vp, vp, i32, i64, C.POINTER(i32), vp],
+        "stmg_dist_nccl_unique_id": [vp, i32],
+        "stmg_dist_create": [vp, vp, vp, vp, vp, C.c_char_p, i32, vp, i32, i32, i32, vp, i32, i64,
+                             C.POINTER(vp)],
+        "stmg_dist_info": [vp, C.POINTER(i32), C.POINTER(i64), C.POINTER(i64), C.POINTER(i32),
+                           C.POINTER(i64)],
+        "stmg_dist_mg_solve": [vp, vp, vp, vp, vp, vp, i32],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -81,6 +88,8 @@ def _load():
         fn.restype = C.c_int
     lib.stmg_hierarchy_destroy.argtypes = [vp]
     lib.stmg_hierarchy_destroy.restype = None
+    lib.stmg_dist_destroy.argtypes = [vp]
+    lib.stmg_dist_destroy.restype = None
     return lib
 
 
@@ -538,6 +547,96 @@ def mg_solve(h: LevelHierarchy, b, u, opts: Optional[SolveOptions] = None) -> So
                        [float(v) for v in hist[: rep.n_history]], bool(rep.absolute_norms),
                        rep.seconds, rep.device_seconds, rep.smoother_dof_updates, rep.kernel_launches,
                        kt)
+
+
+# ---- time-slab multi-GPU ------------------------------------------
+def dist_partition(n_t_per_level: Sequence[int], dirs: Sequence[int], world: int,
+                   min_slab: int = 16) -> tuple[int, np.ndarray]:
+    """(number of distributed levels Lg, bounds[Lg, world+1]) of the time-slab split."""
+    nts = np.ascontiguousarray(n_t_per_level, np.int64)
+    d = np.ascontiguousarray(list(dirs) if len(dirs) else [0], np.int32)
+    lg = C.c_int32()
+    bounds = np.zeros(nts.size * (world + 1), np.int64)
+    _check(_lib.stmg_dist_partition(nts.size, nts.ctypes.data, d.ctypes.data, int(world),
+                                    int(min_slab), C.byref(lg), bounds.ctypes.data))
+    return lg.value, bounds[: lg.value * (world + 1)].reshape(lg.value, world + 1)
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    _check(_lib.stmg_dist_nccl_unique_id(buf, 128))
+    return bytes(buf)
+
+
+class DistHierarchy:
+    """Time-slab distributed hierarchy (include/stmg_b200.h, stmg_dist_*)."""
+
+    def __init__(self, handle, levels, world, rank):
+        self._h = handle
+        self.levels = levels
+        self.world = world
+        self.rank = rank
+        lg, lo, hi, nl, db = C.c_int32(), C.c_int64(), C.c_int64(), C.c_int32(), C.c_int64()
+        _check(_lib.stmg_dist_info(self._h, C.byref(lg), C.byref(lo), C.byref(hi), C.byref(nl), C.byref(db)))
+        self.n_distributed = lg.value
+        self.row_lo, self.row_hi, self.n_local, self.device_bytes = lo.value, hi.value, nl.value, db.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.stmg_dist_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+
+def build_dist_hierarchy(fine: SpaceTimeGrid, method, path: CoarseningPath, world: int, rank: int = 0,
+                         nccl_id: Optional[bytes] = None, device: int = 0, adjoint: bool = False,
+                         chi=None, mat=None, min_slab: int = 16) -> DistHierarchy:
+    """Distributed (time-slab) hierarchy.  nccl_id=None: loopback (all ranks in this process)."""
+    if not fine.has_materials():
+        raise ValueError("build_hierarchy: fine grid has no materials")
+    k = _f64(fine.k, fine.n_el)
+    c = _f64(fine.c, fine.n_el)
+    chi_a = None if chi is None else _f64(chi, fine.n_el)
+    m = None if mat is None else MaterialPair.of(mat)._c()
+    dirs = np.array([int(d) for d in path.dirs], np.int32)
+    idbuf = None if nccl_id is None else (C.c_char * 128).from_buffer_copy(nccl_id)
+    h = C.c_void_p()
+    gc = fine._c()
+    _check(_lib.stmg_dist_create(C.byref(gc), k.ctypes.data, c.ctypes.data,
+                                 None if chi_a is None else chi_a.ctypes.data,
+                                 None if m is None else C.byref(m), str(method).encode(), dirs.size,
+                                 dirs.ctypes.data if dirs.size else None, 1 if adjoint else 0,
+                                 int(world), int(rank), idbuf, int(device), int(min_slab), C.byref(h)))
+    levels = []
+    ne, nt = fine.n_el, fine.n_t
+    levels.append(LevelInfo(ne, nt, 0.0))
+    for d in dirs:
+        if d == 0:
+            ne //= 2
+        else:
+            nt //= 2
+        levels.append(LevelInfo(ne, nt, 0.0))
+    return DistHierarchy(h, levels, world, rank)
+
+
+def mg_solve_dist(h: DistHierarchy, b, u, opts: Optional[SolveOptions] = None) -> SolveReport:
+    """Distributed solve; b, u full-size; u receives this process's slab rows (loopback: all)."""
+    o = opts or SolveOptions()
+    n = h.levels[0].n_dofs
+    if _numel(b) != n or _numel(u) != n:
+        raise ValueError("mg_solve: vector size mismatch")
+    hist = np.zeros(max(o.max_cycles, 0) + 1, np.float64)
+    rep = _SolveRep()
+    co = _SolveOpts(int(o.nu), float(o.omega), float(o.tol), float(o.div_tol), int(o.max_cycles))
+    _check(_lib.stmg_dist_mg_solve(h.handle, _ptr(b), _ptr(u), C.byref(co), C.byref(rep),
+                                   hist.ctypes.data, hist.size))
+    return SolveReport(SolveStatus(rep.status), rep.cycles, rep.factor,
+                       [float(v) for v in hist[: rep.n_history]], bool(rep.absolute_norms),
+                       rep.seconds, rep.device_seconds, rep.smoother_dof_updates, rep.kernel_launches)
 
 
 def set_kernel_variant(v: int) -> None:

@@ -1,0 +1,81 @@
+"""Time-slab multi-GPU path, validated on one GPU with the loopback transport:
+all `world` ranks of the exact product code path (slab kernels, ghost
+exchanges, all-reduced norms, gather / tail solve / broadcast) run in one
+process, and must reproduce the single-domain solve: identical iterate
+(bitwise), same cycle count, histories equal up to norm summation order."""
+import numpy as np
+import pytest
+
+from tests._cases import case
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need CUDA (no CPU fallback exists)"
+    from paper_2505_10168_b200 import stmg
+
+    return stmg
+
+
+def grid_path(S, cs, port):
+    dirs = cs.plan(port)
+    g = S.build_fine_grid(cs.L, cs.tT, cs.n_el, cs.n_t)
+    g.k, g.c = cs.k, cs.c
+    return g, S.CoarseningPath([S.CoarseningDirection(int(d)) for d in dirs])
+
+
+@pytest.mark.parametrize("name,world", [("cfg1_mini", 2), ("cfg1_mini", 4), ("cfg1_mini_adj", 4),
+                                        ("cfg4_mini", 8), ("cfgD", 2), ("cfg0_deep", 2), ("cfg2_mini", 4)])
+def test_loopback_slabs_match_single_domain(S, port, name, world):
+    cs = case(name)
+    g, path = grid_path(S, cs, port)
+    b = cs.rhs_vector(port)
+    opts = S.SolveOptions(nu=cs.nu, tol=cs.tol, max_cycles=cs.max_cycles)
+    h = S.build_hierarchy(g, cs.method, path, chi=cs.chi, mat=cs.mat)
+    if cs.adjoint:
+        h = S.transposed_hierarchy(h)
+    u1 = np.zeros_like(b)
+    r1 = S.mg_solve(h, b, u1, opts)
+    dh = S.build_dist_hierarchy(g, cs.method, path, world, adjoint=cs.adjoint, chi=cs.chi, mat=cs.mat,
+                                min_slab=8)
+    assert dh.n_distributed >= 1
+    u2 = np.zeros_like(b)
+    r2 = S.mg_solve_dist(dh, b, u2, opts)
+    assert r2.cycles == r1.cycles and r2.status == r1.status
+    assert np.array_equal(u1.view(np.uint64), u2.view(np.uint64))
+    assert np.allclose(r2.history, r1.history, rtol=1e-12, atol=0)
+
+
+def test_partition_rules(S):
+    # cfg1 path x,x,x,t,x,t,t,x,t: n_t per level 4096 x4, 2048 x2, 1024, 512 x2, 256
+    nts = [4096, 4096, 4096, 4096, 2048, 2048, 1024, 512, 512, 256]
+    dirs = [0, 0, 0, 1, 0, 1, 1, 0, 1]
+    lg, b = S.dist_partition(nts, dirs, 8, 16)
+    assert lg == 9  # the coarsest level is always gathered
+    assert list(b[0]) == [0, 512, 1024, 1536, 2048, 2560, 3072, 3584, 4097]
+    assert list(b[3])[-1] == 4097 and b[4][1] == 256
+    lg, _ = S.dist_partition(nts, dirs, 8, 128)
+    assert lg == 7  # level 7 has 512/8 = 64 < 128 steps per slab
+    lg, _ = S.dist_partition([30, 15], [1], 4, 8)
+    assert lg == 0  # 30 steps do not split into 4 slabs
+
+
+def test_nccl_transport_world1_matches_single_domain(S, port):
+    """The NCCL transport itself (dlopen'ed libnccl, communicator init, NCCL
+    calls captured in the V-cycle graph) on a one-rank communicator."""
+    cs = case("cfg1_mini")
+    g, path = grid_path(S, cs, port)
+    b = cs.rhs_vector(port)
+    opts = S.SolveOptions(nu=cs.nu, tol=cs.tol, max_cycles=cs.max_cycles)
+    h = S.build_hierarchy(g, cs.method, path)
+    u1 = np.zeros_like(b)
+    r1 = S.mg_solve(h, b, u1, opts)
+    dh = S.build_dist_hierarchy(g, cs.method, path, 1, rank=0, nccl_id=S.nccl_unique_id(), min_slab=8)
+    u2 = np.zeros_like(b)
+    r2 = S.mg_solve_dist(dh, b, u2, opts)
+    assert r2.cycles == r1.cycles
+    assert np.array_equal(u1.view(np.uint64), u2.view(np.uint64))
