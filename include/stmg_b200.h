@@ -206,6 +206,44 @@ int stmg_residual_norm(stmg_hierarchy* h, const double* f, const double* x, doub
 int stmg_norm2(stmg_hierarchy* h, const double* x, int64_t n, double* norm);
 int stmg_synchronize(stmg_hierarchy* h);
 
+/* ---- topology-optimisation driver (BASELINE config 4) ---------------------------
+ * optimise(), proj/src/optimisation.cpp:83-186: per iteration apply_design ->
+ * plan_coarsening -> build (here: coefficients refreshed in place when the path
+ * is unchanged) -> warm primal mg_solve -> objective -> adjoint mg_solve on the
+ * transposed hierarchy -> sensitivities (on the GPU, the reference's
+ * arithmetic) -> MMA design update (host, restating proj/src/mma.cpp). */
+typedef struct stmg_optimise_options {
+  stmg_material_pair mat;
+  char method[4];       /* "CR" (OptimisationOptions default), "CK", "CD" */
+  int32_t strategy;     /* stmg_strategy */
+  int32_t n_levels;
+  double lambda_crit;
+  int64_t min_elements;
+  int32_t warm_start;
+  double volume_limit;
+  double theta_ref;
+  double chi_init;
+  int32_t max_iterations;
+  double rel_change_tol;
+  int32_t stable_iterations;
+  stmg_solve_options solve;
+  double mma_x_min, mma_x_max, mma_move_limit, mma_asym_init, mma_asym_shrink, mma_asym_grow;
+} stmg_optimise_options;
+
+/* IterationRecord, proj/include/stmg/optimisation.hpp:77-92 (path as dirs). */
+typedef struct stmg_iteration_record {
+  int32_t iteration;
+  double theta, volume, constraint, change;
+  int32_t primal_status, adjoint_status, primal_cycles, adjoint_cycles;
+  double primal_factor, adjoint_factor, primal_seconds, adjoint_seconds;
+} stmg_iteration_record;
+
+/* Fills chi_out (n_el, the final post-update design), records (max_iterations),
+ * and the scalars; returns STMG_OK or an error code. */
+int stmg_optimise(const stmg_grid* geom, const stmg_optimise_options* opts, int32_t device,
+                  double* chi_out, stmg_iteration_record* records, int32_t* n_records,
+                  double* theta, int32_t* converged, double* seconds);
+
 /* ---- time-slab multi-GPU ------------------------------------
  * A distributed hierarchy splits the time axis of every level that can be cut
  * into `world` equal slabs (>= min_slab levels, even where the next step

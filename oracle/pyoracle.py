@@ -241,6 +241,9 @@ class Ref:
         lib.ref_norm2.argtypes = [_dp, C.c_longlong]
         lib.ref_norm2.restype = f64
         lib.ref_set_backend.argtypes = [i32]
+        lib.ref_optimise.argtypes = [f64, f64, i32, i32, _dp, C.c_char_p, i32, i32, f64, i32, i32, f64, f64,
+                                     f64, i32, f64, i32, i32, f64, f64, f64, i32, _dp, _dp,
+                                     C.POINTER(i32), C.POINTER(f64), C.POINTER(i32), C.POINTER(f64)]
         self.lib = lib
 
     def _chk(self, rc):
@@ -283,6 +286,23 @@ class Ref:
 
     def norm2(self, x):
         return self.lib.ref_norm2(np.ascontiguousarray(x, np.float64), x.size)
+
+    def optimise(self, L, tT, n_el, n_t, mat, method="CR", strategy=3, n_levels=6, lambda_crit=0.25,
+                 min_elements=0, warm_start=True, volume_limit=0.5, theta_ref=1e6, chi_init=0.5,
+                 max_iterations=10, rel_change_tol=1e-3, stable_iterations=5, nu=20, omega=0.5,
+                 tol=1e-9, div_tol=1e9, max_cycles=100):
+        chi = np.zeros(n_el)
+        rec = np.zeros(12 * max_iterations)
+        nr, conv = C.c_int(), C.c_int()
+        th, secs = C.c_double(), C.c_double()
+        self._chk(self.lib.ref_optimise(L, tT, n_el, n_t, np.ascontiguousarray(mat, np.float64),
+                                        method.encode(), strategy, n_levels, lambda_crit, min_elements,
+                                        1 if warm_start else 0, volume_limit, theta_ref, chi_init,
+                                        max_iterations, rel_change_tol, stable_iterations, nu, omega,
+                                        tol, div_tol, max_cycles, chi, rec, C.byref(nr), C.byref(th),
+                                        C.byref(conv), C.byref(secs)))
+        return dict(chi=chi, records=rec[: 12 * nr.value].reshape(nr.value, 12), theta=th.value,
+                    converged=bool(conv.value), seconds=secs.value)
 
 
 class RefHier:

@@ -295,6 +295,52 @@ int ref_apply_design(const double* chi, int n, const double* mat6, double* k, do
   });
 }
 
+// optimise(), proj/src/optimisation.cpp:83-186.  rec: per iteration 12 doubles
+// {theta, volume, constraint, change, primal_status, adjoint_status,
+//  primal_cycles, adjoint_cycles, primal_factor, adjoint_factor, primal_s, adjoint_s}
+int ref_optimise(double L, double tT, int n_el, int n_t, const double* mat6, const char* method,
+                 int strategy, int n_levels, double lambda_crit, int min_elements, int warm_start,
+                 double volume_limit, double theta_ref, double chi_init, int max_iterations,
+                 double rel_change_tol, int stable_iterations, int nu, double omega, double tol,
+                 double div_tol, int max_cycles, double* chi_out, double* rec, int* n_rec,
+                 double* theta, int* converged, double* seconds) {
+  return guarded([&] {
+    const SpaceTimeGrid g = build_fine_grid(L, tT, n_el, n_t);
+    OptimisationOptions o;
+    o.method = parse_method(method);
+    o.strategy = to_strategy(strategy);
+    o.n_levels = n_levels;
+    o.lambda_crit = lambda_crit;
+    o.min_elements = min_elements;
+    o.warm_start = warm_start != 0;
+    o.volume_limit = volume_limit;
+    o.theta_ref = theta_ref;
+    o.chi_init = chi_init;
+    o.max_iterations = max_iterations;
+    o.rel_change_tol = rel_change_tol;
+    o.stable_iterations = stable_iterations;
+    o.solve.nu = nu;
+    o.solve.omega = omega;
+    o.solve.tol = tol;
+    o.solve.div_tol = div_tol;
+    o.solve.max_cycles = max_cycles;
+    const OptimisationResult r = optimise(g, make_mat(mat6), o);
+    std::memcpy(chi_out, r.chi.chi.data(), sizeof(double) * r.chi.chi.size());
+    for (std::size_t i = 0; i < r.history.size(); ++i) {
+      const IterationRecord& h = r.history[i];
+      double* d = rec + 12 * i;
+      d[0] = h.theta; d[1] = h.volume; d[2] = h.constraint; d[3] = h.change;
+      d[4] = static_cast<double>(h.primal_status); d[5] = static_cast<double>(h.adjoint_status);
+      d[6] = h.primal_cycles; d[7] = h.adjoint_cycles; d[8] = h.primal_factor;
+      d[9] = h.adjoint_factor; d[10] = h.primal_seconds; d[11] = h.adjoint_seconds;
+    }
+    *n_rec = static_cast<int>(r.history.size());
+    *theta = r.theta;
+    *converged = r.converged ? 1 : 0;
+    *seconds = r.seconds;
+  });
+}
+
 double ref_norm2(const double* x, long long n) {
   return kernels::norm2({x, static_cast<std::size_t>(n)});
 }

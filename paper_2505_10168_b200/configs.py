@@ -181,8 +181,10 @@ def cfg4(n_el=4096, n_t=16384) -> Config:
     chi = np.full(n_el, 0.5)
     mat = (1e-3, 1.0, 1.0, 1.0, 3.0, 2.0)
     k, c = simp(chi, mat)
+    # OptimisationOptions defaults (proj/include/stmg/optimisation.hpp:59-75): CR, 6 levels,
+    # nu = 20; strategy DesignIndependent as the paper's optimisation study
     return Config("cfg4", 1.0, 1.0, n_el, n_t, chi, mat, k, c, 3, (), "CR",
-                  PLAN_DESIGN_INDEPENDENT, n_levels=14, nu=1, tol=1e-8)
+                  PLAN_DESIGN_INDEPENDENT, n_levels=6, nu=20, tol=1e-8)
 
 
 def adjoint_uniform_rhs(n_el: int, n_t: int, L: float = 1.0, t_T: float = 1.0) -> np.ndarray:

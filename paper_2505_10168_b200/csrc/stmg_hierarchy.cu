@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -922,6 +923,269 @@ std::vector<HostLevel> make_host_levels(const stmg_grid* g, const double* k, con
   return host;
 }
 
+// Replace the host levels of an existing hierarchy whose level shapes are
+// unchanged (same grid and path, new materials) and refresh the device
+// coefficient and PCR tables in place; graphs are re-captured on next use
+// because w / 1/w are captured by value.
+void refresh_levels(stmg_hierarchy* h, std::vector<HostLevel> host) {
+  if (host.size() != h->host.size()) throw std::logic_error("refresh_levels: level count changed");
+  DeviceGuard dg(h->device);
+  cuda_check(cudaStreamSynchronize(h->stream), "sync");
+  h->host = std::move(host);
+  for (size_t l = 0; l < h->host.size(); ++l) {
+    const HostLevel& hl = h->host[l];
+    const std::vector<double> t = hl.table(h->adjoint);
+    if (static_cast<int64_t>(t.size()) != h->coef[l]->n) throw std::logic_error("refresh_levels: shape changed");
+    cuda_check(cudaMemcpy(h->coef[l]->p, t.data(), t.size() * 8, cudaMemcpyHostToDevice), "coef upload");
+    h->views[l].w = hl.w;
+    h->views[l].inv_w = hl.inv_w;
+  }
+  auto a = std::move(h->pcr_alpha);
+  auto g = std::move(h->pcr_gamma);
+  auto b = std::move(h->pcr_bfin);
+  build_pcr(h);  // fresh factor tables (old ones freed after the sync above)
+  for (auto& kv : h->graphs) {
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+    for (auto& t : kv.second.timed) {
+      cudaEventDestroy(t.start);
+      cudaEventDestroy(t.stop);
+    }
+  }
+  h->graphs.clear();
+}
+
+// MmaUpdater / mma_subsolve, restated from proj/src/mma.cpp:19-157 with the
+// same loop order (sequential sums), so the design update is the reference's.
+struct Mma {
+  double x_min, x_max, move, asym_init, shrink, grow;
+  size_t n;
+  int iter = 0;
+  std::vector<double> x_prev, x_prev2, low_, upp_;
+
+  std::vector<double> subsolve(const std::vector<double>& x, const std::vector<double>& df,
+                               const std::vector<double>& dg, double g, const std::vector<double>& lower,
+                               const std::vector<double>& upper, const std::vector<double>& alpha,
+                               const std::vector<double>& beta) const {
+    std::vector<double> p0(n), q0(n), p1(n), q1(n), y(n);
+    double r1 = g;
+    for (size_t j = 0; j < n; ++j) {
+      if (!(lower[j] < x[j] && x[j] < upper[j]))
+        throw std::invalid_argument("mma_subsolve: x outside the asymptotes");
+      const double du = upper[j] - x[j];
+      const double dl = x[j] - lower[j];
+      p0[j] = du * du * std::max(df[j], 0.0);
+      q0[j] = dl * dl * std::max(-df[j], 0.0);
+      p1[j] = du * du * std::max(dg[j], 0.0);
+      q1[j] = dl * dl * std::max(-dg[j], 0.0);
+      r1 -= p1[j] / du + q1[j] / dl;
+    }
+    auto x_of_eta = [&](double eta) {
+      for (size_t j = 0; j < n; ++j) {
+        const double p = p0[j] + eta * p1[j];
+        const double q = q0[j] + eta * q1[j];
+        double v;
+        if (p == 0.0 && q == 0.0) {
+          v = x[j];
+        } else {
+          const double sp = std::sqrt(p);
+          const double sq = std::sqrt(q);
+          v = (sp * lower[j] + sq * upper[j]) / (sp + sq);
+        }
+        y[j] = std::clamp(v, alpha[j], beta[j]);
+      }
+    };
+    auto g_hat = [&] {
+      double sacc = r1;
+      for (size_t j = 0; j < n; ++j) sacc += p1[j] / (upper[j] - y[j]) + q1[j] / (y[j] - lower[j]);
+      return sacc;
+    };
+    x_of_eta(0.0);
+    if (g_hat() <= 0.0) return y;
+    double eta_lo = 0.0, eta_hi = 1.0;
+    x_of_eta(eta_hi);
+    int guard = 0;
+    while (g_hat() > 0.0) {
+      eta_lo = eta_hi;
+      eta_hi *= 2.0;
+      x_of_eta(eta_hi);
+      if (++guard > 100)
+        throw std::runtime_error("mma_subsolve: constraint unreachable within the move limits");
+    }
+    for (int it = 0; it < 100; ++it) {
+      const double mid = 0.5 * (eta_lo + eta_hi);
+      x_of_eta(mid);
+      if (g_hat() > 0.0) eta_lo = mid;
+      else eta_hi = mid;
+    }
+    x_of_eta(eta_hi);
+    return y;
+  }
+
+  std::vector<double> update(const std::vector<double>& x, const std::vector<double>& df,
+                             const std::vector<double>& dg, double g) {
+    const double range = x_max - x_min;
+    ++iter;
+    std::vector<double> low(n), upp(n);
+    if (iter <= 2) {
+      for (size_t j = 0; j < n; ++j) {
+        low[j] = x[j] - asym_init * range;
+        upp[j] = x[j] + asym_init * range;
+      }
+    } else {
+      for (size_t j = 0; j < n; ++j) {
+        const double osc = (x[j] - x_prev[j]) * (x_prev[j] - x_prev2[j]);
+        const double gamma = osc < 0.0 ? shrink : osc > 0.0 ? grow : 1.0;
+        low[j] = x[j] - gamma * (x_prev[j] - low_[j]);
+        upp[j] = x[j] + gamma * (upp_[j] - x_prev[j]);
+        low[j] = std::clamp(low[j], x[j] - 10.0 * range, x[j] - 0.01 * range);
+        upp[j] = std::clamp(upp[j], x[j] + 0.01 * range, x[j] + 10.0 * range);
+      }
+    }
+    std::vector<double> alpha(n), beta(n);
+    for (size_t j = 0; j < n; ++j) {
+      alpha[j] = std::max({x_min, low[j] + 0.1 * (x[j] - low[j]), x[j] - move * range});
+      beta[j] = std::min({x_max, upp[j] - 0.1 * (upp[j] - x[j]), x[j] + move * range});
+    }
+    std::vector<double> x_new = subsolve(x, df, dg, g, low, upp, alpha, beta);
+    x_prev2 = iter >= 2 ? x_prev : x;
+    x_prev = x;
+    low_ = std::move(low);
+    upp_ = std::move(upp);
+    return x_new;
+  }
+};
+
+// optimise, proj/src/optimisation.cpp:83-186 (host loop; solves, objective and
+// sensitivities on the GPU)
+void optimise(const stmg_grid* geom, const stmg_optimise_options& o, int device, double* chi_out,
+              stmg_iteration_record* recs, int32_t* n_records, double* theta_out, int32_t* converged,
+              double* seconds) {
+  if (o.volume_limit <= 0.0 || o.volume_limit > 1.0)
+    throw std::invalid_argument("optimise: volume limit must be in (0, 1]");
+  if (o.max_iterations < 1 || o.stable_iterations < 1 || o.rel_change_tol <= 0.0 || o.theta_ref <= 0.0)
+    throw std::invalid_argument("optimise: invalid options");
+  if (!(o.mma_x_min < o.mma_x_max)) throw std::invalid_argument("MmaUpdater: empty box");
+  if (o.mma_move_limit <= 0.0 || o.mma_asym_init <= 0.0 || o.mma_asym_shrink <= 0.0 ||
+      o.mma_asym_shrink >= 1.0 || o.mma_asym_grow <= 1.0)
+    throw std::invalid_argument("MmaUpdater: invalid options");
+  const auto t0 = std::chrono::steady_clock::now();
+  const HostGrid g = make_grid(geom->L, geom->t_T, geom->n_el, geom->n_t);
+  const int64_t ne = g.n_el, nn = ne + 1, ndof = nn * (g.n_t + 1);
+  std::vector<double> chi(static_cast<size_t>(ne), o.chi_init), k(ne), c(ne);
+  std::vector<double> b(static_cast<size_t>(ndof));
+  load_vector_impl(g, [&](double x, double t) { return source_value(3, nullptr, x, t, g.L, g.t_T); },
+                   true, b.data());
+  const double scale = g.dt / o.theta_ref;
+  std::vector<double> cvec(b);
+  for (double& v : cvec) v *= scale;  // adjoint_rhs, optimisation.cpp:26-32
+  const std::vector<double> dg(static_cast<size_t>(ne), g.dx / (o.volume_limit * g.L));
+  Mma mma{o.mma_x_min, o.mma_x_max, o.mma_move_limit, o.mma_asym_init, o.mma_asym_shrink,
+          o.mma_asym_grow, static_cast<size_t>(ne)};
+  DeviceGuard dgd(device);
+  DeviceBuf d_b(ndof), d_c(ndof), d_u(ndof), d_lam(ndof), d_dk(ne), d_dc(ne), d_sens(ne), d_part(1184 * 2),
+      d_s(2);
+  cuda_check(cudaMemcpy(d_b.p, b.data(), ndof * 8, cudaMemcpyHostToDevice), "b upload");
+  cuda_check(cudaMemcpy(d_c.p, cvec.data(), ndof * 8, cudaMemcpyHostToDevice), "c upload");
+  cuda_check(cudaMemset(d_u.p, 0, ndof * 8), "memset");
+  cuda_check(cudaMemset(d_lam.p, 0, ndof * 8), "memset");
+  std::unique_ptr<stmg_hierarchy> h, ht;
+  std::vector<int32_t> cur_dirs;
+  const stmg_grid gc{g.L, g.t_T, g.n_el, g.n_t};
+  const stmg_plan_request preq{o.n_levels, o.lambda_crit, o.strategy, parse_method(o.method), o.min_elements};
+  std::vector<double> hist(static_cast<size_t>(std::max(o.solve.max_cycles, 0)) + 1);
+  double theta_prev = std::numeric_limits<double>::quiet_NaN();
+  int stable = 0;
+  *converged = 0;
+  *n_records = 0;
+  for (int it = 1; it <= o.max_iterations; ++it) {
+    simp(chi.data(), ne, o.mat, k.data(), c.data());
+    std::vector<int32_t> dirs(static_cast<size_t>(std::max(o.n_levels - 1, 0)));
+    plan(g, k.data(), c.data(), chi.data(), &o.mat, preq, dirs.data(), nullptr);
+    std::vector<HostLevel> host =
+        make_host_levels(&gc, k.data(), c.data(), chi.data(), &o.mat, o.method,
+                         static_cast<int32_t>(dirs.size()), dirs.data(), nullptr);
+    if (h && dirs == cur_dirs) {
+      refresh_levels(h.get(), host);
+      refresh_levels(ht.get(), std::move(host));
+    } else {
+      ht.reset();
+      h.reset();
+      auto nh = std::make_unique<stmg_hierarchy>();
+      nh->device = device;
+      nh->dirs = dirs;
+      nh->host = std::move(host);
+      finish_create(nh.get(), false, nullptr);
+      stmg_hierarchy* tp = nullptr;
+      const int rc = stmg_hierarchy_transposed(nh.get(), &tp);
+      if (rc != STMG_OK) throw std::runtime_error(g_error);
+      h = std::move(nh);
+      ht.reset(tp);
+      cur_dirs = dirs;
+    }
+    if (!o.warm_start) cuda_check(cudaMemset(d_u.p, 0, ndof * 8), "memset");
+    stmg_solve_report pr{}, ar{};
+    solve(h.get(), d_b.p, d_u.p, o.solve, &pr, hist.data(), static_cast<int32_t>(hist.size()));
+    // objective_value = dot(b, u) dt / theta_ref (optimisation.cpp:21-24)
+    int64_t np = 0;
+    launch_check(launch_dot(d_b.p, d_u.p, ndof, d_part.p, &np, h->stream), "dot");
+    launch_check(launch_finalize_sum(d_part.p, np, d_s.p, h->stream), "finalize");
+    double dotbu = 0.0;
+    cuda_check(cudaMemcpyAsync(&dotbu, d_s.p, 8, cudaMemcpyDeviceToHost, h->stream), "d2h");
+    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+    const double theta = dotbu * g.dt / o.theta_ref;
+    if (!o.warm_start) cuda_check(cudaMemset(d_lam.p, 0, ndof * 8), "memset");
+    solve(ht.get(), d_c.p, d_lam.p, o.solve, &ar, hist.data(), static_cast<int32_t>(hist.size()));
+    double vsum = 0.0;
+    for (double v : chi) vsum += v;
+    const double vol = vsum * g.dx / g.L;
+    const double g_val = vol / o.volume_limit - 1.0;
+    const double change = it == 1 ? std::numeric_limits<double>::infinity()
+                                  : std::abs(theta - theta_prev) / std::abs(theta);
+    stmg_iteration_record& r = recs[it - 1];
+    r.iteration = it;
+    r.theta = theta;
+    r.volume = vol;
+    r.constraint = g_val;
+    r.change = change;
+    r.primal_status = pr.status;
+    r.adjoint_status = ar.status;
+    r.primal_cycles = pr.cycles;
+    r.adjoint_cycles = ar.cycles;
+    r.primal_factor = pr.factor;
+    r.adjoint_factor = ar.factor;
+    r.primal_seconds = pr.seconds;
+    r.adjoint_seconds = ar.seconds;
+    *n_records = it;
+    *theta_out = theta;
+    theta_prev = theta;
+    stable = change < o.rel_change_tol ? stable + 1 : 0;
+    if (stable >= o.stable_iterations) {
+      *converged = 1;
+      break;
+    }
+    if (it == o.max_iterations) break;
+    // objective_sensitivities (optimisation.cpp:34-73) on the GPU
+    std::vector<double> dk(ne), dc(ne), sens(ne);
+    for (int64_t e = 0; e < ne; ++e) {
+      if (!(chi[e] >= 0.0 && chi[e] <= 1.0)) throw std::invalid_argument("volume fraction outside [0, 1]");
+      const double dkv = o.mat.p_k * (o.mat.k_con - o.mat.k_ins) * std::pow(chi[e], o.mat.p_k - 1.0);
+      const double dcv = o.mat.p_c * (o.mat.c_con - o.mat.c_ins) * std::pow(chi[e], o.mat.p_c - 1.0);
+      dk[e] = dkv / g.dx;
+      dc[e] = dcv * g.dx / 6;
+    }
+    cuda_check(cudaMemcpyAsync(d_dk.p, dk.data(), ne * 8, cudaMemcpyHostToDevice, h->stream), "h2d");
+    cuda_check(cudaMemcpyAsync(d_dc.p, dc.data(), ne * 8, cudaMemcpyHostToDevice, h->stream), "h2d");
+    launch_check(launch_sensitivities(ne, g.n_t, g.dt, d_dk.p, d_dc.p, d_u.p, d_lam.p, d_sens.p, h->stream),
+                 "sensitivities");
+    cuda_check(cudaMemcpyAsync(sens.data(), d_sens.p, ne * 8, cudaMemcpyDeviceToHost, h->stream), "d2h");
+    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+    chi = mma.update(chi, sens, dg, g_val);
+  }
+  std::memcpy(chi_out, chi.data(), sizeof(double) * static_cast<size_t>(ne));
+  *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
 }  // namespace
 }  // namespace stmgb
 
@@ -1199,6 +1463,16 @@ int stmg_norm2(stmg_hierarchy* h, const double* x, int64_t n, double* norm) {
 // were captured with.
 int stmg_debug_set_kernel_variant(int32_t v) {
   return guarded([&] { set_kernel_variant(v); });
+}
+
+int stmg_optimise(const stmg_grid* geom, const stmg_optimise_options* opts, int32_t device,
+                  double* chi_out, stmg_iteration_record* records, int32_t* n_records, double* theta,
+                  int32_t* converged, double* seconds) {
+  return guarded([&] {
+    if (!geom || !opts || !chi_out || !records || !n_records || !theta || !converged || !seconds)
+      throw std::invalid_argument("optimise: null argument");
+    optimise(geom, *opts, device, chi_out, records, n_records, theta, converged, seconds);
+  });
 }
 
 // ---- time-slab multi-GPU --------------------------------------------------------

@@ -73,6 +73,13 @@ int launch_finalize_sum(const double* partials, int64_t n, double* out, cudaStre
 // Sum of squares of x[0..n) into partials (fixed grid) then *out.
 int launch_sumsq(const double* x, int64_t n, double* partials, int64_t* n_partials, cudaStream_t s);
 int64_t sweep_partials_needed(const LevelView& L);
+// objective_sensitivities (proj/src/optimisation.cpp:34-73), one thread per element
+int launch_sensitivities(int64_t n_el, int64_t n_t, double dt, const double* dk_dx,
+                         const double* dc_dx6, const double* u, const double* lam, double* sens,
+                         cudaStream_t s);
+// sum x*y into fixed-grid partials (then launch_finalize_sum)
+int launch_dot(const double* x, const double* y, int64_t n, double* partials, int64_t* n_partials,
+               cudaStream_t s);
 int kernels_init();  // once per device
 // Kernel design selection for benchmarking (0 = production default).
 void set_kernel_variant(int v);

@@ -1157,6 +1157,35 @@ __global__ void __launch_bounds__(32) k_coarsest_warp(CoarsestView cv, const dou
   }
 }
 
+// Adjoint sensitivities of the heat-compliance objective
+// (objective_sensitivities, proj/src/optimisation.cpp:34-73): one thread per
+// element, time levels accumulated in the reference's order, masked DOFs read
+// as zero, so the result is the reference's bit for bit for the same u, lambda.
+__global__ void k_sensitivities(int64_t n_el, int64_t n_t, double dt, const double* __restrict__ dk_dx,
+                                const double* __restrict__ dc_dx6, const double* __restrict__ u,
+                                const double* __restrict__ lam, double* __restrict__ sens) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n_el) return;
+  const int64_t nn = n_el + 1;
+  const double kd = dk_dx[e], cd = dc_dx6[e];
+  auto at = [&](const double* v, int64_t n, int64_t i) -> double {
+    return (n == 0 || i == 0) ? 0.0 : v[n * nn + i];
+  };
+  double acc = 0.0;
+  for (int64_t n = 1; n <= n_t; ++n) {
+    const double u0 = at(u, n, e), u1 = at(u, n, e + 1);
+    const double l0 = at(lam, n, e), l1 = at(lam, n, e + 1);
+    acc = acc + (kd * (u0 - u1)) * (l0 - l1);
+    const double v0 = (u0 - at(u, n - 1, e)) / dt;
+    const double v1 = (u1 - at(u, n - 1, e + 1)) / dt;
+    acc = acc + cd * (l0 * (2.0 * v0 + v1) + l1 * (v0 + 2.0 * v1));
+  }
+  sens[e] = -acc;
+}
+
+__global__ void k_dot(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                      double* __restrict__ partials);
+
 __global__ void k_sumsq(const double* __restrict__ x, int64_t n, double* __restrict__ partials) {
   double acc = 0.0;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
@@ -1164,6 +1193,16 @@ __global__ void k_sumsq(const double* __restrict__ x, int64_t n, double* __restr
     const double v = x[idx];
     acc = acc + v * v;
   }
+  const double s = block_sum(acc);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+__global__ void k_dot(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                      double* __restrict__ partials) {
+  double acc = 0.0;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+       idx += (int64_t)gridDim.x * blockDim.x)
+    acc = acc + x[idx] * y[idx];
   const double s = block_sum(acc);
   if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
@@ -1412,6 +1451,20 @@ int kernels_init() {
 
 int launch_finalize_sum(const double* partials, int64_t n, double* out, cudaStream_t s) {
   k_finalize_sum<<<1, 1024, 0, s>>>(partials, n, out);
+  return check_launch();
+}
+
+int launch_sensitivities(int64_t n_el, int64_t n_t, double dt, const double* dk_dx,
+                         const double* dc_dx6, const double* u, const double* lam, double* sens,
+                         cudaStream_t s) {
+  k_sensitivities<<<(unsigned)((n_el + 127) / 128), 128, 0, s>>>(n_el, n_t, dt, dk_dx, dc_dx6, u, lam, sens);
+  return check_launch();
+}
+
+int launch_dot(const double* x, const double* y, int64_t n, double* partials, int64_t* n_partials,
+               cudaStream_t s) {
+  k_dot<<<kSumGrid, 256, 0, s>>>(x, y, n, partials);
+  if (n_partials) *n_partials = kSumGrid;
   return check_launch();
 }
 

@@ -75,6 +75,8 @@ def _load():
         "stmg_synchronize": [vp],
         "stmg_debug_set_kernel_variant": [i32],
         "stmg_dist_partition": [i32, vp, vp, i32, i64, C.POINTER(i32), vp],
+        "stmg_optimise": [vp, vp, i32, vp, vp, C.POINTER(i32), C.POINTER(f64), C.POINTER(i32),
+                          C.POINTER(f64)],
         "stmg_dist_nccl_unique_id": [vp, i32],
         "stmg_dist_create": [vp, vp, vp, vp, vp, C.c_char_p, i32, vp, i32, i32, i32, vp, i32, i64,
                              C.POINTER(vp)],
@@ -130,6 +132,24 @@ class _PlanReq(C.Structure):
 class _SolveOpts(C.Structure):
     _fields_ = [("nu", C.c_int32), ("omega", C.c_double), ("tol", C.c_double),
                 ("div_tol", C.c_double), ("max_cycles", C.c_int32)]
+
+
+class _OptOpts(C.Structure):
+    _fields_ = [("mat", _Mat), ("method", C.c_char * 4), ("strategy", C.c_int32), ("n_levels", C.c_int32),
+                ("lambda_crit", C.c_double), ("min_elements", C.c_int64), ("warm_start", C.c_int32),
+                ("volume_limit", C.c_double), ("theta_ref", C.c_double), ("chi_init", C.c_double),
+                ("max_iterations", C.c_int32), ("rel_change_tol", C.c_double),
+                ("stable_iterations", C.c_int32), ("solve", _SolveOpts), ("mma_x_min", C.c_double),
+                ("mma_x_max", C.c_double), ("mma_move_limit", C.c_double), ("mma_asym_init", C.c_double),
+                ("mma_asym_shrink", C.c_double), ("mma_asym_grow", C.c_double)]
+
+
+class _IterRec(C.Structure):
+    _fields_ = [("iteration", C.c_int32), ("theta", C.c_double), ("volume", C.c_double),
+                ("constraint", C.c_double), ("change", C.c_double), ("primal_status", C.c_int32),
+                ("adjoint_status", C.c_int32), ("primal_cycles", C.c_int32), ("adjoint_cycles", C.c_int32),
+                ("primal_factor", C.c_double), ("adjoint_factor", C.c_double),
+                ("primal_seconds", C.c_double), ("adjoint_seconds", C.c_double)]
 
 
 class _SolveRep(C.Structure):
@@ -547,6 +567,63 @@ def mg_solve(h: LevelHierarchy, b, u, opts: Optional[SolveOptions] = None) -> So
                        [float(v) for v in hist[: rep.n_history]], bool(rep.absolute_norms),
                        rep.seconds, rep.device_seconds, rep.smoother_dof_updates, rep.kernel_launches,
                        kt)
+
+
+# ---- topology optimisation (BASELINE config 4; proj/src/optimisation.cpp:83-186) -----
+@dataclass
+class OptimisationOptions:
+    """proj/include/stmg/optimisation.hpp:59-75 (+ MmaOptions, mma.hpp:23-30)."""
+    method: str = "CR"
+    strategy: PlanStrategy = PlanStrategy.Contrast
+    n_levels: int = 6
+    lambda_crit: float = 0.25
+    min_elements: int = 0
+    warm_start: bool = True
+    volume_limit: float = 0.5
+    theta_ref: float = 1e6
+    chi_init: float = 0.5
+    max_iterations: int = 500
+    rel_change_tol: float = 1e-3
+    stable_iterations: int = 5
+    solve: SolveOptions = field(default_factory=lambda: SolveOptions(nu=20))
+    mma_x_min: float = 0.0
+    mma_x_max: float = 1.0
+    mma_move_limit: float = 0.2
+    mma_asym_init: float = 0.5
+    mma_asym_shrink: float = 0.7
+    mma_asym_grow: float = 1.2
+
+
+@dataclass
+class OptimisationResult:
+    chi: np.ndarray
+    theta: float
+    converged: bool
+    iterations: int
+    history: list
+    seconds: float
+
+
+def optimise(geom: SpaceTimeGrid, mat, opts: Optional[OptimisationOptions] = None,
+             device: int = 0) -> OptimisationResult:
+    o = opts or OptimisationOptions()
+    so = o.solve
+    co = _OptOpts(MaterialPair.of(mat)._c(), o.method.encode(), int(o.strategy), int(o.n_levels),
+                  float(o.lambda_crit), int(o.min_elements), 1 if o.warm_start else 0,
+                  float(o.volume_limit), float(o.theta_ref), float(o.chi_init), int(o.max_iterations),
+                  float(o.rel_change_tol), int(o.stable_iterations),
+                  _SolveOpts(int(so.nu), float(so.omega), float(so.tol), float(so.div_tol), int(so.max_cycles)),
+                  o.mma_x_min, o.mma_x_max, o.mma_move_limit, o.mma_asym_init, o.mma_asym_shrink,
+                  o.mma_asym_grow)
+    chi = np.zeros(geom.n_el)
+    recs = (_IterRec * int(o.max_iterations))()
+    nr, conv = C.c_int32(), C.c_int32()
+    th, secs = C.c_double(), C.c_double()
+    gc = geom._c()
+    _check(_lib.stmg_optimise(C.byref(gc), C.byref(co), int(device), chi.ctypes.data, recs, C.byref(nr),
+                              C.byref(th), C.byref(conv), C.byref(secs)))
+    hist = [{f: getattr(recs[i], f) for f, _ in _IterRec._fields_} for i in range(nr.value)]
+    return OptimisationResult(chi, th.value, bool(conv.value), nr.value, hist, secs.value)
 
 
 # ---- time-slab multi-GPU (SURVEY.md §8(e)) ------------------------------------------

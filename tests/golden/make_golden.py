@@ -78,8 +78,19 @@ def cfg1_full(ref, port):
                 ref_seconds=secs, ref_build_seconds=h.build_seconds)
 
 
+OPT_SMALL = dict(L=1.0, tT=1.0, n_el=64, n_t=128, mat=(1e-3, 1.0, 1.0, 1.0, 3.0, 2.0), method="CR",
+                 strategy=3, n_levels=6, max_iterations=8, nu=5, tol=1e-8, stable_iterations=100)
+
+
+def opt_small(ref):
+    o = dict(OPT_SMALL)
+    r = ref.optimise(o.pop("L"), o.pop("tT"), o.pop("n_el"), o.pop("n_t"), o.pop("mat"), **o)
+    return dict(chi=r["chi"], records=r["records"], theta=r["theta"])
+
+
 def main():
     ref, port = Ref(), Port()
+    np.savez_compressed(os.path.join(HERE, "opt_small.npz"), **opt_small(ref))
     with open(os.path.join(HERE, "plans.json"), "w") as fh:
         json.dump(plans(ref), fh, indent=1)
     for name in GOLDEN_CASES:
