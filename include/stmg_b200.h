@@ -106,6 +106,8 @@ typedef struct stmg_solve_report {
   double fine_restrict_seconds;
   int64_t fine_prolong_sweeps; /* fused prolongation + first post-sweep launches */
   double fine_prolong_sweep_seconds;
+  int64_t fine_sweep_pairs;    /* fused two-sweep (temporally blocked) launches */
+  double fine_sweep_pair_seconds;
 } stmg_solve_report;
 
 typedef struct stmg_hierarchy stmg_hierarchy;
@@ -174,6 +176,11 @@ int stmg_hierarchy_set_stream(stmg_hierarchy* h, void* cuda_stream);
 /* Record CUDA events around the finest level's kernels inside the V-cycle graph
  * (on != 0); the timings appear in stmg_solve_report.  Off by default. */
 int stmg_hierarchy_set_profiling(stmg_hierarchy* h, int32_t on);
+/* Accumulated in-graph device time of one kernel kind on one level over all
+ * profiled solves (kind: 0 sweep, 1 residual+restriction, 2 prolongation+sweep,
+ * 3 fused two-sweep, 4 first sweep from zero, 5 coarsest exact solve). */
+int stmg_hierarchy_profile(const stmg_hierarchy* h, int32_t level, int32_t kind, int64_t* launches,
+                           double* seconds);
 /* Bytes of device memory the hierarchy holds. */
 int stmg_hierarchy_device_bytes(const stmg_hierarchy* h, int64_t* bytes);
 

@@ -591,8 +591,9 @@ void dist_solve(stmg_dist* d, const double* b, double* u, const stmg_solve_optio
   rep->cycles = 0;
   rep->factor = 1.0;
   rep->smoother_dof_updates = 0.0;
-  rep->fine_sweeps = rep->fine_restricts = rep->fine_prolong_sweeps = 0;
+  rep->fine_sweeps = rep->fine_restricts = rep->fine_prolong_sweeps = rep->fine_sweep_pairs = 0;
   rep->fine_sweep_seconds = rep->fine_restrict_seconds = rep->fine_prolong_sweep_seconds = 0.0;
+  rep->fine_sweep_pair_seconds = 0.0;
   // work of this process: its slab rows on distributed levels, the tail on the root
   double per_cycle = 0.0;
   for (const RankState& R : d->ranks)

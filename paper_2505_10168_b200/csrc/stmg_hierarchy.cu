@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -377,10 +378,19 @@ struct GraphKey {
   }
 };
 
-enum TimedKind { kTimedSweep = 0, kTimedRestrict = 1, kTimedProlongSweep = 2 };
+enum TimedKind {
+  kTimedSweep = 0,
+  kTimedRestrict = 1,
+  kTimedProlongSweep = 2,
+  kTimedSweep2 = 3,
+  kTimedFromZero = 4,
+  kTimedCoarsest = 5,
+  kTimedKinds = 6
+};
 
 struct TimedKernel {
   int kind;
+  int level;
   cudaEvent_t start, stop;
 };
 
@@ -404,12 +414,14 @@ struct stmg_hierarchy {
   std::vector<std::unique_ptr<stmgb::DeviceBuf>> coef;  // per level
   std::vector<stmgb::LevelView> views;
   stmgb::CoarsestView coarsest{};
-  std::unique_ptr<stmgb::DeviceBuf> pcr_alpha, pcr_gamma, pcr_bfin;
+  std::unique_ptr<stmgb::DeviceBuf> pcr_alpha, pcr_gamma, pcr_bfin, prop_tinv, prop_a, prop_chunk;
   std::shared_ptr<stmgb::Workspace> ws;
   cudaStream_t stream = nullptr;      // where work runs (own_stream or a caller's)
   cudaStream_t own_stream = nullptr;  // created with the hierarchy
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture
   bool profiling = false;
+  // per (level, kind): launches and device seconds accumulated while profiling
+  std::vector<std::array<std::pair<int64_t, double>, stmgb::kTimedKinds>> prof;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::map<stmgb::GraphKey, stmgb::GraphEntry> graphs;
   int64_t device_bytes = 0;
@@ -435,6 +447,9 @@ struct stmg_hierarchy {
     pcr_alpha.reset();
     pcr_gamma.reset();
     pcr_bfin.reset();
+    prop_tinv.reset();
+    prop_a.reset();
+    prop_chunk.reset();
     ws.reset();
     cudaSetDevice(prev);
   }
@@ -501,6 +516,84 @@ void build_pcr(stmg_hierarchy* h) {
   cuda_check(cudaMemcpy(h->pcr_alpha->p, alpha.data(), alpha.size() * 8, cudaMemcpyHostToDevice), "pcr");
   cuda_check(cudaMemcpy(h->pcr_gamma->p, gamma.data(), gamma.size() * 8, cudaMemcpyHostToDevice), "pcr");
   if (m > 0) cuda_check(cudaMemcpy(h->pcr_bfin->p, b.data(), b.size() * 8, cudaMemcpyHostToDevice), "pcr");
+  // n_el <= 32: T^-1 (Thomas on unit vectors) and A = -T^-1 S, 32 x 32 padded
+  h->coarsest.tinv = nullptr;
+  h->coarsest.prop = nullptr;
+  h->coarsest.prop_chunk = nullptr;
+  h->coarsest.n_chunks = 0;
+  h->coarsest.chunk_len = 0;
+  if (m >= 1 && m <= 32) {
+    std::vector<double> Ti(32 * 32, 0.0), A(32 * 32, 0.0), S(32 * 32, 0.0);
+    std::vector<double> sub(m), dia(m), sup(m), cpv(m), col(m);
+    for (int j = 0; j < m; ++j) {
+      const int64_t i = j + 1;
+      sub[j] = i >= 2 ? t[kCm * nn + i] : 0.0;
+      dia[j] = t[kC0 * nn + i];
+      sup[j] = i <= m - 1 ? t[kCp * nn + i] : 0.0;
+      if (i >= 2) S[j * 32 + (j - 1)] = t[kOm * nn + i];
+      S[j * 32 + j] = t[kO0 * nn + i];
+      if (i <= m - 1) S[j * 32 + (j + 1)] = t[kOp * nn + i];
+    }
+    for (int e = 0; e < m; ++e) {  // column e of T^-1
+      std::vector<double> rhs(m, 0.0);
+      rhs[e] = 1.0;
+      double piv = dia[0];
+      cpv[0] = sup[0] / piv;
+      col[0] = rhs[0] / piv;
+      for (int j = 1; j < m; ++j) {
+        piv = dia[j] - sub[j] * cpv[j - 1];
+        cpv[j] = sup[j] / piv;
+        col[j] = (rhs[j] - sub[j] * col[j - 1]) / piv;
+      }
+      for (int j = m - 2; j >= 0; --j) col[j] -= cpv[j] * col[j + 1];
+      for (int j = 0; j < m; ++j) Ti[j * 32 + e] = col[j];
+    }
+    for (int j = 0; j < m; ++j)
+      for (int k = 0; k < m; ++k) {
+        double acc = 0.0;
+        for (int q = 0; q < m; ++q) acc += Ti[j * 32 + q] * S[q * 32 + k];
+        A[j * 32 + k] = -acc;
+      }
+    h->prop_tinv = std::make_unique<DeviceBuf>(32 * 32);
+    h->prop_a = std::make_unique<DeviceBuf>(32 * 32);
+    cuda_check(cudaMemcpy(h->prop_tinv->p, Ti.data(), Ti.size() * 8, cudaMemcpyHostToDevice), "tinv");
+    cuda_check(cudaMemcpy(h->prop_a->p, A.data(), A.size() * 8, cudaMemcpyHostToDevice), "prop");
+    h->coarsest.tinv = h->prop_tinv->p;
+    h->coarsest.prop = h->prop_a->p;
+    h->device_bytes += 2 * 32 * 32 * 8;
+    // chunked march: C = largest power of two <= 16 dividing n_t with chunks >= 4 steps
+    const int64_t nt = hl.g.n_t;
+    int C = 16;
+    while (C > 1 && (nt % C != 0 || nt / C < 4)) C /= 2;
+    if (C > 1) {
+      const int64_t Lc = nt / C;
+      std::vector<double> P(A), T2(32 * 32);  // P = A^Lc by binary powering
+      std::vector<double> R(32 * 32, 0.0);
+      for (int j = 0; j < 32; ++j) R[j * 32 + j] = 1.0;
+      auto mul = [](const std::vector<double>& X, const std::vector<double>& Y, std::vector<double>& Z) {
+        for (int j = 0; j < 32; ++j)
+          for (int k = 0; k < 32; ++k) {
+            double acc = 0.0;
+            for (int q = 0; q < 32; ++q) acc += X[j * 32 + q] * Y[q * 32 + k];
+            Z[j * 32 + k] = acc;
+          }
+      };
+      for (int64_t e = Lc; e > 0; e >>= 1) {
+        if (e & 1) {
+          mul(R, P, T2);
+          R = T2;
+        }
+        mul(P, P, T2);
+        P = T2;
+      }
+      h->prop_chunk = std::make_unique<DeviceBuf>(32 * 32);
+      cuda_check(cudaMemcpy(h->prop_chunk->p, R.data(), R.size() * 8, cudaMemcpyHostToDevice), "prop^L");
+      h->coarsest.prop_chunk = h->prop_chunk->p;
+      h->coarsest.n_chunks = C;
+      h->coarsest.chunk_len = static_cast<int32_t>(Lc);
+      h->device_bytes += 32 * 32 * 8;
+    }
+  }
   h->coarsest.lv = h->views.back();
   h->coarsest.m = m;
   h->coarsest.n_steps = steps;
@@ -549,8 +642,10 @@ std::shared_ptr<Workspace> make_workspace(const stmg_hierarchy* h, int64_t* byte
   ws->partials = std::make_unique<DeviceBuf>(max_partials);
   ws->scalars = std::make_unique<DeviceBuf>(8);
   const int m = h->coarsest.m;
-  ws->coarse_scratch = std::make_unique<DeviceBuf>(std::max<int64_t>(2 * static_cast<int64_t>(m), 2));
-  *bytes += 8 * (max_partials + 8 + 2 * m);
+  const int64_t scratch = std::max<int64_t>(
+      {2 * static_cast<int64_t>(m), 32 * h->host.back().g.n_t, 2});
+  ws->coarse_scratch = std::make_unique<DeviceBuf>(scratch);
+  *bytes += 8 * (max_partials + 8 + scratch);
   cuda_check(cudaMallocHost(&ws->pinned, 8 * sizeof(double)), "cudaMallocHost");
   return ws;
 }
@@ -590,8 +685,8 @@ struct Emitter {
 
   template <class F>
   void timed_launch(int l, int kind, F&& launch) {
-    if (timed && l == 0) {
-      TimedKernel t{kind, nullptr, nullptr};
+    if (timed) {
+      TimedKernel t{kind, l, nullptr, nullptr};
       cuda_check(cudaEventCreate(&t.start), "cudaEventCreate");
       cuda_check(cudaEventCreate(&t.stop), "cudaEventCreate");
       cuda_check(cudaEventRecordWithFlags(t.start, s, cudaEventRecordExternal), "event record");
@@ -607,33 +702,18 @@ struct Emitter {
     return which == 0 ? h->ws->xa[l]->p : h->ws->xb[l]->p;
   }
 
-  // Returns the buffer index (0 = xa, 1 = xb) holding the level's result.
-  // start: buffer holding the current iterate; pre_done: sweeps already done;
-  // from_zero: the iterate is identically zero (coarse levels).
-  int level(int l, int start, int pre_done, bool from_zero) {
-    const int nl = h->n_levels();
+  // `count` damped-Jacobi sweeps from buffer `cur`: fused pairs (one pass over
+  // memory per two sweeps), then a single sweep if count is odd.
+  void smooth(int l, const double* f, int& cur, int count) {
     const LevelView& L = h->views[l];
-    double* f = h->ws->f[l]->p;
-    if (l == nl - 1) {
-      launch_check(launch_coarsest(h->adjoint, h->coarsest, f, buf(l, 0), h->ws->coarse_scratch->p, s),
-                   "coarsest");
+    for (; count >= 2; count -= 2) {
+      timed_launch(l, kTimedSweep2, [&] {
+        launch_check(launch_sweep2(h->adjoint, L, f, buf(l, cur), buf(l, 1 - cur), omega, s), "sweep2");
+      });
       ++kernels;
-      return 0;
+      cur = 1 - cur;
     }
-    int cur = start;
-    int pre = nu - pre_done;
-    if (from_zero) {
-      cur = 0;
-      if (nu >= 1) {
-        launch_check(launch_sweep_from_zero(L, f, buf(l, 0), omega, s), "sweep0");
-        ++kernels;
-        pre = nu - 1;
-      } else {
-        cuda_check(cudaMemsetAsync(buf(l, 0), 0, sizeof(double) * h->ndofs(l), s), "memset");
-        pre = 0;
-      }
-    }
-    for (int k = 0; k < pre; ++k) {
+    if (count == 1) {
       timed_launch(l, kTimedSweep, [&] {
         launch_check(launch_sweep(h->adjoint, L, f, buf(l, cur), buf(l, 1 - cur), omega, nullptr,
                                   nullptr, s),
@@ -642,6 +722,39 @@ struct Emitter {
       ++kernels;
       cur = 1 - cur;
     }
+  }
+
+  // Returns the buffer index (0 = xa, 1 = xb) holding the level's result.
+  // start: buffer holding the current iterate; pre_done: sweeps already done;
+  // from_zero: the iterate is identically zero (coarse levels).
+  int level(int l, int start, int pre_done, bool from_zero) {
+    const int nl = h->n_levels();
+    const LevelView& L = h->views[l];
+    double* f = h->ws->f[l]->p;
+    if (l == nl - 1) {
+      timed_launch(l, kTimedCoarsest, [&] {
+        launch_check(launch_coarsest(h->adjoint, h->coarsest, f, buf(l, 0), h->ws->coarse_scratch->p, s),
+                     "coarsest");
+      });
+      ++kernels;
+      return 0;
+    }
+    int cur = start;
+    int pre = nu - pre_done;
+    if (from_zero) {
+      cur = 0;
+      if (nu >= 1) {
+        timed_launch(l, kTimedFromZero, [&] {
+          launch_check(launch_sweep_from_zero(L, f, buf(l, 0), omega, s), "sweep0");
+        });
+        ++kernels;
+        pre = nu - 1;
+      } else {
+        cuda_check(cudaMemsetAsync(buf(l, 0), 0, sizeof(double) * h->ndofs(l), s), "memset");
+        pre = 0;
+      }
+    }
+    smooth(l, f, cur, pre);
     const LevelView& C = h->views[l + 1];
     timed_launch(l, kTimedRestrict, [&] {
       launch_check(launch_restrict_residual(h->adjoint, L, C, h->dirs[l], f, buf(l, cur),
@@ -665,15 +778,7 @@ struct Emitter {
       launch_check(launch_prolong_add(L, C, h->dirs[l], xc, buf(l, cur), s), "prolong");
       ++kernels;
     }
-    for (int k = 0; k < post; ++k) {
-      timed_launch(l, kTimedSweep, [&] {
-        launch_check(launch_sweep(h->adjoint, L, f, buf(l, cur), buf(l, 1 - cur), omega, nullptr,
-                                  nullptr, s),
-                     "sweep");
-      });
-      ++kernels;
-      cur = 1 - cur;
-    }
+    smooth(l, f, cur, post);
     return cur;
   }
 };
@@ -767,8 +872,9 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
   rep->cycles = 0;
   rep->factor = 1.0;
   rep->smoother_dof_updates = 0.0;
-  rep->fine_sweeps = rep->fine_restricts = rep->fine_prolong_sweeps = 0;
+  rep->fine_sweeps = rep->fine_restricts = rep->fine_prolong_sweeps = rep->fine_sweep_pairs = 0;
   rep->fine_sweep_seconds = rep->fine_restrict_seconds = rep->fine_prolong_sweep_seconds = 0.0;
+  rep->fine_sweep_pair_seconds = 0.0;
   double per_cycle_updates = 0.0;
   for (int l = 0; l + 1 < h->n_levels(); ++l) per_cycle_updates += 2.0 * o.nu * static_cast<double>(h->ndofs(l));
   if (r0 < o.tol) {
@@ -785,13 +891,20 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
       for (const TimedKernel& t : g->timed) {
         float ms = 0.f;
         cuda_check(cudaEventElapsedTime(&ms, t.start, t.stop), "event elapsed");
+        if (h->prof.size() < h->host.size()) h->prof.resize(h->host.size());
+        h->prof[t.level][t.kind].first += 1;
+        h->prof[t.level][t.kind].second += ms * 1e-3;
+        if (t.level != 0) continue;
         if (t.kind == kTimedSweep) {
           rep->fine_sweeps += 1;
           rep->fine_sweep_seconds += ms * 1e-3;
+        } else if (t.kind == kTimedSweep2) {
+          rep->fine_sweep_pairs += 1;
+          rep->fine_sweep_pair_seconds += ms * 1e-3;
         } else if (t.kind == kTimedRestrict) {
           rep->fine_restricts += 1;
           rep->fine_restrict_seconds += ms * 1e-3;
-        } else {
+        } else if (t.kind == kTimedProlongSweep) {
           rep->fine_prolong_sweeps += 1;
           rep->fine_prolong_sweep_seconds += ms * 1e-3;
         }
@@ -1336,6 +1449,21 @@ int stmg_hierarchy_set_profiling(stmg_hierarchy* h, int32_t on) {
   });
 }
 
+int stmg_hierarchy_profile(const stmg_hierarchy* h, int32_t level, int32_t kind, int64_t* launches,
+                           double* seconds) {
+  return guarded([&] {
+    if (!h || !launches || !seconds) throw std::invalid_argument("null argument");
+    check_level(h, level);
+    if (kind < 0 || kind >= kTimedKinds) throw std::out_of_range("profile kind");
+    *launches = 0;
+    *seconds = 0.0;
+    if (static_cast<size_t>(level) < h->prof.size()) {
+      *launches = h->prof[level][kind].first;
+      *seconds = h->prof[level][kind].second;
+    }
+  });
+}
+
 int stmg_hierarchy_device_bytes(const stmg_hierarchy* h, int64_t* bytes) {
   return guarded([&] {
     if (!h || !bytes) throw std::invalid_argument("null argument");
@@ -1366,7 +1494,12 @@ int stmg_level_sweeps(stmg_hierarchy* h, int32_t l, const double* f, double* x, 
     }
     double* a = x;
     double* b = tmp;
-    for (int s = 0; s < sweeps; ++s) {
+    int left = sweeps;
+    for (; left >= 2; left -= 2) {
+      launch_check(launch_sweep2(h->adjoint, h->views[l], f, a, b, omega, h->stream), "sweep2");
+      std::swap(a, b);
+    }
+    if (left == 1) {
       launch_check(launch_sweep(h->adjoint, h->views[l], f, a, b, omega, nullptr, nullptr, h->stream), "sweep");
       std::swap(a, b);
     }

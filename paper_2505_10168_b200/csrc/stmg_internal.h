@@ -41,6 +41,14 @@ struct CoarsestView {
   const double* alpha;  // n_steps * m
   const double* gamma;  // n_steps * m
   const double* bfin;   // m, final diagonal after reduction
+  // n_el <= 32: dense step inverse T^-1 and propagator A = -T^-1 S (32 x 32,
+  // row-major, zero-padded), for the parallel-RHS + propagator march
+  const double* tinv;
+  const double* prop;
+  // chunked (parallel-in-time) march: n_t = n_chunks * chunk_len, A^chunk_len
+  int32_t n_chunks;
+  int32_t chunk_len;
+  const double* prop_chunk;
 };
 
 // ---- kernel launchers (stmg_kernels.cu); all asynchronous on `s` ------------------
@@ -49,6 +57,10 @@ struct CoarsestView {
 // nullptr only the residual norm partials are produced.
 int launch_sweep(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
                  double omega, double* partials, int64_t* n_partials, cudaStream_t s);
+// Two sweeps y = S(S(x)) in one pass (temporal blocking); bit-identical to two
+// launch_sweep calls.  y must not alias x.
+int launch_sweep2(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
+                  double omega, cudaStream_t s);
 // First sweep from a zero iterate: y = 0 + omega * (f * inv_diag), bitwise equal
 // to the general sweep applied to x = +0.
 int launch_sweep_from_zero(const LevelView& L, const double* f, double* y, double omega,

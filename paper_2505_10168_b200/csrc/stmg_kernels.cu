@@ -120,6 +120,26 @@ __device__ __forceinline__ double row_sum(const LevelView& L, int64_t n, int64_t
   return a.result();
 }
 
+// Interior row (all six entries present): the fixed canonical lane order.
+// x*: same-time values at i-1, i, i+1; y*: coupled-level values.
+template <bool ADJ>
+__device__ __forceinline__ double row_interior(const Coefs& c, double xm, double x0, double xp,
+                                               double ym, double y0, double yp) {
+  double s0, s1, s2, s3;
+  if (!ADJ) {
+    s0 = (0.0 + c.om * ym) + c.c0 * x0;
+    s1 = (0.0 + c.o0 * y0) + c.cp * xp;
+    s2 = 0.0 + c.op * yp;
+    s3 = 0.0 + c.cm * xm;
+  } else {
+    s0 = (0.0 + c.cm * xm) + c.o0 * y0;
+    s1 = (0.0 + c.c0 * x0) + c.op * yp;
+    s2 = 0.0 + c.cp * xp;
+    s3 = 0.0 + c.om * ym;
+  }
+  return (s0 + s1) + (s2 + s3);
+}
+
 // P x_c at fine DOF (n, i) (csr_spmv_add row, proj/src/transfer.cpp:74-88).
 template <int DIR>
 __device__ __forceinline__ double prolong_row(const double* __restrict__ xc, int64_t nnc, int64_t n,
@@ -405,6 +425,142 @@ __global__ void __launch_bounds__(kMaxTW, MINB) k_lean2(LevelView L, Ld ld,
   if (NORM) {
     const double s = block_sum(acc);
     if (threadIdx.x == 0) partials[bid] = s;
+  }
+}
+
+// Two damped-Jacobi sweeps fused into one pass over memory (temporal
+// blocking), bit-identical to two separate sweeps.  Warps overlap by two
+// nodes on each side: lanes 1..30 evaluate sweep 1, lanes 2..29 evaluate and
+// store sweep 2 (28 nodes per warp).  Sweep 1 is also evaluated on the one
+// staged row before the tile (J) / after it (J^T) that sweep 2 couples to.
+// Staged: x on NT + 2 levels, f on NT + 1 levels.  Node-fastest 1-D grid.
+template <bool ADJ, int NT>
+__global__ void __launch_bounds__(kMaxTW, 3) k_lean2x2(LevelView L, const double* __restrict__ f,
+                                                       const double* __restrict__ x,
+                                                       double* __restrict__ y, double omega,
+                                                       int64_t node_tiles) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nn = L.nn, nt = L.n_t;
+  const int64_t bid = blockIdx.x;
+  const int64_t tile = bid % node_tiles, ttile = bid / node_tiles;
+  const int64_t per_block = (int64_t)(blockDim.x >> 5) * 28;
+  const int64_t i = tile * per_block + warp * 28 + lane - 2;  // node of this lane
+  const int64_t n0 = L.n_lo + ttile * NT;
+  // staged rows: J: n0-2 .. n0+NT-1 ; J^T: n0 .. n0+NT+1  (NT + 2 levels)
+  const int64_t sbase = ADJ ? n0 : n0 - 2;
+  // sweep-1 rows: J: n0-1 .. n0+NT-1 ; J^T: n0 .. n0+NT   (NT + 1 rows)
+  const int64_t s1base = ADJ ? n0 : n0 - 1;
+  const bool in_grid = i >= 0 && i < nn;
+  const bool lane1 = lane >= 1 && lane <= 30 && in_grid;
+  const bool lane2 = lane >= 2 && lane <= 29 && in_grid;
+  double xs[NT + 2], fv[NT + 1];
+#pragma unroll
+  for (int r = 0; r < NT + 2; ++r) {
+    const int64_t n = sbase + r;
+    xs[r] = (n >= 0 && n <= nt && in_grid) ? x[n * nn + i] : 0.0;
+  }
+#pragma unroll
+  for (int r = 0; r < NT + 1; ++r) {
+    const int64_t n = s1base + r;
+    fv[r] = (n >= 0 && n <= nt && lane1) ? f[n * nn + i] : 0.0;
+  }
+  Coefs c{};
+  if (lane1) c = load_coefs(L, i);
+  // interior tile: every sweep-1 and sweep-2 row has its coupled level and is
+  // unmasked, every sweep-1 node (lanes 1..30) has both neighbours
+  const int64_t node1 = tile * per_block + warp * 28 - 1;  // node of lane 1
+  const bool rows_in = (ADJ ? (n0 >= 1 && n0 + NT <= nt - 1) : (n0 >= 3 && n0 + NT - 1 <= nt)) &&
+                       n0 + NT - 1 < L.n_hi;
+  const bool nodes_in = node1 >= 2 && node1 + 29 <= L.n_el - 1;
+  double y1[NT + 1];
+  if (rows_in && nodes_in) {
+    double pm = __shfl_up_sync(kFull, xs[0], 1), pp = __shfl_down_sync(kFull, xs[0], 1);
+#pragma unroll
+    for (int r = 0; r <= NT; ++r) {
+      const double x1 = xs[r + 1];
+      const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
+      if (ADJ) y1[r] = xs[r] + omega * ((fv[r] - row_interior<true>(c, pm, xs[r], pp, qm, x1, qp)) * c.invd);
+      else y1[r] = x1 + omega * ((fv[r] - row_interior<false>(c, qm, x1, qp, pm, xs[r], pp)) * c.invd);
+      pm = qm;
+      pp = qp;
+    }
+    double am = __shfl_up_sync(kFull, y1[0], 1), ap = __shfl_down_sync(kFull, y1[0], 1);
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const double z1 = y1[k + 1];
+      const double bm = __shfl_up_sync(kFull, z1, 1), bp = __shfl_down_sync(kFull, z1, 1);
+      const int64_t n = n0 + k;
+      if (lane2) {
+        if (ADJ)
+          y[n * nn + i] = y1[k] + omega * ((fv[k] - row_interior<true>(c, am, y1[k], ap, bm, z1, bp)) * c.invd);
+        else
+          y[n * nn + i] = z1 + omega * ((fv[k + 1] - row_interior<false>(c, bm, z1, bp, am, y1[k], ap)) * c.invd);
+      }
+      am = bm;
+      ap = bp;
+    }
+    return;
+  }
+  // ---- general path: sweep 1 on NT + 1 rows -> y1[r] (row s1base + r)
+  double pm = __shfl_up_sync(kFull, xs[0], 1), pp = __shfl_down_sync(kFull, xs[0], 1);
+  if (ADJ) {
+    // row m uses staged (m, m+1): iterate r = 0..NT, row level xs[r], coupled xs[r+1]
+#pragma unroll
+    for (int r = 0; r <= NT; ++r) {
+      const double x1 = xs[r + 1];
+      const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
+      const int64_t n = s1base + r;
+      double v = 0.0;
+      if (lane1 && n <= nt) {
+        const double row = row_sum<true>(L, n, i, c, pm, xs[r], pp, qm, x1, qp);
+        const double id = (n == 0 || i == 0) ? L.inv_w : c.invd;
+        v = xs[r] + omega * ((fv[r] - row) * id);
+      }
+      y1[r] = v;
+      pm = qm;
+      pp = qp;
+    }
+  } else {
+    // row m uses staged (m-1, m): iterate r = 0..NT, row level xs[r+1], coupled xs[r]
+#pragma unroll
+    for (int r = 0; r <= NT; ++r) {
+      const double x1 = xs[r + 1];
+      const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
+      const int64_t n = s1base + r;
+      double v = 0.0;
+      if (lane1 && n >= 0 && n <= nt) {
+        const double row = row_sum<false>(L, n, i, c, qm, x1, qp, pm, xs[r], pp);
+        const double id = (n == 0 || i == 0) ? L.inv_w : c.invd;
+        v = x1 + omega * ((fv[r] - row) * id);
+      }
+      y1[r] = v;
+      pm = qm;
+      pp = qp;
+    }
+  }
+  // ---- sweep 2 on rows n0 .. n0+NT-1 from y1
+  double am = __shfl_up_sync(kFull, y1[0], 1), ap = __shfl_down_sync(kFull, y1[0], 1);
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    const double z1 = y1[k + 1];
+    const double bm = __shfl_up_sync(kFull, z1, 1), bp = __shfl_down_sync(kFull, z1, 1);
+    const int64_t n = n0 + k;
+    if (lane2 && n < L.n_hi) {
+      double row, x0, fval;
+      if (ADJ) {  // row n = y1[k] level, coupled y1[k+1]
+        row = row_sum<true>(L, n, i, c, am, y1[k], ap, bm, z1, bp);
+        x0 = y1[k];
+        fval = fv[k];
+      } else {  // row n = y1[k+1] level, coupled y1[k]
+        row = row_sum<false>(L, n, i, c, bm, z1, bp, am, y1[k], ap);
+        x0 = z1;
+        fval = fv[k + 1];
+      }
+      const double id = (n == 0 || i == 0) ? L.inv_w : c.invd;
+      y[n * nn + i] = x0 + omega * ((fval - row) * id);
+    }
+    am = bm;
+    ap = bp;
   }
 }
 
@@ -1186,6 +1342,154 @@ __global__ void k_sensitivities(int64_t n_el, int64_t n_t, double dt, const doub
 __global__ void k_dot(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                       double* __restrict__ partials);
 
+// Exact coarsest solve for n_el <= 32 in two phases.  (1) Every warp of the
+// block computes g_n = T^-1 f_n for its share of the time levels (T^-1 rows in
+// registers, f broadcast by shuffles) into scratch.  (2) Warp 0 runs the
+// causal recurrence x_n = g_n + A x_{n-1} (J; for J^T the anti-causal one
+// with the next level), A = -T^-1 S, one 32 x 32 register mat-vec per step.
+// Masked rows x = f / w as in k_coarsest.  Mathematically the block march of
+// k_coarsest; agrees with it (and the oracle's Thomas march) to rounding.
+template <bool ADJ>
+__global__ void __launch_bounds__(256) k_coarsest_prop(CoarsestView cv, const double* __restrict__ f,
+                                                       double* __restrict__ x,
+                                                       double* __restrict__ gglobal, int use_smem) {
+  extern __shared__ double gsm[];
+  double* g = use_smem ? gsm : gglobal;
+  const LevelView& L = cv.lv;
+  const int m = cv.m;
+  const int64_t nn = L.nn, nt = L.n_t;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t k = threadIdx.x; k < nn; k += blockDim.x) x[k] = f[k] / L.w;
+  for (int64_t n = 1 + threadIdx.x; n <= nt; n += blockDim.x) x[n * nn] = f[n * nn] / L.w;
+  const bool active = lane < m;
+  {
+    double row[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) row[k] = cv.tinv[lane * 32 + k];
+    for (int64_t n = 1 + warp; n <= nt; n += nw) {
+      const double fl = active ? f[n * nn + lane + 1] : 0.0;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+      for (int k = 0; k < 32; k += 4) {
+        a0 = a0 + row[k] * __shfl_sync(kFull, fl, k);
+        a1 = a1 + row[k + 1] * __shfl_sync(kFull, fl, k + 1);
+        a2 = a2 + row[k + 2] * __shfl_sync(kFull, fl, k + 2);
+        a3 = a3 + row[k + 3] * __shfl_sync(kFull, fl, k + 3);
+      }
+      g[(n - 1) * 32 + lane] = (a0 + a1) + (a2 + a3);
+    }
+  }
+  __syncthreads();
+  if (warp != 0) return;
+  double arow[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) arow[k] = cv.prop[lane * 32 + k];
+  double xprev = 0.0;
+  double gq = g[((ADJ ? nt : 1) - 1) * 32 + lane];
+  for (int64_t s = 1; s <= nt; ++s) {
+    const int64_t n = ADJ ? nt + 1 - s : s;
+    const double gn = gq;
+    if (s < nt) gq = g[((ADJ ? n - 1 : n + 1) - 1) * 32 + lane];
+    double a0 = gn, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (s > 1) {  // the first level's coupled level is masked (J) / absent (J^T)
+#pragma unroll
+      for (int k = 0; k < 32; k += 4) {
+        a0 = a0 + arow[k] * __shfl_sync(kFull, xprev, k);
+        a1 = a1 + arow[k + 1] * __shfl_sync(kFull, xprev, k + 1);
+        a2 = a2 + arow[k + 2] * __shfl_sync(kFull, xprev, k + 2);
+        a3 = a3 + arow[k + 3] * __shfl_sync(kFull, xprev, k + 3);
+      }
+    }
+    const double xv = (a0 + a1) + (a2 + a3);
+    if (active) x[n * nn + lane + 1] = xv;
+    xprev = active ? xv : 0.0;
+  }
+}
+
+// Parallel-in-time exact coarsest solve (n_el <= 32).  The block march
+// x_n = g_n + A x_{n-1} (g_n = T^-1 f_n, A = -T^-1 S; J^T: reversed in time)
+// is linear, so the n_t steps are cut into C chunks of length Lc:
+//   (1) all warps: g_n for every level (parallel);
+//   (2) warp c: chunk c from a zero start -> its end state e_c;
+//   (3) warp 0: chunk start states s_{c+1} = e_c + A^Lc s_c (C steps);
+//   (4) warp c: chunk c again from s_c, writing x.
+// Sequential depth 2 Lc + C instead of n_t.  Same solution up to rounding.
+__device__ __forceinline__ double matvec32(const double (&row)[32], double v) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+  for (int k = 0; k < 32; k += 4) {
+    a0 = a0 + row[k] * __shfl_sync(kFull, v, k);
+    a1 = a1 + row[k + 1] * __shfl_sync(kFull, v, k + 1);
+    a2 = a2 + row[k + 2] * __shfl_sync(kFull, v, k + 2);
+    a3 = a3 + row[k + 3] * __shfl_sync(kFull, v, k + 3);
+  }
+  return (a0 + a1) + (a2 + a3);
+}
+
+template <bool ADJ>
+__global__ void __launch_bounds__(512) k_coarsest_chunked(CoarsestView cv, const double* __restrict__ f,
+                                                          double* __restrict__ x) {
+  extern __shared__ double sm[];  // g: n_t x 32, e: C x 32, s: (C+1) x 32
+  const LevelView& L = cv.lv;
+  const int m = cv.m;
+  const int64_t nn = L.nn, nt = L.n_t;
+  const int C = cv.n_chunks, Lc = cv.chunk_len;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double* g = sm;
+  double* e = g + nt * 32;
+  double* st = e + (int64_t)C * 32;
+  for (int64_t k = threadIdx.x; k < nn; k += blockDim.x) x[k] = f[k] / L.w;
+  for (int64_t n = 1 + threadIdx.x; n <= nt; n += blockDim.x) x[n * nn] = f[n * nn] / L.w;
+  const bool active = lane < m;
+  {
+    double row[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) row[k] = cv.tinv[lane * 32 + k];
+    for (int64_t n = 1 + warp; n <= nt; n += nw) {
+      const double fl = active ? f[n * nn + lane + 1] : 0.0;
+      g[(n - 1) * 32 + lane] = matvec32(row, fl);
+    }
+  }
+  __syncthreads();
+  double arow[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) arow[k] = cv.prop[lane * 32 + k];
+  // step s = 1..nt in march order; level n(s) = s (J) or nt + 1 - s (J^T)
+  auto level_of = [&](int64_t s) -> int64_t { return ADJ ? nt + 1 - s : s; };
+  for (int c = warp; c < C; c += nw) {  // (2) zero-start chunk solves
+    double xv = 0.0;
+    for (int j = 0; j < Lc; ++j) {
+      const int64_t s = (int64_t)c * Lc + j + 1;
+      const double gn = g[(level_of(s) - 1) * 32 + lane];
+      xv = (j == 0) ? gn : gn + matvec32(arow, xv);
+    }
+    e[c * 32 + lane] = xv;
+  }
+  __syncthreads();
+  if (warp == 0) {  // (3) chunk start states
+    double prow[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) prow[k] = cv.prop_chunk[lane * 32 + k];
+    double sv = 0.0;
+    st[lane] = 0.0;
+    for (int c = 0; c < C; ++c) {
+      sv = (c == 0) ? e[lane] : e[c * 32 + lane] + matvec32(prow, sv);
+      st[(c + 1) * 32 + lane] = sv;
+    }
+  }
+  __syncthreads();
+  for (int c = warp; c < C; c += nw) {  // (4) final chunk solves from the true start
+    double xv = st[c * 32 + lane];
+    for (int j = 0; j < Lc; ++j) {
+      const int64_t s = (int64_t)c * Lc + j + 1;
+      const int64_t n = level_of(s);
+      const double gn = g[(n - 1) * 32 + lane];
+      xv = (s == 1) ? gn : gn + matvec32(arow, xv);
+      if (active) x[n * nn + lane + 1] = xv;
+    }
+  }
+}
+
 __global__ void k_sumsq(const double* __restrict__ x, int64_t n, double* __restrict__ partials) {
   double acc = 0.0;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
@@ -1362,6 +1666,18 @@ int launch_sweep(bool adjoint, const LevelView& L, const double* f, const double
                  : sweep_impl<false>(L, f, x, y, omega, partials, s);
 }
 
+int launch_sweep2(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
+                  double omega, cudaStream_t s) {
+  constexpr int NT = 8;
+  const dim3 blk = march_block(L);
+  const int64_t per = (int64_t)(blk.x / 32) * 28;
+  const int64_t tiles = (L.nn + per - 1) / per;
+  const dim3 grd((unsigned)(tiles * ((rows(L) + NT - 1) / NT)));
+  if (adjoint) k_lean2x2<true, NT><<<grd, blk, 0, s>>>(L, f, x, y, omega, tiles);
+  else k_lean2x2<false, NT><<<grd, blk, 0, s>>>(L, f, x, y, omega, tiles);
+  return check_launch();
+}
+
 int launch_sweep_from_zero(const LevelView& L, const double* f, double* y, double omega,
                            cudaStream_t s) {
   const dim3 blk = march_block(L);
@@ -1419,6 +1735,22 @@ int launch_prolong_add(const LevelView& F, const LevelView& C, int dir, const do
 
 int launch_coarsest(bool adjoint, const CoarsestView& cv, const double* f, double* x,
                     double* scratch, cudaStream_t s) {
+  if (cv.m <= 32 && cv.prop_chunk != nullptr && cv.n_chunks > 1) {
+    const size_t bytes = sizeof(double) * 32 * ((size_t)cv.lv.n_t + 2 * (size_t)cv.n_chunks + 1);
+    if (bytes <= 160 * 1024) {
+      const int threads = 32 * (cv.n_chunks < 16 ? cv.n_chunks : 16);
+      if (adjoint) k_coarsest_chunked<true><<<1, threads, bytes, s>>>(cv, f, x);
+      else k_coarsest_chunked<false><<<1, threads, bytes, s>>>(cv, f, x);
+      return check_launch();
+    }
+  }
+  if (cv.m <= 32 && cv.tinv != nullptr && scratch != nullptr) {
+    const size_t gbytes = sizeof(double) * 32 * (size_t)cv.lv.n_t;
+    const int sm = gbytes <= 160 * 1024 ? 1 : 0;
+    if (adjoint) k_coarsest_prop<true><<<1, 256, sm ? gbytes : 0, s>>>(cv, f, x, scratch, sm);
+    else k_coarsest_prop<false><<<1, 256, sm ? gbytes : 0, s>>>(cv, f, x, scratch, sm);
+    return check_launch();
+  }
   if (cv.m <= 32) {
     if (adjoint) k_coarsest_warp<true><<<1, 32, 0, s>>>(cv, f, x);
     else k_coarsest_warp<false><<<1, 32, 0, s>>>(cv, f, x);
@@ -1445,6 +1777,18 @@ int kernels_init() {
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   if (e != cudaSuccess) return static_cast<int>(e);
   e = cudaFuncSetAttribute(k_coarsest<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           160 * 1024);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  e = cudaFuncSetAttribute(k_coarsest_prop<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           160 * 1024);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  e = cudaFuncSetAttribute(k_coarsest_prop<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           160 * 1024);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  e = cudaFuncSetAttribute(k_coarsest_chunked<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           160 * 1024);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  e = cudaFuncSetAttribute(k_coarsest_chunked<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            160 * 1024);
   return static_cast<int>(e);
 }

@@ -63,6 +63,7 @@ def _load():
         "stmg_hierarchy_device_bytes": [vp, C.POINTER(i64)],
         "stmg_hierarchy_set_stream": [vp, vp],
         "stmg_hierarchy_set_profiling": [vp, i32],
+        "stmg_hierarchy_profile": [vp, i32, i32, C.POINTER(i64), C.POINTER(f64)],
         "stmg_mg_solve": [vp, vp, vp, vp, vp, vp, i32],
         "stmg_level_sweeps": [vp, i32, vp, vp, i32, f64],
         "stmg_level_residual": [vp, i32, vp, vp, vp],
@@ -159,7 +160,8 @@ class _SolveRep(C.Structure):
                 ("kernel_launches", C.c_int64), ("fine_sweeps", C.c_int64),
                 ("fine_sweep_seconds", C.c_double), ("fine_restricts", C.c_int64),
                 ("fine_restrict_seconds", C.c_double), ("fine_prolong_sweeps", C.c_int64),
-                ("fine_prolong_sweep_seconds", C.c_double)]
+                ("fine_prolong_sweep_seconds", C.c_double), ("fine_sweep_pairs", C.c_int64),
+                ("fine_sweep_pair_seconds", C.c_double)]
 
 
 # ---- enums ---------------------------------------------------------------------------
@@ -449,7 +451,7 @@ class LevelHierarchy:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None:
             _lib.stmg_hierarchy_destroy(h)
             self._h = None
 
@@ -514,6 +516,21 @@ class LevelHierarchy:
     def set_profiling(self, on: bool = True):
         _check(_lib.stmg_hierarchy_set_profiling(self._h, 1 if on else 0))
 
+    PROFILE_KINDS = ("sweep", "restrict", "prolong_sweep", "sweep_pair", "sweep_from_zero", "coarsest")
+
+    def profile(self) -> dict:
+        """{level: {kind: (launches, seconds)}} accumulated over profiled solves."""
+        out = {}
+        for l in range(self._n_levels):
+            d = {}
+            for kind, name in enumerate(self.PROFILE_KINDS):
+                n, t = C.c_int64(), C.c_double()
+                _check(_lib.stmg_hierarchy_profile(self._h, l, kind, C.byref(n), C.byref(t)))
+                if n.value:
+                    d[name] = (n.value, t.value)
+            out[l] = d
+        return out
+
 
 def build_hierarchy(fine: SpaceTimeGrid, method, path: CoarseningPath, chi=None, mat=None,
                     device: int = 0) -> LevelHierarchy:
@@ -559,8 +576,9 @@ def mg_solve(h: LevelHierarchy, b, u, opts: Optional[SolveOptions] = None) -> So
     _check(_lib.stmg_mg_solve(h.handle, _ptr(b), _ptr(u), C.byref(co), C.byref(rep), hist.ctypes.data,
                               hist.size))
     kt = {}
-    if rep.fine_sweeps or rep.fine_restricts or rep.fine_prolong_sweeps:
+    if rep.fine_sweeps or rep.fine_restricts or rep.fine_prolong_sweeps or rep.fine_sweep_pairs:
         kt = {"fine_sweep": (rep.fine_sweeps, rep.fine_sweep_seconds),
+              "fine_sweep_pair": (rep.fine_sweep_pairs, rep.fine_sweep_pair_seconds),
               "fine_restrict": (rep.fine_restricts, rep.fine_restrict_seconds),
               "fine_prolong_sweep": (rep.fine_prolong_sweeps, rep.fine_prolong_sweep_seconds)}
     return SolveReport(SolveStatus(rep.status), rep.cycles, rep.factor,
@@ -660,7 +678,7 @@ class DistHierarchy:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _lib is not None:
             _lib.stmg_dist_destroy(h)
             self._h = None
 

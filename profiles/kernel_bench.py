@@ -65,11 +65,14 @@ def main():
             best = ms if best is None else min(best, ms)
         return best
 
-    ms = timed(lambda: h.sweeps(0, f, x, args.sweeps), args.reps)
+    # single sweeps: the level API ping-pongs and copies back on odd counts, so
+    # the single-sweep kernel is timed through its residual twin (same kernel,
+    # same 24 B/DOF) below; the fused pair is timed directly
+    ms = timed(lambda: h.sweeps(0, f, x, 2 * args.sweeps), args.reps)
     per = ms / args.sweeps
-    out["sweep_ms"] = per
-    out["sweep_GBps"] = 24.0 * n0 / (per * 1e-3) / 1e9
-    out["sweep_dof_updates_per_s"] = n0 / (per * 1e-3)
+    out["sweep_pair_ms"] = per
+    out["sweep_pair_GBps"] = 24.0 * n0 / (per * 1e-3) / 1e9
+    out["sweep_pair_dof_updates_per_s"] = 2 * n0 / (per * 1e-3)
     ms = timed(lambda: h.restrict_residual(0, f, x, fc), args.reps)
     out["restrict_x_ms"] = ms
     out["restrict_x_GBps"] = (16.0 * n0 + 8.0 * n1) / (ms * 1e-3) / 1e9
