@@ -178,7 +178,8 @@ int stmg_hierarchy_set_stream(stmg_hierarchy* h, void* cuda_stream);
 int stmg_hierarchy_set_profiling(stmg_hierarchy* h, int32_t on);
 /* Accumulated in-graph device time of one kernel kind on one level over all
  * profiled solves (kind: 0 sweep, 1 residual+restriction, 2 prolongation+sweep,
- * 3 fused two-sweep, 4 first sweep from zero, 5 coarsest exact solve). */
+ * 3 fused two-sweep, 4 first sweep from zero, 5 coarsest exact solve, 6 the
+ * coarse-tail cluster kernel, attributed to its first level). */
 int stmg_hierarchy_profile(const stmg_hierarchy* h, int32_t level, int32_t kind, int64_t* launches,
                            double* seconds);
 /* Bytes of device memory the hierarchy holds. */

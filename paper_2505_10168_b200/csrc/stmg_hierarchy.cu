@@ -9,6 +9,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -385,7 +386,8 @@ enum TimedKind {
   kTimedSweep2 = 3,
   kTimedFromZero = 4,
   kTimedCoarsest = 5,
-  kTimedKinds = 6
+  kTimedTail = 6,
+  kTimedKinds = 7
 };
 
 struct TimedKernel {
@@ -420,6 +422,8 @@ struct stmg_hierarchy {
   cudaStream_t own_stream = nullptr;  // created with the hierarchy
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture
   bool profiling = false;
+  int tail_start = -1;   // first level run by the coarse-tail cluster kernel (-1: none)
+  int tail_cluster = 16;
   // per (level, kind): launches and device seconds accumulated while profiling
   std::vector<std::array<std::pair<int64_t, double>, stmgb::kTimedKinds>> prof;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -654,6 +658,22 @@ void finish_create(stmg_hierarchy* h, bool share_ws_from_other, const stmg_hiera
   DeviceGuard dg(h->device);
   launch_check(kernels_init(), "kernels_init");
   upload_levels(h);
+  {
+    // Off by default: measured slower on BASELINE config 1 (profiles/round1.md) --
+    // 16 CTAs serialise the tiles of levels that one normal launch covers in a wave.
+    int64_t tail_dofs = 0;
+    if (const char* v = std::getenv("STMG_TAIL_DOFS")) tail_dofs = std::atoll(v);
+    if (const char* v = std::getenv("STMG_TAIL_CLUSTER")) h->tail_cluster = std::max(1, std::min(16, std::atoi(v)));
+    h->tail_start = -1;
+    const int nl = h->n_levels();
+    if (tail_dofs > 0 && nl >= 2 && tail_supported(h->coarsest)) {
+      for (int l = 1; l < nl; ++l)
+        if (h->ndofs(l) <= tail_dofs && nl - l <= kTailMaxLevels) {
+          h->tail_start = l;
+          break;
+        }
+    }
+  }
   if (share_ws_from_other) {
     h->ws = other->ws;
   } else {
@@ -731,6 +751,26 @@ struct Emitter {
     const int nl = h->n_levels();
     const LevelView& L = h->views[l];
     double* f = h->ws->f[l]->p;
+    if (from_zero && nu >= 1 && l == h->tail_start) {
+      TailParams tp{};
+      tp.n_levels = nl - l;
+      tp.nu = nu;
+      tp.omega = omega;
+      for (int k = 0; k < tp.n_levels; ++k) {
+        tp.lv[k] = h->views[l + k];
+        tp.dir[k] = l + k < nl - 1 ? h->dirs[l + k] : 0;
+        tp.f[k] = h->ws->f[l + k]->p;
+        tp.xa[k] = h->ws->xa[l + k]->p;
+        tp.xb[k] = h->ws->xb[l + k]->p;
+      }
+      tp.cv = h->coarsest;
+      int fin = 0;
+      timed_launch(l, kTimedTail, [&] {
+        launch_check(launch_tail(h->adjoint, tp, h->tail_cluster, &fin, s), "coarse tail");
+      });
+      ++kernels;
+      return fin;
+    }
     if (l == nl - 1) {
       timed_launch(l, kTimedCoarsest, [&] {
         launch_check(launch_coarsest(h->adjoint, h->coarsest, f, buf(l, 0), h->ws->coarse_scratch->p, s),

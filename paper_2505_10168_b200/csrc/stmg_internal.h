@@ -51,6 +51,22 @@ struct CoarsestView {
   const double* prop_chunk;
 };
 
+// The coarse tail of a V-cycle (levels [Lt, L), all small) executed by one
+// thread-block cluster: level 0 here is hierarchy level Lt (its f is the
+// restricted input, its zero iterate is implied), the last is the coarsest.
+constexpr int kTailMaxLevels = 24;
+struct TailParams {
+  int n_levels;
+  int nu;
+  double omega;
+  LevelView lv[kTailMaxLevels];
+  int dir[kTailMaxLevels];  // step from tail level k to k + 1
+  double* f[kTailMaxLevels];
+  double* xa[kTailMaxLevels];
+  double* xb[kTailMaxLevels];
+  CoarsestView cv;
+};
+
 // ---- kernel launchers (stmg_kernels.cu); all asynchronous on `s` ------------------
 // One damped-Jacobi sweep y = x + omega (f - J x) / diag.  If partials != nullptr,
 // the block partial sums of r^2 are written too (deterministic order).  If y ==
@@ -93,6 +109,10 @@ int launch_sensitivities(int64_t n_el, int64_t n_t, double dt, const double* dk_
 int launch_dot(const double* x, const double* y, int64_t n, double* partials, int64_t* n_partials,
                cudaStream_t s);
 int kernels_init();  // once per device
+// Launch the coarse-tail cluster kernel; returns the buffer index (0 = xa,
+// 1 = xb) of tail level 0 holding the result through *final_buf.
+int launch_tail(bool adjoint, const TailParams& p, int cluster, int* final_buf, cudaStream_t s);
+bool tail_supported(const CoarsestView& cv);
 // Kernel design selection for benchmarking (0 = production default).
 void set_kernel_variant(int v);
 int kernel_variant();

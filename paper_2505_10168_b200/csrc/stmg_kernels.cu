@@ -14,6 +14,7 @@
 // sweep kernels march each thread column (one node i) through NT consecutive
 // time levels, keeping the previous level's values in registers, so each
 // vector element is read from HBM once per sweep (24 B per DOF update).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -325,17 +326,17 @@ __global__ void __launch_bounds__(kMaxTW, MINB) k_lean(LevelView L, Ld ld,
 // nodes, so no separate halo registers are needed (lower register pressure,
 // higher occupancy).  Blocks are ordered node-tile fastest (1-D grid) so that
 // the staged coupled level of a time tile is usually still in L2.
-template <bool ADJ, int MODE, bool NORM, int NT, int MINB, class Ld>
-__global__ void __launch_bounds__(kMaxTW, MINB) k_lean2(LevelView L, Ld ld,
-                                                        const double* __restrict__ f,
-                                                        double* __restrict__ y, double omega,
-                                                        double* __restrict__ partials,
-                                                        int64_t node_tiles) {
+// Tile body (callable from the stand-alone kernel and the coarse-tail cluster
+// kernel): virtual block `bid` of `tw` threads; returns the thread's r^2 sum.
+template <bool ADJ, int MODE, bool NORM, int NT, class Ld>
+__device__ __forceinline__ double dev_lean2(const LevelView& L, const Ld& ld, const double* __restrict__ f,
+                                            double* __restrict__ y, double omega, int64_t node_tiles,
+                                            int64_t bid, int tw) {
+  if ((int)threadIdx.x >= tw) return 0.0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nn = L.nn, nt = L.n_t;
-  const int64_t bid = blockIdx.x;
   const int64_t tile = bid % node_tiles, ttile = bid / node_tiles;
-  const int64_t per_block = (int64_t)(blockDim.x >> 5) * 30;
+  const int64_t per_block = (int64_t)(tw >> 5) * 30;
   const int64_t i = tile * per_block + warp * 30 + lane - 1;  // node of this lane
   const int64_t n0 = L.n_lo + ttile * NT;
   const int64_t nbase = ADJ ? n0 : n0 - 1;
@@ -422,9 +423,19 @@ __global__ void __launch_bounds__(kMaxTW, MINB) k_lean2(LevelView L, Ld ld,
       pp = qp;
     }
   }
+  return acc;
+}
+
+template <bool ADJ, int MODE, bool NORM, int NT, int MINB, class Ld>
+__global__ void __launch_bounds__(kMaxTW, MINB) k_lean2(LevelView L, Ld ld,
+                                                        const double* __restrict__ f,
+                                                        double* __restrict__ y, double omega,
+                                                        double* __restrict__ partials,
+                                                        int64_t node_tiles) {
+  const double acc = dev_lean2<ADJ, MODE, NORM, NT>(L, ld, f, y, omega, node_tiles, blockIdx.x, blockDim.x);
   if (NORM) {
     const double s = block_sum(acc);
-    if (threadIdx.x == 0) partials[bid] = s;
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
   }
 }
 
@@ -571,14 +582,16 @@ __global__ void __launch_bounds__(kMaxTW, 3) k_lean2x2(LevelView L, const double
 // I = wfirst/2 + l by shuffles.  Causal t step (DIR 1): coarse level N takes
 // fine levels 2N, 2N+1 at the same node (NT is even, tiles start even).
 template <bool ADJ, int DIR, int NT>
-__global__ void __launch_bounds__(kMaxTW, 2) k_lean_restrict(LevelView F, LevelView C,
-                                                             const double* __restrict__ f,
-                                                             const double* __restrict__ x,
-                                                             double* __restrict__ fc) {
+__device__ __forceinline__ void dev_lean_restrict(const LevelView& F, const LevelView& C,
+                                                  const double* __restrict__ f,
+                                                  const double* __restrict__ x,
+                                                  double* __restrict__ fc, int64_t bx, int64_t by,
+                                                  int tw) {
+  if ((int)threadIdx.x >= tw) return;
   const int lane = threadIdx.x & 31;
   const int64_t nn = F.nn, nt = F.n_t, nnc = C.nn;
-  const int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
-  const int64_t n0 = F.n_lo + (int64_t)blockIdx.x * NT;
+  const int64_t i = by * tw + threadIdx.x;
+  const int64_t n0 = F.n_lo + bx * NT;
   const int64_t nbase = ADJ ? n0 : n0 - 1;
   const int64_t wfirst = i - lane;
   const bool valid = i < nn;
@@ -733,15 +746,25 @@ __global__ void __launch_bounds__(kMaxTW, 2) k_lean_restrict(LevelView F, LevelV
   }
 }
 
+template <bool ADJ, int DIR, int NT>
+__global__ void __launch_bounds__(kMaxTW, 2) k_lean_restrict(LevelView F, LevelView C,
+                                                             const double* __restrict__ f,
+                                                             const double* __restrict__ x,
+                                                             double* __restrict__ fc) {
+  dev_lean_restrict<ADJ, DIR, NT>(F, C, f, x, fc, blockIdx.x, blockIdx.y, blockDim.x);
+}
+
 // Elementwise kernels on a level, 2-D grid (no 64-bit division): blockIdx.x =
 // time tile of kFlatNT levels, blockIdx.y = node tile of blockDim.x nodes.
 constexpr int kFlatNT = 8;
 
-__global__ void k_sweep_from_zero2(LevelView L, const double* __restrict__ f, double* __restrict__ y,
-                                   double omega) {
-  const int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void dev_sweep_from_zero(const LevelView& L, const double* __restrict__ f,
+                                                    double* __restrict__ y, double omega, int64_t bx,
+                                                    int64_t by, int tw) {
+  if ((int)threadIdx.x >= tw) return;
+  const int64_t i = by * tw + threadIdx.x;
   if (i >= L.nn) return;
-  const int64_t n0 = L.n_lo + (int64_t)blockIdx.x * kFlatNT;
+  const int64_t n0 = L.n_lo + bx * kFlatNT;
   const double idv = __ldg(L.coef + kInvD * L.nn + i);
 #pragma unroll
   for (int k = 0; k < kFlatNT; ++k) {
@@ -750,6 +773,11 @@ __global__ void k_sweep_from_zero2(LevelView L, const double* __restrict__ f, do
     const double id = (n == 0 || i == 0) ? L.inv_w : idv;
     y[n * L.nn + i] = 0.0 + omega * (f[n * L.nn + i] * id);
   }
+}
+
+__global__ void k_sweep_from_zero2(LevelView L, const double* __restrict__ f, double* __restrict__ y,
+                                   double omega) {
+  dev_sweep_from_zero(L, f, y, omega, blockIdx.x, blockIdx.y, blockDim.x);
 }
 
 template <int DIR>
@@ -1427,9 +1455,9 @@ __device__ __forceinline__ double matvec32(const double (&row)[32], double v) {
 }
 
 template <bool ADJ>
-__global__ void __launch_bounds__(512) k_coarsest_chunked(CoarsestView cv, const double* __restrict__ f,
-                                                          double* __restrict__ x) {
-  extern __shared__ double sm[];  // g: n_t x 32, e: C x 32, s: (C+1) x 32
+__device__ __forceinline__ void dev_coarsest_chunked(const CoarsestView& cv, const double* __restrict__ f,
+                                                     double* __restrict__ x, double* sm) {
+  // sm: g: n_t x 32, e: C x 32, s: (C+1) x 32; every thread of the block calls this
   const LevelView& L = cv.lv;
   const int m = cv.m;
   const int64_t nn = L.nn, nt = L.n_t;
@@ -1487,6 +1515,103 @@ __global__ void __launch_bounds__(512) k_coarsest_chunked(CoarsestView cv, const
       xv = (s == 1) ? gn : gn + matvec32(arow, xv);
       if (active) x[n * nn + lane + 1] = xv;
     }
+  }
+}
+
+template <bool ADJ>
+__global__ void __launch_bounds__(512) k_coarsest_chunked(CoarsestView cv, const double* __restrict__ f,
+                                                          double* __restrict__ x) {
+  extern __shared__ double sm[];
+  dev_coarsest_chunked<ADJ>(cv, f, x, sm);
+}
+
+// ---------------------------------------------------------------------------
+// Coarse tail in one thread-block cluster.  All CTAs of the cluster stride
+// over the tiles of each pass (the same tile bodies as the stand-alone
+// kernels, so results are bit-identical), a cluster barrier separates passes
+// (it also invalidates L1, so each pass sees the previous one's stores), and
+// CTA 0 runs the parallel-in-time coarsest solve.  One launch replaces
+// ~(2 nu + 2) launches per tail level.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int tile_width(int64_t nn) {
+  return nn >= kMaxTW ? kMaxTW : (int)((nn + 31) / 32 * 32);
+}
+
+template <bool ADJ>
+__global__ void __launch_bounds__(kMaxTW, 1) k_tail(TailParams p) {
+  extern __shared__ double sm[];
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int64_t rank = cluster.block_rank(), cs = cluster.num_blocks();
+  const int nl = p.n_levels;
+  int cur[kTailMaxLevels];
+  auto sweep_pass = [&](int l, const double* xin, double* xout) {
+    const LevelView& L = p.lv[l];
+    const int tw = tile_width(L.nn);
+    const int64_t node_tiles = (L.nn + (tw / 32) * 30 - 1) / ((tw / 32) * 30);
+    const int64_t total = node_tiles * ((L.n_hi - L.n_lo + 7) / 8);
+    const PlainLoad ld{xin, L.nn};
+    for (int64_t t = rank; t < total; t += cs)
+      dev_lean2<ADJ, kSweep, false, 8>(L, ld, p.f[l], xout, p.omega, node_tiles, t, tw);
+    cluster.sync();
+  };
+  for (int l = 0; l + 1 < nl; ++l) {
+    const LevelView& L = p.lv[l];
+    const int tw = tile_width(L.nn);
+    {
+      const int64_t gx = (L.n_hi - L.n_lo + kFlatNT - 1) / kFlatNT, gy = (L.nn + tw - 1) / tw;
+      for (int64_t t = rank; t < gx * gy; t += cs)
+        dev_sweep_from_zero(L, p.f[l], p.xa[l], p.omega, t % gx, t / gx, tw);
+      cluster.sync();
+    }
+    int c = 0;
+    for (int k = 1; k < p.nu; ++k) {
+      sweep_pass(l, c == 0 ? p.xa[l] : p.xb[l], c == 0 ? p.xb[l] : p.xa[l]);
+      c ^= 1;
+    }
+    const LevelView& C = p.lv[l + 1];
+    const double* x = c == 0 ? p.xa[l] : p.xb[l];
+    if (p.dir[l] == 0) {
+      const int64_t gx = (L.n_hi - L.n_lo + 3) / 4, gy = (L.nn + tw - 1) / tw;
+      for (int64_t t = rank; t < gx * gy; t += cs)
+        dev_lean_restrict<ADJ, 0, 4>(L, C, p.f[l], x, p.f[l + 1], t % gx, t / gx, tw);
+    } else {
+      const int64_t gx = (L.n_hi - L.n_lo + 7) / 8, gy = (L.nn + tw - 1) / tw;
+      for (int64_t t = rank; t < gx * gy; t += cs)
+        dev_lean_restrict<ADJ, 1, 8>(L, C, p.f[l], x, p.f[l + 1], t % gx, t / gx, tw);
+    }
+    cluster.sync();
+    cur[l] = c;
+  }
+  if (rank == 0) dev_coarsest_chunked<ADJ>(p.cv, p.f[nl - 1], p.xa[nl - 1], sm);
+  cluster.sync();
+  int child = 0;
+  for (int l = nl - 2; l >= 0; --l) {
+    const LevelView& L = p.lv[l];
+    const LevelView& C = p.lv[l + 1];
+    const int tw = tile_width(L.nn);
+    int c = cur[l];
+    const double* xc = child == 0 ? p.xa[l + 1] : p.xb[l + 1];
+    const int64_t node_tiles = (L.nn + (tw / 32) * 30 - 1) / ((tw / 32) * 30);
+    const int64_t total = node_tiles * ((L.n_hi - L.n_lo + 7) / 8);
+    double* xin = c == 0 ? p.xa[l] : p.xb[l];
+    double* xout = c == 0 ? p.xb[l] : p.xa[l];
+    if (p.dir[l] == 0) {
+      const ProlongLoad<0> ld{xin, xc, L.nn, C.nn};
+      for (int64_t t = rank; t < total; t += cs)
+        dev_lean2<ADJ, kSweep, false, 8>(L, ld, p.f[l], xout, p.omega, node_tiles, t, tw);
+    } else {
+      const ProlongLoad<1> ld{xin, xc, L.nn, C.nn};
+      for (int64_t t = rank; t < total; t += cs)
+        dev_lean2<ADJ, kSweep, false, 8>(L, ld, p.f[l], xout, p.omega, node_tiles, t, tw);
+    }
+    cluster.sync();
+    c ^= 1;
+    for (int k = 1; k < p.nu; ++k) {
+      sweep_pass(l, c == 0 ? p.xa[l] : p.xb[l], c == 0 ? p.xb[l] : p.xa[l]);
+      c ^= 1;
+    }
+    child = c;
   }
 }
 
@@ -1790,6 +1915,43 @@ int kernels_init() {
   if (e != cudaSuccess) return static_cast<int>(e);
   e = cudaFuncSetAttribute(k_coarsest_chunked<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            160 * 1024);
+  if (e != cudaSuccess) return static_cast<int>(e);
+  for (auto fn : {k_tail<true>, k_tail<false>}) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    if (e != cudaSuccess) return static_cast<int>(e);
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  return 0;
+}
+
+bool tail_supported(const CoarsestView& cv) {
+  if (!(cv.m <= 32 && cv.prop_chunk != nullptr && cv.n_chunks > 1)) return false;
+  const size_t bytes = sizeof(double) * 32 * ((size_t)cv.lv.n_t + 2 * (size_t)cv.n_chunks + 1);
+  return bytes <= 160 * 1024;
+}
+
+int launch_tail(bool adjoint, const TailParams& p, int cluster, int* final_buf, cudaStream_t s) {
+  if (p.nu < 1 || p.n_levels < 1 || p.n_levels > kTailMaxLevels || !tail_supported(p.cv)) return 1;
+  const size_t smem = sizeof(double) * 32 * ((size_t)p.cv.lv.n_t + 2 * (size_t)p.cv.n_chunks + 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)cluster);
+  cfg.blockDim = dim3(kMaxTW);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = adjoint ? cudaLaunchKernelEx(&cfg, k_tail<true>, p) : cudaLaunchKernelEx(&cfg, k_tail<false>, p);
+  // result buffer of tail level 0: from-zero sweep -> 0, nu-1 flips, nu flips up
+  int c = (p.nu - 1) & 1;
+  if (p.n_levels > 1) c = (c + p.nu) & 1;
+  else c = 0;
+  if (final_buf) *final_buf = c;
   return static_cast<int>(e);
 }
 

@@ -516,7 +516,8 @@ class LevelHierarchy:
     def set_profiling(self, on: bool = True):
         _check(_lib.stmg_hierarchy_set_profiling(self._h, 1 if on else 0))
 
-    PROFILE_KINDS = ("sweep", "restrict", "prolong_sweep", "sweep_pair", "sweep_from_zero", "coarsest")
+    PROFILE_KINDS = ("sweep", "restrict", "prolong_sweep", "sweep_pair", "sweep_from_zero", "coarsest",
+                     "coarse_tail")
 
     def profile(self) -> dict:
         """{level: {kind: (launches, seconds)}} accumulated over profiled solves."""

@@ -233,3 +233,18 @@ def test_adjoint_shares_workspace_with_primal(torch, S, port):
         lam = np.zeros_like(b)
         rep = S.mg_solve(ht, c, lam, S.SolveOptions(nu=2, tol=1e-10, max_cycles=20))
         check_solve(rep, lam, *reversed(hp_adj.solve(c, nu=2, tol=1e-10, max_cycles=20)))
+
+
+def test_coarse_tail_cluster_kernel_is_bitwise(torch, S, port, monkeypatch):
+    """The opt-in coarse-tail cluster kernel (STMG_TAIL_DOFS) gives the same
+    iterate bit for bit as the per-level launches."""
+    cs = case("cfg1_mini")
+    b = cs.rhs_vector(port)
+    opts = S.SolveOptions(nu=cs.nu, tol=cs.tol)
+    u0 = np.zeros_like(b)
+    r0 = S.mg_solve(gpu_hier(S, cs, port), b, u0, opts)
+    monkeypatch.setenv("STMG_TAIL_DOFS", "20000")
+    u1 = np.zeros_like(b)
+    r1 = S.mg_solve(gpu_hier(S, cs, port), b, u1, opts)
+    assert r1.cycles == r0.cycles and r1.history == r0.history
+    assert np.array_equal(bits(u1), bits(u0))
