@@ -173,8 +173,9 @@ int stmg_hierarchy_level_coeffs(const stmg_hierarchy* h, int32_t level, double* 
  * hierarchy's own stream).  Graphs are captured on a private stream and launched
  * on this one. */
 int stmg_hierarchy_set_stream(stmg_hierarchy* h, void* cuda_stream);
-/* Record CUDA events around the finest level's kernels inside the V-cycle graph
- * (on != 0); the timings appear in stmg_solve_report.  Off by default. */
+/* Record CUDA events around kernels inside the V-cycle graph: on = 1 the finest
+ * level's kernels (timings in stmg_solve_report), on = 2 every kernel of every
+ * level (stmg_hierarchy_profile; adds a few us per kernel).  0 = off (default). */
 int stmg_hierarchy_set_profiling(stmg_hierarchy* h, int32_t on);
 /* Accumulated in-graph device time of one kernel kind on one level over all
  * profiled solves (kind: 0 sweep, 1 residual+restriction, 2 prolongation+sweep,
@@ -196,6 +197,12 @@ int stmg_mg_solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solv
 /* `sweeps` damped-Jacobi sweeps in place (csr_residual + jacobi_update). */
 int stmg_level_sweeps(stmg_hierarchy* h, int32_t level, const double* f, double* x,
                       int32_t sweeps, double omega);
+/* Benchmark form: `launches` back-to-back kernel launches ping-ponging between
+ * x and y (x -> y -> x ...), each a single sweep (fused_pairs = 0) or a fused
+ * two-sweep pass (fused_pairs = 1); asynchronous on the hierarchy's stream, no
+ * copies.  The iterate ends in x after an even number of launches. */
+int stmg_level_sweep_kernels(stmg_hierarchy* h, int32_t level, const double* f, double* x, double* y,
+                             int32_t launches, int32_t fused_pairs, double omega);
 /* r = f - J_l x  (csr_residual) */
 int stmg_level_residual(stmg_hierarchy* h, int32_t level, const double* f, const double* x,
                         double* r);

@@ -512,7 +512,7 @@ void dist_build(stmg_dist* d, int world, int rank, const void* nccl_id, int64_t 
 }
 
 GraphEntry& dist_graph(stmg_dist* d, int nu, double omega) {
-  const GraphKey key{nu, omega, false};
+  const GraphKey key{nu, omega, 0};
   auto it = d->graphs.find(key);
   if (it != d->graphs.end()) return it->second;
   GraphEntry e;

@@ -373,7 +373,7 @@ struct Workspace {
 struct GraphKey {
   int nu;
   double omega;
-  bool profiling;
+  int profiling;
   bool operator<(const GraphKey& o) const {
     return std::tie(nu, omega, profiling) < std::tie(o.nu, o.omega, o.profiling);
   }
@@ -421,7 +421,7 @@ struct stmg_hierarchy {
   cudaStream_t stream = nullptr;      // where work runs (own_stream or a caller's)
   cudaStream_t own_stream = nullptr;  // created with the hierarchy
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture
-  bool profiling = false;
+  int profiling = 0;  // 0 off, 1 finest-level kernels, 2 every kernel
   int tail_start = -1;   // first level run by the coarse-tail cluster kernel (-1: none)
   int tail_cluster = 16;
   // per (level, kind): launches and device seconds accumulated while profiling
@@ -701,11 +701,12 @@ struct Emitter {
   double omega;
   cudaStream_t s;
   int64_t kernels = 0;
-  std::vector<TimedKernel>* timed = nullptr;  // non-null: profile the finest level
+  std::vector<TimedKernel>* timed = nullptr;  // non-null: profiling
+  int prof_mode = 0;
 
   template <class F>
   void timed_launch(int l, int kind, F&& launch) {
-    if (timed) {
+    if (timed && (prof_mode >= 2 || l == 0)) {
       TimedKernel t{kind, l, nullptr, nullptr};
       cuda_check(cudaEventCreate(&t.start), "cudaEventCreate");
       cuda_check(cudaEventCreate(&t.stop), "cudaEventCreate");
@@ -826,12 +827,15 @@ struct Emitter {
 bool speculative(const stmg_hierarchy* h, int nu) { return h->n_levels() > 1 && nu >= 1; }
 
 GraphEntry& get_graph(stmg_hierarchy* h, int nu, double omega) {
-  const GraphKey key{nu, omega, h->profiling};
+  const GraphKey key{nu, omega, h->profiling};  // (int mode; 0 = off)
   auto it = h->graphs.find(key);
   if (it != h->graphs.end()) return it->second;
   GraphEntry e;
   Emitter em{h, nu, omega, h->cap_stream};
-  if (h->profiling) em.timed = &e.timed;
+  if (h->profiling) {
+    em.timed = &e.timed;
+    em.prof_mode = h->profiling;
+  }
   cuda_check(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal), "capture");
   const bool spec = speculative(h, nu);
   e.final_buf = em.level(0, spec ? 1 : 0, spec ? 1 : 0, false);
@@ -1485,7 +1489,7 @@ int stmg_hierarchy_set_stream(stmg_hierarchy* h, void* cuda_stream) {
 int stmg_hierarchy_set_profiling(stmg_hierarchy* h, int32_t on) {
   return guarded([&] {
     checked(h);
-    h->profiling = on != 0;
+    h->profiling = on < 0 ? 0 : (on > 2 ? 2 : on);
   });
 }
 
@@ -1546,6 +1550,25 @@ int stmg_level_sweeps(stmg_hierarchy* h, int32_t l, const double* f, double* x, 
     if (a != x)
       cuda_check(cudaMemcpyAsync(x, a, sizeof(double) * h->ndofs(l), cudaMemcpyDeviceToDevice, h->stream), "copy");
     cuda_check(cudaStreamSynchronize(h->stream), "sync");
+  });
+}
+
+int stmg_level_sweep_kernels(stmg_hierarchy* h, int32_t l, const double* f, double* x, double* y,
+                             int32_t launches, int32_t fused_pairs, double omega) {
+  return guarded([&] {
+    checked(h);
+    check_level(h, l);
+    if (!f || !x || !y || x == y || launches < 0) throw std::invalid_argument("sweep_kernels: bad arguments");
+    DeviceGuard dg(h->device);
+    double* a = x;
+    double* b = y;
+    for (int k = 0; k < launches; ++k) {
+      if (fused_pairs)
+        launch_check(launch_sweep2(h->adjoint, h->views[l], f, a, b, omega, h->stream), "sweep2");
+      else
+        launch_check(launch_sweep(h->adjoint, h->views[l], f, a, b, omega, nullptr, nullptr, h->stream), "sweep");
+      std::swap(a, b);
+    }
   });
 }
 

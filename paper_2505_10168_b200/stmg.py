@@ -67,6 +67,7 @@ def _load():
         "stmg_mg_solve": [vp, vp, vp, vp, vp, vp, i32],
         "stmg_level_sweeps": [vp, i32, vp, vp, i32, f64],
         "stmg_level_residual": [vp, i32, vp, vp, vp],
+        "stmg_level_sweep_kernels": [vp, i32, vp, vp, vp, i32, i32, f64],
         "stmg_level_restrict_residual": [vp, i32, vp, vp, vp],
         "stmg_level_restrict": [vp, i32, vp, vp],
         "stmg_level_prolong_add": [vp, i32, vp, vp],
@@ -480,6 +481,11 @@ class LevelHierarchy:
     def sweeps(self, l, f, x, n, omega=0.5):
         _check(_lib.stmg_level_sweeps(self._h, l, _ptr(f), _ptr(x), int(n), float(omega)))
 
+    def sweep_kernels(self, l, f, x, y, launches, fused_pairs=False, omega=0.5):
+        """Benchmark form (asynchronous): ping-pong x <-> y for `launches` launches."""
+        _check(_lib.stmg_level_sweep_kernels(self._h, l, _ptr(f), _ptr(x), _ptr(y), int(launches),
+                                             1 if fused_pairs else 0, float(omega)))
+
     def residual(self, l, f, x, r):
         _check(_lib.stmg_level_residual(self._h, l, _ptr(f), _ptr(x), _ptr(r)))
 
@@ -513,8 +519,9 @@ class LevelHierarchy:
         raw = getattr(stream, "cuda_stream", stream)
         _check(_lib.stmg_hierarchy_set_stream(self._h, C.c_void_p(raw) if raw else None))
 
-    def set_profiling(self, on: bool = True):
-        _check(_lib.stmg_hierarchy_set_profiling(self._h, 1 if on else 0))
+    def set_profiling(self, on=True):
+        """True / 1: finest-level kernels; 2: every kernel (see stmg_b200.h)."""
+        _check(_lib.stmg_hierarchy_set_profiling(self._h, int(on)))
 
     PROFILE_KINDS = ("sweep", "restrict", "prolong_sweep", "sweep_pair", "sweep_from_zero", "coarsest",
                      "coarse_tail")

@@ -35,7 +35,7 @@ def main():
     ap_prof = os.environ.get("STMG_PROFILE_LEVELS") == "1"
     for k in range(a.solves):
         if ap_prof and k == a.solves - 1:
-            h.set_profiling(True)
+            h.set_profiling(2)
         u = torch.zeros_like(b)
         rep = S.mg_solve(h, b, u, S.SolveOptions(nu=cfg.nu, tol=cfg.tol, max_cycles=cfg.max_cycles))
     print(f"{cfg.name} path={S.path_to_string(path)} cycles={rep.cycles} seconds={rep.seconds:.4f} "

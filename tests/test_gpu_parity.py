@@ -248,3 +248,22 @@ def test_coarse_tail_cluster_kernel_is_bitwise(torch, S, port, monkeypatch):
     r1 = S.mg_solve(gpu_hier(S, cs, port), b, u1, opts)
     assert r1.cycles == r0.cycles and r1.history == r0.history
     assert np.array_equal(bits(u1), bits(u0))
+
+
+@pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "wide_short", "cfg0_deep"])
+def test_sweep_kernel_forms_bitwise(torch, S, port, name):
+    """Single-sweep and fused two-sweep kernels, launched back to back."""
+    cs = case(name)
+    h = gpu_hier(S, cs, port)
+    hp = port_hier(port, cs)
+    rng = np.random.default_rng(3)
+    for l in range(h.n_levels()):
+        n = hp.ndofs(l)
+        x, f = special_values(rng, n), special_values(rng, n)
+        want = hp.sweeps(l, f, x, 4)
+        for pairs, launches in ((False, 4), (True, 2)):
+            xt, ft = torch.from_numpy(x).cuda(), torch.from_numpy(f).cuda()
+            yt = torch.empty_like(xt)
+            h.sweep_kernels(l, ft, xt, yt, launches, pairs)
+            torch.cuda.synchronize()
+            assert np.array_equal(bits(xt), bits(want)), (l, pairs)
