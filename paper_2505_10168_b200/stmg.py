@@ -34,7 +34,8 @@ from typing import Callable, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstmg_b200.so")
+# STMG_LIB_PATH: benchmarking override (A/B builds); the in-tree build otherwise.
+LIB_PATH = os.environ.get("STMG_LIB_PATH") or os.path.join(_HERE, "libstmg_b200.so")
 
 
 class StmgCudaError(RuntimeError):
