@@ -75,60 +75,105 @@ def rhs_for(cfg, S, g):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled DURING the timed region (the recipe's
+    nvidia-smi clocks line, read through NVML so the first sample is taken
+    synchronously on entry and the poll period, 5 ms, resolves a ~250 ms region).
+    Falls back to `nvidia-smi -lms 50` when NVML is unavailable."""
 
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
-        self.index = index
-        self.proc = None
-        self.path = None
+    def __init__(self, device):
+        self.device = device
+        self.sm, self.mx, self.reasons = [], [], set()
+        self.source = None
+        self._stop = threading.Event()
+        self._thread = None
+        self._proc = None
+        self._path = None
+
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+
+        pynvml.nvmlInit()
+        p = torch.cuda.get_device_properties(self.device)
+        try:
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(int(self.device))
+
+    def _sample(self, nv, h):
+        self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+        self.mx.append(float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)))
+        bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        for name, const in self.REASONS:
+            if bits & getattr(nv, const):
+                self.reasons.add(name)
 
     def __enter__(self):
-        fd, self.path = tempfile.mkstemp(suffix=".csv")
-        os.close(fd)
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            nv, h = self._nvml_handle()
+            self._sample(nv, h)
+            self.source = "nvml"
+
+            def loop():
+                while not self._stop.wait(0.005):
+                    self._sample(nv, h)
+
+            self._thread = threading.Thread(target=loop, daemon=True)
+            self._thread.start()
         except Exception:
-            self.proc = None
+            self.source = "nvidia-smi"
+            fd, self._path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            try:
+                idx = int(self.device) if not hasattr(self.device, "index") else int(self.device.index or 0)
+                self._proc = subprocess.Popen(
+                    ["nvidia-smi", f"--id={idx}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits", "-lms", "50"],
+                    stdout=open(self._path, "w"), stderr=subprocess.DEVNULL)
+            except Exception:
+                self._proc = None
         return self
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
+        if self._thread:
+            self._stop.set()
+            self._thread.join(timeout=5)
+        if self._proc:
+            self._proc.terminate()
             try:
-                self.proc.wait(timeout=5)
+                self._proc.wait(timeout=5)
             except Exception:
-                self.proc.kill()
+                self._proc.kill()
+        if self._path and os.path.exists(self._path):
+            with open(self._path) as fh:
+                for line in fh:
+                    parts = [q.strip() for q in line.split(",")]
+                    if len(parts) < 9:
+                        continue
+                    try:
+                        self.sm.append(float(parts[1]))
+                        self.mx.append(float(parts[2]))
+                    except ValueError:
+                        continue
+                    for (name, _), v in zip(self.REASONS, parts[5:9]):
+                        if v.lower() == "active":
+                            self.reasons.add(name)
+            os.unlink(self._path)
 
     def summary(self):
-        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        if not self.path or not os.path.exists(self.path):
-            return out
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        with open(self.path) as fh:
-            for line in fh:
-                parts = [p.strip() for p in line.split(",")]
-                if len(parts) < 9:
-                    continue
-                try:
-                    sm.append(float(parts[1]))
-                    mx.append(float(parts[2]))
-                except ValueError:
-                    continue
-                for nm, v in zip(names, parts[5:9]):
-                    if v.lower() == "active":
-                        reasons.add(nm)
-        os.unlink(self.path)
-        if sm:
-            out.update(sm_mhz=statistics.median(sm), sm_max_mhz=max(mx), samples=len(sm))
-        out["reasons"] = sorted(reasons)
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": sorted(self.reasons),
+               "samples": len(self.sm), "source": self.source}
+        if self.sm:
+            out.update(sm_mhz=statistics.median(self.sm), sm_max_mhz=max(self.mx))
         return out
 
 
@@ -389,7 +434,7 @@ def main():
     torch.cuda.synchronize(dev)
     reps = []
     step_ms = []
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         for _ in range(args.steps):
             with torch.cuda.stream(stream):
                 flush.fill_(1.0)

@@ -1418,13 +1418,14 @@ int stmg_hierarchy_create(const stmg_grid* g, const double* k, const double* c, 
     if (!out) throw std::invalid_argument("build_hierarchy: null output handle");
     *out = nullptr;
     if (!g) throw std::invalid_argument("build_hierarchy: null grid");
+    auto h = std::make_unique<stmg_hierarchy>();
+    // argument errors (the reference's invalid_argument) are raised before any device work
+    h->host = make_host_levels(g, k, c, chi, mat, method, n_dirs, dirs, &h->reassembly);
     int n_dev = 0;
     cuda_check(cudaGetDeviceCount(&n_dev), "cudaGetDeviceCount");
     if (device < 0 || device >= n_dev) throw std::invalid_argument("build_hierarchy: bad device ordinal");
-    auto h = std::make_unique<stmg_hierarchy>();
     h->device = device;
     h->dirs.assign(dirs, dirs + n_dirs);
-    h->host = make_host_levels(g, k, c, chi, mat, method, n_dirs, dirs, &h->reassembly);
     finish_create(h.get(), false, nullptr);
     *out = h.release();
   });
@@ -1705,15 +1706,16 @@ int stmg_dist_create(const stmg_grid* g, const double* k, const double* c, const
     if (!out) throw std::invalid_argument("dist_create: null output handle");
     *out = nullptr;
     if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("dist_create: bad rank/world");
+    if (!g) throw std::invalid_argument("dist_create: null grid");
+    auto d = std::make_unique<stmg_dist>();
+    d->host = make_host_levels(g, k, c, chi, mat, method, n_dirs, dirs, nullptr);
+    if (d->host.size() < 2) throw std::invalid_argument("dist_create: need at least two levels");
     int n_dev = 0;
     cuda_check(cudaGetDeviceCount(&n_dev), "cudaGetDeviceCount");
     if (device < 0 || device >= n_dev) throw std::invalid_argument("dist_create: bad device ordinal");
-    auto d = std::make_unique<stmg_dist>();
     d->device = device;
     d->adjoint = adjoint != 0;
     d->dirs.assign(dirs, dirs + n_dirs);
-    d->host = make_host_levels(g, k, c, chi, mat, method, n_dirs, dirs, nullptr);
-    if (d->host.size() < 2) throw std::invalid_argument("dist_create: need at least two levels");
     dist_build(d.get(), world, rank, nccl_id, min_slab);
     *out = d.release();
   });

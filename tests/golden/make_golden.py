@@ -88,6 +88,20 @@ def opt_small(ref):
     return dict(chi=r["chi"], records=r["records"], theta=r["theta"])
 
 
+def cfg1_adj_full(ref):
+    """Adjoint solve (transposed hierarchy) on the full config-1 grid and design with the
+    config-3 right-hand side (dx*dt at unmasked DOFs): the adjoint path at full size."""
+    cfg = C.cfg1()
+    dirs, _ = ref.plan(cfg.L, cfg.t_T, cfg.n_el, cfg.n_t, cfg.k, cfg.c, cfg.n_levels,
+                       strategy=cfg.strategy, reassembly=cfg.reassembly, chi=cfg.chi, mat=cfg.mat)
+    c = C.adjoint_uniform_rhs(cfg.n_el, cfg.n_t, cfg.L, cfg.t_T)
+    h = ref.hierarchy(cfg.L, cfg.t_T, cfg.n_el, cfg.n_t, cfg.k, cfg.c, dirs, method=cfg.method, adjoint=True)
+    lam, rep = h.solve(c, nu=cfg.nu, tol=cfg.tol, max_cycles=cfg.max_cycles)
+    U = lam.reshape(cfg.n_t + 1, cfg.n_el + 1)
+    return dict(history=rep.history, cycles=rep.cycles, status=rep.status, level_sums=U.sum(axis=1),
+                u_max=np.abs(lam).max(), dirs=np.asarray(dirs, np.int32), ref_seconds=rep.seconds)
+
+
 def main():
     ref, port = Ref(), Port()
     np.savez_compressed(os.path.join(HERE, "opt_small.npz"), **opt_small(ref))
@@ -99,6 +113,9 @@ def main():
     if "--full" in sys.argv:
         np.savez_compressed(os.path.join(HERE, "cfg1_full.npz"), **cfg1_full(ref, port))
         print("wrote cfg1_full")
+    if "--full" in sys.argv or "--adj" in sys.argv:
+        np.savez_compressed(os.path.join(HERE, "cfg1_adj_full.npz"), **cfg1_adj_full(ref))
+        print("wrote cfg1_adj_full")
 
 
 if __name__ == "__main__":

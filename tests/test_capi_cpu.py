@@ -154,3 +154,12 @@ def test_no_silent_cpu_fallback_without_gpu():
     g.k, g.c = np.ones(4), np.ones(4)
     with pytest.raises(S.StmgCudaError):
         S.build_hierarchy(g, "CK", S.CoarseningPath([]))
+
+
+def test_dist_create_argument_errors_before_device_work():
+    from paper_2505_10168_b200 import stmg as S
+
+    g = S.build_fine_grid(1.0, 1.0, 8, 8)
+    g.k, g.c = np.ones(8), np.ones(8)
+    with pytest.raises(ValueError):  # Galerkin P is out of scope: rejected in the C layer, no device touched
+        S.build_dist_hierarchy(g, "CP", S.CoarseningPath([S.CoarseningDirection(0)]), world=1, rank=0)

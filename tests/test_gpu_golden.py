@@ -141,3 +141,30 @@ def test_cfg2_full_scale_properties(S):
     assert torch.equal(u1, u2) and r1.history == r2.history
     true = h.residual_norm(b1, u1) / h.norm2(b1)
     assert abs(true - r1.history[-1]) <= 1e-12 * r1.history[-1]
+
+
+def test_cfg1_adjoint_full_size_matches_reference(S):
+    """Adjoint (transposed hierarchy) at full config-1 size vs the reference."""
+    path = os.path.join(GOLD, "cfg1_adj_full.npz")
+    if not os.path.exists(path):
+        pytest.skip("cfg1_adj_full fixture not generated")
+    import torch
+
+    from paper_2505_10168_b200 import configs as C
+    from tests._tol import histories_match, j_inf_norm, residual_floor
+
+    gold = dict(np.load(path))
+    cfg = C.cfg1()
+    g = S.build_fine_grid(cfg.L, cfg.t_T, cfg.n_el, cfg.n_t)
+    g.k, g.c = cfg.k, cfg.c
+    h = S.transposed_hierarchy(
+        S.build_hierarchy(g, cfg.method, S.CoarseningPath([S.CoarseningDirection(int(d)) for d in gold["dirs"]])))
+    c = torch.from_numpy(C.adjoint_uniform_rhs(cfg.n_el, cfg.n_t, cfg.L, cfg.t_T)).cuda()
+    lam = torch.zeros_like(c)
+    rep = S.mg_solve(h, c, lam, S.SolveOptions(nu=cfg.nu, tol=cfg.tol, max_cycles=cfg.max_cycles))
+    assert rep.cycles == int(gold["cycles"]) and int(rep.status) == int(gold["status"])
+    ln = lam.cpu().numpy()
+    floor = residual_floor(j_inf_norm(h.level_coeffs(0), h.levels[0].w_diri), ln, c.cpu().numpy())
+    assert histories_match(rep.history, gold["history"], floor)
+    U = ln.reshape(cfg.n_t + 1, cfg.n_el + 1)
+    assert np.max(np.abs(U.sum(axis=1) - gold["level_sums"])) <= 1e-10 * np.max(np.abs(gold["level_sums"]))
