@@ -423,7 +423,7 @@ struct stmg_hierarchy {
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture
   int profiling = 0;  // 0 off, 1 finest-level kernels, 2 every kernel
   int tail_start = -1;   // first level run by the coarse-tail cluster kernel (-1: none)
-  int tail_cluster = 16;
+  int tail_cluster = 0;   // 0: grid-wide cooperative tail; 1..16: one cluster
   // per (level, kind): launches and device seconds accumulated while profiling
   std::vector<std::array<std::pair<int64_t, double>, stmgb::kTimedKinds>> prof;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -663,7 +663,7 @@ void finish_create(stmg_hierarchy* h, bool share_ws_from_other, const stmg_hiera
     // 16 CTAs serialise the tiles of levels that one normal launch covers in a wave.
     int64_t tail_dofs = 0;
     if (const char* v = std::getenv("STMG_TAIL_DOFS")) tail_dofs = std::atoll(v);
-    if (const char* v = std::getenv("STMG_TAIL_CLUSTER")) h->tail_cluster = std::max(1, std::min(16, std::atoi(v)));
+    if (const char* v = std::getenv("STMG_TAIL_CLUSTER")) h->tail_cluster = std::max(0, std::min(16, std::atoi(v)));
     h->tail_start = -1;
     const int nl = h->n_levels();
     if (tail_dofs > 0 && nl >= 2 && tail_supported(h->coarsest)) {

@@ -111,6 +111,8 @@ int launch_dot(const double* x, const double* y, int64_t n, double* partials, in
 int kernels_init();  // once per device
 // Launch the coarse-tail cluster kernel; returns the buffer index (0 = xa,
 // 1 = xb) of tail level 0 holding the result through *final_buf.
+// cluster >= 1: one thread-block cluster of that many CTAs; cluster <= 0: a cooperative
+// launch over every SM (grid-wide barriers between passes).
 int launch_tail(bool adjoint, const TailParams& p, int cluster, int* final_buf, cudaStream_t s);
 bool tail_supported(const CoarsestView& cv);
 // Kernel design selection for benchmarking (0 = production default).

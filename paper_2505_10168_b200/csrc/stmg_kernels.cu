@@ -19,6 +19,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <utility>
 
 #include "stmg_internal.h"
 
@@ -30,6 +31,36 @@ constexpr int kNT = 8;           // time levels per thread column
 constexpr int kMaxTW = 256;      // threads per block along x (nodes)
 constexpr int kFlatBlock = 256;  // flat kernels
 constexpr int kSumGrid = 148 * 8;
+
+// Programmatic dependent launch.  Every kernel is launched with programmatic
+// stream serialization, so inside a captured V-cycle graph the next kernel's
+// launch and CTA rasterisation overlap the tail of the current one.  Each
+// kernel therefore begins with griddepcontrol.wait (returns once the preceding
+// grid has completed and its writes are visible; a no-op for ordinary
+// launches) before touching memory, and then releases its own dependents.
+// STMG_PDL=0 turns the attribute off (A/B measurements).
+bool g_pdl = true;
+
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <class... KArgs, class... Args>
+inline void pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // Canonical 4-lane accumulator for rows whose entry pattern is not the
 // interior one (boundaries, masked columns).
@@ -65,6 +96,25 @@ __device__ __forceinline__ Coefs load_coefs(const LevelView& L, int64_t i) {
   return c;
 }
 
+// Interior row (all six entries present): the fixed canonical lane order.
+// x*: same-time values at i-1, i, i+1; y*: coupled-level values.
+template <bool ADJ>
+__device__ __forceinline__ double row_interior(const Coefs& c, double xm, double x0, double xp,
+                                               double ym, double y0, double yp) {
+  // Canonical lanes: s0 = (0 + a) + b, s1 = (0 + c) + d, s2 = 0 + e, s3 = 0 + g,
+  // row = (s0 + s1) + (s2 + s3).  "0 + v" equals v as a real number and only
+  // turns an exact -0 into +0, so every intermediate equals the raw sum's in
+  // value; and a sum of operands none of which is -0 is never -0.  Hence the
+  // canonical row is the raw sum with a final -0 -> +0, i.e. raw + 0.0:
+  // bit-identical, 6 additions instead of 10.
+  double raw;
+  if (!ADJ)
+    raw = ((c.om * ym + c.c0 * x0) + (c.o0 * y0 + c.cp * xp)) + (c.op * yp + c.cm * xm);
+  else
+    raw = ((c.cm * xm + c.o0 * y0) + (c.c0 * x0 + c.op * yp)) + (c.cp * xp + c.om * ym);
+  return raw + 0.0;
+}
+
 // Row (n, i) of J (ADJ = false) or J^T (ADJ = true) applied to x, given the
 // same-time values (xm, x0, xp) at i-1, i, i+1 and the other-time values
 // (ym, y0, yp): time n-1 for J, n+1 for J^T.
@@ -77,27 +127,12 @@ __device__ __forceinline__ double row_sum(const LevelView& L, int64_t n, int64_t
                                           double xm, double x0, double xp, double ym, double y0,
                                           double yp) {
   if (n == 0 || i == 0) {
-    const double s0 = 0.0 + L.w * x0;
-    return (s0 + 0.0) + (0.0 + 0.0);
+    return 0.0 + L.w * x0;  // = (s0 + 0) + (0 + 0) with s0 = 0 + w x0 (never -0)
   }
   const bool has_m = i >= 2;
   const bool has_p = i <= L.n_el - 1;
   const bool has_o = ADJ ? (n <= L.n_t - 1) : (n >= 2);
-  if (has_m && has_p && has_o) {
-    double s0, s1, s2, s3;
-    if (!ADJ) {
-      s0 = (0.0 + c.om * ym) + c.c0 * x0;
-      s1 = (0.0 + c.o0 * y0) + c.cp * xp;
-      s2 = 0.0 + c.op * yp;
-      s3 = 0.0 + c.cm * xm;
-    } else {
-      s0 = (0.0 + c.cm * xm) + c.o0 * y0;
-      s1 = (0.0 + c.c0 * x0) + c.op * yp;
-      s2 = 0.0 + c.cp * xp;
-      s3 = 0.0 + c.om * ym;
-    }
-    return (s0 + s1) + (s2 + s3);
-  }
+  if (has_m && has_p && has_o) return row_interior<ADJ>(c, xm, x0, xp, ym, y0, yp);
   Acc a;
   if (!ADJ) {
     if (has_o) {
@@ -121,48 +156,29 @@ __device__ __forceinline__ double row_sum(const LevelView& L, int64_t n, int64_t
   return a.result();
 }
 
-// Interior row (all six entries present): the fixed canonical lane order.
-// x*: same-time values at i-1, i, i+1; y*: coupled-level values.
-template <bool ADJ>
-__device__ __forceinline__ double row_interior(const Coefs& c, double xm, double x0, double xp,
-                                               double ym, double y0, double yp) {
-  double s0, s1, s2, s3;
-  if (!ADJ) {
-    s0 = (0.0 + c.om * ym) + c.c0 * x0;
-    s1 = (0.0 + c.o0 * y0) + c.cp * xp;
-    s2 = 0.0 + c.op * yp;
-    s3 = 0.0 + c.cm * xm;
-  } else {
-    s0 = (0.0 + c.cm * xm) + c.o0 * y0;
-    s1 = (0.0 + c.c0 * x0) + c.op * yp;
-    s2 = 0.0 + c.cp * xp;
-    s3 = 0.0 + c.om * ym;
-  }
-  return (s0 + s1) + (s2 + s3);
-}
 
 // P x_c at fine DOF (n, i) (csr_spmv_add row, proj/src/transfer.cpp:74-88).
 template <int DIR>
 __device__ __forceinline__ double prolong_row(const double* __restrict__ xc, int64_t nnc, int64_t n,
                                               int64_t i) {
+  // canonical lanes with the "0 +" initialisations folded into one final +0.0
+  // (see row_interior): bit-identical to ((0 + a) + (0 + b)) + (0 + 0)
   if (DIR == 0) {
-    if ((i & 1) == 0) {
-      const double s0 = 0.0 + 1.0 * __ldg(xc + n * nnc + (i >> 1));
-      return (s0 + 0.0) + (0.0 + 0.0);
-    }
-    const double s0 = 0.0 + 0.5 * __ldg(xc + n * nnc + ((i - 1) >> 1));
-    const double s1 = 0.0 + 0.5 * __ldg(xc + n * nnc + ((i + 1) >> 1));
-    return (s0 + s1) + (0.0 + 0.0);
+    if ((i & 1) == 0) return 0.0 + 1.0 * __ldg(xc + n * nnc + (i >> 1));
+    return (0.5 * __ldg(xc + n * nnc + ((i - 1) >> 1)) + 0.5 * __ldg(xc + n * nnc + ((i + 1) >> 1))) + 0.0;
   } else {
-    const double s0 = 0.0 + 1.0 * __ldg(xc + (n >> 1) * nnc + i);
-    return (s0 + 0.0) + (0.0 + 0.0);
+    return 0.0 + 1.0 * __ldg(xc + (n >> 1) * nnc + i);
   }
 }
 
+// Staged-row loaders.  operator() is the per-lane form (any lane subset);
+// warp_row() is called by all 32 lanes of a warp whose nodes wfirst-1 ..
+// wfirst+30 are all inside the grid (interior tiles).
 struct PlainLoad {
   const double* __restrict__ x;
   int64_t nn;
   __device__ __forceinline__ double operator()(int64_t n, int64_t i) const { return x[n * nn + i]; }
+  __device__ __forceinline__ double warp_row(int64_t n, int64_t i, int64_t, int) const { return x[n * nn + i]; }
 };
 
 template <int DIR>
@@ -172,6 +188,21 @@ struct ProlongLoad {
   int64_t nn, nnc;
   __device__ __forceinline__ double operator()(int64_t n, int64_t i) const {
     return x[n * nn + i] + prolong_row<DIR>(xc, nnc, n, i);
+  }
+  // x step: the warp's fine nodes need coarse nodes c0 .. c0+16, c0 = (wfirst-1)/2;
+  // lanes 0..17 load them once (coalesced) and every lane takes its one or two
+  // values by shuffle; even/odd rows are selected, not branched.  Same
+  // arithmetic as prolong_row.
+  __device__ __forceinline__ double warp_row(int64_t n, int64_t i, int64_t wfirst, int lane) const {
+    if (DIR == 1) return x[n * nn + i] + prolong_row<1>(xc, nnc, n, i);
+    const int64_t c0 = (wfirst - 1) >> 1;
+    const double v = (lane <= 17 && c0 + lane < nnc) ? __ldg(xc + n * nnc + c0 + lane) : 0.0;
+    const int k0 = (int)((i >> 1) - c0);
+    const double va = __shfl_sync(kFull, v, k0);      // xc[i/2] (even), xc[(i-1)/2] (odd)
+    const double vb = __shfl_sync(kFull, v, k0 + 1);  // xc[(i+1)/2] (odd)
+    const double pe = 0.0 + 1.0 * va;
+    const double po = (0.5 * va + 0.5 * vb) + 0.0;
+    return x[n * nn + i] + ((i & 1) == 0 ? pe : po);
   }
 };
 
@@ -207,6 +238,7 @@ __global__ void __launch_bounds__(kMaxTW, MINB) k_lean(LevelView L, Ld ld,
                                                        const double* __restrict__ f,
                                                        double* __restrict__ y, double omega,
                                                        double* __restrict__ partials) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int64_t nn = L.nn, nt = L.n_t;
   const int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
@@ -324,37 +356,40 @@ __global__ void __launch_bounds__(kMaxTW, MINB) k_lean(LevelView L, Ld ld,
 // Lean variant with overlapping warps: each warp covers 32 consecutive nodes
 // but only lanes 1..30 compute and store; lanes 0 and 31 load the strip-edge
 // nodes, so no separate halo registers are needed (lower register pressure,
-// higher occupancy).  Blocks are ordered node-tile fastest (1-D grid) so that
-// the staged coupled level of a time tile is usually still in L2.
-// Tile body (callable from the stand-alone kernel and the coarse-tail cluster
-// kernel): virtual block `bid` of `tw` threads; returns the thread's r^2 sum.
+// higher occupancy).  Grid: blockIdx.x = node tile (fastest, so the staged
+// coupled level of a time tile is usually still in L2), blockIdx.y strides
+// over time tiles.  Interior tiles (the overwhelming majority) are detected
+// before any load and take a predicate-free path: row pointers computed once,
+// unconditional loads, the fixed interior lane order.
+// Tile body (callable from the stand-alone kernel and the coarse-tail kernel):
+// node tile `tile`, time tile `ttile`, `tw` threads; returns the thread's r^2 sum.
 template <bool ADJ, int MODE, bool NORM, int NT, class Ld>
 __device__ __forceinline__ double dev_lean2(const LevelView& L, const Ld& ld, const double* __restrict__ f,
-                                            double* __restrict__ y, double omega, int64_t node_tiles,
-                                            int64_t bid, int tw) {
+                                            double* __restrict__ y, double omega, int64_t tile,
+                                            int64_t ttile, int tw) {
   if ((int)threadIdx.x >= tw) return 0.0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nn = L.nn, nt = L.n_t;
-  const int64_t tile = bid % node_tiles, ttile = bid / node_tiles;
-  const int64_t per_block = (int64_t)(tw >> 5) * 30;
-  const int64_t i = tile * per_block + warp * 30 + lane - 1;  // node of this lane
+  const int64_t wfirst = tile * ((tw >> 5) * 30) + warp * 30;  // first computing node of the warp
+  if (wfirst >= nn) return 0.0;                                  // whole warp past the grid
+  const int64_t i = wfirst + lane - 1;                           // node of this lane
   const int64_t n0 = L.n_lo + ttile * NT;
   const int64_t nbase = ADJ ? n0 : n0 - 1;
-  const bool in_grid = i >= 0 && i < nn;
-  const bool computes = lane >= 1 && lane <= 30 && in_grid;
-  const int64_t wfirst = tile * per_block + warp * 30;  // first computing node
   const bool rows_in = (ADJ ? (n0 >= 1 && n0 + NT - 1 <= nt - 1) : (n0 >= 2 && n0 + NT - 1 <= nt)) &&
                        n0 + NT - 1 < L.n_hi;
   const bool nodes_in = wfirst >= 2 && wfirst + 29 <= L.n_el - 1;
   double xr[NT + 1], fv[NT];
-  Coefs c{};
   double acc = 0.0;
   if (rows_in && nodes_in) {
+    // every lane's node is inside the grid: lanes 0 / 31 load too (unused values)
+    const bool computes = lane >= 1 && lane <= 30;
+    const double* fp = f + (n0 * nn + i);
 #pragma unroll
-    for (int k = 0; k < NT; ++k) fv[k] = computes ? f[(n0 + k) * nn + i] : 0.0;
+    for (int k = 0; k < NT; ++k) fv[k] = fp[k * nn];
 #pragma unroll
-    for (int r = 0; r <= NT; ++r) xr[r] = ld(nbase + r, i);
-    if (computes) c = load_coefs(L, i);
+    for (int r = 0; r <= NT; ++r) xr[r] = ld.warp_row(nbase + r, i, wfirst, lane);
+    const Coefs c = load_coefs(L, i);
+    double* yp = y + (n0 * nn + i);
     double pm = __shfl_up_sync(kFull, xr[0], 1);
     double pp = __shfl_down_sync(kFull, xr[0], 1);
 #pragma unroll
@@ -362,80 +397,77 @@ __device__ __forceinline__ double dev_lean2(const LevelView& L, const Ld& ld, co
       const double x1 = xr[k + 1];
       const double qm = __shfl_up_sync(kFull, x1, 1);
       const double qp = __shfl_down_sync(kFull, x1, 1);
-      double s0, s1, s2, s3, x0;
-      if (!ADJ) {
-        x0 = x1;
-        s0 = (0.0 + c.om * pm) + c.c0 * x1;
-        s1 = (0.0 + c.o0 * xr[k]) + c.cp * qp;
-        s2 = 0.0 + c.op * pp;
-        s3 = 0.0 + c.cm * qm;
-      } else {
-        x0 = xr[k];
-        s0 = (0.0 + c.cm * pm) + c.o0 * x1;
-        s1 = (0.0 + c.c0 * x0) + c.op * qp;
-        s2 = 0.0 + c.cp * pp;
-        s3 = 0.0 + c.om * qm;
-      }
-      const double r = fv[k] - ((s0 + s1) + (s2 + s3));
+      const double x0 = ADJ ? xr[k] : x1;
+      const double row = ADJ ? row_interior<true>(c, pm, xr[k], pp, qm, x1, qp)
+                             : row_interior<false>(c, qm, x1, qp, pm, xr[k], pp);
+      const double r = fv[k] - row;
       if (computes) {
         if (NORM) acc = acc + r * r;
-        if (MODE == kSweep) y[(n0 + k) * nn + i] = x0 + omega * (r * c.invd);
-        else if (MODE == kResidual) y[(n0 + k) * nn + i] = r;
+        if (MODE == kSweep) yp[k * nn] = x0 + omega * (r * c.invd);
+        else if (MODE == kResidual) yp[k * nn] = r;
       }
       pm = qm;
       pp = qp;
     }
-  } else {
+    return acc;
+  }
+  const bool in_grid = i >= 0 && i < nn;
+  const bool computes = lane >= 1 && lane <= 30 && in_grid;
 #pragma unroll
-    for (int k = 0; k < NT; ++k) {
-      const int64_t n = n0 + k;
-      fv[k] = (computes && n < L.n_hi) ? f[n * nn + i] : 0.0;
-    }
+  for (int k = 0; k < NT; ++k) {
+    const int64_t n = n0 + k;
+    fv[k] = (computes && n < L.n_hi) ? f[n * nn + i] : 0.0;
+  }
 #pragma unroll
-    for (int r = 0; r <= NT; ++r) {
-      const int64_t n = nbase + r;
-      xr[r] = (n >= 0 && n <= nt && in_grid) ? ld(n, i) : 0.0;
-    }
-    if (computes) c = load_coefs(L, i);
-    double pm = __shfl_up_sync(kFull, xr[0], 1);
-    double pp = __shfl_down_sync(kFull, xr[0], 1);
+  for (int r = 0; r <= NT; ++r) {
+    const int64_t n = nbase + r;
+    xr[r] = (n >= 0 && n <= nt && in_grid) ? ld(n, i) : 0.0;
+  }
+  Coefs c{};
+  if (computes) c = load_coefs(L, i);
+  double pm = __shfl_up_sync(kFull, xr[0], 1);
+  double pp = __shfl_down_sync(kFull, xr[0], 1);
 #pragma unroll
-    for (int k = 0; k < NT; ++k) {
-      const int64_t n = n0 + k;
-      if (n >= L.n_hi) break;
-      const double x1 = xr[k + 1];
-      const double qm = __shfl_up_sync(kFull, x1, 1);
-      const double qp = __shfl_down_sync(kFull, x1, 1);
-      if (computes) {
-        const double row = ADJ ? row_sum<true>(L, n, i, c, pm, xr[k], pp, qm, x1, qp)
-                               : row_sum<false>(L, n, i, c, qm, x1, qp, pm, xr[k], pp);
-        const double x0 = ADJ ? xr[k] : x1;
-        const double r = fv[k] - row;
-        if (NORM) acc = acc + r * r;
-        if (MODE == kSweep) {
-          const double id = (n == 0 || i == 0) ? L.inv_w : c.invd;
-          y[n * nn + i] = x0 + omega * (r * id);
-        } else if (MODE == kResidual) {
-          y[n * nn + i] = r;
-        }
+  for (int k = 0; k < NT; ++k) {
+    const int64_t n = n0 + k;
+    if (n >= L.n_hi) break;
+    const double x1 = xr[k + 1];
+    const double qm = __shfl_up_sync(kFull, x1, 1);
+    const double qp = __shfl_down_sync(kFull, x1, 1);
+    if (computes) {
+      const double row = ADJ ? row_sum<true>(L, n, i, c, pm, xr[k], pp, qm, x1, qp)
+                             : row_sum<false>(L, n, i, c, qm, x1, qp, pm, xr[k], pp);
+      const double x0 = ADJ ? xr[k] : x1;
+      const double r = fv[k] - row;
+      if (NORM) acc = acc + r * r;
+      if (MODE == kSweep) {
+        const double id = (n == 0 || i == 0) ? L.inv_w : c.invd;
+        y[n * nn + i] = x0 + omega * (r * id);
+      } else if (MODE == kResidual) {
+        y[n * nn + i] = r;
       }
-      pm = qm;
-      pp = qp;
     }
+    pm = qm;
+    pp = qp;
   }
   return acc;
 }
+
+inline __host__ __device__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 template <bool ADJ, int MODE, bool NORM, int NT, int MINB, class Ld>
 __global__ void __launch_bounds__(kMaxTW, MINB) k_lean2(LevelView L, Ld ld,
                                                         const double* __restrict__ f,
                                                         double* __restrict__ y, double omega,
-                                                        double* __restrict__ partials,
-                                                        int64_t node_tiles) {
-  const double acc = dev_lean2<ADJ, MODE, NORM, NT>(L, ld, f, y, omega, node_tiles, blockIdx.x, blockDim.x);
+                                                        double* __restrict__ partials) {
+  pdl_entry();
+  const int64_t tt = (int64_t)blockIdx.z * gridDim.y + blockIdx.y;  // time tile
+  double acc = 0.0;
+  if (tt < ceil_div(L.n_hi - L.n_lo, NT))
+    acc = dev_lean2<ADJ, MODE, NORM, NT>(L, ld, f, y, omega, blockIdx.x, tt, blockDim.x);
   if (NORM) {
     const double s = block_sum(acc);
-    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+    if (threadIdx.x == 0) partials[tt * gridDim.x + blockIdx.x] = s;
   }
 }
 
@@ -444,27 +476,66 @@ __global__ void __launch_bounds__(kMaxTW, MINB) k_lean2(LevelView L, Ld ld,
 // nodes on each side: lanes 1..30 evaluate sweep 1, lanes 2..29 evaluate and
 // store sweep 2 (28 nodes per warp).  Sweep 1 is also evaluated on the one
 // staged row before the tile (J) / after it (J^T) that sweep 2 couples to.
-// Staged: x on NT + 2 levels, f on NT + 1 levels.  Node-fastest 1-D grid.
+// Staged: x on NT + 2 levels, f on NT + 1 levels.  Grid as k_lean2.
 template <bool ADJ, int NT>
-__global__ void __launch_bounds__(kMaxTW, 3) k_lean2x2(LevelView L, const double* __restrict__ f,
-                                                       const double* __restrict__ x,
-                                                       double* __restrict__ y, double omega,
-                                                       int64_t node_tiles) {
+__device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __restrict__ f,
+                                            const double* __restrict__ x, double* __restrict__ y,
+                                            double omega, int64_t tile, int64_t ttile) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nn = L.nn, nt = L.n_t;
-  const int64_t bid = blockIdx.x;
-  const int64_t tile = bid % node_tiles, ttile = bid / node_tiles;
-  const int64_t per_block = (int64_t)(blockDim.x >> 5) * 28;
-  const int64_t i = tile * per_block + warp * 28 + lane - 2;  // node of this lane
+  const int64_t node1 = tile * ((int64_t)(blockDim.x >> 5) * 28) + warp * 28 - 1;  // node of lane 1
+  if (node1 + 1 >= nn) return;  // no stored node in this warp (whole warp exits)
+  const int64_t i = node1 + lane - 1;  // node of this lane
   const int64_t n0 = L.n_lo + ttile * NT;
   // staged rows: J: n0-2 .. n0+NT-1 ; J^T: n0 .. n0+NT+1  (NT + 2 levels)
   const int64_t sbase = ADJ ? n0 : n0 - 2;
   // sweep-1 rows: J: n0-1 .. n0+NT-1 ; J^T: n0 .. n0+NT   (NT + 1 rows)
   const int64_t s1base = ADJ ? n0 : n0 - 1;
+  // interior tile: every sweep-1 and sweep-2 row has its coupled level and is
+  // unmasked, every sweep-1 node (lanes 1..30) has both neighbours
+  const bool rows_in = (ADJ ? (n0 >= 1 && n0 + NT <= nt - 1) : (n0 >= 3 && n0 + NT - 1 <= nt)) &&
+                       n0 + NT - 1 < L.n_hi;
+  const bool nodes_in = node1 >= 2 && node1 + 29 <= L.n_el - 1;
+  double xs[NT + 2], fv[NT + 1], y1[NT + 1];
+  if (rows_in && nodes_in) {
+    const double* xp = x + (sbase * nn + i);
+    const double* fp = f + (s1base * nn + i);
+#pragma unroll
+    for (int r = 0; r < NT + 2; ++r) xs[r] = xp[r * nn];
+#pragma unroll
+    for (int r = 0; r < NT + 1; ++r) fv[r] = fp[r * nn];
+    const Coefs c = load_coefs(L, i);
+    double pm = __shfl_up_sync(kFull, xs[0], 1), pp = __shfl_down_sync(kFull, xs[0], 1);
+#pragma unroll
+    for (int r = 0; r <= NT; ++r) {
+      const double x1 = xs[r + 1];
+      const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
+      if (ADJ) y1[r] = xs[r] + omega * ((fv[r] - row_interior<true>(c, pm, xs[r], pp, qm, x1, qp)) * c.invd);
+      else y1[r] = x1 + omega * ((fv[r] - row_interior<false>(c, qm, x1, qp, pm, xs[r], pp)) * c.invd);
+      pm = qm;
+      pp = qp;
+    }
+    const bool lane2 = lane >= 2 && lane <= 29;
+    double* yp = y + (n0 * nn + i);
+    double am = __shfl_up_sync(kFull, y1[0], 1), ap = __shfl_down_sync(kFull, y1[0], 1);
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const double z1 = y1[k + 1];
+      const double bm = __shfl_up_sync(kFull, z1, 1), bp = __shfl_down_sync(kFull, z1, 1);
+      if (lane2) {
+        if (ADJ)
+          yp[k * nn] = y1[k] + omega * ((fv[k] - row_interior<true>(c, am, y1[k], ap, bm, z1, bp)) * c.invd);
+        else
+          yp[k * nn] = z1 + omega * ((fv[k + 1] - row_interior<false>(c, bm, z1, bp, am, y1[k], ap)) * c.invd);
+      }
+      am = bm;
+      ap = bp;
+    }
+    return;
+  }
   const bool in_grid = i >= 0 && i < nn;
   const bool lane1 = lane >= 1 && lane <= 30 && in_grid;
   const bool lane2 = lane >= 2 && lane <= 29 && in_grid;
-  double xs[NT + 2], fv[NT + 1];
 #pragma unroll
   for (int r = 0; r < NT + 2; ++r) {
     const int64_t n = sbase + r;
@@ -477,41 +548,6 @@ __global__ void __launch_bounds__(kMaxTW, 3) k_lean2x2(LevelView L, const double
   }
   Coefs c{};
   if (lane1) c = load_coefs(L, i);
-  // interior tile: every sweep-1 and sweep-2 row has its coupled level and is
-  // unmasked, every sweep-1 node (lanes 1..30) has both neighbours
-  const int64_t node1 = tile * per_block + warp * 28 - 1;  // node of lane 1
-  const bool rows_in = (ADJ ? (n0 >= 1 && n0 + NT <= nt - 1) : (n0 >= 3 && n0 + NT - 1 <= nt)) &&
-                       n0 + NT - 1 < L.n_hi;
-  const bool nodes_in = node1 >= 2 && node1 + 29 <= L.n_el - 1;
-  double y1[NT + 1];
-  if (rows_in && nodes_in) {
-    double pm = __shfl_up_sync(kFull, xs[0], 1), pp = __shfl_down_sync(kFull, xs[0], 1);
-#pragma unroll
-    for (int r = 0; r <= NT; ++r) {
-      const double x1 = xs[r + 1];
-      const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
-      if (ADJ) y1[r] = xs[r] + omega * ((fv[r] - row_interior<true>(c, pm, xs[r], pp, qm, x1, qp)) * c.invd);
-      else y1[r] = x1 + omega * ((fv[r] - row_interior<false>(c, qm, x1, qp, pm, xs[r], pp)) * c.invd);
-      pm = qm;
-      pp = qp;
-    }
-    double am = __shfl_up_sync(kFull, y1[0], 1), ap = __shfl_down_sync(kFull, y1[0], 1);
-#pragma unroll
-    for (int k = 0; k < NT; ++k) {
-      const double z1 = y1[k + 1];
-      const double bm = __shfl_up_sync(kFull, z1, 1), bp = __shfl_down_sync(kFull, z1, 1);
-      const int64_t n = n0 + k;
-      if (lane2) {
-        if (ADJ)
-          y[n * nn + i] = y1[k] + omega * ((fv[k] - row_interior<true>(c, am, y1[k], ap, bm, z1, bp)) * c.invd);
-        else
-          y[n * nn + i] = z1 + omega * ((fv[k + 1] - row_interior<false>(c, bm, z1, bp, am, y1[k], ap)) * c.invd);
-      }
-      am = bm;
-      ap = bp;
-    }
-    return;
-  }
   // ---- general path: sweep 1 on NT + 1 rows -> y1[r] (row s1base + r)
   double pm = __shfl_up_sync(kFull, xs[0], 1), pp = __shfl_down_sync(kFull, xs[0], 1);
   if (ADJ) {
@@ -573,6 +609,15 @@ __global__ void __launch_bounds__(kMaxTW, 3) k_lean2x2(LevelView L, const double
     am = bm;
     ap = bp;
   }
+}
+
+template <bool ADJ, int NT>
+__global__ void __launch_bounds__(kMaxTW, 3) k_lean2x2(LevelView L, const double* __restrict__ f,
+                                                       const double* __restrict__ x,
+                                                       double* __restrict__ y, double omega) {
+  pdl_entry();
+  const int64_t tt = (int64_t)blockIdx.z * gridDim.y + blockIdx.y;  // time tile
+  if (tt < ceil_div(L.n_hi - L.n_lo, NT)) dev_lean2x2<ADJ, NT>(L, f, x, y, omega, blockIdx.x, tt);
 }
 
 // f_c = R (f - J x) over one lean tile, R = s P^T (proj/src/transfer.cpp:95-104);
@@ -751,7 +796,137 @@ __global__ void __launch_bounds__(kMaxTW, 2) k_lean_restrict(LevelView F, LevelV
                                                              const double* __restrict__ f,
                                                              const double* __restrict__ x,
                                                              double* __restrict__ fc) {
+  pdl_entry();
   dev_lean_restrict<ADJ, DIR, NT>(F, C, f, x, fc, blockIdx.x, blockIdx.y, blockDim.x);
+}
+
+// Residual + restriction on the overlapping-warp chassis (production).  Lane l
+// of a warp holds node base - 1 + l; lanes 1..30 evaluate the fine residual.
+// x step (DIR 0): coarse node I = base/2 + j, j = 1..14, takes fine nodes
+// 2I-1, 2I, 2I+1 = lanes 2j, 2j+1, 2j+2 (shuffles); warps advance 28 fine
+// nodes (14 coarse), base = 28 w - 2 so that warp 0 owns coarse node 0.
+// Causal t step (DIR 1): coarse level N = fine levels 2N, 2N+1 at the same
+// node; warps advance 30 nodes (NT even, tiles start even).  Interior tiles
+// take a predicate-free path with the folded canonical orders; bitwise equal
+// to csr_spmv(R, r) of the stored fine residual (proj/src/multigrid.cpp:199).
+template <bool ADJ, int DIR, int NT>
+__device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelView& C,
+                                              const double* __restrict__ f, const double* __restrict__ x,
+                                              double* __restrict__ fc, int64_t tile, int64_t ttile, int tw) {
+  if ((int)threadIdx.x >= tw) return;
+  constexpr int kAdv = DIR == 0 ? 28 : 30;  // nodes per warp
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nn = F.nn, nt = F.n_t, nnc = C.nn;
+  const int64_t base = tile * ((tw >> 5) * kAdv) + warp * kAdv + (DIR == 0 ? -2 : 0);
+  if (DIR == 0 ? (base / 2 + 1 >= nnc) : (base >= nn)) return;  // whole warp past the grid
+  const int64_t i = base - 1 + lane;
+  const int64_t n0 = F.n_lo + ttile * NT;
+  const int64_t nbase = ADJ ? n0 : n0 - 1;
+  const bool rows_in = (ADJ ? (n0 >= 1 && n0 + NT - 1 <= nt - 1) : (n0 >= 2 && n0 + NT - 1 <= nt)) &&
+                       n0 + NT - 1 < F.n_hi;
+  const bool nodes_in = base >= 2 && base + 29 <= F.n_el - 1;
+  double xr[NT + 1], fv[NT];
+  if (rows_in && nodes_in) {
+    const double* fp = f + (n0 * nn + i);
+    const double* xp = x + (nbase * nn + i);
+#pragma unroll
+    for (int k = 0; k < NT; ++k) fv[k] = fp[k * nn];
+#pragma unroll
+    for (int r = 0; r <= NT; ++r) xr[r] = xp[r * nn];
+    const Coefs c = load_coefs(F, i);
+    double pm = __shfl_up_sync(kFull, xr[0], 1), pp = __shfl_down_sync(kFull, xr[0], 1);
+    double r_even = 0.0;
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const double x1 = xr[k + 1];
+      const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
+      const double r = fv[k] - (ADJ ? row_interior<true>(c, pm, xr[k], pp, qm, x1, qp)
+                                    : row_interior<false>(c, qm, x1, qp, pm, xr[k], pp));
+      if (DIR == 0) {
+        const int src = 2 * lane;
+        const double ra = __shfl_sync(kFull, r, src & 31);
+        const double rb = __shfl_sync(kFull, r, (src + 1) & 31);
+        const double rc = __shfl_sync(kFull, r, (src + 2) & 31);
+        // canonical ((0 + .5 ra) + (0 + rb)) + ((0 + .5 rc) + 0), folded (see row_interior)
+        if (lane >= 1 && lane <= 14)
+          fc[(n0 + k) * nnc + base / 2 + lane] = ((0.5 * ra + 1.0 * rb) + 0.5 * rc) + 0.0;
+      } else {
+        if ((k & 1) == 0) {
+          r_even = r;
+        } else if (lane >= 1 && lane <= 30) {
+          fc[((n0 + k) >> 1) * nnc + i] = (0.5 * r_even + 0.5 * r) + 0.0;
+        }
+      }
+      pm = qm;
+      pp = qp;
+    }
+    return;
+  }
+  const bool in_grid = i >= 0 && i < nn;
+  const bool computes = lane >= 1 && lane <= 30 && in_grid;
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    const int64_t n = n0 + k;
+    fv[k] = (computes && n < F.n_hi) ? f[n * nn + i] : 0.0;
+  }
+#pragma unroll
+  for (int r = 0; r <= NT; ++r) {
+    const int64_t n = nbase + r;
+    xr[r] = (n >= 0 && n <= nt && in_grid) ? x[n * nn + i] : 0.0;
+  }
+  Coefs c{};
+  if (computes) c = load_coefs(F, i);
+  double pm = __shfl_up_sync(kFull, xr[0], 1), pp = __shfl_down_sync(kFull, xr[0], 1);
+  double r_even = 0.0;
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    const int64_t n = n0 + k;
+    if (n >= F.n_hi) break;
+    const double x1 = xr[k + 1];
+    const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
+    double r = 0.0;
+    if (computes)
+      r = fv[k] - (ADJ ? row_sum<true>(F, n, i, c, pm, xr[k], pp, qm, x1, qp)
+                       : row_sum<false>(F, n, i, c, qm, x1, qp, pm, xr[k], pp));
+    if (DIR == 0) {
+      const int src = 2 * lane;
+      const double ra = __shfl_sync(kFull, r, src & 31);
+      const double rb = __shfl_sync(kFull, r, (src + 1) & 31);
+      const double rc = __shfl_sync(kFull, r, (src + 2) & 31);
+      const int64_t I = base / 2 + lane;
+      if (lane >= 1 && lane <= 14 && I >= 0 && I < nnc) {
+        Acc a;
+        if (I >= 1) a.add(0.5 * ra);
+        a.add(1.0 * rb);
+        if (2 * I + 1 <= F.n_el) a.add(0.5 * rc);
+        fc[n * nnc + I] = a.result();
+      }
+    } else if (computes) {
+      if ((k & 1) == 0) {
+        r_even = r;
+        if (n == nt) {  // last coarse level: truncated row, 0.5 * r(2N) only
+          Acc a;
+          a.add(0.5 * r);
+          fc[(n >> 1) * nnc + i] = a.result();
+        }
+      } else {
+        Acc a;
+        a.add(0.5 * r_even);
+        a.add(0.5 * r);
+        fc[(n >> 1) * nnc + i] = a.result();
+      }
+    }
+    pm = qm;
+    pp = qp;
+  }
+}
+
+template <bool ADJ, int DIR, int NT>
+__global__ void __launch_bounds__(kMaxTW, 3) k_restrict2(LevelView F, LevelView C, const double* __restrict__ f,
+                                                         const double* __restrict__ x, double* __restrict__ fc) {
+  pdl_entry();
+  const int64_t tt = (int64_t)blockIdx.z * gridDim.y + blockIdx.y;
+  if (tt < ceil_div(F.n_hi - F.n_lo, NT)) dev_restrict2<ADJ, DIR, NT>(F, C, f, x, fc, blockIdx.x, tt, blockDim.x);
 }
 
 // Elementwise kernels on a level, 2-D grid (no 64-bit division): blockIdx.x =
@@ -777,12 +952,14 @@ __device__ __forceinline__ void dev_sweep_from_zero(const LevelView& L, const do
 
 __global__ void k_sweep_from_zero2(LevelView L, const double* __restrict__ f, double* __restrict__ y,
                                    double omega) {
+  pdl_entry();
   dev_sweep_from_zero(L, f, y, omega, blockIdx.x, blockIdx.y, blockDim.x);
 }
 
 template <int DIR>
 __global__ void k_prolong_add2(LevelView F, LevelView C, const double* __restrict__ xc,
                                double* __restrict__ x) {
+  pdl_entry();
   const int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
   if (i >= F.nn) return;
   const int64_t n0 = F.n_lo + (int64_t)blockIdx.x * kFlatNT;
@@ -843,6 +1020,7 @@ __global__ void __launch_bounds__(kMaxTW, MINB) k_tile(LevelView L, Ld ld,
                                                        const double* __restrict__ f,
                                                        double* __restrict__ y, double omega,
                                                        double* __restrict__ partials) {
+  pdl_entry();
   extern __shared__ double tile[];
   const TileGeom g = tile_geom<ADJ, NT>();
   const int t = threadIdx.x, W = blockDim.x + 2;
@@ -893,6 +1071,7 @@ __global__ void __launch_bounds__(kMaxTW) k_restrict_tile(LevelView F, LevelView
                                                           const double* __restrict__ f,
                                                           const double* __restrict__ x,
                                                           double* __restrict__ fc) {
+  pdl_entry();
   extern __shared__ double smem[];
   const TileGeom g = tile_geom<ADJ, NT>();
   const int t = threadIdx.x, tw = blockDim.x;
@@ -1057,6 +1236,7 @@ template <bool ADJ, int MODE, bool NORM, class Ld>
 __global__ void __launch_bounds__(kMaxTW, 2) k_stream(LevelView L, Ld ld, const double* __restrict__ f,
                                                       double* __restrict__ y, double omega,
                                                       double* __restrict__ partials, int64_t chunk) {
+  pdl_entry();
   const StreamGeom g = stream_geom<ADJ>(L, chunk);
   const int64_t nn = L.nn;
   const int64_t i = g.i0 + threadIdx.x;
@@ -1097,6 +1277,7 @@ __global__ void __launch_bounds__(kMaxTW, 2) k_restrict_stream(LevelView F, Leve
                                                                const double* __restrict__ x,
                                                                double* __restrict__ fc,
                                                                int64_t chunk) {
+  pdl_entry();
   const StreamGeom g = stream_geom<ADJ>(F, chunk);
   const int lane = threadIdx.x & 31;
   const int64_t nn = F.nn, nnc = C.nn;
@@ -1157,6 +1338,7 @@ __global__ void __launch_bounds__(kMaxTW, 2) k_restrict_stream(LevelView F, Leve
 
 __global__ void k_sweep_from_zero(LevelView L, const double* __restrict__ f, double* __restrict__ y,
                                   double omega, int64_t total) {
+  pdl_entry();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= total) return;
   const int64_t n = idx / L.nn, i = idx - n * L.nn;
@@ -1170,6 +1352,7 @@ __global__ void k_sweep_from_zero(LevelView L, const double* __restrict__ f, dou
 template <bool ADJ, int DIR, bool FROM_R>
 __global__ void k_restrict(LevelView F, LevelView C, const double* __restrict__ f,
                            const double* __restrict__ x, double* __restrict__ fc, int64_t total) {
+  pdl_entry();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= total) return;
   const int64_t nnf = F.nn, nnc = C.nn;
@@ -1201,6 +1384,7 @@ __global__ void k_restrict(LevelView F, LevelView C, const double* __restrict__ 
 template <int DIR>
 __global__ void k_prolong_add(LevelView F, LevelView C, const double* __restrict__ xc,
                               double* __restrict__ x, int64_t total) {
+  pdl_entry();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= total) return;
   const int64_t n = idx / F.nn, i = idx - n * F.nn;
@@ -1216,6 +1400,7 @@ template <bool ADJ>
 __global__ void __launch_bounds__(1024) k_coarsest(CoarsestView cv, const double* __restrict__ f,
                                                    double* __restrict__ x, double* gscratch,
                                                    int use_smem) {
+  pdl_entry();
   extern __shared__ double smem[];
   const LevelView& L = cv.lv;
   const int m = cv.m;
@@ -1272,6 +1457,7 @@ constexpr int kPF = 8;
 template <bool ADJ>
 __global__ void __launch_bounds__(32) k_coarsest_warp(CoarsestView cv, const double* __restrict__ f,
                                                       double* __restrict__ x) {
+  pdl_entry();
   const LevelView& L = cv.lv;
   const int m = cv.m;
   const int64_t nn = L.nn, nt = L.n_t;
@@ -1348,6 +1534,7 @@ __global__ void __launch_bounds__(32) k_coarsest_warp(CoarsestView cv, const dou
 __global__ void k_sensitivities(int64_t n_el, int64_t n_t, double dt, const double* __restrict__ dk_dx,
                                 const double* __restrict__ dc_dx6, const double* __restrict__ u,
                                 const double* __restrict__ lam, double* __restrict__ sens) {
+  pdl_entry();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n_el) return;
   const int64_t nn = n_el + 1;
@@ -1381,6 +1568,7 @@ template <bool ADJ>
 __global__ void __launch_bounds__(256) k_coarsest_prop(CoarsestView cv, const double* __restrict__ f,
                                                        double* __restrict__ x,
                                                        double* __restrict__ gglobal, int use_smem) {
+  pdl_entry();
   extern __shared__ double gsm[];
   double* g = use_smem ? gsm : gglobal;
   const LevelView& L = cv.lv;
@@ -1521,6 +1709,7 @@ __device__ __forceinline__ void dev_coarsest_chunked(const CoarsestView& cv, con
 template <bool ADJ>
 __global__ void __launch_bounds__(512) k_coarsest_chunked(CoarsestView cv, const double* __restrict__ f,
                                                           double* __restrict__ x) {
+  pdl_entry();
   extern __shared__ double sm[];
   dev_coarsest_chunked<ADJ>(cv, f, x, sm);
 }
@@ -1537,12 +1726,29 @@ __device__ __forceinline__ int tile_width(int64_t nn) {
   return nn >= kMaxTW ? kMaxTW : (int)((nn + 31) / 32 * 32);
 }
 
-template <bool ADJ>
+// Barrier scopes for the tail: one thread-block cluster (<= 16 CTAs), or the
+// whole grid of a cooperative launch (every SM; cg's grid barrier arrives with
+// a release and polls with an acquire, so each pass sees the previous one's
+// stores).
+struct ClusterScope {
+  __device__ static int64_t rank() { return cooperative_groups::this_cluster().block_rank(); }
+  __device__ static int64_t size() { return cooperative_groups::this_cluster().num_blocks(); }
+  __device__ static void sync() { cooperative_groups::this_cluster().sync(); }
+};
+struct GridScope {
+  __device__ static int64_t rank() { return blockIdx.x; }
+  __device__ static int64_t size() { return gridDim.x; }
+  __device__ static void sync() { cooperative_groups::this_grid().sync(); }
+};
+
+template <bool ADJ, class Scope>
 __global__ void __launch_bounds__(kMaxTW, 1) k_tail(TailParams p) {
+  pdl_entry();
   extern __shared__ double sm[];
-  namespace cg = cooperative_groups;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int64_t rank = cluster.block_rank(), cs = cluster.num_blocks();
+  struct {
+    __device__ void sync() const { Scope::sync(); }
+  } cluster;
+  const int64_t rank = Scope::rank(), cs = Scope::size();
   const int nl = p.n_levels;
   int cur[kTailMaxLevels];
   auto sweep_pass = [&](int l, const double* xin, double* xout) {
@@ -1552,7 +1758,7 @@ __global__ void __launch_bounds__(kMaxTW, 1) k_tail(TailParams p) {
     const int64_t total = node_tiles * ((L.n_hi - L.n_lo + 7) / 8);
     const PlainLoad ld{xin, L.nn};
     for (int64_t t = rank; t < total; t += cs)
-      dev_lean2<ADJ, kSweep, false, 8>(L, ld, p.f[l], xout, p.omega, node_tiles, t, tw);
+      dev_lean2<ADJ, kSweep, false, 8>(L, ld, p.f[l], xout, p.omega, t % node_tiles, t / node_tiles, tw);
     cluster.sync();
   };
   for (int l = 0; l + 1 < nl; ++l) {
@@ -1571,14 +1777,14 @@ __global__ void __launch_bounds__(kMaxTW, 1) k_tail(TailParams p) {
     }
     const LevelView& C = p.lv[l + 1];
     const double* x = c == 0 ? p.xa[l] : p.xb[l];
-    if (p.dir[l] == 0) {
-      const int64_t gx = (L.n_hi - L.n_lo + 3) / 4, gy = (L.nn + tw - 1) / tw;
-      for (int64_t t = rank; t < gx * gy; t += cs)
-        dev_lean_restrict<ADJ, 0, 4>(L, C, p.f[l], x, p.f[l + 1], t % gx, t / gx, tw);
-    } else {
-      const int64_t gx = (L.n_hi - L.n_lo + 7) / 8, gy = (L.nn + tw - 1) / tw;
-      for (int64_t t = rank; t < gx * gy; t += cs)
-        dev_lean_restrict<ADJ, 1, 8>(L, C, p.f[l], x, p.f[l + 1], t % gx, t / gx, tw);
+    {
+      const int64_t warps = tw >> 5;
+      const int64_t tiles = p.dir[l] == 0 ? ceil_div(ceil_div(C.nn, 14), warps) : ceil_div(L.nn, warps * 30);
+      const int64_t total = tiles * ceil_div(L.n_hi - L.n_lo, 8);
+      for (int64_t t = rank; t < total; t += cs) {
+        if (p.dir[l] == 0) dev_restrict2<ADJ, 0, 8>(L, C, p.f[l], x, p.f[l + 1], t % tiles, t / tiles, tw);
+        else dev_restrict2<ADJ, 1, 8>(L, C, p.f[l], x, p.f[l + 1], t % tiles, t / tiles, tw);
+      }
     }
     cluster.sync();
     cur[l] = c;
@@ -1599,11 +1805,11 @@ __global__ void __launch_bounds__(kMaxTW, 1) k_tail(TailParams p) {
     if (p.dir[l] == 0) {
       const ProlongLoad<0> ld{xin, xc, L.nn, C.nn};
       for (int64_t t = rank; t < total; t += cs)
-        dev_lean2<ADJ, kSweep, false, 8>(L, ld, p.f[l], xout, p.omega, node_tiles, t, tw);
+        dev_lean2<ADJ, kSweep, false, 8>(L, ld, p.f[l], xout, p.omega, t % node_tiles, t / node_tiles, tw);
     } else {
       const ProlongLoad<1> ld{xin, xc, L.nn, C.nn};
       for (int64_t t = rank; t < total; t += cs)
-        dev_lean2<ADJ, kSweep, false, 8>(L, ld, p.f[l], xout, p.omega, node_tiles, t, tw);
+        dev_lean2<ADJ, kSweep, false, 8>(L, ld, p.f[l], xout, p.omega, t % node_tiles, t / node_tiles, tw);
     }
     cluster.sync();
     c ^= 1;
@@ -1616,6 +1822,7 @@ __global__ void __launch_bounds__(kMaxTW, 1) k_tail(TailParams p) {
 }
 
 __global__ void k_sumsq(const double* __restrict__ x, int64_t n, double* __restrict__ partials) {
+  pdl_entry();
   double acc = 0.0;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
        idx += (int64_t)gridDim.x * blockDim.x) {
@@ -1628,6 +1835,7 @@ __global__ void k_sumsq(const double* __restrict__ x, int64_t n, double* __restr
 
 __global__ void k_dot(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
                       double* __restrict__ partials) {
+  pdl_entry();
   double acc = 0.0;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
        idx += (int64_t)gridDim.x * blockDim.x)
@@ -1637,6 +1845,7 @@ __global__ void k_dot(const double* __restrict__ x, const double* __restrict__ y
 }
 
 __global__ void k_finalize_sum(const double* __restrict__ partials, int64_t n, double* out) {
+  pdl_entry();
   double acc = 0.0;
   for (int64_t idx = threadIdx.x; idx < n; idx += blockDim.x) acc = acc + partials[idx];
   const double s = block_sum(acc);
@@ -1676,10 +1885,16 @@ inline int64_t lean2_tiles(const LevelView& L, dim3 blk) {
 inline int64_t rows(const LevelView& L) { return L.n_hi - L.n_lo; }
 // Sub-range (slab) launches always use the production design.
 inline int eff_variant(const LevelView& L) { return full_range(L) ? g_variant : kDefaultVariant; }
+// time tiles on (y, z): tile = z * gridDim.y + y (gridDim.y <= 65535)
+inline dim3 tgrid(int64_t x, int64_t t) {
+  if (t < 1) t = 1;
+  const int64_t y = t < 65535 ? t : 65535;
+  return dim3((unsigned)x, (unsigned)y, (unsigned)((t + y - 1) / y));
+}
 inline dim3 grid_for(const LevelView& L, dim3 blk, int v) {
   if (v == 5 || v == 6) {
     const int nt = variant_nt(v);
-    return dim3((unsigned)(lean2_tiles(L, blk) * ((rows(L) + nt - 1) / nt)));
+    return tgrid(lean2_tiles(L, blk), (rows(L) + nt - 1) / nt);
   }
   const unsigned tiles = (unsigned)((L.nn + blk.x - 1) / blk.x);
   if (v == 3) {
@@ -1699,25 +1914,25 @@ void launch_pass(const LevelView& L, const Ld& ld, const double* f, double* y, d
   const dim3 blk = march_block(L), grd = grid_for(L, blk, v);
   switch (v) {
     case 1:
-      k_lean<ADJ, MODE, NORM, 4, 3><<<grd, blk, 0, s>>>(L, ld, f, y, omega, partials);
+      pdl_launch(k_lean<ADJ, MODE, NORM, 4, 3, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
       break;
     case 2:
-      k_tile<ADJ, MODE, NORM, 4, 4><<<grd, blk, tile_smem(blk, 4, 2), s>>>(L, ld, f, y, omega, partials);
+      pdl_launch(k_tile<ADJ, MODE, NORM, 4, 4, Ld>, grd, blk, tile_smem(blk, 4, 2), s, L, ld, f, y, omega, partials);
       break;
     case 3:
-      k_stream<ADJ, MODE, NORM><<<grd, blk, 0, s>>>(L, ld, f, y, omega, partials, stream_chunk(L, blk));
+      pdl_launch(k_stream<ADJ, MODE, NORM, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials, stream_chunk(L, blk));
       break;
     case 4:
-      k_tile<ADJ, MODE, NORM, 8, 2><<<grd, blk, tile_smem(blk, 8, 2), s>>>(L, ld, f, y, omega, partials);
+      pdl_launch(k_tile<ADJ, MODE, NORM, 8, 2, Ld>, grd, blk, tile_smem(blk, 8, 2), s, L, ld, f, y, omega, partials);
       break;
     case 5:
-      k_lean2<ADJ, MODE, NORM, 8, 3><<<grd, blk, 0, s>>>(L, ld, f, y, omega, partials, lean2_tiles(L, blk));
+      pdl_launch(k_lean2<ADJ, MODE, NORM, 8, 3, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
       break;
     case 6:
-      k_lean2<ADJ, MODE, NORM, 16, 2><<<grd, blk, 0, s>>>(L, ld, f, y, omega, partials, lean2_tiles(L, blk));
+      pdl_launch(k_lean2<ADJ, MODE, NORM, 16, 2, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
       break;
     default:
-      k_lean<ADJ, MODE, NORM, 8, 2><<<grd, blk, 0, s>>>(L, ld, f, y, omega, partials);
+      pdl_launch(k_lean<ADJ, MODE, NORM, 8, 2, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
   }
 }
 
@@ -1747,22 +1962,30 @@ int restrict_tile_impl(const LevelView& F, const LevelView& C, const double* f, 
                        double* fc, cudaStream_t s) {
   const dim3 blk = march_block(F);
   const int v = eff_variant(F);
-  if (v == 0 || v == 1 || v == 5 || v == 6) {
+  if (v == 5 || v == 6) {
+    constexpr int NT = 8;
+    const int64_t per = (int64_t)(blk.x / 32) * (DIR == 0 ? 28 : 30);
+    // DIR 0: warp w owns coarse nodes 14 w .. 14 w + 13
+    const int64_t tiles = DIR == 0 ? ceil_div(ceil_div(C.nn, 14), blk.x / 32) : ceil_div(F.nn, per);
+    pdl_launch(k_restrict2<ADJ, DIR, NT>, tgrid(tiles, (rows(F) + NT - 1) / NT), blk, 0, s, F, C, f, x, fc);
+    return check_launch();
+  }
+  if (v == 0 || v == 1) {
     constexpr int NT = DIR == 0 ? 4 : 8;
     const dim3 grd((unsigned)((rows(F) + NT - 1) / NT), (unsigned)((F.nn + blk.x - 1) / blk.x));
-    k_lean_restrict<ADJ, DIR, NT><<<grd, blk, 0, s>>>(F, C, f, x, fc);
+    pdl_launch(k_lean_restrict<ADJ, DIR, NT>, grd, blk, 0, s, F, C, f, x, fc);
     return check_launch();
   }
   if (v == 3) {
     const dim3 grd = grid_for(F, blk, 3);
-    k_restrict_stream<ADJ, DIR><<<grd, blk, 0, s>>>(F, C, f, x, fc, stream_chunk(F, blk));
+    pdl_launch(k_restrict_stream<ADJ, DIR>, grd, blk, 0, s, F, C, f, x, fc, stream_chunk(F, blk));
     return check_launch();
   }
   constexpr int NT = 8;
   const dim3 grd = grid_for(F, blk, 4);  // NT = 8 tiles
   size_t sm = tile_smem(blk, NT, DIR == 0 ? 3 : 2);
   if (DIR == 0) sm += sizeof(double) * NT * (blk.x + 1);
-  k_restrict_tile<ADJ, DIR, NT><<<grd, blk, sm, s>>>(F, C, f, x, fc);
+  pdl_launch(k_restrict_tile<ADJ, DIR, NT>, grd, blk, sm, s, F, C, f, x, fc);
   return check_launch();
 }
 
@@ -1772,7 +1995,7 @@ int64_t sweep_partials_needed(const LevelView& L) {
   // the largest grid any variant launches for this level
   const dim3 blk = march_block(L);
   const dim3 g1 = grid_for(L, blk, 1), g5 = grid_for(L, blk, 5);
-  const int64_t a = (int64_t)g1.x * g1.y, b = (int64_t)g5.x * g5.y;
+  const int64_t a = (int64_t)g1.x * g1.y * g1.z, b = (int64_t)g5.x * g5.y * g5.z;
   return a > b ? a : b;
 }
 
@@ -1785,7 +2008,7 @@ int launch_sweep(bool adjoint, const LevelView& L, const double* f, const double
                  double omega, double* partials, int64_t* n_partials, cudaStream_t s) {
   if (n_partials) {
     const dim3 blk = march_block(L), grd = grid_for(L, blk, eff_variant(L));
-    *n_partials = (int64_t)grd.x * grd.y;
+    *n_partials = (int64_t)grd.x * grd.y * grd.z;
   }
   return adjoint ? sweep_impl<true>(L, f, x, y, omega, partials, s)
                  : sweep_impl<false>(L, f, x, y, omega, partials, s);
@@ -1797,9 +2020,9 @@ int launch_sweep2(bool adjoint, const LevelView& L, const double* f, const doubl
   const dim3 blk = march_block(L);
   const int64_t per = (int64_t)(blk.x / 32) * 28;
   const int64_t tiles = (L.nn + per - 1) / per;
-  const dim3 grd((unsigned)(tiles * ((rows(L) + NT - 1) / NT)));
-  if (adjoint) k_lean2x2<true, NT><<<grd, blk, 0, s>>>(L, f, x, y, omega, tiles);
-  else k_lean2x2<false, NT><<<grd, blk, 0, s>>>(L, f, x, y, omega, tiles);
+  const dim3 grd = tgrid(tiles, (rows(L) + NT - 1) / NT);
+  if (adjoint) pdl_launch(k_lean2x2<true, NT>, grd, blk, 0, s, L, f, x, y, omega);
+  else pdl_launch(k_lean2x2<false, NT>, grd, blk, 0, s, L, f, x, y, omega);
   return check_launch();
 }
 
@@ -1807,7 +2030,7 @@ int launch_sweep_from_zero(const LevelView& L, const double* f, double* y, doubl
                            cudaStream_t s) {
   const dim3 blk = march_block(L);
   const dim3 grd((unsigned)((rows(L) + kFlatNT - 1) / kFlatNT), (unsigned)((L.nn + blk.x - 1) / blk.x));
-  k_sweep_from_zero2<<<grd, blk, 0, s>>>(L, f, y, omega);
+  pdl_launch(k_sweep_from_zero2, grd, blk, 0, s, L, f, y, omega);
   return check_launch();
 }
 
@@ -1844,8 +2067,8 @@ int launch_restrict(const LevelView& F, const LevelView& C, int dir, const doubl
                     cudaStream_t s) {
   const int64_t total = C.nn * (C.n_t + 1);
   const unsigned g = flat_grid(total);
-  if (dir == 0) k_restrict<false, 0, true><<<g, kFlatBlock, 0, s>>>(F, C, nullptr, r, fc, total);
-  else k_restrict<false, 1, true><<<g, kFlatBlock, 0, s>>>(F, C, nullptr, r, fc, total);
+  if (dir == 0) pdl_launch(k_restrict<false, 0, true>, g, kFlatBlock, 0, s, F, C, nullptr, r, fc, total);
+  else pdl_launch(k_restrict<false, 1, true>, g, kFlatBlock, 0, s, F, C, nullptr, r, fc, total);
   return check_launch();
 }
 
@@ -1853,8 +2076,8 @@ int launch_prolong_add(const LevelView& F, const LevelView& C, int dir, const do
                        cudaStream_t s) {
   const dim3 blk = march_block(F);
   const dim3 grd((unsigned)((rows(F) + kFlatNT - 1) / kFlatNT), (unsigned)((F.nn + blk.x - 1) / blk.x));
-  if (dir == 0) k_prolong_add2<0><<<grd, blk, 0, s>>>(F, C, xc, x);
-  else k_prolong_add2<1><<<grd, blk, 0, s>>>(F, C, xc, x);
+  if (dir == 0) pdl_launch(k_prolong_add2<0>, grd, blk, 0, s, F, C, xc, x);
+  else pdl_launch(k_prolong_add2<1>, grd, blk, 0, s, F, C, xc, x);
   return check_launch();
 }
 
@@ -1864,21 +2087,21 @@ int launch_coarsest(bool adjoint, const CoarsestView& cv, const double* f, doubl
     const size_t bytes = sizeof(double) * 32 * ((size_t)cv.lv.n_t + 2 * (size_t)cv.n_chunks + 1);
     if (bytes <= 160 * 1024) {
       const int threads = 32 * (cv.n_chunks < 16 ? cv.n_chunks : 16);
-      if (adjoint) k_coarsest_chunked<true><<<1, threads, bytes, s>>>(cv, f, x);
-      else k_coarsest_chunked<false><<<1, threads, bytes, s>>>(cv, f, x);
+      if (adjoint) pdl_launch(k_coarsest_chunked<true>, 1, threads, bytes, s, cv, f, x);
+      else pdl_launch(k_coarsest_chunked<false>, 1, threads, bytes, s, cv, f, x);
       return check_launch();
     }
   }
   if (cv.m <= 32 && cv.tinv != nullptr && scratch != nullptr) {
     const size_t gbytes = sizeof(double) * 32 * (size_t)cv.lv.n_t;
     const int sm = gbytes <= 160 * 1024 ? 1 : 0;
-    if (adjoint) k_coarsest_prop<true><<<1, 256, sm ? gbytes : 0, s>>>(cv, f, x, scratch, sm);
-    else k_coarsest_prop<false><<<1, 256, sm ? gbytes : 0, s>>>(cv, f, x, scratch, sm);
+    if (adjoint) pdl_launch(k_coarsest_prop<true>, 1, 256, sm ? gbytes : 0, s, cv, f, x, scratch, sm);
+    else pdl_launch(k_coarsest_prop<false>, 1, 256, sm ? gbytes : 0, s, cv, f, x, scratch, sm);
     return check_launch();
   }
   if (cv.m <= 32) {
-    if (adjoint) k_coarsest_warp<true><<<1, 32, 0, s>>>(cv, f, x);
-    else k_coarsest_warp<false><<<1, 32, 0, s>>>(cv, f, x);
+    if (adjoint) pdl_launch(k_coarsest_warp<true>, 1, 32, 0, s, cv, f, x);
+    else pdl_launch(k_coarsest_warp<false>, 1, 32, 0, s, cv, f, x);
     return check_launch();
   }
   const size_t smem = sizeof(double) * 2 * (size_t)cv.m;
@@ -1886,8 +2109,8 @@ int launch_coarsest(bool adjoint, const CoarsestView& cv, const double* f, doubl
   int threads = cv.m >= 1024 ? 1024 : (int)((cv.m + 31) / 32 * 32);
   if (threads < 32) threads = 32;
   const size_t dyn = use_smem ? smem : 0;
-  if (adjoint) k_coarsest<true><<<1, threads, dyn, s>>>(cv, f, x, scratch, use_smem);
-  else k_coarsest<false><<<1, threads, dyn, s>>>(cv, f, x, scratch, use_smem);
+  if (adjoint) pdl_launch(k_coarsest<true>, 1, threads, dyn, s, cv, f, x, scratch, use_smem);
+  else pdl_launch(k_coarsest<false>, 1, threads, dyn, s, cv, f, x, scratch, use_smem);
   return check_launch();
 }
 
@@ -1896,6 +2119,7 @@ int kernels_init() {
   if (!env_read) {  // STMG_KERNEL_VARIANT lets the test suite exercise every design
     env_read = true;
     if (const char* v = std::getenv("STMG_KERNEL_VARIANT")) set_kernel_variant(std::atoi(v));
+    if (const char* v = std::getenv("STMG_PDL")) g_pdl = std::atoi(v) != 0;
   }
   // The coarsest march keeps its two PCR work vectors in shared memory up to 160 KB.
   cudaError_t e = cudaFuncSetAttribute(k_coarsest<true>,
@@ -1916,10 +2140,14 @@ int kernels_init() {
   e = cudaFuncSetAttribute(k_coarsest_chunked<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            160 * 1024);
   if (e != cudaSuccess) return static_cast<int>(e);
-  for (auto fn : {k_tail<true>, k_tail<false>}) {
+  for (auto fn : {k_tail<true, ClusterScope>, k_tail<false, ClusterScope>}) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     if (e != cudaSuccess) return static_cast<int>(e);
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  for (auto fn : {k_tail<true, GridScope>, k_tail<false, GridScope>}) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     if (e != cudaSuccess) return static_cast<int>(e);
   }
   return 0;
@@ -1931,51 +2159,81 @@ bool tail_supported(const CoarsestView& cv) {
   return bytes <= 160 * 1024;
 }
 
+int tail_grid_blocks(const TailParams& p) {
+  const size_t smem = sizeof(double) * 32 * ((size_t)p.cv.lv.n_t + 2 * (size_t)p.cv.n_chunks + 1);
+  int per_sm = 0, dev = 0, sms = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail<false, GridScope>, kMaxTW, smem) != cudaSuccess)
+    return 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return 0;
+  return per_sm * sms;
+}
+
 int launch_tail(bool adjoint, const TailParams& p, int cluster, int* final_buf, cudaStream_t s) {
   if (p.nu < 1 || p.n_levels < 1 || p.n_levels > kTailMaxLevels || !tail_supported(p.cv)) return 1;
   const size_t smem = sizeof(double) * 32 * ((size_t)p.cv.lv.n_t + 2 * (size_t)p.cv.n_chunks + 1);
+  int c = (p.nu - 1) & 1;  // result buffer of tail level 0: from-zero sweep -> 0, nu-1 flips, nu flips up
+  if (p.n_levels > 1) c = (c + p.nu) & 1;
+  else c = 0;
+  if (final_buf) *final_buf = c;
+  if (cluster <= 0) {  // whole-grid cooperative launch, every CTA co-resident
+    const int blocks = tail_grid_blocks(p);
+    if (blocks < 1) return 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(kMaxTW);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = adjoint ? cudaLaunchKernelEx(&cfg, k_tail<true, GridScope>, p)
+                                  : cudaLaunchKernelEx(&cfg, k_tail<false, GridScope>, p);
+    return static_cast<int>(e);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)cluster);
   cfg.blockDim = dim3(kMaxTW);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = (unsigned)cluster;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaError_t e = adjoint ? cudaLaunchKernelEx(&cfg, k_tail<true>, p) : cudaLaunchKernelEx(&cfg, k_tail<false>, p);
-  // result buffer of tail level 0: from-zero sweep -> 0, nu-1 flips, nu flips up
-  int c = (p.nu - 1) & 1;
-  if (p.n_levels > 1) c = (c + p.nu) & 1;
-  else c = 0;
-  if (final_buf) *final_buf = c;
+  cfg.numAttrs = g_pdl ? 2 : 1;
+  const cudaError_t e = adjoint ? cudaLaunchKernelEx(&cfg, k_tail<true, ClusterScope>, p)
+                                : cudaLaunchKernelEx(&cfg, k_tail<false, ClusterScope>, p);
   return static_cast<int>(e);
 }
 
 int launch_finalize_sum(const double* partials, int64_t n, double* out, cudaStream_t s) {
-  k_finalize_sum<<<1, 1024, 0, s>>>(partials, n, out);
+  pdl_launch(k_finalize_sum, 1, 1024, 0, s, partials, n, out);
   return check_launch();
 }
 
 int launch_sensitivities(int64_t n_el, int64_t n_t, double dt, const double* dk_dx,
                          const double* dc_dx6, const double* u, const double* lam, double* sens,
                          cudaStream_t s) {
-  k_sensitivities<<<(unsigned)((n_el + 127) / 128), 128, 0, s>>>(n_el, n_t, dt, dk_dx, dc_dx6, u, lam, sens);
+  pdl_launch(k_sensitivities, (unsigned)((n_el + 127) / 128), 128, 0, s, n_el, n_t, dt, dk_dx, dc_dx6, u, lam, sens);
   return check_launch();
 }
 
 int launch_dot(const double* x, const double* y, int64_t n, double* partials, int64_t* n_partials,
                cudaStream_t s) {
-  k_dot<<<kSumGrid, 256, 0, s>>>(x, y, n, partials);
+  pdl_launch(k_dot, kSumGrid, 256, 0, s, x, y, n, partials);
   if (n_partials) *n_partials = kSumGrid;
   return check_launch();
 }
 
 int launch_sumsq(const double* x, int64_t n, double* partials, int64_t* n_partials, cudaStream_t s) {
-  k_sumsq<<<kSumGrid, 256, 0, s>>>(x, n, partials);
+  pdl_launch(k_sumsq, kSumGrid, 256, 0, s, x, n, partials);
   if (n_partials) *n_partials = kSumGrid;
   return check_launch();
 }

@@ -235,14 +235,19 @@ def test_adjoint_shares_workspace_with_primal(torch, S, port):
         check_solve(rep, lam, *reversed(hp_adj.solve(c, nu=2, tol=1e-10, max_cycles=20)))
 
 
-def test_coarse_tail_cluster_kernel_is_bitwise(torch, S, port, monkeypatch):
-    """The opt-in coarse-tail cluster kernel (STMG_TAIL_DOFS) gives the same
-    iterate bit for bit as the per-level launches."""
-    cs = case("cfg1_mini")
+@pytest.mark.parametrize("scope", ["0", "16"])
+@pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "time_first"])
+def test_coarse_tail_kernel_is_bitwise(torch, S, port, monkeypatch, name, scope):
+    """The persistent coarse-tail kernel (STMG_TAIL_DOFS; grid-wide cooperative
+    launch for scope 0, one 16-CTA cluster otherwise) gives the same iterate
+    bit for bit as the per-level launches."""
+    cs = case(name)
     b = cs.rhs_vector(port)
     opts = S.SolveOptions(nu=cs.nu, tol=cs.tol)
+    monkeypatch.setenv("STMG_TAIL_DOFS", "0")
     u0 = np.zeros_like(b)
     r0 = S.mg_solve(gpu_hier(S, cs, port), b, u0, opts)
+    monkeypatch.setenv("STMG_TAIL_CLUSTER", scope)
     monkeypatch.setenv("STMG_TAIL_DOFS", "20000")
     u1 = np.zeros_like(b)
     r1 = S.mg_solve(gpu_hier(S, cs, port), b, u1, opts)
