@@ -345,6 +345,8 @@ def main():
     ap.add_argument("--ref-cores", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--hbm-roofline", type=int, default=1)
+    ap.add_argument("--profile-steps", type=int, default=3,
+                    help="extra solves with in-graph kernel timers (roofline), after the timed steps")
     ap.add_argument("--dist", action="store_true",
                     help="use the time-slab (NCCL) path even at N=1 (smoke test of that path)")
     args = ap.parse_args()
@@ -424,9 +426,6 @@ def main():
 
     for _ in range(args.warmup):
         rep = one_solve()
-    if h is not None:
-        h.set_profiling(True)
-    rep = one_solve()  # capture the profiled graph outside the timed region
     # L2 flush buffer (> 126 MB L2): written between timed steps, outside the events
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
     torch.cuda.synchronize(dev)
@@ -448,7 +447,25 @@ def main():
             step_ms.append(e0.elapsed_time(e1))
     torch.cuda.synchronize(dev)
     barrier()
-    if h is not None:
+    # Kernel-level timing (roofline): the same solves again with CUDA event
+    # nodes around the fine-level kernels inside the graph.  Kept out of the
+    # timed steps above: each event node adds launch-gap overhead (~10 us per
+    # bracketed kernel when every level is profiled).
+    prof_reps, prof_ms = [], []
+    if h is not None and args.profile_steps > 0:
+        h.set_profiling(True)
+        one_solve()  # capture the profiled graph
+        for _ in range(args.profile_steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(1.0)
+                u_dev.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            prof_reps.append(solve_on(b_dev, u_dev))
+            e1.record(stream)
+            e1.synchronize()
+            prof_ms.append(e0.elapsed_time(e1))
         h.set_profiling(False)
     ms = sum(step_ms)
     updates = sum(r.smoother_dof_updates for r in reps)
@@ -472,7 +489,7 @@ def main():
 
     def tot(key):
         c, t_ = 0, 0.0
-        for r in reps:
+        for r in prof_reps:
             cc, ss = r.kernel_times.get(key, (0, 0.0))
             c += cc
             t_ += ss
@@ -495,7 +512,7 @@ def main():
     kt = {}
     for key in ("fine_sweep", "fine_sweep_pair", "fine_restrict", "fine_prolong_sweep"):
         c, s_ = 0, 0.0
-        for r in reps:
+        for r in prof_reps:
             cc, ss = r.kernel_times.get(key, (0, 0.0))
             c += cc
             s_ += ss
@@ -503,8 +520,10 @@ def main():
             kt[key] = {"launches": c, "avg_ms": 1e3 * s_ / c}
     step_ms_avg = t_max / max(args.steps, 1)
     if kt:
+        kt["profiled_steps"] = len(prof_ms)
+        kt["profiled_ms_per_step"] = sum(prof_ms) / len(prof_ms)
         kt["fine_share_of_step"] = sum(v["launches"] * v["avg_ms"] for v in kt.values()
-                                       if isinstance(v, dict)) / max(t_max, 1e-9)
+                                       if isinstance(v, dict)) / max(sum(prof_ms), 1e-9)
 
     # e2e through the C ABI with pinned host buffers
     e2e = None

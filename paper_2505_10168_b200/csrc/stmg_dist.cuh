@@ -465,6 +465,7 @@ void dist_build(stmg_dist* d, int world, int rank, const void* nccl_id, int64_t 
     auto buf = std::make_unique<DeviceBuf>(static_cast<int64_t>(t.size()));
     cuda_check(cudaMemcpy(buf->p, t.data(), t.size() * 8, cudaMemcpyHostToDevice), "coef upload");
     LevelView v{hl.g.n_el, hl.g.n_t, hl.g.n_el + 1, hl.w, hl.inv_w, buf->p, 0, hl.g.n_t + 1};
+    v.tile_nt = tile_nt_for(v.nn * (v.n_t + 1));
     d->full_views.push_back(v);
     d->device_bytes += static_cast<int64_t>(t.size() * 8);
     d->coef.push_back(std::move(buf));

@@ -607,6 +607,16 @@ void build_pcr(stmg_hierarchy* h) {
   h->device_bytes += static_cast<int64_t>((alpha.size() * 2 + b.size()) * 8);
 }
 
+// Levels with at most this many DOFs use 4-level time tiles in the stencil
+// kernels (shorter serial chains where a launch is latency-bound).
+// STMG_SMALL_NT_DOFS overrides; read when a hierarchy is built.
+constexpr int64_t kSmallNtDofs = 2500000;  // measured: cfg1 solve 66.2 -> 57.7 ms (profiles/round1.md)
+int64_t tile_nt_for(int64_t dofs) {
+  int64_t lim = kSmallNtDofs;
+  if (const char* v = std::getenv("STMG_SMALL_NT_DOFS")) lim = std::atoll(v);
+  return dofs <= lim ? 4 : 8;
+}
+
 void upload_levels(stmg_hierarchy* h) {
   h->coef.clear();
   h->views.clear();
@@ -623,6 +633,7 @@ void upload_levels(stmg_hierarchy* h) {
     v.coef = buf->p;
     v.n_lo = 0;
     v.n_hi = hl.g.n_t + 1;
+    v.tile_nt = tile_nt_for(v.nn * (v.n_t + 1));
     h->views.push_back(v);
     h->device_bytes += static_cast<int64_t>(t.size() * 8);
     h->coef.push_back(std::move(buf));
@@ -675,6 +686,9 @@ void finish_create(stmg_hierarchy* h, bool share_ws_from_other, const stmg_hiera
     }
   }
   if (share_ws_from_other) {
+    // same tiling as the hierarchy whose workspace (norm partials) is shared
+    for (size_t l = 0; l < h->views.size() && l < other->views.size(); ++l)
+      h->views[l].tile_nt = other->views[l].tile_nt;
     h->ws = other->ws;
   } else {
     int64_t bytes = 0;

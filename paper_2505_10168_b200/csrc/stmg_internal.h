@@ -26,6 +26,9 @@ struct LevelView {
   // stay full-size and globally indexed; only the slab is read and written).
   int64_t n_lo;
   int64_t n_hi;
+  // Time levels per tile of the overlapping-warp kernels (8, or 4 on small,
+  // latency-bound levels); fixed when the hierarchy is built.
+  int64_t tile_nt = 8;
 };
 
 inline bool full_range(const LevelView& L) { return L.n_lo == 0 && L.n_hi == L.n_t + 1; }

@@ -1864,6 +1864,7 @@ constexpr int kNumSMs = 148;
 constexpr int kDefaultVariant = 5;
 int g_variant = kDefaultVariant;
 
+inline int64_t rows(const LevelView& L) { return L.n_hi - L.n_lo; }
 inline dim3 march_block(const LevelView& L) {
   int tw = L.nn >= kMaxTW ? kMaxTW : (int)((L.nn + 31) / 32 * 32);
   return dim3(tw);
@@ -1878,11 +1879,19 @@ inline int64_t stream_chunk(const LevelView& L, dim3 blk) {
   return chunk;
 }
 inline int variant_nt(int v) { return (v == 1 || v == 2) ? 4 : v == 6 ? 16 : 8; }
+// Overlapping-warp kernels: warps per block chosen so that the node tiles cover
+// the level evenly (<= 8 warps per block).  E.g. 257 nodes -> 2 blocks of 5
+// warps, not one full and one almost empty block of 8.
+inline dim3 balanced_block(int64_t warps) {
+  if (warps < 1) warps = 1;
+  const int64_t bx = (warps + 7) / 8;
+  return dim3((unsigned)(32 * ((warps + bx - 1) / bx)));
+}
+inline int lean_nt(const LevelView& L) { return L.tile_nt == 4 ? 4 : 8; }
 inline int64_t lean2_tiles(const LevelView& L, dim3 blk) {
   const int64_t per = (int64_t)(blk.x / 32) * 30;
   return (L.nn + per - 1) / per;
 }
-inline int64_t rows(const LevelView& L) { return L.n_hi - L.n_lo; }
 // Sub-range (slab) launches always use the production design.
 inline int eff_variant(const LevelView& L) { return full_range(L) ? g_variant : kDefaultVariant; }
 // time tiles on (y, z): tile = z * gridDim.y + y (gridDim.y <= 65535)
@@ -1891,9 +1900,12 @@ inline dim3 tgrid(int64_t x, int64_t t) {
   const int64_t y = t < 65535 ? t : 65535;
   return dim3((unsigned)x, (unsigned)y, (unsigned)((t + y - 1) / y));
 }
+inline dim3 pass_block(const LevelView& L, int v) {
+  return (v == 5 || v == 6) ? balanced_block((L.nn + 29) / 30) : march_block(L);
+}
 inline dim3 grid_for(const LevelView& L, dim3 blk, int v) {
   if (v == 5 || v == 6) {
-    const int nt = variant_nt(v);
+    const int nt = v == 5 ? lean_nt(L) : 16;
     return tgrid(lean2_tiles(L, blk), (rows(L) + nt - 1) / nt);
   }
   const unsigned tiles = (unsigned)((L.nn + blk.x - 1) / blk.x);
@@ -1911,7 +1923,7 @@ template <bool ADJ, int MODE, bool NORM, class Ld>
 void launch_pass(const LevelView& L, const Ld& ld, const double* f, double* y, double omega,
                  double* partials, cudaStream_t s) {
   const int v = eff_variant(L);
-  const dim3 blk = march_block(L), grd = grid_for(L, blk, v);
+  const dim3 blk = pass_block(L, v), grd = grid_for(L, blk, v);
   switch (v) {
     case 1:
       pdl_launch(k_lean<ADJ, MODE, NORM, 4, 3, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
@@ -1926,7 +1938,10 @@ void launch_pass(const LevelView& L, const Ld& ld, const double* f, double* y, d
       pdl_launch(k_tile<ADJ, MODE, NORM, 8, 2, Ld>, grd, blk, tile_smem(blk, 8, 2), s, L, ld, f, y, omega, partials);
       break;
     case 5:
-      pdl_launch(k_lean2<ADJ, MODE, NORM, 8, 3, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
+      if (lean_nt(L) == 4)
+        pdl_launch(k_lean2<ADJ, MODE, NORM, 4, 3, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
+      else
+        pdl_launch(k_lean2<ADJ, MODE, NORM, 8, 3, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
       break;
     case 6:
       pdl_launch(k_lean2<ADJ, MODE, NORM, 16, 2, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
@@ -1963,11 +1978,14 @@ int restrict_tile_impl(const LevelView& F, const LevelView& C, const double* f, 
   const dim3 blk = march_block(F);
   const int v = eff_variant(F);
   if (v == 5 || v == 6) {
-    constexpr int NT = 8;
-    const int64_t per = (int64_t)(blk.x / 32) * (DIR == 0 ? 28 : 30);
-    // DIR 0: warp w owns coarse nodes 14 w .. 14 w + 13
-    const int64_t tiles = DIR == 0 ? ceil_div(ceil_div(C.nn, 14), blk.x / 32) : ceil_div(F.nn, per);
-    pdl_launch(k_restrict2<ADJ, DIR, NT>, tgrid(tiles, (rows(F) + NT - 1) / NT), blk, 0, s, F, C, f, x, fc);
+    // DIR 0: warp w owns coarse nodes 14 w .. 14 w + 13; DIR 1: fine nodes 30 w ..
+    const int64_t warps = DIR == 0 ? ceil_div(C.nn, 14) : ceil_div(F.nn, 30);
+    const dim3 rb = balanced_block(warps);
+    const int64_t tiles = ceil_div(warps, rb.x / 32);
+    if (lean_nt(F) == 4)
+      pdl_launch(k_restrict2<ADJ, DIR, 4>, tgrid(tiles, (rows(F) + 3) / 4), rb, 0, s, F, C, f, x, fc);
+    else
+      pdl_launch(k_restrict2<ADJ, DIR, 8>, tgrid(tiles, (rows(F) + 7) / 8), rb, 0, s, F, C, f, x, fc);
     return check_launch();
   }
   if (v == 0 || v == 1) {
@@ -1993,8 +2011,7 @@ int restrict_tile_impl(const LevelView& F, const LevelView& C, const double* f, 
 
 int64_t sweep_partials_needed(const LevelView& L) {
   // the largest grid any variant launches for this level
-  const dim3 blk = march_block(L);
-  const dim3 g1 = grid_for(L, blk, 1), g5 = grid_for(L, blk, 5);
+  const dim3 g1 = grid_for(L, march_block(L), 1), g5 = grid_for(L, pass_block(L, 5), 5);
   const int64_t a = (int64_t)g1.x * g1.y * g1.z, b = (int64_t)g5.x * g5.y * g5.z;
   return a > b ? a : b;
 }
@@ -2007,7 +2024,8 @@ int64_t sumsq_partials_needed(int64_t) { return kSumGrid; }
 int launch_sweep(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
                  double omega, double* partials, int64_t* n_partials, cudaStream_t s) {
   if (n_partials) {
-    const dim3 blk = march_block(L), grd = grid_for(L, blk, eff_variant(L));
+    const int v = eff_variant(L);
+    const dim3 grd = grid_for(L, pass_block(L, v), v);
     *n_partials = (int64_t)grd.x * grd.y * grd.z;
   }
   return adjoint ? sweep_impl<true>(L, f, x, y, omega, partials, s)
@@ -2016,13 +2034,18 @@ int launch_sweep(bool adjoint, const LevelView& L, const double* f, const double
 
 int launch_sweep2(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
                   double omega, cudaStream_t s) {
-  constexpr int NT = 8;
-  const dim3 blk = march_block(L);
-  const int64_t per = (int64_t)(blk.x / 32) * 28;
-  const int64_t tiles = (L.nn + per - 1) / per;
-  const dim3 grd = tgrid(tiles, (rows(L) + NT - 1) / NT);
-  if (adjoint) pdl_launch(k_lean2x2<true, NT>, grd, blk, 0, s, L, f, x, y, omega);
-  else pdl_launch(k_lean2x2<false, NT>, grd, blk, 0, s, L, f, x, y, omega);
+  const int64_t warps = ceil_div(L.nn, 28);
+  const dim3 blk = balanced_block(warps);
+  const int64_t tiles = ceil_div(warps, blk.x / 32);
+  if (lean_nt(L) == 4) {
+    const dim3 grd = tgrid(tiles, (rows(L) + 3) / 4);
+    if (adjoint) pdl_launch(k_lean2x2<true, 4>, grd, blk, 0, s, L, f, x, y, omega);
+    else pdl_launch(k_lean2x2<false, 4>, grd, blk, 0, s, L, f, x, y, omega);
+  } else {
+    const dim3 grd = tgrid(tiles, (rows(L) + 7) / 8);
+    if (adjoint) pdl_launch(k_lean2x2<true, 8>, grd, blk, 0, s, L, f, x, y, omega);
+    else pdl_launch(k_lean2x2<false, 8>, grd, blk, 0, s, L, f, x, y, omega);
+  }
   return check_launch();
 }
 

@@ -272,3 +272,32 @@ def test_sweep_kernel_forms_bitwise(torch, S, port, name):
             h.sweep_kernels(l, ft, xt, yt, launches, pairs)
             torch.cuda.synchronize()
             assert np.array_equal(bits(xt), bits(want)), (l, pairs)
+
+
+@pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "time_first", "wide_short", "cfg0_deep"])
+def test_short_time_tiles_bitwise(torch, S, port, monkeypatch, name):
+    """4-level time tiles (STMG_SMALL_NT_DOFS, used on small latency-bound
+    levels) on every level: kernels bit-identical to the oracle, solve parity."""
+    monkeypatch.setenv("STMG_SMALL_NT_DOFS", str(10 ** 15))
+    cs = case(name)
+    h = gpu_hier(S, cs, port)
+    hp = port_hier(port, cs)
+    rng = np.random.default_rng(17)
+    dev = torch.device("cuda:0")
+    for l in range(h.n_levels() - 1):
+        n = hp.ndofs(l)
+        x, f = special_values(rng, n), special_values(rng, n)
+        xt, ft = torch.from_numpy(x).to(dev), torch.from_numpy(f).to(dev)
+        for pairs, launches in ((False, 4), (True, 2)):
+            xs, ys = xt.clone(), torch.empty_like(xt)
+            h.sweep_kernels(l, ft, xs, ys, launches, pairs)
+            torch.cuda.synchronize()
+            assert np.array_equal(bits(xs), bits(hp.sweeps(l, f, x, 4))), (l, pairs)
+        fc = torch.empty(hp.ndofs(l + 1), dtype=torch.float64, device=dev)
+        h.restrict_residual(l, ft, xt, fc)
+        assert np.array_equal(bits(fc), bits(hp.restrict(l, hp.residual(l, f, x)))), l
+    b = cs.rhs_vector(port)
+    u_p, rep_p = hp.solve(b, nu=cs.nu, tol=cs.tol, max_cycles=cs.max_cycles)
+    u = np.zeros_like(b)
+    rep = S.mg_solve(h, b, u, S.SolveOptions(nu=cs.nu, tol=cs.tol, max_cycles=cs.max_cycles))
+    check_solve(rep, u, rep_p, u_p)
