@@ -558,10 +558,19 @@ void build_pcr(stmg_hierarchy* h) {
         for (int q = 0; q < m; ++q) acc += Ti[j * 32 + q] * S[q * 32 + k];
         A[j * 32 + k] = -acc;
       }
+    // device copies are column-major (element (j, k) at k * 32 + j): lane j
+    // loads its row with 32 coalesced loads
+    auto colmajor = [](const std::vector<double>& M) {
+      std::vector<double> T(32 * 32);
+      for (int j = 0; j < 32; ++j)
+        for (int k = 0; k < 32; ++k) T[k * 32 + j] = M[j * 32 + k];
+      return T;
+    };
+    const std::vector<double> TiT = colmajor(Ti), AT = colmajor(A);
     h->prop_tinv = std::make_unique<DeviceBuf>(32 * 32);
     h->prop_a = std::make_unique<DeviceBuf>(32 * 32);
-    cuda_check(cudaMemcpy(h->prop_tinv->p, Ti.data(), Ti.size() * 8, cudaMemcpyHostToDevice), "tinv");
-    cuda_check(cudaMemcpy(h->prop_a->p, A.data(), A.size() * 8, cudaMemcpyHostToDevice), "prop");
+    cuda_check(cudaMemcpy(h->prop_tinv->p, TiT.data(), TiT.size() * 8, cudaMemcpyHostToDevice), "tinv");
+    cuda_check(cudaMemcpy(h->prop_a->p, AT.data(), AT.size() * 8, cudaMemcpyHostToDevice), "prop");
     h->coarsest.tinv = h->prop_tinv->p;
     h->coarsest.prop = h->prop_a->p;
     h->device_bytes += 2 * 32 * 32 * 8;
@@ -591,7 +600,8 @@ void build_pcr(stmg_hierarchy* h) {
         P = T2;
       }
       h->prop_chunk = std::make_unique<DeviceBuf>(32 * 32);
-      cuda_check(cudaMemcpy(h->prop_chunk->p, R.data(), R.size() * 8, cudaMemcpyHostToDevice), "prop^L");
+      const std::vector<double> RT = colmajor(R);
+      cuda_check(cudaMemcpy(h->prop_chunk->p, RT.data(), RT.size() * 8, cudaMemcpyHostToDevice), "prop^L");
       h->coarsest.prop_chunk = h->prop_chunk->p;
       h->coarsest.n_chunks = C;
       h->coarsest.chunk_len = static_cast<int32_t>(Lc);
@@ -605,6 +615,14 @@ void build_pcr(stmg_hierarchy* h) {
   h->coarsest.gamma = h->pcr_gamma->p;
   h->coarsest.bfin = h->pcr_bfin->p;
   h->device_bytes += static_cast<int64_t>((alpha.size() * 2 + b.size()) * 8);
+}
+
+// Level-API calls complete before returning, except while the caller is
+// capturing the stream into a CUDA graph (then the launch is only recorded).
+void sync_unless_capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cuda_check(cudaStreamIsCapturing(s, &st), "cudaStreamIsCapturing");
+  if (st == cudaStreamCaptureStatusNone) cuda_check(cudaStreamSynchronize(s), "sync");
 }
 
 // Levels with at most this many DOFs use 4-level time tiles in the stencil
@@ -1101,7 +1119,7 @@ std::vector<HostLevel> make_host_levels(const stmg_grid* g, const double* k, con
 void refresh_levels(stmg_hierarchy* h, std::vector<HostLevel> host) {
   if (host.size() != h->host.size()) throw std::logic_error("refresh_levels: level count changed");
   DeviceGuard dg(h->device);
-  cuda_check(cudaStreamSynchronize(h->stream), "sync");
+  sync_unless_capturing(h->stream);
   h->host = std::move(host);
   for (size_t l = 0; l < h->host.size(); ++l) {
     const HostLevel& hl = h->host[l];
@@ -1303,7 +1321,7 @@ void optimise(const stmg_grid* geom, const stmg_optimise_options& o, int device,
     launch_check(launch_finalize_sum(d_part.p, np, d_s.p, h->stream), "finalize");
     double dotbu = 0.0;
     cuda_check(cudaMemcpyAsync(&dotbu, d_s.p, 8, cudaMemcpyDeviceToHost, h->stream), "d2h");
-    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+    sync_unless_capturing(h->stream);
     const double theta = dotbu * g.dt / o.theta_ref;
     if (!o.warm_start) cuda_check(cudaMemset(d_lam.p, 0, ndof * 8), "memset");
     solve(ht.get(), d_c.p, d_lam.p, o.solve, &ar, hist.data(), static_cast<int32_t>(hist.size()));
@@ -1350,7 +1368,7 @@ void optimise(const stmg_grid* geom, const stmg_optimise_options& o, int device,
     launch_check(launch_sensitivities(ne, g.n_t, g.dt, d_dk.p, d_dc.p, d_u.p, d_lam.p, d_sens.p, h->stream),
                  "sensitivities");
     cuda_check(cudaMemcpyAsync(sens.data(), d_sens.p, ne * 8, cudaMemcpyDeviceToHost, h->stream), "d2h");
-    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+    sync_unless_capturing(h->stream);
     chi = mma.update(chi, sens, dg, g_val);
   }
   std::memcpy(chi_out, chi.data(), sizeof(double) * static_cast<size_t>(ne));
@@ -1496,7 +1514,7 @@ int stmg_hierarchy_set_stream(stmg_hierarchy* h, void* cuda_stream) {
   return guarded([&] {
     checked(h);
     DeviceGuard dg(h->device);
-    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+    sync_unless_capturing(h->stream);
     h->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : h->own_stream;
   });
 }
@@ -1564,7 +1582,7 @@ int stmg_level_sweeps(stmg_hierarchy* h, int32_t l, const double* f, double* x, 
     }
     if (a != x)
       cuda_check(cudaMemcpyAsync(x, a, sizeof(double) * h->ndofs(l), cudaMemcpyDeviceToDevice, h->stream), "copy");
-    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+    sync_unless_capturing(h->stream);
   });
 }
 
@@ -1593,7 +1611,7 @@ int stmg_level_residual(stmg_hierarchy* h, int32_t l, const double* f, const dou
     check_level(h, l);
     DeviceGuard dg(h->device);
     launch_check(launch_residual(h->adjoint, h->views[l], f, x, r, h->stream), "residual");
-    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+    sync_unless_capturing(h->stream);
   });
 }
 
@@ -1607,7 +1625,7 @@ int stmg_level_restrict_residual(stmg_hierarchy* h, int32_t l, const double* f, 
     launch_check(launch_restrict_residual(h->adjoint, h->views[l], h->views[l + 1], h->dirs[l], f, x,
                                           fc, h->stream),
                  "restrict");
-    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+    sync_unless_capturing(h->stream);
   });
 }
 
@@ -1618,7 +1636,7 @@ int stmg_level_restrict(stmg_hierarchy* h, int32_t l, const double* r, double* f
     if (l + 1 >= h->n_levels()) throw std::out_of_range("no coarser level");
     DeviceGuard dg(h->device);
     launch_check(launch_restrict(h->views[l], h->views[l + 1], h->dirs[l], r, fc, h->stream), "restrict");
-    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+    sync_unless_capturing(h->stream);
   });
 }
 
@@ -1629,7 +1647,7 @@ int stmg_level_prolong_add(stmg_hierarchy* h, int32_t l, const double* xc, doubl
     if (l + 1 >= h->n_levels()) throw std::out_of_range("no coarser level");
     DeviceGuard dg(h->device);
     launch_check(launch_prolong_add(h->views[l], h->views[l + 1], h->dirs[l], xc, x, h->stream), "prolong");
-    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+    sync_unless_capturing(h->stream);
   });
 }
 
@@ -1639,7 +1657,7 @@ int stmg_coarsest_solve(stmg_hierarchy* h, const double* f, double* x) {
     DeviceGuard dg(h->device);
     launch_check(launch_coarsest(h->adjoint, h->coarsest, f, x, h->ws->coarse_scratch->p, h->stream),
                  "coarsest");
-    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+    sync_unless_capturing(h->stream);
   });
 }
 
@@ -1761,7 +1779,7 @@ int stmg_synchronize(stmg_hierarchy* h) {
   return guarded([&] {
     checked(h);
     DeviceGuard dg(h->device);
-    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+    sync_unless_capturing(h->stream);
   });
 }
 

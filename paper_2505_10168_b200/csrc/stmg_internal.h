@@ -45,7 +45,7 @@ struct CoarsestView {
   const double* gamma;  // n_steps * m
   const double* bfin;   // m, final diagonal after reduction
   // n_el <= 32: dense step inverse T^-1 and propagator A = -T^-1 S (32 x 32,
-  // row-major, zero-padded), for the parallel-RHS + propagator march
+  // column-major, zero-padded), for the parallel-RHS + propagator march
   const double* tinv;
   const double* prop;
   // chunked (parallel-in-time) march: n_t = n_chunks * chunk_len, A^chunk_len
@@ -53,6 +53,12 @@ struct CoarsestView {
   int32_t chunk_len;
   const double* prop_chunk;
 };
+
+// Shared memory of the chunked coarsest march: g (n_t x 32), chunk end and
+// start states (2 C + 1) x 32, one 32-double vector slot per warp (<= 16).
+inline size_t coarsest_chunked_smem(const CoarsestView& cv) {
+  return sizeof(double) * 32 * ((size_t)cv.lv.n_t + 2 * (size_t)cv.n_chunks + 1 + 16);
+}
 
 // The coarse tail of a V-cycle (levels [Lt, L), all small) executed by one
 // thread-block cluster: level 0 here is hierarchy level Lt (its f is the

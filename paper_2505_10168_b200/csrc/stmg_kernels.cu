@@ -1581,7 +1581,7 @@ __global__ void __launch_bounds__(256) k_coarsest_prop(CoarsestView cv, const do
   {
     double row[32];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) row[k] = cv.tinv[lane * 32 + k];
+    for (int k = 0; k < 32; ++k) row[k] = cv.tinv[k * 32 + lane];
     for (int64_t n = 1 + warp; n <= nt; n += nw) {
       const double fl = active ? f[n * nn + lane + 1] : 0.0;
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -1599,7 +1599,7 @@ __global__ void __launch_bounds__(256) k_coarsest_prop(CoarsestView cv, const do
   if (warp != 0) return;
   double arow[32];
 #pragma unroll
-  for (int k = 0; k < 32; ++k) arow[k] = cv.prop[lane * 32 + k];
+  for (int k = 0; k < 32; ++k) arow[k] = cv.prop[k * 32 + lane];
   double xprev = 0.0;
   double gq = g[((ADJ ? nt : 1) - 1) * 32 + lane];
   for (int64_t s = 1; s <= nt; ++s) {
@@ -1630,14 +1630,24 @@ __global__ void __launch_bounds__(256) k_coarsest_prop(CoarsestView cv, const do
 //   (3) warp 0: chunk start states s_{c+1} = e_c + A^Lc s_c (C steps);
 //   (4) warp c: chunk c again from s_c, writing x.
 // Sequential depth 2 Lc + C instead of n_t.  Same solution up to rounding.
-__device__ __forceinline__ double matvec32(const double (&row)[32], double v) {
+
+// Row `lane` of a 32 x 32 matrix (in registers) times v: four fused
+// multiply-add accumulators over k mod 4, v broadcast through a per-warp
+// shared slot (16 LDS.128).  The exact coarsest solve is not a bitwise-parity
+// kernel (the reference factorises with a sparse LU), so FMA is used here.
+__device__ __forceinline__ double matvec32s(const double (&row)[32], double v, double* vs) {
+  __syncwarp();
+  vs[threadIdx.x & 31] = v;
+  __syncwarp();
+  const double2* v2 = reinterpret_cast<const double2*>(vs);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
   for (int k = 0; k < 32; k += 4) {
-    a0 = a0 + row[k] * __shfl_sync(kFull, v, k);
-    a1 = a1 + row[k + 1] * __shfl_sync(kFull, v, k + 1);
-    a2 = a2 + row[k + 2] * __shfl_sync(kFull, v, k + 2);
-    a3 = a3 + row[k + 3] * __shfl_sync(kFull, v, k + 3);
+    const double2 p = v2[k / 2], q = v2[k / 2 + 1];
+    a0 = __fma_rn(row[k], p.x, a0);
+    a1 = __fma_rn(row[k + 1], p.y, a1);
+    a2 = __fma_rn(row[k + 2], q.x, a2);
+    a3 = __fma_rn(row[k + 3], q.y, a3);
   }
   return (a0 + a1) + (a2 + a3);
 }
@@ -1645,7 +1655,7 @@ __device__ __forceinline__ double matvec32(const double (&row)[32], double v) {
 template <bool ADJ>
 __device__ __forceinline__ void dev_coarsest_chunked(const CoarsestView& cv, const double* __restrict__ f,
                                                      double* __restrict__ x, double* sm) {
-  // sm: g: n_t x 32, e: C x 32, s: (C+1) x 32; every thread of the block calls this
+  // sm: coarsest_chunked_smem(cv) bytes; every thread of the block calls this
   const LevelView& L = cv.lv;
   const int m = cv.m;
   const int64_t nn = L.nn, nt = L.n_t;
@@ -1654,22 +1664,23 @@ __device__ __forceinline__ void dev_coarsest_chunked(const CoarsestView& cv, con
   double* g = sm;
   double* e = g + nt * 32;
   double* st = e + (int64_t)C * 32;
+  double* vs = st + (int64_t)(C + 1) * 32 + warp * 32;  // this warp's vector slot
   for (int64_t k = threadIdx.x; k < nn; k += blockDim.x) x[k] = f[k] / L.w;
   for (int64_t n = 1 + threadIdx.x; n <= nt; n += blockDim.x) x[n * nn] = f[n * nn] / L.w;
   const bool active = lane < m;
   {
     double row[32];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) row[k] = cv.tinv[lane * 32 + k];
+    for (int k = 0; k < 32; ++k) row[k] = cv.tinv[k * 32 + lane];
     for (int64_t n = 1 + warp; n <= nt; n += nw) {
       const double fl = active ? f[n * nn + lane + 1] : 0.0;
-      g[(n - 1) * 32 + lane] = matvec32(row, fl);
+      g[(n - 1) * 32 + lane] = matvec32s(row, fl, vs);
     }
   }
   __syncthreads();
   double arow[32];
 #pragma unroll
-  for (int k = 0; k < 32; ++k) arow[k] = cv.prop[lane * 32 + k];
+  for (int k = 0; k < 32; ++k) arow[k] = cv.prop[k * 32 + lane];
   // step s = 1..nt in march order; level n(s) = s (J) or nt + 1 - s (J^T)
   auto level_of = [&](int64_t s) -> int64_t { return ADJ ? nt + 1 - s : s; };
   for (int c = warp; c < C; c += nw) {  // (2) zero-start chunk solves
@@ -1677,7 +1688,7 @@ __device__ __forceinline__ void dev_coarsest_chunked(const CoarsestView& cv, con
     for (int j = 0; j < Lc; ++j) {
       const int64_t s = (int64_t)c * Lc + j + 1;
       const double gn = g[(level_of(s) - 1) * 32 + lane];
-      xv = (j == 0) ? gn : gn + matvec32(arow, xv);
+      xv = (j == 0) ? gn : gn + matvec32s(arow, xv, vs);
     }
     e[c * 32 + lane] = xv;
   }
@@ -1685,11 +1696,11 @@ __device__ __forceinline__ void dev_coarsest_chunked(const CoarsestView& cv, con
   if (warp == 0) {  // (3) chunk start states
     double prow[32];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) prow[k] = cv.prop_chunk[lane * 32 + k];
+    for (int k = 0; k < 32; ++k) prow[k] = cv.prop_chunk[k * 32 + lane];
     double sv = 0.0;
     st[lane] = 0.0;
     for (int c = 0; c < C; ++c) {
-      sv = (c == 0) ? e[lane] : e[c * 32 + lane] + matvec32(prow, sv);
+      sv = (c == 0) ? e[lane] : e[c * 32 + lane] + matvec32s(prow, sv, vs);
       st[(c + 1) * 32 + lane] = sv;
     }
   }
@@ -1700,7 +1711,7 @@ __device__ __forceinline__ void dev_coarsest_chunked(const CoarsestView& cv, con
       const int64_t s = (int64_t)c * Lc + j + 1;
       const int64_t n = level_of(s);
       const double gn = g[(n - 1) * 32 + lane];
-      xv = (s == 1) ? gn : gn + matvec32(arow, xv);
+      xv = (s == 1) ? gn : gn + matvec32s(arow, xv, vs);
       if (active) x[n * nn + lane + 1] = xv;
     }
   }
@@ -2107,7 +2118,7 @@ int launch_prolong_add(const LevelView& F, const LevelView& C, int dir, const do
 int launch_coarsest(bool adjoint, const CoarsestView& cv, const double* f, double* x,
                     double* scratch, cudaStream_t s) {
   if (cv.m <= 32 && cv.prop_chunk != nullptr && cv.n_chunks > 1) {
-    const size_t bytes = sizeof(double) * 32 * ((size_t)cv.lv.n_t + 2 * (size_t)cv.n_chunks + 1);
+    const size_t bytes = coarsest_chunked_smem(cv);
     if (bytes <= 160 * 1024) {
       const int threads = 32 * (cv.n_chunks < 16 ? cv.n_chunks : 16);
       if (adjoint) pdl_launch(k_coarsest_chunked<true>, 1, threads, bytes, s, cv, f, x);
@@ -2178,12 +2189,12 @@ int kernels_init() {
 
 bool tail_supported(const CoarsestView& cv) {
   if (!(cv.m <= 32 && cv.prop_chunk != nullptr && cv.n_chunks > 1)) return false;
-  const size_t bytes = sizeof(double) * 32 * ((size_t)cv.lv.n_t + 2 * (size_t)cv.n_chunks + 1);
+  const size_t bytes = coarsest_chunked_smem(cv);
   return bytes <= 160 * 1024;
 }
 
 int tail_grid_blocks(const TailParams& p) {
-  const size_t smem = sizeof(double) * 32 * ((size_t)p.cv.lv.n_t + 2 * (size_t)p.cv.n_chunks + 1);
+  const size_t smem = coarsest_chunked_smem(p.cv);
   int per_sm = 0, dev = 0, sms = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tail<false, GridScope>, kMaxTW, smem) != cudaSuccess)
     return 0;
@@ -2195,7 +2206,7 @@ int tail_grid_blocks(const TailParams& p) {
 
 int launch_tail(bool adjoint, const TailParams& p, int cluster, int* final_buf, cudaStream_t s) {
   if (p.nu < 1 || p.n_levels < 1 || p.n_levels > kTailMaxLevels || !tail_supported(p.cv)) return 1;
-  const size_t smem = sizeof(double) * 32 * ((size_t)p.cv.lv.n_t + 2 * (size_t)p.cv.n_chunks + 1);
+  const size_t smem = coarsest_chunked_smem(p.cv);
   int c = (p.nu - 1) & 1;  // result buffer of tail level 0: from-zero sweep -> 0, nu-1 flips, nu flips up
   if (p.n_levels > 1) c = (c + p.nu) & 1;
   else c = 0;

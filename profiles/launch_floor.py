@@ -43,30 +43,47 @@ def main():
         y = torch.empty_like(x)
         row = {"level": l, "n_el": lv.n_el, "n_t": lv.n_t, "dofs": n}
         for name, pairs in (("sweep_us", False), ("pair_us", True)):
-            s = torch.cuda.Stream()
-            h.set_stream(s)
-            with torch.cuda.stream(s):
-                h.sweep_kernels(l, f, x, y, 2, pairs)  # warm (module load)
-            s.synchronize()
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, stream=s):  # captures on s, the hierarchy's stream
-                h.sweep_kernels(l, f, x, y, a.k, pairs)
-            h.set_stream(None)
-            graph.replay()
-            torch.cuda.synchronize()
-            best = None
-            for _ in range(a.reps):
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                graph.replay()
-                e1.record()
-                e1.synchronize()
-                t = e0.elapsed_time(e1) * 1e3 / a.k
-                best = t if best is None else min(best, t)
-            row[name] = round(best, 2)
-            del graph
+            row[name] = graph_time(h, lambda: h.sweep_kernels(l, f, x, y, a.k, pairs), a.k, a.reps)
+        nc = h.levels[l + 1].n_dofs
+        fc = torch.empty(nc, dtype=torch.float64, device="cuda")
+        row["restrict_us"] = graph_time(h, lambda: [h.restrict_residual(l, f, x, fc) for _ in range(a.k)],
+                                        a.k, a.reps)
         out.append(row)
         print(json.dumps(row), flush=True)
+    lv = h.levels[-1]
+    f = torch.randn(lv.n_dofs, dtype=torch.float64, device="cuda")
+    x = torch.zeros_like(f)
+    k = max(a.k // 10, 5)
+    print(json.dumps({"level": len(h.levels) - 1, "n_el": lv.n_el, "n_t": lv.n_t, "dofs": lv.n_dofs,
+                      "coarsest_us": graph_time(h, lambda: [h.coarsest_solve(f, x) for _ in range(k)], k,
+                                                a.reps)}), flush=True)
+
+
+def graph_time(h, body, k, reps):
+    """us per launch of `body` (k launches) captured into one CUDA graph on the hierarchy stream."""
+    import torch
+
+    s = torch.cuda.Stream()
+    h.set_stream(s)
+    with torch.cuda.stream(s):
+        body()
+    s.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        body()
+    h.set_stream(None)
+    graph.replay()
+    torch.cuda.synchronize()
+    best = None
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        graph.replay()
+        e1.record()
+        e1.synchronize()
+        t = e0.elapsed_time(e1) * 1e3 / k
+        best = t if best is None else min(best, t)
+    return round(best, 2)
 
 
 if __name__ == "__main__":
