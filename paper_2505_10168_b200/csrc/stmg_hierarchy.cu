@@ -780,7 +780,9 @@ struct Emitter {
   // Returns the buffer index (0 = xa, 1 = xb) holding the level's result.
   // start: buffer holding the current iterate; pre_done: sweeps already done;
   // from_zero: the iterate is identically zero (coarse levels).
-  int level(int l, int start, int pre_done, bool from_zero) {
+  // zero_done: the first sweep from zero was already written into buffer 0 by
+  // the parent's restriction (launch_restrict_residual with xc0).
+  int level(int l, int start, int pre_done, bool from_zero, bool zero_done = false) {
     const int nl = h->n_levels();
     const LevelView& L = h->views[l];
     double* f = h->ws->f[l]->p;
@@ -816,7 +818,9 @@ struct Emitter {
     int pre = nu - pre_done;
     if (from_zero) {
       cur = 0;
-      if (nu >= 1) {
+      if (nu >= 1 && zero_done) {
+        pre = nu - 1;
+      } else if (nu >= 1) {
         timed_launch(l, kTimedFromZero, [&] {
           launch_check(launch_sweep_from_zero(L, f, buf(l, 0), omega, s), "sweep0");
         });
@@ -829,13 +833,17 @@ struct Emitter {
     }
     smooth(l, f, cur, pre);
     const LevelView& C = h->views[l + 1];
+    // the child's first pre-smoothing sweep (from zero) is fused into this
+    // restriction unless the child is the coarsest level or the coarse tail
+    const bool fuse_zero = nu >= 1 && l + 1 < nl - 1 && l + 1 != h->tail_start;
     timed_launch(l, kTimedRestrict, [&] {
       launch_check(launch_restrict_residual(h->adjoint, L, C, h->dirs[l], f, buf(l, cur),
-                                            h->ws->f[l + 1]->p, s),
+                                            h->ws->f[l + 1]->p, s, fuse_zero ? buf(l + 1, 0) : nullptr,
+                                            omega),
                    "restrict");
     });
     ++kernels;
-    const int child = level(l + 1, 0, 0, true);
+    const int child = level(l + 1, 0, 0, true, fuse_zero);
     const double* xc = buf(l + 1, child);
     int post = nu;
     if (nu >= 1) {

@@ -97,8 +97,12 @@ int launch_sweep_prolong(bool adjoint, const LevelView& L, const LevelView& C, i
                          double omega, cudaStream_t s);
 int launch_residual(bool adjoint, const LevelView& L, const double* f, const double* x, double* r,
                     cudaStream_t s);
+// fc = R (f - J x).  If xc0 != nullptr, also the coarse level's first sweep
+// from a zero iterate, xc0 = 0 + omega (fc * inv_diag_c) (bitwise equal to
+// launch_sweep_from_zero on fc).
 int launch_restrict_residual(bool adjoint, const LevelView& F, const LevelView& C, int dir,
-                             const double* f, const double* x, double* fc, cudaStream_t s);
+                             const double* f, const double* x, double* fc, cudaStream_t s,
+                             double* xc0 = nullptr, double omega = 0.0);
 int launch_restrict(const LevelView& F, const LevelView& C, int dir, const double* r, double* fc,
                     cudaStream_t s);
 int launch_prolong_add(const LevelView& F, const LevelView& C, int dir, const double* xc, double* x,

@@ -809,10 +809,20 @@ __global__ void __launch_bounds__(kMaxTW, 2) k_lean_restrict(LevelView F, LevelV
 // node; warps advance 30 nodes (NT even, tiles start even).  Interior tiles
 // take a predicate-free path with the folded canonical orders; bitwise equal
 // to csr_spmv(R, r) of the stored fine residual (proj/src/multigrid.cpp:199).
+// First coarse sweep from a zero iterate, 0 + omega (f * inv_diag), at coarse
+// DOF (N, I) -- the dev_sweep_from_zero expression, fused into the restriction
+// that produces f.
+__device__ __forceinline__ double coarse_from_zero(const LevelView& C, int64_t N, int64_t I, double fv,
+                                                   double omega) {
+  const double id = (N == 0 || I == 0) ? C.inv_w : __ldg(C.coef + kInvD * C.nn + I);
+  return 0.0 + omega * (fv * id);
+}
+
 template <bool ADJ, int DIR, int NT>
 __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelView& C,
                                               const double* __restrict__ f, const double* __restrict__ x,
-                                              double* __restrict__ fc, int64_t tile, int64_t ttile, int tw) {
+                                              double* __restrict__ fc, int64_t tile, int64_t ttile, int tw,
+                                              double* __restrict__ xc0 = nullptr, double omega = 0.0) {
   if ((int)threadIdx.x >= tw) return;
   constexpr int kAdv = DIR == 0 ? 28 : 30;  // nodes per warp
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -834,6 +844,12 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
 #pragma unroll
     for (int r = 0; r <= NT; ++r) xr[r] = xp[r * nn];
     const Coefs c = load_coefs(F, i);
+    // coarse inverse diagonal at this lane's coarse node (first coarse sweep from zero)
+    double idc = 0.0;
+    if (xc0 != nullptr) {
+      const int64_t I = DIR == 0 ? base / 2 + lane : i;
+      if (DIR == 1 || (lane >= 1 && lane <= 14)) idc = __ldg(C.coef + kInvD * nnc + I);
+    }
     double pm = __shfl_up_sync(kFull, xr[0], 1), pp = __shfl_down_sync(kFull, xr[0], 1);
     double r_even = 0.0;
 #pragma unroll
@@ -848,13 +864,18 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
         const double rb = __shfl_sync(kFull, r, (src + 1) & 31);
         const double rc = __shfl_sync(kFull, r, (src + 2) & 31);
         // canonical ((0 + .5 ra) + (0 + rb)) + ((0 + .5 rc) + 0), folded (see row_interior)
-        if (lane >= 1 && lane <= 14)
-          fc[(n0 + k) * nnc + base / 2 + lane] = ((0.5 * ra + 1.0 * rb) + 0.5 * rc) + 0.0;
+        if (lane >= 1 && lane <= 14) {
+          const double v = ((0.5 * ra + 1.0 * rb) + 0.5 * rc) + 0.0;
+          fc[(n0 + k) * nnc + base / 2 + lane] = v;
+          if (xc0 != nullptr) xc0[(n0 + k) * nnc + base / 2 + lane] = 0.0 + omega * (v * idc);
+        }
       } else {
         if ((k & 1) == 0) {
           r_even = r;
         } else if (lane >= 1 && lane <= 30) {
-          fc[((n0 + k) >> 1) * nnc + i] = (0.5 * r_even + 0.5 * r) + 0.0;
+          const double v = (0.5 * r_even + 0.5 * r) + 0.0;
+          fc[((n0 + k) >> 1) * nnc + i] = v;
+          if (xc0 != nullptr) xc0[((n0 + k) >> 1) * nnc + i] = 0.0 + omega * (v * idc);
         }
       }
       pm = qm;
@@ -899,7 +920,9 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
         if (I >= 1) a.add(0.5 * ra);
         a.add(1.0 * rb);
         if (2 * I + 1 <= F.n_el) a.add(0.5 * rc);
-        fc[n * nnc + I] = a.result();
+        const double v = a.result();
+        fc[n * nnc + I] = v;
+        if (xc0 != nullptr) xc0[n * nnc + I] = coarse_from_zero(C, n, I, v, omega);
       }
     } else if (computes) {
       if ((k & 1) == 0) {
@@ -907,13 +930,17 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
         if (n == nt) {  // last coarse level: truncated row, 0.5 * r(2N) only
           Acc a;
           a.add(0.5 * r);
-          fc[(n >> 1) * nnc + i] = a.result();
+          const double v = a.result();
+          fc[(n >> 1) * nnc + i] = v;
+          if (xc0 != nullptr) xc0[(n >> 1) * nnc + i] = coarse_from_zero(C, n >> 1, i, v, omega);
         }
       } else {
         Acc a;
         a.add(0.5 * r_even);
         a.add(0.5 * r);
-        fc[(n >> 1) * nnc + i] = a.result();
+        const double v = a.result();
+        fc[(n >> 1) * nnc + i] = v;
+        if (xc0 != nullptr) xc0[(n >> 1) * nnc + i] = coarse_from_zero(C, n >> 1, i, v, omega);
       }
     }
     pm = qm;
@@ -923,10 +950,12 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
 
 template <bool ADJ, int DIR, int NT>
 __global__ void __launch_bounds__(kMaxTW, 3) k_restrict2(LevelView F, LevelView C, const double* __restrict__ f,
-                                                         const double* __restrict__ x, double* __restrict__ fc) {
+                                                         const double* __restrict__ x, double* __restrict__ fc,
+                                                         double* __restrict__ xc0, double omega) {
   pdl_entry();
   const int64_t tt = (int64_t)blockIdx.z * gridDim.y + blockIdx.y;
-  if (tt < ceil_div(F.n_hi - F.n_lo, NT)) dev_restrict2<ADJ, DIR, NT>(F, C, f, x, fc, blockIdx.x, tt, blockDim.x);
+  if (tt < ceil_div(F.n_hi - F.n_lo, NT))
+    dev_restrict2<ADJ, DIR, NT>(F, C, f, x, fc, blockIdx.x, tt, blockDim.x, xc0, omega);
 }
 
 // Elementwise kernels on a level, 2-D grid (no 64-bit division): blockIdx.x =
@@ -1985,18 +2014,22 @@ int sweep_prolong_impl(const LevelView& L, const LevelView& C, const double* f, 
 
 template <bool ADJ, int DIR>
 int restrict_tile_impl(const LevelView& F, const LevelView& C, const double* f, const double* x,
-                       double* fc, cudaStream_t s) {
+                       double* fc, cudaStream_t s, double* xc0, double omega) {
   const dim3 blk = march_block(F);
   const int v = eff_variant(F);
+  if (xc0 != nullptr && !(v == 5 || v == 6)) {  // other designs: separate first coarse sweep
+    const int e = restrict_tile_impl<ADJ, DIR>(F, C, f, x, fc, s, nullptr, 0.0);
+    return e ? e : launch_sweep_from_zero(C, fc, xc0, omega, s);
+  }
   if (v == 5 || v == 6) {
     // DIR 0: warp w owns coarse nodes 14 w .. 14 w + 13; DIR 1: fine nodes 30 w ..
     const int64_t warps = DIR == 0 ? ceil_div(C.nn, 14) : ceil_div(F.nn, 30);
     const dim3 rb = balanced_block(warps);
     const int64_t tiles = ceil_div(warps, rb.x / 32);
     if (lean_nt(F) == 4)
-      pdl_launch(k_restrict2<ADJ, DIR, 4>, tgrid(tiles, (rows(F) + 3) / 4), rb, 0, s, F, C, f, x, fc);
+      pdl_launch(k_restrict2<ADJ, DIR, 4>, tgrid(tiles, (rows(F) + 3) / 4), rb, 0, s, F, C, f, x, fc, xc0, omega);
     else
-      pdl_launch(k_restrict2<ADJ, DIR, 8>, tgrid(tiles, (rows(F) + 7) / 8), rb, 0, s, F, C, f, x, fc);
+      pdl_launch(k_restrict2<ADJ, DIR, 8>, tgrid(tiles, (rows(F) + 7) / 8), rb, 0, s, F, C, f, x, fc, xc0, omega);
     return check_launch();
   }
   if (v == 0 || v == 1) {
@@ -2089,12 +2122,13 @@ int launch_residual(bool adjoint, const LevelView& L, const double* f, const dou
 }
 
 int launch_restrict_residual(bool adjoint, const LevelView& F, const LevelView& C, int dir,
-                             const double* f, const double* x, double* fc, cudaStream_t s) {
+                             const double* f, const double* x, double* fc, cudaStream_t s, double* xc0,
+                             double omega) {
   if (adjoint)
-    return dir == 0 ? restrict_tile_impl<true, 0>(F, C, f, x, fc, s)
-                    : restrict_tile_impl<true, 1>(F, C, f, x, fc, s);
-  return dir == 0 ? restrict_tile_impl<false, 0>(F, C, f, x, fc, s)
-                  : restrict_tile_impl<false, 1>(F, C, f, x, fc, s);
+    return dir == 0 ? restrict_tile_impl<true, 0>(F, C, f, x, fc, s, xc0, omega)
+                    : restrict_tile_impl<true, 1>(F, C, f, x, fc, s, xc0, omega);
+  return dir == 0 ? restrict_tile_impl<false, 0>(F, C, f, x, fc, s, xc0, omega)
+                  : restrict_tile_impl<false, 1>(F, C, f, x, fc, s, xc0, omega);
 }
 
 int launch_restrict(const LevelView& F, const LevelView& C, int dir, const double* r, double* fc,
