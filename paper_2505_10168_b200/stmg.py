@@ -744,7 +744,7 @@ def mg_solve_dist(h: DistHierarchy, b, u, opts: Optional[SolveOptions] = None) -
 
 
 def set_kernel_variant(v: int) -> None:
-    """Benchmarking knob: stencil kernel design (0 is the production default)."""
+    """Benchmarking knob: stencil kernel design (5 is the production default; see stmg_kernels.cu)."""
     _check(_lib.stmg_debug_set_kernel_variant(int(v)))
 
 

@@ -301,3 +301,38 @@ def test_short_time_tiles_bitwise(torch, S, port, monkeypatch, name):
     u = np.zeros_like(b)
     rep = S.mg_solve(h, b, u, S.SolveOptions(nu=cs.nu, tol=cs.tol, max_cycles=cs.max_cycles))
     check_solve(rep, u, rep_p, u_p)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 6])
+@pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "time_first"])
+def test_alternative_kernel_designs_bitwise(torch, S, port, name, variant):
+    """Every selectable stencil design (STMG_KERNEL_VARIANT / set_kernel_variant;
+    5 is production): sweeps, residual and residual-restriction bit-identical
+    to the oracle, and a whole solve with the same cycles and history."""
+    cs = case(name)
+    h = gpu_hier(S, cs, port)
+    hp = port_hier(port, cs)
+    rng = np.random.default_rng(23)
+    dev = torch.device("cuda:0")
+    S.set_kernel_variant(variant)
+    try:
+        for l in range(h.n_levels() - 1):
+            n = hp.ndofs(l)
+            x, f = special_values(rng, n), special_values(rng, n)
+            xt, ft = torch.from_numpy(x).to(dev), torch.from_numpy(f).to(dev)
+            r = torch.empty_like(xt)
+            h.residual(l, ft, xt, r)
+            assert np.array_equal(bits(r), bits(hp.residual(l, f, x))), l
+            xs = xt.clone()
+            h.sweeps(l, ft, xs, 3)
+            assert np.array_equal(bits(xs), bits(hp.sweeps(l, f, x, 3))), l
+            fc = torch.empty(hp.ndofs(l + 1), dtype=torch.float64, device=dev)
+            h.restrict_residual(l, ft, xt, fc)
+            assert np.array_equal(bits(fc), bits(hp.restrict(l, hp.residual(l, f, x)))), l
+        b = cs.rhs_vector(port)
+        u_p, rep_p = hp.solve(b, nu=cs.nu, tol=cs.tol, max_cycles=cs.max_cycles)
+        u = np.zeros_like(b)
+        rep = S.mg_solve(h, b, u, S.SolveOptions(nu=cs.nu, tol=cs.tol, max_cycles=cs.max_cycles))
+        check_solve(rep, u, rep_p, u_p)
+    finally:
+        S.set_kernel_variant(5)
