@@ -198,9 +198,10 @@ int stmg_mg_solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solv
 int stmg_level_sweeps(stmg_hierarchy* h, int32_t level, const double* f, double* x,
                       int32_t sweeps, double omega);
 /* Benchmark form: `launches` back-to-back kernel launches ping-ponging between
- * x and y (x -> y -> x ...), each a single sweep (fused_pairs = 0) or a fused
- * two-sweep pass (fused_pairs = 1); asynchronous on the hierarchy's stream, no
- * copies.  The iterate ends in x after an even number of launches. */
+ * x and y (x -> y -> x ...), each a single sweep (fused_pairs = 0), a fused
+ * two-sweep pass (fused_pairs = 1) or a fused 3- or 4-sweep pass (fused_pairs =
+ * 3, 4); asynchronous on the hierarchy's stream, no copies.  The iterate ends
+ * in x after an even number of launches. */
 int stmg_level_sweep_kernels(stmg_hierarchy* h, int32_t level, const double* f, double* x, double* y,
                              int32_t launches, int32_t fused_pairs, double omega);
 /* r = f - J_l x  (csr_residual) */

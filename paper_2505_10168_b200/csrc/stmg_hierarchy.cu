@@ -629,10 +629,22 @@ void sync_unless_capturing(cudaStream_t s) {
 // kernels (shorter serial chains where a launch is latency-bound).
 // STMG_SMALL_NT_DOFS overrides; read when a hierarchy is built.
 constexpr int64_t kSmallNtDofs = 2500000;  // measured: cfg1 solve 66.2 -> 57.7 ms (profiles/round1.md)
+// Levels with at most kTinyNtDofs DOFs use 2-level tiles (STMG_TINY_NT_DOFS).
+constexpr int64_t kTinyNtDofs = 1100000;  // measured: cfg1 solve 53.3 -> 50.8 ms
 int64_t tile_nt_for(int64_t dofs) {
-  int64_t lim = kSmallNtDofs;
+  int64_t lim = kSmallNtDofs, tiny = kTinyNtDofs;
   if (const char* v = std::getenv("STMG_SMALL_NT_DOFS")) lim = std::atoll(v);
-  return dofs <= lim ? 4 : 8;
+  if (const char* v = std::getenv("STMG_TINY_NT_DOFS")) tiny = std::atoll(v);
+  return dofs <= tiny ? 2 : dofs <= lim ? 4 : 8;
+}
+// Levels with at most this many DOFs smooth with depth-STMG_DEEP_DEPTH fused
+// kernels (one launch for 3 or 4 sweeps); STMG_DEEP_DOFS / STMG_DEEP_DEPTH override.
+constexpr int64_t kDeepDofs = 0;
+int64_t sweep_depth_for(int64_t dofs) {
+  int64_t lim = kDeepDofs, depth = 4;
+  if (const char* v = std::getenv("STMG_DEEP_DOFS")) lim = std::atoll(v);
+  if (const char* v = std::getenv("STMG_DEEP_DEPTH")) depth = std::atoll(v);
+  return (dofs <= lim && (depth == 3 || depth == 4)) ? depth : 2;
 }
 
 void upload_levels(stmg_hierarchy* h) {
@@ -652,6 +664,7 @@ void upload_levels(stmg_hierarchy* h) {
     v.n_lo = 0;
     v.n_hi = hl.g.n_t + 1;
     v.tile_nt = tile_nt_for(v.nn * (v.n_t + 1));
+    v.sweep_depth = sweep_depth_for(v.nn * (v.n_t + 1));
     h->views.push_back(v);
     h->device_bytes += static_cast<int64_t>(t.size() * 8);
     h->coef.push_back(std::move(buf));
@@ -707,6 +720,8 @@ void finish_create(stmg_hierarchy* h, bool share_ws_from_other, const stmg_hiera
     // same tiling as the hierarchy whose workspace (norm partials) is shared
     for (size_t l = 0; l < h->views.size() && l < other->views.size(); ++l)
       h->views[l].tile_nt = other->views[l].tile_nt;
+    for (size_t l = 0; l < h->views.size() && l < other->views.size(); ++l)
+      h->views[l].sweep_depth = other->views[l].sweep_depth;
     h->ws = other->ws;
   } else {
     int64_t bytes = 0;
@@ -759,6 +774,15 @@ struct Emitter {
   // memory per two sweeps), then a single sweep if count is odd.
   void smooth(int l, const double* f, int& cur, int count) {
     const LevelView& L = h->views[l];
+    const int depth = static_cast<int>(L.sweep_depth);
+    for (; depth > 2 && count >= depth; count -= depth) {
+      timed_launch(l, kTimedSweep2, [&] {
+        launch_check(launch_sweep_deep(h->adjoint, L, depth, f, buf(l, cur), buf(l, 1 - cur), omega, s),
+                     "sweep_deep");
+      });
+      ++kernels;
+      cur = 1 - cur;
+    }
     for (; count >= 2; count -= 2) {
       timed_launch(l, kTimedSweep2, [&] {
         launch_check(launch_sweep2(h->adjoint, L, f, buf(l, cur), buf(l, 1 - cur), omega, s), "sweep2");
@@ -1604,7 +1628,10 @@ int stmg_level_sweep_kernels(stmg_hierarchy* h, int32_t l, const double* f, doub
     double* a = x;
     double* b = y;
     for (int k = 0; k < launches; ++k) {
-      if (fused_pairs)
+      if (fused_pairs == 3 || fused_pairs == 4)
+        launch_check(launch_sweep_deep(h->adjoint, h->views[l], fused_pairs, f, a, b, omega, h->stream),
+                     "sweep_deep");
+      else if (fused_pairs)
         launch_check(launch_sweep2(h->adjoint, h->views[l], f, a, b, omega, h->stream), "sweep2");
       else
         launch_check(launch_sweep(h->adjoint, h->views[l], f, a, b, omega, nullptr, nullptr, h->stream), "sweep");

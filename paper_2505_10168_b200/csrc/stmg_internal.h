@@ -26,9 +26,12 @@ struct LevelView {
   // stay full-size and globally indexed; only the slab is read and written).
   int64_t n_lo;
   int64_t n_hi;
-  // Time levels per tile of the overlapping-warp kernels (8, or 4 on small,
+  // Time levels per tile of the overlapping-warp kernels (8, or 4 / 2 on small,
   // latency-bound levels); fixed when the hierarchy is built.
   int64_t tile_nt = 8;
+  // Deepest fused smoothing kernel used on this level (2: pairs; 3, 4: k_leanD
+  // on small levels where a launch is latency-bound); fixed at build.
+  int64_t sweep_depth = 2;
 };
 
 inline bool full_range(const LevelView& L) { return L.n_lo == 0 && L.n_hi == L.n_t + 1; }
@@ -86,6 +89,9 @@ int launch_sweep(bool adjoint, const LevelView& L, const double* f, const double
 // launch_sweep calls.  y must not alias x.
 int launch_sweep2(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
                   double omega, cudaStream_t s);
+// depth (3 or 4) sweeps y = S^depth(x) in one pass; full-range levels only.
+int launch_sweep_deep(bool adjoint, const LevelView& L, int depth, const double* f, const double* x,
+                      double* y, double omega, cudaStream_t s);
 // First sweep from a zero iterate: y = 0 + omega * (f * inv_diag), bitwise equal
 // to the general sweep applied to x = +0.
 int launch_sweep_from_zero(const LevelView& L, const double* f, double* y, double omega,

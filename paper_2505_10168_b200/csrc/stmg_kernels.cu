@@ -620,6 +620,104 @@ __global__ void __launch_bounds__(kMaxTW, 3) k_lean2x2(LevelView L, const double
   if (tt < ceil_div(L.n_hi - L.n_lo, NT)) dev_lean2x2<ADJ, NT>(L, f, x, y, omega, blockIdx.x, tt);
 }
 
+// D damped-Jacobi sweeps fused into one pass (temporal blocking of depth D,
+// the generalisation of k_lean2x2), bit-identical to D separate sweeps.  Lane
+// l holds node first - D + l; stage s (1..D) is valid on lanes s..31-s, so
+// lanes D..31-D (32 - 2D nodes per warp) are stored.  J: staged x rows
+// n0-D .. n0+NT-1, stage s produces rows n0-D+s .. n0+NT-1 in place (row j of
+// the stage array: own level j+1, coupled level j).  J^T: staged rows n0 ..
+// n0+NT+D-1, stage s produces rows n0 .. n0+NT+D-1-s (own j, coupled j+1).
+// Used on small, latency-bound levels, where one launch replaces D/2 pair
+// launches; full-range levels only (slab solves exchange ghosts every sweep).
+template <bool ADJ, int NT, int D, bool EDGE>
+__device__ __forceinline__ void leanD_body(const LevelView& L, const double* __restrict__ f,
+                                           const double* __restrict__ x, double* __restrict__ y,
+                                           double omega, int64_t first, int64_t n0, int lane) {
+  constexpr int S = NT + D;      // staged x rows
+  constexpr int F = NT + D - 1;  // f rows
+  const int64_t nn = L.nn, nt = L.n_t;
+  const int64_t i = first + lane - D;
+  const int64_t sbase = ADJ ? n0 : n0 - D;
+  const int64_t fbase = ADJ ? n0 : n0 - D + 1;
+  const bool in_grid = !EDGE || (i >= 0 && i < nn);
+  double v[S], fv[F];
+  Coefs c{};
+  if (!EDGE) {
+    const double* xp = x + (sbase * nn + i);
+    const double* fp = f + (fbase * nn + i);
+#pragma unroll
+    for (int j = 0; j < S; ++j) v[j] = xp[j * nn];
+#pragma unroll
+    for (int j = 0; j < F; ++j) fv[j] = fp[j * nn];
+    c = load_coefs(L, i);
+  } else {
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      const int64_t n = sbase + j;
+      v[j] = (n >= 0 && n <= nt && in_grid) ? x[n * nn + i] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < F; ++j) {
+      const int64_t n = fbase + j;
+      fv[j] = (n >= 0 && n <= nt && in_grid) ? f[n * nn + i] : 0.0;
+    }
+    if (in_grid) c = load_coefs(L, i);
+  }
+#pragma unroll
+  for (int st = 1; st <= D; ++st) {
+    double pm = __shfl_up_sync(kFull, v[0], 1), pp = __shfl_down_sync(kFull, v[0], 1);
+#pragma unroll
+    for (int j = 0; j < S - st; ++j) {
+      const double x1 = v[j + 1];
+      const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
+      const int64_t n = ADJ ? sbase + j : sbase + st + j;
+      const double fval = ADJ ? fv[j] : fv[st - 1 + j];
+      const double own = ADJ ? v[j] : x1;
+      double out;
+      if (!EDGE) {
+        const double row = ADJ ? row_interior<true>(c, pm, v[j], pp, qm, x1, qp)
+                               : row_interior<false>(c, qm, x1, qp, pm, v[j], pp);
+        out = own + omega * ((fval - row) * c.invd);
+      } else {
+        out = 0.0;
+        if (in_grid && n >= 0 && n <= nt) {
+          const double row = ADJ ? row_sum<true>(L, n, i, c, pm, v[j], pp, qm, x1, qp)
+                                 : row_sum<false>(L, n, i, c, qm, x1, qp, pm, v[j], pp);
+          const double id = (n == 0 || i == 0) ? L.inv_w : c.invd;
+          out = own + omega * ((fval - row) * id);
+        }
+      }
+      v[j] = out;
+      pm = qm;
+      pp = qp;
+    }
+  }
+  if (lane >= D && lane <= 31 - D && in_grid) {
+    double* yp = y + (n0 * nn + i);
+#pragma unroll
+    for (int k = 0; k < NT; ++k)
+      if (!EDGE || n0 + k < L.n_hi) yp[k * nn] = v[k];
+  }
+}
+
+template <bool ADJ, int NT, int D>
+__global__ void __launch_bounds__(kMaxTW, 3) k_leanD(LevelView L, const double* __restrict__ f,
+                                                     const double* __restrict__ x, double* __restrict__ y,
+                                                     double omega) {
+  pdl_entry();
+  const int64_t tt = (int64_t)blockIdx.z * gridDim.y + blockIdx.y;  // time tile
+  if (tt >= ceil_div(L.n_hi - L.n_lo, NT)) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t first = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * (32 - 2 * D);  // first stored node
+  if (first >= L.nn) return;
+  const int64_t n0 = L.n_lo + tt * NT, nt = L.n_t;
+  const bool rows_in = (ADJ ? (n0 >= 1 && n0 + NT + D - 1 <= nt) : (n0 >= D + 1 && n0 + NT - 1 <= nt)) &&
+                       n0 + NT - 1 < L.n_hi;
+  const bool nodes_in = first - D + 1 >= 2 && first - D + 30 <= L.n_el - 1;
+  if (rows_in && nodes_in) leanD_body<ADJ, NT, D, false>(L, f, x, y, omega, first, n0, lane);
+  else leanD_body<ADJ, NT, D, true>(L, f, x, y, omega, first, n0, lane);
+}
+
 // f_c = R (f - J x) over one lean tile, R = s P^T (proj/src/transfer.cpp:95-104);
 // the fine residual never reaches memory.  x step (DIR 0): lane l computes the
 // residual at its node (lane 0 also at the node before its strip, from an
@@ -1927,7 +2025,7 @@ inline dim3 balanced_block(int64_t warps) {
   const int64_t bx = (warps + 7) / 8;
   return dim3((unsigned)(32 * ((warps + bx - 1) / bx)));
 }
-inline int lean_nt(const LevelView& L) { return L.tile_nt == 4 ? 4 : 8; }
+inline int lean_nt(const LevelView& L) { return L.tile_nt == 2 ? 2 : L.tile_nt == 4 ? 4 : 8; }
 inline int64_t lean2_tiles(const LevelView& L, dim3 blk) {
   const int64_t per = (int64_t)(blk.x / 32) * 30;
   return (L.nn + per - 1) / per;
@@ -1978,7 +2076,9 @@ void launch_pass(const LevelView& L, const Ld& ld, const double* f, double* y, d
       pdl_launch(k_tile<ADJ, MODE, NORM, 8, 2, Ld>, grd, blk, tile_smem(blk, 8, 2), s, L, ld, f, y, omega, partials);
       break;
     case 5:
-      if (lean_nt(L) == 4)
+      if (lean_nt(L) == 2)
+        pdl_launch(k_lean2<ADJ, MODE, NORM, 2, 3, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
+      else if (lean_nt(L) == 4)
         pdl_launch(k_lean2<ADJ, MODE, NORM, 4, 3, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
       else
         pdl_launch(k_lean2<ADJ, MODE, NORM, 8, 3, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
@@ -2026,7 +2126,9 @@ int restrict_tile_impl(const LevelView& F, const LevelView& C, const double* f, 
     const int64_t warps = DIR == 0 ? ceil_div(C.nn, 14) : ceil_div(F.nn, 30);
     const dim3 rb = balanced_block(warps);
     const int64_t tiles = ceil_div(warps, rb.x / 32);
-    if (lean_nt(F) == 4)
+    if (lean_nt(F) == 2)
+      pdl_launch(k_restrict2<ADJ, DIR, 2>, tgrid(tiles, (rows(F) + 1) / 2), rb, 0, s, F, C, f, x, fc, xc0, omega);
+    else if (lean_nt(F) == 4)
       pdl_launch(k_restrict2<ADJ, DIR, 4>, tgrid(tiles, (rows(F) + 3) / 4), rb, 0, s, F, C, f, x, fc, xc0, omega);
     else
       pdl_launch(k_restrict2<ADJ, DIR, 8>, tgrid(tiles, (rows(F) + 7) / 8), rb, 0, s, F, C, f, x, fc, xc0, omega);
@@ -2081,7 +2183,11 @@ int launch_sweep2(bool adjoint, const LevelView& L, const double* f, const doubl
   const int64_t warps = ceil_div(L.nn, 28);
   const dim3 blk = balanced_block(warps);
   const int64_t tiles = ceil_div(warps, blk.x / 32);
-  if (lean_nt(L) == 4) {
+  if (lean_nt(L) == 2) {
+    const dim3 grd = tgrid(tiles, (rows(L) + 1) / 2);
+    if (adjoint) pdl_launch(k_lean2x2<true, 2>, grd, blk, 0, s, L, f, x, y, omega);
+    else pdl_launch(k_lean2x2<false, 2>, grd, blk, 0, s, L, f, x, y, omega);
+  } else if (lean_nt(L) == 4) {
     const dim3 grd = tgrid(tiles, (rows(L) + 3) / 4);
     if (adjoint) pdl_launch(k_lean2x2<true, 4>, grd, blk, 0, s, L, f, x, y, omega);
     else pdl_launch(k_lean2x2<false, 4>, grd, blk, 0, s, L, f, x, y, omega);
@@ -2089,6 +2195,34 @@ int launch_sweep2(bool adjoint, const LevelView& L, const double* f, const doubl
     const dim3 grd = tgrid(tiles, (rows(L) + 7) / 8);
     if (adjoint) pdl_launch(k_lean2x2<true, 8>, grd, blk, 0, s, L, f, x, y, omega);
     else pdl_launch(k_lean2x2<false, 8>, grd, blk, 0, s, L, f, x, y, omega);
+  }
+  return check_launch();
+}
+
+int launch_sweep_deep(bool adjoint, const LevelView& L, int depth, const double* f, const double* x,
+                      double* y, double omega, cudaStream_t s) {
+  if (!full_range(L) || (depth != 3 && depth != 4)) return static_cast<int>(cudaErrorInvalidValue);
+  const int64_t warps = ceil_div(L.nn, 32 - 2 * depth);
+  const dim3 blk = balanced_block(warps);
+  const int64_t tiles = ceil_div(warps, blk.x / 32);
+  if (lean_nt(L) == 2) {  // the level's time-tile depth (2, else 4)
+    const dim3 grd = tgrid(tiles, (rows(L) + 1) / 2);
+    if (depth == 3) {
+      if (adjoint) pdl_launch(k_leanD<true, 2, 3>, grd, blk, 0, s, L, f, x, y, omega);
+      else pdl_launch(k_leanD<false, 2, 3>, grd, blk, 0, s, L, f, x, y, omega);
+    } else {
+      if (adjoint) pdl_launch(k_leanD<true, 2, 4>, grd, blk, 0, s, L, f, x, y, omega);
+      else pdl_launch(k_leanD<false, 2, 4>, grd, blk, 0, s, L, f, x, y, omega);
+    }
+    return check_launch();
+  }
+  const dim3 grd = tgrid(tiles, (rows(L) + 3) / 4);
+  if (depth == 3) {
+    if (adjoint) pdl_launch(k_leanD<true, 4, 3>, grd, blk, 0, s, L, f, x, y, omega);
+    else pdl_launch(k_leanD<false, 4, 3>, grd, blk, 0, s, L, f, x, y, omega);
+  } else {
+    if (adjoint) pdl_launch(k_leanD<true, 4, 4>, grd, blk, 0, s, L, f, x, y, omega);
+    else pdl_launch(k_leanD<false, 4, 4>, grd, blk, 0, s, L, f, x, y, omega);
   }
   return check_launch();
 }

@@ -483,9 +483,10 @@ class LevelHierarchy:
         _check(_lib.stmg_level_sweeps(self._h, l, _ptr(f), _ptr(x), int(n), float(omega)))
 
     def sweep_kernels(self, l, f, x, y, launches, fused_pairs=False, omega=0.5):
-        """Benchmark form (asynchronous): ping-pong x <-> y for `launches` launches."""
+        """Benchmark form (asynchronous): ping-pong x <-> y for `launches` launches of a
+        single sweep (False / 0), a fused pair (True / 1) or a fused 3- / 4-sweep pass (3, 4)."""
         _check(_lib.stmg_level_sweep_kernels(self._h, l, _ptr(f), _ptr(x), _ptr(y), int(launches),
-                                             1 if fused_pairs else 0, float(omega)))
+                                             int(fused_pairs), float(omega)))
 
     def residual(self, l, f, x, r):
         _check(_lib.stmg_level_residual(self._h, l, _ptr(f), _ptr(x), _ptr(r)))

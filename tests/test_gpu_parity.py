@@ -274,11 +274,13 @@ def test_sweep_kernel_forms_bitwise(torch, S, port, name):
             assert np.array_equal(bits(xt), bits(want)), (l, pairs)
 
 
+@pytest.mark.parametrize("env", ["STMG_SMALL_NT_DOFS", "STMG_TINY_NT_DOFS"])
 @pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "time_first", "wide_short", "cfg0_deep"])
-def test_short_time_tiles_bitwise(torch, S, port, monkeypatch, name):
-    """4-level time tiles (STMG_SMALL_NT_DOFS, used on small latency-bound
-    levels) on every level: kernels bit-identical to the oracle, solve parity."""
-    monkeypatch.setenv("STMG_SMALL_NT_DOFS", str(10 ** 15))
+def test_short_time_tiles_bitwise(torch, S, port, monkeypatch, name, env):
+    """4-level (STMG_SMALL_NT_DOFS) and 2-level (STMG_TINY_NT_DOFS) time tiles,
+    used on small latency-bound levels, on every level: kernels bit-identical
+    to the oracle, solve parity."""
+    monkeypatch.setenv(env, str(10 ** 15))
     cs = case(name)
     h = gpu_hier(S, cs, port)
     hp = port_hier(port, cs)
@@ -336,3 +338,43 @@ def test_alternative_kernel_designs_bitwise(torch, S, port, name, variant):
         check_solve(rep, u, rep_p, u_p)
     finally:
         S.set_kernel_variant(5)
+
+
+@pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "time_first", "wide_short", "cfg0_deep", "tiny"])
+def test_deep_sweep_kernels_bitwise(torch, S, port, name):
+    """3- and 4-deep temporally blocked sweep kernels: one launch equals 3 / 4
+    reference sweeps bit for bit on every level (interior and boundary tiles)."""
+    cs = case(name)
+    h = gpu_hier(S, cs, port)
+    hp = port_hier(port, cs)
+    rng = np.random.default_rng(29)
+    dev = torch.device("cuda:0")
+    for l in range(h.n_levels()):
+        n = hp.ndofs(l)
+        x, f = special_values(rng, n), special_values(rng, n)
+        ft = torch.from_numpy(f).to(dev)
+        for depth in (3, 4):
+            xt = torch.from_numpy(x).to(dev)
+            yt = torch.empty_like(xt)
+            h.sweep_kernels(l, ft, xt, yt, 1, depth)
+            torch.cuda.synchronize()
+            assert np.array_equal(bits(yt), bits(hp.sweeps(l, f, x, depth))), (l, depth)
+
+
+@pytest.mark.parametrize("depth", ["3", "4"])
+@pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "cfg4_mini", "cfg0_deep"])
+def test_solve_with_deep_smoothing(torch, S, port, monkeypatch, name, depth):
+    """Every level smoothed with the deep kernels (STMG_DEEP_DOFS): the iterate
+    is bit-identical to the default schedule, and parity with the oracle holds."""
+    cs = case(name)
+    b = cs.rhs_vector(port)
+    opts = S.SolveOptions(nu=cs.nu, tol=cs.tol, max_cycles=cs.max_cycles)
+    monkeypatch.setenv("STMG_DEEP_DOFS", "0")
+    u0 = np.zeros_like(b)
+    r0 = S.mg_solve(gpu_hier(S, cs, port), b, u0, opts)
+    monkeypatch.setenv("STMG_DEEP_DOFS", str(10 ** 15))
+    monkeypatch.setenv("STMG_DEEP_DEPTH", depth)
+    u1 = np.zeros_like(b)
+    r1 = S.mg_solve(gpu_hier(S, cs, port), b, u1, opts)
+    assert r1.cycles == r0.cycles and r1.history == r0.history
+    assert np.array_equal(bits(u1), bits(u0))
