@@ -144,11 +144,15 @@ int stmg_plan_coarsening(const stmg_grid* g, const double* k, const double* c, c
 /* ---- hierarchy (proj/src/multigrid.cpp:86-160) ------------------------------------- */
 
 /* build_hierarchy, proj/include/stmg/multigrid.hpp:70-74.  method is the reference's
- * two-letter name (parse_method, proj/include/stmg/rediscretisation.hpp:45); this
- * build supports causal transfers with K, D or R reassembly ("CK", "CD", "CR").
- * dirs: n_dirs coarsening directions (STMG_DIR_X / STMG_DIR_T).  device: CUDA
- * ordinal.  Level operators, transfers and the coarsest exact solver all live on
- * the device; no CSR matrix is formed. */
+ * two-letter name (parse_method, proj/src/rediscretisation.cpp:19-38): interpolation
+ * C (causal) or B (bilinear, proj/src/transfer.cpp:64-68) and reassembly K, D, R or
+ * P (Galerkin R J P, proj/src/rediscretisation.cpp:112-115).  dirs: n_dirs coarsening
+ * directions (STMG_DIR_X / STMG_DIR_T / STMG_DIR_XT; XT is causal-only, as in
+ * proj/src/transfer.cpp:44-47).  device: CUDA ordinal.  Level operators, transfers
+ * and the coarsest exact solver all live on the device; no CSR matrix is formed
+ * (Galerkin levels are stored as per-DOF 9-point stencils, and a Galerkin coarsest
+ * level is solved by a block-tridiagonal march over dense host-factored blocks,
+ * which fails with STMG_ERUNTIME beyond 4 GB of factors). */
 int stmg_hierarchy_create(const stmg_grid* g, const double* k, const double* c,
                           const double* chi, const stmg_material_pair* mat, const char* method,
                           int32_t n_dirs, const int32_t* dirs, int32_t device,
@@ -169,6 +173,20 @@ int stmg_hierarchy_level_info(const stmg_hierarchy* h, int32_t level, int64_t* n
 int stmg_hierarchy_level_coeffs(const stmg_hierarchy* h, int32_t level, double* cur_m,
                                 double* cur_0, double* cur_p, double* oth_m, double* oth_0,
                                 double* oth_p, double* inv_diag);
+/* Any level's operator as a 9-point stencil in the hierarchy's orientation (host
+ * arrays): v9[k * ndofs + r] is row r's entry at column (n + dn, i + di) with
+ * k = 3 (dn + 1) + (di + 1), mask[r] bit k set where the reference's CSR row
+ * stores that entry, inv_diag[r] = 1 / diagonal.  ndofs = (n_el + 1)(n_t + 1).
+ * stmg_hierarchy_level_coeffs fails with STMG_EINVAL on a Galerkin level. */
+int stmg_hierarchy_level_stencil9(const stmg_hierarchy* h, int32_t level, double* v9, uint16_t* mask,
+                                  double* inv_diag);
+/* Host-only form of the same (no device work): build_hierarchy's host half for
+ * the given inputs, then level `level`'s operator (transposed if adjoint != 0).
+ * Lets CPU-only hosts pin the Galerkin R J P build against the reference. */
+int stmg_level_stencil9_host(const stmg_grid* g, const double* k, const double* c, const double* chi,
+                             const stmg_material_pair* mat, const char* method, int32_t n_dirs,
+                             const int32_t* dirs, int32_t level, int32_t adjoint, double* v9,
+                             uint16_t* mask, double* inv_diag);
 /* Run this hierarchy's work on a caller stream (cudaStream_t, NULL restores the
  * hierarchy's own stream).  Graphs are captured on a private stream and launched
  * on this one. */

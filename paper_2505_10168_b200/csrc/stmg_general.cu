@@ -1,0 +1,292 @@
+// sm_100a kernels for the general coarse discretisations:
+//   * Galerkin (P) coarse operators R J P, stored per DOF as a 9-point stencil
+//     (proj/src/rediscretisation.cpp:112-115; proj/src/sparse.cpp:121-162);
+//   * bilinear temporal transfers and combined space-time (FullST) coarsening
+//     (proj/src/transfer.cpp:39-104), applied as index arithmetic;
+//   * the exact coarsest solve of a Galerkin level, a block-tridiagonal (in time)
+//     forward/backward march over host-factored dense blocks (replacing the
+//     reference's Eigen SparseLU, proj/src/multigrid.cpp:20-57).
+//
+// Every row reduction keeps the reference's canonical CSR order
+// (proj/src/kernels/kernels.cpp:39-46): stored entries in ascending column
+// order go to lanes p & 3 from 0.0, row = (s0 + s1) + (s2 + s3); the library is
+// compiled --fmad=false.  Sweeps, residuals and transfers are therefore
+// bit-identical to the reference's CSR kernels; the block march is an exact
+// solve (FMA allowed), like the reference's LU it agrees to rounding.
+//
+// These levels are not on the BASELINE configs' hot path, so the kernels are
+// plain one-thread-per-row streaming kernels (coalesced slot-major loads).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "stmg_internal.h"
+
+namespace stmgb {
+namespace {
+
+constexpr int kBlock = 256;
+constexpr int kDirX = 0, kDirT = 1;  // stmg_direction (include/stmg_b200.h)
+
+int check() {
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : static_cast<int>(e);
+}
+
+unsigned grid_for(int64_t n) {
+  int64_t g = (n + kBlock - 1) / kBlock;
+  return static_cast<unsigned>(g < 1 ? 1 : g);
+}
+
+struct Lanes {
+  double s[4] = {0.0, 0.0, 0.0, 0.0};
+  int p = 0;
+  __device__ __forceinline__ void add(double prod) {
+    s[p & 3] = s[p & 3] + prod;
+    ++p;
+  }
+  __device__ __forceinline__ double result() const { return (s[0] + s[1]) + (s[2] + s[3]); }
+};
+
+// Canonical row dot of a 9-point level: slots k = 3 (dn + 1) + (di + 1) are in
+// ascending column order because |di| <= 1 < nn.
+__device__ __forceinline__ double row9(const Dia9View& A, int64_t r, const double* __restrict__ x) {
+  const int64_t nd = A.nn * (A.n_t + 1);
+  const unsigned m = A.mask[r];
+  Lanes acc;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    if ((m >> k) & 1u) {
+      const int64_t col = r + (k / 3 - 1) * A.nn + (k % 3 - 1);
+      acc.add(A.v[k * nd + r] * x[col]);
+    }
+  }
+  return acc.result();
+}
+
+// mode 0: y = x + omega (r * inv_diag) (csr_residual + jacobi_update,
+// kernels.cpp:62-73); mode 1: y = f - J x (csr_residual).
+template <int kMode>
+__global__ void k_dia9(Dia9View A, const double* __restrict__ f, const double* __restrict__ x,
+                       double* __restrict__ y, double omega) {
+  const int64_t nd = A.nn * (A.n_t + 1);
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nd;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const double res = f[r] - row9(A, r, x);
+    if (kMode == 0) y[r] = x[r] + omega * (res * A.inv_diag[r]);
+    else y[r] = res;
+  }
+}
+
+// First sweep from a zero iterate: the general sweep at x = +0 (every product
+// is +-0, each lane sums to +0, so r = f) -- bitwise 0 + omega (f * inv_diag).
+__global__ void k_dia9_from_zero(Dia9View A, const double* __restrict__ f, double* __restrict__ y,
+                                 double omega) {
+  const int64_t nd = A.nn * (A.n_t + 1);
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nd;
+       r += (int64_t)gridDim.x * blockDim.x)
+    y[r] = 0.0 + omega * ((f[r] - 0.0) * A.inv_diag[r]);
+}
+
+// Temporal stencil of P (proj/src/transfer.cpp:57-68): fine level 2N + dn.
+struct TimeTerms {
+  int n;
+  int dn[3];
+  double w[3];
+};
+__device__ __forceinline__ TimeTerms time_terms(const XferView& T) {
+  TimeTerms t{};
+  if (T.dir == kDirX) {
+    t.n = 1;
+    t.dn[0] = 0;
+    t.w[0] = 1.0;
+  } else if (!T.bilinear) {
+    t.n = 2;
+    t.dn[0] = 0;
+    t.w[0] = 1.0;
+    t.dn[1] = 1;
+    t.w[1] = 1.0;
+  } else {
+    t.n = 3;
+    t.dn[0] = -1;
+    t.w[0] = 0.5;
+    t.dn[1] = 0;
+    t.w[1] = 1.0;
+    t.dn[2] = 1;
+    t.w[2] = 0.5;
+  }
+  return t;
+}
+
+// fc = R r with R = s P^T (csr_spmv, multigrid.cpp:199; transfer.cpp:95-104).
+// Row (N, I) of R holds P's column (N, I): fine (2N + dn, 2I + dx) in ascending
+// flat order, value (P value) * s.
+__global__ void k_xfer_restrict(XferView T, const double* __restrict__ r, double* __restrict__ fc) {
+  const bool hx = T.dir != kDirT, ht = T.dir != kDirX;
+  const double s = T.dir == kDirX ? 1.0 : 0.5;  // restriction_scale, transfer.cpp:35-37
+  const int64_t nc = T.c_nn * (T.c_nt + 1);
+  const int64_t f_nel = T.f_nn - 1;
+  const TimeTerms tt = time_terms(T);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nc;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t N = q / T.c_nn, I = q - N * T.c_nn;
+    Lanes acc;
+    for (int te = 0; te < tt.n; ++te) {
+      const int64_t nf = ht ? 2 * N + tt.dn[te] : N;
+      if (nf < 0 || nf > T.f_nt) continue;  // truncated (transfer.cpp:74)
+      const double wt = tt.w[te];
+      const double* rowp = r + nf * T.f_nn;
+      if (hx) {
+        const int64_t i0 = 2 * I;
+        if (i0 - 1 >= 0) acc.add(((0.5 * wt) * s) * rowp[i0 - 1]);
+        acc.add((wt * s) * rowp[i0]);
+        if (i0 + 1 <= f_nel) acc.add(((0.5 * wt) * s) * rowp[i0 + 1]);
+      } else {
+        acc.add((wt * s) * rowp[I]);
+      }
+    }
+    fc[q] = acc.result();
+  }
+}
+
+// y = x + P xc (csr_spmv_add, multigrid.cpp:202; y may be x).  Row (n, i) of
+// P: coarse columns (N, I) in ascending flat order (time outer, space inner).
+__global__ void k_xfer_prolong_add(XferView T, const double* __restrict__ xc, const double* x, double* y) {
+  const bool hx = T.dir != kDirT, ht = T.dir != kDirX;
+  const int64_t nf_tot = T.f_nn * (T.f_nt + 1);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nf_tot;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = q / T.f_nn, i = q - n * T.f_nn;
+    int64_t Nc[2];
+    double wt[2];
+    int ntm = 0;
+    if (!ht) {
+      Nc[0] = n;
+      wt[0] = 1.0;
+      ntm = 1;
+    } else if (!T.bilinear) {
+      Nc[0] = n >> 1;  // fine 2N (dn 0) or 2N + 1 (dn 1), both weight 1
+      wt[0] = 1.0;
+      ntm = 1;
+    } else if ((n & 1) == 0) {
+      Nc[0] = n >> 1;
+      wt[0] = 1.0;
+      ntm = 1;
+    } else {
+      Nc[0] = (n - 1) >> 1;  // dn = +1
+      wt[0] = 0.5;
+      Nc[1] = (n + 1) >> 1;  // dn = -1
+      wt[1] = 0.5;
+      ntm = 2;
+    }
+    Lanes acc;
+    for (int a = 0; a < ntm; ++a) {
+      const double* row = xc + Nc[a] * T.c_nn;
+      if (!hx) {
+        acc.add(wt[a] * row[i]);
+      } else if ((i & 1) == 0) {
+        acc.add(wt[a] * row[i >> 1]);
+      } else {
+        acc.add((0.5 * wt[a]) * row[(i - 1) >> 1]);
+        acc.add((0.5 * wt[a]) * row[(i + 1) >> 1]);
+      }
+    }
+    y[q] = x[q] + acc.result();
+  }
+}
+
+// Block-tridiagonal march (one CTA): forward y_n = G_n (f_n - A_n y_{n-1}),
+// backward x_n = y_n - H_n x_{n+1}; G_n = M_n^-1 and H_n = M_n^-1 C_n are
+// column-major m x m host factors, A_n the level's dn = -1 slots.
+__global__ void __launch_bounds__(512) k_block_march(BlockMarchView B, const double* __restrict__ f,
+                                                     double* __restrict__ x) {
+  extern __shared__ double sm[];
+  const int64_t m = B.m;
+  double* prev = sm;      // y_{n-1} / x_{n+1}
+  double* v = sm + m;     // f_n - A_n y_{n-1}
+  const int64_t nd = m * (B.n_t + 1);
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) prev[i] = 0.0;
+  __syncthreads();
+  for (int64_t n = 0; n <= B.n_t; ++n) {
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+      const int64_t r = n * m + i;
+      double acc = f[r];
+      if (n > 0) {
+        const unsigned msk = B.A.mask[r];
+        for (int k = 0; k < 3; ++k)
+          if ((msk >> k) & 1u) acc -= B.A.v[k * nd + r] * prev[i + (k - 1)];
+      }
+      v[i] = acc;
+    }
+    __syncthreads();
+    const double* G = B.G + n * m * m;
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+      double acc = 0.0;
+      for (int64_t j = 0; j < m; ++j) acc = fma(G[j * m + i], v[j], acc);
+      x[n * m + i] = acc;
+    }
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) prev[i] = x[n * m + i];
+    __syncthreads();
+  }
+  if (!B.has_upper) return;
+  // prev holds x_{n_t}
+  for (int64_t n = B.n_t - 1; n >= 0; --n) {
+    const double* H = B.H + n * m * m;
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+      double acc = 0.0;
+      for (int64_t j = 0; j < m; ++j) acc = fma(H[j * m + i], prev[j], acc);
+      v[i] = x[n * m + i] - acc;
+    }
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+      prev[i] = v[i];
+      x[n * m + i] = v[i];
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+int launch_g_sweep(const Dia9View& A, const double* f, const double* x, double* y, double omega,
+                   cudaStream_t s) {
+  k_dia9<0><<<grid_for(A.nn * (A.n_t + 1)), kBlock, 0, s>>>(A, f, x, y, omega);
+  return check();
+}
+
+int launch_g_residual(const Dia9View& A, const double* f, const double* x, double* r, cudaStream_t s) {
+  k_dia9<1><<<grid_for(A.nn * (A.n_t + 1)), kBlock, 0, s>>>(A, f, x, r, 0.0);
+  return check();
+}
+
+int launch_g_from_zero(const Dia9View& A, const double* f, double* y, double omega, cudaStream_t s) {
+  k_dia9_from_zero<<<grid_for(A.nn * (A.n_t + 1)), kBlock, 0, s>>>(A, f, y, omega);
+  return check();
+}
+
+int launch_xfer_restrict(const XferView& T, const double* r, double* fc, cudaStream_t s) {
+  k_xfer_restrict<<<grid_for(T.c_nn * (T.c_nt + 1)), kBlock, 0, s>>>(T, r, fc);
+  return check();
+}
+
+int launch_xfer_prolong_add(const XferView& T, const double* xc, const double* x, double* y,
+                            cudaStream_t s) {
+  k_xfer_prolong_add<<<grid_for(T.f_nn * (T.f_nt + 1)), kBlock, 0, s>>>(T, xc, x, y);
+  return check();
+}
+
+int launch_block_march(const BlockMarchView& B, const double* f, double* x, cudaStream_t s) {
+  const size_t smem = 2 * sizeof(double) * static_cast<size_t>(B.m);
+  if (smem > 48 * 1024) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(k_block_march, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  int threads = static_cast<int>(((B.m + 31) / 32) * 32);
+  if (threads > 512) threads = 512;
+  k_block_march<<<1, threads, smem, s>>>(B, f, x);
+  return check();
+}
+
+}  // namespace stmgb

@@ -22,6 +22,7 @@
 
 #include "../../include/stmg_b200.h"
 #include "stmg_internal.h"
+#include "stmg_galerkin.h"
 
 namespace stmgb {
 namespace {
@@ -321,7 +322,9 @@ struct HostLevel {
   }
 };
 
-int parse_method(const char* name) {
+// parse_method, proj/src/rediscretisation.cpp:19-38 (two letters: interpolation C/B,
+// reassembly K/D/R/P); *bilinear receives the interpolation.
+int parse_method(const char* name, bool* bilinear = nullptr) {
   if (!name || std::strlen(name) != 2) throw std::invalid_argument("parse_method: expected two letters");
   if (name[0] != 'C' && name[0] != 'B')
     throw std::invalid_argument("parse_method: unknown interpolation letter");
@@ -333,10 +336,7 @@ int parse_method(const char* name) {
     case 'P': re = STMG_REASM_P; break;
     default: throw std::invalid_argument("parse_method: unknown reassembly letter");
   }
-  if (name[0] == 'B')
-    throw std::invalid_argument("stmg_b200: bilinear temporal transfers are not supported (causal only)");
-  if (re == STMG_REASM_P)
-    throw std::invalid_argument("stmg_b200: Galerkin (P) coarse operators are not supported");
+  if (bilinear) *bilinear = name[0] == 'B';
   return re;
 }
 
@@ -429,6 +429,24 @@ struct stmg_hierarchy {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::map<stmgb::GraphKey, stmgb::GraphEntry> graphs;
   int64_t device_bytes = 0;
+  // General coarse discretisations.
+  bool bilinear = false;                 // temporal interpolation of the t transfers
+  std::vector<stmgb::Dia9Host> gal;      // P reassembly: primal 9-point operators (level 0 empty)
+  std::vector<std::unique_ptr<stmgb::DeviceBuf>> gbuf;  // per level: Galerkin v | inv_diag | mask
+  std::vector<stmgb::Dia9View> dviews;   // per level; v == nullptr: per-node (rediscretised) level
+  std::vector<stmgb::XferView> xviews;   // per transfer
+  stmgb::BlockMarchView block{};         // Galerkin coarsest level's exact solver
+  std::unique_ptr<stmgb::DeviceBuf> block_g, block_h;
+  bool galerkin(int l) const { return l < static_cast<int>(dviews.size()) && dviews[l].v != nullptr; }
+  // transfers the per-node fused kernels do not cover: bilinear t, FullST
+  bool gen_xfer(int l) const {
+    return dirs[l] == STMG_DIR_XT || (bilinear && dirs[l] == STMG_DIR_T);
+  }
+  bool general() const {
+    for (int l = 0; l < n_levels(); ++l)
+      if (galerkin(l) || (l + 1 < n_levels() && gen_xfer(l))) return true;
+    return false;
+  }
 
   ~stmg_hierarchy() {
     int prev = 0;
@@ -448,6 +466,9 @@ struct stmg_hierarchy {
     if (own_stream) cudaStreamDestroy(own_stream);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     coef.clear();
+    gbuf.clear();
+    block_g.reset();
+    block_h.reset();
     pcr_alpha.reset();
     pcr_gamma.reset();
     pcr_bfin.reset();
@@ -647,6 +668,62 @@ int64_t sweep_depth_for(int64_t dofs) {
   return (dofs <= lim && (depth == 3 || depth == 4)) ? depth : 2;
 }
 
+// Device tables of the general coarse discretisations: Galerkin levels' 9-point
+// operators (transposed for an adjoint hierarchy, proj/src/multigrid.cpp:145-160),
+// transfer descriptors, and the dense block factors of a Galerkin coarsest level.
+constexpr int64_t kBlockTableBytes = int64_t{4} << 30;
+void upload_general(stmg_hierarchy* h) {
+  const int nl = h->n_levels();
+  h->dviews.assign(static_cast<size_t>(nl), Dia9View{});
+  h->gbuf.clear();
+  h->gbuf.resize(static_cast<size_t>(nl));
+  h->xviews.clear();
+  h->block_g.reset();
+  h->block_h.reset();
+  h->block = BlockMarchView{};
+  for (int l = 0; l < nl; ++l) {
+    Dia9View& v = h->dviews[l];
+    v.n_el = h->host[l].g.n_el;
+    v.n_t = h->host[l].g.n_t;
+    v.nn = v.n_el + 1;
+    if (l + 1 < nl) {
+      const HostGrid& fg = h->host[l].g;
+      const HostGrid& cg = h->host[l + 1].g;
+      h->xviews.push_back(XferView{fg.n_el + 1, fg.n_t, cg.n_el + 1, cg.n_t, h->dirs[l], h->bilinear ? 1 : 0});
+    }
+    if (l >= static_cast<int>(h->gal.size()) || h->gal[l].mask.empty()) continue;
+    Dia9Host tr;
+    const Dia9Host* A = &h->gal[l];
+    if (h->adjoint) {
+      tr = dia9_transposed(*A);
+      A = &tr;
+    }
+    const int64_t nd = A->ndofs();
+    const int64_t words = 10 * nd + (2 * nd + 7) / 8;
+    auto buf = std::make_unique<DeviceBuf>(words);
+    cuda_check(cudaMemcpy(buf->p, A->v.data(), 9 * nd * 8, cudaMemcpyHostToDevice), "galerkin upload");
+    cuda_check(cudaMemcpy(buf->p + 9 * nd, A->inv_diag.data(), nd * 8, cudaMemcpyHostToDevice), "galerkin upload");
+    cuda_check(cudaMemcpy(buf->p + 10 * nd, A->mask.data(), nd * 2, cudaMemcpyHostToDevice), "galerkin upload");
+    v.v = buf->p;
+    v.inv_diag = buf->p + 9 * nd;
+    v.mask = reinterpret_cast<const uint16_t*>(buf->p + 10 * nd);
+    h->device_bytes += words * 8;
+    if (l == nl - 1) {
+      const BlockTables bt = block_tables(*A, kBlockTableBytes);
+      h->block_g = std::make_unique<DeviceBuf>(static_cast<int64_t>(bt.G.size()));
+      cuda_check(cudaMemcpy(h->block_g->p, bt.G.data(), bt.G.size() * 8, cudaMemcpyHostToDevice), "block upload");
+      if (bt.has_upper) {
+        h->block_h = std::make_unique<DeviceBuf>(static_cast<int64_t>(bt.H.size()));
+        cuda_check(cudaMemcpy(h->block_h->p, bt.H.data(), bt.H.size() * 8, cudaMemcpyHostToDevice), "block upload");
+      }
+      h->device_bytes += static_cast<int64_t>(bt.G.size() + bt.H.size()) * 8;
+      h->block = BlockMarchView{bt.m, bt.n_t, h->block_g->p, bt.has_upper ? h->block_h->p : nullptr,
+                                bt.has_upper ? 1 : 0, v};
+    }
+    h->gbuf[l] = std::move(buf);
+  }
+}
+
 void upload_levels(stmg_hierarchy* h) {
   h->coef.clear();
   h->views.clear();
@@ -670,6 +747,7 @@ void upload_levels(stmg_hierarchy* h) {
     h->coef.push_back(std::move(buf));
   }
   build_pcr(h);
+  upload_general(h);
 }
 
 std::shared_ptr<Workspace> make_workspace(const stmg_hierarchy* h, int64_t* bytes) {
@@ -708,7 +786,7 @@ void finish_create(stmg_hierarchy* h, bool share_ws_from_other, const stmg_hiera
     if (const char* v = std::getenv("STMG_TAIL_CLUSTER")) h->tail_cluster = std::max(0, std::min(16, std::atoi(v)));
     h->tail_start = -1;
     const int nl = h->n_levels();
-    if (tail_dofs > 0 && nl >= 2 && tail_supported(h->coarsest)) {
+    if (tail_dofs > 0 && nl >= 2 && tail_supported(h->coarsest) && !h->general()) {
       for (int l = 1; l < nl; ++l)
         if (h->ndofs(l) <= tail_dofs && nl - l <= kTailMaxLevels) {
           h->tail_start = l;
@@ -770,9 +848,28 @@ struct Emitter {
     return which == 0 ? h->ws->xa[l]->p : h->ws->xb[l]->p;
   }
 
+  // kernel launches (= buffer flips) smooth(l, ., ., count) issues
+  int smooth_launches(int l, int count) const {
+    if (h->galerkin(l)) return count;
+    const int depth = static_cast<int>(h->views[l].sweep_depth);
+    int n = 0;
+    for (; depth > 2 && count >= depth; count -= depth) ++n;
+    return n + count / 2 + count % 2;
+  }
+
   // `count` damped-Jacobi sweeps from buffer `cur`: fused pairs (one pass over
   // memory per two sweeps), then a single sweep if count is odd.
   void smooth(int l, const double* f, int& cur, int count) {
+    if (h->galerkin(l)) {  // 9-point level: one launch per sweep
+      for (; count > 0; --count) {
+        timed_launch(l, kTimedSweep, [&] {
+          launch_check(launch_g_sweep(h->dviews[l], f, buf(l, cur), buf(l, 1 - cur), omega, s), "g_sweep");
+        });
+        ++kernels;
+        cur = 1 - cur;
+      }
+      return;
+    }
     const LevelView& L = h->views[l];
     const int depth = static_cast<int>(L.sweep_depth);
     for (; depth > 2 && count >= depth; count -= depth) {
@@ -832,8 +929,11 @@ struct Emitter {
     }
     if (l == nl - 1) {
       timed_launch(l, kTimedCoarsest, [&] {
-        launch_check(launch_coarsest(h->adjoint, h->coarsest, f, buf(l, 0), h->ws->coarse_scratch->p, s),
-                     "coarsest");
+        if (h->galerkin(l))
+          launch_check(launch_block_march(h->block, f, buf(l, 0), s), "block march");
+        else
+          launch_check(launch_coarsest(h->adjoint, h->coarsest, f, buf(l, 0), h->ws->coarse_scratch->p, s),
+                       "coarsest");
       });
       ++kernels;
       return 0;
@@ -846,7 +946,10 @@ struct Emitter {
         pre = nu - 1;
       } else if (nu >= 1) {
         timed_launch(l, kTimedFromZero, [&] {
-          launch_check(launch_sweep_from_zero(L, f, buf(l, 0), omega, s), "sweep0");
+          if (h->galerkin(l))
+            launch_check(launch_g_from_zero(h->dviews[l], f, buf(l, 0), omega, s), "g_sweep0");
+          else
+            launch_check(launch_sweep_from_zero(L, f, buf(l, 0), omega, s), "sweep0");
         });
         ++kernels;
         pre = nu - 1;
@@ -857,20 +960,43 @@ struct Emitter {
     }
     smooth(l, f, cur, pre);
     const LevelView& C = h->views[l + 1];
+    // per-node level and causal x / t transfer: the fused kernels
+    const bool fused = !h->galerkin(l) && !h->gen_xfer(l);
     // the child's first pre-smoothing sweep (from zero) is fused into this
     // restriction unless the child is the coarsest level or the coarse tail
-    const bool fuse_zero = nu >= 1 && l + 1 < nl - 1 && l + 1 != h->tail_start;
-    timed_launch(l, kTimedRestrict, [&] {
-      launch_check(launch_restrict_residual(h->adjoint, L, C, h->dirs[l], f, buf(l, cur),
-                                            h->ws->f[l + 1]->p, s, fuse_zero ? buf(l + 1, 0) : nullptr,
-                                            omega),
-                   "restrict");
-    });
-    ++kernels;
+    const bool fuse_zero =
+        fused && nu >= 1 && l + 1 < nl - 1 && l + 1 != h->tail_start && !h->galerkin(l + 1);
+    if (fused) {
+      timed_launch(l, kTimedRestrict, [&] {
+        launch_check(launch_restrict_residual(h->adjoint, L, C, h->dirs[l], f, buf(l, cur),
+                                              h->ws->f[l + 1]->p, s, fuse_zero ? buf(l + 1, 0) : nullptr,
+                                              omega),
+                     "restrict");
+      });
+      ++kernels;
+    } else {
+      // r = f - J x into the idle ping-pong buffer, then f_{l+1} = R r
+      timed_launch(l, kTimedRestrict, [&] {
+        if (h->galerkin(l))
+          launch_check(launch_g_residual(h->dviews[l], f, buf(l, cur), buf(l, 1 - cur), s), "g_residual");
+        else
+          launch_check(launch_residual(h->adjoint, L, f, buf(l, cur), buf(l, 1 - cur), s), "residual");
+        launch_check(launch_xfer_restrict(h->xviews[l], buf(l, 1 - cur), h->ws->f[l + 1]->p, s), "restrict");
+      });
+      kernels += 2;
+    }
     const int child = level(l + 1, 0, 0, true, fuse_zero);
     const double* xc = buf(l + 1, child);
     int post = nu;
-    if (nu >= 1) {
+    if (!fused) {
+      // level 0 must end in buffer 0 (the solve reads it): prolong out of place
+      // when the post-smoothing launches would otherwise leave it in buffer 1
+      const bool flip = l == 0 && (cur + smooth_launches(l, post)) % 2 != 0;
+      launch_check(launch_xfer_prolong_add(h->xviews[l], xc, buf(l, cur), buf(l, flip ? 1 - cur : cur), s),
+                   "prolong");
+      ++kernels;
+      if (flip) cur = 1 - cur;
+    } else if (nu >= 1) {
       timed_launch(l, kTimedProlongSweep, [&] {
         launch_check(launch_sweep_prolong(h->adjoint, L, C, h->dirs[l], f, buf(l, cur), xc,
                                           buf(l, 1 - cur), omega, s),
@@ -1102,14 +1228,19 @@ void load_vector_impl(const HostGrid& g, Q&& q, bool masked, double* b) {
 
 // build_hierarchy's host half (proj/src/multigrid.cpp:86-143): level grids,
 // coarse materials and per-node coefficients, no device work.
+// With P reassembly, *gal receives every level's operator as a 9-point stencil
+// (level 0 assembled, coarser levels R J P, primal orientation); *bilinear_out
+// the temporal interpolation.
 std::vector<HostLevel> make_host_levels(const stmg_grid* g, const double* k, const double* c,
                                         const double* chi, const stmg_material_pair* mat,
                                         const char* method, int32_t n_dirs, const int32_t* dirs,
-                                        int* reasm_out) {
+                                        int* reasm_out, bool* bilinear_out = nullptr,
+                                        std::vector<Dia9Host>* gal = nullptr) {
   if (!g) throw std::invalid_argument("build_hierarchy: null grid");
   const HostGrid fine = make_grid(g->L, g->t_T, g->n_el, g->n_t);
   if (!k || !c) throw std::invalid_argument("build_hierarchy: fine grid has no materials");
-  const int reasm = parse_method(method);
+  bool bilinear = false;
+  const int reasm = parse_method(method, &bilinear);
   if (reasm == STMG_REASM_D && (!chi || !mat))
     throw std::invalid_argument("build_hierarchy: D reassembly needs the design field and materials");
   if (n_dirs < 0 || (n_dirs > 0 && !dirs)) throw std::invalid_argument("build_hierarchy: bad path");
@@ -1123,9 +1254,8 @@ std::vector<HostLevel> make_host_levels(const stmg_grid* g, const double* k, con
   host.push_back(std::move(l0));
   for (int32_t s = 0; s < n_dirs; ++s) {
     const int dir = dirs[s];
-    if (dir == STMG_DIR_XT)
-      throw std::invalid_argument("stmg_b200: combined space-time (FullST) coarsening is not supported");
-    if (dir != STMG_DIR_X && dir != STMG_DIR_T) throw std::invalid_argument("build_hierarchy: bad direction");
+    if (dir != STMG_DIR_X && dir != STMG_DIR_T && dir != STMG_DIR_XT)
+      throw std::invalid_argument("build_hierarchy: bad direction");
     const HostLevel& p = host.back();
     HostLevel lc;
     lc.g = coarsen(p.g, dir);
@@ -1138,9 +1268,28 @@ std::vector<HostLevel> make_host_levels(const stmg_grid* g, const double* k, con
       if (reasm != STMG_REASM_D) lc.chi.clear();
     }
     lc.build();
+    // build_transfer -> build_prolongation's check (proj/src/transfer.cpp:44-47)
+    if (dir == STMG_DIR_XT && bilinear)
+      throw std::invalid_argument("build_prolongation: combined coarsening is causal-only");
     host.push_back(std::move(lc));
   }
   if (reasm_out) *reasm_out = reasm;
+  if (bilinear_out) *bilinear_out = bilinear;
+  if (gal) {
+    gal->clear();
+    if (reasm == STMG_REASM_P) {
+      // lc.J = galerkin_operator(t.R, prev.J, t.P) (proj/src/multigrid.cpp:131-134)
+      const HostLevel& h0 = host[0];
+      gal->push_back(dia9_assembled(h0.g.n_el, h0.g.n_t, h0.W, h0.D, h0.E, h0.SW, h0.S, h0.SE, h0.w));
+      for (int32_t s = 0; s < n_dirs; ++s) {
+        const HostGrid& cg = host[s + 1].g;
+        Dia9Host A = dia9_galerkin(gal->back(), dirs[s], bilinear, cg.n_el, cg.n_t);
+        dia9_invert_diagonal(A);
+        gal->push_back(std::move(A));
+      }
+      if (n_dirs > 0) (*gal)[0] = Dia9Host();  // level 0 stays the assembled (fast-path) operator
+    }
+  }
   return host;
 }
 
@@ -1323,10 +1472,14 @@ void optimise(const stmg_grid* geom, const stmg_optimise_options& o, int device,
     simp(chi.data(), ne, o.mat, k.data(), c.data());
     std::vector<int32_t> dirs(static_cast<size_t>(std::max(o.n_levels - 1, 0)));
     plan(g, k.data(), c.data(), chi.data(), &o.mat, preq, dirs.data(), nullptr);
+    bool bilinear = false;
+    std::vector<Dia9Host> gal;
     std::vector<HostLevel> host =
         make_host_levels(&gc, k.data(), c.data(), chi.data(), &o.mat, o.method,
-                         static_cast<int32_t>(dirs.size()), dirs.data(), nullptr);
-    if (h && dirs == cur_dirs) {
+                         static_cast<int32_t>(dirs.size()), dirs.data(), nullptr, &bilinear, &gal);
+    // per-node levels with an unchanged path: refresh the coefficient tables in
+    // place; Galerkin levels are rebuilt (their operators are per DOF)
+    if (h && dirs == cur_dirs && gal.empty()) {
       refresh_levels(h.get(), host);
       refresh_levels(ht.get(), std::move(host));
     } else {
@@ -1336,6 +1489,9 @@ void optimise(const stmg_grid* geom, const stmg_optimise_options& o, int device,
       nh->device = device;
       nh->dirs = dirs;
       nh->host = std::move(host);
+      nh->bilinear = bilinear;
+      nh->gal = std::move(gal);
+      nh->reassembly = parse_method(o.method);
       finish_create(nh.get(), false, nullptr);
       stmg_hierarchy* tp = nullptr;
       const int rc = stmg_hierarchy_transposed(nh.get(), &tp);
@@ -1484,7 +1640,7 @@ int stmg_hierarchy_create(const stmg_grid* g, const double* k, const double* c, 
     if (!g) throw std::invalid_argument("build_hierarchy: null grid");
     auto h = std::make_unique<stmg_hierarchy>();
     // argument errors (the reference's invalid_argument) are raised before any device work
-    h->host = make_host_levels(g, k, c, chi, mat, method, n_dirs, dirs, &h->reassembly);
+    h->host = make_host_levels(g, k, c, chi, mat, method, n_dirs, dirs, &h->reassembly, &h->bilinear, &h->gal);
     int n_dev = 0;
     cuda_check(cudaGetDeviceCount(&n_dev), "cudaGetDeviceCount");
     if (device < 0 || device >= n_dev) throw std::invalid_argument("build_hierarchy: bad device ordinal");
@@ -1504,6 +1660,8 @@ int stmg_hierarchy_transposed(const stmg_hierarchy* src, stmg_hierarchy** out) {
     h->reassembly = src->reassembly;
     h->dirs = src->dirs;
     h->host = src->host;
+    h->bilinear = src->bilinear;
+    h->gal = src->gal;
     finish_create(h.get(), true, src);
     *out = h.release();
   });
@@ -1534,11 +1692,61 @@ int stmg_hierarchy_level_coeffs(const stmg_hierarchy* h, int32_t l, double* cm, 
   return guarded([&] {
     if (!h) throw std::invalid_argument("null hierarchy handle");
     check_level(h, l);
+    if (h->galerkin(l))
+      throw std::invalid_argument("level_coeffs: Galerkin level (per-DOF operator); use stmg_hierarchy_level_stencil9");
     const std::vector<double> t = h->host[l].table(h->adjoint);
     const size_t nn = static_cast<size_t>(h->host[l].g.n_el + 1);
     double* outs[7] = {cm, c0, cp, om, o0, op, invd};
     for (int k = 0; k < 7; ++k)
       if (outs[k]) std::memcpy(outs[k], t.data() + k * nn, nn * sizeof(double));
+  });
+}
+
+int stmg_hierarchy_level_stencil9(const stmg_hierarchy* h, int32_t l, double* v9, uint16_t* mask,
+                                  double* invd) {
+  return guarded([&] {
+    if (!h) throw std::invalid_argument("null hierarchy handle");
+    check_level(h, l);
+    Dia9Host A;
+    if (l < static_cast<int>(h->gal.size()) && !h->gal[l].mask.empty()) {
+      A = h->gal[l];
+    } else {
+      const HostLevel& hl = h->host[l];
+      A = dia9_assembled(hl.g.n_el, hl.g.n_t, hl.W, hl.D, hl.E, hl.SW, hl.S, hl.SE, hl.w);
+      dia9_invert_diagonal(A);
+    }
+    if (h->adjoint) A = dia9_transposed(A);
+    const size_t nd = static_cast<size_t>(A.ndofs());
+    if (v9) std::memcpy(v9, A.v.data(), 9 * nd * sizeof(double));
+    if (mask) std::memcpy(mask, A.mask.data(), nd * sizeof(uint16_t));
+    if (invd) std::memcpy(invd, A.inv_diag.data(), nd * sizeof(double));
+  });
+}
+
+int stmg_level_stencil9_host(const stmg_grid* g, const double* k, const double* c, const double* chi,
+                             const stmg_material_pair* mat, const char* method, int32_t n_dirs,
+                             const int32_t* dirs, int32_t level, int32_t adjoint, double* v9,
+                             uint16_t* mask, double* invd) {
+  return guarded([&] {
+    int reasm = 0;
+    bool bilinear = false;
+    std::vector<Dia9Host> gal;
+    const std::vector<HostLevel> host =
+        make_host_levels(g, k, c, chi, mat, method, n_dirs, dirs, &reasm, &bilinear, &gal);
+    if (level < 0 || level >= static_cast<int32_t>(host.size())) throw std::out_of_range("level out of range");
+    Dia9Host A;
+    if (level < static_cast<int32_t>(gal.size()) && !gal[level].mask.empty()) {
+      A = std::move(gal[level]);
+    } else {
+      const HostLevel& hl = host[level];
+      A = dia9_assembled(hl.g.n_el, hl.g.n_t, hl.W, hl.D, hl.E, hl.SW, hl.S, hl.SE, hl.w);
+      dia9_invert_diagonal(A);
+    }
+    if (adjoint) A = dia9_transposed(A);
+    const size_t nd = static_cast<size_t>(A.ndofs());
+    if (v9) std::memcpy(v9, A.v.data(), 9 * nd * sizeof(double));
+    if (mask) std::memcpy(mask, A.mask.data(), nd * sizeof(uint16_t));
+    if (invd) std::memcpy(invd, A.inv_diag.data(), nd * sizeof(double));
   });
 }
 
@@ -1604,6 +1812,10 @@ int stmg_level_sweeps(stmg_hierarchy* h, int32_t l, const double* f, double* x, 
     double* a = x;
     double* b = tmp;
     int left = sweeps;
+    for (; h->galerkin(l) && left >= 1; --left) {
+      launch_check(launch_g_sweep(h->dviews[l], f, a, b, omega, h->stream), "g_sweep");
+      std::swap(a, b);
+    }
     for (; left >= 2; left -= 2) {
       launch_check(launch_sweep2(h->adjoint, h->views[l], f, a, b, omega, h->stream), "sweep2");
       std::swap(a, b);
@@ -1628,7 +1840,9 @@ int stmg_level_sweep_kernels(stmg_hierarchy* h, int32_t l, const double* f, doub
     double* a = x;
     double* b = y;
     for (int k = 0; k < launches; ++k) {
-      if (fused_pairs == 3 || fused_pairs == 4)
+      if (h->galerkin(l))
+        launch_check(launch_g_sweep(h->dviews[l], f, a, b, omega, h->stream), "g_sweep");
+      else if (fused_pairs == 3 || fused_pairs == 4)
         launch_check(launch_sweep_deep(h->adjoint, h->views[l], fused_pairs, f, a, b, omega, h->stream),
                      "sweep_deep");
       else if (fused_pairs)
@@ -1645,7 +1859,8 @@ int stmg_level_residual(stmg_hierarchy* h, int32_t l, const double* f, const dou
     checked(h);
     check_level(h, l);
     DeviceGuard dg(h->device);
-    launch_check(launch_residual(h->adjoint, h->views[l], f, x, r, h->stream), "residual");
+    if (h->galerkin(l)) launch_check(launch_g_residual(h->dviews[l], f, x, r, h->stream), "g_residual");
+    else launch_check(launch_residual(h->adjoint, h->views[l], f, x, r, h->stream), "residual");
     sync_unless_capturing(h->stream);
   });
 }
@@ -1657,9 +1872,17 @@ int stmg_level_restrict_residual(stmg_hierarchy* h, int32_t l, const double* f, 
     check_level(h, l);
     if (l + 1 >= h->n_levels()) throw std::out_of_range("no coarser level");
     DeviceGuard dg(h->device);
-    launch_check(launch_restrict_residual(h->adjoint, h->views[l], h->views[l + 1], h->dirs[l], f, x,
-                                          fc, h->stream),
-                 "restrict");
+    if (h->galerkin(l) || h->gen_xfer(l)) {
+      DeviceBuf r(h->ndofs(l));
+      if (h->galerkin(l)) launch_check(launch_g_residual(h->dviews[l], f, x, r.p, h->stream), "g_residual");
+      else launch_check(launch_residual(h->adjoint, h->views[l], f, x, r.p, h->stream), "residual");
+      launch_check(launch_xfer_restrict(h->xviews[l], r.p, fc, h->stream), "restrict");
+      cuda_check(cudaStreamSynchronize(h->stream), "sync");  // r is freed on return
+    } else {
+      launch_check(launch_restrict_residual(h->adjoint, h->views[l], h->views[l + 1], h->dirs[l], f, x,
+                                            fc, h->stream),
+                   "restrict");
+    }
     sync_unless_capturing(h->stream);
   });
 }
@@ -1670,7 +1893,8 @@ int stmg_level_restrict(stmg_hierarchy* h, int32_t l, const double* r, double* f
     check_level(h, l);
     if (l + 1 >= h->n_levels()) throw std::out_of_range("no coarser level");
     DeviceGuard dg(h->device);
-    launch_check(launch_restrict(h->views[l], h->views[l + 1], h->dirs[l], r, fc, h->stream), "restrict");
+    if (h->gen_xfer(l)) launch_check(launch_xfer_restrict(h->xviews[l], r, fc, h->stream), "restrict");
+    else launch_check(launch_restrict(h->views[l], h->views[l + 1], h->dirs[l], r, fc, h->stream), "restrict");
     sync_unless_capturing(h->stream);
   });
 }
@@ -1681,7 +1905,8 @@ int stmg_level_prolong_add(stmg_hierarchy* h, int32_t l, const double* xc, doubl
     check_level(h, l);
     if (l + 1 >= h->n_levels()) throw std::out_of_range("no coarser level");
     DeviceGuard dg(h->device);
-    launch_check(launch_prolong_add(h->views[l], h->views[l + 1], h->dirs[l], xc, x, h->stream), "prolong");
+    if (h->gen_xfer(l)) launch_check(launch_xfer_prolong_add(h->xviews[l], xc, x, x, h->stream), "prolong");
+    else launch_check(launch_prolong_add(h->views[l], h->views[l + 1], h->dirs[l], xc, x, h->stream), "prolong");
     sync_unless_capturing(h->stream);
   });
 }
@@ -1690,8 +1915,11 @@ int stmg_coarsest_solve(stmg_hierarchy* h, const double* f, double* x) {
   return guarded([&] {
     checked(h);
     DeviceGuard dg(h->device);
-    launch_check(launch_coarsest(h->adjoint, h->coarsest, f, x, h->ws->coarse_scratch->p, h->stream),
-                 "coarsest");
+    if (h->galerkin(h->n_levels() - 1))
+      launch_check(launch_block_march(h->block, f, x, h->stream), "block march");
+    else
+      launch_check(launch_coarsest(h->adjoint, h->coarsest, f, x, h->ws->coarse_scratch->p, h->stream),
+                   "coarsest");
     sync_unless_capturing(h->stream);
   });
 }
@@ -1775,7 +2003,14 @@ int stmg_dist_create(const stmg_grid* g, const double* k, const double* c, const
     if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("dist_create: bad rank/world");
     if (!g) throw std::invalid_argument("dist_create: null grid");
     auto d = std::make_unique<stmg_dist>();
-    d->host = make_host_levels(g, k, c, chi, mat, method, n_dirs, dirs, nullptr);
+    bool bilinear = false;
+    int reasm = 0;
+    d->host = make_host_levels(g, k, c, chi, mat, method, n_dirs, dirs, &reasm, &bilinear);
+    bool xt = false;
+    for (int32_t s = 0; s < n_dirs; ++s) xt = xt || dirs[s] == STMG_DIR_XT;
+    if (bilinear || reasm == STMG_REASM_P || xt)
+      throw std::invalid_argument(
+          "dist_create: time-slab hierarchies take causal x / t transfers with K, D or R reassembly");
     if (d->host.size() < 2) throw std::invalid_argument("dist_create: need at least two levels");
     int n_dev = 0;
     cuda_check(cudaGetDeviceCount(&n_dev), "cudaGetDeviceCount");

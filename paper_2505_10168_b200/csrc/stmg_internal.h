@@ -79,6 +79,43 @@ struct TailParams {
   CoarsestView cv;
 };
 
+// ---- general coarse discretisations (stmg_general.cu) ------------------------------
+// Per-DOF 9-point operator of a Galerkin (R J P) level, in the hierarchy's row
+// orientation: slot k = 3 (dn + 1) + (di + 1) holds the entry at column
+// (n + dn, i + di); mask bit k is set where the reference's CSR row stores it.
+struct Dia9View {
+  int64_t n_el;
+  int64_t n_t;
+  int64_t nn;
+  const double* v;         // 9 * ndofs, slot-major: v[k * ndofs + r]
+  const uint16_t* mask;    // ndofs
+  const double* inv_diag;  // ndofs
+};
+// One transfer (level l fine, l + 1 coarse), proj/src/transfer.cpp:39-104.
+struct XferView {
+  int64_t f_nn, f_nt, c_nn, c_nt;
+  int dir;       // 0 x, 1 t, 2 x and t (FullST)
+  int bilinear;  // temporal stencil: 0 causal, 1 bilinear
+};
+// Exact block-tridiagonal solve of a Galerkin coarsest level.
+struct BlockMarchView {
+  int64_t m;    // nodes per time level (n_el + 1)
+  int64_t n_t;
+  const double* G;  // (n_t + 1) column-major m x m blocks M_n^-1
+  const double* H;  // n_t blocks M_n^-1 C_n (null when the operator is causal)
+  int has_upper;
+  Dia9View A;  // dn = -1 slots
+};
+int launch_g_sweep(const Dia9View& A, const double* f, const double* x, double* y, double omega,
+                   cudaStream_t s);
+int launch_g_residual(const Dia9View& A, const double* f, const double* x, double* r, cudaStream_t s);
+int launch_g_from_zero(const Dia9View& A, const double* f, double* y, double omega, cudaStream_t s);
+int launch_xfer_restrict(const XferView& T, const double* r, double* fc, cudaStream_t s);
+// y = x + P xc (y may alias x)
+int launch_xfer_prolong_add(const XferView& T, const double* xc, const double* x, double* y,
+                            cudaStream_t s);
+int launch_block_march(const BlockMarchView& B, const double* f, double* x, cudaStream_t s);
+
 // ---- kernel launchers (stmg_kernels.cu); all asynchronous on `s` ------------------
 // One damped-Jacobi sweep y = x + omega (f - J x) / diag.  If partials != nullptr,
 // the block partial sums of r^2 are written too (deterministic order).  If y ==

@@ -11,7 +11,7 @@ can switch to the B200 path:
     dof_is_masked (assembly.hpp:68)         dof_is_masked
     plan_coarsening (strategy.hpp:104-105)  plan_coarsening
     path_to_string (strategy.hpp:99)        path_to_string
-    parse_method (rediscretisation.hpp:45)  (method strings "CK", "CD", "CR")
+    parse_method (rediscretisation.cpp:19-38)  (method strings C|B + K|D|R|P)
     build_hierarchy (multigrid.hpp:70-74)   build_hierarchy
     transposed_hierarchy (multigrid.hpp:77) transposed_hierarchy
     mg_solve (multigrid.hpp:107-108)        mg_solve
@@ -62,6 +62,8 @@ def _load():
         "stmg_hierarchy_level_info": [vp, i32, C.POINTER(i64), C.POINTER(i64), C.POINTER(f64)],
         "stmg_hierarchy_level_coeffs": [vp, i32, vp, vp, vp, vp, vp, vp, vp],
         "stmg_hierarchy_device_bytes": [vp, C.POINTER(i64)],
+        "stmg_hierarchy_level_stencil9": [vp, i32, vp, vp, vp],
+        "stmg_level_stencil9_host": [vp, vp, vp, vp, vp, C.c_char_p, i32, vp, i32, i32, vp, vp, vp],
         "stmg_hierarchy_set_stream": [vp, vp],
         "stmg_hierarchy_set_profiling": [vp, i32],
         "stmg_hierarchy_profile": [vp, i32, i32, C.POINTER(i64), C.POINTER(f64)],
@@ -478,6 +480,15 @@ class LevelHierarchy:
         _check(_lib.stmg_hierarchy_level_coeffs(self._h, l, *[a.ctypes.data for a in arrs]))
         return dict(zip(["cur_m", "cur_0", "cur_p", "oth_m", "oth_0", "oth_p", "inv_diag"], arrs))
 
+    def level_stencil9(self, l: int) -> dict:
+        """Level l's operator as a 9-point stencil (any level, Galerkin included)."""
+        lv = self.levels[l]
+        nd = (lv.n_el + 1) * (lv.n_t + 1)
+        v9, mask, inv = np.zeros(9 * nd), np.zeros(nd, np.uint16), np.zeros(nd)
+        _check(_lib.stmg_hierarchy_level_stencil9(self._h, l, v9.ctypes.data, mask.ctypes.data,
+                                                  inv.ctypes.data))
+        return dict(v9=v9.reshape(9, nd), mask=mask, inv_diag=inv)
+
     # -- level kernels on device vectors (torch tensors on this hierarchy's device) --
     def sweeps(self, l, f, x, n, omega=0.5):
         _check(_lib.stmg_level_sweeps(self._h, l, _ptr(f), _ptr(x), int(n), float(omega)))
@@ -544,7 +555,8 @@ class LevelHierarchy:
 
 def build_hierarchy(fine: SpaceTimeGrid, method, path: CoarseningPath, chi=None, mat=None,
                     device: int = 0) -> LevelHierarchy:
-    """proj/src/multigrid.cpp:86-143 (causal transfers; K, D or R coarse operators)."""
+    """proj/src/multigrid.cpp:86-143: method "CK"/"CD"/"CR"/"CP" (causal) or "BK"/"BD"/"BR"/"BP"
+    (bilinear temporal transfers); path directions x, t or xt (FullST, causal only)."""
     if not fine.has_materials():
         raise ValueError("build_hierarchy: fine grid has no materials")
     name = method if isinstance(method, str) else str(method)
@@ -561,6 +573,32 @@ def build_hierarchy(fine: SpaceTimeGrid, method, path: CoarseningPath, chi=None,
                                       dirs.ctypes.data if dirs.size else None, int(device),
                                       C.byref(h)))
     return LevelHierarchy(h, path, name, device)
+
+
+def level_stencil9_host(fine: SpaceTimeGrid, method, path: CoarseningPath, level: int, chi=None,
+                        mat=None, adjoint: bool = False) -> dict:
+    """build_hierarchy's host half only (no GPU): level `level`'s operator as a
+    9-point stencil, transposed when `adjoint` (see include/stmg_b200.h)."""
+    if not fine.has_materials():
+        raise ValueError("build_hierarchy: fine grid has no materials")
+    k = _f64(fine.k, fine.n_el)
+    c = _f64(fine.c, fine.n_el)
+    chi_a = None if chi is None else _f64(chi.chi if hasattr(chi, "chi") else chi, fine.n_el)
+    m = None if mat is None else MaterialPair.of(mat)._c()
+    dirs = np.array([int(d) for d in path.dirs], np.int32)
+    ne, nt = fine.n_el, fine.n_t
+    for d in dirs[:level]:
+        ne, nt = (ne // 2 if d != 1 else ne), (nt // 2 if d != 0 else nt)
+    nd = (ne + 1) * (nt + 1)
+    v9, mask, inv = np.zeros(9 * nd), np.zeros(nd, np.uint16), np.zeros(nd)
+    gc = fine._c()
+    _check(_lib.stmg_level_stencil9_host(C.byref(gc), k.ctypes.data, c.ctypes.data,
+                                         None if chi_a is None else chi_a.ctypes.data,
+                                         None if m is None else C.byref(m), str(method).encode(),
+                                         dirs.size, dirs.ctypes.data if dirs.size else None,
+                                         int(level), 1 if adjoint else 0, v9.ctypes.data,
+                                         mask.ctypes.data, inv.ctypes.data))
+    return dict(v9=v9.reshape(9, nd), mask=mask, inv_diag=inv, n_el=ne, n_t=nt)
 
 
 def transposed_hierarchy(h: LevelHierarchy) -> LevelHierarchy:

@@ -110,7 +110,38 @@ def case(name: str) -> Case:
         return cc
     if name == "cfg4_mini":
         return _from_cfg(name, C.cfg4(n_el=256, n_t=1024), n_levels=8, nu=5)
+    if name in GENERAL:
+        kind, ne, nt, method, dirs, adjoint, nu = GENERAL[name]
+        if kind == "cfg1":
+            cc = _from_cfg(name, C.cfg1(n_el=ne, n_t=nt), n_levels=len(dirs) + 1, nu=nu, method=method,
+                           adjoint=adjoint)
+        else:
+            cc = _uniform(name, ne, nt, len(dirs) + 1, method=method, nu=nu, adjoint=adjoint)
+        cc.dirs = np.asarray(dirs, np.int32)
+        cc.max_cycles = 40
+        return cc
     raise KeyError(name)
+
+
+# General coarse discretisations: Galerkin (P) coarse
+# operators, bilinear temporal transfers (B*), combined space-time steps (2 =
+# FullST).  Explicit paths (the planners never emit FullST).  Outcomes under the
+# reference: converged (gen_bk, gen_br_deep, gen_cp_x4), diverged (gen_bp_div),
+# the rest reach max_cycles = 40.
+GENERAL = {
+    # name: (inputs, n_el, n_t, method, dirs, adjoint, nu)
+    "gen_cp": ("cfg1", 32, 64, "CP", [0, 1, 0], False, 2),
+    "gen_bp_div": ("cfg1", 32, 64, "BP", [1, 0, 1], False, 2),
+    "gen_cp_xt_adj": ("cfg1", 32, 64, "CP", [2, 0], True, 2),
+    "gen_bk": ("cfg1", 32, 64, "BK", [1, 1, 0], False, 2),
+    "gen_br_adj": ("cfg1", 32, 64, "BR", [0, 1, 1], True, 2),
+    "gen_ck_xt": ("cfg1", 32, 64, "CK", [2, 2], False, 1),
+    "gen_bd": ("cfg1", 32, 64, "BD", [0, 1], False, 2),
+    "gen_br_deep": ("uniform", 32, 64, "BR", [0, 0, 1, 0, 1], False, 3),
+    "gen_cp_x4": ("uniform", 128, 128, "CP", [0, 0, 0, 0], False, 1),
+    "gen_bp_uni": ("uniform", 32, 64, "BP", [1, 0, 1], False, 2),
+}
+GENERAL_CASES = list(GENERAL)
 
 
 SMALL_CASES = ["cfg0", "cfg0_deep", "cfg1_mini", "cfg1_mini_adj", "cfg2_mini", "cfg3_mini", "cfgD",

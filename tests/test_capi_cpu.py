@@ -137,8 +137,8 @@ def test_errors_map_to_reference_exception_classes():
     with pytest.raises(ValueError):  # no materials
         S.build_hierarchy(g, "CK", S.CoarseningPath([]))
     g.k, g.c = np.ones(4), np.ones(4)
-    with pytest.raises(ValueError):  # unsupported method letters fail loudly
-        S.build_hierarchy(g, "CP", S.CoarseningPath([]))
+    with pytest.raises(ValueError):  # FullST is causal-only (proj/src/transfer.cpp:44-47)
+        S.build_hierarchy(g, "BK", S.CoarseningPath([S.CoarseningDirection.FullST]))
     with pytest.raises(ValueError):
         S.build_hierarchy(g, "XX", S.CoarseningPath([]))
 
@@ -161,5 +161,5 @@ def test_dist_create_argument_errors_before_device_work():
 
     g = S.build_fine_grid(1.0, 1.0, 8, 8)
     g.k, g.c = np.ones(8), np.ones(8)
-    with pytest.raises(ValueError):  # Galerkin P is out of scope: rejected in the C layer, no device touched
+    with pytest.raises(ValueError):  # time slabs take causal K/D/R only: rejected in the C layer, no device touched
         S.build_dist_hierarchy(g, "CP", S.CoarseningPath([S.CoarseningDirection(0)]), world=1, rank=0)
