@@ -129,6 +129,14 @@ int stmg_apply_design(const double* chi, int64_t n, const stmg_material_pair* ma
 int stmg_load_vector(const stmg_grid* g, int32_t kind, const double* params, int32_t masked,
                      double* b);
 
+/* The same on the device: b is device memory of
+ * (n_t+1)(n_el+1) doubles on any GPU, filled by a kernel on cuda_stream (a
+ * cudaStream_t; NULL = legacy default stream), which is synchronised unless it is
+ * being captured.  Kinds 0 and 1 are bit-identical to stmg_load_vector; kinds 2 and
+ * 3 use the device sin / cos and agree to a few ulp. */
+int stmg_load_vector_device(const stmg_grid* g, int32_t kind, const double* params, int32_t masked,
+                            double* b, void* cuda_stream);
+
 /* load_vector with a caller callback q(x, t, ctx) (the std::function overload). */
 typedef double (*stmg_source_fn)(double x, double t, void* ctx);
 int stmg_load_vector_cb(const stmg_grid* g, stmg_source_fn q, void* ctx, int32_t masked,

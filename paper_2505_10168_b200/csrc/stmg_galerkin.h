@@ -44,9 +44,9 @@ struct Dia9Host {
 
 // Run f(lo, hi) over [0, n) on the host's cores (row-independent work only).
 template <class F>
-void parallel_rows(int64_t n, F&& f) {
+void parallel_rows(int64_t n, F&& f, int64_t serial_below = 65536) {
   unsigned nt = std::max(1u, std::thread::hardware_concurrency());
-  if (n < 65536) nt = 1;
+  if (n < serial_below) nt = 1;
   nt = std::min<unsigned>(nt, 64);
   if (nt == 1) {
     f(int64_t{0}, n);

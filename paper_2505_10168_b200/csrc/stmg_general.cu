@@ -247,7 +247,77 @@ __global__ void __launch_bounds__(512) k_block_march(BlockMarchView B, const dou
   }
 }
 
+// load_vector (proj/src/assembly.cpp:65-83) on the device, one thread per node:
+// node i of level n >= 1 receives (0.0 + q_{i-1}) + q_i, q_e = q(x_e, n dt) dx / 2
+// in the reference's element order; masked DOFs (n == 0 || i == 0) are zeroed as
+// assemble_system does (:128-130).  Sources: kind 0 uniform p0; 1 p0 on L - x < p1;
+// 2 1 + p0 sin(2 pi p1 t) on L - x < p2; 3 heat_load_value (:59-63).  Kinds 0 and
+// 1 are bit-identical to the host; 2 and 3 use the device sin / cos (<= 2 ulp).
+struct SourceParams {
+  int kind;
+  double p[3];
+  double L, t_T, dx, dt;
+  int64_t n_el, n_t;
+  int masked;
+};
+__device__ __forceinline__ double source_q(const SourceParams& S, double x, double t) {
+  switch (S.kind) {
+    case 0: return S.p[0];
+    case 1: return (S.L - x < S.p[1]) ? S.p[0] : 0.0;
+    case 2: return (S.L - x < S.p[2]) ? 1.0 + S.p[0] * sin(2.0 * 3.141592653589793 * S.p[1] * t) : 0.0;
+    default: {
+      const double xs = x / S.L - 0.5, ts = t / S.t_T - 0.5;
+      return (1.0 + cos(200.0 * (xs * xs + ts * ts))) * 1.0e6;
+    }
+  }
+}
+__global__ void k_load_vector(SourceParams S, double* __restrict__ b) {
+  const int64_t nn = S.n_el + 1, total = nn * (S.n_t + 1);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = q / nn, i = q - n * nn;
+    double v = 0.0;
+    if (n >= 1 && !(S.masked && i == 0)) {
+      const double t = static_cast<double>(n) * S.dt;
+      if (i >= 1) v += source_q(S, (static_cast<double>(i - 1) + 0.5) * S.dx, t) * S.dx / 2.0;
+      if (i <= S.n_el - 1) v += source_q(S, (static_cast<double>(i) + 0.5) * S.dx, t) * S.dx / 2.0;
+    }
+    b[q] = v;
+  }
+}
+
 }  // namespace
+
+int launch_load_vector(int kind, const double* params, int n_params, double L, double t_T, int64_t n_el,
+                       int64_t n_t, int masked, double* b, cudaStream_t s) {
+  SourceParams S{};
+  S.kind = kind;
+  for (int k = 0; k < n_params && k < 3; ++k) S.p[k] = params[k];
+  S.L = L;
+  S.t_T = t_T;
+  S.dx = L / static_cast<double>(n_el);
+  S.dt = t_T / static_cast<double>(n_t);
+  S.n_el = n_el;
+  S.n_t = n_t;
+  S.masked = masked;
+  const int64_t total = (n_el + 1) * (n_t + 1);
+  int64_t g = (total + kBlock - 1) / kBlock;
+  if (g > 148 * 64) g = 148 * 64;
+  k_load_vector<<<static_cast<unsigned>(g < 1 ? 1 : g), kBlock, 0, s>>>(S, b);
+  return check();
+}
+
+__global__ void k_scale(const double* __restrict__ x, double a, double* __restrict__ y, int64_t n) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    y[q] = x[q] * a;
+}
+
+int launch_scale(const double* x, double a, double* y, int64_t n, cudaStream_t s) {
+  int64_t g = (n + kBlock - 1) / kBlock;
+  if (g > 148 * 64) g = 148 * 64;
+  k_scale<<<static_cast<unsigned>(g < 1 ? 1 : g), kBlock, 0, s>>>(x, a, y, n);
+  return check();
+}
 
 int launch_g_sweep(const Dia9View& A, const double* f, const double* x, double* y, double omega,
                    cudaStream_t s) {

@@ -416,7 +416,7 @@ struct stmg_hierarchy {
   std::vector<std::unique_ptr<stmgb::DeviceBuf>> coef;  // per level
   std::vector<stmgb::LevelView> views;
   stmgb::CoarsestView coarsest{};
-  std::unique_ptr<stmgb::DeviceBuf> pcr_alpha, pcr_gamma, pcr_bfin, prop_tinv, prop_a, prop_chunk;
+  std::unique_ptr<stmgb::DeviceBuf> pcr_alpha, pcr_gamma, pcr_bfin, prop_tinv, prop_a, prop_chunk, pint_prop;
   std::shared_ptr<stmgb::Workspace> ws;
   cudaStream_t stream = nullptr;      // where work runs (own_stream or a caller's)
   cudaStream_t own_stream = nullptr;  // created with the hierarchy
@@ -475,6 +475,7 @@ struct stmg_hierarchy {
     prop_tinv.reset();
     prop_a.reset();
     prop_chunk.reset();
+    pint_prop.reset();
     ws.reset();
     cudaSetDevice(prev);
   }
@@ -493,6 +494,33 @@ struct DeviceGuard {
   }
   ~DeviceGuard() { cudaSetDevice(prev); }
 };
+
+// Parallel-in-time march tables for a wide coarsest level (n_el > 32, see
+// k_coarsest_pint): chunk length Lc, a power of two dividing n_t near
+// sqrt(1.5 n_t) (balancing 2 Lc PCR steps against n_t / Lc dense links), and
+// the chunk propagator A^Lc, A = -T^-1 S (column-major m x m), built on the
+// device by m parallel homogeneous marches with the march's own PCR step.
+// STMG_COARSEST_PINT=0 keeps the sequential march.  Needs the PCR tables.
+void build_pint(stmg_hierarchy* h) {
+  if (const char* v = std::getenv("STMG_COARSEST_PINT"))
+    if (std::atoi(v) == 0) return;
+  const int m = h->coarsest.m;
+  const int64_t nt = h->host.back().g.n_t;
+  if (m <= 32 || m > 4096 || nt < 64) return;
+  int64_t Lc = 1;
+  while (Lc * Lc < (3 * nt) / 2) Lc *= 2;
+  while (Lc > 1 && nt % Lc != 0) Lc /= 2;
+  const int64_t C = nt / Lc;
+  if (C < 2 || Lc < 4) return;
+  h->pint_prop = std::make_unique<DeviceBuf>(static_cast<int64_t>(m) * m);
+  h->coarsest.pint_len = static_cast<int32_t>(Lc);
+  launch_check(launch_coarsest_pint_prop(h->coarsest, h->pint_prop->p, h->own_stream ? h->own_stream : nullptr),
+               "pint propagator");
+  cuda_check(cudaStreamSynchronize(h->own_stream ? h->own_stream : nullptr), "sync");
+  h->coarsest.pint_prop = h->pint_prop->p;
+  h->coarsest.pint_chunks = static_cast<int32_t>(C);
+  h->device_bytes += static_cast<int64_t>(m) * m * 8;
+}
 
 // Parallel-cyclic-reduction factors of the coarsest step matrix (rows 1..n_el:
 // sub cm, diag c0, super cp), shared by every time level.
@@ -547,6 +575,9 @@ void build_pcr(stmg_hierarchy* h) {
   h->coarsest.prop_chunk = nullptr;
   h->coarsest.n_chunks = 0;
   h->coarsest.chunk_len = 0;
+  h->coarsest.pint_chunks = 0;
+  h->coarsest.pint_len = 0;
+  h->coarsest.pint_prop = nullptr;
   if (m >= 1 && m <= 32) {
     std::vector<double> Ti(32 * 32, 0.0), A(32 * 32, 0.0), S(32 * 32, 0.0);
     std::vector<double> sub(m), dia(m), sup(m), cpv(m), col(m);
@@ -636,6 +667,7 @@ void build_pcr(stmg_hierarchy* h) {
   h->coarsest.gamma = h->pcr_gamma->p;
   h->coarsest.bfin = h->pcr_bfin->p;
   h->device_bytes += static_cast<int64_t>((alpha.size() * 2 + b.size()) * 8);
+  build_pint(h);
 }
 
 // Level-API calls complete before returning, except while the caller is
@@ -767,7 +799,7 @@ std::shared_ptr<Workspace> make_workspace(const stmg_hierarchy* h, int64_t* byte
   ws->scalars = std::make_unique<DeviceBuf>(8);
   const int m = h->coarsest.m;
   const int64_t scratch = std::max<int64_t>(
-      {2 * static_cast<int64_t>(m), 32 * h->host.back().g.n_t, 2});
+      {2 * static_cast<int64_t>(m), 32 * h->host.back().g.n_t, coarsest_scratch(h->coarsest), 2});
   ws->coarse_scratch = std::make_unique<DeviceBuf>(scratch);
   *bytes += 8 * (max_partials + 8 + scratch);
   cuda_check(cudaMallocHost(&ws->pinned, 8 * sizeof(double)), "cudaMallocHost");
@@ -935,7 +967,7 @@ struct Emitter {
           launch_check(launch_coarsest(h->adjoint, h->coarsest, f, buf(l, 0), h->ws->coarse_scratch->p, s),
                        "coarsest");
       });
-      ++kernels;
+      kernels += h->galerkin(l) ? 1 : coarsest_launches(h->coarsest);
       return 0;
     }
     int cur = start;
@@ -1440,23 +1472,30 @@ void optimise(const stmg_grid* geom, const stmg_optimise_options& o, int device,
       o.mma_asym_shrink >= 1.0 || o.mma_asym_grow <= 1.0)
     throw std::invalid_argument("MmaUpdater: invalid options");
   const auto t0 = std::chrono::steady_clock::now();
+  // STMG_OPT_TIMING=1: per-phase host wall time on stderr (profiling aid)
+  const bool timing = std::getenv("STMG_OPT_TIMING") != nullptr;
+  double ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  auto tick = std::chrono::steady_clock::now();
+  auto lap = [&](int k) {
+    const auto now = std::chrono::steady_clock::now();
+    ph[k] += std::chrono::duration<double>(now - tick).count();
+    tick = now;
+  };
   const HostGrid g = make_grid(geom->L, geom->t_T, geom->n_el, geom->n_t);
   const int64_t ne = g.n_el, nn = ne + 1, ndof = nn * (g.n_t + 1);
   std::vector<double> chi(static_cast<size_t>(ne), o.chi_init), k(ne), c(ne);
-  std::vector<double> b(static_cast<size_t>(ndof));
-  load_vector_impl(g, [&](double x, double t) { return source_value(3, nullptr, x, t, g.L, g.t_T); },
-                   true, b.data());
   const double scale = g.dt / o.theta_ref;
-  std::vector<double> cvec(b);
-  for (double& v : cvec) v *= scale;  // adjoint_rhs, optimisation.cpp:26-32
   const std::vector<double> dg(static_cast<size_t>(ne), g.dx / (o.volume_limit * g.L));
   Mma mma{o.mma_x_min, o.mma_x_max, o.mma_move_limit, o.mma_asym_init, o.mma_asym_shrink,
           o.mma_asym_grow, static_cast<size_t>(ne)};
   DeviceGuard dgd(device);
   DeviceBuf d_b(ndof), d_c(ndof), d_u(ndof), d_lam(ndof), d_dk(ne), d_dc(ne), d_sens(ne), d_part(1184 * 2),
       d_s(2);
-  cuda_check(cudaMemcpy(d_b.p, b.data(), ndof * 8, cudaMemcpyHostToDevice), "b upload");
-  cuda_check(cudaMemcpy(d_c.p, cvec.data(), ndof * 8, cudaMemcpyHostToDevice), "c upload");
+  // b = load_vector(g) with masking (optimisation.cpp:102; assembly.cpp:59-83, 128-130) and
+  // the adjoint right-hand side c = b dt / theta_ref (adjoint_rhs, optimisation.cpp:26-32),
+  // both generated on the device
+  launch_check(launch_load_vector(3, nullptr, 0, g.L, g.t_T, g.n_el, g.n_t, 1, d_b.p, nullptr), "load_vector");
+  launch_check(launch_scale(d_b.p, scale, d_c.p, ndof, nullptr), "scale");
   cuda_check(cudaMemset(d_u.p, 0, ndof * 8), "memset");
   cuda_check(cudaMemset(d_lam.p, 0, ndof * 8), "memset");
   std::unique_ptr<stmg_hierarchy> h, ht;
@@ -1468,6 +1507,7 @@ void optimise(const stmg_grid* geom, const stmg_optimise_options& o, int device,
   int stable = 0;
   *converged = 0;
   *n_records = 0;
+  lap(0);
   for (int it = 1; it <= o.max_iterations; ++it) {
     simp(chi.data(), ne, o.mat, k.data(), c.data());
     std::vector<int32_t> dirs(static_cast<size_t>(std::max(o.n_levels - 1, 0)));
@@ -1500,9 +1540,11 @@ void optimise(const stmg_grid* geom, const stmg_optimise_options& o, int device,
       ht.reset(tp);
       cur_dirs = dirs;
     }
+    lap(1);
     if (!o.warm_start) cuda_check(cudaMemset(d_u.p, 0, ndof * 8), "memset");
     stmg_solve_report pr{}, ar{};
     solve(h.get(), d_b.p, d_u.p, o.solve, &pr, hist.data(), static_cast<int32_t>(hist.size()));
+    lap(2);
     // objective_value = dot(b, u) dt / theta_ref (optimisation.cpp:21-24)
     int64_t np = 0;
     launch_check(launch_dot(d_b.p, d_u.p, ndof, d_part.p, &np, h->stream), "dot");
@@ -1512,7 +1554,9 @@ void optimise(const stmg_grid* geom, const stmg_optimise_options& o, int device,
     sync_unless_capturing(h->stream);
     const double theta = dotbu * g.dt / o.theta_ref;
     if (!o.warm_start) cuda_check(cudaMemset(d_lam.p, 0, ndof * 8), "memset");
+    lap(3);
     solve(ht.get(), d_c.p, d_lam.p, o.solve, &ar, hist.data(), static_cast<int32_t>(hist.size()));
+    lap(4);
     double vsum = 0.0;
     for (double v : chi) vsum += v;
     const double vol = vsum * g.dx / g.L;
@@ -1558,7 +1602,13 @@ void optimise(const stmg_grid* geom, const stmg_optimise_options& o, int device,
     cuda_check(cudaMemcpyAsync(sens.data(), d_sens.p, ne * 8, cudaMemcpyDeviceToHost, h->stream), "d2h");
     sync_unless_capturing(h->stream);
     chi = mma.update(chi, sens, dg, g_val);
+    lap(5);
   }
+  if (timing)
+    std::fprintf(stderr,
+                 "optimise timing [s]: setup %.3f, plan+levels+refresh %.3f, primal %.3f, objective %.3f, "
+                 "adjoint %.3f, sensitivities+mma %.3f\n",
+                 ph[0], ph[1], ph[2], ph[3], ph[4], ph[5]);
   std::memcpy(chi_out, chi.data(), sizeof(double) * static_cast<size_t>(ne));
   *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -1595,6 +1645,27 @@ int stmg_load_vector(const stmg_grid* g, int32_t kind, const double* params, int
     for (int i = 0; i < np; ++i) p[i] = params[i];
     load_vector_impl(hg, [&](double x, double t) { return source_value(kind, p, x, t, hg.L, hg.t_T); },
                      masked != 0, b);
+  });
+}
+
+int stmg_load_vector_device(const stmg_grid* g, int32_t kind, const double* params, int32_t masked,
+                            double* b, void* cuda_stream) {
+  return guarded([&] {
+    if (!g || !b) throw std::invalid_argument("load_vector: null argument");
+    const HostGrid hg = make_grid(g->L, g->t_T, g->n_el, g->n_t);
+    const int np = kind == 0 ? 1 : kind == 1 ? 2 : kind == 2 ? 3 : 0;
+    if (kind < 0 || kind > 3) throw std::invalid_argument("load_vector: unknown source kind");
+    if (np > 0 && !params) throw std::invalid_argument("load_vector: missing source parameters");
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, b) != cudaSuccess || a.type != cudaMemoryTypeDevice) {
+      cudaGetLastError();
+      throw std::invalid_argument("load_vector_device: b is not device memory");
+    }
+    DeviceGuard dg(a.device);
+    launch_check(launch_load_vector(kind, params, np, hg.L, hg.t_T, hg.n_el, hg.n_t, masked != 0, b,
+                                    static_cast<cudaStream_t>(cuda_stream)),
+                 "load_vector");
+    sync_unless_capturing(static_cast<cudaStream_t>(cuda_stream));
   });
 }
 

@@ -55,7 +55,19 @@ struct CoarsestView {
   int32_t n_chunks;
   int32_t chunk_len;
   const double* prop_chunk;
+  // n_el > 32 (wide coarsest levels, e.g. config 4's 256 x 8192): parallel-in-time
+  // march over pint_chunks chunks of pint_len steps, one CTA per chunk, linked by
+  // the dense propagator A^pint_len (m x m, column-major); 0 chunks = sequential.
+  int32_t pint_chunks;
+  int32_t pint_len;
+  const double* pint_prop;
 };
+// Kernel launches one coarsest solve issues (the parallel-in-time march is three).
+inline int coarsest_launches(const CoarsestView& cv) { return cv.m > 32 && cv.pint_chunks > 1 ? 3 : 1; }
+// Scratch doubles the coarsest solve needs (chunk start states of the PinT march).
+inline int64_t coarsest_scratch(const CoarsestView& cv) {
+  return cv.m > 32 && cv.pint_chunks > 1 ? (int64_t)cv.pint_chunks * cv.m : 0;
+}
 
 // Shared memory of the chunked coarsest march: g (n_t x 32), chunk end and
 // start states (2 C + 1) x 32, one 32-double vector slot per warp (<= 16).
@@ -115,6 +127,11 @@ int launch_xfer_restrict(const XferView& T, const double* r, double* fc, cudaStr
 int launch_xfer_prolong_add(const XferView& T, const double* xc, const double* x, double* y,
                             cudaStream_t s);
 int launch_block_march(const BlockMarchView& B, const double* f, double* x, cudaStream_t s);
+// y = x * a (y may alias x)
+int launch_scale(const double* x, double a, double* y, int64_t n, cudaStream_t s);
+// load_vector(g, q) + masking into device memory (source kinds as stmg_load_vector)
+int launch_load_vector(int kind, const double* params, int n_params, double L, double t_T, int64_t n_el,
+                       int64_t n_t, int masked, double* b, cudaStream_t s);
 
 // ---- kernel launchers (stmg_kernels.cu); all asynchronous on `s` ------------------
 // One damped-Jacobi sweep y = x + omega (f - J x) / diag.  If partials != nullptr,
@@ -152,6 +169,8 @@ int launch_prolong_add(const LevelView& F, const LevelView& C, int dir, const do
                        cudaStream_t s);
 int launch_coarsest(bool adjoint, const CoarsestView& cv, const double* f, double* x,
                     double* scratch, cudaStream_t s);
+// A^pint_len (column-major m x m) into P by m parallel homogeneous marches
+int launch_coarsest_pint_prop(const CoarsestView& cv, double* P, cudaStream_t s);
 // Sum of n_partials doubles in a fixed order into *out (device scalar).
 int launch_finalize_sum(const double* partials, int64_t n, double* out, cudaStream_t s);
 // Sum of squares of x[0..n) into partials (fixed grid) then *out.

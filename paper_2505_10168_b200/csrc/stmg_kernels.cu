@@ -1574,6 +1574,125 @@ __global__ void __launch_bounds__(1024) k_coarsest(CoarsestView cv, const double
   }
 }
 
+// Parallel-in-time exact march for wide coarsest levels (n_el > 32).  The march
+// x_n = T^-1 (f_n - S x_{n'}) (n' the coupled level) is affine in its start
+// state, so the n_t steps are cut into C chunks of Lc steps:
+//   PHASE 0 (C CTAs): each chunk marches from a zero start state (chunk 0's first
+//     step is uncoupled, so chunk 0 is exact); CTA 0 also writes masked rows;
+//   link (1 CTA): true chunk-end states s_c = y_end(c) + A^Lc s_{c-1};
+//   PHASE 1 (C - 1 CTAs): chunk c >= 1 adds the homogeneous march from s_{c-1},
+//     z_k = T^-1 (-S z_{k-1}), to its levels.
+// Sequential depth 2 Lc + C instead of n_t.  Per step one tridiagonal solve by
+// PCR over shared memory with the host-precomputed factors (as k_coarsest); the
+// state stays in shared memory.  An exact solve like the reference's SparseLU,
+// agreeing to rounding.
+template <bool ADJ, int PHASE>
+__global__ void __launch_bounds__(1024) k_coarsest_pint(CoarsestView cv, const double* __restrict__ f,
+                                                        double* __restrict__ x,
+                                                        const double* __restrict__ starts) {
+  pdl_entry();
+  extern __shared__ double smem[];
+  const LevelView& L = cv.lv;
+  const int m = cv.m;
+  const int64_t nn = L.nn, nt = L.n_t;
+  const int tid = threadIdx.x, bs = blockDim.x;
+  // PHASE 2 (propagator build): CTA e marches the unit vector e through Lc
+  // homogeneous steps and stores the result as column e of A^Lc (in `x`).
+  const int c = PHASE == 0 ? blockIdx.x : blockIdx.x + 1;
+  double* prev = smem;
+  double* d0 = smem + m;
+  double* d1 = smem + 2 * m;
+  if (PHASE == 0 && c == 0) {
+    for (int64_t i = tid; i < nn; i += bs) x[i] = f[i] / L.w;
+    for (int64_t n = 1 + tid; n <= nt; n += bs) x[n * nn] = f[n * nn] / L.w;
+  }
+  for (int j = tid; j < m; j += bs)
+    prev[j] = PHASE == 0 ? 0.0 : PHASE == 2 ? (j == (int)blockIdx.x ? 1.0 : 0.0) : starts[(int64_t)(c - 1) * m + j];
+  const double* om = L.coef + kOm * nn;
+  const double* o0 = L.coef + kO0 * nn;
+  const double* op = L.coef + kOp * nn;
+  const int64_t s0 = (int64_t)c * cv.pint_len + 1;
+  __syncthreads();
+  for (int64_t s = s0; s < s0 + cv.pint_len; ++s) {
+    const int64_t n = ADJ ? nt + 1 - s : s;
+    const bool coupled = PHASE == 2 || s >= 2;
+    for (int j = tid; j < m; j += bs) {
+      const int64_t i = j + 1;
+      double acc = PHASE == 0 ? f[n * nn + i] : 0.0;
+      if (coupled) {
+        if (i >= 2) acc = acc - om[i] * prev[j - 1];
+        acc = acc - o0[i] * prev[j];
+        if (i <= m - 1) acc = acc - op[i] * prev[j + 1];
+      }
+      d0[j] = acc;
+    }
+    __syncthreads();
+    double* a = d0;
+    double* b = d1;
+    for (int k = 0; k < cv.n_steps; ++k) {
+      const int st = 1 << k;
+      for (int j = tid; j < m; j += bs) {
+        double v = a[j];
+        if (j - st >= 0) v = v + cv.alpha[(int64_t)k * m + j] * a[j - st];
+        if (j + st < m) v = v + cv.gamma[(int64_t)k * m + j] * a[j + st];
+        b[j] = v;
+      }
+      __syncthreads();
+      double* t = a;
+      a = b;
+      b = t;
+    }
+    for (int j = tid; j < m; j += bs) {
+      const double v = a[j] / cv.bfin[j];
+      prev[j] = v;
+      if (PHASE != 2) {
+        double* xp = x + n * nn + j + 1;
+        *xp = PHASE == 0 ? v : *xp + v;
+      }
+    }
+    __syncthreads();
+  }
+  if (PHASE == 2)
+    for (int j = tid; j < m; j += bs) x[(int64_t)blockIdx.x * m + j] = prev[j];
+}
+
+// Chunk links of k_coarsest_pint: starts[c] = y_end(c) + A^Lc starts[c - 1]
+// (starts[0] = y_end(0)); y_end(c) is PHASE 0's value at the chunk's last level.
+template <bool ADJ>
+__global__ void __launch_bounds__(1024) k_coarsest_pint_link(CoarsestView cv, const double* __restrict__ x,
+                                                             double* __restrict__ starts) {
+  pdl_entry();
+  extern __shared__ double sp[];
+  const int m = cv.m;
+  const int64_t nn = cv.lv.nn, nt = cv.lv.n_t;
+  const int tid = threadIdx.x, bs = blockDim.x;
+  auto end_level = [&](int64_t c) {
+    const int64_t s = (c + 1) * cv.pint_len;
+    return ADJ ? nt + 1 - s : s;
+  };
+  for (int j = tid; j < m; j += bs) {
+    const double v = x[end_level(0) * nn + j + 1];
+    sp[j] = v;
+    starts[j] = v;
+  }
+  __syncthreads();
+  for (int64_t c = 1; c < cv.pint_chunks; ++c) {
+    const int64_t ne = end_level(c);
+    double v[4];
+    int cnt = 0;
+    for (int j = tid; j < m; j += bs, ++cnt) {
+      double acc = x[ne * nn + j + 1];
+      for (int k = 0; k < m; ++k) acc = fma(cv.pint_prop[(int64_t)k * m + j], sp[k], acc);
+      v[cnt] = acc;
+      starts[c * m + j] = acc;
+    }
+    __syncthreads();
+    cnt = 0;
+    for (int j = tid; j < m; j += bs, ++cnt) sp[j] = v[cnt];
+    __syncthreads();
+  }
+}
+
 // Coarsest exact solve for n_el <= 32: one warp, lane j owns unmasked node
 // j + 1.  Per time level: right-hand side with the coupled level's values
 // (shuffles), then PCR by shuffles with the same precomputed factors and the
@@ -1658,6 +1777,9 @@ __global__ void __launch_bounds__(32) k_coarsest_warp(CoarsestView cv, const dou
 // (objective_sensitivities, proj/src/optimisation.cpp:34-73): one thread per
 // element, time levels accumulated in the reference's order, masked DOFs read
 // as zero, so the result is the reference's bit for bit for the same u, lambda.
+// The loads of kSensBatch levels are issued before their (sequential)
+// accumulation, so the few element threads keep many loads in flight.
+constexpr int kSensBatch = 16;
 __global__ void k_sensitivities(int64_t n_el, int64_t n_t, double dt, const double* __restrict__ dk_dx,
                                 const double* __restrict__ dc_dx6, const double* __restrict__ u,
                                 const double* __restrict__ lam, double* __restrict__ sens) {
@@ -1666,17 +1788,32 @@ __global__ void k_sensitivities(int64_t n_el, int64_t n_t, double dt, const doub
   if (e >= n_el) return;
   const int64_t nn = n_el + 1;
   const double kd = dk_dx[e], cd = dc_dx6[e];
-  auto at = [&](const double* v, int64_t n, int64_t i) -> double {
-    return (n == 0 || i == 0) ? 0.0 : v[n * nn + i];
-  };
+  const bool left_masked = e == 0;  // node i = e is the Dirichlet node
   double acc = 0.0;
-  for (int64_t n = 1; n <= n_t; ++n) {
-    const double u0 = at(u, n, e), u1 = at(u, n, e + 1);
-    const double l0 = at(lam, n, e), l1 = at(lam, n, e + 1);
-    acc = acc + (kd * (u0 - u1)) * (l0 - l1);
-    const double v0 = (u0 - at(u, n - 1, e)) / dt;
-    const double v1 = (u1 - at(u, n - 1, e + 1)) / dt;
-    acc = acc + cd * (l0 * (2.0 * v0 + v1) + l1 * (v0 + 2.0 * v1));
+  double p0 = 0.0, p1 = 0.0;  // u at level n - 1 (level 0 is masked)
+  for (int64_t n0 = 1; n0 <= n_t; n0 += kSensBatch) {
+    double U0[kSensBatch], U1[kSensBatch], L0[kSensBatch], L1[kSensBatch];
+#pragma unroll
+    for (int k = 0; k < kSensBatch; ++k) {
+      const int64_t n = n0 + k;
+      const bool ok = n <= n_t;
+      const int64_t r = (ok ? n : n_t) * nn + e;
+      U0[k] = ok && !left_masked ? u[r] : 0.0;
+      U1[k] = ok ? u[r + 1] : 0.0;
+      L0[k] = ok && !left_masked ? lam[r] : 0.0;
+      L1[k] = ok ? lam[r + 1] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < kSensBatch; ++k) {
+      if (n0 + k > n_t) break;
+      const double u0 = U0[k], u1 = U1[k], l0 = L0[k], l1 = L1[k];
+      acc = acc + (kd * (u0 - u1)) * (l0 - l1);
+      const double v0 = (u0 - p0) / dt;
+      const double v1 = (u1 - p1) / dt;
+      acc = acc + cd * (l0 * (2.0 * v0 + v1) + l1 * (v0 + 2.0 * v1));
+      p0 = u0;
+      p1 = u1;
+    }
   }
   sens[e] = -acc;
 }
@@ -2283,8 +2420,31 @@ int launch_prolong_add(const LevelView& F, const LevelView& C, int dir, const do
   return check_launch();
 }
 
+int launch_coarsest_pint_prop(const CoarsestView& cv, double* P, cudaStream_t s) {
+  const size_t smem = sizeof(double) * 3 * (size_t)cv.m;
+  const int threads = cv.m >= 1024 ? 1024 : (int)((cv.m + 31) / 32 * 32);
+  pdl_launch(k_coarsest_pint<false, 2>, cv.m, threads, smem, s, cv, (const double*)nullptr, P,
+             (const double*)nullptr);
+  return check_launch();
+}
+
 int launch_coarsest(bool adjoint, const CoarsestView& cv, const double* f, double* x,
                     double* scratch, cudaStream_t s) {
+  if (cv.m > 32 && cv.pint_chunks > 1 && scratch != nullptr) {
+    const size_t smem = sizeof(double) * 3 * (size_t)cv.m;
+    int threads = cv.m >= 1024 ? 1024 : (int)((cv.m + 31) / 32 * 32);
+    const int C = cv.pint_chunks;
+    if (adjoint) {
+      pdl_launch(k_coarsest_pint<true, 0>, C, threads, smem, s, cv, f, x, (const double*)scratch);
+      pdl_launch(k_coarsest_pint_link<true>, 1, threads, sizeof(double) * (size_t)cv.m, s, cv, x, scratch);
+      pdl_launch(k_coarsest_pint<true, 1>, C - 1, threads, smem, s, cv, f, x, (const double*)scratch);
+    } else {
+      pdl_launch(k_coarsest_pint<false, 0>, C, threads, smem, s, cv, f, x, (const double*)scratch);
+      pdl_launch(k_coarsest_pint_link<false>, 1, threads, sizeof(double) * (size_t)cv.m, s, cv, x, scratch);
+      pdl_launch(k_coarsest_pint<false, 1>, C - 1, threads, smem, s, cv, f, x, (const double*)scratch);
+    }
+    return check_launch();
+  }
   if (cv.m <= 32 && cv.prop_chunk != nullptr && cv.n_chunks > 1) {
     const size_t bytes = coarsest_chunked_smem(cv);
     if (bytes <= 160 * 1024) {
@@ -2349,6 +2509,11 @@ int kernels_init() {
     if (e != cudaSuccess) return static_cast<int>(e);
   }
   for (auto fn : {k_tail<true, GridScope>, k_tail<false, GridScope>}) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    if (e != cudaSuccess) return static_cast<int>(e);
+  }
+  for (auto fn : {k_coarsest_pint<true, 0>, k_coarsest_pint<true, 1>, k_coarsest_pint<false, 0>,
+                  k_coarsest_pint<false, 1>, k_coarsest_pint<false, 2>}) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     if (e != cudaSuccess) return static_cast<int>(e);
   }
@@ -2423,7 +2588,8 @@ int launch_finalize_sum(const double* partials, int64_t n, double* out, cudaStre
 int launch_sensitivities(int64_t n_el, int64_t n_t, double dt, const double* dk_dx,
                          const double* dc_dx6, const double* u, const double* lam, double* sens,
                          cudaStream_t s) {
-  pdl_launch(k_sensitivities, (unsigned)((n_el + 127) / 128), 128, 0, s, n_el, n_t, dt, dk_dx, dc_dx6, u, lam, sens);
+  // 32-thread blocks spread the n_el element threads over every SM
+  pdl_launch(k_sensitivities, (unsigned)((n_el + 31) / 32), 32, 0, s, n_el, n_t, dt, dk_dx, dc_dx6, u, lam, sens);
   return check_launch();
 }
 

@@ -55,6 +55,7 @@ def _load():
         "stmg_apply_design": [vp, i64, vp, vp, vp],
         "stmg_load_vector": [vp, i32, vp, i32, vp],
         "stmg_load_vector_cb": [vp, vp, vp, i32, vp],
+        "stmg_load_vector_device": [vp, i32, vp, i32, vp, vp],
         "stmg_plan_coarsening": [vp, vp, vp, vp, vp, vp, vp, vp],
         "stmg_hierarchy_create": [vp, vp, vp, vp, vp, C.c_char_p, i32, vp, i32, C.POINTER(vp)],
         "stmg_hierarchy_transposed": [vp, C.POINTER(vp)],
@@ -334,6 +335,24 @@ def load_vector(g: SpaceTimeGrid, q: Optional[Callable[[float, float], float]] =
         kind = 3
     p = (C.c_double * 4)(*list(params)[:4])
     _check(_lib.stmg_load_vector(C.byref(gc), int(kind), p, 1 if masked else 0, b.ctypes.data))
+    return b
+
+
+def load_vector_device(g: SpaceTimeGrid, *, kind: int = 3, params=(), masked: bool = True, out=None,
+                       stream=None):
+    """load_vector for a preset source ``kind``, evaluated by a CUDA kernel into a
+    float64 torch tensor on the GPU (``out`` or a new tensor on cuda:0); kinds 0/1
+    bit-identical to load_vector, kinds 2/3 within a few ulp (device sin/cos)."""
+    import torch
+
+    b = out if out is not None else torch.empty(g.n_dofs(), dtype=torch.float64, device="cuda:0")
+    if b.numel() != g.n_dofs() or b.dtype != torch.float64 or not b.is_cuda or not b.is_contiguous():
+        raise ValueError("load_vector_device: out must be a contiguous float64 CUDA tensor of n_dofs")
+    gc = g._c()
+    p = (C.c_double * 4)(*list(params)[:4])
+    s = stream if stream is not None else torch.cuda.current_stream(b.device).cuda_stream
+    _check(_lib.stmg_load_vector_device(C.byref(gc), int(kind), p, 1 if masked else 0, b.data_ptr(),
+                                        C.c_void_p(s)))
     return b
 
 

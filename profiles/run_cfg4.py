@@ -29,6 +29,8 @@ def main():
            "iterations": res.iterations, "total_seconds": res.seconds,
            "stmg_seconds": sum(r["primal_seconds"] + r["adjoint_seconds"] for r in h),
            "primal_cycles": [r["primal_cycles"] for r in h], "adjoint_cycles": [r["adjoint_cycles"] for r in h],
+           "primal_seconds": [round(r["primal_seconds"], 5) for r in h],
+           "adjoint_seconds": [round(r["adjoint_seconds"], 5) for r in h],
            "statuses": sorted({(r["primal_status"], r["adjoint_status"]) for r in h}),
            "theta_first_last": [h[0]["theta"], h[-1]["theta"]], "volume_last": h[-1]["volume"]}
     print(json.dumps(out))

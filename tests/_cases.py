@@ -110,6 +110,11 @@ def case(name: str) -> Case:
         return cc
     if name == "cfg4_mini":
         return _from_cfg(name, C.cfg4(n_el=256, n_t=1024), n_levels=8, nu=5)
+    if name in ("wide_coarsest", "wide_coarsest_adj"):  # 64 x 1024 coarsest: the parallel-in-time march
+        cc = _from_cfg(name, C.cfg4(n_el=256, n_t=1024), n_levels=3, nu=5,
+                       adjoint=name.endswith("_adj"))
+        cc.dirs = np.asarray([0, 0], np.int32)
+        return cc
     if name in GENERAL:
         kind, ne, nt, method, dirs, adjoint, nu = GENERAL[name]
         if kind == "cfg1":
@@ -146,4 +151,4 @@ GENERAL_CASES = list(GENERAL)
 
 SMALL_CASES = ["cfg0", "cfg0_deep", "cfg1_mini", "cfg1_mini_adj", "cfg2_mini", "cfg3_mini", "cfgD",
                "cfgK_contrast", "time_first", "space_first", "single_level", "tiny", "wide_short",
-               "cfg4_mini"]
+               "cfg4_mini", "wide_coarsest", "wide_coarsest_adj"]

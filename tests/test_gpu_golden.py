@@ -119,7 +119,8 @@ def test_cfg2_full_scale_properties(S):
                                               reassembly=S.ReassemblyMethod(cfg.reassembly),
                                               min_elements=cfg.min_elements))
     h = S.build_hierarchy(g, cfg.method, path)
-    b1 = torch.from_numpy(S.load_vector(g, kind=cfg.source_kind, params=cfg.source_params, masked=True)).cuda()
+    # right-hand side generated on the device (8.6 GB; tests/test_gpu_load_vector.py pins it)
+    b1 = S.load_vector_device(g, kind=cfg.source_kind, params=cfg.source_params, masked=True)
     gen = torch.Generator(device="cuda").manual_seed(3)
     b2 = torch.rand(b1.numel(), dtype=torch.float64, device="cuda", generator=gen)
     b2.view(cfg.n_t + 1, cfg.n_el + 1)[0].zero_()
