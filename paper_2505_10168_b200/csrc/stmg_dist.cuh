@@ -608,6 +608,7 @@ void dist_solve(stmg_dist* d, const double* b, double* u, const stmg_solve_optio
   } else {
     rep->status = STMG_MAX_CYCLES;
     for (int cycle = 1; cycle <= o.max_cycles; ++cycle) {
+      Nvtx cyc("stmg::dist_v_cycle");
       cuda_check(cudaGraphLaunch(g->exec, d->stream), "graph launch");
       launches += g->kernels;
       if (g->final_buf != 0) throw std::logic_error("dist: level-0 iterate left the primary buffer");

@@ -20,6 +20,8 @@
 #include <tuple>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/stmg_b200.h"
 #include "stmg_internal.h"
 #include "stmg_galerkin.h"
@@ -28,6 +30,15 @@ namespace stmgb {
 namespace {
 
 thread_local std::string g_error;
+
+// NVTX range for Nsight timelines (header-only NVTX 3: a no-op unless a tool
+// is attached).  Graph replays show as one range per V-cycle.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
@@ -1052,6 +1063,7 @@ GraphEntry& get_graph(stmg_hierarchy* h, int nu, double omega) {
   const GraphKey key{nu, omega, h->profiling};  // (int mode; 0 = off)
   auto it = h->graphs.find(key);
   if (it != h->graphs.end()) return it->second;
+  Nvtx range("stmg::capture_v_cycle");
   GraphEntry e;
   Emitter em{h, nu, omega, h->cap_stream};
   if (h->profiling) {
@@ -1106,6 +1118,7 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
     throw std::invalid_argument("mg_solve: invalid options");
   if (!history || cap < o.max_cycles + 1)
     throw std::invalid_argument("mg_solve: history buffer smaller than max_cycles + 1");
+  Nvtx range(h->adjoint ? "stmg::mg_solve(adjoint)" : "stmg::mg_solve");
   DeviceGuard dg(h->device);
   const auto t0 = std::chrono::steady_clock::now();
   const int64_t n = h->ndofs(0);
@@ -1148,6 +1161,7 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
   } else {
     rep->status = STMG_MAX_CYCLES;
     for (int cycle = 1; cycle <= o.max_cycles; ++cycle) {
+      Nvtx cyc("stmg::v_cycle");
       cuda_check(cudaGraphLaunch(g->exec, h->stream), "graph launch");
       launches += g->kernels;
       if (g->final_buf != 0) throw std::logic_error("level-0 iterate left the primary buffer");
@@ -1509,6 +1523,7 @@ void optimise(const stmg_grid* geom, const stmg_optimise_options& o, int device,
   *n_records = 0;
   lap(0);
   for (int it = 1; it <= o.max_iterations; ++it) {
+    Nvtx range("stmg::optimise_iteration");
     simp(chi.data(), ne, o.mat, k.data(), c.data());
     std::vector<int32_t> dirs(static_cast<size_t>(std::max(o.n_levels - 1, 0)));
     plan(g, k.data(), c.data(), chi.data(), &o.mat, preq, dirs.data(), nullptr);
@@ -1709,6 +1724,7 @@ int stmg_hierarchy_create(const stmg_grid* g, const double* k, const double* c, 
     if (!out) throw std::invalid_argument("build_hierarchy: null output handle");
     *out = nullptr;
     if (!g) throw std::invalid_argument("build_hierarchy: null grid");
+    Nvtx range("stmg::build_hierarchy");
     auto h = std::make_unique<stmg_hierarchy>();
     // argument errors (the reference's invalid_argument) are raised before any device work
     h->host = make_host_levels(g, k, c, chi, mat, method, n_dirs, dirs, &h->reassembly, &h->bilinear, &h->gal);
@@ -1725,6 +1741,7 @@ int stmg_hierarchy_create(const stmg_grid* g, const double* k, const double* c, 
 int stmg_hierarchy_transposed(const stmg_hierarchy* src, stmg_hierarchy** out) {
   return guarded([&] {
     if (!src || !out) throw std::invalid_argument("transposed_hierarchy: null argument");
+    Nvtx range("stmg::transposed_hierarchy");
     auto h = std::make_unique<stmg_hierarchy>();
     h->device = src->device;
     h->adjoint = !src->adjoint;
