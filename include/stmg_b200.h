@@ -225,9 +225,11 @@ int stmg_level_sweeps(stmg_hierarchy* h, int32_t level, const double* f, double*
                       int32_t sweeps, double omega);
 /* Benchmark form: `launches` back-to-back kernel launches ping-ponging between
  * x and y (x -> y -> x ...), each a single sweep (fused_pairs = 0), a fused
- * two-sweep pass (fused_pairs = 1) or a fused 3- or 4-sweep pass (fused_pairs =
- * 3, 4); asynchronous on the hierarchy's stream, no copies.  The iterate ends
- * in x after an even number of launches. */
+ * two-sweep pass (fused_pairs = 1), a fused 3- or 4-sweep pass (fused_pairs =
+ * 3, 4) or the fused pair through the bulk-copy pipelined kernel (fused_pairs =
+ * 5; f, x and y then need 512 doubles of tail padding); asynchronous on the
+ * hierarchy's stream, no copies.  The iterate ends in x after an even number of
+ * launches. */
 int stmg_level_sweep_kernels(stmg_hierarchy* h, int32_t level, const double* f, double* x, double* y,
                              int32_t launches, int32_t fused_pairs, double omega);
 /* r = f - J_l x  (csr_residual) */

@@ -767,12 +767,22 @@ void upload_general(stmg_hierarchy* h) {
   }
 }
 
+// Levels with at least this many DOFs run their fused pairs through the
+// bulk-copy pipelined kernel (k_bulk); STMG_BULK_DOFS overrides (0 = never).
+constexpr int64_t kBulkDofs = 0;
+int64_t bulk_for(int64_t dofs) {
+  int64_t lim = kBulkDofs;
+  if (const char* v = std::getenv("STMG_BULK_DOFS")) lim = std::atoll(v);
+  return lim > 0 && dofs >= lim ? 1 : 0;
+}
+
 void upload_levels(stmg_hierarchy* h) {
   h->coef.clear();
   h->views.clear();
   for (const HostLevel& hl : h->host) {
     const std::vector<double> t = hl.table(h->adjoint);
-    auto buf = std::make_unique<DeviceBuf>(static_cast<int64_t>(t.size()));
+    // tail padding: the bulk-copy kernels copy coefficient rows rounded out to 16 bytes
+    auto buf = std::make_unique<DeviceBuf>(static_cast<int64_t>(t.size()) + kVecPad);
     cuda_check(cudaMemcpy(buf->p, t.data(), t.size() * 8, cudaMemcpyHostToDevice), "coef upload");
     LevelView v;
     v.n_el = hl.g.n_el;
@@ -785,8 +795,9 @@ void upload_levels(stmg_hierarchy* h) {
     v.n_hi = hl.g.n_t + 1;
     v.tile_nt = tile_nt_for(v.nn * (v.n_t + 1));
     v.sweep_depth = sweep_depth_for(v.nn * (v.n_t + 1));
+    v.bulk = bulk_for(v.nn * (v.n_t + 1));
     h->views.push_back(v);
-    h->device_bytes += static_cast<int64_t>(t.size() * 8);
+    h->device_bytes += static_cast<int64_t>((t.size() + kVecPad) * 8);
     h->coef.push_back(std::move(buf));
   }
   build_pcr(h);
@@ -799,11 +810,12 @@ std::shared_ptr<Workspace> make_workspace(const stmg_hierarchy* h, int64_t* byte
   int64_t max_partials = sumsq_partials_needed(0);
   for (int l = 0; l < nl; ++l) {
     const int64_t nd = h->ndofs(l);
-    ws->f.push_back(std::make_unique<DeviceBuf>(nd));
-    ws->xa.push_back(std::make_unique<DeviceBuf>(nd));
+    // kVecPad doubles of tail padding: the bulk-copy kernels round row copies out to 16 bytes
+    ws->f.push_back(std::make_unique<DeviceBuf>(nd + kVecPad));
+    ws->xa.push_back(std::make_unique<DeviceBuf>(nd + kVecPad));
     // the coarsest level never ping-pongs unless it is also level 0
-    ws->xb.push_back(std::make_unique<DeviceBuf>(l < nl - 1 || nl == 1 ? nd : 0));
-    *bytes += 8 * (3 * nd);
+    ws->xb.push_back(std::make_unique<DeviceBuf>(l < nl - 1 || nl == 1 ? nd + kVecPad : 0));
+    *bytes += 8 * (3 * (nd + kVecPad));
     max_partials = std::max(max_partials, sweep_partials_needed(h->views[l]));
   }
   ws->partials = std::make_unique<DeviceBuf>(max_partials);
@@ -841,8 +853,10 @@ void finish_create(stmg_hierarchy* h, bool share_ws_from_other, const stmg_hiera
     // same tiling as the hierarchy whose workspace (norm partials) is shared
     for (size_t l = 0; l < h->views.size() && l < other->views.size(); ++l)
       h->views[l].tile_nt = other->views[l].tile_nt;
-    for (size_t l = 0; l < h->views.size() && l < other->views.size(); ++l)
+    for (size_t l = 0; l < h->views.size() && l < other->views.size(); ++l) {
       h->views[l].sweep_depth = other->views[l].sweep_depth;
+      h->views[l].bulk = other->views[l].bulk;
+    }
     h->ws = other->ws;
   } else {
     int64_t bytes = 0;
@@ -925,7 +939,10 @@ struct Emitter {
     }
     for (; count >= 2; count -= 2) {
       timed_launch(l, kTimedSweep2, [&] {
-        launch_check(launch_sweep2(h->adjoint, L, f, buf(l, cur), buf(l, 1 - cur), omega, s), "sweep2");
+        if (L.bulk)
+          launch_check(launch_sweep2_bulk(h->adjoint, L, f, buf(l, cur), buf(l, 1 - cur), omega, s), "sweep2_bulk");
+        else
+          launch_check(launch_sweep2(h->adjoint, L, f, buf(l, cur), buf(l, 1 - cur), omega, s), "sweep2");
       });
       ++kernels;
       cur = 1 - cur;
@@ -1351,7 +1368,8 @@ void refresh_levels(stmg_hierarchy* h, std::vector<HostLevel> host) {
   for (size_t l = 0; l < h->host.size(); ++l) {
     const HostLevel& hl = h->host[l];
     const std::vector<double> t = hl.table(h->adjoint);
-    if (static_cast<int64_t>(t.size()) != h->coef[l]->n) throw std::logic_error("refresh_levels: shape changed");
+    if (static_cast<int64_t>(t.size()) + kVecPad != h->coef[l]->n)
+      throw std::logic_error("refresh_levels: shape changed");
     cuda_check(cudaMemcpy(h->coef[l]->p, t.data(), t.size() * 8, cudaMemcpyHostToDevice), "coef upload");
     h->views[l].w = hl.w;
     h->views[l].inv_w = hl.inv_w;
@@ -1930,6 +1948,8 @@ int stmg_level_sweep_kernels(stmg_hierarchy* h, int32_t l, const double* f, doub
     for (int k = 0; k < launches; ++k) {
       if (h->galerkin(l))
         launch_check(launch_g_sweep(h->dviews[l], f, a, b, omega, h->stream), "g_sweep");
+      else if (fused_pairs == 5)  // bulk-copy pipelined pair (vectors need kVecPad tail padding)
+        launch_check(launch_sweep2_bulk(h->adjoint, h->views[l], f, a, b, omega, h->stream), "sweep2_bulk");
       else if (fused_pairs == 3 || fused_pairs == 4)
         launch_check(launch_sweep_deep(h->adjoint, h->views[l], fused_pairs, f, a, b, omega, h->stream),
                      "sweep_deep");

@@ -32,6 +32,9 @@ struct LevelView {
   // Deepest fused smoothing kernel used on this level (2: pairs; 3, 4: k_leanD
   // on small levels where a launch is latency-bound); fixed at build.
   int64_t sweep_depth = 2;
+  // Fused pairs through the bulk-copy pipelined kernel (k_bulk) instead of
+  // k_lean2x2; fixed at build (STMG_BULK_DOFS: levels with at least that many DOFs).
+  int64_t bulk = 0;
 };
 
 inline bool full_range(const LevelView& L) { return L.n_lo == 0 && L.n_hi == L.n_t + 1; }
@@ -143,6 +146,12 @@ int launch_sweep(bool adjoint, const LevelView& L, const double* f, const double
 // launch_sweep calls.  y must not alias x.
 int launch_sweep2(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
                   double omega, cudaStream_t s);
+// The same two sweeps through the bulk-copy (cp.async.bulk + mbarrier) pipelined
+// persistent kernel; full-range levels only.  f, x and y must be allocated with
+// kVecPad doubles of tail padding (the row copies round out to 16 bytes).
+constexpr int64_t kVecPad = 512;
+int launch_sweep2_bulk(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
+                       double omega, cudaStream_t s);
 // depth (3 or 4) sweeps y = S^depth(x) in one pass; full-range levels only.
 int launch_sweep_deep(bool adjoint, const LevelView& L, int depth, const double* f, const double* x,
                       double* y, double omega, cudaStream_t s);

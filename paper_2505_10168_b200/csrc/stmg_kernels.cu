@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <cstdlib>
 #include <utility>
 
@@ -1574,6 +1575,242 @@ __global__ void __launch_bounds__(1024) k_coarsest(CoarsestView cv, const double
   }
 }
 
+// ---------------------------------------------------------------------------
+// Bulk-copy pipelined fused sweeps (k_bulk): the k_leanD computation (depth D,
+// overlapping warps, canonical row order -- bit-identical to D separate
+// sweeps), fed by cp.async.bulk copies of whole tile rows into a STAGES-deep
+// shared-memory ring instead of per-thread global loads.  The CTAs are
+// persistent (grid = resident CTAs) and walk the tiles node-tile fastest; warp
+// 0 refills a stage as soon as every warp has moved the stage's values into
+// registers, so the copies of the next STAGES - 1 tiles are in flight while a
+// tile is computed.  One copy per staged row: x rows sbase .. sbase+S-1, f rows
+// fbase .. fbase+F-1 of the nodes node0 .. node0+WN-1, the source rounded out
+// to 16-byte boundaries (the smem row carries a 0/1-element shift).  Vectors
+// are allocated with kVecPad doubles of tail padding so the rounding never
+// leaves the allocation; out-of-grid nodes are never used (EDGE path).
+// Full-range levels only.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int NT, int D, int W>
+struct BulkGeom {
+  static constexpr int S = NT + D;           // staged x rows
+  static constexpr int F = NT + D - 1;       // f rows
+  static constexpr int ROWS = S + F + kNumCoef;  // x rows, f rows, the 7 coefficient rows
+  static constexpr int STORED = 32 - 2 * D;  // stored nodes per warp
+  static constexpr int WN = W * STORED + 2 * D;
+  static constexpr int RW = WN + 2;          // even: rows stay 16-byte aligned
+  static constexpr int STAGE = ROWS * RW;    // doubles per stage
+};
+
+// Source range of staged row r of a tile: [gstart, gstart + bytes / 8), and the
+// shift of node0 inside the smem row.
+struct RowCopy {
+  int64_t gstart;
+  uint32_t bytes;
+  int shift;
+};
+template <bool ADJ, int NT, int D, int W>
+__device__ __forceinline__ RowCopy bulk_row(const LevelView& L, int r, int64_t n0, int64_t node0) {
+  using G = BulkGeom<NT, D, W>;
+  const int64_t sbase = ADJ ? n0 : n0 - D;
+  const int64_t fbase = ADJ ? n0 : n0 - D + 1;
+  RowCopy rc{0, 0u, 0};
+  if (r >= G::ROWS) return rc;
+  int64_t gs;
+  if (r >= G::S + G::F) {  // coefficient array k = r - S - F: coef + k nn + node
+    gs = (r - G::S - G::F) * L.nn + node0;
+  } else {
+    const int64_t n = r < G::S ? sbase + r : fbase + (r - G::S);
+    if (n < 0 || n > L.n_t) return rc;
+    gs = n * L.nn + node0;
+  }
+  const int64_t g0 = (gs < 0 ? 0 : gs) & ~int64_t{1};
+  const int64_t g1 = (gs + G::WN + 1) & ~int64_t{1};
+  rc.gstart = g0;
+  rc.bytes = static_cast<uint32_t>((g1 - g0) * 8);
+  rc.shift = static_cast<int>(gs - g0);
+  return rc;
+}
+
+template <bool ADJ, int NT, int D, int W, bool EDGE>
+__device__ __forceinline__ void bulk_body(const LevelView& L, const double* stage, double* __restrict__ y,
+                                          double omega, int64_t n0, int64_t node0, int warp, int lane,
+                                          uint64_t* empty_bar) {
+  using G = BulkGeom<NT, D, W>;
+  constexpr int S = G::S, F = G::F;
+  const int64_t nn = L.nn, nt = L.n_t;
+  const int q = warp * G::STORED + lane;  // smem position of this lane's node
+  const int64_t i = node0 + q;
+  const int64_t sbase = ADJ ? n0 : n0 - D;
+  const int64_t fbase = ADJ ? n0 : n0 - D + 1;
+  const bool in_grid = !EDGE || (i >= 0 && i < nn);
+  double v[S], fv[F];
+  // smem shift of a row: gs - (max(gs, 0) & ~1), gs = n nn + node0 (bulk_row)
+  auto shift = [&](int64_t n) -> int {
+    const int64_t gs = n * nn + node0;
+    return gs < 0 ? static_cast<int>(gs) : static_cast<int>(gs & 1);
+  };
+  auto shift_c = [&](int k) -> int { return shift(k); };  // coefficient row k starts at k nn
+#pragma unroll
+  for (int j = 0; j < S; ++j) {
+    const int64_t n = sbase + j;
+    const bool ok = !EDGE || (in_grid && n >= 0 && n <= nt);
+    v[j] = ok ? stage[j * G::RW + q + shift(n)] : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < F; ++j) {
+    const int64_t n = fbase + j;
+    const bool ok = !EDGE || (in_grid && n >= 0 && n <= nt);
+    fv[j] = ok ? stage[(S + j) * G::RW + q + shift(n)] : 0.0;
+  }
+  Coefs c{};
+  if (in_grid) {
+    const double* cr = stage + (S + F) * G::RW + q;
+    auto coef = [&](int k) { return cr[k * G::RW + shift_c(k)]; };
+    c.cm = coef(kCm);
+    c.c0 = coef(kC0);
+    c.cp = coef(kCp);
+    c.om = coef(kOm);
+    c.o0 = coef(kO0);
+    c.op = coef(kOp);
+    c.invd = coef(kInvD);
+  }
+  // this warp's values are in registers: release the stage to the producer
+  __syncwarp();
+  if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(empty_bar)) : "memory");
+#pragma unroll
+  for (int st = 1; st <= D; ++st) {
+    double pm = __shfl_up_sync(kFull, v[0], 1), pp = __shfl_down_sync(kFull, v[0], 1);
+#pragma unroll
+    for (int j = 0; j < S - st; ++j) {
+      const double x1 = v[j + 1];
+      const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
+      const int64_t n = ADJ ? sbase + j : sbase + st + j;
+      const double fval = ADJ ? fv[j] : fv[st - 1 + j];
+      const double own = ADJ ? v[j] : x1;
+      double out;
+      if (!EDGE) {
+        const double row = ADJ ? row_interior<true>(c, pm, v[j], pp, qm, x1, qp)
+                               : row_interior<false>(c, qm, x1, qp, pm, v[j], pp);
+        out = own + omega * ((fval - row) * c.invd);
+      } else {
+        out = 0.0;
+        if (in_grid && n >= 0 && n <= nt) {
+          const double row = ADJ ? row_sum<true>(L, n, i, c, pm, v[j], pp, qm, x1, qp)
+                                 : row_sum<false>(L, n, i, c, qm, x1, qp, pm, v[j], pp);
+          const double id = (n == 0 || i == 0) ? L.inv_w : c.invd;
+          out = own + omega * ((fval - row) * id);
+        }
+      }
+      v[j] = out;
+      pm = qm;
+      pp = qp;
+    }
+  }
+  if (lane >= D && lane <= 31 - D && in_grid) {
+    double* yp = y + (n0 * nn + i);
+#pragma unroll
+    for (int k = 0; k < NT; ++k)
+      if (!EDGE || n0 + k <= nt) yp[k * nn] = v[k];
+  }
+}
+
+// Tile walk of a persistent CTA: tiles blockIdx.x, +gridDim.x, ... (node tile
+// fastest), advanced without 64-bit division.
+struct TileWalk {
+  int64_t tn, tt, step_tn, step_tt, nnt;
+  __device__ __forceinline__ TileWalk(int64_t first, int64_t step, int64_t n_node_tiles)
+      : tn(first % n_node_tiles), tt(first / n_node_tiles), step_tn(step % n_node_tiles),
+        step_tt(step / n_node_tiles), nnt(n_node_tiles) {}
+  __device__ __forceinline__ void next() {
+    tn += step_tn;
+    tt += step_tt;
+    if (tn >= nnt) {
+      tn -= nnt;
+      ++tt;
+    }
+  }
+};
+
+// Warp-specialised: warp W is the producer (bulk copies into a STAGES-deep
+// ring, full barriers with transaction counts), warps 0..W-1 consume (wait full,
+// move the tile into registers, arrive on the stage's empty barrier, compute).
+// No CTA-wide barrier inside the tile loop.
+template <bool ADJ, int NT, int D, int W, int STAGES, int MINB>
+__global__ void __launch_bounds__((W + 1) * 32, MINB) k_bulk(LevelView L, const double* __restrict__ f,
+                                                            const double* __restrict__ x, double* __restrict__ y,
+                                                            double omega, int64_t n_node_tiles, int64_t n_time_tiles) {
+  using G = BulkGeom<NT, D, W>;
+  extern __shared__ __align__(128) double bsm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(bsm + STAGES * G::STAGE);
+  uint64_t* empty = full + STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < STAGES) {
+    mbar_init(&full[threadIdx.x], 1);
+    mbar_init(&empty[threadIdx.x], W);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  pdl_entry();
+  const int64_t nt = L.n_t;
+  TileWalk tw(blockIdx.x, gridDim.x, n_node_tiles);
+  if (warp == W) {  // producer
+    for (int64_t k = 0; tw.tt < n_time_tiles; ++k, tw.next()) {
+      const int st = static_cast<int>(k % STAGES);
+      if (k >= STAGES) mbar_wait_parity(&empty[st], static_cast<uint32_t>(((k / STAGES) - 1) & 1));
+      const int64_t n0 = tw.tt * NT, node0 = tw.tn * (W * G::STORED) - D;
+      const RowCopy rc = bulk_row<ADJ, NT, D, W>(L, lane, n0, node0);
+      const uint32_t total = __reduce_add_sync(kFull, rc.bytes);
+      if (lane == 0) mbar_arrive_expect_tx(&full[st], total);
+      __syncwarp();
+      if (rc.bytes) {
+        const double* src = lane < G::S ? x : lane < G::S + G::F ? f : L.coef;
+        bulk_g2s(bsm + st * G::STAGE + lane * G::RW, src + rc.gstart, rc.bytes, &full[st]);
+      }
+    }
+    return;
+  }
+  for (int64_t k = 0; tw.tt < n_time_tiles; ++k, tw.next()) {
+    const int st = static_cast<int>(k % STAGES);
+    mbar_wait_parity(&full[st], static_cast<uint32_t>((k / STAGES) & 1));
+    const int64_t n0 = tw.tt * NT, node0 = tw.tn * (W * G::STORED) - D;
+    const double* stage = bsm + st * G::STAGE;
+    const bool rows_in = ADJ ? (n0 >= 1 && n0 + NT + D - 1 <= nt) : (n0 >= D + 1 && n0 + NT - 1 <= nt);
+    const int64_t first = node0 + warp * G::STORED + 1;  // lane 1's node
+    const bool nodes_in = first >= 2 && first + 29 <= L.n_el - 1;
+    if (rows_in && nodes_in) bulk_body<ADJ, NT, D, W, false>(L, stage, y, omega, n0, node0, warp, lane, &empty[st]);
+    else bulk_body<ADJ, NT, D, W, true>(L, stage, y, omega, n0, node0, warp, lane, &empty[st]);
+  }
+}
+
 // Parallel-in-time exact march for wide coarsest levels (n_el > 32).  The march
 // x_n = T^-1 (f_n - S x_{n'}) (n' the coupled level) is affine in its start
 // state, so the n_t steps are cut into C chunks of Lc steps:
@@ -2334,6 +2571,38 @@ int launch_sweep2(bool adjoint, const LevelView& L, const double* f, const doubl
     else pdl_launch(k_lean2x2<false, 8>, grd, blk, 0, s, L, f, x, y, omega);
   }
   return check_launch();
+}
+
+// Fused pair (D = 2) through the bulk-copy pipeline (k_bulk); full-range levels.
+constexpr int kBulkW = 8, kBulkStages = 2, kBulkNT = 8, kBulkMinB = 2;
+template <bool ADJ>
+int bulk_pair_impl(const LevelView& L, const double* f, const double* x, double* y, double omega,
+                   cudaStream_t s) {
+  using G = BulkGeom<kBulkNT, 2, kBulkW>;
+  auto kern = k_bulk<ADJ, kBulkNT, 2, kBulkW, kBulkStages, kBulkMinB>;
+  const size_t smem = sizeof(double) * (size_t)kBulkStages * G::STAGE + 16 * kBulkStages;
+  static int ctas_per_sm[2] = {0, 0};
+  int& cps = ctas_per_sm[ADJ ? 1 : 0];
+  if (cps == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return static_cast<int>(e);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cps, kern, (kBulkW + 1) * 32, smem);
+    if (e != cudaSuccess || cps < 1) return static_cast<int>(e != cudaSuccess ? e : cudaErrorInvalidConfiguration);
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t n_node_tiles = ceil_div(L.nn, (int64_t)kBulkW * G::STORED);
+  const int64_t n_time_tiles = ceil_div(L.n_t + 1, (int64_t)kBulkNT);
+  const int64_t grid = std::min<int64_t>(n_node_tiles * n_time_tiles, (int64_t)sms * cps);
+  pdl_launch(kern, (unsigned)grid, (kBulkW + 1) * 32, smem, s, L, f, x, y, omega, n_node_tiles, n_time_tiles);
+  return check_launch();
+}
+
+int launch_sweep2_bulk(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
+                       double omega, cudaStream_t s) {
+  if (!full_range(L)) return static_cast<int>(cudaErrorInvalidValue);
+  return adjoint ? bulk_pair_impl<true>(L, f, x, y, omega, s) : bulk_pair_impl<false>(L, f, x, y, omega, s);
 }
 
 int launch_sweep_deep(bool adjoint, const LevelView& L, int depth, const double* f, const double* x,

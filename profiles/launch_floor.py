@@ -38,11 +38,13 @@ def main():
     out = []
     for l, lv in enumerate(h.levels[:-1]):
         n = lv.n_dofs
-        f = torch.randn(n, dtype=torch.float64, device="cuda")
-        x = torch.randn(n, dtype=torch.float64, device="cuda")
+        # 512 doubles of tail padding: the bulk-copy kernel (mode 5) rounds row copies out
+        f = torch.randn(n + 512, dtype=torch.float64, device="cuda")
+        x = torch.randn(n + 512, dtype=torch.float64, device="cuda")
         y = torch.empty_like(x)
         row = {"level": l, "n_el": lv.n_el, "n_t": lv.n_t, "dofs": n}
-        for name, pairs in (("sweep_us", False), ("pair_us", True), ("deep3_us", 3), ("deep4_us", 4)):
+        for name, pairs in (("sweep_us", False), ("pair_us", True), ("bulk_pair_us", 5), ("deep3_us", 3),
+                            ("deep4_us", 4)):
             row[name] = graph_time(h, lambda: h.sweep_kernels(l, f, x, y, a.k, pairs), a.k, a.reps)
         nc = h.levels[l + 1].n_dofs
         fc = torch.empty(nc, dtype=torch.float64, device="cuda")
