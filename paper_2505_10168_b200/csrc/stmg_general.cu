@@ -307,6 +307,38 @@ int launch_load_vector(int kind, const double* params, int n_params, double L, d
   return check();
 }
 
+// mg_solve's per-cycle bookkeeping (proj/src/multigrid.cpp:260-273) on the
+// device, for the solve loop run as a conditional WHILE graph node: relative
+// residual from the norm partial sums (scalars[0] = ||b||^2, scalars[1] =
+// ||b - J u||^2), history entry, status, and whether another V-cycle runs.
+// sqrt is correctly rounded, so rn equals the host loop's value bit for bit.
+__global__ void k_cycle_check(const double* __restrict__ scalars, SolveLoopCtl* ctl, double* hist,
+                              cudaGraphConditionalHandle handle) {
+  const double norm_b = sqrt(scalars[0]);
+  const double denom = norm_b == 0.0 ? 1.0 : norm_b;
+  const double rn = sqrt(scalars[1]) / denom;
+  const int c = ctl->cycles + 1;
+  ctl->cycles = c;
+  hist[c] = rn;
+  unsigned go = 1;
+  if (rn < ctl->tol) {
+    ctl->status = 0;  // STMG_CONVERGED
+    go = 0;
+  } else if (!isfinite(rn) || rn > ctl->div_tol) {
+    ctl->status = 2;  // STMG_DIVERGED
+    go = 0;
+  } else if (c >= ctl->max_cycles) {
+    go = 0;  // STMG_MAX_CYCLES (set by the host)
+  }
+  cudaGraphSetConditional(handle, go);
+}
+
+int launch_cycle_check(const double* scalars, SolveLoopCtl* ctl, double* hist,
+                       cudaGraphConditionalHandle handle, cudaStream_t s) {
+  k_cycle_check<<<1, 1, 0, s>>>(scalars, ctl, hist, handle);
+  return check();
+}
+
 __global__ void k_scale(const double* __restrict__ x, double a, double* __restrict__ y, int64_t n) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
     y[q] = x[q] * a;

@@ -372,14 +372,22 @@ struct DeviceBuf {
 // Vector workspaces (f, x, y per level; level 0: b, u, u').  A hierarchy and
 // its transpose share one Workspace (they are never solved concurrently),
 // which halves the footprint for 1e9-DOF grids.
+// Cycle cap of the device-side solve loop (longer solves use the host loop).
+constexpr int kLoopHistory = 4096;
+
 struct Workspace {
   std::vector<std::unique_ptr<DeviceBuf>> f, xa, xb;
   std::unique_ptr<DeviceBuf> partials, scalars, coarse_scratch;
   double* pinned = nullptr;  // 4 host doubles
+  // device solve loop: SolveLoopCtl + history[kLoopHistory + 1], and a pinned mirror
+  std::unique_ptr<DeviceBuf> loop;
+  double* loop_host = nullptr;
   ~Workspace() {
     if (pinned) cudaFreeHost(pinned);
+    if (loop_host) cudaFreeHost(loop_host);
   }
 };
+constexpr int64_t kLoopCtlDoubles = (sizeof(SolveLoopCtl) + 7) / 8;
 
 struct GraphKey {
   int nu;
@@ -413,7 +421,24 @@ struct GraphEntry {
   int64_t kernels = 0;
   int final_buf = 0;
   std::vector<TimedKernel> timed;  // event pairs recorded inside the graph (profiling)
+  // The whole cycle loop as one graph: a conditional WHILE node whose body is
+  // the V-cycle, the residual norm and the bookkeeping kernel (solve_loop).
+  cudaGraph_t loop_graph = nullptr;
+  cudaGraphExec_t loop_exec = nullptr;
+  bool loop_tried = false;
 };
+
+void destroy_graph_entry(GraphEntry& e) {
+  if (e.exec) cudaGraphExecDestroy(e.exec);
+  if (e.graph) cudaGraphDestroy(e.graph);
+  if (e.loop_exec) cudaGraphExecDestroy(e.loop_exec);
+  if (e.loop_graph) cudaGraphDestroy(e.loop_graph);
+  for (auto& t : e.timed) {
+    cudaEventDestroy(t.start);
+    cudaEventDestroy(t.stop);
+  }
+  e = GraphEntry{};
+}
 
 }  // namespace
 }  // namespace stmgb
@@ -464,14 +489,7 @@ struct stmg_hierarchy {
     cudaGetDevice(&prev);
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
-    for (auto& kv : graphs) {
-      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-      if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
-      for (auto& t : kv.second.timed) {
-        cudaEventDestroy(t.start);
-        cudaEventDestroy(t.stop);
-      }
-    }
+    for (auto& kv : graphs) stmgb::destroy_graph_entry(kv.second);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (own_stream) cudaStreamDestroy(own_stream);
@@ -826,6 +844,10 @@ std::shared_ptr<Workspace> make_workspace(const stmg_hierarchy* h, int64_t* byte
   ws->coarse_scratch = std::make_unique<DeviceBuf>(scratch);
   *bytes += 8 * (max_partials + 8 + scratch);
   cuda_check(cudaMallocHost(&ws->pinned, 8 * sizeof(double)), "cudaMallocHost");
+  ws->loop = std::make_unique<DeviceBuf>(kLoopCtlDoubles + kLoopHistory + 1);
+  cuda_check(cudaMallocHost(&ws->loop_host, sizeof(double) * (kLoopCtlDoubles + kLoopHistory + 1)),
+             "cudaMallocHost");
+  *bytes += 8 * (kLoopCtlDoubles + kLoopHistory + 1);
   return ws;
 }
 
@@ -1096,6 +1118,66 @@ GraphEntry& get_graph(stmg_hierarchy* h, int nu, double omega) {
   return h->graphs.emplace(key, e).first->second;
 }
 
+// The solve loop of mg_solve (proj/src/multigrid.cpp:260-273) as one graph: a
+// WHILE conditional node whose body is [V-cycle, speculative norm sweep,
+// finalize, k_cycle_check].  The host launches it once per solve instead of
+// one V-cycle graph plus a norm read-back per cycle.  Returns nullptr (and the
+// host loop is used) when the graph cannot be built.
+cudaGraphExec_t get_loop(stmg_hierarchy* h, int nu, double omega) {
+  GraphEntry& e = get_graph(h, nu, omega);
+  if (e.loop_tried) return e.loop_exec;
+  e.loop_tried = true;
+  if (const char* v = std::getenv("STMG_DEVICE_LOOP"))
+    if (std::atoi(v) == 0) return nullptr;
+  Nvtx range("stmg::capture_solve_loop");
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ex = nullptr;
+  auto fail = [&] {
+    cudaGetLastError();
+    if (ex) cudaGraphExecDestroy(ex);
+    if (g) cudaGraphDestroy(g);
+    return static_cast<cudaGraphExec_t>(nullptr);
+  };
+  if (cudaGraphCreate(&g, 0) != cudaSuccess) return fail();
+  cudaGraphConditionalHandle handle;
+  if (cudaGraphConditionalHandleCreate(&handle, g, 1, cudaGraphCondAssignDefault) != cudaSuccess) return fail();
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = handle;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  if (cudaGraphAddNode(&node, g, nullptr, 0, &cp) != cudaSuccess) return fail();
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  cudaStream_t cs = h->cap_stream;
+  if (cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+    return fail();
+  bool ok = true;
+  try {
+    Emitter em{h, nu, omega, cs};
+    const bool spec = h->n_levels() > 1 && nu >= 1;
+    const int fin = em.level(0, spec ? 1 : 0, spec ? 1 : 0, false);
+    if (fin != 0) throw std::logic_error("level-0 iterate left the primary buffer");
+    Workspace& ws = *h->ws;
+    int64_t np = 0;
+    launch_check(launch_sweep(h->adjoint, h->views[0], ws.f[0]->p, ws.xa[0]->p, spec ? ws.xb[0]->p : nullptr,
+                              omega, ws.partials->p, &np, cs),
+                 "norm sweep");
+    launch_check(launch_finalize_sum(ws.partials->p, np, ws.scalars->p + 1, cs), "finalize");
+    auto* ctl = reinterpret_cast<SolveLoopCtl*>(ws.loop->p);
+    launch_check(launch_cycle_check(ws.scalars->p, ctl, ws.loop->p + kLoopCtlDoubles, handle, cs), "cycle check");
+  } catch (...) {
+    ok = false;
+  }
+  cudaGraph_t captured = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(cs, &captured);
+  if (!ok || ec != cudaSuccess) return fail();
+  if (cudaGraphInstantiate(&ex, g, 0) != cudaSuccess) return fail();
+  e.loop_graph = g;
+  e.loop_exec = ex;
+  return ex;
+}
+
 bool is_device_ptr(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -1173,8 +1255,28 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
   rep->fine_sweep_pair_seconds = 0.0;
   double per_cycle_updates = 0.0;
   for (int l = 0; l + 1 < h->n_levels(); ++l) per_cycle_updates += 2.0 * o.nu * static_cast<double>(h->ndofs(l));
+  cudaGraphExec_t loop = nullptr;
+  if (r0 >= o.tol && o.max_cycles > 0 && o.max_cycles <= kLoopHistory && !h->profiling)
+    loop = get_loop(h, o.nu, o.omega);
   if (r0 < o.tol) {
     rep->status = STMG_CONVERGED;
+  } else if (loop) {
+    // the whole cycle loop on the device: one launch, one read-back
+    auto* ctl = reinterpret_cast<SolveLoopCtl*>(ws.loop_host);
+    *ctl = SolveLoopCtl{o.tol, o.div_tol, o.max_cycles, 0, STMG_MAX_CYCLES, 0};
+    cuda_check(cudaMemcpyAsync(ws.loop->p, ws.loop_host, sizeof(SolveLoopCtl), cudaMemcpyHostToDevice, h->stream),
+               "loop ctl");
+    cuda_check(cudaGraphLaunch(loop, h->stream), "loop graph launch");
+    cuda_check(cudaMemcpyAsync(ws.loop_host, ws.loop->p, sizeof(double) * (kLoopCtlDoubles + o.max_cycles + 1),
+                               cudaMemcpyDeviceToHost, h->stream),
+               "loop read-back");
+    cuda_check(cudaStreamSynchronize(h->stream), "stream sync");
+    const double* dh = ws.loop_host + kLoopCtlDoubles;
+    for (int c = 1; c <= ctl->cycles; ++c) history[nh++] = dh[c];
+    rep->cycles = ctl->cycles;
+    rep->status = ctl->status;
+    rep->smoother_dof_updates = per_cycle_updates * ctl->cycles;
+    launches += static_cast<int64_t>(ctl->cycles) * (g->kernels + 3);
   } else {
     rep->status = STMG_MAX_CYCLES;
     for (int cycle = 1; cycle <= o.max_cycles; ++cycle) {
@@ -1378,14 +1480,7 @@ void refresh_levels(stmg_hierarchy* h, std::vector<HostLevel> host) {
   auto g = std::move(h->pcr_gamma);
   auto b = std::move(h->pcr_bfin);
   build_pcr(h);  // fresh factor tables (old ones freed after the sync above)
-  for (auto& kv : h->graphs) {
-    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-    if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
-    for (auto& t : kv.second.timed) {
-      cudaEventDestroy(t.start);
-      cudaEventDestroy(t.stop);
-    }
-  }
+  for (auto& kv : h->graphs) destroy_graph_entry(kv.second);
   h->graphs.clear();
 }
 

@@ -130,6 +130,18 @@ int launch_xfer_restrict(const XferView& T, const double* r, double* fc, cudaStr
 int launch_xfer_prolong_add(const XferView& T, const double* xc, const double* x, double* y,
                             cudaStream_t s);
 int launch_block_march(const BlockMarchView& B, const double* f, double* x, cudaStream_t s);
+// Device-side state of a solve loop run as a conditional WHILE graph node.
+struct SolveLoopCtl {
+  double tol;
+  double div_tol;
+  int32_t max_cycles;
+  int32_t cycles;  // V-cycles done
+  int32_t status;  // stmg_solve_status
+  int32_t pad;
+};
+// One cycle's bookkeeping (history, status) and the loop's continue flag.
+int launch_cycle_check(const double* scalars, SolveLoopCtl* ctl, double* hist,
+                       cudaGraphConditionalHandle handle, cudaStream_t s);
 // y = x * a (y may alias x)
 int launch_scale(const double* x, double a, double* y, int64_t n, cudaStream_t s);
 // load_vector(g, q) + masking into device memory (source kinds as stmg_load_vector)
