@@ -219,6 +219,17 @@ int stmg_hierarchy_device_bytes(const stmg_hierarchy* h, int64_t* bytes);
 int stmg_mg_solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_options* opts,
                   stmg_solve_report* report, double* history, int32_t history_cap);
 
+/* Independent solves run concurrently (SURVEY.md §2.2 "data parallel over
+ * independent solves", §8(f) item 4 "experiment sweeps as batched replicas"):
+ * entry i is mg_solve(hs[i], bs[i], us[i], opts) with reports[i] and
+ * histories[i] (history_cap doubles each).  Each hierarchy works on its own
+ * stream and device, so the solves overlap on one GPU and spread over several.
+ * Entries must not share a workspace (no repeats, not a hierarchy together with
+ * its transpose).  On failure the first failing entry's error is returned. */
+int stmg_mg_solve_batch(int32_t count, stmg_hierarchy* const* hs, const double* const* bs, double* const* us,
+                        const stmg_solve_options* opts, stmg_solve_report* reports, double* const* histories,
+                        int32_t history_cap);
+
 /* ---- level kernels on device vectors (parity tests, profiling) ------------------- */
 /* `sweeps` damped-Jacobi sweeps in place (csr_residual + jacobi_update). */
 int stmg_level_sweeps(stmg_hierarchy* h, int32_t level, const double* f, double* x,

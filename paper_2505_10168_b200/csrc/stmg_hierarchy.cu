@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -1995,6 +1996,50 @@ int stmg_mg_solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solv
     checked(h);
     if (!opts || !report) throw std::invalid_argument("mg_solve: null argument");
     solve(h, b, u, *opts, report, history, cap);
+  });
+}
+
+int stmg_mg_solve_batch(int32_t count, stmg_hierarchy* const* hs, const double* const* bs, double* const* us,
+                        const stmg_solve_options* opts, stmg_solve_report* reports, double* const* histories,
+                        int32_t history_cap) {
+  return guarded([&] {
+    if (count < 0 || !opts) throw std::invalid_argument("mg_solve_batch: bad arguments");
+    if (count == 0) return;
+    if (!hs || !bs || !us || !reports || !histories) throw std::invalid_argument("mg_solve_batch: null argument");
+    for (int32_t i = 0; i < count; ++i) {
+      checked(hs[i]);
+      for (int32_t j = 0; j < i; ++j)
+        if (hs[i] == hs[j] || hs[i]->ws == hs[j]->ws)
+          throw std::invalid_argument(
+              "mg_solve_batch: two entries share a workspace (a repeat, or a hierarchy and its transpose)");
+    }
+    // one host worker per concurrent solve; each hierarchy runs on its own
+    // stream (and device), so the solves overlap on the GPU(s)
+    std::vector<int> rc(static_cast<size_t>(count), STMG_OK);
+    std::vector<std::string> msg(static_cast<size_t>(count));
+    std::atomic<int32_t> next{0};
+    auto worker = [&] {
+      for (int32_t i = next++; i < count; i = next++) {
+        rc[i] = stmg_mg_solve(hs[i], bs[i], us[i], opts, &reports[i], histories[i], history_cap);
+        if (rc[i] != STMG_OK) msg[i] = g_error;
+      }
+    };
+    const int32_t n_workers = std::min<int32_t>(count, 64);
+    std::vector<std::thread> th;
+    for (int32_t w = 1; w < n_workers; ++w) th.emplace_back(worker);
+    worker();
+    for (auto& t : th) t.join();
+    for (int32_t i = 0; i < count; ++i) {
+      if (rc[i] == STMG_OK) continue;
+      const std::string m = "mg_solve_batch[" + std::to_string(i) + "]: " + msg[i];
+      switch (rc[i]) {
+        case STMG_EINVAL: throw std::invalid_argument(m);
+        case STMG_ERANGE: throw std::out_of_range(m);
+        case STMG_ECUDA: throw CudaError(m);
+        case STMG_ENOMEM: throw NoMem(m);
+        default: throw std::runtime_error(m);
+      }
+    }
   });
 }
 

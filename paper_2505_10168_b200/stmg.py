@@ -69,6 +69,7 @@ def _load():
         "stmg_hierarchy_set_profiling": [vp, i32],
         "stmg_hierarchy_profile": [vp, i32, i32, C.POINTER(i64), C.POINTER(f64)],
         "stmg_mg_solve": [vp, vp, vp, vp, vp, vp, i32],
+        "stmg_mg_solve_batch": [i32, vp, vp, vp, vp, vp, vp, i32],
         "stmg_level_sweeps": [vp, i32, vp, vp, i32, f64],
         "stmg_level_residual": [vp, i32, vp, vp, vp],
         "stmg_level_sweep_kernels": [vp, i32, vp, vp, vp, i32, i32, f64],
@@ -652,6 +653,36 @@ def mg_solve(h: LevelHierarchy, b, u, opts: Optional[SolveOptions] = None) -> So
                        [float(v) for v in hist[: rep.n_history]], bool(rep.absolute_norms),
                        rep.seconds, rep.device_seconds, rep.smoother_dof_updates, rep.kernel_launches,
                        kt)
+
+
+def mg_solve_batch(hs: Sequence[LevelHierarchy], bs, us, opts: Optional[SolveOptions] = None) -> list:
+    """Independent solves run concurrently (each hierarchy on its own stream / GPU):
+    entry i is mg_solve(hs[i], bs[i], us[i], opts).  Hierarchies must not share a
+    workspace (a hierarchy and its transpose do)."""
+    o = opts or SolveOptions()
+    k = len(hs)
+    if len(bs) != k or len(us) != k:
+        raise ValueError("mg_solve_batch: hs, bs and us differ in length")
+    for h, b, u in zip(hs, bs, us):
+        n = h.levels[0].n_dofs
+        if _numel(b) != n or _numel(u) != n:
+            raise ValueError("mg_solve_batch: vector size mismatch")
+    cap = max(o.max_cycles, 0) + 1
+    hist = np.zeros((max(k, 1), cap), np.float64)
+    reps = (_SolveRep * max(k, 1))()
+    co = _SolveOpts(int(o.nu), float(o.omega), float(o.tol), float(o.div_tol), int(o.max_cycles))
+    H = (C.c_void_p * max(k, 1))(*[h.handle.value for h in hs])
+    B = (C.c_void_p * max(k, 1))(*[_ptr(b) for b in bs])
+    U = (C.c_void_p * max(k, 1))(*[_ptr(u) for u in us])
+    P = (C.c_void_p * max(k, 1))(*[hist[i].ctypes.data for i in range(k)])
+    _check(_lib.stmg_mg_solve_batch(k, H, B, U, C.byref(co), reps, P, cap))
+    out = []
+    for i in range(k):
+        r = reps[i]
+        out.append(SolveReport(SolveStatus(r.status), r.cycles, r.factor, [float(v) for v in hist[i, : r.n_history]],
+                               bool(r.absolute_norms), r.seconds, r.device_seconds, r.smoother_dof_updates,
+                               r.kernel_launches))
+    return out
 
 
 # ---- topology optimisation (BASELINE config 4; proj/src/optimisation.cpp:83-186) -----
