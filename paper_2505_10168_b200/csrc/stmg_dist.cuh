@@ -93,9 +93,10 @@ struct Comm {
   int rank0 = 0;  // global rank of local slot 0
   virtual ~Comm() = default;
   virtual const char* name() const = 0;
-  // ghost exchange of one vector per local rank (rows of level partition b, nn doubles per row)
+  // ghost exchange of one vector per local rank (rows of level partition b, nn doubles per
+  // row): `depth` levels on each side of every slab boundary
   virtual void exchange(const std::vector<double*>& v, const std::vector<int64_t>& b, int64_t nn,
-                        cudaStream_t s) = 0;
+                        int depth, cudaStream_t s) = 0;
   virtual void allreduce_sum(const std::vector<double*>& in, const std::vector<double*>& out,
                              cudaStream_t s) = 0;
   // rows [lo_g, hi_g) of every rank's src (full-size, nn per row) -> dst on rank 0
@@ -118,12 +119,12 @@ struct LoopbackComm : Comm {
     rank0 = 0;
   }
   const char* name() const override { return "loopback"; }
-  void exchange(const std::vector<double*>& v, const std::vector<int64_t>& b, int64_t nn,
+  void exchange(const std::vector<double*>& v, const std::vector<int64_t>& b, int64_t nn, int depth,
                 cudaStream_t s) override {
-    const size_t bytes = sizeof(double) * static_cast<size_t>(nn);
+    const size_t bytes = sizeof(double) * static_cast<size_t>(nn * depth);
     for (int g = 1; g < world; ++g) {
-      // last row of g-1 -> leading ghost of g ; first row of g -> trailing ghost of g-1
-      cuda_check(cudaMemcpyAsync(v[g] + (b[g] - 1) * nn, v[g - 1] + (b[g] - 1) * nn, bytes,
+      // last rows of g-1 -> leading ghosts of g ; first rows of g -> trailing ghosts of g-1
+      cuda_check(cudaMemcpyAsync(v[g] + (b[g] - depth) * nn, v[g - 1] + (b[g] - depth) * nn, bytes,
                                  cudaMemcpyDeviceToDevice, s), "ghost copy");
       cuda_check(cudaMemcpyAsync(v[g - 1] + b[g] * nn, v[g] + b[g] * nn, bytes,
                                  cudaMemcpyDeviceToDevice, s), "ghost copy");
@@ -222,19 +223,20 @@ struct NcclComm : Comm {
     if (comm) nccl().CommDestroy(comm);
   }
   const char* name() const override { return "nccl"; }
-  void exchange(const std::vector<double*>& v, const std::vector<int64_t>& b, int64_t nn,
+  void exchange(const std::vector<double*>& v, const std::vector<int64_t>& b, int64_t nn, int depth,
                 cudaStream_t s) override {
     const int g = rank0;
     double* x = v[0];
     const auto& A = nccl();
+    const size_t cnt = static_cast<size_t>(nn * depth);
     nccl_check(A.GroupStart(), "group");
     if (g > 0) {
-      nccl_check(A.Send(x + b[g] * nn, nn, ncclDouble, g - 1, comm, s), "send");
-      nccl_check(A.Recv(x + (b[g] - 1) * nn, nn, ncclDouble, g - 1, comm, s), "recv");
+      nccl_check(A.Send(x + b[g] * nn, cnt, ncclDouble, g - 1, comm, s), "send");
+      nccl_check(A.Recv(x + (b[g] - depth) * nn, cnt, ncclDouble, g - 1, comm, s), "recv");
     }
     if (g < world - 1) {
-      nccl_check(A.Send(x + (b[g + 1] - 1) * nn, nn, ncclDouble, g + 1, comm, s), "send");
-      nccl_check(A.Recv(x + b[g + 1] * nn, nn, ncclDouble, g + 1, comm, s), "recv");
+      nccl_check(A.Send(x + (b[g + 1] - depth) * nn, cnt, ncclDouble, g + 1, comm, s), "send");
+      nccl_check(A.Recv(x + b[g + 1] * nn, cnt, ncclDouble, g + 1, comm, s), "recv");
     }
     nccl_check(A.GroupEnd(), "group");
   }
@@ -344,7 +346,9 @@ struct DistEmitter {
     for (int k = 0; k < W(); ++k) v.push_back(buf(k, l, which));
     return v;
   }
-  void exchange(int l, int which) { d->comm->exchange(bufs(l, which), d->plan.bounds[l], d->nn(l), s); }
+  void exchange(int l, int which, int depth = 1) {
+    d->comm->exchange(bufs(l, which), d->plan.bounds[l], d->nn(l), depth, s);
+  }
   void sweep_all(int l, int cur) {
     exchange(l, cur);
     for (int k = 0; k < W(); ++k) {
@@ -398,10 +402,14 @@ struct DistEmitter {
       }
       pre = nu >= 1 ? nu - 1 : 0;
     }
-    for (int it = 0; it < pre; ++it) {
-      sweep_all(l, cur);
-      cur = 1 - cur;
+    if (from_zero && l > 0 && pre >= 2) {
+      // the fused pair's first sweep also runs on the ghost level next to the slab,
+      // which needs that level's right-hand side from the neighbour
+      std::vector<double*> fv;
+      for (int k = 0; k < W(); ++k) fv.push_back(d->ranks[k].f[l]->p);
+      d->comm->exchange(fv, d->plan.bounds[l], d->nn(l), 1, s);
     }
+    smooth_all(l, cur, pre);
     // residual + restriction into level l+1 (slab rows of l+1, or the rows this
     // rank contributes to the first gathered level)
     exchange(l, cur);
@@ -437,11 +445,27 @@ struct DistEmitter {
         ++kernels;
       }
     }
-    for (int it = 0; it < post; ++it) {
+    smooth_all(l, cur, post);
+    return cur;
+  }
+
+  // `count` sweeps on every rank's slab: fused pairs after a two-level ghost
+  // exchange (one exchange per two sweeps), then a single sweep if count is odd.
+  void smooth_all(int l, int& cur, int count) {
+    for (; count >= 2; count -= 2) {
+      exchange(l, cur, 2);
+      for (int k = 0; k < W(); ++k) {
+        launch_check(launch_sweep2(d->adjoint, d->ranks[k].views[l], d->ranks[k].f[l]->p, buf(k, l, cur),
+                                   buf(k, l, 1 - cur), omega, s),
+                     "dist sweep2");
+        ++kernels;
+      }
+      cur = 1 - cur;
+    }
+    if (count == 1) {
       sweep_all(l, cur);
       cur = 1 - cur;
     }
-    return cur;
   }
 };
 
@@ -531,7 +555,7 @@ GraphEntry& dist_graph(stmg_dist* d, int nu, double omega) {
 void dist_norm(stmg_dist* d, bool spec, double omega, int slot) {
   std::vector<double*> X, in, out;
   for (auto& R : d->ranks) X.push_back(R.xa[0]->p);
-  d->comm->exchange(X, d->plan.bounds[0], d->nn(0), d->stream);
+  d->comm->exchange(X, d->plan.bounds[0], d->nn(0), 1, d->stream);
   for (auto& R : d->ranks) {
     int64_t np = 0;
     launch_check(launch_sweep(d->adjoint, R.views[0], R.f[0]->p, R.xa[0]->p, spec ? R.xb[0]->p : nullptr,
