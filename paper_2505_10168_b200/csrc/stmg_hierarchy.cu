@@ -453,7 +453,7 @@ struct stmg_hierarchy {
   std::vector<std::unique_ptr<stmgb::DeviceBuf>> coef;  // per level
   std::vector<stmgb::LevelView> views;
   stmgb::CoarsestView coarsest{};
-  std::unique_ptr<stmgb::DeviceBuf> pcr_alpha, pcr_gamma, pcr_bfin, prop_tinv, prop_a, prop_chunk, pint_prop;
+  std::unique_ptr<stmgb::DeviceBuf> pcr_alpha, pcr_gamma, pcr_bfin, prop_tinv, prop_a, prop_chunk, pint_pow;
   std::shared_ptr<stmgb::Workspace> ws;
   cudaStream_t stream = nullptr;      // where work runs (own_stream or a caller's)
   cudaStream_t own_stream = nullptr;  // created with the hierarchy
@@ -505,7 +505,7 @@ struct stmg_hierarchy {
     prop_tinv.reset();
     prop_a.reset();
     prop_chunk.reset();
-    pint_prop.reset();
+    pint_pow.reset();
     ws.reset();
     cudaSetDevice(prev);
   }
@@ -536,20 +536,26 @@ void build_pint(stmg_hierarchy* h) {
     if (std::atoi(v) == 0) return;
   const int m = h->coarsest.m;
   const int64_t nt = h->host.back().g.n_t;
-  if (m <= 32 || m > 4096 || nt < 64) return;
+  if (m <= 32 || m > 2048 || nt < 64) return;
   int64_t Lc = 1;
   while (Lc * Lc < (3 * nt) / 2) Lc *= 2;
   while (Lc > 1 && nt % Lc != 0) Lc /= 2;
   const int64_t C = nt / Lc;
   if (C < 2 || Lc < 4) return;
-  h->pint_prop = std::make_unique<DeviceBuf>(static_cast<int64_t>(m) * m);
+  int rounds = 0;
+  while ((int64_t{1} << rounds) < C) ++rounds;
+  // reused across refresh_levels (optimise() rebuilds it every design iteration)
+  const int64_t need = static_cast<int64_t>(rounds) * m * m;
+  if (!h->pint_pow || h->pint_pow->n != need) h->pint_pow = std::make_unique<DeviceBuf>(need);
   h->coarsest.pint_len = static_cast<int32_t>(Lc);
-  launch_check(launch_coarsest_pint_prop(h->coarsest, h->pint_prop->p, h->own_stream ? h->own_stream : nullptr),
+  launch_check(launch_coarsest_pint_prop(h->coarsest, h->pint_pow->p, rounds,
+                                         h->own_stream ? h->own_stream : nullptr),
                "pint propagator");
   cuda_check(cudaStreamSynchronize(h->own_stream ? h->own_stream : nullptr), "sync");
-  h->coarsest.pint_prop = h->pint_prop->p;
+  h->coarsest.pint_pow = h->pint_pow->p;
+  h->coarsest.pint_rounds = rounds;
   h->coarsest.pint_chunks = static_cast<int32_t>(C);
-  h->device_bytes += static_cast<int64_t>(m) * m * 8;
+  h->device_bytes += static_cast<int64_t>(rounds) * m * m * 8;
 }
 
 // Parallel-cyclic-reduction factors of the coarsest step matrix (rows 1..n_el:
@@ -607,7 +613,8 @@ void build_pcr(stmg_hierarchy* h) {
   h->coarsest.chunk_len = 0;
   h->coarsest.pint_chunks = 0;
   h->coarsest.pint_len = 0;
-  h->coarsest.pint_prop = nullptr;
+  h->coarsest.pint_rounds = 0;
+  h->coarsest.pint_pow = nullptr;
   if (m >= 1 && m <= 32) {
     std::vector<double> Ti(32 * 32, 0.0), A(32 * 32, 0.0), S(32 * 32, 0.0);
     std::vector<double> sub(m), dia(m), sup(m), cpv(m), col(m);

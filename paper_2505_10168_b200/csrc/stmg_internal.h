@@ -60,16 +60,21 @@ struct CoarsestView {
   const double* prop_chunk;
   // n_el > 32 (wide coarsest levels, e.g. config 4's 256 x 8192): parallel-in-time
   // march over pint_chunks chunks of pint_len steps, one CTA per chunk, linked by
-  // the dense propagator A^pint_len (m x m, column-major); 0 chunks = sequential.
+  // a log-depth scan with the powers Q^(2^r), Q = A^pint_len (pint_rounds m x m
+  // column-major matrices, contiguous); 0 chunks = sequential march.
   int32_t pint_chunks;
   int32_t pint_len;
-  const double* pint_prop;
+  int32_t pint_rounds;
+  const double* pint_pow;
 };
-// Kernel launches one coarsest solve issues (the parallel-in-time march is three).
-inline int coarsest_launches(const CoarsestView& cv) { return cv.m > 32 && cv.pint_chunks > 1 ? 3 : 1; }
-// Scratch doubles the coarsest solve needs (chunk start states of the PinT march).
+// Kernel launches one coarsest solve issues (the parallel-in-time march: the
+// chunk marches, one launch per scan round, the chunk corrections).
+inline int coarsest_launches(const CoarsestView& cv) {
+  return cv.m > 32 && cv.pint_chunks > 1 ? 2 + cv.pint_rounds : 1;
+}
+// Scratch doubles the coarsest solve needs (two buffers of chunk end states).
 inline int64_t coarsest_scratch(const CoarsestView& cv) {
-  return cv.m > 32 && cv.pint_chunks > 1 ? (int64_t)cv.pint_chunks * cv.m : 0;
+  return cv.m > 32 && cv.pint_chunks > 1 ? 2 * (int64_t)cv.pint_chunks * cv.m : 0;
 }
 
 // Shared memory of the chunked coarsest march: g (n_t x 32), chunk end and
@@ -190,8 +195,9 @@ int launch_prolong_add(const LevelView& F, const LevelView& C, int dir, const do
                        cudaStream_t s);
 int launch_coarsest(bool adjoint, const CoarsestView& cv, const double* f, double* x,
                     double* scratch, cudaStream_t s);
-// A^pint_len (column-major m x m) into P by m parallel homogeneous marches
-int launch_coarsest_pint_prop(const CoarsestView& cv, double* P, cudaStream_t s);
+// Q = A^pint_len (column-major m x m) into P by m parallel homogeneous marches,
+// then its squares Q^2, Q^4, ... into P + m^2, P + 2 m^2, ... (rounds matrices in all)
+int launch_coarsest_pint_prop(const CoarsestView& cv, double* P, int rounds, cudaStream_t s);
 // Sum of n_partials doubles in a fixed order into *out (device scalar).
 int launch_finalize_sum(const double* partials, int64_t n, double* out, cudaStream_t s);
 // Sum of squares of x[0..n) into partials (fixed grid) then *out.

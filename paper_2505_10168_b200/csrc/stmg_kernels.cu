@@ -1893,41 +1893,57 @@ __global__ void __launch_bounds__(1024) k_coarsest_pint(CoarsestView cv, const d
     for (int j = tid; j < m; j += bs) x[(int64_t)blockIdx.x * m + j] = prev[j];
 }
 
-// Chunk links of k_coarsest_pint: starts[c] = y_end(c) + A^Lc starts[c - 1]
-// (starts[0] = y_end(0)); y_end(c) is PHASE 0's value at the chunk's last level.
+// Chunk links of k_coarsest_pint by a Kogge-Stone scan.  The true end state of
+// chunk c is s_c = sum_{j <= c} Q^(c-j) y_j (y_j: PHASE 0's end state of chunk j,
+// Q = A^Lc).  Round r (stride d = 2^r) maps v_c <- v_c + Q^d v_{c-d} for c >= d,
+// starting from v = y; after ceil(log2 C) rounds v_c = s_c.  One CTA per chunk,
+// the matvec rows across threads (Q^d column-major, coalesced), the operand
+// vector in shared memory.  Round 0 reads y from the chunk end levels of x.
 template <bool ADJ>
-__global__ void __launch_bounds__(1024) k_coarsest_pint_link(CoarsestView cv, const double* __restrict__ x,
-                                                             double* __restrict__ starts) {
+__global__ void __launch_bounds__(1024) k_coarsest_pint_round(CoarsestView cv, const double* __restrict__ x,
+                                                              const double* __restrict__ vin,
+                                                              double* __restrict__ vout, int r) {
   pdl_entry();
-  extern __shared__ double sp[];
+  extern __shared__ double sv[];
   const int m = cv.m;
   const int64_t nn = cv.lv.nn, nt = cv.lv.n_t;
-  const int tid = threadIdx.x, bs = blockDim.x;
-  auto end_level = [&](int64_t c) {
-    const int64_t s = (c + 1) * cv.pint_len;
-    return ADJ ? nt + 1 - s : s;
+  const int c = blockIdx.x, tid = threadIdx.x, bs = blockDim.x;
+  const int d = 1 << r;
+  auto end_row = [&](int64_t cc) -> const double* {
+    const int64_t s = (cc + 1) * cv.pint_len;
+    return x + (ADJ ? nt + 1 - s : s) * nn + 1;
   };
-  for (int j = tid; j < m; j += bs) {
-    const double v = x[end_level(0) * nn + j + 1];
-    sp[j] = v;
-    starts[j] = v;
+  const double* own = r == 0 ? end_row(c) : vin + (int64_t)c * m;
+  if (c < d) {
+    for (int j = tid; j < m; j += bs) vout[(int64_t)c * m + j] = own[j];
+    return;
   }
+  const double* src = r == 0 ? end_row(c - d) : vin + (int64_t)(c - d) * m;
+  for (int j = tid; j < m; j += bs) sv[j] = src[j];
   __syncthreads();
-  for (int64_t c = 1; c < cv.pint_chunks; ++c) {
-    const int64_t ne = end_level(c);
-    double v[4];
-    int cnt = 0;
-    for (int j = tid; j < m; j += bs, ++cnt) {
-      double acc = x[ne * nn + j + 1];
-      for (int k = 0; k < m; ++k) acc = fma(cv.pint_prop[(int64_t)k * m + j], sp[k], acc);
-      v[cnt] = acc;
-      starts[c * m + j] = acc;
-    }
+  const double* Q = cv.pint_pow + (int64_t)r * m * m;
+  for (int j = tid; j < m; j += bs) {
+    double acc = own[j];
+    for (int k = 0; k < m; ++k) acc = fma(Q[(int64_t)k * m + j], sv[k], acc);
+    vout[(int64_t)c * m + j] = acc;
+  }
+}
+
+// C = A B for column-major m x m (the propagator squares; one-off per hierarchy).
+__global__ void k_square(const double* __restrict__ A, double* __restrict__ C, int m) {
+  __shared__ double ta[16][17], tb[16][17];
+  const int i = blockIdx.y * 16 + threadIdx.y, j = blockIdx.x * 16 + threadIdx.x;
+  double acc = 0.0;
+  for (int k0 = 0; k0 < m; k0 += 16) {
+    // A(i, k) at k * m + i; B = A
+    ta[threadIdx.y][threadIdx.x] = (i < m && k0 + threadIdx.x < m) ? A[(int64_t)(k0 + threadIdx.x) * m + i] : 0.0;
+    tb[threadIdx.y][threadIdx.x] = (k0 + threadIdx.y < m && j < m) ? A[(int64_t)j * m + k0 + threadIdx.y] : 0.0;
     __syncthreads();
-    cnt = 0;
-    for (int j = tid; j < m; j += bs, ++cnt) sp[j] = v[cnt];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc = fma(ta[threadIdx.y][k], tb[k][threadIdx.x], acc);
     __syncthreads();
   }
+  if (i < m && j < m) C[(int64_t)j * m + i] = acc;
 }
 
 // Coarsest exact solve for n_el <= 32: one warp, lane j owns unmasked node
@@ -2689,11 +2705,14 @@ int launch_prolong_add(const LevelView& F, const LevelView& C, int dir, const do
   return check_launch();
 }
 
-int launch_coarsest_pint_prop(const CoarsestView& cv, double* P, cudaStream_t s) {
+int launch_coarsest_pint_prop(const CoarsestView& cv, double* P, int rounds, cudaStream_t s) {
   const size_t smem = sizeof(double) * 3 * (size_t)cv.m;
   const int threads = cv.m >= 1024 ? 1024 : (int)((cv.m + 31) / 32 * 32);
   pdl_launch(k_coarsest_pint<false, 2>, cv.m, threads, smem, s, cv, (const double*)nullptr, P,
              (const double*)nullptr);
+  const int64_t mm = (int64_t)cv.m * cv.m;
+  const dim3 blk(16, 16), grd((cv.m + 15) / 16, (cv.m + 15) / 16);
+  for (int r = 1; r < rounds; ++r) k_square<<<grd, blk, 0, s>>>(P + (r - 1) * mm, P + r * mm, cv.m);
   return check_launch();
 }
 
@@ -2703,14 +2722,24 @@ int launch_coarsest(bool adjoint, const CoarsestView& cv, const double* f, doubl
     const size_t smem = sizeof(double) * 3 * (size_t)cv.m;
     int threads = cv.m >= 1024 ? 1024 : (int)((cv.m + 31) / 32 * 32);
     const int C = cv.pint_chunks;
+    // scan rounds ping-pong between the two halves of scratch; the last round
+    // writes the half that PHASE 1 reads
+    double* half[2] = {scratch, scratch + (int64_t)C * cv.m};
+    const int R = cv.pint_rounds;
+    const size_t vsm = sizeof(double) * (size_t)cv.m;
+    auto outbuf = [&](int r) { return half[(R - 1 - r) & 1]; };
     if (adjoint) {
-      pdl_launch(k_coarsest_pint<true, 0>, C, threads, smem, s, cv, f, x, (const double*)scratch);
-      pdl_launch(k_coarsest_pint_link<true>, 1, threads, sizeof(double) * (size_t)cv.m, s, cv, x, scratch);
-      pdl_launch(k_coarsest_pint<true, 1>, C - 1, threads, smem, s, cv, f, x, (const double*)scratch);
+      pdl_launch(k_coarsest_pint<true, 0>, C, threads, smem, s, cv, f, x, (const double*)nullptr);
+      for (int r = 0; r < R; ++r)
+        pdl_launch(k_coarsest_pint_round<true>, C, threads, vsm, s, cv, (const double*)x,
+                   (const double*)(r == 0 ? nullptr : outbuf(r - 1)), outbuf(r), r);
+      pdl_launch(k_coarsest_pint<true, 1>, C - 1, threads, smem, s, cv, f, x, (const double*)half[0]);
     } else {
-      pdl_launch(k_coarsest_pint<false, 0>, C, threads, smem, s, cv, f, x, (const double*)scratch);
-      pdl_launch(k_coarsest_pint_link<false>, 1, threads, sizeof(double) * (size_t)cv.m, s, cv, x, scratch);
-      pdl_launch(k_coarsest_pint<false, 1>, C - 1, threads, smem, s, cv, f, x, (const double*)scratch);
+      pdl_launch(k_coarsest_pint<false, 0>, C, threads, smem, s, cv, f, x, (const double*)nullptr);
+      for (int r = 0; r < R; ++r)
+        pdl_launch(k_coarsest_pint_round<false>, C, threads, vsm, s, cv, (const double*)x,
+                   (const double*)(r == 0 ? nullptr : outbuf(r - 1)), outbuf(r), r);
+      pdl_launch(k_coarsest_pint<false, 1>, C - 1, threads, smem, s, cv, f, x, (const double*)half[0]);
     }
     return check_launch();
   }
