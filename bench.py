@@ -503,8 +503,15 @@ def main():
         cnt, secs = (pairs, pair_s) if use_pair else (singles, single_s)
         avg = secs / cnt
         achieved = 24.0 * n0 / avg / 1e9
+        # DRAM bytes per launch of the same kernel at this size from the committed
+        # `ncu --set full` capture (profiles/round1.md: k_lean2x2<0,8>, grid (5, 513)):
+        # 67.317 MB read + 8.611 MB written; ncu replays cold-cache, so this is the
+        # L2-miss traffic of an isolated launch, an upper bound for the in-solve one
+        traffic = (67.317248e6 + 8.611328e6) if (use_pair and n0 == 1025 * 4097) else None
         roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                    "frac": achieved / hbm, "traffic": None,
+                    "frac": achieved / hbm, "traffic": traffic,
+                    "traffic_source": ("ncu --set full, profiles/round1.md (cold-cache replay)"
+                                       if traffic else None),
                     "kernel": ("k_lean2x2 (two fused Jacobi sweeps, fine level, in-graph CUDA events)"
                                if use_pair else "k_lean2<sweep> (fine level, in-graph CUDA events)"),
                     "algorithmic_bytes_per_launch": 24 * n0, "dof_updates_per_launch": (2 if use_pair else 1) * n0,
