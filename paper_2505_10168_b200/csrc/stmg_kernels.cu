@@ -175,11 +175,19 @@ __device__ __forceinline__ double prolong_row(const double* __restrict__ xc, int
 // Staged-row loaders.  operator() is the per-lane form (any lane subset);
 // warp_row() is called by all 32 lanes of a warp whose nodes wfirst-1 ..
 // wfirst+30 are all inside the grid (interior tiles).
+// Interior staging is split in two phases: warp_load issues every global load
+// of a row (all rows of a tile first, so the loads are in flight together),
+// warp_finish combines them (shuffles) once they are needed.
 struct PlainLoad {
   const double* __restrict__ x;
   int64_t nn;
   __device__ __forceinline__ double operator()(int64_t n, int64_t i) const { return x[n * nn + i]; }
   __device__ __forceinline__ double warp_row(int64_t n, int64_t i, int64_t, int) const { return x[n * nn + i]; }
+  struct Raw {
+    double x;
+  };
+  __device__ __forceinline__ Raw warp_load(int64_t n, int64_t i, int64_t, int) const { return {x[n * nn + i]}; }
+  __device__ __forceinline__ double warp_finish(const Raw& r, int64_t, int64_t, int) const { return r.x; }
 };
 
 template <int DIR>
@@ -195,15 +203,31 @@ struct ProlongLoad {
   // values by shuffle; even/odd rows are selected, not branched.  Same
   // arithmetic as prolong_row.
   __device__ __forceinline__ double warp_row(int64_t n, int64_t i, int64_t wfirst, int lane) const {
-    if (DIR == 1) return x[n * nn + i] + prolong_row<1>(xc, nnc, n, i);
+    return warp_finish(warp_load(n, i, wfirst, lane), i, wfirst, lane);
+  }
+  struct Raw {
+    double x, v;
+  };
+  __device__ __forceinline__ Raw warp_load(int64_t n, int64_t i, int64_t wfirst, int lane) const {
+    Raw r;
+    r.x = x[n * nn + i];
+    if (DIR == 1) {
+      r.v = __ldg(xc + (n >> 1) * nnc + i);
+    } else {
+      const int64_t c0 = (wfirst - 1) >> 1;
+      r.v = (lane <= 17 && c0 + lane < nnc) ? __ldg(xc + n * nnc + c0 + lane) : 0.0;
+    }
+    return r;
+  }
+  __device__ __forceinline__ double warp_finish(const Raw& r, int64_t i, int64_t wfirst, int) const {
+    if (DIR == 1) return r.x + (0.0 + 1.0 * r.v);  // prolong_row<1>
     const int64_t c0 = (wfirst - 1) >> 1;
-    const double v = (lane <= 17 && c0 + lane < nnc) ? __ldg(xc + n * nnc + c0 + lane) : 0.0;
     const int k0 = (int)((i >> 1) - c0);
-    const double va = __shfl_sync(kFull, v, k0);      // xc[i/2] (even), xc[(i-1)/2] (odd)
-    const double vb = __shfl_sync(kFull, v, k0 + 1);  // xc[(i+1)/2] (odd)
+    const double va = __shfl_sync(kFull, r.v, k0);      // xc[i/2] (even), xc[(i-1)/2] (odd)
+    const double vb = __shfl_sync(kFull, r.v, k0 + 1);  // xc[(i+1)/2] (odd)
     const double pe = 0.0 + 1.0 * va;
     const double po = (0.5 * va + 0.5 * vb) + 0.0;
-    return x[n * nn + i] + ((i & 1) == 0 ? pe : po);
+    return r.x + ((i & 1) == 0 ? pe : po);
   }
 };
 
@@ -387,9 +411,12 @@ __device__ __forceinline__ double dev_lean2(const LevelView& L, const Ld& ld, co
     const double* fp = f + (n0 * nn + i);
 #pragma unroll
     for (int k = 0; k < NT; ++k) fv[k] = fp[k * nn];
+    typename Ld::Raw raw[NT + 1];
 #pragma unroll
-    for (int r = 0; r <= NT; ++r) xr[r] = ld.warp_row(nbase + r, i, wfirst, lane);
+    for (int r = 0; r <= NT; ++r) raw[r] = ld.warp_load(nbase + r, i, wfirst, lane);
     const Coefs c = load_coefs(L, i);
+#pragma unroll
+    for (int r = 0; r <= NT; ++r) xr[r] = ld.warp_finish(raw[r], i, wfirst, lane);
     double* yp = y + (n0 * nn + i);
     double pm = __shfl_up_sync(kFull, xr[0], 1);
     double pp = __shfl_down_sync(kFull, xr[0], 1);
