@@ -145,6 +145,10 @@ GENERAL = {
     "gen_br_deep": ("uniform", 32, 64, "BR", [0, 0, 1, 0, 1], False, 3),
     "gen_cp_x4": ("uniform", 128, 128, "CP", [0, 0, 0, 0], False, 1),
     "gen_bp_uni": ("uniform", 32, 64, "BP", [1, 0, 1], False, 2),
+    # bilinear transfers above a rediscretised 64 x 64 coarsest level: the parallel-in-time march
+    "gen_br_wide": ("cfg1", 64, 256, "BR", [1, 1], False, 2),
+    "gen_bd_adj": ("cfg1", 32, 64, "BD", [0, 1, 1], True, 2),
+    "gen_cp_deep_adj": ("uniform", 64, 128, "CP", [0, 1, 0, 1], True, 1),
 }
 GENERAL_CASES = list(GENERAL)
 
