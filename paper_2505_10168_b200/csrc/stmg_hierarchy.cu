@@ -718,7 +718,7 @@ void sync_unless_capturing(cudaStream_t s) {
 // Levels with at most this many DOFs use 4-level time tiles in the stencil
 // kernels (shorter serial chains where a launch is latency-bound).
 // STMG_SMALL_NT_DOFS overrides; read when a hierarchy is built.
-constexpr int64_t kSmallNtDofs = 2500000;  // measured: cfg1 solve 66.2 -> 57.7 ms (profiles/round1.md)
+constexpr int64_t kSmallNtDofs = 5000000;  // measured: cfg1 solve 66.2 -> 57.7 ms (2.5M); 49.82 -> 49.68 ms (5M, A/B)
 // Levels with at most kTinyNtDofs DOFs use 2-level tiles (STMG_TINY_NT_DOFS).
 constexpr int64_t kTinyNtDofs = 1100000;  // measured: cfg1 solve 53.3 -> 50.8 ms
 int64_t tile_nt_for(int64_t dofs) {
