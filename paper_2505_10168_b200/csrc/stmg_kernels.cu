@@ -640,7 +640,7 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
 }
 
 template <bool ADJ, int NT>
-__global__ void __launch_bounds__(kMaxTW, (NT <= 4 ? 4 : 3)) k_lean2x2(LevelView L, const double* __restrict__ f,
+__global__ void __launch_bounds__(kMaxTW, (NT <= 2 ? 5 : NT <= 4 ? 4 : 3)) k_lean2x2(LevelView L, const double* __restrict__ f,
                                                        const double* __restrict__ x,
                                                        double* __restrict__ y, double omega) {
   pdl_entry();
@@ -1075,7 +1075,7 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
 }
 
 template <bool ADJ, int DIR, int NT>
-__global__ void __launch_bounds__(kMaxTW, (NT <= 4 ? 4 : 3)) k_restrict2(LevelView F, LevelView C, const double* __restrict__ f,
+__global__ void __launch_bounds__(kMaxTW, (NT <= 2 ? 5 : NT <= 4 ? 4 : 3)) k_restrict2(LevelView F, LevelView C, const double* __restrict__ f,
                                                          const double* __restrict__ x, double* __restrict__ fc,
                                                          double* __restrict__ xc0, double omega) {
   pdl_entry();
@@ -2494,7 +2494,7 @@ void launch_pass(const LevelView& L, const Ld& ld, const double* f, double* y, d
       break;
     case 5:
       if (lean_nt(L) == 2)
-        pdl_launch(k_lean2<ADJ, MODE, NORM, 2, 4, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
+        pdl_launch(k_lean2<ADJ, MODE, NORM, 2, 5, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
       else if (lean_nt(L) == 4)
         pdl_launch(k_lean2<ADJ, MODE, NORM, 4, 4, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
       else
