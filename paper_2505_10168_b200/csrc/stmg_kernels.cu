@@ -639,8 +639,16 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
   }
 }
 
-template <bool ADJ, int NT>
-__global__ void __launch_bounds__(kMaxTW, (NT <= 2 ? 5 : NT <= 4 ? 4 : 3)) k_lean2x2(LevelView L, const double* __restrict__ f,
+// Resident blocks per SM the kernels are compiled for: 5 (48 registers) pays on
+// mid-sized levels, where the launch fills the GPU and latency is hidden by
+// warps; on small levels the few blocks never fill the SMs and the spills of the
+// tighter register budget cost latency, so 3 is used there (launch sites).
+constexpr int64_t kMinB5Dofs = 200000;
+template <int NT>
+constexpr int minb_for_nt() { return NT <= 2 ? 5 : NT <= 4 ? 4 : 3; }
+
+template <bool ADJ, int NT, int MINB = minb_for_nt<NT>()>
+__global__ void __launch_bounds__(kMaxTW, MINB) k_lean2x2(LevelView L, const double* __restrict__ f,
                                                        const double* __restrict__ x,
                                                        double* __restrict__ y, double omega) {
   pdl_entry();
@@ -1074,8 +1082,8 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
   }
 }
 
-template <bool ADJ, int DIR, int NT>
-__global__ void __launch_bounds__(kMaxTW, (NT <= 2 ? 5 : NT <= 4 ? 4 : 3)) k_restrict2(LevelView F, LevelView C, const double* __restrict__ f,
+template <bool ADJ, int DIR, int NT, int MINB = minb_for_nt<NT>()>
+__global__ void __launch_bounds__(kMaxTW, MINB) k_restrict2(LevelView F, LevelView C, const double* __restrict__ f,
                                                          const double* __restrict__ x, double* __restrict__ fc,
                                                          double* __restrict__ xc0, double omega) {
   pdl_entry();
@@ -2493,8 +2501,10 @@ void launch_pass(const LevelView& L, const Ld& ld, const double* f, double* y, d
       pdl_launch(k_tile<ADJ, MODE, NORM, 8, 2, Ld>, grd, blk, tile_smem(blk, 8, 2), s, L, ld, f, y, omega, partials);
       break;
     case 5:
-      if (lean_nt(L) == 2)
+      if (lean_nt(L) == 2 && L.nn * (L.n_t + 1) >= kMinB5Dofs)
         pdl_launch(k_lean2<ADJ, MODE, NORM, 2, 5, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
+      else if (lean_nt(L) == 2)
+        pdl_launch(k_lean2<ADJ, MODE, NORM, 2, 3, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
       else if (lean_nt(L) == 4)
         pdl_launch(k_lean2<ADJ, MODE, NORM, 4, 4, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
       else
@@ -2543,8 +2553,10 @@ int restrict_tile_impl(const LevelView& F, const LevelView& C, const double* f, 
     const int64_t warps = DIR == 0 ? ceil_div(C.nn, 14) : ceil_div(F.nn, 30);
     const dim3 rb = balanced_block(warps);
     const int64_t tiles = ceil_div(warps, rb.x / 32);
-    if (lean_nt(F) == 2)
+    if (lean_nt(F) == 2 && F.nn * (F.n_t + 1) >= kMinB5Dofs)
       pdl_launch(k_restrict2<ADJ, DIR, 2>, tgrid(tiles, (rows(F) + 1) / 2), rb, 0, s, F, C, f, x, fc, xc0, omega);
+    else if (lean_nt(F) == 2)
+      pdl_launch(k_restrict2<ADJ, DIR, 2, 3>, tgrid(tiles, (rows(F) + 1) / 2), rb, 0, s, F, C, f, x, fc, xc0, omega);
     else if (lean_nt(F) == 4)
       pdl_launch(k_restrict2<ADJ, DIR, 4>, tgrid(tiles, (rows(F) + 3) / 4), rb, 0, s, F, C, f, x, fc, xc0, omega);
     else
@@ -2602,8 +2614,13 @@ int launch_sweep2(bool adjoint, const LevelView& L, const double* f, const doubl
   const int64_t tiles = ceil_div(warps, blk.x / 32);
   if (lean_nt(L) == 2) {
     const dim3 grd = tgrid(tiles, (rows(L) + 1) / 2);
-    if (adjoint) pdl_launch(k_lean2x2<true, 2>, grd, blk, 0, s, L, f, x, y, omega);
-    else pdl_launch(k_lean2x2<false, 2>, grd, blk, 0, s, L, f, x, y, omega);
+    if (L.nn * (L.n_t + 1) >= kMinB5Dofs) {
+      if (adjoint) pdl_launch(k_lean2x2<true, 2>, grd, blk, 0, s, L, f, x, y, omega);
+      else pdl_launch(k_lean2x2<false, 2>, grd, blk, 0, s, L, f, x, y, omega);
+    } else {
+      if (adjoint) pdl_launch(k_lean2x2<true, 2, 3>, grd, blk, 0, s, L, f, x, y, omega);
+      else pdl_launch(k_lean2x2<false, 2, 3>, grd, blk, 0, s, L, f, x, y, omega);
+    }
   } else if (lean_nt(L) == 4) {
     const dim3 grd = tgrid(tiles, (rows(L) + 3) / 4);
     if (adjoint) pdl_launch(k_lean2x2<true, 4>, grd, blk, 0, s, L, f, x, y, omega);
