@@ -802,6 +802,16 @@ int64_t bulk_for(int64_t dofs) {
   return lim > 0 && dofs >= lim ? 1 : 0;
 }
 
+// Levels with at least this many DOFs run their fused pairs through the
+// streaming march (k_march2); STMG_MARCH_DOFS overrides (0 = never).  Measured
+// slower than k_lean2x2 on every BASELINE config 1 level (profiles/round1.md).
+constexpr int64_t kMarchDofs = 0;
+int64_t march_for(int64_t dofs) {
+  int64_t lim = kMarchDofs;
+  if (const char* v = std::getenv("STMG_MARCH_DOFS")) lim = std::atoll(v);
+  return lim > 0 && dofs >= lim ? 1 : 0;
+}
+
 void upload_levels(stmg_hierarchy* h) {
   h->coef.clear();
   h->views.clear();
@@ -822,6 +832,7 @@ void upload_levels(stmg_hierarchy* h) {
     v.tile_nt = tile_nt_for(v.nn * (v.n_t + 1));
     v.sweep_depth = sweep_depth_for(v.nn * (v.n_t + 1));
     v.bulk = bulk_for(v.nn * (v.n_t + 1));
+    v.march = march_for(v.nn * (v.n_t + 1));
     h->views.push_back(v);
     h->device_bytes += static_cast<int64_t>((t.size() + kVecPad) * 8);
     h->coef.push_back(std::move(buf));
@@ -886,6 +897,7 @@ void finish_create(stmg_hierarchy* h, bool share_ws_from_other, const stmg_hiera
     for (size_t l = 0; l < h->views.size() && l < other->views.size(); ++l) {
       h->views[l].sweep_depth = other->views[l].sweep_depth;
       h->views[l].bulk = other->views[l].bulk;
+      h->views[l].march = other->views[l].march;
     }
     h->ws = other->ws;
   } else {

@@ -35,6 +35,9 @@ struct LevelView {
   // Fused pairs through the bulk-copy pipelined kernel (k_bulk) instead of
   // k_lean2x2; fixed at build (STMG_BULK_DOFS: levels with at least that many DOFs).
   int64_t bulk = 0;
+  // Fused pairs through the streaming march (k_march2) instead of k_lean2x2;
+  // fixed at build (STMG_MARCH_DOFS: levels with at least that many DOFs).
+  int64_t march = 0;
 };
 
 inline bool full_range(const LevelView& L) { return L.n_lo == 0 && L.n_hi == L.n_t + 1; }

@@ -20,6 +20,7 @@
 #include <cstdint>
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 #include <utility>
 
 #include "stmg_internal.h"
@@ -752,6 +753,156 @@ __global__ void __launch_bounds__(kMaxTW, 3) k_leanD(LevelView L, const double* 
   const bool nodes_in = first - D + 1 >= 2 && first - D + 30 <= L.n_el - 1;
   if (rows_in && nodes_in) leanD_body<ADJ, NT, D, false>(L, f, x, y, omega, first, n0, lane);
   else leanD_body<ADJ, NT, D, true>(L, f, x, y, omega, first, n0, lane);
+}
+
+// Streaming fused pair: two damped-Jacobi sweeps in one pass, bit-identical to
+// k_lean2x2 (same overlapping-warp strips: lane l holds node node1 + l - 1,
+// sweep 1 valid on lanes 1..30, lanes 2..29 stored), but each warp marches
+// its strip through a whole segment [a, b) of S rows instead of an NT-row tile.
+// Both sweeps of row m are evaluated in the step that stages level m: sweep 1
+// from (x_m, x_{m-1}) and sweep 2 from (y1_m, y1_{m-1}), the coupled level and
+// its shuffled neighbours carried in registers from the previous step (J
+// marches up in time; J^T couples to m + 1 and marches down).  x and f of the
+// next Q rows are in flight in a register queue.  Per stored row this is
+// 2 loads, 1 store, 2 row evaluations and 4 shuffles of 64-bit values, with
+// one redundant sweep-1 row per segment (k_lean2x2 with NT = 4 evaluates
+// 9 rows and re-stages 2 levels per 4 stored rows).
+template <bool ADJ, int Q>
+__device__ __forceinline__ void march2_body(const LevelView& L, const double* __restrict__ f,
+                                            const double* __restrict__ x, double* __restrict__ y,
+                                            double omega, int64_t node1, int64_t a, int S, int lane) {
+  const int64_t nn = L.nn;
+  const int64_t i = node1 + lane - 1;
+  const bool lane2 = lane >= 2 && lane <= 29;
+  const int64_t dn = ADJ ? -nn : nn;            // element step between consecutive rows
+  const int64_t m0 = ADJ ? a + S : a - 1;       // sweep-1-only row
+  const Coefs c = load_coefs(L, i);
+  const double* px = x + ((m0 - (ADJ ? -1 : 1)) * nn + i);  // its staged coupled level
+  const double* pf = f + (m0 * nn + i);
+  double* py = y + (m0 * nn + i);
+  double xprev = px[0];
+  px += dn;
+  double x1 = px[0], fm = pf[0];
+  px += dn;
+  pf += dn;
+  double qx[Q], qf[Q];
+#pragma unroll
+  for (int k = 0; k < Q; ++k) {
+    qx[k] = px[0];
+    qf[k] = pf[0];
+    px += dn;
+    pf += dn;
+  }
+  // row m0: sweep 1 only
+  double pm = __shfl_up_sync(kFull, xprev, 1), pp = __shfl_down_sync(kFull, xprev, 1);
+  double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
+  double y1prev = x1 + omega * ((fm - row_interior<ADJ>(c, qm, x1, qp, pm, xprev, pp)) * c.invd);
+  double am = __shfl_up_sync(kFull, y1prev, 1), ap = __shfl_down_sync(kFull, y1prev, 1);
+  xprev = x1;
+  pm = qm;
+  pp = qp;
+  py += dn;
+  // one queue group of Q rows; PRE: refill the queue with the next group
+  auto group = [&](auto pre) {
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {
+      x1 = qx[k];
+      fm = qf[k];
+      if (decltype(pre)::value) {
+        qx[k] = px[0];
+        qf[k] = pf[0];
+        px += dn;
+        pf += dn;
+      }
+      qm = __shfl_up_sync(kFull, x1, 1);
+      qp = __shfl_down_sync(kFull, x1, 1);
+      const double y1 = x1 + omega * ((fm - row_interior<ADJ>(c, qm, x1, qp, pm, xprev, pp)) * c.invd);
+      const double bm = __shfl_up_sync(kFull, y1, 1), bp = __shfl_down_sync(kFull, y1, 1);
+      if (lane2) *py = y1 + omega * ((fm - row_interior<ADJ>(c, bm, y1, bp, am, y1prev, ap)) * c.invd);
+      py += dn;
+      xprev = x1;
+      pm = qm;
+      pp = qp;
+      y1prev = y1;
+      am = bm;
+      ap = bp;
+    }
+  };
+  for (int g = Q; g < S; g += Q) group(std::true_type{});
+  group(std::false_type{});
+}
+
+// Boundary segments (time 0 / n_t, the first or last nodes, a short last
+// segment) stream through the same march with the general row evaluation.
+// Not inlined: its registers do not count against the interior march's budget.
+template <bool ADJ>
+__device__ __noinline__ void march2_edge(const LevelView& L, const double* __restrict__ f,
+                                         const double* __restrict__ x, double* __restrict__ y,
+                                         double omega, int64_t node1, int64_t a, int64_t b) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nn = L.nn, nt = L.n_t;
+  const int64_t i = node1 + lane - 1;
+  const bool in_grid = i >= 0 && i < nn;
+  const bool lane1 = lane >= 1 && lane <= 30 && in_grid;
+  const bool lane2 = lane >= 2 && lane <= 29 && in_grid;
+  const int64_t step = ADJ ? -1 : 1;
+  const int64_t m0 = ADJ ? b : a - 1;  // first sweep-1 row
+  const int64_t s0 = m0 - step;        // its staged coupled level
+  Coefs c{};
+  if (lane1) c = load_coefs(L, i);
+  double xprev = (s0 >= 0 && s0 <= nt && in_grid) ? x[s0 * nn + i] : 0.0;
+  double pm = __shfl_up_sync(kFull, xprev, 1), pp = __shfl_down_sync(kFull, xprev, 1);
+  double y1prev = 0.0, am = 0.0, ap = 0.0;
+  for (int64_t j = 0, m = m0; j <= b - a; ++j, m += step) {
+    const bool ok = m >= 0 && m <= nt;
+    const double x1 = (ok && in_grid) ? x[m * nn + i] : 0.0;
+    const double fm = (ok && lane1) ? f[m * nn + i] : 0.0;
+    const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
+    double y1 = 0.0;
+    if (lane1 && ok) {
+      const double row = row_sum<ADJ>(L, m, i, c, qm, x1, qp, pm, xprev, pp);
+      const double id = (m == 0 || i == 0) ? L.inv_w : c.invd;
+      y1 = x1 + omega * ((fm - row) * id);
+    }
+    const double bm = __shfl_up_sync(kFull, y1, 1), bp = __shfl_down_sync(kFull, y1, 1);
+    if (j >= 1 && lane2) {
+      const double row = row_sum<ADJ>(L, m, i, c, bm, y1, bp, am, y1prev, ap);
+      const double id = (m == 0 || i == 0) ? L.inv_w : c.invd;
+      y[m * nn + i] = y1 + omega * ((fm - row) * id);
+    }
+    xprev = x1;
+    pm = qm;
+    pp = qp;
+    y1prev = y1;
+    am = bm;
+    ap = bp;
+  }
+}
+
+// seg is a multiple of Q: a segment that touches a boundary or is cut short by
+// the end of the level takes march2_edge.
+template <bool ADJ, int Q, int MINB>
+__global__ void __launch_bounds__(kMaxTW, MINB) k_march2(LevelView L, const double* __restrict__ f,
+                                                      const double* __restrict__ x, double* __restrict__ y,
+                                                      double omega, int64_t seg) {
+  pdl_entry();
+  const int64_t tt = (int64_t)blockIdx.z * gridDim.y + blockIdx.y;  // segment
+  const int64_t a = L.n_lo + tt * seg;
+  if (a >= L.n_hi) return;
+  const int64_t b = a + seg < L.n_hi ? a + seg : L.n_hi;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t node1 = (int64_t)blockIdx.x * ((int64_t)(blockDim.x >> 5) * 28) + warp * 28 - 1;
+  if (node1 + 1 >= L.nn) return;  // no stored node in this warp
+  const int64_t nt = L.n_t;
+  // every sweep-1 row has its coupled level and is unmasked; every sweep-1
+  // node (lanes 1..30) has both neighbours
+  const bool rows_in = ADJ ? (a >= 1 && b <= nt - 1) : (a >= 3);
+  const bool nodes_in = node1 >= 2 && node1 + 29 <= L.n_el - 1;
+  if (rows_in && nodes_in && b - a == seg) {
+    march2_body<ADJ, Q>(L, f, x, y, omega, node1, a, (int)seg, lane);
+  } else {
+    march2_edge<ADJ>(L, f, x, y, omega, node1, a, b);
+  }
 }
 
 // f_c = R (f - J x) over one lean tile, R = s P^T (proj/src/transfer.cpp:95-104);
@@ -2607,8 +2758,49 @@ int launch_sweep(bool adjoint, const LevelView& L, const double* f, const double
                  : sweep_impl<false>(L, f, x, y, omega, partials, s);
 }
 
+// Streaming pair (k_march2) on levels built with L.march (STMG_MARCH_DOFS).
+// Segments are sized so that the grid holds about g_march_waves x (148 SMs x
+// resident warps per SM) warps; queue depth and residency: STMG_MARCH_Q / _MINB.
+int g_march_q = 4;
+double g_march_waves = 1.0;
+int g_march_minb = 4;
+
+template <bool ADJ, int Q>
+void march2_launch(const LevelView& L, dim3 grd, dim3 blk, int64_t seg, const double* f, const double* x,
+                   double* y, double omega, cudaStream_t s) {
+  if (g_march_minb >= 4) pdl_launch(k_march2<ADJ, Q, 4>, grd, blk, 0, s, L, f, x, y, omega, seg);
+  else pdl_launch(k_march2<ADJ, Q, 3>, grd, blk, 0, s, L, f, x, y, omega, seg);
+}
+
+int launch_sweep2_march(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
+                        double omega, cudaStream_t s) {
+  const int64_t warps = ceil_div(L.nn, 28);
+  const dim3 blk = balanced_block(warps);
+  const int64_t tiles = ceil_div(warps, blk.x / 32);
+  const int64_t grid_warps = tiles * (blk.x / 32);
+  const int64_t target = (int64_t)(g_march_waves * kNumSMs * 8 * (g_march_minb >= 4 ? 4 : 3));
+  int64_t segs = target / grid_warps;
+  if (segs < 1) segs = 1;
+  int64_t seg = ceil_div(rows(L), segs);
+  const int64_t q = g_march_q == 8 ? 8 : g_march_q == 2 ? 2 : 4;
+  seg = ceil_div(seg, q) * q;  // whole queue groups
+  const dim3 grd = tgrid(tiles, ceil_div(rows(L), seg));
+  if (g_march_q == 8) {
+    if (adjoint) march2_launch<true, 8>(L, grd, blk, seg, f, x, y, omega, s);
+    else march2_launch<false, 8>(L, grd, blk, seg, f, x, y, omega, s);
+  } else if (g_march_q == 2) {
+    if (adjoint) march2_launch<true, 2>(L, grd, blk, seg, f, x, y, omega, s);
+    else march2_launch<false, 2>(L, grd, blk, seg, f, x, y, omega, s);
+  } else {
+    if (adjoint) march2_launch<true, 4>(L, grd, blk, seg, f, x, y, omega, s);
+    else march2_launch<false, 4>(L, grd, blk, seg, f, x, y, omega, s);
+  }
+  return check_launch();
+}
+
 int launch_sweep2(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
                   double omega, cudaStream_t s) {
+  if (L.march) return launch_sweep2_march(adjoint, L, f, x, y, omega, s);
   const int64_t warps = ceil_div(L.nn, 28);
   const dim3 blk = balanced_block(warps);
   const int64_t tiles = ceil_div(warps, blk.x / 32);
@@ -2824,6 +3016,9 @@ int kernels_init() {
     env_read = true;
     if (const char* v = std::getenv("STMG_KERNEL_VARIANT")) set_kernel_variant(std::atoi(v));
     if (const char* v = std::getenv("STMG_PDL")) g_pdl = std::atoi(v) != 0;
+    if (const char* v = std::getenv("STMG_MARCH_Q")) g_march_q = std::atoi(v);
+    if (const char* v = std::getenv("STMG_MARCH_WAVES")) g_march_waves = std::atof(v);
+    if (const char* v = std::getenv("STMG_MARCH_MINB")) g_march_minb = std::atoi(v);
   }
   // The coarsest march keeps its two PCR work vectors in shared memory up to 160 KB.
   cudaError_t e = cudaFuncSetAttribute(k_coarsest<true>,
