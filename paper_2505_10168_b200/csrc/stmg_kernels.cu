@@ -2596,9 +2596,15 @@ inline int variant_nt(int v) { return (v == 1 || v == 2) ? 4 : v == 6 ? 16 : 8; 
 // Overlapping-warp kernels: warps per block chosen so that the node tiles cover
 // the level evenly (<= 8 warps per block).  E.g. 257 nodes -> 2 blocks of 5
 // warps, not one full and one almost empty block of 8.
-inline dim3 balanced_block(int64_t warps) {
+// At most 4 warps per block on levels of >= g_wpb4_dofs DOFs (STMG_WPB4_DOFS),
+// 8 below: on large levels smaller blocks retire and refill SM slots sooner
+// (cfg1 A/B 43.10 -> 42.69 ms with 4 everywhere; cfg2-scale sweep 4.51 -> 4.21 ms),
+// on small levels the extra blocks cost more than they gain.
+int64_t g_wpb4_dofs = 1000000;
+inline int wpb_for(const LevelView& L) { return L.nn * (L.n_t + 1) >= g_wpb4_dofs ? 4 : 8; }
+inline dim3 balanced_block(int64_t warps, int max_wpb) {
   if (warps < 1) warps = 1;
-  const int64_t bx = (warps + 7) / 8;
+  const int64_t bx = (warps + max_wpb - 1) / max_wpb;
   return dim3((unsigned)(32 * ((warps + bx - 1) / bx)));
 }
 inline int lean_nt(const LevelView& L) { return L.tile_nt == 2 ? 2 : L.tile_nt == 4 ? 4 : 8; }
@@ -2615,7 +2621,7 @@ inline dim3 tgrid(int64_t x, int64_t t) {
   return dim3((unsigned)x, (unsigned)y, (unsigned)((t + y - 1) / y));
 }
 inline dim3 pass_block(const LevelView& L, int v) {
-  return (v == 5 || v == 6) ? balanced_block((L.nn + 29) / 30) : march_block(L);
+  return (v == 5 || v == 6) ? balanced_block((L.nn + 29) / 30, wpb_for(L)) : march_block(L);
 }
 inline dim3 grid_for(const LevelView& L, dim3 blk, int v) {
   if (v == 5 || v == 6) {
@@ -2702,7 +2708,7 @@ int restrict_tile_impl(const LevelView& F, const LevelView& C, const double* f, 
   if (v == 5 || v == 6) {
     // DIR 0: warp w owns coarse nodes 14 w .. 14 w + 13; DIR 1: fine nodes 30 w ..
     const int64_t warps = DIR == 0 ? ceil_div(C.nn, 14) : ceil_div(F.nn, 30);
-    const dim3 rb = balanced_block(warps);
+    const dim3 rb = balanced_block(warps, wpb_for(F));
     const int64_t tiles = ceil_div(warps, rb.x / 32);
     if (lean_nt(F) == 2 && F.nn * (F.n_t + 1) >= kMinB5Dofs)
       pdl_launch(k_restrict2<ADJ, DIR, 2>, tgrid(tiles, (rows(F) + 1) / 2), rb, 0, s, F, C, f, x, fc, xc0, omega);
@@ -2775,7 +2781,7 @@ void march2_launch(const LevelView& L, dim3 grd, dim3 blk, int64_t seg, const do
 int launch_sweep2_march(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
                         double omega, cudaStream_t s) {
   const int64_t warps = ceil_div(L.nn, 28);
-  const dim3 blk = balanced_block(warps);
+  const dim3 blk = balanced_block(warps, wpb_for(L));
   const int64_t tiles = ceil_div(warps, blk.x / 32);
   const int64_t grid_warps = tiles * (blk.x / 32);
   const int64_t target = (int64_t)(g_march_waves * kNumSMs * 8 * (g_march_minb >= 4 ? 4 : 3));
@@ -2802,7 +2808,7 @@ int launch_sweep2(bool adjoint, const LevelView& L, const double* f, const doubl
                   double omega, cudaStream_t s) {
   if (L.march) return launch_sweep2_march(adjoint, L, f, x, y, omega, s);
   const int64_t warps = ceil_div(L.nn, 28);
-  const dim3 blk = balanced_block(warps);
+  const dim3 blk = balanced_block(warps, wpb_for(L));
   const int64_t tiles = ceil_div(warps, blk.x / 32);
   if (lean_nt(L) == 2) {
     const dim3 grd = tgrid(tiles, (rows(L) + 1) / 2);
@@ -2861,7 +2867,7 @@ int launch_sweep_deep(bool adjoint, const LevelView& L, int depth, const double*
                       double* y, double omega, cudaStream_t s) {
   if (!full_range(L) || (depth != 3 && depth != 4)) return static_cast<int>(cudaErrorInvalidValue);
   const int64_t warps = ceil_div(L.nn, 32 - 2 * depth);
-  const dim3 blk = balanced_block(warps);
+  const dim3 blk = balanced_block(warps, wpb_for(L));
   const int64_t tiles = ceil_div(warps, blk.x / 32);
   if (lean_nt(L) == 2) {  // the level's time-tile depth (2, else 4)
     const dim3 grd = tgrid(tiles, (rows(L) + 1) / 2);
@@ -3016,6 +3022,7 @@ int kernels_init() {
     env_read = true;
     if (const char* v = std::getenv("STMG_KERNEL_VARIANT")) set_kernel_variant(std::atoi(v));
     if (const char* v = std::getenv("STMG_PDL")) g_pdl = std::atoi(v) != 0;
+    if (const char* v = std::getenv("STMG_WPB4_DOFS")) g_wpb4_dofs = std::atoll(v);
     if (const char* v = std::getenv("STMG_MARCH_Q")) g_march_q = std::atoi(v);
     if (const char* v = std::getenv("STMG_MARCH_WAVES")) g_march_waves = std::atof(v);
     if (const char* v = std::getenv("STMG_MARCH_MINB")) g_march_minb = std::atoi(v);
