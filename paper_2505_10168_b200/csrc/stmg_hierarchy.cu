@@ -720,7 +720,7 @@ void sync_unless_capturing(cudaStream_t s) {
 // STMG_SMALL_NT_DOFS overrides; read when a hierarchy is built.
 constexpr int64_t kSmallNtDofs = 5000000;  // measured: cfg1 solve 66.2 -> 57.7 ms (2.5M); 49.82 -> 49.68 ms (5M, A/B)
 // Levels with at most kTinyNtDofs DOFs use 2-level tiles (STMG_TINY_NT_DOFS).
-constexpr int64_t kTinyNtDofs = 1100000;  // measured: cfg1 solve 53.3 -> 50.8 ms
+constexpr int64_t kTinyNtDofs = 600000;  // measured: cfg1 solve 53.3 -> 50.8 ms (1.1M); 41.34 -> 41.09 ms (600K, A/B)
 int64_t tile_nt_for(int64_t dofs) {
   int64_t lim = kSmallNtDofs, tiny = kTinyNtDofs;
   if (const char* v = std::getenv("STMG_SMALL_NT_DOFS")) lim = std::atoll(v);
