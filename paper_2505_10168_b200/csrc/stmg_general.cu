@@ -307,30 +307,11 @@ int launch_load_vector(int kind, const double* params, int n_params, double L, d
   return check();
 }
 
-// mg_solve's per-cycle bookkeeping (proj/src/multigrid.cpp:260-273) on the
-// device, for the solve loop run as a conditional WHILE graph node: relative
-// residual from the norm partial sums (scalars[0] = ||b||^2, scalars[1] =
-// ||b - J u||^2), history entry, status, and whether another V-cycle runs.
-// sqrt is correctly rounded, so rn equals the host loop's value bit for bit.
+// mg_solve's per-cycle bookkeeping on the device, for the solve loop run as a
+// conditional WHILE graph node (scalars[0] = ||b||^2, scalars[1] = ||b - J u||^2).
 __global__ void k_cycle_check(const double* __restrict__ scalars, SolveLoopCtl* ctl, double* hist,
                               cudaGraphConditionalHandle handle) {
-  const double norm_b = sqrt(scalars[0]);
-  const double denom = norm_b == 0.0 ? 1.0 : norm_b;
-  const double rn = sqrt(scalars[1]) / denom;
-  const int c = ctl->cycles + 1;
-  ctl->cycles = c;
-  hist[c] = rn;
-  unsigned go = 1;
-  if (rn < ctl->tol) {
-    ctl->status = 0;  // STMG_CONVERGED
-    go = 0;
-  } else if (!isfinite(rn) || rn > ctl->div_tol) {
-    ctl->status = 2;  // STMG_DIVERGED
-    go = 0;
-  } else if (c >= ctl->max_cycles) {
-    go = 0;  // STMG_MAX_CYCLES (set by the host)
-  }
-  cudaGraphSetConditional(handle, go);
+  cycle_check_body(scalars[0], scalars[1], ctl, hist, handle);
 }
 
 int launch_cycle_check(const double* scalars, SolveLoopCtl* ctl, double* hist,

@@ -1183,9 +1183,10 @@ cudaGraphExec_t get_loop(stmg_hierarchy* h, int nu, double omega) {
     launch_check(launch_sweep(h->adjoint, h->views[0], ws.f[0]->p, ws.xa[0]->p, spec ? ws.xb[0]->p : nullptr,
                               omega, ws.partials->p, &np, cs),
                  "norm sweep");
-    launch_check(launch_finalize_sum(ws.partials->p, np, ws.scalars->p + 1, cs), "finalize");
     auto* ctl = reinterpret_cast<SolveLoopCtl*>(ws.loop->p);
-    launch_check(launch_cycle_check(ws.scalars->p, ctl, ws.loop->p + kLoopCtlDoubles, handle, cs), "cycle check");
+    launch_check(launch_finalize_check(ws.partials->p, np, ws.scalars->p, ctl, ws.loop->p + kLoopCtlDoubles,
+                                       handle, cs),
+                 "finalize + cycle check");
   } catch (...) {
     ok = false;
   }
@@ -1296,7 +1297,7 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
     rep->cycles = ctl->cycles;
     rep->status = ctl->status;
     rep->smoother_dof_updates = per_cycle_updates * ctl->cycles;
-    launches += static_cast<int64_t>(ctl->cycles) * (g->kernels + 3);
+    launches += static_cast<int64_t>(ctl->cycles) * (g->kernels + 2);
   } else {
     rep->status = STMG_MAX_CYCLES;
     for (int cycle = 1; cycle <= o.max_cycles; ++cycle) {

@@ -150,6 +150,35 @@ struct SolveLoopCtl {
 // One cycle's bookkeeping (history, status) and the loop's continue flag.
 int launch_cycle_check(const double* scalars, SolveLoopCtl* ctl, double* hist,
                        cudaGraphConditionalHandle handle, cudaStream_t s);
+// launch_finalize_sum(partials, n, scalars + 1) and launch_cycle_check in one
+// kernel (same summation order, so the same bits).
+int launch_finalize_check(const double* partials, int64_t n, double* scalars, SolveLoopCtl* ctl, double* hist,
+                          cudaGraphConditionalHandle handle, cudaStream_t s);
+#ifdef __CUDACC__
+// mg_solve's per-cycle bookkeeping (proj/src/multigrid.cpp:260-273) from the
+// squared norms ||b||^2 and ||b - J u||^2; sqrt is correctly rounded, so rn
+// equals the host loop's value bit for bit.
+__device__ __forceinline__ void cycle_check_body(double bb, double rr, SolveLoopCtl* ctl, double* hist,
+                                                 cudaGraphConditionalHandle handle) {
+  const double norm_b = sqrt(bb);
+  const double denom = norm_b == 0.0 ? 1.0 : norm_b;
+  const double rn = sqrt(rr) / denom;
+  const int c = ctl->cycles + 1;
+  ctl->cycles = c;
+  hist[c] = rn;
+  unsigned go = 1;
+  if (rn < ctl->tol) {
+    ctl->status = 0;  // STMG_CONVERGED
+    go = 0;
+  } else if (!isfinite(rn) || rn > ctl->div_tol) {
+    ctl->status = 2;  // STMG_DIVERGED
+    go = 0;
+  } else if (c >= ctl->max_cycles) {
+    go = 0;  // STMG_MAX_CYCLES (set by the host)
+  }
+  cudaGraphSetConditional(handle, go);
+}
+#endif
 // y = x * a (y may alias x)
 int launch_scale(const double* x, double a, double* y, int64_t n, cudaStream_t s);
 // load_vector(g, q) + masking into device memory (source kinds as stmg_load_vector)

@@ -2566,6 +2566,20 @@ __global__ void k_finalize_sum(const double* __restrict__ partials, int64_t n, d
   if (threadIdx.x == 0) *out = s;
 }
 
+// k_finalize_sum into scalars[1], then the cycle bookkeeping (one launch less
+// per cycle of the device-side solve loop).
+__global__ void k_finalize_check(const double* __restrict__ partials, int64_t n, double* scalars,
+                                 SolveLoopCtl* ctl, double* hist, cudaGraphConditionalHandle handle) {
+  pdl_entry();
+  double acc = 0.0;
+  for (int64_t idx = threadIdx.x; idx < n; idx += blockDim.x) acc = acc + partials[idx];
+  const double s = block_sum(acc);
+  if (threadIdx.x == 0) {
+    scalars[1] = s;
+    cycle_check_body(scalars[0], s, ctl, hist, handle);
+  }
+}
+
 // Launchers return the cudaError_t of the launch (0 on success).
 inline int check_launch() { return static_cast<int>(cudaGetLastError()); }
 
@@ -3126,6 +3140,12 @@ int launch_tail(bool adjoint, const TailParams& p, int cluster, int* final_buf, 
 
 int launch_finalize_sum(const double* partials, int64_t n, double* out, cudaStream_t s) {
   pdl_launch(k_finalize_sum, 1, 1024, 0, s, partials, n, out);
+  return check_launch();
+}
+
+int launch_finalize_check(const double* partials, int64_t n, double* scalars, SolveLoopCtl* ctl, double* hist,
+                          cudaGraphConditionalHandle handle, cudaStream_t s) {
+  pdl_launch(k_finalize_check, 1, 1024, 0, s, partials, n, scalars, ctl, hist, handle);
   return check_launch();
 }
 
