@@ -64,6 +64,19 @@ inline void pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// The pointer's value, hidden from the optimiser: a 32-bit element offset from
+// it then costs one IMAD.WIDE per access instead of being folded back into
+// 64-bit index arithmetic.
+template <class T>
+__device__ __forceinline__ T* opaque(T* p) {
+  asm("mov.b64 %0, %0;" : "+l"(p));
+  return p;
+}
+
+__device__ __forceinline__ void st_global(double* p, double v) {
+  asm volatile("st.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
 // Canonical 4-lane accumulator for rows whose entry pattern is not the
 // interior one (boundaries, masked columns).
 struct Acc {
@@ -527,12 +540,21 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
   const bool nodes_in = node1 >= 2 && node1 + 29 <= L.n_el - 1;
   double xs[NT + 2], fv[NT + 1], y1[NT + 1];
   if (rows_in && nodes_in) {
-    const double* xp = x + (sbase * nn + i);
-    const double* fp = f + (s1base * nn + i);
+    // one 64-bit row base for x, f and y; 32-bit element offsets from it
+    // (o[j] = node i on staged row sbase + j), so each access is one IMAD.WIDE
+    const int64_t rowbase = sbase * nn;
+    const double* __restrict__ xb = opaque(x + rowbase);
+    const double* __restrict__ fb = opaque(f + rowbase);
+    double* __restrict__ yb = opaque(y + rowbase);
+    const uint32_t nn32 = (uint32_t)nn;
+    uint32_t o[NT + 2];
+    o[0] = (uint32_t)i;
 #pragma unroll
-    for (int r = 0; r < NT + 2; ++r) xs[r] = xp[r * nn];
+    for (int r = 1; r < NT + 2; ++r) o[r] = o[r - 1] + nn32;
 #pragma unroll
-    for (int r = 0; r < NT + 1; ++r) fv[r] = fp[r * nn];
+    for (int r = 0; r < NT + 2; ++r) xs[r] = __ldg(xb + o[r]);
+#pragma unroll
+    for (int r = 0; r < NT + 1; ++r) fv[r] = __ldg(fb + o[ADJ ? r : r + 1]);  // f rows s1base + r
     const Coefs c = load_coefs(L, i);
     double pm = __shfl_up_sync(kFull, xs[0], 1), pp = __shfl_down_sync(kFull, xs[0], 1);
 #pragma unroll
@@ -545,18 +567,17 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
       pp = qp;
     }
     const bool lane2 = lane >= 2 && lane <= 29;
-    double* yp = y + (n0 * nn + i);
     double am = __shfl_up_sync(kFull, y1[0], 1), ap = __shfl_down_sync(kFull, y1[0], 1);
 #pragma unroll
     for (int k = 0; k < NT; ++k) {
       const double z1 = y1[k + 1];
       const double bm = __shfl_up_sync(kFull, z1, 1), bp = __shfl_down_sync(kFull, z1, 1);
-      if (lane2) {
-        if (ADJ)
-          yp[k * nn] = y1[k] + omega * ((fv[k] - row_interior<true>(c, am, y1[k], ap, bm, z1, bp)) * c.invd);
-        else
-          yp[k * nn] = z1 + omega * ((fv[k + 1] - row_interior<false>(c, bm, z1, bp, am, y1[k], ap)) * c.invd);
-      }
+      // evaluated on every lane (no divergence around the shuffles); stored on
+      // lanes 2..29; row n0 + k is staged row k (J^T) / k + 2 (J)
+      const double v =
+          ADJ ? y1[k] + omega * ((fv[k] - row_interior<true>(c, am, y1[k], ap, bm, z1, bp)) * c.invd)
+              : z1 + omega * ((fv[k + 1] - row_interior<false>(c, bm, z1, bp, am, y1[k], ap)) * c.invd);
+      if (lane2) st_global(yb + o[ADJ ? k : k + 2], v);
       am = bm;
       ap = bp;
     }
