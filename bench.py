@@ -328,6 +328,10 @@ def _ref_worker(config, argd, sample_nt):
 
 
 def main():
+    # NCCL_DEBUG=VERSION (set on some images) prints a banner on stdout at
+    # communicator creation; the bench prints exactly one JSON line there
+    if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
+        os.environ["NCCL_DEBUG"] = "WARN"
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
