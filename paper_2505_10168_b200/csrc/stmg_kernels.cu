@@ -2803,6 +2803,12 @@ int launch_sweep(bool adjoint, const LevelView& L, const double* f, const double
                  : sweep_impl<false>(L, f, x, y, omega, partials, s);
 }
 
+// Fused pairs with 16-level time tiles on 8-level-tile levels of >= g_pair16_dofs
+// DOFs (STMG_PAIR16_DOFS; off by default), 2 or 3 resident 256-thread blocks'
+// worth of registers (STMG_PAIR16_MINB).
+int64_t g_pair16_dofs = int64_t{1} << 62;
+int g_pair16_minb = 2;
+
 // Streaming pair (k_march2) on levels built with L.march (STMG_MARCH_DOFS).
 // Segments are sized so that the grid holds about g_march_waves x (148 SMs x
 // resident warps per SM) warps; queue depth and residency: STMG_MARCH_Q / _MINB.
@@ -2862,6 +2868,15 @@ int launch_sweep2(bool adjoint, const LevelView& L, const double* f, const doubl
     const dim3 grd = tgrid(tiles, (rows(L) + 3) / 4);
     if (adjoint) pdl_launch(k_lean2x2<true, 4>, grd, blk, 0, s, L, f, x, y, omega);
     else pdl_launch(k_lean2x2<false, 4>, grd, blk, 0, s, L, f, x, y, omega);
+  } else if (L.nn * (L.n_t + 1) >= g_pair16_dofs) {
+    const dim3 grd = tgrid(tiles, (rows(L) + 15) / 16);
+    if (g_pair16_minb >= 3) {
+      if (adjoint) pdl_launch(k_lean2x2<true, 16, 3>, grd, blk, 0, s, L, f, x, y, omega);
+      else pdl_launch(k_lean2x2<false, 16, 3>, grd, blk, 0, s, L, f, x, y, omega);
+    } else {
+      if (adjoint) pdl_launch(k_lean2x2<true, 16, 2>, grd, blk, 0, s, L, f, x, y, omega);
+      else pdl_launch(k_lean2x2<false, 16, 2>, grd, blk, 0, s, L, f, x, y, omega);
+    }
   } else {
     const dim3 grd = tgrid(tiles, (rows(L) + 7) / 8);
     if (adjoint) pdl_launch(k_lean2x2<true, 8>, grd, blk, 0, s, L, f, x, y, omega);
@@ -3062,6 +3077,8 @@ int kernels_init() {
     if (const char* v = std::getenv("STMG_KERNEL_VARIANT")) set_kernel_variant(std::atoi(v));
     if (const char* v = std::getenv("STMG_PDL")) g_pdl = std::atoi(v) != 0;
     if (const char* v = std::getenv("STMG_WPB4_DOFS")) g_wpb4_dofs = std::atoll(v);
+    if (const char* v = std::getenv("STMG_PAIR16_DOFS")) g_pair16_dofs = std::atoll(v);
+    if (const char* v = std::getenv("STMG_PAIR16_MINB")) g_pair16_minb = std::atoi(v);
     if (const char* v = std::getenv("STMG_PROLONG_WPB8_DOFS")) g_prolong_wpb8_dofs = std::atoll(v);
     if (const char* v = std::getenv("STMG_MARCH_Q")) g_march_q = std::atoi(v);
     if (const char* v = std::getenv("STMG_MARCH_WAVES")) g_march_waves = std::atof(v);
