@@ -461,7 +461,6 @@ struct stmg_hierarchy {
   int profiling = 0;  // 0 off, 1 finest-level kernels, 2 every kernel
   int tail_start = -1;   // first level run by the coarse-tail cluster kernel (-1: none)
   int tail_cluster = 0;   // 0: grid-wide cooperative tail; 1..16: one cluster
-  bool tail_v2 = false;   // the tail is k_tail2 (first sweep from zero fused into the parent's restriction)
   // per (level, kind): launches and device seconds accumulated while profiling
   std::vector<std::array<std::pair<int64_t, double>, stmgb::kTimedKinds>> prof;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -813,10 +812,6 @@ int64_t march_for(int64_t dofs) {
   return lim > 0 && dofs >= lim ? 1 : 0;
 }
 
-// Levels with at most this many DOFs (and the coarsest) run as one k_tail2
-// cluster launch per V-cycle; STMG_TAIL2_DOFS overrides (0 = never).
-constexpr int64_t kTail2Dofs = 0;
-
 void upload_levels(stmg_hierarchy* h) {
   h->coef.clear();
   h->views.clear();
@@ -886,23 +881,11 @@ void finish_create(stmg_hierarchy* h, bool share_ws_from_other, const stmg_hiera
     if (const char* v = std::getenv("STMG_TAIL_DOFS")) tail_dofs = std::atoll(v);
     if (const char* v = std::getenv("STMG_TAIL_CLUSTER")) h->tail_cluster = std::max(0, std::min(16, std::atoi(v)));
     h->tail_start = -1;
-    h->tail_v2 = false;
     const int nl = h->n_levels();
     if (tail_dofs > 0 && nl >= 2 && tail_supported(h->coarsest) && !h->general()) {
       for (int l = 1; l < nl; ++l)
         if (h->ndofs(l) <= tail_dofs && nl - l <= kTailMaxLevels) {
           h->tail_start = l;
-          break;
-        }
-    }
-    // k_tail2 (STMG_TAIL2_DOFS): levels of <= that many DOFs, at least one above the coarsest
-    int64_t tail2_dofs = kTail2Dofs;
-    if (const char* v = std::getenv("STMG_TAIL2_DOFS")) tail2_dofs = std::atoll(v);
-    if (h->tail_start < 0 && tail2_dofs > 0 && nl >= 3 && tail_supported(h->coarsest) && !h->general()) {
-      for (int l = 1; l + 1 < nl; ++l)
-        if (h->ndofs(l) <= tail2_dofs && nl - l <= kTailMaxLevels) {
-          h->tail_start = l;
-          h->tail_v2 = true;
           break;
         }
     }
@@ -1041,12 +1024,7 @@ struct Emitter {
       tp.cv = h->coarsest;
       int fin = 0;
       timed_launch(l, kTimedTail, [&] {
-        if (h->tail_v2) {
-          if (!zero_done) throw std::logic_error("k_tail2 needs the parent's fused first sweep");
-          launch_check(launch_tail2(h->adjoint, tp, &fin, s), "coarse tail");
-        } else {
-          launch_check(launch_tail(h->adjoint, tp, h->tail_cluster, &fin, s), "coarse tail");
-        }
+        launch_check(launch_tail(h->adjoint, tp, h->tail_cluster, &fin, s), "coarse tail");
       });
       ++kernels;
       return fin;
@@ -1089,7 +1067,7 @@ struct Emitter {
     // the child's first pre-smoothing sweep (from zero) is fused into this
     // restriction unless the child is the coarsest level or the coarse tail
     const bool fuse_zero =
-        fused && nu >= 1 && l + 1 < nl - 1 && (l + 1 != h->tail_start || h->tail_v2) && !h->galerkin(l + 1);
+        fused && nu >= 1 && l + 1 < nl - 1 && l + 1 != h->tail_start && !h->galerkin(l + 1);
     if (fused) {
       timed_launch(l, kTimedRestrict, [&] {
         launch_check(launch_restrict_residual(h->adjoint, L, C, h->dirs[l], f, buf(l, cur),

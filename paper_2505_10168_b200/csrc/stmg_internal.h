@@ -248,9 +248,6 @@ int kernels_init();  // once per device
 // cluster >= 1: one thread-block cluster of that many CTAs; cluster <= 0: a cooperative
 // launch over every SM (grid-wide barriers between passes).
 int launch_tail(bool adjoint, const TailParams& p, int cluster, int* final_buf, cudaStream_t s);
-// Second tail design (k_tail2): its first level's from-zero sweep comes from the
-// parent's restriction; at least one level above the coarsest.
-int launch_tail2(bool adjoint, const TailParams& p, int* final_buf, cudaStream_t s);
 bool tail_supported(const CoarsestView& cv);
 // Kernel design selection for benchmarking (0 = production default).
 void set_kernel_variant(int v);

@@ -402,14 +402,14 @@ __global__ void __launch_bounds__(kMaxTW, MINB) k_lean(LevelView L, Ld ld,
 // unconditional loads, the fixed interior lane order.
 // Tile body (callable from the stand-alone kernel and the coarse-tail kernel):
 // node tile `tile`, time tile `ttile`, `tw` threads; returns the thread's r^2 sum.
-// dev_lean2_w: the same body for the warp whose strip is number `wslot` along x.
 template <bool ADJ, int MODE, bool NORM, int NT, class Ld>
-__device__ __forceinline__ double dev_lean2_w(const LevelView& L, const Ld& ld, const double* __restrict__ f,
-                                              double* __restrict__ y, double omega, int64_t wslot,
-                                              int64_t ttile) {
-  const int lane = threadIdx.x & 31;
+__device__ __forceinline__ double dev_lean2(const LevelView& L, const Ld& ld, const double* __restrict__ f,
+                                            double* __restrict__ y, double omega, int64_t tile,
+                                            int64_t ttile, int tw) {
+  if ((int)threadIdx.x >= tw) return 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nn = L.nn, nt = L.n_t;
-  const int64_t wfirst = wslot * 30;  // first computing node of the warp
+  const int64_t wfirst = tile * ((tw >> 5) * 30) + warp * 30;  // first computing node of the warp
   if (wfirst >= nn) return 0.0;                                  // whole warp past the grid
   const int64_t i = wfirst + lane - 1;                           // node of this lane
   const int64_t n0 = L.n_lo + ttile * NT;
@@ -497,14 +497,6 @@ __device__ __forceinline__ double dev_lean2_w(const LevelView& L, const Ld& ld, 
 
 inline __host__ __device__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-template <bool ADJ, int MODE, bool NORM, int NT, class Ld>
-__device__ __forceinline__ double dev_lean2(const LevelView& L, const Ld& ld, const double* __restrict__ f,
-                                            double* __restrict__ y, double omega, int64_t tile,
-                                            int64_t ttile, int tw) {
-  if ((int)threadIdx.x >= tw) return 0.0;
-  return dev_lean2_w<ADJ, MODE, NORM, NT>(L, ld, f, y, omega, tile * (tw >> 5) + (threadIdx.x >> 5), ttile);
-}
-
 template <bool ADJ, int MODE, bool NORM, int NT, int MINB, class Ld>
 __global__ void __launch_bounds__(kMaxTW, MINB) k_lean2(LevelView L, Ld ld,
                                                         const double* __restrict__ f,
@@ -530,10 +522,10 @@ __global__ void __launch_bounds__(kMaxTW, MINB) k_lean2(LevelView L, Ld ld,
 template <bool ADJ, int NT>
 __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __restrict__ f,
                                             const double* __restrict__ x, double* __restrict__ y,
-                                            double omega, int64_t wslot, int64_t ttile) {
-  const int lane = threadIdx.x & 31;
+                                            double omega, int64_t tile, int64_t ttile) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nn = L.nn, nt = L.n_t;
-  const int64_t node1 = wslot * 28 - 1;  // node of lane 1 (warp strip number wslot along x)
+  const int64_t node1 = tile * ((int64_t)(blockDim.x >> 5) * 28) + warp * 28 - 1;  // node of lane 1
   if (node1 + 1 >= nn) return;  // no stored node in this warp (whole warp exits)
   const int64_t i = node1 + lane - 1;  // node of this lane
   const int64_t n0 = L.n_lo + ttile * NT;
@@ -683,8 +675,7 @@ __global__ void __launch_bounds__(kMaxTW, MINB) k_lean2x2(LevelView L, const dou
                                                        double* __restrict__ y, double omega) {
   pdl_entry();
   const int64_t tt = (int64_t)blockIdx.z * gridDim.y + blockIdx.y;  // time tile
-  if (tt < ceil_div(L.n_hi - L.n_lo, NT))
-    dev_lean2x2<ADJ, NT>(L, f, x, y, omega, (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), tt);
+  if (tt < ceil_div(L.n_hi - L.n_lo, NT)) dev_lean2x2<ADJ, NT>(L, f, x, y, omega, blockIdx.x, tt);
 }
 
 // D damped-Jacobi sweeps fused into one pass (temporal blocking of depth D,
@@ -1134,14 +1125,15 @@ __device__ __forceinline__ double coarse_from_zero(const LevelView& C, int64_t N
 }
 
 template <bool ADJ, int DIR, int NT>
-__device__ __forceinline__ void dev_restrict2_w(const LevelView& F, const LevelView& C,
-                                                const double* __restrict__ f, const double* __restrict__ x,
-                                                double* __restrict__ fc, int64_t wslot, int64_t ttile,
-                                                double* __restrict__ xc0 = nullptr, double omega = 0.0) {
+__device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelView& C,
+                                              const double* __restrict__ f, const double* __restrict__ x,
+                                              double* __restrict__ fc, int64_t tile, int64_t ttile, int tw,
+                                              double* __restrict__ xc0 = nullptr, double omega = 0.0) {
+  if ((int)threadIdx.x >= tw) return;
   constexpr int kAdv = DIR == 0 ? 28 : 30;  // nodes per warp
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nn = F.nn, nt = F.n_t, nnc = C.nn;
-  const int64_t base = wslot * kAdv + (DIR == 0 ? -2 : 0);
+  const int64_t base = tile * ((tw >> 5) * kAdv) + warp * kAdv + (DIR == 0 ? -2 : 0);
   if (DIR == 0 ? (base / 2 + 1 >= nnc) : (base >= nn)) return;  // whole warp past the grid
   const int64_t i = base - 1 + lane;
   const int64_t n0 = F.n_lo + ttile * NT;
@@ -1260,15 +1252,6 @@ __device__ __forceinline__ void dev_restrict2_w(const LevelView& F, const LevelV
     pm = qm;
     pp = qp;
   }
-}
-
-template <bool ADJ, int DIR, int NT>
-__device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelView& C,
-                                              const double* __restrict__ f, const double* __restrict__ x,
-                                              double* __restrict__ fc, int64_t tile, int64_t ttile, int tw,
-                                              double* __restrict__ xc0 = nullptr, double omega = 0.0) {
-  if ((int)threadIdx.x >= tw) return;
-  dev_restrict2_w<ADJ, DIR, NT>(F, C, f, x, fc, tile * (tw >> 5) + (threadIdx.x >> 5), ttile, xc0, omega);
 }
 
 template <bool ADJ, int DIR, int NT, int MINB = minb_for_nt<NT>()>
@@ -2419,8 +2402,6 @@ __device__ __forceinline__ void dev_coarsest_chunked(const CoarsestView& cv, con
     }
   }
   __syncthreads();
-  // A's rows stay in registers from (2) to (4).  Reloading them for (4) instead
-  // removes the spills at 128 registers but costs more (24.4 -> 25.1 us at cfg1).
   double arow[32];
 #pragma unroll
   for (int k = 0; k < 32; ++k) arow[k] = cv.prop[k * 32 + lane];
@@ -2571,88 +2552,6 @@ __global__ void __launch_bounds__(kMaxTW, 1) k_tail(TailParams p) {
       sweep_pass(l, c == 0 ? p.xa[l] : p.xb[l], c == 0 ? p.xb[l] : p.xa[l]);
       c ^= 1;
     }
-    child = c;
-  }
-}
-
-// Coarse tail, second design: one 16-CTA cluster of 512-thread CTAs runs the
-// V-cycle below a size threshold.  Work is handed out per warp strip (every
-// warp of the cluster strides over the (strip, 2-level time tile) tasks of a
-// pass, so one round covers a small level), smoothing uses the fused pairs,
-// each restriction also writes the child's first sweep from zero (the tail's
-// first level gets it from the parent's restriction), CTA 0 runs the chunked
-// coarsest march with all 16 warps, and a cluster barrier separates passes.
-// The tile bodies are the stand-alone kernels', so results are bit-identical.
-constexpr int kTail2Threads = 512;
-constexpr int kTail2Cluster = 16;
-template <bool ADJ>
-__global__ void __launch_bounds__(kTail2Threads, 1) k_tail2(TailParams p) {
-  pdl_entry();
-  extern __shared__ double sm[];
-  namespace cg = cooperative_groups;
-  cg::cluster_group cl = cg::this_cluster();
-  const int64_t nwarps = (int64_t)cl.num_blocks() * (blockDim.x >> 5);
-  const int64_t gw = (int64_t)cl.block_rank() * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int nl = p.n_levels;
-  const double om = p.omega;
-  int cur[kTailMaxLevels];
-  auto buf = [&](int l, int c) { return c == 0 ? p.xa[l] : p.xb[l]; };
-  // `count` sweeps on level l from buffer c: fused pairs, then a single sweep
-  auto smooth = [&](int l, int& c, int count) {
-    const LevelView& L = p.lv[l];
-    const int64_t tts = ceil_div(L.n_hi - L.n_lo, 2);
-    for (; count >= 2; count -= 2) {
-      const int64_t wx = ceil_div(L.nn, 28);
-      for (int64_t t = gw; t < wx * tts; t += nwarps)
-        dev_lean2x2<ADJ, 2>(L, p.f[l], buf(l, c), buf(l, 1 - c), om, t % wx, t / wx);
-      cl.sync();
-      c ^= 1;
-    }
-    if (count == 1) {
-      const int64_t wx = ceil_div(L.nn, 30);
-      const PlainLoad ld{buf(l, c), L.nn};
-      for (int64_t t = gw; t < wx * tts; t += nwarps)
-        dev_lean2_w<ADJ, kSweep, false, 2>(L, ld, p.f[l], buf(l, 1 - c), om, t % wx, t / wx);
-      cl.sync();
-      c ^= 1;
-    }
-  };
-  for (int l = 0; l + 1 < nl; ++l) {
-    const LevelView& L = p.lv[l];
-    const LevelView& C = p.lv[l + 1];
-    int c = 0;  // buffer 0 holds the first sweep from zero
-    smooth(l, c, p.nu - 1);
-    double* xc0 = l + 2 < nl ? p.xa[l + 1] : nullptr;  // not for the coarsest child
-    const int64_t wx = p.dir[l] == 0 ? ceil_div(C.nn, 14) : ceil_div(L.nn, 30);
-    const int64_t total = wx * ceil_div(L.n_hi - L.n_lo, 2);
-    for (int64_t t = gw; t < total; t += nwarps) {
-      if (p.dir[l] == 0) dev_restrict2_w<ADJ, 0, 2>(L, C, p.f[l], buf(l, c), p.f[l + 1], t % wx, t / wx, xc0, om);
-      else dev_restrict2_w<ADJ, 1, 2>(L, C, p.f[l], buf(l, c), p.f[l + 1], t % wx, t / wx, xc0, om);
-    }
-    cl.sync();
-    cur[l] = c;
-  }
-  if (cl.block_rank() == 0) dev_coarsest_chunked<ADJ>(p.cv, p.f[nl - 1], p.xa[nl - 1], sm);
-  cl.sync();
-  int child = 0;
-  for (int l = nl - 2; l >= 0; --l) {
-    const LevelView& L = p.lv[l];
-    const LevelView& C = p.lv[l + 1];
-    int c = cur[l];
-    const int64_t wx = ceil_div(L.nn, 30);
-    const int64_t total = wx * ceil_div(L.n_hi - L.n_lo, 2);
-    if (p.dir[l] == 0) {
-      const ProlongLoad<0> ld{buf(l, c), buf(l + 1, child), L.nn, C.nn};
-      for (int64_t t = gw; t < total; t += nwarps)
-        dev_lean2_w<ADJ, kSweep, false, 2>(L, ld, p.f[l], buf(l, 1 - c), om, t % wx, t / wx);
-    } else {
-      const ProlongLoad<1> ld{buf(l, c), buf(l + 1, child), L.nn, C.nn};
-      for (int64_t t = gw; t < total; t += nwarps)
-        dev_lean2_w<ADJ, kSweep, false, 2>(L, ld, p.f[l], buf(l, 1 - c), om, t % wx, t / wx);
-    }
-    cl.sync();
-    c ^= 1;
-    smooth(l, c, p.nu - 1);
     child = c;
   }
 }
@@ -3204,12 +3103,6 @@ int kernels_init() {
   e = cudaFuncSetAttribute(k_coarsest_chunked<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            160 * 1024);
   if (e != cudaSuccess) return static_cast<int>(e);
-  for (auto fn : {k_tail2<true>, k_tail2<false>}) {
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    if (e != cudaSuccess) return static_cast<int>(e);
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return static_cast<int>(e);
-  }
   for (auto fn : {k_tail<true, ClusterScope>, k_tail<false, ClusterScope>}) {
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     if (e != cudaSuccess) return static_cast<int>(e);
@@ -3243,30 +3136,6 @@ int tail_grid_blocks(const TailParams& p) {
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
     return 0;
   return per_sm * sms;
-}
-
-int launch_tail2(bool adjoint, const TailParams& p, int* final_buf, cudaStream_t s) {
-  if (p.nu < 1 || p.n_levels < 2 || p.n_levels > kTailMaxLevels || !tail_supported(p.cv)) return 1;
-  // result buffer of tail level 0: buffer 0 after the from-zero sweep, one flip
-  // per smoothing launch (pairs, then a single), one for the prolong-sweep
-  const int sl = (p.nu - 1) / 2 + (p.nu - 1) % 2;
-  if (final_buf) *final_buf = (2 * sl + 1) & 1;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(kTail2Cluster);
-  cfg.blockDim = dim3(kTail2Threads);
-  cfg.dynamicSmemBytes = coarsest_chunked_smem(p.cv);
-  cfg.stream = s;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = kTail2Cluster;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = g_pdl ? 2 : 1;
-  const cudaError_t e = adjoint ? cudaLaunchKernelEx(&cfg, k_tail2<true>, p) : cudaLaunchKernelEx(&cfg, k_tail2<false>, p);
-  return static_cast<int>(e);
 }
 
 int launch_tail(bool adjoint, const TailParams& p, int cluster, int* final_buf, cudaStream_t s) {

@@ -378,24 +378,3 @@ def test_solve_with_deep_smoothing(torch, S, port, monkeypatch, name, depth):
     r1 = S.mg_solve(gpu_hier(S, cs, port), b, u1, opts)
     assert r1.cycles == r0.cycles and r1.history == r0.history
     assert np.array_equal(bits(u1), bits(u0))
-
-
-@pytest.mark.parametrize("nu", [1, 2, 5])
-@pytest.mark.parametrize("dofs", ["20000", "10000000000"])
-@pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "time_first", "cfg4_mini"])
-def test_coarse_tail2_kernel_is_bitwise(torch, S, port, monkeypatch, name, dofs, nu):
-    """The second coarse-tail design (STMG_TAIL2_DOFS: one 16-CTA cluster, warp
-    strips, fused pairs, first sweeps from zero fused into the restrictions)
-    gives the same iterate bit for bit as the per-level launches, from a tail
-    of the smallest levels up to every level below the finest."""
-    cs = case(name)
-    b = cs.rhs_vector(port)
-    opts = S.SolveOptions(nu=nu, tol=cs.tol, max_cycles=12)
-    monkeypatch.setenv("STMG_TAIL2_DOFS", "0")
-    u0 = np.zeros_like(b)
-    r0 = S.mg_solve(gpu_hier(S, cs, port), b, u0, opts)
-    monkeypatch.setenv("STMG_TAIL2_DOFS", dofs)
-    u1 = np.zeros_like(b)
-    r1 = S.mg_solve(gpu_hier(S, cs, port), b, u1, opts)
-    assert r1.cycles == r0.cycles and r1.history == r0.history
-    assert np.array_equal(bits(u1), bits(u0))
