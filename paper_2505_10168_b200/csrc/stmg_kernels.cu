@@ -2636,9 +2636,6 @@ inline int variant_nt(int v) { return (v == 1 || v == 2) ? 4 : v == 6 ? 16 : 8; 
 // (cfg1 A/B 43.10 -> 42.69 ms with 4 everywhere; cfg2-scale sweep 4.51 -> 4.21 ms),
 // on small levels the extra blocks cost more than they gain.
 int64_t g_wpb4_dofs = 1000000;
-// the fused prolong-sweep keeps 8-warp blocks on levels of >= this many DOFs
-// (STMG_PROLONG_WPB8_DOFS)
-int64_t g_prolong_wpb8_dofs = int64_t{1} << 62;
 inline int wpb_for(const LevelView& L) { return L.nn * (L.n_t + 1) >= g_wpb4_dofs ? 4 : 8; }
 inline dim3 balanced_block(int64_t warps, int max_wpb) {
   if (warps < 1) warps = 1;
@@ -2658,8 +2655,8 @@ inline dim3 tgrid(int64_t x, int64_t t) {
   const int64_t y = t < 65535 ? t : 65535;
   return dim3((unsigned)x, (unsigned)y, (unsigned)((t + y - 1) / y));
 }
-inline dim3 pass_block(const LevelView& L, int v, int wpb = 0) {
-  return (v == 5 || v == 6) ? balanced_block((L.nn + 29) / 30, wpb > 0 ? wpb : wpb_for(L)) : march_block(L);
+inline dim3 pass_block(const LevelView& L, int v) {
+  return (v == 5 || v == 6) ? balanced_block((L.nn + 29) / 30, wpb_for(L)) : march_block(L);
 }
 inline dim3 grid_for(const LevelView& L, dim3 blk, int v) {
   if (v == 5 || v == 6) {
@@ -2679,9 +2676,9 @@ inline unsigned flat_grid(int64_t total) { return (unsigned)((total + kFlatBlock
 
 template <bool ADJ, int MODE, bool NORM, class Ld>
 void launch_pass(const LevelView& L, const Ld& ld, const double* f, double* y, double omega,
-                 double* partials, cudaStream_t s, int wpb = 0) {
+                 double* partials, cudaStream_t s) {
   const int v = eff_variant(L);
-  const dim3 blk = pass_block(L, v, wpb), grd = grid_for(L, blk, v);
+  const dim3 blk = pass_block(L, v), grd = grid_for(L, blk, v);
   switch (v) {
     case 1:
       pdl_launch(k_lean<ADJ, MODE, NORM, 4, 3, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
@@ -2730,8 +2727,7 @@ template <bool ADJ, int DIR>
 int sweep_prolong_impl(const LevelView& L, const LevelView& C, const double* f, const double* x,
                        const double* xc, double* y, double omega, cudaStream_t s) {
   const ProlongLoad<DIR> ld{x, xc, L.nn, C.nn};
-  launch_pass<ADJ, kSweep, false>(L, ld, f, y, omega, nullptr, s,
-                                  L.nn * (L.n_t + 1) >= g_prolong_wpb8_dofs ? 8 : 0);
+  launch_pass<ADJ, kSweep, false>(L, ld, f, y, omega, nullptr, s);
   return check_launch();
 }
 
@@ -2803,12 +2799,6 @@ int launch_sweep(bool adjoint, const LevelView& L, const double* f, const double
                  : sweep_impl<false>(L, f, x, y, omega, partials, s);
 }
 
-// Fused pairs with 16-level time tiles on 8-level-tile levels of >= g_pair16_dofs
-// DOFs (STMG_PAIR16_DOFS; off by default), 2 or 3 resident 256-thread blocks'
-// worth of registers (STMG_PAIR16_MINB).
-int64_t g_pair16_dofs = int64_t{1} << 62;
-int g_pair16_minb = 2;
-
 // Streaming pair (k_march2) on levels built with L.march (STMG_MARCH_DOFS).
 // Segments are sized so that the grid holds about g_march_waves x (148 SMs x
 // resident warps per SM) warps; queue depth and residency: STMG_MARCH_Q / _MINB.
@@ -2868,15 +2858,6 @@ int launch_sweep2(bool adjoint, const LevelView& L, const double* f, const doubl
     const dim3 grd = tgrid(tiles, (rows(L) + 3) / 4);
     if (adjoint) pdl_launch(k_lean2x2<true, 4>, grd, blk, 0, s, L, f, x, y, omega);
     else pdl_launch(k_lean2x2<false, 4>, grd, blk, 0, s, L, f, x, y, omega);
-  } else if (L.nn * (L.n_t + 1) >= g_pair16_dofs) {
-    const dim3 grd = tgrid(tiles, (rows(L) + 15) / 16);
-    if (g_pair16_minb >= 3) {
-      if (adjoint) pdl_launch(k_lean2x2<true, 16, 3>, grd, blk, 0, s, L, f, x, y, omega);
-      else pdl_launch(k_lean2x2<false, 16, 3>, grd, blk, 0, s, L, f, x, y, omega);
-    } else {
-      if (adjoint) pdl_launch(k_lean2x2<true, 16, 2>, grd, blk, 0, s, L, f, x, y, omega);
-      else pdl_launch(k_lean2x2<false, 16, 2>, grd, blk, 0, s, L, f, x, y, omega);
-    }
   } else {
     const dim3 grd = tgrid(tiles, (rows(L) + 7) / 8);
     if (adjoint) pdl_launch(k_lean2x2<true, 8>, grd, blk, 0, s, L, f, x, y, omega);
@@ -3077,9 +3058,6 @@ int kernels_init() {
     if (const char* v = std::getenv("STMG_KERNEL_VARIANT")) set_kernel_variant(std::atoi(v));
     if (const char* v = std::getenv("STMG_PDL")) g_pdl = std::atoi(v) != 0;
     if (const char* v = std::getenv("STMG_WPB4_DOFS")) g_wpb4_dofs = std::atoll(v);
-    if (const char* v = std::getenv("STMG_PAIR16_DOFS")) g_pair16_dofs = std::atoll(v);
-    if (const char* v = std::getenv("STMG_PAIR16_MINB")) g_pair16_minb = std::atoi(v);
-    if (const char* v = std::getenv("STMG_PROLONG_WPB8_DOFS")) g_prolong_wpb8_dofs = std::atoll(v);
     if (const char* v = std::getenv("STMG_MARCH_Q")) g_march_q = std::atoi(v);
     if (const char* v = std::getenv("STMG_MARCH_WAVES")) g_march_waves = std::atof(v);
     if (const char* v = std::getenv("STMG_MARCH_MINB")) g_march_minb = std::atoi(v);
