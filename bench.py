@@ -307,9 +307,14 @@ def reference_arm(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / max(args.steps, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE shapes)",
-        "config": {"workload": f"{cfg.name}-sample", "n_el": cfg.n_el, "n_t": sample_nt,
-                   "full_n_t": cfg.n_t, "nu": cfg.nu, "n_levels": cfg.n_levels,
-                   "min_elements": cfg.min_elements, "method": cfg.method},
+        # the same workload as the GPU arm; each step is a bounded sample of it
+        # (the time-truncated grid below), the metric is a rate
+        "config": {"workload": cfg.name, "n_el": cfg.n_el, "n_t": cfg.n_t,
+                   "dofs": (cfg.n_el + 1) * (cfg.n_t + 1), "method": cfg.method,
+                   "strategy": int(cfg.strategy), "n_levels": cfg.n_levels,
+                   "min_elements": cfg.min_elements, "nu": cfg.nu, "tol": cfg.tol,
+                   "parallelism": f"{cores} host cores, one single-threaded reference solve each",
+                   "adjoint": cfg.adjoint, "sample_n_t": sample_nt},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": info["kind"] if info else "port",
                          "sample": f"{cores} concurrent single-threaded solves of {cfg.name} truncated to "
                                    f"n_t={sample_nt} ({info['dofs'] if info else 0} DOFs, "

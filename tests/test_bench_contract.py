@@ -1,0 +1,50 @@
+"""bench.py's output contract: exactly one JSON line on stdout with the keys the
+driver reads, for the reference arm (CPU, a tiny time-truncated sample) and for
+the GPU arm (BASELINE config 1, one timed step)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+             "scaling", "vs_baseline", "dtype", "data", "config", "e2e", "cpu_baseline"}
+
+
+def run_bench(*args, timeout=600):
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], cwd=ROOT, capture_output=True,
+                       text=True, timeout=timeout)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [l for l in p.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1, p.stdout[-3000:]
+    return json.loads(lines[0])
+
+
+def test_reference_arm_contract():
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libstmg_ref.so")) and \
+            not os.path.exists(os.path.join(ROOT, "oracle", "liboracle_port.so")):
+        pytest.skip("oracle libraries not built (run __graft_entry__.build())")
+    d = run_bench("--impl", "reference", "--steps", "1", "--warmup", "1", "--cpu-sample-nt", "16",
+                  "--ref-cores", "2", timeout=300)
+    assert BASE_KEYS <= set(d)
+    assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
+    assert d["config"]["workload"] == "cfg1" and d["config"]["n_t"] == 4096 and d["config"]["sample_n_t"] == 16
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["cores"] == 2 and d["cpu_baseline"]["kind"] in ("reference", "port")
+
+
+@pytest.mark.gpu
+def test_gpu_arm_contract():
+    d = run_bench("--steps", "1", "--warmup", "3", "--no-cpu-baseline", "--hbm-roofline", "0",
+                  "--profile-steps", "1")
+    assert BASE_KEYS <= set(d) and "impl" not in d
+    assert d["config"]["workload"] == "cfg1" and d["dtype"] == "f64" and d["n_gpus"] == 1
+    assert d["cycles"] == 76 and d["status"] == "converged"  # the reference's count (tests/golden)
+    assert d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 16 * d["config"]["dofs"]
+    assert d["e2e"]["d2h_bytes_per_step"] == 8 * d["config"]["dofs"]
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.5
+    assert "sm_mhz" in d["clocks"]
