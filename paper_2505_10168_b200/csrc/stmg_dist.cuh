@@ -10,10 +10,10 @@
 // tail of the V-cycle as an ordinary single-GPU hierarchy and broadcasts the
 // correction back.
 //
-// Storage.  Every rank keeps full-size, globally indexed level vectors but only
-// reads/writes its slab rows plus one ghost level on each side, so HBM traffic
-// scales as 1/W while indexing and layout stay those of the single-GPU path
-// (capacity does not scale: cfg2's 52 GB fit in one B200).  Before every
+// Storage.  Every rank allocates only its slab rows plus kSlabMargin levels on
+// each side of every distributed level vector (SlabBuf), addressed through a
+// globally indexed base pointer, so both HBM traffic and capacity scale as 1/W
+// while indexing and layout stay those of the single-GPU path.  Before every
 // stencil pass the ghost levels of the input vector are exchanged with the
 // neighbours (J reads level n-1, J^T level n+1; both ghosts are exchanged), the
 // norms are all-reduced.  All operations are pointwise-identical to the
@@ -277,8 +277,30 @@ struct NcclComm : Comm {
 // ---------------------------------------------------------------------------
 // Distributed hierarchy
 // ---------------------------------------------------------------------------
+// Slab-local level vector: only rows [lo, hi) = the rank's slab plus kSlabMargin
+// levels on each side are allocated; `p` is the globally indexed base
+// (p + n * nn + i addresses level n), so the kernels and transports index
+// exactly as on a full-size vector.
+constexpr int64_t kSlabMargin = 4;  // >= the deepest ghost any slab kernel reads (2)
+struct SlabBuf {
+  std::unique_ptr<DeviceBuf> mem;
+  double* p = nullptr;
+  int64_t lo = 0, hi = 0, nn = 0;  // allocated rows [lo, hi), nn doubles per row
+  SlabBuf(int64_t n_lo, int64_t n_hi, int64_t n_t, int64_t nodes)
+      : lo(std::max<int64_t>(0, n_lo - kSlabMargin)), hi(std::min<int64_t>(n_t + 1, n_hi + kSlabMargin)),
+        nn(nodes) {
+    mem = std::make_unique<DeviceBuf>((hi - lo) * nn + kVecPad);
+    p = mem->p - lo * nn;
+    cuda_check(cudaMemset(mem->p, 0, sizeof(double) * static_cast<size_t>((hi - lo) * nn + kVecPad)),
+               "memset");
+  }
+  int64_t count() const { return (hi - lo) * nn; }
+  double* first() const { return p + lo * nn; }
+};
+
 struct RankState {
-  std::vector<std::unique_ptr<DeviceBuf>> f, xa, xb;  // levels [0, Lg): full-size vectors
+  // levels [0, Lg): slab-local, globally indexed (device memory per rank ~ 1/W of a level)
+  std::vector<std::unique_ptr<SlabBuf>> f, xa, xb;
   std::unique_ptr<DeviceBuf> fg, xg;                   // first gathered level: f rows out, x in
   std::unique_ptr<DeviceBuf> partials, scalars;
   std::vector<LevelView> views;  // levels [0, Lg) with this rank's slab row range
@@ -501,16 +523,13 @@ void dist_build(stmg_dist* d, int world, int rank, const void* nccl_id, int64_t 
     RankState& R = d->ranks[k];
     int64_t max_partials = sumsq_partials_needed(0);
     for (int l = 0; l < Lg; ++l) {
-      const int64_t nd = d->ndofs(l);
-      R.f.push_back(std::make_unique<DeviceBuf>(nd));
-      R.xa.push_back(std::make_unique<DeviceBuf>(nd));
-      R.xb.push_back(std::make_unique<DeviceBuf>(nd));
-      cuda_check(cudaMemset(R.xa.back()->p, 0, nd * 8), "memset");
-      cuda_check(cudaMemset(R.xb.back()->p, 0, nd * 8), "memset");
-      d->device_bytes += 3 * 8 * nd;
       LevelView v = d->full_views[l];
       v.n_lo = d->plan.bounds[l][g];
       v.n_hi = d->plan.bounds[l][g + 1];
+      R.f.push_back(std::make_unique<SlabBuf>(v.n_lo, v.n_hi, v.n_t, v.nn));
+      R.xa.push_back(std::make_unique<SlabBuf>(v.n_lo, v.n_hi, v.n_t, v.nn));
+      R.xb.push_back(std::make_unique<SlabBuf>(v.n_lo, v.n_hi, v.n_t, v.nn));
+      d->device_bytes += 3 * 8 * (R.f.back()->count() + kVecPad);
       R.views.push_back(v);
       max_partials = std::max(max_partials, sweep_partials_needed(v));
     }
@@ -584,14 +603,16 @@ void dist_solve(stmg_dist* d, const double* b, double* u, const stmg_solve_optio
     throw std::invalid_argument("mg_solve: history buffer smaller than max_cycles + 1");
   DeviceGuard dg(d->device);
   const auto t0 = std::chrono::steady_clock::now();
-  const int64_t n = d->ndofs(0), nn = d->nn(0);
-  const size_t bytes = sizeof(double) * static_cast<size_t>(n);
+  const int64_t nn = d->nn(0);
   const bool b_dev = is_device_ptr(b), u_dev = is_device_ptr(u);
   for (auto& R : d->ranks) {
-    cuda_check(cudaMemcpyAsync(R.f[0]->p, b, bytes, b_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                               d->stream), "b copy");
-    cuda_check(cudaMemcpyAsync(R.xa[0]->p, u, bytes, u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                               d->stream), "u copy");
+    // the allocated rows (slab + margins) of the global b and u
+    const SlabBuf& F = *R.f[0];
+    const size_t off = static_cast<size_t>(F.lo * nn), bytes = sizeof(double) * static_cast<size_t>(F.count());
+    cuda_check(cudaMemcpyAsync(F.first(), b + off, bytes,
+                               b_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, d->stream), "b copy");
+    cuda_check(cudaMemcpyAsync(R.xa[0]->first(), u + off, bytes,
+                               u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, d->stream), "u copy");
   }
   std::vector<double*> in, out;
   for (auto& R : d->ranks) {

@@ -79,3 +79,24 @@ def test_nccl_transport_world1_matches_single_domain(S, port):
     r2 = S.mg_solve_dist(dh, b, u2, opts)
     assert r2.cycles == r1.cycles
     assert np.array_equal(u1.view(np.uint64), u2.view(np.uint64))
+
+
+def test_slab_storage_scales_with_world(S):
+    """Each rank allocates only its slab (plus a few margin levels) of every
+    distributed level vector, so the loopback process, which hosts all ranks,
+    holds about one full-size copy whatever the world size (full-size rank
+    vectors would grow linearly with it)."""
+    n_el, n_t = 64, 2048
+    g = S.build_fine_grid(1.0, 1.0, n_el, n_t)
+    g.k, g.c = np.ones(n_el), np.ones(n_el)
+    X, T = S.CoarseningDirection.SpaceX, S.CoarseningDirection.TimeT
+    path = S.CoarseningPath([X, T, T, T])
+    sizes = {}
+    for world in (2, 8):
+        dh = S.build_dist_hierarchy(g, "CK", path, world, min_slab=8)
+        assert dh.n_distributed >= 1
+        sizes[world] = dh.device_bytes
+    vec_bytes = 8 * (n_el + 1) * (n_t + 1)
+    # full-size rank storage would grow by at least 6 ranks x 3 level-0 vectors;
+    # slab storage grows only by margins, padding and the small gathered level
+    assert sizes[8] - sizes[2] < 0.15 * 6 * 3 * vec_bytes, sizes
