@@ -308,7 +308,12 @@ int stmg_optimise(const stmg_grid* geom, const stmg_optimise_options* opts, int3
  * it); with nccl_id == NULL this process hosts all `world` ranks on `device`
  * and exchanges through device copies (loopback, for validation).
  * stmg_dist_mg_solve takes full-size b and u (host or device); u receives this
- * process's slab rows of the finest level (loopback: all rows). */
+ * process's slab rows of the finest level (loopback: all rows).
+ * With STMG_DIST_P2P=1 in the environment at create time the ghost levels are
+ * pulled straight from the neighbours' vectors over peer memory (CUDA IPC
+ * mappings across processes, local pointers in loopback) behind a
+ * neighbour-only epoch barrier instead of NCCL send/recv; stmg_dist_transport
+ * names the exchange in use ("nccl", "loopback", "p2p"). */
 typedef struct stmg_dist stmg_dist;
 int stmg_dist_partition(int32_t n_levels, const int64_t* n_t, const int32_t* dirs, int32_t world,
                         int64_t min_slab, int32_t* n_distributed, int64_t* bounds);
@@ -321,6 +326,7 @@ int stmg_dist_info(const stmg_dist* d, int32_t* n_distributed, int64_t* row_lo, 
                    int32_t* n_local, int64_t* device_bytes);
 int stmg_dist_mg_solve(stmg_dist* d, const double* b, double* u, const stmg_solve_options* opts,
                        stmg_solve_report* report, double* history, int32_t history_cap);
+int stmg_dist_transport(const stmg_dist* d, char* name_out, int32_t cap);
 void stmg_dist_destroy(stmg_dist* d);
 
 /* Benchmarking knob, not part of the reference-facing surface: stencil kernel

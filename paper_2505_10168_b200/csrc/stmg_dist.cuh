@@ -178,6 +178,7 @@ struct NcclApi {
   decltype(&ncclGroupEnd) GroupEnd = nullptr;
   decltype(&ncclAllReduce) AllReduce = nullptr;
   decltype(&ncclBroadcast) Broadcast = nullptr;
+  decltype(&ncclAllGather) AllGather = nullptr;
   decltype(&ncclGetErrorString) GetErrorString = nullptr;
 };
 
@@ -201,6 +202,7 @@ const NcclApi& nccl() {
     a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
     a.AllReduce = reinterpret_cast<decltype(a.AllReduce)>(sym("ncclAllReduce"));
     a.Broadcast = reinterpret_cast<decltype(a.Broadcast)>(sym("ncclBroadcast"));
+    a.AllGather = reinterpret_cast<decltype(a.AllGather)>(sym("ncclAllGather"));
     a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
     return a;
   }();
@@ -271,6 +273,141 @@ struct NcclComm : Comm {
                  cudaStream_t s) override {
     nccl_check(nccl().Broadcast(rank0 == 0 ? root : dst[0], dst[0], count, ncclDouble, 0, comm, s),
                "broadcast");
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Peer-memory ghost exchange (STMG_DIST_P2P=1): each rank PULLS its ghost levels
+// straight out of the neighbours' level vectors over NVLink (CUDA IPC
+// mappings; in loopback the neighbours' buffers are local), ordered by a
+// neighbour-only epoch barrier instead of NCCL send/recv:
+//   k_p2p_signal  (1 thread): epoch e = ++mine; fence.sys; store e into my
+//                 slot of each neighbour's flag word (release, system scope).
+//                 Stream order puts it after every kernel that wrote the
+//                 vector, so the rows a neighbour pulls are final.
+//   k_p2p_pull    every block waits (acquire) until both neighbours posted
+//                 epoch >= e, then copies depth levels from each of them.
+// A neighbour overwrites a pulled vector only after a LATER barrier, which
+// needs this rank's next signal, issued after its pull completed (ping-pong
+// buffers: a vector is rewritten two exchanges after it was pulled), so no
+// second handshake is needed.  All ranks issue the same exchange sequence; the
+// loopback host issues every rank's signal before any rank's pull, so its
+// waits are satisfied when they run.  A wait that exceeds 20 s traps instead
+// of hanging the device.  allreduce / gather / broadcast are delegated to the
+// wrapped transport (NCCL or loopback).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// flags: [0] own epoch, [1] posted by the left neighbour, [2] by the right one
+__global__ void k_p2p_signal(unsigned long long* mine, unsigned long long* left_slot,
+                             unsigned long long* right_slot) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long e = mine[0] + 1;
+  mine[0] = e;
+  __threadfence_system();
+  if (left_slot) st_release_sys(left_slot, e);
+  if (right_slot) st_release_sys(right_slot, e);
+}
+__global__ void __launch_bounds__(256) k_p2p_pull(const unsigned long long* mine, double* x,
+                                                  const double* __restrict__ left,
+                                                  const double* __restrict__ right, int64_t lo,
+                                                  int64_t hi, int64_t depth, int64_t nn) {
+  if (threadIdx.x == 0) {
+    const unsigned long long e = mine[0];
+    const unsigned long long t0 = globaltimer_ns();
+    for (int side = 1; side <= 2; ++side) {
+      if ((side == 1 ? left : right) == nullptr) continue;
+      while (ld_acquire_sys(mine + side) < e)
+        if (globaltimer_ns() - t0 > 20000000000ull) __trap();
+    }
+  }
+  __syncthreads();
+  const int64_t cnt = depth * nn;
+  // leading ghosts [lo - depth, lo) from the left rank, trailing [hi, hi + depth) from the right
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < 2 * cnt;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const bool lead = k < cnt;
+    const double* src = lead ? left : right;
+    if (src == nullptr) continue;
+    const int64_t off = (lead ? (lo - depth) * nn : hi * nn) + (lead ? k : k - cnt);
+    x[off] = __ldcv(src + off);
+  }
+}
+
+struct P2pComm : Comm {
+  std::unique_ptr<Comm> base;
+  struct Local {
+    double* flags = nullptr;                   // own flag words (3 x u64)
+    double* left_flags = nullptr;              // neighbours' flag words (peer-mapped or local)
+    double* right_flags = nullptr;
+    std::vector<double*> bufs, left, right;    // globally indexed bases: own / neighbours'
+  };
+  std::vector<Local> loc;
+  std::vector<std::unique_ptr<DeviceBuf>> flag_mem;
+  std::vector<void*> opened;  // IPC mappings to close
+  explicit P2pComm(std::unique_ptr<Comm> b) : base(std::move(b)) {
+    world = base->world;
+    n_local = base->n_local;
+    rank0 = base->rank0;
+    loc.resize(static_cast<size_t>(n_local));
+    for (int k = 0; k < n_local; ++k) {
+      flag_mem.push_back(std::make_unique<DeviceBuf>(3));
+      cuda_check(cudaMemset(flag_mem.back()->p, 0, 3 * sizeof(double)), "memset");
+      loc[k].flags = flag_mem.back()->p;
+    }
+  }
+  ~P2pComm() override {
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+  }
+  const char* name() const override { return "p2p"; }
+  void exchange(const std::vector<double*>& v, const std::vector<int64_t>& b, int64_t nn, int depth,
+                cudaStream_t s) override {
+    using u64 = unsigned long long;
+    for (int k = 0; k < n_local; ++k) {
+      const int g = rank0 + k;
+      Local& L = loc[k];
+      k_p2p_signal<<<1, 32, 0, s>>>(reinterpret_cast<u64*>(L.flags),
+                                    g > 0 ? reinterpret_cast<u64*>(L.left_flags) + 2 : nullptr,
+                                    g < world - 1 ? reinterpret_cast<u64*>(L.right_flags) + 1 : nullptr);
+      launch_check(static_cast<int>(cudaGetLastError()), "p2p signal");
+    }
+    for (int k = 0; k < n_local; ++k) {
+      const int g = rank0 + k;
+      Local& L = loc[k];
+      const auto it = std::find(L.bufs.begin(), L.bufs.end(), v[k]);
+      if (it == L.bufs.end()) throw std::runtime_error("p2p exchange: unregistered vector");
+      const size_t j = static_cast<size_t>(it - L.bufs.begin());
+      const int64_t cnt = 2 * nn * depth;
+      const unsigned grid = static_cast<unsigned>(std::min<int64_t>((cnt + 255) / 256, 148));
+      k_p2p_pull<<<grid, 256, 0, s>>>(reinterpret_cast<const u64*>(L.flags), v[k],
+                                      g > 0 ? L.left[j] : nullptr, g < world - 1 ? L.right[j] : nullptr,
+                                      b[g], b[g + 1], depth, nn);
+      launch_check(static_cast<int>(cudaGetLastError()), "p2p pull");
+    }
+  }
+  void allreduce_sum(const std::vector<double*>& in, const std::vector<double*>& out,
+                     cudaStream_t s) override {
+    base->allreduce_sum(in, out, s);
+  }
+  void gather_rows(const std::vector<double*>& src, double* dst,
+                   const std::vector<std::pair<int64_t, int64_t>>& rows, int64_t nn,
+                   cudaStream_t s) override {
+    base->gather_rows(src, dst, rows, nn, s);
+  }
+  void broadcast(const double* root, const std::vector<double*>& dst, int64_t count,
+                 cudaStream_t s) override {
+    base->broadcast(root, dst, count, s);
   }
 };
 
@@ -491,6 +628,74 @@ struct DistEmitter {
   }
 };
 
+// Switch the ghost exchange to peer-memory pulls (P2pComm): register every
+// distributed level vector of every local rank (f, xa, xb per level) and map the
+// neighbours' copies -- local pointers in loopback, CUDA IPC mappings of the
+// neighbour processes' allocations (handles all-gathered over NCCL) otherwise.
+void enable_p2p(stmg_dist* d) {
+  const int Lg = d->plan.Lg, W = d->plan.world;
+  auto pc = std::make_unique<P2pComm>(std::move(d->comm));
+  const int nl = pc->n_local;
+  auto slabs = [&](int k) {
+    std::vector<const SlabBuf*> v;
+    for (int l = 0; l < Lg; ++l) {
+      v.push_back(d->ranks[k].f[l].get());
+      v.push_back(d->ranks[k].xa[l].get());
+      v.push_back(d->ranks[k].xb[l].get());
+    }
+    return v;
+  };
+  for (int k = 0; k < nl; ++k)
+    for (const SlabBuf* sb : slabs(k)) pc->loc[k].bufs.push_back(sb->p);
+  if (nl == W) {  // loopback: every rank is local
+    for (int k = 0; k < nl; ++k) {
+      P2pComm::Local& L = pc->loc[k];
+      if (k > 0) {
+        L.left = pc->loc[k - 1].bufs;
+        L.left_flags = pc->loc[k - 1].flags;
+      }
+      if (k < W - 1) {
+        L.right = pc->loc[k + 1].bufs;
+        L.right_flags = pc->loc[k + 1].flags;
+      }
+    }
+  } else {
+    auto* nc = dynamic_cast<NcclComm*>(pc->base.get());
+    if (!nc || nl != 1) throw std::runtime_error("dist: p2p needs one NCCL rank per process");
+    const int g = pc->rank0;
+    const std::vector<const SlabBuf*> mine = slabs(0);
+    const size_t n = mine.size() + 1, hb = sizeof(cudaIpcMemHandle_t);
+    std::vector<cudaIpcMemHandle_t> hs(n), all(n * static_cast<size_t>(W));
+    for (size_t j = 0; j < mine.size(); ++j) cuda_check(cudaIpcGetMemHandle(&hs[j], mine[j]->mem->p), "ipc handle");
+    cuda_check(cudaIpcGetMemHandle(&hs[n - 1], pc->loc[0].flags), "ipc handle");
+    DeviceBuf send(static_cast<int64_t>((n * hb + 7) / 8)), recv(static_cast<int64_t>((n * hb * W + 7) / 8));
+    cuda_check(cudaMemcpy(send.p, hs.data(), n * hb, cudaMemcpyHostToDevice), "ipc handles h2d");
+    nccl_check(nccl().AllGather(send.p, recv.p, n * hb, ncclChar, nc->comm, d->stream), "allgather handles");
+    cuda_check(cudaStreamSynchronize(d->stream), "sync");
+    cuda_check(cudaMemcpy(all.data(), recv.p, n * hb * W, cudaMemcpyDeviceToHost), "ipc handles d2h");
+    P2pComm::Local& L = pc->loc[0];
+    for (int r : {g - 1, g + 1}) {
+      if (r < 0 || r >= W) continue;
+      std::vector<double*>& dst = r < g ? L.left : L.right;
+      for (size_t j = 0; j < n; ++j) {
+        void* ptr = nullptr;
+        cuda_check(cudaIpcOpenMemHandle(&ptr, all[static_cast<size_t>(r) * n + j], cudaIpcMemLazyEnablePeerAccess),
+                   "ipc open");
+        pc->opened.push_back(ptr);
+        if (j + 1 == n) {
+          (r < g ? L.left_flags : L.right_flags) = static_cast<double*>(ptr);
+          continue;
+        }
+        // globally indexed base of rank r's slab vector of level l = j / 3
+        const int l = static_cast<int>(j / 3);
+        const int64_t lo = std::max<int64_t>(0, d->plan.bounds[l][r] - kSlabMargin);
+        dst.push_back(static_cast<double*>(ptr) - lo * d->nn(l));
+      }
+    }
+  }
+  d->comm = std::move(pc);
+}
+
 void dist_build(stmg_dist* d, int world, int rank, const void* nccl_id, int64_t min_slab) {
   DeviceGuard dg(d->device);
   launch_check(kernels_init(), "kernels_init");
@@ -552,6 +757,7 @@ void dist_build(stmg_dist* d, int world, int rank, const void* nccl_id, int64_t 
   cuda_check(cudaStreamCreateWithFlags(&d->stream, cudaStreamDefault), "cudaStreamCreate");
   cuda_check(cudaStreamCreateWithFlags(&d->cap_stream, cudaStreamNonBlocking), "cudaStreamCreate");
   cuda_check(cudaMallocHost(&d->pinned, 8 * sizeof(double)), "cudaMallocHost");
+  if (const char* e = std::getenv("STMG_DIST_P2P"); e && std::atoi(e) != 0) enable_p2p(d);
   cuda_check(cudaDeviceSynchronize(), "sync");
 }
 

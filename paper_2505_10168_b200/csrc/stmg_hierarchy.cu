@@ -2311,6 +2311,13 @@ int stmg_dist_mg_solve(stmg_dist* d, const double* b, double* u, const stmg_solv
   });
 }
 
+int stmg_dist_transport(const stmg_dist* d, char* name_out, int32_t cap) {
+  return guarded([&] {
+    if (!d || !name_out || cap < 1) throw std::invalid_argument("null handle or buffer");
+    std::snprintf(name_out, static_cast<size_t>(cap), "%s", d->comm->name());
+  });
+}
+
 void stmg_dist_destroy(stmg_dist* d) { delete d; }
 
 int stmg_synchronize(stmg_hierarchy* h) {

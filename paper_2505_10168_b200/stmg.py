@@ -90,6 +90,7 @@ def _load():
         "stmg_dist_info": [vp, C.POINTER(i32), C.POINTER(i64), C.POINTER(i64), C.POINTER(i32),
                            C.POINTER(i64)],
         "stmg_dist_mg_solve": [vp, vp, vp, vp, vp, vp, i32],
+        "stmg_dist_transport": [vp, C.c_char_p, i32],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -486,6 +487,7 @@ class LevelHierarchy:
     def handle(self):
         return self._h
 
+
     def n_levels(self) -> int:
         return self._n_levels
 
@@ -783,6 +785,13 @@ class DistHierarchy:
     @property
     def handle(self):
         return self._h
+
+    @property
+    def transport(self) -> str:
+        """Ghost-exchange transport: "nccl", "loopback" or "p2p" (STMG_DIST_P2P=1)."""
+        buf = C.create_string_buffer(32)
+        _check(_lib.stmg_dist_transport(self._h, buf, 32))
+        return buf.value.decode()
 
 
 def build_dist_hierarchy(fine: SpaceTimeGrid, method, path: CoarseningPath, world: int, rank: int = 0,

@@ -100,3 +100,33 @@ def test_slab_storage_scales_with_world(S):
     # full-size rank storage would grow by at least 6 ranks x 3 level-0 vectors;
     # slab storage grows only by margins, padding and the small gathered level
     assert sizes[8] - sizes[2] < 0.15 * 6 * 3 * vec_bytes, sizes
+
+
+@pytest.mark.parametrize("name,world", [("cfg1_mini", 2), ("cfg1_mini_adj", 4), ("cfg4_mini", 8),
+                                        ("cfg0_deep", 2)])
+def test_p2p_transport_loopback_matches_single_domain(S, port, monkeypatch, name, world):
+    """Peer-memory ghost pulls behind the neighbour epoch barrier
+    (STMG_DIST_P2P=1), all ranks in this process: bitwise the single-domain
+    iterate, through graph replays and repeated solves (epochs keep counting)."""
+    cs = case(name)
+    g, path = grid_path(S, cs, port)
+    b = cs.rhs_vector(port)
+    opts = S.SolveOptions(nu=cs.nu, tol=cs.tol, max_cycles=cs.max_cycles)
+    h = S.build_hierarchy(g, cs.method, path, chi=cs.chi, mat=cs.mat)
+    if cs.adjoint:
+        h = S.transposed_hierarchy(h)
+    u1 = np.zeros_like(b)
+    r1 = S.mg_solve(h, b, u1, opts)
+    monkeypatch.setenv("STMG_DIST_P2P", "1")
+    dh = S.build_dist_hierarchy(g, cs.method, path, world, adjoint=cs.adjoint, chi=cs.chi, mat=cs.mat,
+                                min_slab=8)
+    assert dh.transport == "p2p"
+    for _ in range(2):
+        u2 = np.zeros_like(b)
+        r2 = S.mg_solve_dist(dh, b, u2, opts)
+        assert r2.cycles == r1.cycles and r2.status == r1.status
+        assert np.array_equal(u1.view(np.uint64), u2.view(np.uint64))
+        assert np.allclose(r2.history, r1.history, rtol=1e-12, atol=0)
+    monkeypatch.delenv("STMG_DIST_P2P")
+    assert S.build_dist_hierarchy(g, cs.method, path, world, adjoint=cs.adjoint, chi=cs.chi, mat=cs.mat,
+                                  min_slab=8).transport == "loopback"
