@@ -281,18 +281,21 @@ struct NcclComm : Comm {
 // straight out of the neighbours' level vectors over NVLink (CUDA IPC
 // mappings; in loopback the neighbours' buffers are local), ordered by a
 // neighbour-only epoch barrier instead of NCCL send/recv:
-//   k_p2p_signal  (1 thread): epoch e = ++mine; fence.sys; store e into my
-//                 slot of each neighbour's flag word (release, system scope).
-//                 Stream order puts it after every kernel that wrote the
-//                 vector, so the rows a neighbour pulls are final.
-//   k_p2p_pull    every block waits (acquire) until both neighbours posted
-//                 epoch >= e, then copies depth levels from each of them.
+//   exchange e = (own completed epoch) + 1.  One kernel per exchange,
+//   k_p2p_pull<POST = true>: block 0 first posts e into its slot of each
+//   neighbour's flag words (fence.sys + release store, system scope) -- stream
+//   order puts that after every kernel that wrote the vector, so the rows a
+//   neighbour pulls are final -- then every block waits (acquire) until both
+//   neighbours posted >= e and copies depth levels from each; the last block
+//   to finish records e as completed.
+//   Loopback (all ranks in this process, one stream) posts every rank's e
+//   with k_p2p_signal before any rank's k_p2p_pull<false>, so its waits are
+//   satisfied when they run; the wait, copy and epoch logic is the same kernel.
 // A neighbour overwrites a pulled vector only after a LATER barrier, which
-// needs this rank's next signal, issued after its pull completed (ping-pong
+// needs this rank's next post, issued after its pull completed (ping-pong
 // buffers: a vector is rewritten two exchanges after it was pulled), so no
-// second handshake is needed.  All ranks issue the same exchange sequence; the
-// loopback host issues every rank's signal before any rank's pull, so its
-// waits are satisfied when they run.  A wait that exceeds 20 s traps instead
+// second handshake is needed.  All ranks issue the same exchange sequence.
+// A world of one has no neighbours and no exchange.  A wait over 20 s traps instead
 // of hanging the device.  allreduce / gather / broadcast are delegated to the
 // wrapped transport (NCCL or loopback).
 // ---------------------------------------------------------------------------
@@ -309,22 +312,31 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// flags: [0] own epoch, [1] posted by the left neighbour, [2] by the right one
-__global__ void k_p2p_signal(unsigned long long* mine, unsigned long long* left_slot,
-                             unsigned long long* right_slot) {
-  if (threadIdx.x != 0) return;
+// flags: [0] own epoch (exchanges completed), [1] posted by the left neighbour,
+// [2] by the right one, [3] block ticket of the running pull kernel
+__device__ __forceinline__ void p2p_post(const unsigned long long* mine, unsigned long long* left_slot,
+                                         unsigned long long* right_slot) {
   const unsigned long long e = mine[0] + 1;
-  mine[0] = e;
   __threadfence_system();
   if (left_slot) st_release_sys(left_slot, e);
   if (right_slot) st_release_sys(right_slot, e);
 }
-__global__ void __launch_bounds__(256) k_p2p_pull(const unsigned long long* mine, double* x,
+// Loopback only: every local rank posts before any rank pulls.
+__global__ void k_p2p_signal(const unsigned long long* mine, unsigned long long* left_slot,
+                             unsigned long long* right_slot) {
+  if (threadIdx.x == 0) p2p_post(mine, left_slot, right_slot);
+}
+// Exchange e = mine[0] + 1: (post, if POST: one rank per process), wait for both
+// neighbours' posts, copy; the last block to finish records epoch e.
+template <bool POST>
+__global__ void __launch_bounds__(256) k_p2p_pull(unsigned long long* mine, unsigned long long* left_slot,
+                                                  unsigned long long* right_slot, double* x,
                                                   const double* __restrict__ left,
                                                   const double* __restrict__ right, int64_t lo,
                                                   int64_t hi, int64_t depth, int64_t nn) {
+  const unsigned long long e = mine[0] + 1;  // mine[0] changes only after every block is done
   if (threadIdx.x == 0) {
-    const unsigned long long e = mine[0];
+    if (POST && blockIdx.x == 0) p2p_post(mine, left_slot, right_slot);
     const unsigned long long t0 = globaltimer_ns();
     for (int side = 1; side <= 2; ++side) {
       if ((side == 1 ? left : right) == nullptr) continue;
@@ -343,12 +355,19 @@ __global__ void __launch_bounds__(256) k_p2p_pull(const unsigned long long* mine
     const int64_t off = (lead ? (lo - depth) * nn : hi * nn) + (lead ? k : k - cnt);
     x[off] = __ldcv(src + off);
   }
+  if (threadIdx.x == 0) {
+    // every block has read e (it did so before its ticket), so the last one may advance the epoch
+    if (atomicAdd(mine + 3, 1ull) == gridDim.x - 1) {
+      mine[3] = 0;
+      mine[0] = e;
+    }
+  }
 }
 
 struct P2pComm : Comm {
   std::unique_ptr<Comm> base;
   struct Local {
-    double* flags = nullptr;                   // own flag words (3 x u64)
+    double* flags = nullptr;                   // own flag words (4 x u64)
     double* left_flags = nullptr;              // neighbours' flag words (peer-mapped or local)
     double* right_flags = nullptr;
     std::vector<double*> bufs, left, right;    // globally indexed bases: own / neighbours'
@@ -362,8 +381,8 @@ struct P2pComm : Comm {
     rank0 = base->rank0;
     loc.resize(static_cast<size_t>(n_local));
     for (int k = 0; k < n_local; ++k) {
-      flag_mem.push_back(std::make_unique<DeviceBuf>(3));
-      cuda_check(cudaMemset(flag_mem.back()->p, 0, 3 * sizeof(double)), "memset");
+      flag_mem.push_back(std::make_unique<DeviceBuf>(4));
+      cuda_check(cudaMemset(flag_mem.back()->p, 0, 4 * sizeof(double)), "memset");
       loc[k].flags = flag_mem.back()->p;
     }
   }
@@ -374,13 +393,20 @@ struct P2pComm : Comm {
   void exchange(const std::vector<double*>& v, const std::vector<int64_t>& b, int64_t nn, int depth,
                 cudaStream_t s) override {
     using u64 = unsigned long long;
-    for (int k = 0; k < n_local; ++k) {
+    if (world == 1) return;  // no neighbours
+    auto slots = [&](int k, u64** ls, u64** rs) {
       const int g = rank0 + k;
-      Local& L = loc[k];
-      k_p2p_signal<<<1, 32, 0, s>>>(reinterpret_cast<u64*>(L.flags),
-                                    g > 0 ? reinterpret_cast<u64*>(L.left_flags) + 2 : nullptr,
-                                    g < world - 1 ? reinterpret_cast<u64*>(L.right_flags) + 1 : nullptr);
-      launch_check(static_cast<int>(cudaGetLastError()), "p2p signal");
+      *ls = g > 0 ? reinterpret_cast<u64*>(loc[k].left_flags) + 2 : nullptr;
+      *rs = g < world - 1 ? reinterpret_cast<u64*>(loc[k].right_flags) + 1 : nullptr;
+    };
+    const bool loopback = n_local > 1;
+    if (loopback) {
+      for (int k = 0; k < n_local; ++k) {
+        u64 *ls, *rs;
+        slots(k, &ls, &rs);
+        k_p2p_signal<<<1, 32, 0, s>>>(reinterpret_cast<const u64*>(loc[k].flags), ls, rs);
+        launch_check(static_cast<int>(cudaGetLastError()), "p2p signal");
+      }
     }
     for (int k = 0; k < n_local; ++k) {
       const int g = rank0 + k;
@@ -390,9 +416,15 @@ struct P2pComm : Comm {
       const size_t j = static_cast<size_t>(it - L.bufs.begin());
       const int64_t cnt = 2 * nn * depth;
       const unsigned grid = static_cast<unsigned>(std::min<int64_t>((cnt + 255) / 256, 148));
-      k_p2p_pull<<<grid, 256, 0, s>>>(reinterpret_cast<const u64*>(L.flags), v[k],
-                                      g > 0 ? L.left[j] : nullptr, g < world - 1 ? L.right[j] : nullptr,
-                                      b[g], b[g + 1], depth, nn);
+      u64 *ls, *rs;
+      slots(k, &ls, &rs);
+      const double* lp = g > 0 ? L.left[j] : nullptr;
+      const double* rp = g < world - 1 ? L.right[j] : nullptr;
+      u64* mine = reinterpret_cast<u64*>(L.flags);
+      if (loopback)
+        k_p2p_pull<false><<<grid, 256, 0, s>>>(mine, ls, rs, v[k], lp, rp, b[g], b[g + 1], depth, nn);
+      else
+        k_p2p_pull<true><<<grid, 256, 0, s>>>(mine, ls, rs, v[k], lp, rp, b[g], b[g + 1], depth, nn);
       launch_check(static_cast<int>(cudaGetLastError()), "p2p pull");
     }
   }
