@@ -679,7 +679,8 @@ void enable_p2p(stmg_dist* d) {
   };
   for (int k = 0; k < nl; ++k)
     for (const SlabBuf* sb : slabs(k)) pc->loc[k].bufs.push_back(sb->p);
-  if (nl == W) {  // loopback: every rank is local
+  auto* nc = dynamic_cast<NcclComm*>(pc->base.get());
+  if (!nc) {  // loopback: every rank is local
     for (int k = 0; k < nl; ++k) {
       P2pComm::Local& L = pc->loc[k];
       if (k > 0) {
@@ -692,8 +693,7 @@ void enable_p2p(stmg_dist* d) {
       }
     }
   } else {
-    auto* nc = dynamic_cast<NcclComm*>(pc->base.get());
-    if (!nc || nl != 1) throw std::runtime_error("dist: p2p needs one NCCL rank per process");
+    // one NCCL rank per process (a world of one still gathers its handles)
     const int g = pc->rank0;
     const std::vector<const SlabBuf*> mine = slabs(0);
     const size_t n = mine.size() + 1, hb = sizeof(cudaIpcMemHandle_t);

@@ -130,3 +130,23 @@ def test_p2p_transport_loopback_matches_single_domain(S, port, monkeypatch, name
     monkeypatch.delenv("STMG_DIST_P2P")
     assert S.build_dist_hierarchy(g, cs.method, path, world, adjoint=cs.adjoint, chi=cs.chi, mat=cs.mat,
                                   min_slab=8).transport == "loopback"
+
+
+def test_p2p_over_nccl_world1_gathers_handles_and_matches(S, port, monkeypatch):
+    """STMG_DIST_P2P=1 on a real NCCL communicator: the CUDA IPC handles of
+    every slab vector are all-gathered over NCCL (no neighbour to map in a
+    world of one), and the solve equals the single-domain one bitwise."""
+    cs = case("cfg1_mini")
+    g, path = grid_path(S, cs, port)
+    b = cs.rhs_vector(port)
+    opts = S.SolveOptions(nu=cs.nu, tol=cs.tol, max_cycles=cs.max_cycles)
+    h = S.build_hierarchy(g, cs.method, path)
+    u1 = np.zeros_like(b)
+    r1 = S.mg_solve(h, b, u1, opts)
+    monkeypatch.setenv("STMG_DIST_P2P", "1")
+    dh = S.build_dist_hierarchy(g, cs.method, path, 1, rank=0, nccl_id=S.nccl_unique_id(), min_slab=8)
+    assert dh.transport == "p2p"
+    u2 = np.zeros_like(b)
+    r2 = S.mg_solve_dist(dh, b, u2, opts)
+    assert r2.cycles == r1.cycles
+    assert np.array_equal(u1.view(np.uint64), u2.view(np.uint64))
