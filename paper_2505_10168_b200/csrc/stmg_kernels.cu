@@ -519,7 +519,10 @@ __global__ void __launch_bounds__(kMaxTW, MINB) k_lean2(LevelView L, Ld ld,
 // store sweep 2 (28 nodes per warp).  Sweep 1 is also evaluated on the one
 // staged row before the tile (J) / after it (J^T) that sweep 2 couples to.
 // Staged: x on NT + 2 levels, f on NT + 1 levels.  Grid as k_lean2.
-template <bool ADJ, int NT>
+// W2: omega is an exact power of two (the reference's 1/2), so
+// omega * (r * invd) == r * (omega * invd) bit for bit (scaling by 2^k commutes
+// with rounding for normal results) and the interior rows save one DMUL each.
+template <bool ADJ, int NT, bool W2 = false>
 __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __restrict__ f,
                                             const double* __restrict__ x, double* __restrict__ y,
                                             double omega, int64_t tile, int64_t ttile) {
@@ -556,13 +559,17 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
 #pragma unroll
     for (int r = 0; r < NT + 1; ++r) fv[r] = __ldg(fb + o[ADJ ? r : r + 1]);  // f rows s1base + r
     const Coefs c = load_coefs(L, i);
+    const double sc = c.invd * omega;  // used only when W2
+    auto upd = [&](double x0, double fval, double row) {
+      return W2 ? x0 + (fval - row) * sc : x0 + omega * ((fval - row) * c.invd);
+    };
     double pm = __shfl_up_sync(kFull, xs[0], 1), pp = __shfl_down_sync(kFull, xs[0], 1);
 #pragma unroll
     for (int r = 0; r <= NT; ++r) {
       const double x1 = xs[r + 1];
       const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
-      if (ADJ) y1[r] = xs[r] + omega * ((fv[r] - row_interior<true>(c, pm, xs[r], pp, qm, x1, qp)) * c.invd);
-      else y1[r] = x1 + omega * ((fv[r] - row_interior<false>(c, qm, x1, qp, pm, xs[r], pp)) * c.invd);
+      if (ADJ) y1[r] = upd(xs[r], fv[r], row_interior<true>(c, pm, xs[r], pp, qm, x1, qp));
+      else y1[r] = upd(x1, fv[r], row_interior<false>(c, qm, x1, qp, pm, xs[r], pp));
       pm = qm;
       pp = qp;
     }
@@ -574,9 +581,8 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
       const double bm = __shfl_up_sync(kFull, z1, 1), bp = __shfl_down_sync(kFull, z1, 1);
       // evaluated on every lane (no divergence around the shuffles); stored on
       // lanes 2..29; row n0 + k is staged row k (J^T) / k + 2 (J)
-      const double v =
-          ADJ ? y1[k] + omega * ((fv[k] - row_interior<true>(c, am, y1[k], ap, bm, z1, bp)) * c.invd)
-              : z1 + omega * ((fv[k + 1] - row_interior<false>(c, bm, z1, bp, am, y1[k], ap)) * c.invd);
+      const double v = ADJ ? upd(y1[k], fv[k], row_interior<true>(c, am, y1[k], ap, bm, z1, bp))
+                           : upd(z1, fv[k + 1], row_interior<false>(c, bm, z1, bp, am, y1[k], ap));
       if (lane2) st_global(yb + o[ADJ ? k : k + 2], v);
       am = bm;
       ap = bp;
@@ -669,13 +675,13 @@ constexpr int64_t kMinB5Dofs = 200000;
 template <int NT>
 constexpr int minb_for_nt() { return NT <= 2 ? 5 : NT <= 4 ? 4 : 3; }
 
-template <bool ADJ, int NT, int MINB = minb_for_nt<NT>()>
+template <bool ADJ, int NT, int MINB = minb_for_nt<NT>(), bool W2 = false>
 __global__ void __launch_bounds__(kMaxTW, MINB) k_lean2x2(LevelView L, const double* __restrict__ f,
                                                        const double* __restrict__ x,
                                                        double* __restrict__ y, double omega) {
   pdl_entry();
   const int64_t tt = (int64_t)blockIdx.z * gridDim.y + blockIdx.y;  // time tile
-  if (tt < ceil_div(L.n_hi - L.n_lo, NT)) dev_lean2x2<ADJ, NT>(L, f, x, y, omega, blockIdx.x, tt);
+  if (tt < ceil_div(L.n_hi - L.n_lo, NT)) dev_lean2x2<ADJ, NT, W2>(L, f, x, y, omega, blockIdx.x, tt);
 }
 
 // D damped-Jacobi sweeps fused into one pass (temporal blocking of depth D,
@@ -2839,29 +2845,42 @@ int launch_sweep2_march(bool adjoint, const LevelView& L, const double* f, const
   return check_launch();
 }
 
+// Power-of-two omega fast path of the fused pair (STMG_OMEGA_POW2=0 disables it
+// for A/B measurements; read by kernels_init).
+bool g_omega_pow2 = true;
+inline bool omega_is_pow2(double w) {
+  int e = 0;
+  return w > 0.0 && std::isfinite(w) && std::frexp(w, &e) == 0.5;
+}
+
 int launch_sweep2(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
                   double omega, cudaStream_t s) {
   if (L.march) return launch_sweep2_march(adjoint, L, f, x, y, omega, s);
   const int64_t warps = ceil_div(L.nn, 28);
   const dim3 blk = balanced_block(warps, wpb_for(L));
   const int64_t tiles = ceil_div(warps, blk.x / 32);
+  const bool w2 = g_omega_pow2 && omega_is_pow2(omega);
+  auto go = [&](auto kern_w2, auto kern, dim3 grd) {
+    if (w2) pdl_launch(kern_w2, grd, blk, 0, s, L, f, x, y, omega);
+    else pdl_launch(kern, grd, blk, 0, s, L, f, x, y, omega);
+  };
   if (lean_nt(L) == 2) {
     const dim3 grd = tgrid(tiles, (rows(L) + 1) / 2);
     if (L.nn * (L.n_t + 1) >= kMinB5Dofs) {
-      if (adjoint) pdl_launch(k_lean2x2<true, 2>, grd, blk, 0, s, L, f, x, y, omega);
-      else pdl_launch(k_lean2x2<false, 2>, grd, blk, 0, s, L, f, x, y, omega);
+      if (adjoint) go(k_lean2x2<true, 2, minb_for_nt<2>(), true>, k_lean2x2<true, 2>, grd);
+      else go(k_lean2x2<false, 2, minb_for_nt<2>(), true>, k_lean2x2<false, 2>, grd);
     } else {
-      if (adjoint) pdl_launch(k_lean2x2<true, 2, 3>, grd, blk, 0, s, L, f, x, y, omega);
-      else pdl_launch(k_lean2x2<false, 2, 3>, grd, blk, 0, s, L, f, x, y, omega);
+      if (adjoint) go(k_lean2x2<true, 2, 3, true>, k_lean2x2<true, 2, 3>, grd);
+      else go(k_lean2x2<false, 2, 3, true>, k_lean2x2<false, 2, 3>, grd);
     }
   } else if (lean_nt(L) == 4) {
     const dim3 grd = tgrid(tiles, (rows(L) + 3) / 4);
-    if (adjoint) pdl_launch(k_lean2x2<true, 4>, grd, blk, 0, s, L, f, x, y, omega);
-    else pdl_launch(k_lean2x2<false, 4>, grd, blk, 0, s, L, f, x, y, omega);
+    if (adjoint) go(k_lean2x2<true, 4, minb_for_nt<4>(), true>, k_lean2x2<true, 4>, grd);
+    else go(k_lean2x2<false, 4, minb_for_nt<4>(), true>, k_lean2x2<false, 4>, grd);
   } else {
     const dim3 grd = tgrid(tiles, (rows(L) + 7) / 8);
-    if (adjoint) pdl_launch(k_lean2x2<true, 8>, grd, blk, 0, s, L, f, x, y, omega);
-    else pdl_launch(k_lean2x2<false, 8>, grd, blk, 0, s, L, f, x, y, omega);
+    if (adjoint) go(k_lean2x2<true, 8, minb_for_nt<8>(), true>, k_lean2x2<true, 8>, grd);
+    else go(k_lean2x2<false, 8, minb_for_nt<8>(), true>, k_lean2x2<false, 8>, grd);
   }
   return check_launch();
 }
@@ -3057,6 +3076,7 @@ int kernels_init() {
     env_read = true;
     if (const char* v = std::getenv("STMG_KERNEL_VARIANT")) set_kernel_variant(std::atoi(v));
     if (const char* v = std::getenv("STMG_PDL")) g_pdl = std::atoi(v) != 0;
+    if (const char* v = std::getenv("STMG_OMEGA_POW2")) g_omega_pow2 = std::atoi(v) != 0;
     if (const char* v = std::getenv("STMG_WPB4_DOFS")) g_wpb4_dofs = std::atoll(v);
     if (const char* v = std::getenv("STMG_MARCH_Q")) g_march_q = std::atoi(v);
     if (const char* v = std::getenv("STMG_MARCH_WAVES")) g_march_waves = std::atof(v);

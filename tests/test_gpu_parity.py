@@ -378,3 +378,23 @@ def test_solve_with_deep_smoothing(torch, S, port, monkeypatch, name, depth):
     r1 = S.mg_solve(gpu_hier(S, cs, port), b, u1, opts)
     assert r1.cycles == r0.cycles and r1.history == r0.history
     assert np.array_equal(bits(u1), bits(u0))
+
+
+@pytest.mark.parametrize("omega", [0.5, 0.25, 1.0, 0.6, 2.0 / 3.0])
+@pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj"])
+def test_pair_kernel_omega_forms_bitwise(torch, S, port, name, omega):
+    """Fused pairs for power-of-two omega (one product r * (omega * invd)) and
+    for any other omega (omega * (r * invd)), against the oracle's sweeps."""
+    cs = case(name)
+    h = gpu_hier(S, cs, port)
+    hp = port_hier(port, cs)
+    rng = np.random.default_rng(11)
+    for l in range(h.n_levels() - 1):
+        n = hp.ndofs(l)
+        x, f = special_values(rng, n), special_values(rng, n)
+        want = hp.sweeps(l, f, x, 4, omega)
+        xt, ft = torch.from_numpy(x).cuda(), torch.from_numpy(f).cuda()
+        yt = torch.empty_like(xt)
+        h.sweep_kernels(l, ft, xt, yt, 2, True, omega)
+        torch.cuda.synchronize()
+        assert np.array_equal(bits(xt), bits(want)), (l, omega)
