@@ -513,11 +513,11 @@ def main():
         avg = secs / cnt
         achieved = 24.0 * n0 / avg / 1e9
         # DRAM bytes per launch of the same kernel at this size from the committed
-        # `ncu --set full` capture (profiles/round1.md, session 3: k_lean2x2<0,4,4>,
-        # grid (10, 1025) x 128 threads): 67.295 MB read + 8.322 MB written; ncu
+        # `ncu --set full` capture (profiles/round1.md, session 4: k_lean2x2<0,4,4,1>,
+        # grid (10, 1025) x 128 threads): 67.297 MB read + 8.578 MB written; ncu
         # replays cold-cache, so this is the L2-miss traffic of an isolated launch,
         # an upper bound for the in-solve one
-        traffic = (67.295232e6 + 8.322048e6) if (use_pair and n0 == 1025 * 4097) else None
+        traffic = (67.296768e6 + 8.578304e6) if (use_pair and n0 == 1025 * 4097) else None
         roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                     "frac": achieved / hbm, "traffic": traffic,
                     "traffic_source": ("ncu --set full, profiles/round1.md (cold-cache replay)"
