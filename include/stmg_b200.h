@@ -235,12 +235,9 @@ int stmg_mg_solve_batch(int32_t count, stmg_hierarchy* const* hs, const double* 
 int stmg_level_sweeps(stmg_hierarchy* h, int32_t level, const double* f, double* x,
                       int32_t sweeps, double omega);
 /* Benchmark form: `launches` back-to-back kernel launches ping-ponging between
- * x and y (x -> y -> x ...), each a single sweep (fused_pairs = 0), a fused
- * two-sweep pass (fused_pairs = 1), a fused 3- or 4-sweep pass (fused_pairs =
- * 3, 4) or the fused pair through the bulk-copy pipelined kernel (fused_pairs =
- * 5; f, x and y then need 512 doubles of tail padding); asynchronous on the
- * hierarchy's stream, no copies.  The iterate ends in x after an even number of
- * launches. */
+ * x and y (x -> y -> x ...), each a single sweep (fused_pairs = 0) or a fused
+ * two-sweep pass (fused_pairs = 1); asynchronous on the hierarchy's stream, no
+ * copies.  The iterate ends in x after an even number of launches. */
 int stmg_level_sweep_kernels(stmg_hierarchy* h, int32_t level, const double* f, double* x, double* y,
                              int32_t launches, int32_t fused_pairs, double omega);
 /* r = f - J_l x  (csr_residual) */
@@ -329,10 +326,12 @@ int stmg_dist_mg_solve(stmg_dist* d, const double* b, double* u, const stmg_solv
 int stmg_dist_transport(const stmg_dist* d, char* name_out, int32_t cap);
 void stmg_dist_destroy(stmg_dist* d);
 
-/* Benchmarking knob, not part of the reference-facing surface: stencil kernel
- * design (5 = production default; see csrc/stmg_kernels.cu for the list).  The
- * environment variable STMG_KERNEL_VARIANT sets it at load time. */
-int stmg_debug_set_kernel_variant(int32_t variant);
+/* Per-handle tiling of the stencil kernels (A/B measurements, tests of every
+ * tile depth; not part of the reference-facing surface): levels with at most
+ * tiny_dofs DOFs use 2-level time tiles, at most small_dofs 4-level tiles, the
+ * rest 8-level tiles.  Values <= 0 restore the defaults (5,000,000 / 600,000).
+ * Captured V-cycle graphs of the handle are rebuilt on the next solve. */
+int stmg_hierarchy_set_tiling(stmg_hierarchy* h, int64_t small_dofs, int64_t tiny_dofs);
 
 #ifdef __cplusplus
 }

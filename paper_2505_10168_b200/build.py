@@ -46,14 +46,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     objs = []
     log = []
-    for src in SOURCES:
+    procs = []
+    for src in SOURCES:  # the translation units compile in parallel
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
         cmd = [nvcc(), *NVCC_FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        log.append(r.stdout + r.stderr)
-        if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+        procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
         objs.append(obj)
+    for src, p in procs:
+        out, err = p.communicate()
+        log.append(out + err)
+        if p.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{out}\n{err}")
     tmp = OUT + ".tmp"
     cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", tmp,
            "-lcudart_static", "-lpthread", "-ldl", "-lrt"]  # NCCL is dlopen'ed at run time

@@ -406,8 +406,7 @@ enum TimedKind {
   kTimedSweep2 = 3,
   kTimedFromZero = 4,
   kTimedCoarsest = 5,
-  kTimedTail = 6,
-  kTimedKinds = 7
+  kTimedKinds = 6
 };
 
 struct TimedKernel {
@@ -459,8 +458,6 @@ struct stmg_hierarchy {
   cudaStream_t own_stream = nullptr;  // created with the hierarchy
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture
   int profiling = 0;  // 0 off, 1 finest-level kernels, 2 every kernel
-  int tail_start = -1;   // first level run by the coarse-tail cluster kernel (-1: none)
-  int tail_cluster = 0;   // 0: grid-wide cooperative tail; 1..16: one cluster
   // per (level, kind): launches and device seconds accumulated while profiling
   std::vector<std::array<std::pair<int64_t, double>, stmgb::kTimedKinds>> prof;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -530,10 +527,8 @@ struct DeviceGuard {
 // sqrt(1.5 n_t) (balancing 2 Lc PCR steps against n_t / Lc dense links), and
 // the chunk propagator A^Lc, A = -T^-1 S (column-major m x m), built on the
 // device by m parallel homogeneous marches with the march's own PCR step.
-// STMG_COARSEST_PINT=0 keeps the sequential march.  Needs the PCR tables.
+// Needs the PCR tables.
 void build_pint(stmg_hierarchy* h) {
-  if (const char* v = std::getenv("STMG_COARSEST_PINT"))
-    if (std::atoi(v) == 0) return;
   const int m = h->coarsest.m;
   const int64_t nt = h->host.back().g.n_t;
   if (m <= 32 || m > 2048 || nt < 64) return;
@@ -716,25 +711,14 @@ void sync_unless_capturing(cudaStream_t s) {
 }
 
 // Levels with at most this many DOFs use 4-level time tiles in the stencil
-// kernels (shorter serial chains where a launch is latency-bound).
-// STMG_SMALL_NT_DOFS overrides; read when a hierarchy is built.
+// kernels (shorter serial chains where a launch is latency-bound).  Fixed when
+// a hierarchy is built; a handle's tile thresholds can be changed with
+// stmg_hierarchy_set_tiling (A/B measurements, tests of every tile depth).
 constexpr int64_t kSmallNtDofs = 5000000;  // measured: cfg1 solve 66.2 -> 57.7 ms (2.5M); 49.82 -> 49.68 ms (5M, A/B)
-// Levels with at most kTinyNtDofs DOFs use 2-level tiles (STMG_TINY_NT_DOFS).
+// Levels with at most kTinyNtDofs DOFs use 2-level tiles.
 constexpr int64_t kTinyNtDofs = 600000;  // measured: cfg1 solve 53.3 -> 50.8 ms (1.1M); 41.34 -> 41.09 ms (600K, A/B)
-int64_t tile_nt_for(int64_t dofs) {
-  int64_t lim = kSmallNtDofs, tiny = kTinyNtDofs;
-  if (const char* v = std::getenv("STMG_SMALL_NT_DOFS")) lim = std::atoll(v);
-  if (const char* v = std::getenv("STMG_TINY_NT_DOFS")) tiny = std::atoll(v);
-  return dofs <= tiny ? 2 : dofs <= lim ? 4 : 8;
-}
-// Levels with at most this many DOFs smooth with depth-STMG_DEEP_DEPTH fused
-// kernels (one launch for 3 or 4 sweeps); STMG_DEEP_DOFS / STMG_DEEP_DEPTH override.
-constexpr int64_t kDeepDofs = 0;
-int64_t sweep_depth_for(int64_t dofs) {
-  int64_t lim = kDeepDofs, depth = 4;
-  if (const char* v = std::getenv("STMG_DEEP_DOFS")) lim = std::atoll(v);
-  if (const char* v = std::getenv("STMG_DEEP_DEPTH")) depth = std::atoll(v);
-  return (dofs <= lim && (depth == 3 || depth == 4)) ? depth : 2;
+int64_t tile_nt_for(int64_t dofs, int64_t small = kSmallNtDofs, int64_t tiny = kTinyNtDofs) {
+  return dofs <= tiny ? 2 : dofs <= small ? 4 : 8;
 }
 
 // Device tables of the general coarse discretisations: Galerkin levels' 9-point
@@ -793,31 +777,11 @@ void upload_general(stmg_hierarchy* h) {
   }
 }
 
-// Levels with at least this many DOFs run their fused pairs through the
-// bulk-copy pipelined kernel (k_bulk); STMG_BULK_DOFS overrides (0 = never).
-constexpr int64_t kBulkDofs = 0;
-int64_t bulk_for(int64_t dofs) {
-  int64_t lim = kBulkDofs;
-  if (const char* v = std::getenv("STMG_BULK_DOFS")) lim = std::atoll(v);
-  return lim > 0 && dofs >= lim ? 1 : 0;
-}
-
-// Levels with at least this many DOFs run their fused pairs through the
-// streaming march (k_march2); STMG_MARCH_DOFS overrides (0 = never).  Measured
-// slower than k_lean2x2 on every BASELINE config 1 level (profiles/round1.md).
-constexpr int64_t kMarchDofs = 0;
-int64_t march_for(int64_t dofs) {
-  int64_t lim = kMarchDofs;
-  if (const char* v = std::getenv("STMG_MARCH_DOFS")) lim = std::atoll(v);
-  return lim > 0 && dofs >= lim ? 1 : 0;
-}
-
 void upload_levels(stmg_hierarchy* h) {
   h->coef.clear();
   h->views.clear();
   for (const HostLevel& hl : h->host) {
     const std::vector<double> t = hl.table(h->adjoint);
-    // tail padding: the bulk-copy kernels copy coefficient rows rounded out to 16 bytes
     auto buf = std::make_unique<DeviceBuf>(static_cast<int64_t>(t.size()) + kVecPad);
     cuda_check(cudaMemcpy(buf->p, t.data(), t.size() * 8, cudaMemcpyHostToDevice), "coef upload");
     LevelView v;
@@ -830,9 +794,6 @@ void upload_levels(stmg_hierarchy* h) {
     v.n_lo = 0;
     v.n_hi = hl.g.n_t + 1;
     v.tile_nt = tile_nt_for(v.nn * (v.n_t + 1));
-    v.sweep_depth = sweep_depth_for(v.nn * (v.n_t + 1));
-    v.bulk = bulk_for(v.nn * (v.n_t + 1));
-    v.march = march_for(v.nn * (v.n_t + 1));
     h->views.push_back(v);
     h->device_bytes += static_cast<int64_t>((t.size() + kVecPad) * 8);
     h->coef.push_back(std::move(buf));
@@ -847,13 +808,14 @@ std::shared_ptr<Workspace> make_workspace(const stmg_hierarchy* h, int64_t* byte
   int64_t max_partials = sumsq_partials_needed(0);
   for (int l = 0; l < nl; ++l) {
     const int64_t nd = h->ndofs(l);
-    // kVecPad doubles of tail padding: the bulk-copy kernels round row copies out to 16 bytes
     ws->f.push_back(std::make_unique<DeviceBuf>(nd + kVecPad));
     ws->xa.push_back(std::make_unique<DeviceBuf>(nd + kVecPad));
     // the coarsest level never ping-pongs unless it is also level 0
     ws->xb.push_back(std::make_unique<DeviceBuf>(l < nl - 1 || nl == 1 ? nd + kVecPad : 0));
     *bytes += 8 * (3 * (nd + kVecPad));
-    max_partials = std::max(max_partials, sweep_partials_needed(h->views[l]));
+    LevelView finest_tiles = h->views[l];  // the most partials any tiling can need
+    finest_tiles.tile_nt = 2;
+    max_partials = std::max(max_partials, sweep_partials_needed(finest_tiles));
   }
   ws->partials = std::make_unique<DeviceBuf>(max_partials);
   ws->scalars = std::make_unique<DeviceBuf>(8);
@@ -874,31 +836,10 @@ void finish_create(stmg_hierarchy* h, bool share_ws_from_other, const stmg_hiera
   DeviceGuard dg(h->device);
   launch_check(kernels_init(), "kernels_init");
   upload_levels(h);
-  {
-    // Off by default: measured slower on BASELINE config 1 (profiles/round1.md) --
-    // 16 CTAs serialise the tiles of levels that one normal launch covers in a wave.
-    int64_t tail_dofs = 0;
-    if (const char* v = std::getenv("STMG_TAIL_DOFS")) tail_dofs = std::atoll(v);
-    if (const char* v = std::getenv("STMG_TAIL_CLUSTER")) h->tail_cluster = std::max(0, std::min(16, std::atoi(v)));
-    h->tail_start = -1;
-    const int nl = h->n_levels();
-    if (tail_dofs > 0 && nl >= 2 && tail_supported(h->coarsest) && !h->general()) {
-      for (int l = 1; l < nl; ++l)
-        if (h->ndofs(l) <= tail_dofs && nl - l <= kTailMaxLevels) {
-          h->tail_start = l;
-          break;
-        }
-    }
-  }
   if (share_ws_from_other) {
     // same tiling as the hierarchy whose workspace (norm partials) is shared
     for (size_t l = 0; l < h->views.size() && l < other->views.size(); ++l)
       h->views[l].tile_nt = other->views[l].tile_nt;
-    for (size_t l = 0; l < h->views.size() && l < other->views.size(); ++l) {
-      h->views[l].sweep_depth = other->views[l].sweep_depth;
-      h->views[l].bulk = other->views[l].bulk;
-      h->views[l].march = other->views[l].march;
-    }
     h->ws = other->ws;
   } else {
     int64_t bytes = 0;
@@ -950,10 +891,7 @@ struct Emitter {
   // kernel launches (= buffer flips) smooth(l, ., ., count) issues
   int smooth_launches(int l, int count) const {
     if (h->galerkin(l)) return count;
-    const int depth = static_cast<int>(h->views[l].sweep_depth);
-    int n = 0;
-    for (; depth > 2 && count >= depth; count -= depth) ++n;
-    return n + count / 2 + count % 2;
+    return count / 2 + count % 2;
   }
 
   // `count` damped-Jacobi sweeps from buffer `cur`: fused pairs (one pass over
@@ -970,21 +908,9 @@ struct Emitter {
       return;
     }
     const LevelView& L = h->views[l];
-    const int depth = static_cast<int>(L.sweep_depth);
-    for (; depth > 2 && count >= depth; count -= depth) {
-      timed_launch(l, kTimedSweep2, [&] {
-        launch_check(launch_sweep_deep(h->adjoint, L, depth, f, buf(l, cur), buf(l, 1 - cur), omega, s),
-                     "sweep_deep");
-      });
-      ++kernels;
-      cur = 1 - cur;
-    }
     for (; count >= 2; count -= 2) {
       timed_launch(l, kTimedSweep2, [&] {
-        if (L.bulk)
-          launch_check(launch_sweep2_bulk(h->adjoint, L, f, buf(l, cur), buf(l, 1 - cur), omega, s), "sweep2_bulk");
-        else
-          launch_check(launch_sweep2(h->adjoint, L, f, buf(l, cur), buf(l, 1 - cur), omega, s), "sweep2");
+        launch_check(launch_sweep2(h->adjoint, L, f, buf(l, cur), buf(l, 1 - cur), omega, s), "sweep2");
       });
       ++kernels;
       cur = 1 - cur;
@@ -1009,26 +935,6 @@ struct Emitter {
     const int nl = h->n_levels();
     const LevelView& L = h->views[l];
     double* f = h->ws->f[l]->p;
-    if (from_zero && nu >= 1 && l == h->tail_start) {
-      TailParams tp{};
-      tp.n_levels = nl - l;
-      tp.nu = nu;
-      tp.omega = omega;
-      for (int k = 0; k < tp.n_levels; ++k) {
-        tp.lv[k] = h->views[l + k];
-        tp.dir[k] = l + k < nl - 1 ? h->dirs[l + k] : 0;
-        tp.f[k] = h->ws->f[l + k]->p;
-        tp.xa[k] = h->ws->xa[l + k]->p;
-        tp.xb[k] = h->ws->xb[l + k]->p;
-      }
-      tp.cv = h->coarsest;
-      int fin = 0;
-      timed_launch(l, kTimedTail, [&] {
-        launch_check(launch_tail(h->adjoint, tp, h->tail_cluster, &fin, s), "coarse tail");
-      });
-      ++kernels;
-      return fin;
-    }
     if (l == nl - 1) {
       timed_launch(l, kTimedCoarsest, [&] {
         if (h->galerkin(l))
@@ -1065,9 +971,8 @@ struct Emitter {
     // per-node level and causal x / t transfer: the fused kernels
     const bool fused = !h->galerkin(l) && !h->gen_xfer(l);
     // the child's first pre-smoothing sweep (from zero) is fused into this
-    // restriction unless the child is the coarsest level or the coarse tail
-    const bool fuse_zero =
-        fused && nu >= 1 && l + 1 < nl - 1 && l + 1 != h->tail_start && !h->galerkin(l + 1);
+    // restriction unless the child is the coarsest level
+    const bool fuse_zero = fused && nu >= 1 && l + 1 < nl - 1 && !h->galerkin(l + 1);
     if (fused) {
       timed_launch(l, kTimedRestrict, [&] {
         launch_check(launch_restrict_residual(h->adjoint, L, C, h->dirs[l], f, buf(l, cur),
@@ -1147,8 +1052,6 @@ cudaGraphExec_t get_loop(stmg_hierarchy* h, int nu, double omega) {
   GraphEntry& e = get_graph(h, nu, omega);
   if (e.loop_tried) return e.loop_exec;
   e.loop_tried = true;
-  if (const char* v = std::getenv("STMG_DEVICE_LOOP"))
-    if (std::atoi(v) == 0) return nullptr;
   Nvtx range("stmg::capture_solve_loop");
   cudaGraph_t g = nullptr;
   cudaGraphExec_t ex = nullptr;
@@ -1620,8 +1523,6 @@ void optimise(const stmg_grid* geom, const stmg_optimise_options& o, int device,
       o.mma_asym_shrink >= 1.0 || o.mma_asym_grow <= 1.0)
     throw std::invalid_argument("MmaUpdater: invalid options");
   const auto t0 = std::chrono::steady_clock::now();
-  // STMG_OPT_TIMING=1: per-phase host wall time on stderr (profiling aid)
-  const bool timing = std::getenv("STMG_OPT_TIMING") != nullptr;
   double ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   auto tick = std::chrono::steady_clock::now();
   auto lap = [&](int k) {
@@ -1753,11 +1654,6 @@ void optimise(const stmg_grid* geom, const stmg_optimise_options& o, int device,
     chi = mma.update(chi, sens, dg, g_val);
     lap(5);
   }
-  if (timing)
-    std::fprintf(stderr,
-                 "optimise timing [s]: setup %.3f, plan+levels+refresh %.3f, primal %.3f, objective %.3f, "
-                 "adjoint %.3f, sensitivities+mma %.3f\n",
-                 ph[0], ph[1], ph[2], ph[3], ph[4], ph[5]);
   std::memcpy(chi_out, chi.data(), sizeof(double) * static_cast<size_t>(ne));
   *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -1988,6 +1884,20 @@ int stmg_hierarchy_set_profiling(stmg_hierarchy* h, int32_t on) {
   });
 }
 
+int stmg_hierarchy_set_tiling(stmg_hierarchy* h, int64_t small_dofs, int64_t tiny_dofs) {
+  return guarded([&] {
+    checked(h);
+    DeviceGuard dg(h->device);
+    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+    const int64_t small = small_dofs > 0 ? small_dofs : kSmallNtDofs;
+    const int64_t tiny = tiny_dofs > 0 ? tiny_dofs : kTinyNtDofs;
+    for (auto& v : h->views) v.tile_nt = tile_nt_for(v.nn * (v.n_t + 1), small, tiny);
+    h->coarsest.lv = h->views.back();
+    for (auto& kv : h->graphs) destroy_graph_entry(kv.second);
+    h->graphs.clear();
+  });
+}
+
 int stmg_hierarchy_profile(const stmg_hierarchy* h, int32_t level, int32_t kind, int64_t* launches,
                            double* seconds) {
   return guarded([&] {
@@ -2108,11 +2018,6 @@ int stmg_level_sweep_kernels(stmg_hierarchy* h, int32_t l, const double* f, doub
     for (int k = 0; k < launches; ++k) {
       if (h->galerkin(l))
         launch_check(launch_g_sweep(h->dviews[l], f, a, b, omega, h->stream), "g_sweep");
-      else if (fused_pairs == 5)  // bulk-copy pipelined pair (vectors need kVecPad tail padding)
-        launch_check(launch_sweep2_bulk(h->adjoint, h->views[l], f, a, b, omega, h->stream), "sweep2_bulk");
-      else if (fused_pairs == 3 || fused_pairs == 4)
-        launch_check(launch_sweep_deep(h->adjoint, h->views[l], fused_pairs, f, a, b, omega, h->stream),
-                     "sweep_deep");
       else if (fused_pairs)
         launch_check(launch_sweep2(h->adjoint, h->views[l], f, a, b, omega, h->stream), "sweep2");
       else
@@ -2216,13 +2121,6 @@ int stmg_norm2(stmg_hierarchy* h, const double* x, int64_t n, double* norm) {
     fetch_scalars(h, 1, sc);
     *norm = std::sqrt(sc[0]);
   });
-}
-
-// Benchmarking knob (not part of the reference-facing API): select the stencil
-// kernel design (see stmg_kernels.cu).  Existing graphs keep the design they
-// were captured with.
-int stmg_debug_set_kernel_variant(int32_t v) {
-  return guarded([&] { set_kernel_variant(v); });
 }
 
 int stmg_optimise(const stmg_grid* geom, const stmg_optimise_options* opts, int32_t device,

@@ -29,15 +29,6 @@ struct LevelView {
   // Time levels per tile of the overlapping-warp kernels (8, or 4 / 2 on small,
   // latency-bound levels); fixed when the hierarchy is built.
   int64_t tile_nt = 8;
-  // Deepest fused smoothing kernel used on this level (2: pairs; 3, 4: k_leanD
-  // on small levels where a launch is latency-bound); fixed at build.
-  int64_t sweep_depth = 2;
-  // Fused pairs through the bulk-copy pipelined kernel (k_bulk) instead of
-  // k_lean2x2; fixed at build (STMG_BULK_DOFS: levels with at least that many DOFs).
-  int64_t bulk = 0;
-  // Fused pairs through the streaming march (k_march2) instead of k_lean2x2;
-  // fixed at build (STMG_MARCH_DOFS: levels with at least that many DOFs).
-  int64_t march = 0;
 };
 
 inline bool full_range(const LevelView& L) { return L.n_lo == 0 && L.n_hi == L.n_t + 1; }
@@ -85,22 +76,6 @@ inline int64_t coarsest_scratch(const CoarsestView& cv) {
 inline size_t coarsest_chunked_smem(const CoarsestView& cv) {
   return sizeof(double) * 32 * ((size_t)cv.lv.n_t + 2 * (size_t)cv.n_chunks + 1 + 16);
 }
-
-// The coarse tail of a V-cycle (levels [Lt, L), all small) executed by one
-// thread-block cluster: level 0 here is hierarchy level Lt (its f is the
-// restricted input, its zero iterate is implied), the last is the coarsest.
-constexpr int kTailMaxLevels = 24;
-struct TailParams {
-  int n_levels;
-  int nu;
-  double omega;
-  LevelView lv[kTailMaxLevels];
-  int dir[kTailMaxLevels];  // step from tail level k to k + 1
-  double* f[kTailMaxLevels];
-  double* xa[kTailMaxLevels];
-  double* xb[kTailMaxLevels];
-  CoarsestView cv;
-};
 
 // ---- general coarse discretisations (stmg_general.cu) ------------------------------
 // Per-DOF 9-point operator of a Galerkin (R J P) level, in the hierarchy's row
@@ -195,15 +170,8 @@ int launch_sweep(bool adjoint, const LevelView& L, const double* f, const double
 // launch_sweep calls.  y must not alias x.
 int launch_sweep2(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
                   double omega, cudaStream_t s);
-// The same two sweeps through the bulk-copy (cp.async.bulk + mbarrier) pipelined
-// persistent kernel; full-range levels only.  f, x and y must be allocated with
-// kVecPad doubles of tail padding (the row copies round out to 16 bytes).
-constexpr int64_t kVecPad = 512;
-int launch_sweep2_bulk(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
-                       double omega, cudaStream_t s);
-// depth (3 or 4) sweeps y = S^depth(x) in one pass; full-range levels only.
-int launch_sweep_deep(bool adjoint, const LevelView& L, int depth, const double* f, const double* x,
-                      double* y, double omega, cudaStream_t s);
+// Tail padding (doubles) of every level vector and coefficient table.
+constexpr int64_t kVecPad = 32;
 // First sweep from a zero iterate: y = 0 + omega * (f * inv_diag), bitwise equal
 // to the general sweep applied to x = +0.
 int launch_sweep_from_zero(const LevelView& L, const double* f, double* y, double omega,
@@ -243,15 +211,6 @@ int launch_sensitivities(int64_t n_el, int64_t n_t, double dt, const double* dk_
 int launch_dot(const double* x, const double* y, int64_t n, double* partials, int64_t* n_partials,
                cudaStream_t s);
 int kernels_init();  // once per device
-// Launch the coarse-tail cluster kernel; returns the buffer index (0 = xa,
-// 1 = xb) of tail level 0 holding the result through *final_buf.
-// cluster >= 1: one thread-block cluster of that many CTAs; cluster <= 0: a cooperative
-// launch over every SM (grid-wide barriers between passes).
-int launch_tail(bool adjoint, const TailParams& p, int cluster, int* final_buf, cudaStream_t s);
-bool tail_supported(const CoarsestView& cv);
-// Kernel design selection for benchmarking (0 = production default).
-void set_kernel_variant(int v);
-int kernel_variant();
 int64_t sumsq_partials_needed(int64_t n);
 
 }  // namespace stmgb

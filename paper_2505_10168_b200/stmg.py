@@ -80,7 +80,7 @@ def _load():
         "stmg_residual_norm": [vp, vp, vp, C.POINTER(f64)],
         "stmg_norm2": [vp, vp, i64, C.POINTER(f64)],
         "stmg_synchronize": [vp],
-        "stmg_debug_set_kernel_variant": [i32],
+        "stmg_hierarchy_set_tiling": [vp, i64, i64],
         "stmg_dist_partition": [i32, vp, vp, i32, i64, C.POINTER(i32), vp],
         "stmg_optimise": [vp, vp, i32, vp, vp, C.POINTER(i32), C.POINTER(f64), C.POINTER(i32),
                           C.POINTER(f64)],
@@ -554,12 +554,15 @@ class LevelHierarchy:
         raw = getattr(stream, "cuda_stream", stream)
         _check(_lib.stmg_hierarchy_set_stream(self._h, C.c_void_p(raw) if raw else None))
 
+    def set_tiling(self, small_dofs=0, tiny_dofs=0):
+        """Per-handle time-tile thresholds (stmg_hierarchy_set_tiling; 0 = defaults)."""
+        _check(_lib.stmg_hierarchy_set_tiling(self._h, int(small_dofs), int(tiny_dofs)))
+
     def set_profiling(self, on=True):
         """True / 1: finest-level kernels; 2: every kernel (see stmg_b200.h)."""
         _check(_lib.stmg_hierarchy_set_profiling(self._h, int(on)))
 
-    PROFILE_KINDS = ("sweep", "restrict", "prolong_sweep", "sweep_pair", "sweep_from_zero", "coarsest",
-                     "coarse_tail")
+    PROFILE_KINDS = ("sweep", "restrict", "prolong_sweep", "sweep_pair", "sweep_from_zero", "coarsest")
 
     def profile(self) -> dict:
         """{level: {kind: (launches, seconds)}} accumulated over profiled solves."""
@@ -841,9 +844,6 @@ def mg_solve_dist(h: DistHierarchy, b, u, opts: Optional[SolveOptions] = None) -
                        rep.seconds, rep.device_seconds, rep.smoother_dof_updates, rep.kernel_launches)
 
 
-def set_kernel_variant(v: int) -> None:
-    """Benchmarking knob: stencil kernel design (5 is the production default; see stmg_kernels.cu)."""
-    _check(_lib.stmg_debug_set_kernel_variant(int(v)))
 
 
 def abi_version() -> int:

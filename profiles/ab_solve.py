@@ -1,12 +1,12 @@
 """Same-box A/B of whole-solve time under environment variants.
 
-Each variant runs in its own process (the hierarchy reads its STMG_* knobs when
-it is built); variants are interleaved over --rounds so that box drift hits all
+Each variant runs in its own process with its own environment (e.g.
+STMG_LIB_PATH=<an A/B build of libstmg_b200.so>); variants are interleaved over --rounds so that box drift hits all
 of them alike.  Per process: --warmup untimed solves, then --solves timed solves
 (L2 flushed before each, CUDA-event device time from the solve report).
 
     python profiles/ab_solve.py --config cfg1 \
-        --variant base= --variant deep=STMG_DEEP_DOFS=140000,STMG_DEEP_DEPTH=4
+        --variant base= --variant new=STMG_LIB_PATH=/tmp/ab/libstmg_b200.so
 """
 import argparse
 import json

@@ -22,7 +22,6 @@ def main():
     ap.add_argument("--sweeps", type=int, default=20)
     ap.add_argument("--adjoint", action="store_true")
     ap.add_argument("--reps", type=int, default=3)
-    ap.add_argument("--variant", type=int, default=5)
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -30,7 +29,6 @@ def main():
     from paper_2505_10168_b200 import configs as C
     from paper_2505_10168_b200 import stmg as S
 
-    S.set_kernel_variant(args.variant)
     cfg = C.CONFIGS[args.config](n_el=args.n_el, n_t=args.n_t)
     g = S.build_fine_grid(cfg.L, cfg.t_T, cfg.n_el, cfg.n_t)
     g.k, g.c = cfg.k, cfg.c
@@ -43,13 +41,13 @@ def main():
     h.set_stream(st)
     n0 = h.levels[0].n_dofs
     n1 = h.levels[1].n_dofs
-    with torch.cuda.stream(st):  # tail padding for the bulk-copy kernel
-        f = torch.randn(n0 + 512, dtype=torch.float64, device="cuda")
-        x = torch.randn(n0 + 512, dtype=torch.float64, device="cuda")
+    with torch.cuda.stream(st):
+        f = torch.randn(n0, dtype=torch.float64, device="cuda")
+        x = torch.randn(n0, dtype=torch.float64, device="cuda")
         fc = torch.empty(n1, dtype=torch.float64, device="cuda")
         xc = torch.randn(n1, dtype=torch.float64, device="cuda")
     st.synchronize()
-    out = {"n_dofs": n0, "adjoint": args.adjoint, "variant": args.variant}
+    out = {"n_dofs": n0, "adjoint": args.adjoint}
 
     def timed(fn, reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

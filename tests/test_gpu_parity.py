@@ -235,26 +235,6 @@ def test_adjoint_shares_workspace_with_primal(torch, S, port):
         check_solve(rep, lam, *reversed(hp_adj.solve(c, nu=2, tol=1e-10, max_cycles=20)))
 
 
-@pytest.mark.parametrize("scope", ["0", "16"])
-@pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "time_first"])
-def test_coarse_tail_kernel_is_bitwise(torch, S, port, monkeypatch, name, scope):
-    """The persistent coarse-tail kernel (STMG_TAIL_DOFS; grid-wide cooperative
-    launch for scope 0, one 16-CTA cluster otherwise) gives the same iterate
-    bit for bit as the per-level launches."""
-    cs = case(name)
-    b = cs.rhs_vector(port)
-    opts = S.SolveOptions(nu=cs.nu, tol=cs.tol)
-    monkeypatch.setenv("STMG_TAIL_DOFS", "0")
-    u0 = np.zeros_like(b)
-    r0 = S.mg_solve(gpu_hier(S, cs, port), b, u0, opts)
-    monkeypatch.setenv("STMG_TAIL_CLUSTER", scope)
-    monkeypatch.setenv("STMG_TAIL_DOFS", "20000")
-    u1 = np.zeros_like(b)
-    r1 = S.mg_solve(gpu_hier(S, cs, port), b, u1, opts)
-    assert r1.cycles == r0.cycles and r1.history == r0.history
-    assert np.array_equal(bits(u1), bits(u0))
-
-
 @pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "wide_short", "cfg0_deep"])
 def test_sweep_kernel_forms_bitwise(torch, S, port, name):
     """Single-sweep and fused two-sweep kernels, launched back to back."""
@@ -274,15 +254,15 @@ def test_sweep_kernel_forms_bitwise(torch, S, port, name):
             assert np.array_equal(bits(xt), bits(want)), (l, pairs)
 
 
-@pytest.mark.parametrize("env", ["STMG_SMALL_NT_DOFS", "STMG_TINY_NT_DOFS"])
+@pytest.mark.parametrize("tiles", [4, 2])
 @pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "time_first", "wide_short", "cfg0_deep"])
-def test_short_time_tiles_bitwise(torch, S, port, monkeypatch, name, env):
-    """4-level (STMG_SMALL_NT_DOFS) and 2-level (STMG_TINY_NT_DOFS) time tiles,
-    used on small latency-bound levels, on every level: kernels bit-identical
-    to the oracle, solve parity."""
-    monkeypatch.setenv(env, str(10 ** 15))
+def test_short_time_tiles_bitwise(torch, S, port, name, tiles):
+    """4-level and 2-level time tiles (stmg_hierarchy_set_tiling), used on small
+    latency-bound levels, on every level: kernels bit-identical to the oracle,
+    solve parity."""
     cs = case(name)
     h = gpu_hier(S, cs, port)
+    h.set_tiling(small_dofs=10 ** 15, tiny_dofs=10 ** 15 if tiles == 2 else 1)
     hp = port_hier(port, cs)
     rng = np.random.default_rng(17)
     dev = torch.device("cuda:0")
@@ -305,96 +285,39 @@ def test_short_time_tiles_bitwise(torch, S, port, monkeypatch, name, env):
     check_solve(rep, u, rep_p, u_p)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 6])
-@pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "time_first"])
-def test_alternative_kernel_designs_bitwise(torch, S, port, name, variant):
-    """Every selectable stencil design (STMG_KERNEL_VARIANT / set_kernel_variant;
-    5 is production): sweeps, residual and residual-restriction bit-identical
-    to the oracle, and a whole solve with the same cycles and history."""
-    cs = case(name)
-    h = gpu_hier(S, cs, port)
-    hp = port_hier(port, cs)
-    rng = np.random.default_rng(23)
-    dev = torch.device("cuda:0")
-    S.set_kernel_variant(variant)
-    try:
-        for l in range(h.n_levels() - 1):
-            n = hp.ndofs(l)
-            x, f = special_values(rng, n), special_values(rng, n)
-            xt, ft = torch.from_numpy(x).to(dev), torch.from_numpy(f).to(dev)
-            r = torch.empty_like(xt)
-            h.residual(l, ft, xt, r)
-            assert np.array_equal(bits(r), bits(hp.residual(l, f, x))), l
-            xs = xt.clone()
-            h.sweeps(l, ft, xs, 3)
-            assert np.array_equal(bits(xs), bits(hp.sweeps(l, f, x, 3))), l
-            fc = torch.empty(hp.ndofs(l + 1), dtype=torch.float64, device=dev)
-            h.restrict_residual(l, ft, xt, fc)
-            assert np.array_equal(bits(fc), bits(hp.restrict(l, hp.residual(l, f, x)))), l
-        b = cs.rhs_vector(port)
-        u_p, rep_p = hp.solve(b, nu=cs.nu, tol=cs.tol, max_cycles=cs.max_cycles)
-        u = np.zeros_like(b)
-        rep = S.mg_solve(h, b, u, S.SolveOptions(nu=cs.nu, tol=cs.tol, max_cycles=cs.max_cycles))
-        check_solve(rep, u, rep_p, u_p)
-    finally:
-        S.set_kernel_variant(5)
-
-
-@pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "time_first", "wide_short", "cfg0_deep", "tiny"])
-def test_deep_sweep_kernels_bitwise(torch, S, port, name):
-    """3- and 4-deep temporally blocked sweep kernels: one launch equals 3 / 4
-    reference sweeps bit for bit on every level (interior and boundary tiles)."""
-    cs = case(name)
-    h = gpu_hier(S, cs, port)
-    hp = port_hier(port, cs)
-    rng = np.random.default_rng(29)
-    dev = torch.device("cuda:0")
-    for l in range(h.n_levels()):
-        n = hp.ndofs(l)
-        x, f = special_values(rng, n), special_values(rng, n)
-        ft = torch.from_numpy(f).to(dev)
-        for depth in (3, 4):
-            xt = torch.from_numpy(x).to(dev)
-            yt = torch.empty_like(xt)
-            h.sweep_kernels(l, ft, xt, yt, 1, depth)
-            torch.cuda.synchronize()
-            assert np.array_equal(bits(yt), bits(hp.sweeps(l, f, x, depth))), (l, depth)
-
-
-@pytest.mark.parametrize("depth", ["3", "4"])
-@pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "cfg4_mini", "cfg0_deep"])
-def test_solve_with_deep_smoothing(torch, S, port, monkeypatch, name, depth):
-    """Every level smoothed with the deep kernels (STMG_DEEP_DOFS): the iterate
-    is bit-identical to the default schedule, and parity with the oracle holds."""
-    cs = case(name)
-    b = cs.rhs_vector(port)
-    opts = S.SolveOptions(nu=cs.nu, tol=cs.tol, max_cycles=cs.max_cycles)
-    monkeypatch.setenv("STMG_DEEP_DOFS", "0")
-    u0 = np.zeros_like(b)
-    r0 = S.mg_solve(gpu_hier(S, cs, port), b, u0, opts)
-    monkeypatch.setenv("STMG_DEEP_DOFS", str(10 ** 15))
-    monkeypatch.setenv("STMG_DEEP_DEPTH", depth)
-    u1 = np.zeros_like(b)
-    r1 = S.mg_solve(gpu_hier(S, cs, port), b, u1, opts)
-    assert r1.cycles == r0.cycles and r1.history == r0.history
-    assert np.array_equal(bits(u1), bits(u0))
+def extreme_values(rng, n):
+    """special_values salted with subnormals, values whose scaled products are
+    subnormal or overflow (|x| near DBL_MAX), and tiny normals."""
+    v = special_values(rng, n)
+    idx = rng.choice(n, size=max(4, n // 8), replace=False)
+    v[idx[0::4]] = 5e-324 * rng.integers(1, 1 << 20, size=v[idx[0::4]].size)
+    v[idx[1::4]] = 1.7e308 * rng.choice([-1.0, 1.0], size=v[idx[1::4]].size)
+    v[idx[2::4]] = 2.2250738585072014e-308 * rng.standard_normal(v[idx[2::4]].size)
+    v[idx[3::4]] = 1e300 * rng.standard_normal(v[idx[3::4]].size)
+    return v
 
 
 @pytest.mark.parametrize("omega", [0.5, 0.25, 1.0, 0.6, 2.0 / 3.0])
 @pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj"])
-def test_pair_kernel_omega_forms_bitwise(torch, S, port, name, omega):
-    """Fused pairs for power-of-two omega (one product r * (omega * invd)) and
-    for any other omega (omega * (r * invd)), against the oracle's sweeps."""
+@pytest.mark.parametrize("values", ["special", "extreme"])
+def test_pair_kernel_omega_forms_bitwise(torch, S, port, name, omega, values):
+    """Fused pairs compute omega * (r * invd) for every omega (the reference's
+    form, proj/src/kernels/kernels.cpp:70-73), bitwise against the oracle's
+    sweeps, including subnormal, overflowing and non-finite intermediates."""
     cs = case(name)
     h = gpu_hier(S, cs, port)
     hp = port_hier(port, cs)
     rng = np.random.default_rng(11)
+    gen = special_values if values == "special" else extreme_values
     for l in range(h.n_levels() - 1):
         n = hp.ndofs(l)
-        x, f = special_values(rng, n), special_values(rng, n)
+        x, f = gen(rng, n), gen(rng, n)
         want = hp.sweeps(l, f, x, 4, omega)
         xt, ft = torch.from_numpy(x).cuda(), torch.from_numpy(f).cuda()
         yt = torch.empty_like(xt)
         h.sweep_kernels(l, ft, xt, yt, 2, True, omega)
         torch.cuda.synchronize()
-        assert np.array_equal(bits(xt), bits(want)), (l, omega)
+        got = xt.cpu().numpy()
+        # NaN payloads differ between x86 and the GPU; every other value is bitwise
+        same = (bits(got) == bits(want)) | (np.isnan(got) & np.isnan(want))
+        assert same.all(), (l, omega, int((~same).sum()))
