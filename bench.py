@@ -1,19 +1,28 @@
 #!/usr/bin/env python
 """Benchmark: STMG solve on B200 (BASELINE metric: space-time DOF smoother
-updates/s; STMG solve time to the config's relative-residual tolerance).
+updates/s; STMG solve time).
 
-A step is one complete STMG solve (cold start u = 0) of the configured
-workload through the public C ABI.  `value` is whole-job smoother DOF updates
-per second with b already resident in HBM; `e2e` is the same metric through
-the C ABI with pinned HOST buffers (h2d of b and u, d2h of u inside the timed
-region).  `roofline` is the fine-level Jacobi sweep kernel (24 B per DOF
-update: read u, read f, write u'), timed by CUDA events recorded inside the
-V-cycle graph during the timed steps.  `cpu_baseline` is the compiled
-reference (oracle/_ref) timed on a bounded, time-truncated sample of the same
-workload on one host core.
+Workload (N = 1): BASELINE configs[2], the largest single-GPU config:
+cfg2 = 16384 x 65536 (1.07e9 space-time DOFs, 8.6 GB per vector), CR,
+Resolution planner (M = 256), 18 levels, V(1,1), run under the reference's
+own stopping rule (tol 1e-10, div_tol 1e9, proj/src/multigrid.cpp:260-273):
+the i.i.d. 1e4-contrast design makes the reference algorithm diverge, and both
+the reference (tests/golden/cfg2_mini.npz) and this build stop with Diverged
+after the same V-cycles (3 at full size).  A step is one such solve.
+
+* `value`: smoother DOF updates per second (sum over non-coarsest levels of
+  2 nu N_l per cycle) with b and u resident in HBM, CUDA events on the solve's
+  stream, max over ranks.  Inputs exceed L2 (3 x 8.6 GB), so no flush is needed.
+* `e2e`: the same solve through the C ABI with pinned HOST b and u (h2d of b and
+  u and d2h of u inside the timed region).
+* `roofline`: the level-0 kernel with the largest share of the profiled solves
+  (in-graph CUDA events), algorithmic bytes per launch / its launch time.
+* `cpu_baseline`: the compiled reference (oracle/_ref) on one host core, on a
+  bounded sample of the same workload (the cfg2 grid truncated in time).
+* `cfg1`: BASELINE config 1 (1024 x 4096, V(5,5), to 1e-10) as an extra key.
 
 Launch: python bench.py [--gpus N --steps K --warmup W --config cfg2]
-        torchrun --nproc-per-node N bench.py --gpus N ...   (N > 1)
+        torchrun --nproc-per-node N bench.py --gpus N ...   (N > 1: time slabs, strong scaling)
         python bench.py --impl reference ...                (reference CPU arm)
 """
 from __future__ import annotations
@@ -22,6 +31,7 @@ import argparse
 import json
 import math
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -34,19 +44,47 @@ sys.path.insert(0, ROOT)
 
 METRIC = "space-time DOF smoother updates/s; STMG solve time to 1e-10 rel residual"
 UNIT = "DOF-updates/s"
+# algorithmic HBM bytes per fine DOF of the level-0 kernels
+KERNEL_BYTES = {
+    "fine_norm_pass": 24,      # residual norm + first sweep: read u, f; write u'
+    "fine_sweep": 24,          # read u, f; write u'
+    "fine_sweep_pair": 24,     # two sweeps in one pass: read u, f; write u''
+    "fine_restrict": 20,       # read u, f; write f_c (half size: 4 B per fine DOF)
+    "fine_prolong_sweep": 28,  # read u, f, x_c (4 B per fine DOF); write u'
+}
+KERNEL_NAMES = {
+    "fine_norm_pass": "k_lean2<sweep, norm> (residual norm + speculative first sweep)",
+    "fine_sweep": "k_lean2<sweep>",
+    "fine_sweep_pair": "k_lean2x2 (two fused Jacobi sweeps)",
+    "fine_restrict": "k_restrict2 (residual + restriction)",
+    "fine_prolong_sweep": "k_lean2<sweep, ProlongLoad> (prolongation + first post-sweep)",
+}
 
 
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
             p = json.load(fh)
-        return float(p["hbm_gbs"]), "measured"
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def host_info():
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
 
 
 def bench_config(name: str, args):
-    """The workload and its pinned solver parameters (Appendix B of SURVEY)."""
+    """The workload and its pinned solver parameters."""
     from paper_2505_10168_b200 import configs as C
 
     kw = {}
@@ -72,6 +110,13 @@ def rhs_for(cfg, S, g):
     if cfg.rhs == "adjoint_uniform":
         return C.adjoint_uniform_rhs(cfg.n_el, cfg.n_t, cfg.L, cfg.t_T)
     return S.load_vector(g, kind=cfg.source_kind, params=cfg.source_params, masked=True)
+
+
+def plan_for(S, cfg, g):
+    req = S.PlanRequest(n_levels=cfg.n_levels, lambda_crit=cfg.lambda_crit, strategy=S.PlanStrategy(cfg.strategy),
+                        reassembly=S.ReassemblyMethod(cfg.reassembly), min_elements=cfg.min_elements,
+                        chi=cfg.chi, mat=cfg.mat)
+    return S.plan_coarsening(g, req)
 
 
 class ClockSampler:
@@ -177,159 +222,250 @@ class ClockSampler:
         return out
 
 
-def cpu_sample_config(cfg, sample_nt: int):
-    """Bounded CPU sample: the same config truncated to sample_nt time steps."""
-    from paper_2505_10168_b200 import configs as C
-
+def truncated_sample(cfg, sample_nt: int, dirs):
+    """Bounded CPU sample of a workload: the same grid and design truncated to
+    sample_nt time steps (same dt), coarsened along the workload's own path for
+    as long as the truncated grid allows it."""
     import copy
 
     s = copy.copy(cfg)
+    s.t_T = cfg.t_T * sample_nt / cfg.n_t
     s.n_t = sample_nt
-    return s
-
-
-def run_cpu_sample(cfg, sample_nt: int, prefer_ref: bool = True):
-    """Reference (oracle/_ref) or the C port on a time-truncated sample; returns dict."""
-    import numpy as np
-
-    from oracle import pyoracle
-
-    s = cpu_sample_config(cfg, sample_nt)
-    port = pyoracle.Port()
-    dirs, _ = port.plan(s.L, s.t_T, s.n_el, s.n_t, s.k, s.c, s.n_levels, strategy=s.strategy,
-                        reassembly=s.reassembly, min_elements=s.min_elements, chi=s.chi, mat=s.mat)
-    if s.rhs == "adjoint_uniform":
-        from paper_2505_10168_b200 import configs as C
-
-        b = C.adjoint_uniform_rhs(s.n_el, s.n_t, s.L, s.t_T)
-    else:
-        b = port.load_vector(s.L, s.t_T, s.n_el, s.n_t, s.source_kind, s.source_params)
-    kind = "port"
-    if prefer_ref and pyoracle.ref_available():
-        ref = pyoracle.Ref()
-        dirs_r, _ = ref.plan(s.L, s.t_T, s.n_el, s.n_t, s.k, s.c, s.n_levels, strategy=s.strategy,
-                             reassembly=s.reassembly, min_elements=s.min_elements, chi=s.chi,
-                             mat=s.mat)
-        h = ref.hierarchy(s.L, s.t_T, s.n_el, s.n_t, s.k, s.c, dirs_r, method=s.method,
-                          adjoint=s.adjoint, chi=s.chi, mat=s.mat)
-        kind = "reference"
-        dirs = dirs_r
-    else:
-        h = port.hierarchy(s.L, s.t_T, s.n_el, s.n_t, s.k, s.c, dirs, reassembly=s.reassembly,
-                           adjoint=s.adjoint, chi=s.chi, mat=s.mat)
-    t0 = time.perf_counter()
-    u, rep = h.solve(b, nu=s.nu, tol=s.tol, max_cycles=s.max_cycles)
-    wall = time.perf_counter() - t0
-    secs = rep.seconds if rep.seconds > 0 else wall
-    # smoother DOF updates of this solve: sum over non-coarsest levels of 2 nu N_l per cycle
-    ne, nt = s.n_el, s.n_t
-    per_cycle = 0.0
+    ne, nt, pre = s.n_el, s.n_t, []
     for d in dirs:
-        per_cycle += 2 * s.nu * (ne + 1) * (nt + 1)
+        d = int(d)
+        if (d == 0 and (ne < 2 or ne % 2)) or (d == 1 and (nt < 4 or nt % 2)):
+            break
+        pre.append(d)
+        if d == 0:
+            ne //= 2
+        else:
+            nt //= 2
+    return s, pre
+
+
+def per_cycle_updates(s, dirs, nu):
+    """Smoother DOF updates of one V(nu, nu) cycle: 2 nu N_l over the non-coarsest levels."""
+    ne, nt, total = s.n_el, s.n_t, 0.0
+    for d in dirs:
+        total += 2 * nu * (ne + 1) * (nt + 1)
         if int(d) == 0:
             ne //= 2
         else:
             nt //= 2
-    updates = per_cycle * rep.cycles
-    return {"kind": kind, "updates": updates, "seconds": secs, "cycles": rep.cycles,
-            "status": rep.status, "dofs": (s.n_el + 1) * (s.n_t + 1), "n_t": s.n_t,
-            "build_seconds": getattr(rep, "build_seconds", 0.0)}
+    return total
 
 
-def hbm_scale_sweep(S, torch, dev, hbm_peak, n_el=16384, n_t=65536, sweeps=10):
-    """Fine-level Jacobi sweep on the cfg2 grid (1.07e9 DOFs, 8.6 GB per vector,
-    far beyond L2): algorithmic 24 B per DOF update over CUDA-event time."""
+def sample_rhs(s, lib):
     from paper_2505_10168_b200 import configs as C
 
+    if s.rhs == "adjoint_uniform":
+        return C.adjoint_uniform_rhs(s.n_el, s.n_t, s.L, s.t_T)
+    return lib.load_vector(s.L, s.t_T, s.n_el, s.n_t, s.source_kind, s.source_params)
+
+
+def run_cpu_sample(cfg, sample_nt: int, dirs):
+    """The compiled reference (oracle/_ref; the C port if it is absent) on the
+    truncated sample: hierarchy built outside the timed region, one solve."""
+    from oracle import pyoracle
+
+    s, pre = truncated_sample(cfg, sample_nt, dirs)
+    if pyoracle.ref_available():
+        lib, kind = pyoracle.Ref(), "reference"
+        h = lib.hierarchy(s.L, s.t_T, s.n_el, s.n_t, s.k, s.c, pre, method=s.method, adjoint=s.adjoint,
+                          chi=s.chi, mat=s.mat)
+    else:
+        lib, kind = pyoracle.Port(), "port"
+        h = lib.hierarchy(s.L, s.t_T, s.n_el, s.n_t, s.k, s.c, pre, reassembly=s.reassembly, adjoint=s.adjoint,
+                          chi=s.chi, mat=s.mat)
+    b = sample_rhs(s, lib)
+    t0 = time.perf_counter()
+    u, rep = h.solve(b, nu=s.nu, omega=s.omega, tol=s.tol, div_tol=s.div_tol, max_cycles=s.max_cycles)
+    wall = time.perf_counter() - t0
+    secs = rep.seconds if rep.seconds > 0 else wall
+    return {"kind": kind, "updates": per_cycle_updates(s, pre, s.nu) * rep.cycles, "seconds": secs,
+            "cycles": rep.cycles, "status": rep.status, "dofs": (s.n_el + 1) * (s.n_t + 1), "n_t": s.n_t,
+            "levels": len(pre) + 1}
+
+
+def _ref_worker(conn, config, argd, sample_nt, dirs):
+    """--impl reference worker: one single-threaded reference solve per request
+    on the bounded sample; the hierarchy is built once, before the timed steps."""
     try:
-        cfg = C.cfg2(n_el=n_el, n_t=n_t)
-        g = S.build_fine_grid(cfg.L, cfg.t_T, n_el, n_t)
-        g.k, g.c = cfg.k, cfg.c
-        h2 = S.build_hierarchy(g, cfg.method, S.CoarseningPath([]), device=dev.index or 0)
-        st = torch.cuda.Stream(device=dev)
-        h2.set_stream(st)
-        n0 = (n_el + 1) * (n_t + 1)
-        with torch.cuda.stream(st):
-            f = torch.rand(n0, dtype=torch.float64, device=dev)
-            x = torch.rand(n0, dtype=torch.float64, device=dev)
-            y = torch.empty_like(x)
-        out = {"grid": f"{n_el}x{n_t}", "dofs": n0, "peak": hbm_peak, "unit": "GB/s",
-               "bytes_per_launch": 24 * n0}
-        for label, pairs in (("single_sweep", False), ("fused_two_sweeps", True)):
-            h2.sweep_kernels(0, f, x, y, 2, pairs)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(st)
-            h2.sweep_kernels(0, f, x, y, sweeps, pairs)
-            e1.record(st)
-            e1.synchronize()
-            ms = e0.elapsed_time(e1) / sweeps
-            achieved = 24.0 * n0 / (ms * 1e-3) / 1e9
-            out[label] = {"avg_launch_ms": ms, "achieved": achieved, "frac": achieved / hbm_peak,
-                          "dof_updates_per_s": (2 if pairs else 1) * n0 / (ms * 1e-3)}
-        out["achieved"] = out["single_sweep"]["achieved"]
-        out["frac"] = out["single_sweep"]["frac"]
-        out["avg_launch_ms"] = out["single_sweep"]["avg_launch_ms"]
-        del f, x, y, h2
-        torch.cuda.empty_cache()
-        return out
-    except Exception as e:  # reported, never required
-        return {"error": str(e)}
+        from oracle import pyoracle
+
+        cfg = bench_config(config, argparse.Namespace(**argd))
+        s, pre = truncated_sample(cfg, sample_nt, dirs)
+        ref = pyoracle.Ref()
+        h = ref.hierarchy(s.L, s.t_T, s.n_el, s.n_t, s.k, s.c, pre, method=s.method, adjoint=s.adjoint,
+                          chi=s.chi, mat=s.mat)
+        b = sample_rhs(s, ref)
+        upc = per_cycle_updates(s, pre, s.nu)
+        conn.send(("ready", (s.n_el + 1) * (s.n_t + 1), len(pre) + 1))
+        while True:
+            if conn.recv() == "stop":
+                break
+            u, rep = h.solve(b, nu=s.nu, omega=s.omega, tol=s.tol, div_tol=s.div_tol, max_cycles=s.max_cycles)
+            conn.send((upc * rep.cycles, rep.seconds, rep.cycles, int(rep.status)))
+    except Exception as e:  # reported by the parent
+        conn.send(("error", repr(e)))
+
+
+def planned_dirs(cfg):
+    """The GPU arm's coarsening path, planned by the product's planner on the host
+    (pinned bitwise to the reference planner, tests/test_capi_cpu.py)."""
+    from paper_2505_10168_b200 import stmg as S
+
+    g = S.build_fine_grid(cfg.L, cfg.t_T, cfg.n_el, cfg.n_t)
+    g.k, g.c = cfg.k, cfg.c
+    return [int(d) for d in plan_for(S, cfg, g).dirs]
 
 
 def reference_arm(args):
-    """--impl reference: the reference's own CPU path on all host cores (one
-    single-threaded reference solve per core, the reference has no threads)."""
+    """--impl reference: the reference's own CPU path on all host cores.  The
+    reference is single-threaded (no threads in proj/src), so each core runs one
+    reference solve of the bounded sample per step; a step ends when every core
+    is done.  value = all cores' smoother DOF updates / summed step wall time."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     import multiprocessing as mp
 
     cfg = bench_config(args.config, args)
-    cores = min(os.cpu_count() or 1, args.ref_cores)
-    sample_nt = args.cpu_sample_nt
+    dirs = planned_dirs(cfg)
+    cores = max(1, min(os.cpu_count() or 1, args.ref_cores))
+    sample_nt = min(args.cpu_sample_nt, cfg.n_t)
     ctx = mp.get_context("spawn")
-    vals = []
-    info = None
-    with ctx.Pool(cores) as pool:
-        for step in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
-            res = pool.starmap(_ref_worker, [(args.config, vars(args), sample_nt)] * cores)
-            wall = time.perf_counter() - t0
-            if step >= args.warmup:
-                upd = sum(r["updates"] for r in res)
-                vals.append((upd, wall, max(r["seconds"] for r in res)))
-                info = res[0]
-    upd = sum(v[0] for v in vals)
-    wall = sum(v[1] for v in vals)
+    pipes, procs = [], []
+    for _ in range(cores):
+        a, b_ = ctx.Pipe()
+        p = ctx.Process(target=_ref_worker, args=(b_, args.config, vars(args), sample_nt, dirs), daemon=True)
+        p.start()
+        pipes.append(a)
+        procs.append(p)
+    t_build = time.perf_counter()
+    info = [c.recv() for c in pipes]
+    t_build = time.perf_counter() - t_build
+    for m in info:
+        if m[0] != "ready":
+            raise RuntimeError(f"reference worker failed: {m[1]}")
+    dofs, levels = info[0][1], info[0][2]
+    upd = wall = 0.0
+    last = None
+    for step in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        for c in pipes:
+            c.send("go")
+        res = [c.recv() for c in pipes]
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            upd += sum(r[0] for r in res)
+            wall += dt
+            last = res[0]
+    for c in pipes:
+        c.send("stop")
+    for p in procs:
+        p.join(timeout=30)
     value = upd / wall if wall > 0 else 0.0
+    status = {0: "converged", 1: "max_cycles", 2: "diverged"}.get(last[3], str(last[3])) if last else None
+    sample = (f"{cores} concurrent single-threaded reference solves, each of {cfg.name} truncated to "
+              f"n_t={sample_nt} ({dofs} DOFs, {levels} levels along the GPU arm's path, nu={cfg.nu}, "
+              f"{last[2] if last else 0} V-cycles to {status}); hierarchies built once before the timed steps "
+              f"({t_build:.1f} s)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / max(args.steps, 1),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE shapes)",
-        # the same workload as the GPU arm; each step is a bounded sample of it
-        # (the time-truncated grid below), the metric is a rate
-        "config": {"workload": cfg.name, "n_el": cfg.n_el, "n_t": cfg.n_t,
-                   "dofs": (cfg.n_el + 1) * (cfg.n_t + 1), "method": cfg.method,
-                   "strategy": int(cfg.strategy), "n_levels": cfg.n_levels,
-                   "min_elements": cfg.min_elements, "nu": cfg.nu, "tol": cfg.tol,
+        "config": {"workload": cfg.name, "n_el": cfg.n_el, "n_t": cfg.n_t, "dofs": (cfg.n_el + 1) * (cfg.n_t + 1),
+                   "method": cfg.method, "strategy": int(cfg.strategy), "n_levels": cfg.n_levels,
+                   "min_elements": cfg.min_elements, "nu": cfg.nu, "tol": cfg.tol, "div_tol": cfg.div_tol,
                    "parallelism": f"{cores} host cores, one single-threaded reference solve each",
-                   "adjoint": cfg.adjoint, "sample_n_t": sample_nt},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": info["kind"] if info else "port",
-                         "sample": f"{cores} concurrent single-threaded solves of {cfg.name} truncated to "
-                                   f"n_t={sample_nt} ({info['dofs'] if info else 0} DOFs, "
-                                   f"{info['cycles'] if info else 0} V-cycles each)"},
+                   "adjoint": cfg.adjoint, "sample_n_t": sample_nt, "sample_dofs": dofs},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample,
+                         **host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "solve_seconds_sample": info["seconds"] if info else None,
+        "solve_seconds_sample": last[1] if last else None,
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def _ref_worker(config, argd, sample_nt):
-    ns = argparse.Namespace(**argd)
-    cfg = bench_config(config, ns)
-    return run_cpu_sample(cfg, sample_nt, prefer_ref=True)
+def kernel_table(prof_reps, n0, hbm):
+    """Level-0 kernels of the profiled solves: launches, mean launch time and the
+    algorithmic bandwidth (KERNEL_BYTES x fine DOFs per launch / mean time)."""
+    kt = {}
+    for key, bpd in KERNEL_BYTES.items():
+        c, secs = 0, 0.0
+        for r in prof_reps:
+            cc, ss = r.kernel_times.get(key, (0, 0.0))
+            c += cc
+            secs += ss
+        if c:
+            avg = secs / c
+            ach = bpd * n0 / avg / 1e9
+            kt[key] = {"launches": c, "avg_ms": 1e3 * avg, "total_ms": 1e3 * secs, "bytes_per_dof": bpd,
+                       "achieved_GBps": ach, "frac": ach / hbm}
+    return kt
+
+
+def ncu_traffic(config_name, kernel_key):
+    """DRAM bytes per launch of the roofline kernel from the committed ncu --set full
+    capture of the same workload (profiles/round2_ncu_<config>.json), or None."""
+    path = os.path.join(ROOT, "profiles", f"round2_ncu_{config_name}.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        k = d["kernels"][kernel_key]
+        return float(k["dram_bytes_read"]) + float(k["dram_bytes_write"]), os.path.relpath(path, ROOT)
+    except Exception:
+        return None, None
+
+
+def cfg1_extra(S, torch, dev, args):
+    """BASELINE config 1 (4.2e6 DOFs, V(5,5), 10 levels) to 1e-10 from u = 0, b and u
+    in HBM, L2 flushed before each solve; the reference's full-grid solve time of the
+    same problem is the committed golden's (tests/golden/cfg1_full.npz, one core)."""
+    import numpy as np
+
+    from paper_2505_10168_b200 import configs as C
+
+    cfg = C.cfg1()
+    g = S.build_fine_grid(cfg.L, cfg.t_T, cfg.n_el, cfg.n_t)
+    g.k, g.c = cfg.k, cfg.c
+    path = plan_for(S, cfg, g)
+    h = S.build_hierarchy(g, cfg.method, path, chi=cfg.chi, mat=cfg.mat, device=dev.index or 0)
+    st = torch.cuda.Stream(device=dev)
+    h.set_stream(st)
+    b = torch.from_numpy(rhs_for(cfg, S, g)).to(dev)
+    u = torch.zeros_like(b)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    opts = S.SolveOptions(nu=cfg.nu, omega=cfg.omega, tol=cfg.tol, div_tol=cfg.div_tol, max_cycles=cfg.max_cycles)
+    ts, reps = [], []
+    for k in range(args.cfg1_warmup + args.cfg1_steps):
+        with torch.cuda.stream(st):
+            flush.fill_(1.0)
+            u.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        rep = S.mg_solve(h, b, u, opts)
+        e1.record(st)
+        e1.synchronize()
+        if k >= args.cfg1_warmup:
+            ts.append(e0.elapsed_time(e1))
+            reps.append(rep)
+    ms = sum(ts) / len(ts)
+    out = {"grid": "1024x4096", "dofs": (cfg.n_el + 1) * (cfg.n_t + 1), "nu": cfg.nu, "n_levels": cfg.n_levels,
+           "solves": len(ts), "solve_ms": ms, "cycles": reps[-1].cycles,
+           "status": S.status_name(reps[-1].status), "final_rel_residual": reps[-1].history[-1],
+           "value": reps[-1].smoother_dof_updates / (ms * 1e-3), "l2": "flushed (256 MB write) before each solve"}
+    try:
+        gold = np.load(os.path.join(ROOT, "tests", "golden", "cfg1_full.npz"))
+        out["reference_full_grid"] = {"cycles": int(gold["cycles"]), "solve_seconds": float(gold["ref_seconds"]),
+                                      "cores": 1, "where": "builder container (tests/golden/make_golden.py --full)"}
+    except Exception:
+        pass
+    return out
 
 
 def main():
@@ -339,9 +475,9 @@ def main():
         os.environ["NCCL_DEBUG"] = "WARN"
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg1")
+    ap.add_argument("--config", default="cfg2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--nu", type=int, default=None)
     ap.add_argument("--n-levels", type=int, default=None)
@@ -353,9 +489,11 @@ def main():
     ap.add_argument("--cpu-sample-nt", type=int, default=512)
     ap.add_argument("--ref-cores", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--hbm-roofline", type=int, default=1)
-    ap.add_argument("--profile-steps", type=int, default=3,
+    ap.add_argument("--profile-steps", type=int, default=2,
                     help="extra solves with in-graph kernel timers (roofline), after the timed steps")
+    ap.add_argument("--cfg1", type=int, default=1, help="also time BASELINE config 1 (extra key)")
+    ap.add_argument("--cfg1-steps", type=int, default=5)
+    ap.add_argument("--cfg1-warmup", type=int, default=3)
     ap.add_argument("--dist", action="store_true",
                     help="use the time-slab (NCCL) path even at N=1 (smoke test of that path)")
     args = ap.parse_args()
@@ -363,7 +501,6 @@ def main():
     if args.impl == "reference":
         return reference_arm(args)
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -381,20 +518,17 @@ def main():
         if world > 1:
             dist.barrier()
 
-    cfg = bench_config(args.config, args)
-    if world > 1 and args.config == "cfg1":
-        from paper_2505_10168_b200 import configs as Cf
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
-        nu_, nl_ = cfg.nu, cfg.n_levels
-        cfg = Cf.cfg1_weak(world)
-        cfg.nu, cfg.n_levels = nu_, nl_
+    cfg = bench_config(args.config, args)
     g = S.build_fine_grid(cfg.L, cfg.t_T, cfg.n_el, cfg.n_t)
     g.k, g.c = cfg.k, cfg.c
-    req = S.PlanRequest(n_levels=cfg.n_levels, lambda_crit=cfg.lambda_crit,
-                        strategy=S.PlanStrategy(cfg.strategy),
-                        reassembly=S.ReassemblyMethod(cfg.reassembly), min_elements=cfg.min_elements,
-                        chi=cfg.chi, mat=cfg.mat)
-    path = S.plan_coarsening(g, req)
+    path = plan_for(S, cfg, g)
     t_build = time.perf_counter()
     dh = None
     if world > 1 or args.dist:
@@ -412,15 +546,18 @@ def main():
     t_build = time.perf_counter() - t_build
     b_host = rhs_for(cfg, S, g)
     n = b_host.size
+    n0 = (cfg.n_el + 1) * (cfg.n_t + 1)
     stream = torch.cuda.Stream(device=dev)
     if h is not None:
         h.set_stream(stream)
-    opts = S.SolveOptions(nu=cfg.nu, omega=cfg.omega, tol=cfg.tol, div_tol=cfg.div_tol,
-                          max_cycles=cfg.max_cycles)
+    opts = S.SolveOptions(nu=cfg.nu, omega=cfg.omega, tol=cfg.tol, div_tol=cfg.div_tol, max_cycles=cfg.max_cycles)
     with torch.cuda.stream(stream):
         b_dev = torch.from_numpy(b_host).to(dev)
         u_dev = torch.zeros_like(b_dev)
     stream.synchronize()
+    l2_note = ("inputs larger than L2 (b, u, u' = 3 x {:.1f} GB)".format(8 * n0 / 1e9) if 24 * n0 > 126e6 else
+               "L2 flushed (256 MB write) before every timed step")
+    flush = None if 24 * n0 > 126e6 else torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
 
     def solve_on(bv, uv):
         if dh is not None:
@@ -428,24 +565,12 @@ def main():
             return S.mg_solve_dist(dh, bv, uv, opts)
         return S.mg_solve(h, bv, uv, opts)
 
-    def one_solve():
-        with torch.cuda.stream(stream):
-            u_dev.zero_()
-        return solve_on(b_dev, u_dev)
-
-    for _ in range(args.warmup):
-        rep = one_solve()
-    # L2 flush buffer (> 126 MB L2): written between timed steps, outside the events
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
-    torch.cuda.synchronize(dev)
-    barrier()
-    torch.cuda.synchronize(dev)
-    reps = []
-    step_ms = []
-    with ClockSampler(dev) as clk:
-        for _ in range(args.steps):
+    def timed_solves(count):
+        reps, ms = [], []
+        for _ in range(count):
             with torch.cuda.stream(stream):
-                flush.fill_(1.0)
+                if flush is not None:
+                    flush.fill_(1.0)
                 u_dev.zero_()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -453,96 +578,55 @@ def main():
             reps.append(solve_on(b_dev, u_dev))
             e1.record(stream)
             e1.synchronize()
-            step_ms.append(e0.elapsed_time(e1))
+            ms.append(e0.elapsed_time(e1))
+        return reps, ms
+
+    timed_solves(args.warmup)
     torch.cuda.synchronize(dev)
     barrier()
-    # Kernel-level timing (roofline): the same solves again with CUDA event
-    # nodes around the fine-level kernels inside the graph.  Kept out of the
-    # timed steps above: each event node adds launch-gap overhead (~10 us per
-    # bracketed kernel when every level is profiled).
-    prof_reps, prof_ms = [], []
-    if h is not None and args.profile_steps > 0:
-        h.set_profiling(True)
-        one_solve()  # capture the profiled graph
-        for _ in range(args.profile_steps):
-            with torch.cuda.stream(stream):
-                flush.fill_(1.0)
-                u_dev.zero_()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            prof_reps.append(solve_on(b_dev, u_dev))
-            e1.record(stream)
-            e1.synchronize()
-            prof_ms.append(e0.elapsed_time(e1))
-        h.set_profiling(False)
-    ms = sum(step_ms)
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev) as clk:
+        reps, step_ms = timed_solves(args.steps)
+    torch.cuda.synchronize(dev)
+    barrier()
+    clocks = clk.summary()
+    t_max = max_over_ranks(sum(step_ms))
     updates = sum(r.smoother_dof_updates for r in reps)
-    t_max = ms
-    upd_total = updates
     if world > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt.item())
         uu = torch.tensor([updates], dtype=torch.float64, device=dev)
         dist.all_reduce(uu, op=dist.ReduceOp.SUM)
-        upd_total = float(uu.item())
-    value = upd_total / (t_max * 1e-3)
+        updates = float(uu.item())
+    value = updates / (t_max * 1e-3)
     last = reps[-1]
-
-    # roofline: the dominant fine-level kernel from in-graph CUDA events.  The
-    # fused two-sweep kernel (temporal blocking) moves 24 B/DOF (read u, f;
-    # write u'') for two DOF updates; a single sweep 24 B/DOF for one.
-    n0 = (cfg.n_el + 1) * (cfg.n_t + 1)
     hbm, peak_kind = peaks()
 
-    def tot(key):
-        c, t_ = 0, 0.0
-        for r in prof_reps:
-            cc, ss = r.kernel_times.get(key, (0, 0.0))
-            c += cc
-            t_ += ss
-        return c, t_
-
+    # Kernel-level timing (roofline): further solves with CUDA event nodes around
+    # the level-0 kernels inside the graph (host cycle loop).  Kept out of the
+    # timed steps: each event node adds launch-gap overhead.
+    kt, prof_ms = {}, []
+    if h is not None and args.profile_steps > 0:
+        h.set_profiling(True)
+        timed_solves(1)  # capture the profiled graph
+        prof_reps, prof_ms = timed_solves(args.profile_steps)
+        h.set_profiling(False)
+        kt = kernel_table(prof_reps, n0, hbm)
     roofline = None
-    pairs, pair_s = tot("fine_sweep_pair")
-    singles, single_s = tot("fine_sweep")
-    if pairs or singles:
-        use_pair = pair_s >= single_s
-        cnt, secs = (pairs, pair_s) if use_pair else (singles, single_s)
-        avg = secs / cnt
-        achieved = 24.0 * n0 / avg / 1e9
-        # DRAM bytes per launch of the same kernel at this size from the committed
-        # `ncu --set full` capture (profiles/round1.md, session 4: k_lean2x2<0,4,4,1>,
-        # grid (10, 1025) x 128 threads): 67.297 MB read + 8.578 MB written; ncu
-        # replays cold-cache, so this is the L2-miss traffic of an isolated launch,
-        # an upper bound for the in-solve one
-        traffic = (67.296768e6 + 8.578304e6) if (use_pair and n0 == 1025 * 4097) else None
-        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                    "frac": achieved / hbm, "traffic": traffic,
-                    "traffic_source": ("ncu --set full, profiles/round1.md (cold-cache replay)"
-                                       if traffic else None),
-                    "kernel": ("k_lean2x2 (two fused Jacobi sweeps, fine level, in-graph CUDA events)"
-                               if use_pair else "k_lean2<sweep> (fine level, in-graph CUDA events)"),
-                    "algorithmic_bytes_per_launch": 24 * n0, "dof_updates_per_launch": (2 if use_pair else 1) * n0,
-                    "avg_launch_ms": avg * 1e3, "launches_timed": cnt, "peak_source": peak_kind}
-    kt = {}
-    for key in ("fine_sweep", "fine_sweep_pair", "fine_restrict", "fine_prolong_sweep"):
-        c, s_ = 0, 0.0
-        for r in prof_reps:
-            cc, ss = r.kernel_times.get(key, (0, 0.0))
-            c += cc
-            s_ += ss
-        if c:
-            kt[key] = {"launches": c, "avg_ms": 1e3 * s_ / c}
-    step_ms_avg = t_max / max(args.steps, 1)
     if kt:
+        key = max(kt, key=lambda k_: kt[k_]["total_ms"])
+        k = kt[key]
+        traffic, tsrc = ncu_traffic(cfg.name, key)
+        roofline = {"bound": "hbm", "achieved": k["achieved_GBps"], "peak": hbm, "unit": "GB/s",
+                    "frac": k["frac"], "traffic": traffic, "traffic_source": tsrc,
+                    "kernel": f"{KERNEL_NAMES[key]}, level 0 of the {cfg.name} solve (in-graph CUDA events)",
+                    "kernel_key": key, "algorithmic_bytes_per_launch": k["bytes_per_dof"] * n0,
+                    "algorithmic_bytes_per_dof": k["bytes_per_dof"], "avg_launch_ms": k["avg_ms"],
+                    "launches_timed": k["launches"], "peak_source": peak_kind}
         kt["profiled_steps"] = len(prof_ms)
         kt["profiled_ms_per_step"] = sum(prof_ms) / len(prof_ms)
-        kt["fine_share_of_step"] = sum(v["launches"] * v["avg_ms"] for v in kt.values()
-                                       if isinstance(v, dict)) / max(sum(prof_ms), 1e-9)
+        kt["level0_share_of_step"] = sum(v["total_ms"] for v in kt.values() if isinstance(v, dict)) / max(
+            sum(prof_ms), 1e-9)
 
-    # e2e through the C ABI with pinned host buffers
+    # e2e through the C ABI with pinned host buffers (copies inside the timed region)
     e2e = None
     if args.e2e_steps > 0:
         bh = torch.from_numpy(b_host).pin_memory()
@@ -560,62 +644,57 @@ def main():
             e1.synchronize()
             tot_ms += e0.elapsed_time(e1)
             tot_upd += r.smoother_dof_updates
+        tot_ms = max_over_ranks(tot_ms)
         if world > 1:
-            tt = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            tot_ms = float(tt.item())
             uu = torch.tensor([tot_upd], dtype=torch.float64, device=dev)
             dist.all_reduce(uu, op=dist.ReduceOp.SUM)
             tot_upd = float(uu.item())
-        e2e = {"value": tot_upd / (tot_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 16 * n * world,
-               "d2h_bytes_per_step": 8 * n * world, "solve_seconds": tot_ms * 1e-3 / args.e2e_steps}
-
-    hbm_scale = None
-    if rank == 0 and args.hbm_roofline:
-        hbm_scale = hbm_scale_sweep(S, torch, dev, hbm)
-        if hbm_scale is not None and roofline is not None:
-            roofline["hbm_scale_cfg2_sweep"] = hbm_scale
-        elif hbm_scale is not None and "achieved" in hbm_scale:
-            # distributed solves carry no in-graph event timers: report the same kernel at HBM scale
-            roofline = {"bound": "hbm", "achieved": hbm_scale["achieved"], "peak": hbm, "unit": "GB/s",
-                        "frac": hbm_scale["frac"], "traffic": None,
-                        "kernel": "k_lean2<sweep> on the cfg2 grid (in-graph timers off for slab solves)",
-                        "algorithmic_bytes_per_launch": 24 * hbm_scale["dofs"],
-                        "avg_launch_ms": hbm_scale["avg_launch_ms"], "peak_source": peak_kind,
-                        "hbm_scale_cfg2_sweep": hbm_scale}
+        e2e = {"value": tot_upd / (tot_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 16 * n,
+               "d2h_bytes_per_step": 8 * n, "solve_seconds": tot_ms * 1e-3 / args.e2e_steps}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            res = run_cpu_sample(cfg, args.cpu_sample_nt, prefer_ref=True)
-            cpu = {"value": res["updates"] / res["seconds"] if res["seconds"] > 0 else None,
-                   "unit": UNIT, "cores": 1, "kind": res["kind"],
-                   "sample": f"{cfg.name} truncated to n_t={res['n_t']} ({res['dofs']} DOFs), one full "
-                             f"solve, {res['cycles']} V-cycles, {res['seconds']:.2f} s on 1 core"}
-        except Exception as e:  # the baseline is reported, never required
-            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
-                   "sample": f"unavailable: {e}"}
+    cfg1 = None
+    if rank == 0 and world == 1:
+        if args.cfg1 and cfg.name != "cfg1":
+            try:
+                del b_dev, u_dev
+                torch.cuda.empty_cache()
+                cfg1 = cfg1_extra(S, torch, dev, args)
+            except Exception as e:  # an extra key, never required
+                cfg1 = {"error": repr(e)}
+        if not args.no_cpu_baseline:
+            try:
+                res = run_cpu_sample(cfg, args.cpu_sample_nt, [int(d) for d in path.dirs])
+                cpu = {"value": res["updates"] / res["seconds"] if res["seconds"] > 0 else None,
+                       "unit": UNIT, "cores": 1, "kind": res["kind"],
+                       "sample": f"{cfg.name} truncated to n_t={res['n_t']} ({res['dofs']} DOFs, {res['levels']} "
+                                 f"levels along the GPU arm's path), one solve after an untimed hierarchy build, "
+                                 f"{res['cycles']} V-cycles to status {res['status']}, {res['seconds']:.2f} s on "
+                                 f"1 core", **host_info()}
+            except Exception as e:  # the baseline is reported, never required
+                cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
 
-    clocks = clk.summary()
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms_avg, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "warmup": args.warmup, "ms_per_step": t_max / max(args.steps, 1), "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded mt19937_64 designs, BASELINE shapes)",
             "config": {"workload": cfg.name, "n_el": cfg.n_el, "n_t": cfg.n_t, "dofs": n0,
                        "method": cfg.method, "strategy": int(cfg.strategy), "n_levels": cfg.n_levels,
-                       "min_elements": cfg.min_elements, "nu": cfg.nu, "tol": cfg.tol,
-                       "path": S.path_to_string(path),
+                       "min_elements": cfg.min_elements, "nu": cfg.nu, "tol": cfg.tol, "div_tol": cfg.div_tol,
+                       "max_cycles": cfg.max_cycles, "path": S.path_to_string(path),
+                       "stop_rule": "the reference's (proj/src/multigrid.cpp:260-273): converged below tol, "
+                                    "diverged above div_tol",
                        "parallelism": (f"time-slabs{world} (NCCL, {dh.n_distributed} distributed levels)"
                                        if dh is not None else "single"),
-                       "l2": ("inputs larger than L2" if n0 * 8 * 3 > 126e6 else
-                              "L2 flushed (256 MB write) before every timed step"),
-                       "adjoint": cfg.adjoint},
-            "solve_seconds": step_ms_avg * 1e-3, "cycles": last.cycles, "status": S.status_name(last.status),
-            "final_rel_residual": last.history[-1], "gpu_launches": int(sum(r.kernel_launches for r in reps)),
+                       "l2": l2_note, "adjoint": cfg.adjoint},
+            "solve_seconds": t_max * 1e-3 / max(args.steps, 1), "cycles": last.cycles,
+            "status": S.status_name(last.status), "history": last.history,
+            "gpu_launches": int(sum(r.kernel_launches for r in reps)),
             "roofline": roofline, "kernels": kt, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
-            "build_seconds": t_build, "device_bytes": h.device_bytes() if h is not None else dh.device_bytes,
+            "cfg1": cfg1, "build_seconds": t_build,
+            "device_bytes": h.device_bytes() if h is not None else dh.device_bytes,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -108,6 +108,10 @@ typedef struct stmg_solve_report {
   double fine_prolong_sweep_seconds;
   int64_t fine_sweep_pairs;    /* fused two-sweep (temporally blocked) launches */
   double fine_sweep_pair_seconds;
+  /* the level-0 pass closing each cycle: residual norm + speculative first sweep
+   * (+ the next cycle's level-0 restriction under STMG_FUSE_FINE_DOWN) */
+  int64_t fine_norm_passes;
+  double fine_norm_pass_seconds;
 } stmg_solve_report;
 
 typedef struct stmg_hierarchy stmg_hierarchy;
@@ -246,6 +250,24 @@ int stmg_level_residual(stmg_hierarchy* h, int32_t level, const double* f, const
 /* f_{l+1} = R (f - J_l x), residual recomputed on the fly (csr_residual + csr_spmv) */
 int stmg_level_restrict_residual(stmg_hierarchy* h, int32_t level, const double* f,
                                  const double* x, double* f_coarse);
+/* Fused V-cycle kernel forms (parity tests of the fusions; S = one damped-Jacobi
+ * sweep, S(0) = 0 + omega (f * inv_diag) the first sweep from a zero iterate,
+ * recomputed from f, never read from memory):
+ *   STMG_FUSED_ZERO_SWEEP          y = S(S(0))
+ *   STMG_FUSED_ZERO_PAIR           y = S(S(S(0)))
+ *   STMG_FUSED_ZERO_RESTRICT       f_coarse = R (f - J S(0))
+ *   STMG_FUSED_ZERO_PROLONG_SWEEP  y = S(S(0) + P x_coarse)
+ *   STMG_FUSED_FINE_DOWN           y = S(x), f_coarse = R (f - J y), *norm2 = ||f - J x||^2
+ * Unused pointers may be null. */
+enum {
+  STMG_FUSED_ZERO_SWEEP = 0,
+  STMG_FUSED_ZERO_PAIR = 1,
+  STMG_FUSED_ZERO_RESTRICT = 2,
+  STMG_FUSED_ZERO_PROLONG_SWEEP = 3,
+  STMG_FUSED_FINE_DOWN = 4
+};
+int stmg_level_fused(stmg_hierarchy* h, int32_t level, int32_t kind, const double* f, const double* x,
+                     const double* x_coarse, double* y, double* f_coarse, double omega, double* norm2);
 /* f_{l+1} = R r  (csr_spmv with R = s P^T) */
 int stmg_level_restrict(stmg_hierarchy* h, int32_t level, const double* r, double* f_coarse);
 /* x_l += P x_{l+1}  (csr_spmv_add) */
@@ -332,6 +354,16 @@ void stmg_dist_destroy(stmg_dist* d);
  * rest 8-level tiles.  Values <= 0 restore the defaults (5,000,000 / 600,000).
  * Captured V-cycle graphs of the handle are rebuilt on the next solve. */
 int stmg_hierarchy_set_tiling(stmg_hierarchy* h, int64_t small_dofs, int64_t tiny_dofs);
+/* Per-handle V-cycle fusions (A/B measurements and bitwise tests; default
+ * STMG_FUSE_DEFAULT = STMG_FUSE_VIRTUAL_ZERO, the combination measured fastest).
+ * Every combination gives bit-identical iterates.
+ *   STMG_FUSE_VIRTUAL_ZERO: a coarse level's first sweep from zero is recomputed
+ *     from f by the kernels that read it instead of being stored and re-read;
+ *   STMG_FUSE_FINE_DOWN: for nu = 1, level 0's residual norm, pre-smoothing sweep
+ *     and residual restriction run as one pass over memory.
+ * Captured graphs of the handle are rebuilt on the next solve. */
+enum { STMG_FUSE_VIRTUAL_ZERO = 1, STMG_FUSE_FINE_DOWN = 2, STMG_FUSE_ALL = 3, STMG_FUSE_DEFAULT = 1 };
+int stmg_hierarchy_set_fusion(stmg_hierarchy* h, int32_t flags);
 
 #ifdef __cplusplus
 }

@@ -18,9 +18,11 @@
 #include "stmg_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <unistd.h>
 
 static __thread char g_err[512];
 static int fail(int code, const char* msg) {
@@ -152,35 +154,110 @@ static inline int row_entries(const or_level* l, int adjoint, int64_t n, int64_t
   return p;
 }
 
+/* ------------------------------------------------------------------ */
+/* Level passes run over time levels on host threads (OR_THREADS, default */
+/* every online core, at most 64).  Each entry is computed by one thread   */
+/* with the same arithmetic, so results do not depend on the thread count; */
+/* reductions (norms, dots) stay sequential in the reference's order.      */
+/* ------------------------------------------------------------------ */
+typedef void (*range_fn)(void* ctx, int64_t lo, int64_t hi);
+typedef struct {
+  range_fn fn;
+  void* ctx;
+  int64_t lo, hi;
+} par_job;
+static void* par_run(void* a) {
+  par_job* j = (par_job*)a;
+  j->fn(j->ctx, j->lo, j->hi);
+  return NULL;
+}
+static int n_threads(void) {
+  const char* e = getenv("OR_THREADS");
+  long t = e ? atol(e) : sysconf(_SC_NPROCESSORS_ONLN);
+  if (t < 1) t = 1;
+  if (t > 64) t = 64;
+  return (int)t;
+}
+static void par_for(int64_t lo, int64_t hi, int64_t work_per_item, range_fn fn, void* ctx) {
+  const int64_t total = hi - lo;
+  int T = n_threads();
+  if (total * work_per_item < (1 << 18)) T = 1; /* small levels: not worth a thread */
+  if (T > total) T = (int)(total > 0 ? total : 1);
+  if (T <= 1) {
+    fn(ctx, lo, hi);
+    return;
+  }
+  pthread_t th[64];
+  par_job jobs[64];
+  int started[64] = {0};
+  for (int t = 0; t < T; ++t) {
+    jobs[t].fn = fn;
+    jobs[t].ctx = ctx;
+    jobs[t].lo = lo + total * t / T;
+    jobs[t].hi = lo + total * (t + 1) / T;
+    if (t > 0) started[t] = pthread_create(&th[t], NULL, par_run, &jobs[t]) == 0;
+  }
+  par_run(&jobs[0]);
+  for (int t = 1; t < T; ++t) {
+    if (started[t]) pthread_join(th[t], NULL);
+    else par_run(&jobs[t]); /* thread creation failed: run it here */
+  }
+}
+
+typedef struct {
+  const or_level* l;
+  const or_level* c;
+  int adjoint, dir;
+  double omega;
+  const double *f, *x;
+  double* out;
+} pass_ctx;
+
 /* proj/src/kernels/kernels.cpp:62-68 */
-static void residual_level(const or_level* l, int adjoint, const double* f, const double* x, double* r) {
+static void residual_rows(void* vc, int64_t lo, int64_t hi) {
+  const pass_ctx* q = (const pass_ctx*)vc;
+  const or_level* l = q->l;
   const int64_t nn = l->nn;
   double v[6], xv[6];
   int64_t col[6];
-  for (int64_t n = 0; n <= l->n_t; ++n)
+  for (int64_t n = lo; n < hi; ++n)
     for (int64_t i = 0; i < nn; ++i) {
-      const int cnt = row_entries(l, adjoint, n, i, v, col);
-      for (int p = 0; p < cnt; ++p) xv[p] = x[col[p]];
-      r[n * nn + i] = f[n * nn + i] - rowdot(v, xv, cnt);
+      const int cnt = row_entries(l, q->adjoint, n, i, v, col);
+      for (int p = 0; p < cnt; ++p) xv[p] = q->x[col[p]];
+      q->out[n * nn + i] = q->f[n * nn + i] - rowdot(v, xv, cnt);
     }
+}
+static void residual_level(const or_level* l, int adjoint, const double* f, const double* x, double* r) {
+  pass_ctx q = {l, NULL, adjoint, 0, 0.0, f, x, r};
+  par_for(0, l->n_t + 1, l->nn, residual_rows, &q);
 }
 
 /* proj/src/kernels/kernels.cpp:70-73 */
-static void jacobi_level(const or_level* l, double omega, const double* r, double* x) {
+static void jacobi_rows(void* vc, int64_t lo, int64_t hi) {
+  const pass_ctx* q = (const pass_ctx*)vc;
+  const or_level* l = q->l;
   const int64_t nn = l->nn;
-  for (int64_t n = 0; n <= l->n_t; ++n)
+  for (int64_t n = lo; n < hi; ++n)
     for (int64_t i = 0; i < nn; ++i) {
       const double id = (n == 0 || i == 0) ? l->inv_w : l->inv_diag[i];
-      x[n * nn + i] = x[n * nn + i] + omega * (r[n * nn + i] * id);
+      q->out[n * nn + i] = q->out[n * nn + i] + q->omega * (q->x[n * nn + i] * id);
     }
+}
+static void jacobi_level(const or_level* l, double omega, const double* r, double* x) {
+  pass_ctx q = {l, NULL, 0, 0, omega, NULL, r, x};
+  par_for(0, l->n_t + 1, l->nn, jacobi_rows, &q);
 }
 
 /* R = s P^T rows in ascending fine-column order (transfer.cpp:74-104). */
-static void restrict_level(const or_level* fine, const or_level* coarse, int dir, const double* r,
-                           double* fc) {
+static void restrict_rows(void* vc, int64_t lo, int64_t hi) {
+  const pass_ctx* q = (const pass_ctx*)vc;
+  const or_level *fine = q->l, *coarse = q->c;
+  const int dir = q->dir;
+  const double* r = q->x;
+  double* fc = q->out;
   const int64_t nnf = fine->nn, nnc = coarse->nn;
   double v[3], xv[3];
-  for (int64_t N = 0; N <= coarse->n_t; ++N)
+  for (int64_t N = lo; N < hi; ++N)
     for (int64_t I = 0; I < nnc; ++I) {
       int p = 0;
       if (dir == OR_DIR_X) {
@@ -195,13 +272,22 @@ static void restrict_level(const or_level* fine, const or_level* coarse, int dir
       fc[N * nnc + I] = rowdot(v, xv, p);
     }
 }
+static void restrict_level(const or_level* fine, const or_level* coarse, int dir, const double* r,
+                           double* fc) {
+  pass_ctx q = {fine, coarse, 0, dir, 0.0, NULL, r, fc};
+  par_for(0, coarse->n_t + 1, coarse->nn, restrict_rows, &q);
+}
 
 /* P rows (csr_spmv_add, kernels.cpp:55-60). */
-static void prolong_add_level(const or_level* fine, const or_level* coarse, int dir, const double* xc,
-                              double* x) {
+static void prolong_rows(void* vc, int64_t lo, int64_t hi) {
+  const pass_ctx* q = (const pass_ctx*)vc;
+  const or_level *fine = q->l, *coarse = q->c;
+  const int dir = q->dir;
+  const double* xc = q->x;
+  double* x = q->out;
   const int64_t nnf = fine->nn, nnc = coarse->nn;
   double v[2], xv[2];
-  for (int64_t n = 0; n <= fine->n_t; ++n)
+  for (int64_t n = lo; n < hi; ++n)
     for (int64_t i = 0; i < nnf; ++i) {
       int p = 0;
       if (dir == OR_DIR_X) {
@@ -215,6 +301,11 @@ static void prolong_add_level(const or_level* fine, const or_level* coarse, int 
       }
       x[n * nnf + i] = x[n * nnf + i] + rowdot(v, xv, p);
     }
+}
+static void prolong_add_level(const or_level* fine, const or_level* coarse, int dir, const double* xc,
+                              double* x) {
+  pass_ctx q = {fine, coarse, 0, dir, 0.0, NULL, xc, x};
+  par_for(0, fine->n_t + 1, fine->nn, prolong_rows, &q);
 }
 
 /* Exact solve of the coarsest system.  Masked rows: x = f / w.  Unmasked
@@ -648,20 +739,37 @@ static double source_value(int kind, const double* p, double x, double t, double
   return NAN;
 }
 
+typedef struct {
+  double L, t_T, dx, dt;
+  int64_t n_el;
+  int kind;
+  const double* params;
+  double* b;
+} load_ctx;
+/* time levels [lo, hi) of proj/src/assembly.cpp:65-83 (each level independent) */
+static void load_rows(void* vc, int64_t lo, int64_t hi) {
+  const load_ctx* q = (const load_ctx*)vc;
+  const int64_t nn = q->n_el + 1;
+  for (int64_t n = lo; n < hi; ++n) {
+    if (n == 0) continue;
+    const double t = (double)n * q->dt;
+    double* row = q->b + n * nn;
+    for (int64_t e = 0; e < q->n_el; ++e) {
+      const double qe = source_value(q->kind, q->params, ((double)e + 0.5) * q->dx, t, q->L, q->t_T) * q->dx / 2.0;
+      row[e] += qe;
+      row[e + 1] += qe;
+    }
+  }
+}
+
 int or_load_vector(double L, double t_T, int64_t n_el, int64_t n_t, int kind, const double* params,
                    int masked, double* b) {
   if (kind < 0 || kind > 3) return fail(OR_EINVAL, "load_vector: unknown source kind");
   const int64_t nn = n_el + 1;
   const double dx = L / (double)n_el, dt = t_T / (double)n_t;
   memset(b, 0, sizeof(double) * (size_t)((n_t + 1) * nn));
-  for (int64_t n = 1; n <= n_t; ++n) {
-    const double t = (double)n * dt;
-    for (int64_t e = 0; e < n_el; ++e) {
-      const double qe = source_value(kind, params, ((double)e + 0.5) * dx, t, L, t_T) * dx / 2.0;
-      b[n * nn + e] += qe;
-      b[n * nn + e + 1] += qe;
-    }
-  }
+  load_ctx q = {L, t_T, dx, dt, n_el, kind, params, b};
+  par_for(0, n_t + 1, nn, load_rows, &q);
   if (masked) {
     for (int64_t i = 0; i < nn; ++i) b[i] = 0.0;
     for (int64_t n = 1; n <= n_t; ++n) b[n * nn] = 0.0;

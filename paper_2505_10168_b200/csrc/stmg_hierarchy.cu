@@ -394,9 +394,28 @@ struct GraphKey {
   int nu;
   double omega;
   int profiling;
+  // level-0 vectors the graph reads and writes (the caller's b and u when they
+  // are bound in place, else the workspace's)
+  const void* b;
+  const void* x;
   bool operator<(const GraphKey& o) const {
-    return std::tie(nu, omega, profiling) < std::tie(o.nu, o.omega, o.profiling);
+    return std::tie(nu, omega, profiling, b, x) < std::tie(o.nu, o.omega, o.profiling, o.b, o.x);
   }
+};
+// Graphs kept per hierarchy; a solve with new bound pointers beyond this many
+// drops the cache (callers normally reuse the same b / u buffers).
+constexpr size_t kMaxGraphs = 16;
+
+// V-cycle fusions (stmg_hierarchy_set_fusion; all on by default).  Every
+// combination gives bit-identical iterates; they differ in HBM traffic only.
+enum FusionFlags {
+  kFuseVirtualZero = 1,  // coarse first sweep from zero recomputed from f where read
+  kFuseFineDown = 2,     // level 0 (nu = 1): norm + sweep + residual restriction in one pass
+  kFuseAll = 3,
+  // measured (cfg2, profiles/round2_fusion_ab.txt): the virtual zero iterate pays,
+  // the fine down-pass does not (k_down is issue-bound: 1.06 ms vs 0.51 + 0.55 ms
+  // for the separate sweep and restriction on a 1.3e8-DOF level)
+  kFuseDefault = kFuseVirtualZero
 };
 
 enum TimedKind {
@@ -458,11 +477,18 @@ struct stmg_hierarchy {
   cudaStream_t own_stream = nullptr;  // created with the hierarchy
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture
   int profiling = 0;  // 0 off, 1 finest-level kernels, 2 every kernel
+  int fusion = stmgb::kFuseDefault;  // stmgb::kFuse* flags (stmg_hierarchy_set_fusion)
   // per (level, kind): launches and device seconds accumulated while profiling
   std::vector<std::array<std::pair<int64_t, double>, stmgb::kTimedKinds>> prof;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, norm_ev0 = nullptr, norm_ev1 = nullptr;
   std::map<stmgb::GraphKey, stmgb::GraphEntry> graphs;
   int64_t device_bytes = 0;
+  // Level-0 right-hand side and iterate bound in place for the current solve
+  // (the caller's device b and u, no copies); null: the workspace's f / xa.
+  const double* bind_b = nullptr;
+  double* bind_x = nullptr;
+  double* f_ptr(int l) const { return l == 0 && bind_b ? const_cast<double*>(bind_b) : ws->f[l]->p; }
+  double* xa_ptr(int l) const { return l == 0 && bind_x ? bind_x : ws->xa[l]->p; }
   // General coarse discretisations.
   bool bilinear = false;                 // temporal interpolation of the t transfers
   std::vector<stmgb::Dia9Host> gal;      // P reassembly: primal 9-point operators (level 0 empty)
@@ -490,6 +516,8 @@ struct stmg_hierarchy {
     for (auto& kv : graphs) stmgb::destroy_graph_entry(kv.second);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (norm_ev0) cudaEventDestroy(norm_ev0);
+    if (norm_ev1) cudaEventDestroy(norm_ev1);
     if (own_stream) cudaStreamDestroy(own_stream);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     coef.clear();
@@ -816,6 +844,8 @@ std::shared_ptr<Workspace> make_workspace(const stmg_hierarchy* h, int64_t* byte
     LevelView finest_tiles = h->views[l];  // the most partials any tiling can need
     finest_tiles.tile_nt = 2;
     max_partials = std::max(max_partials, sweep_partials_needed(finest_tiles));
+    if (l == 0 && nl > 1)
+      max_partials = std::max(max_partials, down_partials_needed(finest_tiles, h->views[1], h->dirs[0]));
   }
   ws->partials = std::make_unique<DeviceBuf>(max_partials);
   ws->scalars = std::make_unique<DeviceBuf>(8);
@@ -854,11 +884,34 @@ void finish_create(stmg_hierarchy* h, bool share_ws_from_other, const stmg_hiera
   h->stream = h->own_stream;
   cuda_check(cudaEventCreate(&h->ev0), "cudaEventCreate");
   cuda_check(cudaEventCreate(&h->ev1), "cudaEventCreate");
+  cuda_check(cudaEventCreate(&h->norm_ev0), "cudaEventCreate");
+  cuda_check(cudaEventCreate(&h->norm_ev1), "cudaEventCreate");
 }
 
 // ---------------------------------------------------------------------------
 // V-cycle emission (proj/src/multigrid.cpp:184-208), recorded into a graph
 // ---------------------------------------------------------------------------
+
+// nu = 1 cycles whose level-0 residual restriction runs inside the norm pass
+// that closes the previous cycle (k_down: norm + sweep + restriction).
+bool fine_down(const stmg_hierarchy* h, int nu) {
+  return (h->fusion & kFuseFineDown) && nu == 1 && h->n_levels() >= 2 && !h->galerkin(0) && !h->gen_xfer(0);
+}
+
+// How level l + 1 gets its first sweep from zero: recomputed from f where it
+// is read (virt), written by level l's restriction (store), or neither (the
+// coarsest level, Galerkin levels, nu = 0).
+struct ZeroMode {
+  bool virt = false, store = false;
+};
+ZeroMode child_zero_mode(const stmg_hierarchy* h, int l, int nu) {
+  ZeroMode m;
+  const bool fused = !h->galerkin(l) && !h->gen_xfer(l);
+  const bool plain = fused && nu >= 1 && l + 1 < h->n_levels() - 1 && !h->galerkin(l + 1);
+  m.virt = plain && (h->fusion & kFuseVirtualZero) && !h->gen_xfer(l + 1);
+  m.store = plain && !m.virt;
+  return m;
+}
 
 struct Emitter {
   stmg_hierarchy* h;
@@ -868,6 +921,9 @@ struct Emitter {
   int64_t kernels = 0;
   std::vector<TimedKernel>* timed = nullptr;  // non-null: profiling
   int prof_mode = 0;
+  // level 0's restriction was done by the norm pass closing the previous cycle
+  // (fine_down); the V-cycle then starts at level 1
+  bool down_done = false;
 
   template <class F>
   void timed_launch(int l, int kind, F&& launch) {
@@ -885,7 +941,7 @@ struct Emitter {
   }
 
   double* buf(int l, int which) {
-    return which == 0 ? h->ws->xa[l]->p : h->ws->xb[l]->p;
+    return which == 0 ? h->xa_ptr(l) : h->ws->xb[l]->p;
   }
 
   // kernel launches (= buffer flips) smooth(l, ., ., count) issues
@@ -895,8 +951,17 @@ struct Emitter {
   }
 
   // `count` damped-Jacobi sweeps from buffer `cur`: fused pairs (one pass over
-  // memory per two sweeps), then a single sweep if count is odd.
-  void smooth(int l, const double* f, int& cur, int count) {
+  // memory per two sweeps), then a single sweep if count is odd.  virt: the
+  // iterate is the first sweep from zero, S(0), not stored; the first launch
+  // recomputes it from f (and clears virt).
+  void smooth(int l, const double* f, int& cur, int count, bool* virt = nullptr) {
+    auto xin = [&]() -> const double* {
+      if (virt && *virt) {
+        *virt = false;
+        return nullptr;
+      }
+      return buf(l, cur);
+    };
     if (h->galerkin(l)) {  // 9-point level: one launch per sweep
       for (; count > 0; --count) {
         timed_launch(l, kTimedSweep, [&] {
@@ -910,15 +975,14 @@ struct Emitter {
     const LevelView& L = h->views[l];
     for (; count >= 2; count -= 2) {
       timed_launch(l, kTimedSweep2, [&] {
-        launch_check(launch_sweep2(h->adjoint, L, f, buf(l, cur), buf(l, 1 - cur), omega, s), "sweep2");
+        launch_check(launch_sweep2(h->adjoint, L, f, xin(), buf(l, 1 - cur), omega, s), "sweep2");
       });
       ++kernels;
       cur = 1 - cur;
     }
     if (count == 1) {
       timed_launch(l, kTimedSweep, [&] {
-        launch_check(launch_sweep(h->adjoint, L, f, buf(l, cur), buf(l, 1 - cur), omega, nullptr,
-                                  nullptr, s),
+        launch_check(launch_sweep(h->adjoint, L, f, xin(), buf(l, 1 - cur), omega, nullptr, nullptr, s),
                      "sweep");
       });
       ++kernels;
@@ -931,10 +995,15 @@ struct Emitter {
   // from_zero: the iterate is identically zero (coarse levels).
   // zero_done: the first sweep from zero was already written into buffer 0 by
   // the parent's restriction (launch_restrict_residual with xc0).
-  int level(int l, int start, int pre_done, bool from_zero, bool zero_done = false) {
+  // zero_virtual: the first sweep from zero, S(0) = 0 + omega (f * inv_diag), is
+  // never stored: the kernels that read this level's iterate next recompute it
+  // from f (the first pre-smoothing launch; for nu = 1 the restriction and the
+  // fused prolong-sweep), so the parent writes no iterate and this level
+  // reads none (bit-identical to storing it).
+  int level(int l, int start, int pre_done, bool from_zero, bool zero_done = false, bool zero_virtual = false) {
     const int nl = h->n_levels();
     const LevelView& L = h->views[l];
-    double* f = h->ws->f[l]->p;
+    double* f = h->f_ptr(l);
     if (l == nl - 1) {
       timed_launch(l, kTimedCoarsest, [&] {
         if (h->galerkin(l))
@@ -948,9 +1017,13 @@ struct Emitter {
     }
     int cur = start;
     int pre = nu - pre_done;
+    bool virt = false;
     if (from_zero) {
       cur = 0;
-      if (nu >= 1 && zero_done) {
+      if (nu >= 1 && zero_virtual) {
+        virt = true;
+        pre = nu - 1;
+      } else if (nu >= 1 && zero_done) {
         pre = nu - 1;
       } else if (nu >= 1) {
         timed_launch(l, kTimedFromZero, [&] {
@@ -966,16 +1039,20 @@ struct Emitter {
         pre = 0;
       }
     }
-    smooth(l, f, cur, pre);
+    smooth(l, f, cur, pre, &virt);
     const LevelView& C = h->views[l + 1];
     // per-node level and causal x / t transfer: the fused kernels
     const bool fused = !h->galerkin(l) && !h->gen_xfer(l);
-    // the child's first pre-smoothing sweep (from zero) is fused into this
-    // restriction unless the child is the coarsest level
-    const bool fuse_zero = fused && nu >= 1 && l + 1 < nl - 1 && !h->galerkin(l + 1);
-    if (fused) {
+    // the child's first pre-smoothing sweep (from zero): recomputed where it is
+    // read (per-node child with fused transfers of its own), else written by
+    // this restriction; the coarsest level starts from its exact solve
+    const ZeroMode zm = child_zero_mode(h, l, nu);
+    const bool virt_zero = zm.virt, fuse_zero = zm.store;
+    if (l == 0 && down_done) {
+      if (!fused || pre != 0 || virt) throw std::logic_error("fine down-pass on a level that smooths first");
+    } else if (fused) {
       timed_launch(l, kTimedRestrict, [&] {
-        launch_check(launch_restrict_residual(h->adjoint, L, C, h->dirs[l], f, buf(l, cur),
+        launch_check(launch_restrict_residual(h->adjoint, L, C, h->dirs[l], f, virt ? nullptr : buf(l, cur),
                                               h->ws->f[l + 1]->p, s, fuse_zero ? buf(l + 1, 0) : nullptr,
                                               omega),
                      "restrict");
@@ -992,9 +1069,10 @@ struct Emitter {
       });
       kernels += 2;
     }
-    const int child = level(l + 1, 0, 0, true, fuse_zero);
+    const int child = level(l + 1, 0, 0, true, fuse_zero, virt_zero);
     const double* xc = buf(l + 1, child);
     int post = nu;
+    if (virt && !fused) throw std::logic_error("virtual zero iterate on a level without fused transfers");
     if (!fused) {
       // level 0 must end in buffer 0 (the solve reads it): prolong out of place
       // when the post-smoothing launches would otherwise leave it in buffer 1
@@ -1005,7 +1083,7 @@ struct Emitter {
       if (flip) cur = 1 - cur;
     } else if (nu >= 1) {
       timed_launch(l, kTimedProlongSweep, [&] {
-        launch_check(launch_sweep_prolong(h->adjoint, L, C, h->dirs[l], f, buf(l, cur), xc,
+        launch_check(launch_sweep_prolong(h->adjoint, L, C, h->dirs[l], f, virt ? nullptr : buf(l, cur), xc,
                                           buf(l, 1 - cur), omega, s),
                      "sweep_prolong");
       });
@@ -1023,13 +1101,35 @@ struct Emitter {
 
 bool speculative(const stmg_hierarchy* h, int nu) { return h->n_levels() > 1 && nu >= 1; }
 
+// The level-0 pass that closes a cycle (and opens the solve): block partials
+// of ||f - J x||^2 and, when the next cycle is speculated, its first
+// pre-smoothing sweep into y; under fine_down also level 1's right-hand side
+// (and stored zero iterate), i.e. the next cycle's level-0 restriction.
+void launch_norm_pass(stmg_hierarchy* h, int nu, const double* f, const double* x, double* y, double omega,
+                      cudaStream_t s, int64_t* np) {
+  Workspace& ws = *h->ws;
+  if (y != nullptr && fine_down(h, nu)) {
+    const ZeroMode zm = child_zero_mode(h, 0, nu);
+    launch_check(launch_down(h->adjoint, h->views[0], h->views[1], h->dirs[0], f, x, y, ws.f[1]->p,
+                             zm.store ? ws.xa[1]->p : nullptr, omega, ws.partials->p, np, s),
+                 "norm + sweep + restrict");
+    return;
+  }
+  launch_check(launch_sweep(h->adjoint, h->views[0], f, x, y, omega, ws.partials->p, np, s), "norm sweep");
+}
+
 GraphEntry& get_graph(stmg_hierarchy* h, int nu, double omega) {
-  const GraphKey key{nu, omega, h->profiling};  // (int mode; 0 = off)
+  const GraphKey key{nu, omega, h->profiling, h->f_ptr(0), h->xa_ptr(0)};  // profiling: int mode, 0 = off
   auto it = h->graphs.find(key);
   if (it != h->graphs.end()) return it->second;
+  if (h->graphs.size() >= kMaxGraphs) {
+    for (auto& kv : h->graphs) destroy_graph_entry(kv.second);
+    h->graphs.clear();
+  }
   Nvtx range("stmg::capture_v_cycle");
   GraphEntry e;
   Emitter em{h, nu, omega, h->cap_stream};
+  em.down_done = fine_down(h, nu);
   if (h->profiling) {
     em.timed = &e.timed;
     em.prof_mode = h->profiling;
@@ -1078,14 +1178,13 @@ cudaGraphExec_t get_loop(stmg_hierarchy* h, int nu, double omega) {
   bool ok = true;
   try {
     Emitter em{h, nu, omega, cs};
+    em.down_done = fine_down(h, nu);
     const bool spec = h->n_levels() > 1 && nu >= 1;
     const int fin = em.level(0, spec ? 1 : 0, spec ? 1 : 0, false);
     if (fin != 0) throw std::logic_error("level-0 iterate left the primary buffer");
     Workspace& ws = *h->ws;
     int64_t np = 0;
-    launch_check(launch_sweep(h->adjoint, h->views[0], ws.f[0]->p, ws.xa[0]->p, spec ? ws.xb[0]->p : nullptr,
-                              omega, ws.partials->p, &np, cs),
-                 "norm sweep");
+    launch_norm_pass(h, nu, h->f_ptr(0), h->xa_ptr(0), spec ? ws.xb[0]->p : nullptr, omega, cs, &np);
     auto* ctl = reinterpret_cast<SolveLoopCtl*>(ws.loop->p);
     launch_check(launch_finalize_check(ws.partials->p, np, ws.scalars->p, ctl, ws.loop->p + kLoopCtlDoubles,
                                        handle, cs),
@@ -1102,23 +1201,35 @@ cudaGraphExec_t get_loop(stmg_hierarchy* h, int nu, double omega) {
   return ex;
 }
 
-bool is_device_ptr(const void* p) {
+bool is_device_ptr(const void* p, int* device = nullptr) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
+  if (device) *device = a.device;
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// Binds the caller's level-0 vectors for the duration of one solve.
+struct Bind {
+  stmg_hierarchy* h;
+  Bind(stmg_hierarchy* hh, const double* b, double* x) : h(hh) {
+    h->bind_b = b;
+    h->bind_x = x;
+  }
+  ~Bind() {
+    h->bind_b = nullptr;
+    h->bind_x = nullptr;
+  }
+};
+
 // sum of squares of the level-0 residual (and optionally a speculative sweep
 // into xb) -> scalars[slot]
-int64_t emit_norm(stmg_hierarchy* h, const double* f, const double* x, double* y, double omega,
+int64_t emit_norm(stmg_hierarchy* h, int nu, const double* f, const double* x, double* y, double omega,
                   int slot) {
   int64_t np = 0;
-  launch_check(launch_sweep(h->adjoint, h->views[0], f, x, y, omega, h->ws->partials->p, &np,
-                            h->stream),
-               "norm sweep");
+  launch_norm_pass(h, nu, f, x, y, omega, h->stream, &np);
   launch_check(launch_finalize_sum(h->ws->partials->p, np, h->ws->scalars->p + slot, h->stream),
                "finalize");
   return 2;
@@ -1147,13 +1258,25 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
   const int64_t n = h->ndofs(0);
   const size_t bytes = sizeof(double) * static_cast<size_t>(n);
   Workspace& ws = *h->ws;
-  double* B = ws.f[0]->p;
-  double* X = ws.xa[0]->p;
+  int b_device = -1, u_device = -1;
+  const bool b_dev = is_device_ptr(b, &b_device), u_dev = is_device_ptr(u, &u_device);
+  // Device-resident b and u on the hierarchy's device are used in place: the V-cycle
+  // reads b and updates u directly (u is in/out, as in the reference), no copies.
+  // Host vectors (or other devices') are staged through the workspace.
+  const bool in_place = b_dev && u_dev && b_device == h->device && u_device == h->device &&
+                        static_cast<const void*>(b) != static_cast<const void*>(u);
+  Bind bind(h, in_place ? b : nullptr, in_place ? u : nullptr);
+  const double* B = h->f_ptr(0);
+  double* X = h->xa_ptr(0);
   double* Y = ws.xb[0]->p;
-  const bool b_dev = is_device_ptr(b), u_dev = is_device_ptr(u);
   cuda_check(cudaEventRecord(h->ev0, h->stream), "event");
-  cuda_check(cudaMemcpyAsync(B, b, bytes, b_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream), "b copy");
-  cuda_check(cudaMemcpyAsync(X, u, bytes, u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream), "u copy");
+  if (!in_place) {
+    cuda_check(cudaMemcpyAsync(ws.f[0]->p, b, bytes, b_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                               h->stream),
+               "b copy");
+    cuda_check(cudaMemcpyAsync(X, u, bytes, u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream),
+               "u copy");
+  }
   int64_t launches = 0;
   int64_t np = 0;
   launch_check(launch_sumsq(B, n, ws.partials->p, &np, h->stream), "sumsq");
@@ -1162,7 +1285,7 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
   const bool spec = speculative(h, o.nu);
   GraphEntry* g = nullptr;
   if (o.max_cycles > 0) g = &get_graph(h, o.nu, o.omega);
-  launches += emit_norm(h, B, X, spec && o.max_cycles > 0 ? Y : nullptr, o.omega, 1);
+  launches += emit_norm(h, o.nu, B, X, spec && o.max_cycles > 0 ? Y : nullptr, o.omega, 1);
   double sc[2];
   fetch_scalars(h, 2, sc);
   const double norm_b = std::sqrt(sc[0]);
@@ -1177,6 +1300,8 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
   rep->fine_sweeps = rep->fine_restricts = rep->fine_prolong_sweeps = rep->fine_sweep_pairs = 0;
   rep->fine_sweep_seconds = rep->fine_restrict_seconds = rep->fine_prolong_sweep_seconds = 0.0;
   rep->fine_sweep_pair_seconds = 0.0;
+  rep->fine_norm_passes = 0;
+  rep->fine_norm_pass_seconds = 0.0;
   double per_cycle_updates = 0.0;
   for (int l = 0; l + 1 < h->n_levels(); ++l) per_cycle_updates += 2.0 * o.nu * static_cast<double>(h->ndofs(l));
   cudaGraphExec_t loop = nullptr;
@@ -1209,8 +1334,16 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
       launches += g->kernels;
       if (g->final_buf != 0) throw std::logic_error("level-0 iterate left the primary buffer");
       const bool more = cycle < o.max_cycles;
-      launches += emit_norm(h, B, X, spec && more ? Y : nullptr, o.omega, 1);
+      if (h->profiling) cuda_check(cudaEventRecord(h->norm_ev0, h->stream), "event");
+      launches += emit_norm(h, o.nu, B, X, spec && more ? Y : nullptr, o.omega, 1);
+      if (h->profiling) cuda_check(cudaEventRecord(h->norm_ev1, h->stream), "event");
       fetch_scalars(h, 2, sc);
+      if (h->profiling) {  // the norm pass (incl. its finalize launch)
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, h->norm_ev0, h->norm_ev1), "event elapsed");
+        rep->fine_norm_passes += 1;
+        rep->fine_norm_pass_seconds += ms * 1e-3;
+      }
       for (const TimedKernel& t : g->timed) {
         float ms = 0.f;
         cuda_check(cudaEventElapsedTime(&ms, t.start, t.stop), "event elapsed");
@@ -1248,7 +1381,9 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
   }
   if (rep->cycles > 0) rep->factor = std::pow(history[nh - 1] / r0, 1.0 / rep->cycles);
   cuda_check(cudaEventRecord(h->ev1, h->stream), "event");
-  cuda_check(cudaMemcpyAsync(u, X, bytes, u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream), "u copy back");
+  if (!in_place)
+    cuda_check(cudaMemcpyAsync(u, X, bytes, u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream),
+               "u copy back");
   cuda_check(cudaStreamSynchronize(h->stream), "stream sync");
   float ms = 0.f;
   cudaEventElapsedTime(&ms, h->ev0, h->ev1);
@@ -1884,6 +2019,18 @@ int stmg_hierarchy_set_profiling(stmg_hierarchy* h, int32_t on) {
   });
 }
 
+int stmg_hierarchy_set_fusion(stmg_hierarchy* h, int32_t flags) {
+  return guarded([&] {
+    checked(h);
+    if (flags < 0 || flags > kFuseAll) throw std::invalid_argument("set_fusion: unknown flags");
+    DeviceGuard dg(h->device);
+    cuda_check(cudaStreamSynchronize(h->stream), "sync");
+    h->fusion = flags;
+    for (auto& kv : h->graphs) destroy_graph_entry(kv.second);
+    h->graphs.clear();
+  });
+}
+
 int stmg_hierarchy_set_tiling(stmg_hierarchy* h, int64_t small_dofs, int64_t tiny_dofs) {
   return guarded([&] {
     checked(h);
@@ -2060,6 +2207,60 @@ int stmg_level_restrict_residual(stmg_hierarchy* h, int32_t l, const double* f, 
   });
 }
 
+// Fused V-cycle kernel forms on device vectors (parity tests of the fusions).
+int stmg_level_fused(stmg_hierarchy* h, int32_t l, int32_t kind, const double* f, const double* x,
+                     const double* xc, double* y, double* fc, double omega, double* norm2) {
+  return guarded([&] {
+    checked(h);
+    check_level(h, l);
+    if (h->galerkin(l)) throw std::invalid_argument("level_fused: per-node levels only");
+    if (!f) throw std::invalid_argument("level_fused: null f");
+    const bool coarse_op = kind == STMG_FUSED_ZERO_RESTRICT || kind == STMG_FUSED_ZERO_PROLONG_SWEEP ||
+                           kind == STMG_FUSED_FINE_DOWN;
+    if (coarse_op && (l + 1 >= h->n_levels() || h->gen_xfer(l)))
+      throw std::out_of_range("level_fused: no fused transfer to a coarser level");
+    DeviceGuard dg(h->device);
+    const LevelView& L = h->views[l];
+    switch (kind) {
+      case STMG_FUSED_ZERO_SWEEP:
+        if (!y) throw std::invalid_argument("level_fused: null y");
+        launch_check(launch_sweep(h->adjoint, L, f, nullptr, y, omega, nullptr, nullptr, h->stream), "sweep");
+        break;
+      case STMG_FUSED_ZERO_PAIR:
+        if (!y) throw std::invalid_argument("level_fused: null y");
+        launch_check(launch_sweep2(h->adjoint, L, f, nullptr, y, omega, h->stream), "sweep2");
+        break;
+      case STMG_FUSED_ZERO_RESTRICT:
+        if (!fc) throw std::invalid_argument("level_fused: null f_coarse");
+        launch_check(launch_restrict_residual(h->adjoint, L, h->views[l + 1], h->dirs[l], f, nullptr, fc, h->stream,
+                                              nullptr, omega),
+                     "restrict");
+        break;
+      case STMG_FUSED_ZERO_PROLONG_SWEEP:
+        if (!y || !xc) throw std::invalid_argument("level_fused: null y / x_coarse");
+        launch_check(launch_sweep_prolong(h->adjoint, L, h->views[l + 1], h->dirs[l], f, nullptr, xc, y, omega,
+                                          h->stream),
+                     "sweep_prolong");
+        break;
+      case STMG_FUSED_FINE_DOWN: {
+        if (!x || !y || !fc) throw std::invalid_argument("level_fused: null x / y / f_coarse");
+        int64_t np = 0;
+        launch_check(launch_down(h->adjoint, L, h->views[l + 1], h->dirs[l], f, x, y, fc, nullptr, omega,
+                                 h->ws->partials->p, &np, h->stream),
+                     "down");
+        launch_check(launch_finalize_sum(h->ws->partials->p, np, h->ws->scalars->p + 2, h->stream), "finalize");
+        double sc[3];
+        fetch_scalars(h, 3, sc);
+        if (norm2) *norm2 = sc[2];
+        break;
+      }
+      default:
+        throw std::invalid_argument("level_fused: unknown kind");
+    }
+    sync_unless_capturing(h->stream);
+  });
+}
+
 int stmg_level_restrict(stmg_hierarchy* h, int32_t l, const double* r, double* fc) {
   return guarded([&] {
     checked(h);
@@ -2102,7 +2303,7 @@ int stmg_residual_norm(stmg_hierarchy* h, const double* f, const double* x, doub
     checked(h);
     if (!norm) throw std::invalid_argument("null argument");
     DeviceGuard dg(h->device);
-    emit_norm(h, f, x, nullptr, 0.5, 1);
+    emit_norm(h, 0, f, x, nullptr, 0.5, 1);
     double sc[2];
     fetch_scalars(h, 2, sc);
     *norm = std::sqrt(sc[1]);

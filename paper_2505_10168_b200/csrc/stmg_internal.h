@@ -163,7 +163,10 @@ int launch_load_vector(int kind, const double* params, int n_params, double L, d
 // ---- kernel launchers (stmg_kernels.cu); all asynchronous on `s` ------------------
 // One damped-Jacobi sweep y = x + omega (f - J x) / diag.  If partials != nullptr,
 // the block partial sums of r^2 are written too (deterministic order).  If y ==
-// nullptr only the residual norm partials are produced.
+// nullptr only the residual norm partials are produced.  x == nullptr: x is the
+// first sweep from zero S(0) = 0 + omega (f * inv_diag), recomputed from f (this
+// convention holds for launch_sweep2, launch_sweep_prolong and
+// launch_restrict_residual too).
 int launch_sweep(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
                  double omega, double* partials, int64_t* n_partials, cudaStream_t s);
 // Two sweeps y = S(S(x)) in one pass (temporal blocking); bit-identical to two
@@ -189,6 +192,13 @@ int launch_residual(bool adjoint, const LevelView& L, const double* f, const dou
 int launch_restrict_residual(bool adjoint, const LevelView& F, const LevelView& C, int dir,
                              const double* f, const double* x, double* fc, cudaStream_t s,
                              double* xc0 = nullptr, double omega = 0.0);
+// Level-0 down-pass of a V(1,1) cycle in one pass: block partials of
+// ||f - J x||^2, y = S(x), fc = R (f - J y) and, if xc0 != nullptr, the coarse
+// first sweep from zero (bitwise the separate sweep / restriction kernels).
+int launch_down(bool adjoint, const LevelView& F, const LevelView& C, int dir, const double* f, const double* x,
+                double* y, double* fc, double* xc0, double omega, double* partials, int64_t* n_partials,
+                cudaStream_t s);
+int64_t down_partials_needed(const LevelView& F, const LevelView& C, int dir);
 int launch_restrict(const LevelView& F, const LevelView& C, int dir, const double* r, double* fc,
                     cudaStream_t s);
 int launch_prolong_add(const LevelView& F, const LevelView& C, int dir, const double* xc, double* x,

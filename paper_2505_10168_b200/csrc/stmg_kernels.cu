@@ -195,12 +195,12 @@ struct PlainLoad {
   const double* __restrict__ x;
   int64_t nn;
   __device__ __forceinline__ double operator()(int64_t n, int64_t i) const { return x[n * nn + i]; }
-  __device__ __forceinline__ double warp_row(int64_t n, int64_t i, int64_t, int) const { return x[n * nn + i]; }
   struct Raw {
     double x;
   };
   __device__ __forceinline__ Raw warp_load(int64_t n, int64_t i, int64_t, int) const { return {x[n * nn + i]}; }
-  __device__ __forceinline__ double warp_finish(const Raw& r, int64_t, int64_t, int) const { return r.x; }
+  // invd: the lane's inverse diagonal (interior tiles: unmasked rows and nodes)
+  __device__ __forceinline__ double warp_finish(const Raw& r, int64_t, int64_t, int, double) const { return r.x; }
 };
 
 template <int DIR>
@@ -215,9 +215,6 @@ struct ProlongLoad {
   // lanes 0..17 load them once (coalesced) and every lane takes its one or two
   // values by shuffle; even/odd rows are selected, not branched.  Same
   // arithmetic as prolong_row.
-  __device__ __forceinline__ double warp_row(int64_t n, int64_t i, int64_t wfirst, int lane) const {
-    return warp_finish(warp_load(n, i, wfirst, lane), i, wfirst, lane);
-  }
   struct Raw {
     double x, v;
   };
@@ -232,7 +229,7 @@ struct ProlongLoad {
     }
     return r;
   }
-  __device__ __forceinline__ double warp_finish(const Raw& r, int64_t i, int64_t wfirst, int) const {
+  __device__ __forceinline__ double warp_finish(const Raw& r, int64_t i, int64_t wfirst, int, double) const {
     if (DIR == 1) return r.x + (0.0 + 1.0 * r.v);  // prolong_row<1>
     const int64_t c0 = (wfirst - 1) >> 1;
     const int k0 = (int)((i >> 1) - c0);
@@ -241,6 +238,69 @@ struct ProlongLoad {
     const double pe = 0.0 + 1.0 * va;
     const double po = (0.5 * va + 0.5 * vb) + 0.0;
     return r.x + ((i & 1) == 0 ? pe : po);
+  }
+};
+
+// The first sweep from a zero iterate, S(0) = 0 + omega (f * inv_diag) (the
+// dev_sweep_from_zero / coarse_from_zero expression), recomputed from f where
+// the iterate is read instead of being stored by the parent's restriction and
+// read back: the coarse-level iterate after its first pre-smoothing sweep.
+__device__ __forceinline__ double zero_sweep(double fv, double id, double omega) { return 0.0 + omega * (fv * id); }
+
+struct ZeroLoad {
+  const double* __restrict__ f;
+  const double* __restrict__ invd;  // the level's inv_diag row (coef + kInvD * nn)
+  double inv_w, omega;
+  int64_t nn;
+  __device__ __forceinline__ double id(int64_t n, int64_t i) const {
+    return (n == 0 || i == 0) ? inv_w : __ldg(invd + i);
+  }
+  __device__ __forceinline__ double operator()(int64_t n, int64_t i) const {
+    return zero_sweep(f[n * nn + i], id(n, i), omega);
+  }
+  struct Raw {
+    double f;
+  };
+  // interior tiles: n >= 1 and i >= 1, so no masked row and id = inv_diag[i]
+  __device__ __forceinline__ Raw warp_load(int64_t n, int64_t i, int64_t, int) const { return {f[n * nn + i]}; }
+  __device__ __forceinline__ double warp_finish(const Raw& r, int64_t, int64_t, int, double invd_i) const {
+    return zero_sweep(r.f, invd_i, omega);
+  }
+};
+
+// ProlongLoad with the fine iterate S(0) recomputed from f (nu = 1 coarse levels).
+template <int DIR>
+struct ProlongZeroLoad {
+  ZeroLoad z;
+  const double* __restrict__ xc;
+  int64_t nnc;
+  __device__ __forceinline__ double operator()(int64_t n, int64_t i) const {
+    return z(n, i) + prolong_row<DIR>(xc, nnc, n, i);
+  }
+  struct Raw {
+    double f, v;
+  };
+  __device__ __forceinline__ Raw warp_load(int64_t n, int64_t i, int64_t wfirst, int lane) const {
+    Raw r;
+    r.f = z.f[n * z.nn + i];
+    if (DIR == 1) {
+      r.v = __ldg(xc + (n >> 1) * nnc + i);
+    } else {
+      const int64_t c0 = (wfirst - 1) >> 1;
+      r.v = (lane <= 17 && c0 + lane < nnc) ? __ldg(xc + n * nnc + c0 + lane) : 0.0;
+    }
+    return r;
+  }
+  __device__ __forceinline__ double warp_finish(const Raw& r, int64_t i, int64_t wfirst, int, double invd_i) const {
+    const double x = zero_sweep(r.f, invd_i, z.omega);
+    if (DIR == 1) return x + (0.0 + 1.0 * r.v);  // prolong_row<1>
+    const int64_t c0 = (wfirst - 1) >> 1;
+    const int k0 = (int)((i >> 1) - c0);
+    const double va = __shfl_sync(kFull, r.v, k0);
+    const double vb = __shfl_sync(kFull, r.v, k0 + 1);
+    const double pe = 0.0 + 1.0 * va;
+    const double po = (0.5 * va + 0.5 * vb) + 0.0;
+    return x + ((i & 1) == 0 ? pe : po);
   }
 };
 
@@ -299,7 +359,7 @@ __device__ __forceinline__ double dev_lean2(const LevelView& L, const Ld& ld, co
     for (int r = 0; r <= NT; ++r) raw[r] = ld.warp_load(nbase + r, i, wfirst, lane);
     const Coefs c = load_coefs(L, i);
 #pragma unroll
-    for (int r = 0; r <= NT; ++r) xr[r] = ld.warp_finish(raw[r], i, wfirst, lane);
+    for (int r = 0; r <= NT; ++r) xr[r] = ld.warp_finish(raw[r], i, wfirst, lane, c.invd);
     double* yp = y + (n0 * nn + i);
     double pm = __shfl_up_sync(kFull, xr[0], 1);
     double pp = __shfl_down_sync(kFull, xr[0], 1);
@@ -388,7 +448,9 @@ __global__ void __launch_bounds__(kMaxTW, MINB) k_lean2(LevelView L, Ld ld,
 // store sweep 2 (28 nodes per warp).  Sweep 1 is also evaluated on the one
 // staged row before the tile (J) / after it (J^T) that sweep 2 couples to.
 // Staged: x on NT + 2 levels, f on NT + 1 levels.  Grid as k_lean2.
-template <bool ADJ, int NT>
+// ZX: x is the first sweep from a zero iterate, S(0) = 0 + omega (f * inv_diag),
+// recomputed from f on the staged levels (x is not read; NT + 2 f levels).
+template <bool ADJ, int NT, bool ZX = false>
 __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __restrict__ f,
                                             const double* __restrict__ x, double* __restrict__ y,
                                             double omega, int64_t tile, int64_t ttile) {
@@ -420,10 +482,22 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
     o[0] = (uint32_t)i;
 #pragma unroll
     for (int r = 1; r < NT + 2; ++r) o[r] = o[r - 1] + nn32;
+    if (ZX) {
+      // staged f rows sbase + r; the sweep-1 rows are staged rows r (J^T) / r + 1 (J)
+      double fs[NT + 2];
 #pragma unroll
-    for (int r = 0; r < NT + 2; ++r) xs[r] = __ldg(xb + o[r]);
+      for (int r = 0; r < NT + 2; ++r) fs[r] = __ldg(fb + o[r]);
 #pragma unroll
-    for (int r = 0; r < NT + 1; ++r) fv[r] = __ldg(fb + o[ADJ ? r : r + 1]);  // f rows s1base + r
+      for (int r = 0; r < NT + 1; ++r) fv[r] = fs[ADJ ? r : r + 1];
+      const double idv = __ldg(L.coef + kInvD * nn + i);
+#pragma unroll
+      for (int r = 0; r < NT + 2; ++r) xs[r] = zero_sweep(fs[r], idv, omega);
+    } else {
+#pragma unroll
+      for (int r = 0; r < NT + 2; ++r) xs[r] = __ldg(xb + o[r]);
+#pragma unroll
+      for (int r = 0; r < NT + 1; ++r) fv[r] = __ldg(fb + o[ADJ ? r : r + 1]);  // f rows s1base + r
+    }
     const Coefs c = load_coefs(L, i);
     auto upd = [&](double x0, double fval, double row) { return x0 + omega * ((fval - row) * c.invd); };
     double pm = __shfl_up_sync(kFull, xs[0], 1), pp = __shfl_down_sync(kFull, xs[0], 1);
@@ -455,10 +529,15 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
   const bool in_grid = i >= 0 && i < nn;
   const bool lane1 = lane >= 1 && lane <= 30 && in_grid;
   const bool lane2 = lane >= 2 && lane <= 29 && in_grid;
+  const double idz = (ZX && in_grid) ? __ldg(L.coef + kInvD * nn + i) : 0.0;
 #pragma unroll
   for (int r = 0; r < NT + 2; ++r) {
     const int64_t n = sbase + r;
-    xs[r] = (n >= 0 && n <= nt && in_grid) ? x[n * nn + i] : 0.0;
+    if (ZX)
+      xs[r] = (n >= 0 && n <= nt && in_grid) ? zero_sweep(f[n * nn + i], (n == 0 || i == 0) ? L.inv_w : idz, omega)
+                                             : 0.0;
+    else
+      xs[r] = (n >= 0 && n <= nt && in_grid) ? x[n * nn + i] : 0.0;
   }
 #pragma unroll
   for (int r = 0; r < NT + 1; ++r) {
@@ -538,13 +617,13 @@ constexpr int64_t kMinB5Dofs = 200000;
 template <int NT>
 constexpr int minb_for_nt() { return NT <= 2 ? 5 : NT <= 4 ? 4 : 3; }
 
-template <bool ADJ, int NT, int MINB = minb_for_nt<NT>()>
+template <bool ADJ, int NT, int MINB = minb_for_nt<NT>(), bool ZX = false>
 __global__ void __launch_bounds__(kMaxTW, MINB) k_lean2x2(LevelView L, const double* __restrict__ f,
                                                        const double* __restrict__ x,
                                                        double* __restrict__ y, double omega) {
   pdl_entry();
   const int64_t tt = (int64_t)blockIdx.z * gridDim.y + blockIdx.y;  // time tile
-  if (tt < ceil_div(L.n_hi - L.n_lo, NT)) dev_lean2x2<ADJ, NT>(L, f, x, y, omega, blockIdx.x, tt);
+  if (tt < ceil_div(L.n_hi - L.n_lo, NT)) dev_lean2x2<ADJ, NT, ZX>(L, f, x, y, omega, blockIdx.x, tt);
 }
 
 // Residual + restriction on the overlapping-warp chassis (production).  Lane l
@@ -565,7 +644,8 @@ __device__ __forceinline__ double coarse_from_zero(const LevelView& C, int64_t N
   return 0.0 + omega * (fv * id);
 }
 
-template <bool ADJ, int DIR, int NT>
+// ZX: x is S(0) = 0 + omega (f * inv_diag), recomputed from f (x is not read).
+template <bool ADJ, int DIR, int NT, bool ZX = false>
 __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelView& C,
                                               const double* __restrict__ f, const double* __restrict__ x,
                                               double* __restrict__ fc, int64_t tile, int64_t ttile, int tw,
@@ -588,9 +668,21 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
     const double* xp = x + (nbase * nn + i);
 #pragma unroll
     for (int k = 0; k < NT; ++k) fv[k] = fp[k * nn];
+    double fx = 0.0;  // ZX: the one staged level outside the f rows
+    if (ZX) fx = ADJ ? fp[NT * nn] : fp[-nn];
+    if (!ZX) {
 #pragma unroll
-    for (int r = 0; r <= NT; ++r) xr[r] = xp[r * nn];
+      for (int r = 0; r <= NT; ++r) xr[r] = xp[r * nn];
+    }
     const Coefs c = load_coefs(F, i);
+    if (ZX) {
+      // staged level nbase + r: f row r - 1 (J) / r (J^T)
+#pragma unroll
+      for (int r = 0; r <= NT; ++r) {
+        const double fr = ADJ ? (r < NT ? fv[r] : fx) : (r == 0 ? fx : fv[r - 1]);
+        xr[r] = zero_sweep(fr, c.invd, omega);
+      }
+    }
     // coarse inverse diagonal at this lane's coarse node (first coarse sweep from zero)
     double idc = 0.0;
     if (xc0 != nullptr) {
@@ -637,10 +729,21 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
     const int64_t n = n0 + k;
     fv[k] = (computes && n < F.n_hi) ? f[n * nn + i] : 0.0;
   }
+  if (!ZX) {
 #pragma unroll
-  for (int r = 0; r <= NT; ++r) {
-    const int64_t n = nbase + r;
-    xr[r] = (n >= 0 && n <= nt && in_grid) ? x[n * nn + i] : 0.0;
+    for (int r = 0; r <= NT; ++r) {
+      const int64_t n = nbase + r;
+      xr[r] = (n >= 0 && n <= nt && in_grid) ? x[n * nn + i] : 0.0;
+    }
+  }
+  if (ZX) {
+    const double idz = in_grid ? __ldg(F.coef + kInvD * nn + i) : 0.0;
+#pragma unroll
+    for (int r = 0; r <= NT; ++r) {
+      const int64_t n = nbase + r;
+      xr[r] = (n >= 0 && n <= nt && in_grid) ? zero_sweep(f[n * nn + i], (n == 0 || i == 0) ? F.inv_w : idz, omega)
+                                             : 0.0;
+    }
   }
   Coefs c{};
   if (computes) c = load_coefs(F, i);
@@ -695,14 +798,248 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
   }
 }
 
-template <bool ADJ, int DIR, int NT, int MINB = minb_for_nt<NT>()>
+// omega: the coarse first sweep's (xc0) and, with ZX, the fine iterate's S(0).
+template <bool ADJ, int DIR, int NT, int MINB = minb_for_nt<NT>(), bool ZX = false>
 __global__ void __launch_bounds__(kMaxTW, MINB) k_restrict2(LevelView F, LevelView C, const double* __restrict__ f,
                                                          const double* __restrict__ x, double* __restrict__ fc,
                                                          double* __restrict__ xc0, double omega) {
   pdl_entry();
   const int64_t tt = (int64_t)blockIdx.z * gridDim.y + blockIdx.y;
   if (tt < ceil_div(F.n_hi - F.n_lo, NT))
-    dev_restrict2<ADJ, DIR, NT>(F, C, f, x, fc, blockIdx.x, tt, blockDim.x, xc0, omega);
+    dev_restrict2<ADJ, DIR, NT, ZX>(F, C, f, x, fc, blockIdx.x, tt, blockDim.x, xc0, omega);
+}
+
+// Fine down-pass of a V(1,1) cycle in one pass over memory (level 0, nu = 1):
+//   stage 1: r1 = f - J x (its squares summed: the cycle's residual norm,
+//            proj/src/multigrid.cpp:246-249), y = x + omega (r1 * inv_diag)
+//            (the one pre-smoothing sweep, :190-193), y stored;
+//   stage 2: r2 = f - J y restricted, f_c = R r2 (:197-199), and optionally the
+//            coarse first sweep from zero x_c0 = S(0) (as dev_restrict2).
+// Temporal blocking as dev_lean2x2: stage 1 is also evaluated on the staged row
+// before the tile (J) / after it (J^T) that stage 2 couples to, and on one
+// node more on each side than stage 2.  Lane l holds node base - 1 + l:
+//   x step (DIR 0): stage 1 on lanes 1..30, stage 2 on lanes 2..29; coarse node
+//     I = base/2 + j (j = 1..13) takes fine nodes 2I-1, 2I, 2I+1 = lanes 2j,
+//     2j+1, 2j+2; warps advance 26 fine nodes (13 coarse), base = 26 w - 2, so
+//     warp w owns coarse nodes 13 w .. 13 w + 12 and fine nodes 26 w .. 26 w + 25
+//     (lanes 3..28: y stores and the norm);
+//   causal t step (DIR 1): lanes 2..29 own nodes 28 w .. 28 w + 27; coarse level
+//     N = fine levels 2N, 2N+1 at the same node (NT even, tiles start even).
+// Every value is the separate kernels' bit for bit: the same row evaluations,
+// lane orders and restriction sums; only the norm's summation order differs
+// (block partials, deterministic).
+template <bool ADJ, int DIR, int NT>
+__device__ __forceinline__ double dev_down(const LevelView& F, const LevelView& C, const double* __restrict__ f,
+                                           const double* __restrict__ x, double* __restrict__ y,
+                                           double* __restrict__ fc, double* __restrict__ xc0, double omega,
+                                           int64_t tile, int64_t ttile) {
+  constexpr int kAdv = DIR == 0 ? 26 : 28;  // owned fine nodes per warp
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nn = F.nn, nt = F.n_t, nnc = C.nn;
+  const int64_t w = tile * (int64_t)(blockDim.x >> 5) + warp;
+  const int64_t base = w * kAdv - 2;
+  if (base + 2 >= nn) return 0.0;  // no owned node (whole warp exits)
+  const int64_t i = base - 1 + lane;
+  const int64_t n0 = F.n_lo + ttile * NT;
+  const int64_t sbase = ADJ ? n0 : n0 - 2;   // staged x rows (NT + 2)
+  const int64_t s1base = ADJ ? n0 : n0 - 1;  // stage-1 rows (NT + 1)
+  const int own_lo = DIR == 0 ? 3 : 2, own_hi = DIR == 0 ? 28 : 29;
+  const bool owns = lane >= own_lo && lane <= own_hi;
+  const bool rows_in = (ADJ ? (n0 >= 1 && n0 + NT <= nt - 1) : (n0 >= 3 && n0 + NT - 1 <= nt)) &&
+                       n0 + NT - 1 < F.n_hi;
+  const bool nodes_in = base >= 2 && base + 29 <= F.n_el - 1;
+  double xs[NT + 2], fv[NT + 1], y1[NT + 1];
+  double acc = 0.0;
+  if (rows_in && nodes_in) {
+    const int64_t rowbase = sbase * nn;
+    const double* __restrict__ xb = opaque(x + rowbase);
+    const double* __restrict__ fb = opaque(f + rowbase);
+    double* __restrict__ yb = opaque(y + rowbase);
+    const uint32_t nn32 = (uint32_t)nn;
+    uint32_t o[NT + 2];
+    o[0] = (uint32_t)i;
+#pragma unroll
+    for (int r = 1; r < NT + 2; ++r) o[r] = o[r - 1] + nn32;
+#pragma unroll
+    for (int r = 0; r < NT + 2; ++r) xs[r] = __ldg(xb + o[r]);
+#pragma unroll
+    for (int r = 0; r < NT + 1; ++r) fv[r] = __ldg(fb + o[ADJ ? r : r + 1]);  // f rows s1base + r
+    const Coefs c = load_coefs(F, i);
+    double idc = 0.0;  // coarse inverse diagonal at this lane's coarse node (x_c0)
+    if (xc0 != nullptr) {
+      const int64_t I = DIR == 0 ? base / 2 + lane : i;
+      if (DIR == 1 || (lane >= 1 && lane <= 13)) idc = __ldg(C.coef + kInvD * nnc + I);
+    }
+    // ---- stage 1: y1[r] = S(x) on row s1base + r; norm on the tile's own rows
+    double pm = __shfl_up_sync(kFull, xs[0], 1), pp = __shfl_down_sync(kFull, xs[0], 1);
+#pragma unroll
+    for (int r = 0; r <= NT; ++r) {
+      const double x1 = xs[r + 1];
+      const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
+      double res, x0;
+      if (ADJ) {
+        res = fv[r] - row_interior<true>(c, pm, xs[r], pp, qm, x1, qp);
+        x0 = xs[r];
+      } else {
+        res = fv[r] - row_interior<false>(c, qm, x1, qp, pm, xs[r], pp);
+        x0 = x1;
+      }
+      y1[r] = x0 + omega * (res * c.invd);
+      const bool own_row = ADJ ? r < NT : r >= 1;  // row n0 .. n0 + NT - 1
+      if (own_row && owns) {
+        acc = acc + res * res;
+        st_global(yb + o[ADJ ? r : r + 1], y1[r]);
+      }
+      pm = qm;
+      pp = qp;
+    }
+    // ---- stage 2: r2 = f - J y on rows n0 .. n0 + NT - 1, restricted
+    double am = __shfl_up_sync(kFull, y1[0], 1), ap = __shfl_down_sync(kFull, y1[0], 1);
+    double r_even = 0.0;
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const double z1 = y1[k + 1];
+      const double bm = __shfl_up_sync(kFull, z1, 1), bp = __shfl_down_sync(kFull, z1, 1);
+      const double r2 = ADJ ? fv[k] - row_interior<true>(c, am, y1[k], ap, bm, z1, bp)
+                            : fv[k + 1] - row_interior<false>(c, bm, z1, bp, am, y1[k], ap);
+      if (DIR == 0) {
+        const int src = 2 * lane;
+        const double ra = __shfl_sync(kFull, r2, src & 31);
+        const double rb = __shfl_sync(kFull, r2, (src + 1) & 31);
+        const double rc = __shfl_sync(kFull, r2, (src + 2) & 31);
+        if (lane >= 1 && lane <= 13) {
+          const double v = ((0.5 * ra + 1.0 * rb) + 0.5 * rc) + 0.0;
+          fc[(n0 + k) * nnc + base / 2 + lane] = v;
+          if (xc0 != nullptr) xc0[(n0 + k) * nnc + base / 2 + lane] = 0.0 + omega * (v * idc);
+        }
+      } else {
+        if ((k & 1) == 0) {
+          r_even = r2;
+        } else if (owns) {
+          const double v = (0.5 * r_even + 0.5 * r2) + 0.0;
+          fc[((n0 + k) >> 1) * nnc + i] = v;
+          if (xc0 != nullptr) xc0[((n0 + k) >> 1) * nnc + i] = 0.0 + omega * (v * idc);
+        }
+      }
+      am = bm;
+      ap = bp;
+    }
+    return acc;
+  }
+  // ---- general path (boundary tiles): per-row-class evaluation
+  const bool in_grid = i >= 0 && i < nn;
+  const bool lane1 = lane >= 1 && lane <= 30 && in_grid;
+  const bool own_g = owns && in_grid;
+#pragma unroll
+  for (int r = 0; r < NT + 2; ++r) {
+    const int64_t n = sbase + r;
+    xs[r] = (n >= 0 && n <= nt && in_grid) ? x[n * nn + i] : 0.0;
+  }
+#pragma unroll
+  for (int r = 0; r < NT + 1; ++r) {
+    const int64_t n = s1base + r;
+    fv[r] = (n >= 0 && n <= nt && lane1) ? f[n * nn + i] : 0.0;
+  }
+  Coefs c{};
+  if (lane1) c = load_coefs(F, i);
+  double pm = __shfl_up_sync(kFull, xs[0], 1), pp = __shfl_down_sync(kFull, xs[0], 1);
+#pragma unroll
+  for (int r = 0; r <= NT; ++r) {
+    const double x1 = xs[r + 1];
+    const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
+    const int64_t n = s1base + r;
+    double v = 0.0;
+    if (lane1 && n >= 0 && n <= nt) {
+      double row, x0;
+      if (ADJ) {
+        row = row_sum<true>(F, n, i, c, pm, xs[r], pp, qm, x1, qp);
+        x0 = xs[r];
+      } else {
+        row = row_sum<false>(F, n, i, c, qm, x1, qp, pm, xs[r], pp);
+        x0 = x1;
+      }
+      const double res = fv[r] - row;
+      const double id = (n == 0 || i == 0) ? F.inv_w : c.invd;
+      v = x0 + omega * (res * id);
+      if (own_g && n >= n0 && n < n0 + NT && n < F.n_hi) {
+        acc = acc + res * res;
+        y[n * nn + i] = v;
+      }
+    }
+    y1[r] = v;
+    pm = qm;
+    pp = qp;
+  }
+  double am = __shfl_up_sync(kFull, y1[0], 1), ap = __shfl_down_sync(kFull, y1[0], 1);
+  double r_even = 0.0;
+  const bool lane2 = lane >= 2 && lane <= 29 && in_grid;
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    const int64_t n = n0 + k;
+    if (n >= F.n_hi) break;
+    const double z1 = y1[k + 1];
+    const double bm = __shfl_up_sync(kFull, z1, 1), bp = __shfl_down_sync(kFull, z1, 1);
+    double r2 = 0.0;
+    if (lane2)
+      r2 = ADJ ? fv[k] - row_sum<true>(F, n, i, c, am, y1[k], ap, bm, z1, bp)
+               : fv[k + 1] - row_sum<false>(F, n, i, c, bm, z1, bp, am, y1[k], ap);
+    if (DIR == 0) {
+      const int src = 2 * lane;
+      const double ra = __shfl_sync(kFull, r2, src & 31);
+      const double rb = __shfl_sync(kFull, r2, (src + 1) & 31);
+      const double rc = __shfl_sync(kFull, r2, (src + 2) & 31);
+      const int64_t I = base / 2 + lane;
+      if (lane >= 1 && lane <= 13 && I >= 0 && I < nnc) {
+        Acc a;
+        if (I >= 1) a.add(0.5 * ra);
+        a.add(1.0 * rb);
+        if (2 * I + 1 <= F.n_el) a.add(0.5 * rc);
+        const double v = a.result();
+        fc[n * nnc + I] = v;
+        if (xc0 != nullptr) xc0[n * nnc + I] = coarse_from_zero(C, n, I, v, omega);
+      }
+    } else if (own_g) {
+      if ((k & 1) == 0) {
+        r_even = r2;
+        if (n == nt) {  // last coarse level: truncated row, 0.5 * r(2N) only
+          Acc a;
+          a.add(0.5 * r2);
+          const double v = a.result();
+          fc[(n >> 1) * nnc + i] = v;
+          if (xc0 != nullptr) xc0[(n >> 1) * nnc + i] = coarse_from_zero(C, n >> 1, i, v, omega);
+        }
+      } else {
+        Acc a;
+        a.add(0.5 * r_even);
+        a.add(0.5 * r2);
+        const double v = a.result();
+        fc[(n >> 1) * nnc + i] = v;
+        if (xc0 != nullptr) xc0[(n >> 1) * nnc + i] = coarse_from_zero(C, n >> 1, i, v, omega);
+      }
+    }
+    am = bm;
+    ap = bp;
+  }
+  return acc;
+}
+
+// Resident 256-thread blocks per SM k_down is compiled for (it stages one
+// level more than the pair and holds both stages: fewer blocks, no spills).
+template <int NT>
+constexpr int down_minb() { return NT <= 2 ? 4 : NT <= 4 ? 3 : 2; }
+
+template <bool ADJ, int DIR, int NT, int MINB = down_minb<NT>()>
+__global__ void __launch_bounds__(kMaxTW, MINB) k_down(LevelView F, LevelView C, const double* __restrict__ f,
+                                                    const double* __restrict__ x, double* __restrict__ y,
+                                                    double* __restrict__ fc, double* __restrict__ xc0, double omega,
+                                                    double* __restrict__ partials) {
+  pdl_entry();
+  const int64_t tt = (int64_t)blockIdx.z * gridDim.y + blockIdx.y;  // time tile
+  double acc = 0.0;
+  if (tt < ceil_div(F.n_hi - F.n_lo, NT))
+    acc = dev_down<ADJ, DIR, NT>(F, C, f, x, y, fc, xc0, omega, blockIdx.x, tt);
+  const double s = block_sum(acc);
+  if (threadIdx.x == 0) partials[tt * gridDim.x + blockIdx.x] = s;
 }
 
 // Elementwise kernels on a level, 2-D grid (no 64-bit division): blockIdx.x =
@@ -1286,9 +1623,18 @@ void launch_pass(const LevelView& L, const Ld& ld, const double* f, double* y, d
     pdl_launch(k_lean2<ADJ, MODE, NORM, 8, 3, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
 }
 
+inline ZeroLoad zero_load(const LevelView& L, const double* f, double omega) {
+  return ZeroLoad{f, L.coef + kInvD * L.nn, L.inv_w, omega, L.nn};
+}
+
 template <bool ADJ>
 int sweep_impl(const LevelView& L, const double* f, const double* x, double* y, double omega,
                double* partials, cudaStream_t s) {
+  if (x == nullptr) {  // x = S(0), recomputed from f
+    if (y == nullptr || partials != nullptr) return static_cast<int>(cudaErrorInvalidValue);
+    launch_pass<ADJ, kSweep, false>(L, zero_load(L, f, omega), f, y, omega, partials, s);
+    return check_launch();
+  }
   const PlainLoad ld{x, L.nn};
   if (y != nullptr && partials != nullptr)
     launch_pass<ADJ, kSweep, true>(L, ld, f, y, omega, partials, s);
@@ -1302,26 +1648,42 @@ int sweep_impl(const LevelView& L, const double* f, const double* x, double* y, 
 template <bool ADJ, int DIR>
 int sweep_prolong_impl(const LevelView& L, const LevelView& C, const double* f, const double* x,
                        const double* xc, double* y, double omega, cudaStream_t s) {
-  const ProlongLoad<DIR> ld{x, xc, L.nn, C.nn};
-  launch_pass<ADJ, kSweep, false>(L, ld, f, y, omega, nullptr, s);
+  if (x == nullptr) {  // fine iterate S(0), recomputed from f
+    const ProlongZeroLoad<DIR> ld{zero_load(L, f, omega), xc, C.nn};
+    launch_pass<ADJ, kSweep, false>(L, ld, f, y, omega, nullptr, s);
+  } else {
+    const ProlongLoad<DIR> ld{x, xc, L.nn, C.nn};
+    launch_pass<ADJ, kSweep, false>(L, ld, f, y, omega, nullptr, s);
+  }
   return check_launch();
 }
 
-template <bool ADJ, int DIR>
-int restrict_impl(const LevelView& F, const LevelView& C, const double* f, const double* x,
-                  double* fc, cudaStream_t s, double* xc0, double omega) {
+template <bool ADJ, int DIR, bool ZX>
+void restrict_launch(const LevelView& F, const LevelView& C, const double* f, const double* x,
+                     double* fc, cudaStream_t s, double* xc0, double omega) {
   // DIR 0: warp w owns coarse nodes 14 w .. 14 w + 13; DIR 1: fine nodes 30 w ..
   const int64_t warps = DIR == 0 ? ceil_div(C.nn, 14) : ceil_div(F.nn, 30);
   const dim3 rb = balanced_block(warps, wpb_for(F));
   const int64_t tiles = ceil_div(warps, rb.x / 32);
   if (lean_nt(F) == 2 && F.nn * (F.n_t + 1) >= kMinB5Dofs)
-    pdl_launch(k_restrict2<ADJ, DIR, 2>, tgrid(tiles, (rows(F) + 1) / 2), rb, 0, s, F, C, f, x, fc, xc0, omega);
+    pdl_launch(k_restrict2<ADJ, DIR, 2, minb_for_nt<2>(), ZX>, tgrid(tiles, (rows(F) + 1) / 2), rb, 0, s, F, C,
+               f, x, fc, xc0, omega);
   else if (lean_nt(F) == 2)
-    pdl_launch(k_restrict2<ADJ, DIR, 2, 3>, tgrid(tiles, (rows(F) + 1) / 2), rb, 0, s, F, C, f, x, fc, xc0, omega);
+    pdl_launch(k_restrict2<ADJ, DIR, 2, 3, ZX>, tgrid(tiles, (rows(F) + 1) / 2), rb, 0, s, F, C, f, x, fc, xc0,
+               omega);
   else if (lean_nt(F) == 4)
-    pdl_launch(k_restrict2<ADJ, DIR, 4>, tgrid(tiles, (rows(F) + 3) / 4), rb, 0, s, F, C, f, x, fc, xc0, omega);
+    pdl_launch(k_restrict2<ADJ, DIR, 4, minb_for_nt<4>(), ZX>, tgrid(tiles, (rows(F) + 3) / 4), rb, 0, s, F, C,
+               f, x, fc, xc0, omega);
   else
-    pdl_launch(k_restrict2<ADJ, DIR, 8>, tgrid(tiles, (rows(F) + 7) / 8), rb, 0, s, F, C, f, x, fc, xc0, omega);
+    pdl_launch(k_restrict2<ADJ, DIR, 8, minb_for_nt<8>(), ZX>, tgrid(tiles, (rows(F) + 7) / 8), rb, 0, s, F, C,
+               f, x, fc, xc0, omega);
+}
+
+template <bool ADJ, int DIR>
+int restrict_impl(const LevelView& F, const LevelView& C, const double* f, const double* x,
+                  double* fc, cudaStream_t s, double* xc0, double omega) {
+  if (x == nullptr) restrict_launch<ADJ, DIR, true>(F, C, f, x, fc, s, xc0, omega);  // x = S(0) from f
+  else restrict_launch<ADJ, DIR, false>(F, C, f, x, fc, s, xc0, omega);
   return check_launch();
 }
 
@@ -1341,28 +1703,78 @@ int launch_sweep(bool adjoint, const LevelView& L, const double* f, const double
                  : sweep_impl<false>(L, f, x, y, omega, partials, s);
 }
 
-int launch_sweep2(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
-                  double omega, cudaStream_t s) {
+namespace {
+template <bool ADJ, bool ZX>
+void sweep2_launch(const LevelView& L, const double* f, const double* x, double* y, double omega, cudaStream_t s) {
   const int64_t warps = ceil_div(L.nn, 28);
   const dim3 blk = balanced_block(warps, wpb_for(L));
   const int64_t tiles = ceil_div(warps, blk.x / 32);
   if (lean_nt(L) == 2) {
     const dim3 grd = tgrid(tiles, (rows(L) + 1) / 2);
-    if (L.nn * (L.n_t + 1) >= kMinB5Dofs) {
-      if (adjoint) pdl_launch(k_lean2x2<true, 2>, grd, blk, 0, s, L, f, x, y, omega);
-      else pdl_launch(k_lean2x2<false, 2>, grd, blk, 0, s, L, f, x, y, omega);
-    } else {
-      if (adjoint) pdl_launch(k_lean2x2<true, 2, 3>, grd, blk, 0, s, L, f, x, y, omega);
-      else pdl_launch(k_lean2x2<false, 2, 3>, grd, blk, 0, s, L, f, x, y, omega);
-    }
+    if (L.nn * (L.n_t + 1) >= kMinB5Dofs)
+      pdl_launch(k_lean2x2<ADJ, 2, minb_for_nt<2>(), ZX>, grd, blk, 0, s, L, f, x, y, omega);
+    else
+      pdl_launch(k_lean2x2<ADJ, 2, 3, ZX>, grd, blk, 0, s, L, f, x, y, omega);
   } else if (lean_nt(L) == 4) {
-    const dim3 grd = tgrid(tiles, (rows(L) + 3) / 4);
-    if (adjoint) pdl_launch(k_lean2x2<true, 4>, grd, blk, 0, s, L, f, x, y, omega);
-    else pdl_launch(k_lean2x2<false, 4>, grd, blk, 0, s, L, f, x, y, omega);
+    pdl_launch(k_lean2x2<ADJ, 4, minb_for_nt<4>(), ZX>, tgrid(tiles, (rows(L) + 3) / 4), blk, 0, s, L, f, x, y,
+               omega);
   } else {
-    const dim3 grd = tgrid(tiles, (rows(L) + 7) / 8);
-    if (adjoint) pdl_launch(k_lean2x2<true, 8>, grd, blk, 0, s, L, f, x, y, omega);
-    else pdl_launch(k_lean2x2<false, 8>, grd, blk, 0, s, L, f, x, y, omega);
+    pdl_launch(k_lean2x2<ADJ, 8, minb_for_nt<8>(), ZX>, tgrid(tiles, (rows(L) + 7) / 8), blk, 0, s, L, f, x, y,
+               omega);
+  }
+}
+}  // namespace
+
+// x == nullptr: x is S(0), recomputed from f (the pair then applies sweeps 2 and 3 from zero)
+int launch_sweep2(bool adjoint, const LevelView& L, const double* f, const double* x, double* y,
+                  double omega, cudaStream_t s) {
+  if (adjoint) {
+    if (x == nullptr) sweep2_launch<true, true>(L, f, x, y, omega, s);
+    else sweep2_launch<true, false>(L, f, x, y, omega, s);
+  } else {
+    if (x == nullptr) sweep2_launch<false, true>(L, f, x, y, omega, s);
+    else sweep2_launch<false, false>(L, f, x, y, omega, s);
+  }
+  return check_launch();
+}
+
+namespace {
+template <bool ADJ, int DIR>
+void down_launch(const LevelView& F, const LevelView& C, const double* f, const double* x, double* y, double* fc,
+                 double* xc0, double omega, double* partials, cudaStream_t s) {
+  const int64_t warps = DIR == 0 ? ceil_div(C.nn, 13) : ceil_div(F.nn, 28);
+  const dim3 blk = balanced_block(warps, wpb_for(F));
+  const int64_t tiles = ceil_div(warps, blk.x / 32);
+  const int nt = lean_nt(F);
+  const dim3 grd = tgrid(tiles, (rows(F) + nt - 1) / nt);
+  if (nt == 2)
+    pdl_launch(k_down<ADJ, DIR, 2>, grd, blk, 0, s, F, C, f, x, y, fc, xc0, omega, partials);
+  else if (nt == 4)
+    pdl_launch(k_down<ADJ, DIR, 4>, grd, blk, 0, s, F, C, f, x, y, fc, xc0, omega, partials);
+  else
+    pdl_launch(k_down<ADJ, DIR, 8>, grd, blk, 0, s, F, C, f, x, y, fc, xc0, omega, partials);
+}
+}  // namespace
+
+int64_t down_partials_needed(const LevelView& F, const LevelView& C, int dir) {
+  const int64_t warps = dir == 0 ? ceil_div(C.nn, 13) : ceil_div(F.nn, 28);
+  const dim3 blk = balanced_block(warps, wpb_for(F));
+  const int64_t tiles = ceil_div(warps, blk.x / 32);
+  const dim3 grd = tgrid(tiles, (rows(F) + lean_nt(F) - 1) / lean_nt(F));
+  return (int64_t)grd.x * grd.y * grd.z;
+}
+
+int launch_down(bool adjoint, const LevelView& F, const LevelView& C, int dir, const double* f, const double* x,
+                double* y, double* fc, double* xc0, double omega, double* partials, int64_t* n_partials,
+                cudaStream_t s) {
+  if (F.tile_nt % 2 != 0 || (F.n_lo & 1) != 0) return static_cast<int>(cudaErrorInvalidValue);
+  if (n_partials) *n_partials = down_partials_needed(F, C, dir);
+  if (adjoint) {
+    if (dir == 0) down_launch<true, 0>(F, C, f, x, y, fc, xc0, omega, partials, s);
+    else down_launch<true, 1>(F, C, f, x, y, fc, xc0, omega, partials, s);
+  } else {
+    if (dir == 0) down_launch<false, 0>(F, C, f, x, y, fc, xc0, omega, partials, s);
+    else down_launch<false, 1>(F, C, f, x, y, fc, xc0, omega, partials, s);
   }
   return check_launch();
 }

@@ -81,6 +81,8 @@ def _load():
         "stmg_norm2": [vp, vp, i64, C.POINTER(f64)],
         "stmg_synchronize": [vp],
         "stmg_hierarchy_set_tiling": [vp, i64, i64],
+        "stmg_hierarchy_set_fusion": [vp, i32],
+        "stmg_level_fused": [vp, i32, i32, vp, vp, vp, vp, vp, f64, C.POINTER(f64)],
         "stmg_dist_partition": [i32, vp, vp, i32, i64, C.POINTER(i32), vp],
         "stmg_optimise": [vp, vp, i32, vp, vp, C.POINTER(i32), C.POINTER(f64), C.POINTER(i32),
                           C.POINTER(f64)],
@@ -168,7 +170,8 @@ class _SolveRep(C.Structure):
                 ("fine_sweep_seconds", C.c_double), ("fine_restricts", C.c_int64),
                 ("fine_restrict_seconds", C.c_double), ("fine_prolong_sweeps", C.c_int64),
                 ("fine_prolong_sweep_seconds", C.c_double), ("fine_sweep_pairs", C.c_int64),
-                ("fine_sweep_pair_seconds", C.c_double)]
+                ("fine_sweep_pair_seconds", C.c_double), ("fine_norm_passes", C.c_int64),
+                ("fine_norm_pass_seconds", C.c_double)]
 
 
 # ---- enums ---------------------------------------------------------------------------
@@ -283,7 +286,9 @@ def _f64(a, n: Optional[int] = None) -> np.ndarray:
 
 
 def _ptr(a) -> int:
-    """Data pointer of a float64 contiguous numpy array or torch tensor."""
+    """Data pointer of a float64 contiguous numpy array or torch tensor (None -> null)."""
+    if a is None:
+        return None
     if isinstance(a, np.ndarray):
         if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"]:
             raise ValueError("expected a C-contiguous float64 array")
@@ -558,6 +563,21 @@ class LevelHierarchy:
         """Per-handle time-tile thresholds (stmg_hierarchy_set_tiling; 0 = defaults)."""
         _check(_lib.stmg_hierarchy_set_tiling(self._h, int(small_dofs), int(tiny_dofs)))
 
+    FUSE_VIRTUAL_ZERO, FUSE_FINE_DOWN, FUSE_ALL, FUSE_DEFAULT = 1, 2, 3, 1
+
+    def set_fusion(self, flags=1):
+        """V-cycle fusions (stmg_hierarchy_set_fusion): bit-identical, traffic differs."""
+        _check(_lib.stmg_hierarchy_set_fusion(self._h, int(flags)))
+
+    FUSED_ZERO_SWEEP, FUSED_ZERO_PAIR, FUSED_ZERO_RESTRICT, FUSED_ZERO_PROLONG_SWEEP, FUSED_FINE_DOWN = range(5)
+
+    def fused_kernel(self, l, kind, f, x=None, xc=None, y=None, fc=None, omega=0.5):
+        """stmg_level_fused on device tensors; returns ||f - J x||^2 for FUSED_FINE_DOWN."""
+        nrm = C.c_double(0.0)
+        _check(_lib.stmg_level_fused(self._h, int(l), int(kind), _ptr(f), _ptr(x), _ptr(xc), _ptr(y), _ptr(fc),
+                                     float(omega), C.byref(nrm)))
+        return nrm.value
+
     def set_profiling(self, on=True):
         """True / 1: finest-level kernels; 2: every kernel (see stmg_b200.h)."""
         _check(_lib.stmg_hierarchy_set_profiling(self._h, int(on)))
@@ -653,7 +673,8 @@ def mg_solve(h: LevelHierarchy, b, u, opts: Optional[SolveOptions] = None) -> So
         kt = {"fine_sweep": (rep.fine_sweeps, rep.fine_sweep_seconds),
               "fine_sweep_pair": (rep.fine_sweep_pairs, rep.fine_sweep_pair_seconds),
               "fine_restrict": (rep.fine_restricts, rep.fine_restrict_seconds),
-              "fine_prolong_sweep": (rep.fine_prolong_sweeps, rep.fine_prolong_sweep_seconds)}
+              "fine_prolong_sweep": (rep.fine_prolong_sweeps, rep.fine_prolong_sweep_seconds),
+              "fine_norm_pass": (rep.fine_norm_passes, rep.fine_norm_pass_seconds)}
     return SolveReport(SolveStatus(rep.status), rep.cycles, rep.factor,
                        [float(v) for v in hist[: rep.n_history]], bool(rep.absolute_norms),
                        rep.seconds, rep.device_seconds, rep.smoother_dof_updates, rep.kernel_launches,
