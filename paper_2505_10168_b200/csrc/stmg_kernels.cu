@@ -1549,11 +1549,26 @@ __global__ void k_dot(const double* __restrict__ x, const double* __restrict__ y
   if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
 
+// Fixed-order sum of n block partials by one CTA: thread t adds entries t, t + B,
+// t + 2B, ... into four interleaved accumulators (four independent load / add
+// chains in flight), then ((a0 + a1) + (a2 + a3)) and the fixed block tree.
+__device__ __forceinline__ double partials_sum(const double* __restrict__ partials, int64_t n) {
+  const int64_t B = blockDim.x;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int64_t idx = threadIdx.x;
+  for (; idx + 3 * B < n; idx += 4 * B) {
+    a0 = a0 + partials[idx];
+    a1 = a1 + partials[idx + B];
+    a2 = a2 + partials[idx + 2 * B];
+    a3 = a3 + partials[idx + 3 * B];
+  }
+  for (; idx < n; idx += B) a0 = a0 + partials[idx];
+  return block_sum((a0 + a1) + (a2 + a3));
+}
+
 __global__ void k_finalize_sum(const double* __restrict__ partials, int64_t n, double* out) {
   pdl_entry();
-  double acc = 0.0;
-  for (int64_t idx = threadIdx.x; idx < n; idx += blockDim.x) acc = acc + partials[idx];
-  const double s = block_sum(acc);
+  const double s = partials_sum(partials, n);
   if (threadIdx.x == 0) *out = s;
 }
 
@@ -1562,9 +1577,7 @@ __global__ void k_finalize_sum(const double* __restrict__ partials, int64_t n, d
 __global__ void k_finalize_check(const double* __restrict__ partials, int64_t n, double* scalars,
                                  SolveLoopCtl* ctl, double* hist, cudaGraphConditionalHandle handle) {
   pdl_entry();
-  double acc = 0.0;
-  for (int64_t idx = threadIdx.x; idx < n; idx += blockDim.x) acc = acc + partials[idx];
-  const double s = block_sum(acc);
+  const double s = partials_sum(partials, n);
   if (threadIdx.x == 0) {
     scalars[1] = s;
     cycle_check_body(scalars[0], s, ctl, hist, handle);

@@ -1,33 +1,29 @@
 """Parity tolerances (BASELINE north_star: 1e-10 relative).
 
-Per-cycle residual norms are compared as |h_a - h_b| <= 1e-10 * h_b + tau with
-tau = 16 eps ||J||_inf ||u||_2 / ||b||_2: the fp64 rounding floor of evaluating
-b - J u in the reference's own arithmetic.  Two exact coarsest solvers (the
-reference's sparse LU and our PCR march) differ by ~1 ulp, which moves every
-later residual by about this floor; once h itself approaches the floor (the
-last cycles before 1e-10) only the absolute floor is meaningful.  Fields are
-compared as max|u_a - u_b| <= 1e-10 max|u_b|.
+Per-cycle relative residual norms are compared as |h_a - h_b| <= 1e-10 h_b +
+floor, with a fixed absolute floor (in units of ||b||):
+
+* HIST_ABS = 1e-13 on the small cases (<= 1.3e5 DOFs);
+* HIST_ABS_FULL = 1e-12 at BASELINE config 1's full size (4.2e6 DOFs).
+
+Two exact coarsest solvers (the reference's sparse LU and the oracle's Thomas
+march, or our parallel-in-time march) agree to ~1 ulp; that moves every later
+residual b - J u by its fp64 evaluation noise, which grows with the grid.  The
+floor is set from a measurement, not a bound: at full cfg1 size the C oracle and
+the compiled reference -- the same algorithm, two exact coarsest solvers -- differ
+by at most 4.4e-13 in any history entry (tests/test_gpu_scale.py re-measures it
+on every run), so 1e-12 is the smallest floor both independent CPU
+implementations pass.  Fields are compared as max|u_a - u_b| <= 1e-10 max|u_b|.
 """
 import numpy as np
 
-EPS = np.finfo(np.float64).eps
 HIST_REL = 1e-10
+HIST_ABS = 1e-13
+HIST_ABS_FULL = 1e-12
 FIELD_REL = 1e-10
 
 
-def j_inf_norm(coeffs: dict, w: float) -> float:
-    rows = sum(np.abs(coeffs[k]) for k in ("cur_m", "cur_0", "cur_p", "oth_m", "oth_0", "oth_p"))
-    return float(max(np.max(rows), abs(w)))
-
-
-def residual_floor(j_norm: float, u: np.ndarray, b: np.ndarray) -> float:
-    nb = float(np.linalg.norm(b))
-    if nb == 0.0:
-        return 16 * EPS * j_norm * float(np.linalg.norm(u))
-    return 16 * EPS * j_norm * float(np.linalg.norm(u)) / nb
-
-
-def histories_match(h_got, h_want, floor: float) -> bool:
+def histories_match(h_got, h_want, floor: float = HIST_ABS) -> bool:
     h_got = np.asarray(h_got, np.float64)
     h_want = np.asarray(h_want, np.float64)
     return h_got.shape == h_want.shape and bool(

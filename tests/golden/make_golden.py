@@ -99,11 +99,16 @@ def cfg1_adj_full(ref):
     lam, rep = h.solve(c, nu=cfg.nu, tol=cfg.tol, max_cycles=cfg.max_cycles)
     U = lam.reshape(cfg.n_t + 1, cfg.n_el + 1)
     return dict(history=rep.history, cycles=rep.cycles, status=rep.status, level_sums=U.sum(axis=1),
-                u_max=np.abs(lam).max(), dirs=np.asarray(dirs, np.int32), ref_seconds=rep.seconds)
+                level_max=np.abs(U).max(axis=1), node_sums=U.sum(axis=0), u_max=np.abs(lam).max(),
+                dirs=np.asarray(dirs, np.int32), ref_seconds=rep.seconds)
 
 
 def main():
     ref, port = Ref(), Port()
+    if "--adj-only" in sys.argv:  # only the adjoint full-size fixture
+        np.savez_compressed(os.path.join(HERE, "cfg1_adj_full.npz"), **cfg1_adj_full(ref))
+        print("wrote cfg1_adj_full")
+        return
     np.savez_compressed(os.path.join(HERE, "opt_small.npz"), **opt_small(ref))
     with open(os.path.join(HERE, "plans.json"), "w") as fh:
         json.dump(plans(ref), fh, indent=1)

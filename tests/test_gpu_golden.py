@@ -39,15 +39,16 @@ def test_gpu_matches_reference_golden(S, port, name):
     b = cs.rhs_vector(port)
     u = np.zeros_like(b)
     rep = S.mg_solve(h, b, u, S.SolveOptions(nu=cs.nu, tol=cs.tol, max_cycles=cs.max_cycles))
-    from tests._tol import j_inf_norm, residual_floor
+    from tests._tol import HIST_ABS
 
-    floor = residual_floor(j_inf_norm(h.level_coeffs(0), h.levels[0].w_diri), u, b)
-    check_against_gold(gold, u, rep.cycles, int(rep.status), rep.history, cs, floor)
+    check_against_gold(gold, u, rep.cycles, int(rep.status), rep.history, cs, HIST_ABS)
 
 
 def test_cfg1_full_size_matches_reference(S):
     """BASELINE config 1 (1024 x 4096, 4.2 M DOFs): same V-cycle count, history
-    within 1e-10 (+1e-13 floor), per-time-level sums of u within 1e-10."""
+    within 1e-10 relative + 1e-12 (tests/_tol.py: the oracle-vs-reference spread at
+    this size is 4.4e-13), per-time-level sums, maxima and per-node sums of u
+    within 1e-10 (the full field against the oracle: tests/test_gpu_scale.py)."""
     path = os.path.join(GOLD, "cfg1_full.npz")
     if not os.path.exists(path):
         pytest.skip("cfg1_full fixture not generated")
@@ -64,14 +65,14 @@ def test_cfg1_full_size_matches_reference(S):
     u = torch.zeros_like(b)
     rep = S.mg_solve(h, b, u, S.SolveOptions(nu=cfg.nu, tol=cfg.tol, max_cycles=cfg.max_cycles))
     assert rep.cycles == int(gold["cycles"]) and int(rep.status) == int(gold["status"])
-    from tests._tol import histories_match, j_inf_norm, residual_floor
+    from tests._tol import HIST_ABS_FULL, histories_match
 
     un = u.cpu().numpy()
-    floor = residual_floor(j_inf_norm(h.level_coeffs(0), h.levels[0].w_diri), un, b.cpu().numpy())
-    assert histories_match(rep.history, gold["history"], floor), floor
+    assert histories_match(rep.history, gold["history"], HIST_ABS_FULL)
     U = un.reshape(cfg.n_t + 1, cfg.n_el + 1)
-    scale = np.max(np.abs(gold["level_sums"]))
-    assert np.max(np.abs(U.sum(axis=1) - gold["level_sums"])) <= 1e-10 * scale
+    for key, got in (("level_sums", U.sum(axis=1)), ("level_max", np.abs(U).max(axis=1)),
+                     ("node_sums", U.sum(axis=0))):
+        assert np.max(np.abs(got - gold[key])) <= 1e-10 * np.max(np.abs(gold[key])), key
     assert abs(np.abs(U).max() - float(gold["u_max"])) <= 1e-10 * float(gold["u_max"])
 
 
@@ -152,7 +153,7 @@ def test_cfg1_adjoint_full_size_matches_reference(S):
     import torch
 
     from paper_2505_10168_b200 import configs as C
-    from tests._tol import histories_match, j_inf_norm, residual_floor
+    from tests._tol import HIST_ABS_FULL, histories_match
 
     gold = dict(np.load(path))
     cfg = C.cfg1()
@@ -165,7 +166,10 @@ def test_cfg1_adjoint_full_size_matches_reference(S):
     rep = S.mg_solve(h, c, lam, S.SolveOptions(nu=cfg.nu, tol=cfg.tol, max_cycles=cfg.max_cycles))
     assert rep.cycles == int(gold["cycles"]) and int(rep.status) == int(gold["status"])
     ln = lam.cpu().numpy()
-    floor = residual_floor(j_inf_norm(h.level_coeffs(0), h.levels[0].w_diri), ln, c.cpu().numpy())
-    assert histories_match(rep.history, gold["history"], floor)
+    assert histories_match(rep.history, gold["history"], HIST_ABS_FULL)
     U = ln.reshape(cfg.n_t + 1, cfg.n_el + 1)
-    assert np.max(np.abs(U.sum(axis=1) - gold["level_sums"])) <= 1e-10 * np.max(np.abs(gold["level_sums"]))
+    keys = [("level_sums", U.sum(axis=1))]
+    if "level_max" in gold:
+        keys += [("level_max", np.abs(U).max(axis=1)), ("node_sums", U.sum(axis=0))]
+    for key, got in keys:
+        assert np.max(np.abs(got - gold[key])) <= 1e-10 * np.max(np.abs(gold[key])), key
