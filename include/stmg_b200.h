@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define STMG_ABI_VERSION 1
+#define STMG_ABI_VERSION 2
 
 enum stmg_status_code {
   STMG_OK = 0,
@@ -304,19 +304,31 @@ typedef struct stmg_optimise_options {
   double mma_x_min, mma_x_max, mma_move_limit, mma_asym_init, mma_asym_shrink, mma_asym_grow;
 } stmg_optimise_options;
 
-/* IterationRecord, proj/include/stmg/optimisation.hpp:77-92 (path as dirs). */
+/* IterationRecord, proj/include/stmg/optimisation.hpp:77-92.  path: the coarsening
+ * path used this iteration as path_to_string writes it (proj/src/strategy.cpp:118-125,
+ * "x,t,..."), NUL-terminated (up to 32 directions). */
 typedef struct stmg_iteration_record {
   int32_t iteration;
   double theta, volume, constraint, change;
   int32_t primal_status, adjoint_status, primal_cycles, adjoint_cycles;
   double primal_factor, adjoint_factor, primal_seconds, adjoint_seconds;
+  char path[96];
 } stmg_iteration_record;
 
 /* Fills chi_out (n_el, the final post-update design), records (max_iterations),
- * and the scalars; returns STMG_OK or an error code. */
+ * and the scalars; design_history (may be NULL; max_iterations x n_el doubles):
+ * row i = the design evaluated at iteration i + 1 (OptimisationResult::design_history,
+ * proj/include/stmg/optimisation.hpp:100-102).  Returns STMG_OK or an error code. */
 int stmg_optimise(const stmg_grid* geom, const stmg_optimise_options* opts, int32_t device,
                   double* chi_out, stmg_iteration_record* records, int32_t* n_records,
-                  double* theta, int32_t* converged, double* seconds);
+                  double* theta, int32_t* converged, double* seconds, double* design_history);
+
+/* objective_sensitivities, proj/src/optimisation.cpp:34-73: d theta / d chi_e (before
+ * the dt / theta_ref scaling of optimise) for states u and lambda ((n_t+1)(n_el+1)
+ * doubles each, host or device), on `device`; bitwise the reference's arithmetic.
+ * sens: host array of n_el. */
+int stmg_objective_sensitivities(const stmg_grid* geom, const stmg_material_pair* mat, const double* chi,
+                                 const double* u, const double* lam, double* sens, int32_t device);
 
 /* ---- time-slab multi-GPU ------------------------------------
  * A distributed hierarchy splits the time axis of every level that can be cut

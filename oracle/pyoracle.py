@@ -3,6 +3,12 @@
 * ``Port``: oracle/liboracle_port.so, the plain-C restatement (stmg_oracle.c).
 * ``Ref``:  oracle/_ref/libstmg_ref.so, the UNMODIFIED reference compiled from
   /root/reference/proj (see oracle/Makefile) behind oracle/ref_harness.cpp.
+  ``Ref(dropin=True)`` loads oracle/_ref/libstmg_dropin.so instead: the same
+  reference objects and harness with multigrid.o replaced by the B200 drop-in
+  (paper_2505_10168_b200/dropin/multigrid_b200.cpp), i.e. the reference's own
+  callers (optimise(), mg_solve) running on libstmg_b200.so.  Only the harness
+  entry points that go through build_hierarchy / transposed_hierarchy / mg_solve /
+  optimise are meaningful there (no host CSR operators exist in the drop-in).
 
 Only tests/, ``__graft_entry__.smoke()`` and ``bench.py`` (cpu_baseline and
 ``--impl reference``) may import this module.  The product path never does.
@@ -19,6 +25,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 PORT_SO = os.path.join(HERE, "liboracle_port.so")
 REF_SO = os.path.join(HERE, "_ref", "libstmg_ref.so")
+DROPIN_SO = os.path.join(HERE, "_ref", "libstmg_dropin.so")
 REF_SRC = "/root/reference/proj"
 
 _dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
@@ -34,10 +41,17 @@ def build_port() -> str:
 
 
 def build_ref() -> str | None:
-    """Compile the reference in place (only possible where /root/reference exists)."""
+    """Compile the reference in place (only possible where /root/reference exists),
+    and the drop-in library over it when libstmg_b200.so is built."""
     if os.path.isdir(REF_SRC):
         subprocess.check_call(["make", "-s", "-j8", "-C", HERE, "ref"])
+        if os.path.exists(os.path.join(os.path.dirname(HERE), "paper_2505_10168_b200", "libstmg_b200.so")):
+            subprocess.check_call(["make", "-s", "-C", HERE, "dropin"])
     return REF_SO if os.path.exists(REF_SO) else None
+
+
+def dropin_available() -> bool:
+    return os.path.exists(DROPIN_SO)
 
 
 def ref_available() -> bool:
@@ -208,12 +222,13 @@ class PortHier:
 
 
 class Ref:
-    """The unmodified reference (requires oracle/_ref/libstmg_ref.so)."""
+    """The unmodified reference (requires oracle/_ref/libstmg_ref.so); dropin=True:
+    the reference's callers over the B200 drop-in (oracle/_ref/libstmg_dropin.so)."""
 
-    def __init__(self):
+    def __init__(self, dropin: bool = False):
         if not ref_available():
             build_ref()
-        lib = C.CDLL(REF_SO)
+        lib = C.CDLL(DROPIN_SO if dropin else REF_SO)
         f64, i32 = C.c_double, C.c_int
         lib.ref_last_error.restype = C.c_char_p
         lib.ref_plan.argtypes = [f64, f64, i32, i32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

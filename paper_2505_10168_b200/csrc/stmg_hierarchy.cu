@@ -1646,9 +1646,23 @@ struct Mma {
 
 // optimise, proj/src/optimisation.cpp:83-186 (host loop; solves, objective and
 // sensitivities on the GPU)
+// Per-element scales of objective_sensitivities (proj/src/optimisation.cpp:54-56):
+// dk_dx = k'(chi) / dx, dc_dx6 = c'(chi) dx / 6, with simp_derivatives'
+// expressions (proj/src/materials.cpp).
+void sensitivity_scales(const double* chi, int64_t ne, const stmg_material_pair& m, double dx, double* dk,
+                        double* dc) {
+  for (int64_t e = 0; e < ne; ++e) {
+    if (!(chi[e] >= 0.0 && chi[e] <= 1.0)) throw std::invalid_argument("volume fraction outside [0, 1]");
+    const double dkv = m.p_k * (m.k_con - m.k_ins) * std::pow(chi[e], m.p_k - 1.0);
+    const double dcv = m.p_c * (m.c_con - m.c_ins) * std::pow(chi[e], m.p_c - 1.0);
+    dk[e] = dkv / dx;
+    dc[e] = dcv * dx / 6;
+  }
+}
+
 void optimise(const stmg_grid* geom, const stmg_optimise_options& o, int device, double* chi_out,
               stmg_iteration_record* recs, int32_t* n_records, double* theta_out, int32_t* converged,
-              double* seconds) {
+              double* seconds, double* design_history) {
   if (o.volume_limit <= 0.0 || o.volume_limit > 1.0)
     throw std::invalid_argument("optimise: volume limit must be in (0, 1]");
   if (o.max_iterations < 1 || o.stable_iterations < 1 || o.rel_change_tol <= 0.0 || o.theta_ref <= 0.0)
@@ -1762,6 +1776,18 @@ void optimise(const stmg_grid* geom, const stmg_optimise_options& o, int device,
     r.adjoint_factor = ar.factor;
     r.primal_seconds = pr.seconds;
     r.adjoint_seconds = ar.seconds;
+    {  // path_to_string (proj/src/strategy.cpp:118-125)
+      std::string ps;
+      for (size_t i = 0; i < dirs.size(); ++i) {
+        if (i) ps += ',';
+        ps += dirs[i] == STMG_DIR_X ? "x" : dirs[i] == STMG_DIR_T ? "t" : "xt";
+      }
+      const size_t m = std::min(ps.size(), sizeof(r.path) - 1);
+      std::memcpy(r.path, ps.data(), m);
+      r.path[m] = '\0';
+    }
+    if (design_history)  // the design this iteration evaluated
+      std::memcpy(design_history + static_cast<size_t>(it - 1) * ne, chi.data(), sizeof(double) * ne);
     *n_records = it;
     *theta_out = theta;
     theta_prev = theta;
@@ -1773,13 +1799,7 @@ void optimise(const stmg_grid* geom, const stmg_optimise_options& o, int device,
     if (it == o.max_iterations) break;
     // objective_sensitivities (optimisation.cpp:34-73) on the GPU
     std::vector<double> dk(ne), dc(ne), sens(ne);
-    for (int64_t e = 0; e < ne; ++e) {
-      if (!(chi[e] >= 0.0 && chi[e] <= 1.0)) throw std::invalid_argument("volume fraction outside [0, 1]");
-      const double dkv = o.mat.p_k * (o.mat.k_con - o.mat.k_ins) * std::pow(chi[e], o.mat.p_k - 1.0);
-      const double dcv = o.mat.p_c * (o.mat.c_con - o.mat.c_ins) * std::pow(chi[e], o.mat.p_c - 1.0);
-      dk[e] = dkv / g.dx;
-      dc[e] = dcv * g.dx / 6;
-    }
+    sensitivity_scales(chi.data(), ne, o.mat, g.dx, dk.data(), dc.data());
     cuda_check(cudaMemcpyAsync(d_dk.p, dk.data(), ne * 8, cudaMemcpyHostToDevice, h->stream), "h2d");
     cuda_check(cudaMemcpyAsync(d_dc.p, dc.data(), ne * 8, cudaMemcpyHostToDevice, h->stream), "h2d");
     launch_check(launch_sensitivities(ne, g.n_t, g.dt, d_dk.p, d_dc.p, d_u.p, d_lam.p, d_sens.p, h->stream),
@@ -2326,11 +2346,43 @@ int stmg_norm2(stmg_hierarchy* h, const double* x, int64_t n, double* norm) {
 
 int stmg_optimise(const stmg_grid* geom, const stmg_optimise_options* opts, int32_t device,
                   double* chi_out, stmg_iteration_record* records, int32_t* n_records, double* theta,
-                  int32_t* converged, double* seconds) {
+                  int32_t* converged, double* seconds, double* design_history) {
   return guarded([&] {
     if (!geom || !opts || !chi_out || !records || !n_records || !theta || !converged || !seconds)
       throw std::invalid_argument("optimise: null argument");
-    optimise(geom, *opts, device, chi_out, records, n_records, theta, converged, seconds);
+    optimise(geom, *opts, device, chi_out, records, n_records, theta, converged, seconds, design_history);
+  });
+}
+
+// objective_sensitivities, proj/src/optimisation.cpp:34-73 (u, lambda host or device)
+int stmg_objective_sensitivities(const stmg_grid* geom, const stmg_material_pair* mat, const double* chi,
+                                 const double* u, const double* lam, double* sens, int32_t device) {
+  return guarded([&] {
+    if (!geom || !mat || !chi || !u || !lam || !sens) throw std::invalid_argument("objective_sensitivities: null argument");
+    const HostGrid g = make_grid(geom->L, geom->t_T, geom->n_el, geom->n_t);
+    const int64_t ne = g.n_el, ndof = (ne + 1) * (g.n_t + 1);
+    std::vector<double> dk(ne), dc(ne);
+    sensitivity_scales(chi, ne, *mat, g.dx, dk.data(), dc.data());
+    DeviceGuard dgd(device);
+    DeviceBuf d_dk(ne), d_dc(ne), d_sens(ne);
+    std::unique_ptr<DeviceBuf> du, dl;
+    const double* pu = u;
+    const double* pl = lam;
+    if (!is_device_ptr(u)) {
+      du = std::make_unique<DeviceBuf>(ndof);
+      cuda_check(cudaMemcpy(du->p, u, ndof * 8, cudaMemcpyHostToDevice), "h2d");
+      pu = du->p;
+    }
+    if (!is_device_ptr(lam)) {
+      dl = std::make_unique<DeviceBuf>(ndof);
+      cuda_check(cudaMemcpy(dl->p, lam, ndof * 8, cudaMemcpyHostToDevice), "h2d");
+      pl = dl->p;
+    }
+    cuda_check(cudaMemcpy(d_dk.p, dk.data(), ne * 8, cudaMemcpyHostToDevice), "h2d");
+    cuda_check(cudaMemcpy(d_dc.p, dc.data(), ne * 8, cudaMemcpyHostToDevice), "h2d");
+    launch_check(kernels_init(), "kernels_init");
+    launch_check(launch_sensitivities(ne, g.n_t, g.dt, d_dk.p, d_dc.p, pu, pl, d_sens.p, nullptr), "sensitivities");
+    cuda_check(cudaMemcpy(sens, d_sens.p, ne * 8, cudaMemcpyDeviceToHost), "d2h");
   });
 }
 

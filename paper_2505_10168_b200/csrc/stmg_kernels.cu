@@ -1311,48 +1311,70 @@ __global__ void k_square(const double* __restrict__ A, double* __restrict__ C, i
 }
 
 // Adjoint sensitivities of the heat-compliance objective
-// (objective_sensitivities, proj/src/optimisation.cpp:34-73): one thread per
-// element, time levels accumulated in the reference's order, masked DOFs read
-// as zero, so the result is the reference's bit for bit for the same u, lambda.
-// The loads of kSensBatch levels are issued before their (sequential)
-// accumulation, so the few element threads keep many loads in flight.
-constexpr int kSensBatch = 16;
-__global__ void k_sensitivities(int64_t n_el, int64_t n_t, double dt, const double* __restrict__ dk_dx,
-                                const double* __restrict__ dc_dx6, const double* __restrict__ u,
-                                const double* __restrict__ lam, double* __restrict__ sens) {
+// (objective_sensitivities, proj/src/optimisation.cpp:34-73), bit for bit: per
+// element e the terms of time level n,
+//   t_n = (dk_dx (u0 - u1)) (l0 - l1),   s_n = dc_dx6 (l0 (2 v0 + v1) + l1 (v0 + 2 v1)),
+// v = (u_n - u_{n-1}) / dt, masked DOFs (n == 0, node 0) read as zero, are
+// accumulated in the reference's order acc = ((acc + t_1) + s_1) + t_2 + ....
+// The terms are independent, the sums are a chain, so a block owns 32 elements
+// (one per lane) and kSensWarps warps: every warp computes the terms of
+// kSensLv consecutive levels from coalesced row loads (u and lambda at nodes e
+// and e + 1, the previous level's u kept in registers) into shared memory, then
+// warp 0 adds the tile's terms in level order.  ceil(n_el / 32) blocks stream
+// u and lambda once (config 4: 128 blocks x 16 warps over 1.07 GB).
+constexpr int kSensWarps = 16, kSensLv = 4, kSensTile = kSensWarps * kSensLv;
+__global__ void __launch_bounds__(kSensWarps * 32) k_sensitivities(
+    int64_t n_el, int64_t n_t, double dt, const double* __restrict__ dk_dx, const double* __restrict__ dc_dx6,
+    const double* __restrict__ u, const double* __restrict__ lam, double* __restrict__ sens) {
   pdl_entry();
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n_el) return;
+  __shared__ double terms[2][kSensTile][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t e = (int64_t)blockIdx.x * 32 + lane;
+  const bool active = e < n_el;
+  const bool lm = e == 0;  // node i = e is the Dirichlet node
   const int64_t nn = n_el + 1;
-  const double kd = dk_dx[e], cd = dc_dx6[e];
-  const bool left_masked = e == 0;  // node i = e is the Dirichlet node
+  const double kd = active ? dk_dx[e] : 0.0, cd = active ? dc_dx6[e] : 0.0;
   double acc = 0.0;
-  double p0 = 0.0, p1 = 0.0;  // u at level n - 1 (level 0 is masked)
-  for (int64_t n0 = 1; n0 <= n_t; n0 += kSensBatch) {
-    double U0[kSensBatch], U1[kSensBatch], L0[kSensBatch], L1[kSensBatch];
+  for (int64_t base = 1; base <= n_t; base += kSensTile) {
+    const int64_t n0 = base + (int64_t)warp * kSensLv;
+    double U0[kSensLv], U1[kSensLv], L0[kSensLv], L1[kSensLv], P0 = 0.0, P1 = 0.0;
+    if (active && n0 <= n_t) {
+      if (n0 - 1 >= 1) {  // level n0 - 1 (level 0 is masked)
+        const int64_t r = (n0 - 1) * nn + e;
+        P0 = lm ? 0.0 : __ldg(u + r);
+        P1 = __ldg(u + r + 1);
+      }
 #pragma unroll
-    for (int k = 0; k < kSensBatch; ++k) {
-      const int64_t n = n0 + k;
-      const bool ok = n <= n_t;
-      const int64_t r = (ok ? n : n_t) * nn + e;
-      U0[k] = ok && !left_masked ? u[r] : 0.0;
-      U1[k] = ok ? u[r + 1] : 0.0;
-      L0[k] = ok && !left_masked ? lam[r] : 0.0;
-      L1[k] = ok ? lam[r + 1] : 0.0;
-    }
+      for (int k = 0; k < kSensLv; ++k) {
+        const int64_t n = n0 + k <= n_t ? n0 + k : n_t;
+        const int64_t r = n * nn + e;
+        U0[k] = lm ? 0.0 : __ldg(u + r);
+        U1[k] = __ldg(u + r + 1);
+        L0[k] = lm ? 0.0 : __ldg(lam + r);
+        L1[k] = __ldg(lam + r + 1);
+      }
 #pragma unroll
-    for (int k = 0; k < kSensBatch; ++k) {
-      if (n0 + k > n_t) break;
-      const double u0 = U0[k], u1 = U1[k], l0 = L0[k], l1 = L1[k];
-      acc = acc + (kd * (u0 - u1)) * (l0 - l1);
-      const double v0 = (u0 - p0) / dt;
-      const double v1 = (u1 - p1) / dt;
-      acc = acc + cd * (l0 * (2.0 * v0 + v1) + l1 * (v0 + 2.0 * v1));
-      p0 = u0;
-      p1 = u1;
+      for (int k = 0; k < kSensLv; ++k) {
+        const double u0 = U0[k], u1 = U1[k], l0 = L0[k], l1 = L1[k];
+        const double v0 = (u0 - P0) / dt;
+        const double v1 = (u1 - P1) / dt;
+        terms[0][warp * kSensLv + k][lane] = (kd * (u0 - u1)) * (l0 - l1);
+        terms[1][warp * kSensLv + k][lane] = cd * (l0 * (2.0 * v0 + v1) + l1 * (v0 + 2.0 * v1));
+        P0 = u0;
+        P1 = u1;
+      }
     }
+    __syncthreads();
+    if (warp == 0 && active) {
+      const int cnt = n_t - base + 1 < kSensTile ? (int)(n_t - base + 1) : kSensTile;
+      for (int j = 0; j < cnt; ++j) {
+        acc = acc + terms[0][j][lane];
+        acc = acc + terms[1][j][lane];
+      }
+    }
+    __syncthreads();
   }
-  sens[e] = -acc;
+  if (warp == 0 && active) sens[e] = -acc;
 }
 
 __global__ void k_dot(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
@@ -1951,8 +1973,9 @@ int launch_finalize_check(const double* partials, int64_t n, double* scalars, So
 int launch_sensitivities(int64_t n_el, int64_t n_t, double dt, const double* dk_dx,
                          const double* dc_dx6, const double* u, const double* lam, double* sens,
                          cudaStream_t s) {
-  // 32-thread blocks spread the n_el element threads over every SM
-  pdl_launch(k_sensitivities, (unsigned)((n_el + 31) / 32), 32, 0, s, n_el, n_t, dt, dk_dx, dc_dx6, u, lam, sens);
+  // one block of kSensWarps warps per 32 elements
+  pdl_launch(k_sensitivities, (unsigned)((n_el + 31) / 32), kSensWarps * 32, 0, s, n_el, n_t, dt, dk_dx, dc_dx6, u,
+             lam, sens);
   return check_launch();
 }
 

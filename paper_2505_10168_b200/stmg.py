@@ -85,7 +85,7 @@ def _load():
         "stmg_level_fused": [vp, i32, i32, vp, vp, vp, vp, vp, f64, C.POINTER(f64)],
         "stmg_dist_partition": [i32, vp, vp, i32, i64, C.POINTER(i32), vp],
         "stmg_optimise": [vp, vp, i32, vp, vp, C.POINTER(i32), C.POINTER(f64), C.POINTER(i32),
-                          C.POINTER(f64)],
+                          C.POINTER(f64), vp],
         "stmg_dist_nccl_unique_id": [vp, i32],
         "stmg_dist_create": [vp, vp, vp, vp, vp, C.c_char_p, i32, vp, i32, i32, i32, vp, i32, i64,
                              C.POINTER(vp)],
@@ -159,7 +159,7 @@ class _IterRec(C.Structure):
                 ("constraint", C.c_double), ("change", C.c_double), ("primal_status", C.c_int32),
                 ("adjoint_status", C.c_int32), ("primal_cycles", C.c_int32), ("adjoint_cycles", C.c_int32),
                 ("primal_factor", C.c_double), ("adjoint_factor", C.c_double),
-                ("primal_seconds", C.c_double), ("adjoint_seconds", C.c_double)]
+                ("primal_seconds", C.c_double), ("adjoint_seconds", C.c_double), ("path", C.c_char * 96)]
 
 
 class _SolveRep(C.Structure):
@@ -744,6 +744,7 @@ class OptimisationResult:
     iterations: int
     history: list
     seconds: float
+    design_history: Optional[np.ndarray] = None  # row i: the design evaluated at iteration i + 1
 
 
 def optimise(geom: SpaceTimeGrid, mat, opts: Optional[OptimisationOptions] = None,
@@ -759,13 +760,19 @@ def optimise(geom: SpaceTimeGrid, mat, opts: Optional[OptimisationOptions] = Non
                   o.mma_asym_grow)
     chi = np.zeros(geom.n_el)
     recs = (_IterRec * int(o.max_iterations))()
+    designs = np.zeros((int(o.max_iterations), geom.n_el))
     nr, conv = C.c_int32(), C.c_int32()
     th, secs = C.c_double(), C.c_double()
     gc = geom._c()
     _check(_lib.stmg_optimise(C.byref(gc), C.byref(co), int(device), chi.ctypes.data, recs, C.byref(nr),
-                              C.byref(th), C.byref(conv), C.byref(secs)))
-    hist = [{f: getattr(recs[i], f) for f, _ in _IterRec._fields_} for i in range(nr.value)]
-    return OptimisationResult(chi, th.value, bool(conv.value), nr.value, hist, secs.value)
+                              C.byref(th), C.byref(conv), C.byref(secs), designs.ctypes.data))
+    hist = []
+    for i in range(nr.value):
+        d = {f: getattr(recs[i], f) for f, _ in _IterRec._fields_}
+        d["path"] = d["path"].decode()
+        hist.append(d)
+    return OptimisationResult(chi, th.value, bool(conv.value), nr.value, hist, secs.value,
+                              designs[: nr.value].copy())
 
 
 # ---- time-slab multi-GPU ------------------------------------------
