@@ -501,6 +501,7 @@ def main():
     if args.impl == "reference":
         return reference_arm(args)
 
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -545,8 +546,11 @@ def main():
             h = S.transposed_hierarchy(h)
     t_build = time.perf_counter() - t_build
     b_host = rhs_for(cfg, S, g)
-    n = b_host.size
     n0 = (cfg.n_el + 1) * (cfg.n_t + 1)
+    if dh is not None:  # slab-local vectors: this process's level-0 rows only (memory ~ 1/W)
+        nn_ = cfg.n_el + 1
+        b_host = np.ascontiguousarray(b_host[dh.row_lo * nn_: dh.row_hi * nn_])
+    n = b_host.size
     stream = torch.cuda.Stream(device=dev)
     if h is not None:
         h.set_stream(stream)
@@ -562,7 +566,7 @@ def main():
     def solve_on(bv, uv):
         if dh is not None:
             stream.synchronize()
-            return S.mg_solve_dist(dh, bv, uv, opts)
+            return S.mg_solve_dist_local(dh, bv, uv, opts)
         return S.mg_solve(h, bv, uv, opts)
 
     def timed_solves(count):
@@ -649,8 +653,13 @@ def main():
             uu = torch.tensor([tot_upd], dtype=torch.float64, device=dev)
             dist.all_reduce(uu, op=dist.ReduceOp.SUM)
             tot_upd = float(uu.item())
-        e2e = {"value": tot_upd / (tot_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 16 * n,
-               "d2h_bytes_per_step": 8 * n, "solve_seconds": tot_ms * 1e-3 / args.e2e_steps}
+        nbytes = n
+        if world > 1:  # every rank copies its own slab rows
+            nb = torch.tensor([float(n)], dtype=torch.float64, device=dev)
+            dist.all_reduce(nb, op=dist.ReduceOp.SUM)
+            nbytes = int(nb.item())
+        e2e = {"value": tot_upd / (tot_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 16 * nbytes,
+               "d2h_bytes_per_step": 8 * nbytes, "solve_seconds": tot_ms * 1e-3 / args.e2e_steps}
 
     cpu = None
     cfg1 = None

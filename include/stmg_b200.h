@@ -357,6 +357,12 @@ int stmg_dist_info(const stmg_dist* d, int32_t* n_distributed, int64_t* row_lo, 
                    int32_t* n_local, int64_t* device_bytes);
 int stmg_dist_mg_solve(stmg_dist* d, const double* b, double* u, const stmg_solve_options* opts,
                        stmg_solve_report* report, double* history, int32_t history_cap);
+/* The same solve with slab-local vectors: b_local and u_local hold only this
+ * process's rows [row_lo, row_hi) of level 0 (stmg_dist_info), (row_hi - row_lo) *
+ * (n_el + 1) doubles each, so the caller's memory scales as 1/W like the
+ * hierarchy's; ghost rows are exchanged by the library. */
+int stmg_dist_mg_solve_local(stmg_dist* d, const double* b_local, double* u_local, const stmg_solve_options* opts,
+                             stmg_solve_report* report, double* history, int32_t history_cap);
 int stmg_dist_transport(const stmg_dist* d, char* name_out, int32_t cap);
 void stmg_dist_destroy(stmg_dist* d);
 

@@ -96,6 +96,7 @@ class Port:
         lib.or_coarsest_solve.argtypes = [C.c_void_p, _dp, _dp]
         lib.or_norm2.argtypes = [_dp, i64]
         lib.or_norm2.restype = f64
+        lib.or_set_norm_mode.argtypes = [i32]
         lib.or_mg_solve.argtypes = [C.c_void_p, _dp, _dp, i32, f64, f64, f64, i32, C.POINTER(i32),
                                     C.POINTER(i32), C.POINTER(f64), C.POINTER(i32), _dp, C.POINTER(i64)]
         lib.or_apply_design.argtypes = [_dp, i64, C.c_void_p, _dp, _dp]
@@ -146,6 +147,10 @@ class Port:
 
     def norm2(self, x):
         return self.lib.or_norm2(np.ascontiguousarray(x, np.float64), x.size)
+
+    def set_norm_mode(self, pairwise: bool):
+        """Residual norms of solve(): the reference's 4-lane order (False) or pairwise (True)."""
+        self.lib.or_set_norm_mode(1 if pairwise else 0)
 
 
 class PortHier:
@@ -253,6 +258,7 @@ class Ref:
                                      C.POINTER(i32), C.POINTER(f64)]
         lib.ref_load_vector.argtypes = [f64, f64, i32, i32, i32, _dp, i32, _dp]
         lib.ref_apply_design.argtypes = [_dp, i32, _dp, _dp, _dp]
+        lib.ref_objective_sensitivities.argtypes = [f64, f64, i32, i32, _dp, _dp, _dp, _dp, _dp]
         lib.ref_norm2.argtypes = [_dp, C.c_longlong]
         lib.ref_norm2.restype = f64
         lib.ref_set_backend.argtypes = [i32]
@@ -301,6 +307,14 @@ class Ref:
 
     def norm2(self, x):
         return self.lib.ref_norm2(np.ascontiguousarray(x, np.float64), x.size)
+
+    def objective_sensitivities(self, L, tT, n_el, n_t, mat, chi, u, lam):
+        sens = np.empty(n_el)
+        self._chk(self.lib.ref_objective_sensitivities(L, tT, n_el, n_t, np.ascontiguousarray(mat, np.float64),
+                                                       np.ascontiguousarray(chi, np.float64),
+                                                       np.ascontiguousarray(u, np.float64),
+                                                       np.ascontiguousarray(lam, np.float64), sens))
+        return sens
 
     def optimise(self, L, tT, n_el, n_t, mat, method="CR", strategy=3, n_levels=6, lambda_crit=0.25,
                  min_elements=0, warm_start=True, volume_limit=0.5, theta_ref=1e6, chi_init=0.5,

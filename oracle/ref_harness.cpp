@@ -341,6 +341,18 @@ int ref_optimise(double L, double tT, int n_el, int n_t, const double* mat6, con
   });
 }
 
+// objective_sensitivities, proj/src/optimisation.cpp:34-73
+int ref_objective_sensitivities(double L, double tT, int n_el, int n_t, const double* mat6, const double* chi,
+                                const double* u, const double* lam, double* sens) {
+  return guarded([&] {
+    const SpaceTimeGrid g = build_fine_grid(L, tT, n_el, n_t);
+    const std::size_t n = g.n_dofs();
+    const std::vector<double> s = objective_sensitivities(
+        g, make_mat(mat6), DesignField{std::vector<double>(chi, chi + n_el)}, {u, n}, {lam, n});
+    std::memcpy(sens, s.data(), sizeof(double) * s.size());
+  });
+}
+
 double ref_norm2(const double* x, long long n) {
   return kernels::norm2({x, static_cast<std::size_t>(n)});
 }

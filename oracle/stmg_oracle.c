@@ -39,7 +39,30 @@ double or_dot(const double* x, const double* y, int64_t n) {
   for (int64_t i = 0; i < n; ++i) s[i & 3] += x[i] * y[i];
   return (s[0] + s[1]) + (s[2] + s[3]);
 }
+/* The solve loop's residual norms (or_mg_solve) in one of two summation orders:
+ *  0: the reference's own 4-lane sequential order (or_norm2, kernels.cpp:23-31);
+ *  1: pairwise -- sequential sums of 1024-entry blocks, then a binary tree over the
+ *     blocks -- accurate to ~1e-13 at 1e9 entries, where the sequential order
+ *     loses up to ~1e-9 (profiles/round2_norm_order.txt).  A checker mode for
+ *     full-size configs; the iterates do not depend on it. */
+static int g_norm_mode = 0;
+void or_set_norm_mode(int mode) { g_norm_mode = mode; }
+
+static double sumsq_pairwise(const double* x, int64_t n) {
+  if (n <= 1024) {
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) s += x[i] * x[i];
+    return s;
+  }
+  int64_t half = ((n / 2) + 1023) / 1024 * 1024;
+  if (half >= n) half = n / 2;
+  return sumsq_pairwise(x, half) + sumsq_pairwise(x + half, n - half);
+}
+
 double or_norm2(const double* x, int64_t n) { return sqrt(or_dot(x, x, n)); }
+static double solve_norm(const double* x, int64_t n) {
+  return g_norm_mode == 1 ? sqrt(sumsq_pairwise(x, n)) : or_norm2(x, n);
+}
 
 static inline double rowdot(const double* v, const double* x, int cnt) {
   double s[4] = {0.0, 0.0, 0.0, 0.0};
@@ -690,11 +713,11 @@ int or_mg_solve(const or_hier* h, const double* b, double* u, int nu, double ome
   }
   {
     const int64_t n = ndofs(&h->lv[0]);
-    const double norm_b = or_norm2(b, n);
+    const double norm_b = solve_norm(b, n);
     *absolute_norms = norm_b == 0.0;
     const double denom = *absolute_norms ? 1.0 : norm_b;
     residual_level(&h->lv[0], h->adjoint, b, u, ws.r[0]);
-    const double r0 = or_norm2(ws.r[0], n) / denom;
+    const double r0 = solve_norm(ws.r[0], n) / denom;
     int64_t nh = 0;
     history[nh++] = r0;
     *cycles = 0;
@@ -708,7 +731,7 @@ int or_mg_solve(const or_hier* h, const double* b, double* u, int nu, double ome
     for (int cyc = 1; cyc <= max_cycles; ++cyc) {
       if ((rc = v_cycle(h, 0, b, u, &ws, nu, omega))) goto out;
       residual_level(&h->lv[0], h->adjoint, b, u, ws.r[0]);
-      const double rn = or_norm2(ws.r[0], n) / denom;
+      const double rn = solve_norm(ws.r[0], n) / denom;
       history[nh++] = rn;
       *cycles = cyc;
       if (rn < tol) { *status = 0; break; }

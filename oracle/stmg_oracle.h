@@ -60,6 +60,8 @@ int or_restrict(const or_hier* h, int l, const double* r_fine, double* f_coarse)
 int or_prolong_add(const or_hier* h, int l, const double* x_coarse, double* x_fine);
 int or_coarsest_solve(const or_hier* h, const double* f, double* x);
 double or_norm2(const double* x, int64_t n);
+/* residual norms of or_mg_solve: 0 = the reference's 4-lane order (default), 1 = pairwise */
+void or_set_norm_mode(int mode);
 double or_dot(const double* x, const double* y, int64_t n);
 
 /* proj/src/multigrid.cpp:212-279.  history must hold max_cycles+1 entries. */

@@ -313,7 +313,10 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 // flags: [0] own epoch (exchanges completed), [1] posted by the left neighbour,
-// [2] by the right one, [3] block ticket of the running pull kernel
+// [2] by the right one, [3] block ticket of the running pull kernel, [4] set
+// when a wait timed out (checked by the host after the solve)
+constexpr int kP2pFlagWords = 8;
+constexpr unsigned long long kP2pTimeoutNs = 20000000000ull;  // 20 s of neighbour skew
 __device__ __forceinline__ void p2p_post(const unsigned long long* mine, unsigned long long* left_slot,
                                          unsigned long long* right_slot) {
   const unsigned long long e = mine[0] + 1;
@@ -337,11 +340,18 @@ __global__ void __launch_bounds__(256) k_p2p_pull(unsigned long long* mine, unsi
   const unsigned long long e = mine[0] + 1;  // mine[0] changes only after every block is done
   if (threadIdx.x == 0) {
     if (POST && blockIdx.x == 0) p2p_post(mine, left_slot, right_slot);
+    // A neighbour later than the timeout (a stopped process, a replayed launch)
+    // does not trap the context: the wait gives up, flags the failure in
+    // mine[4] and the host turns it into STMG_ERUNTIME after the solve.
     const unsigned long long t0 = globaltimer_ns();
     for (int side = 1; side <= 2; ++side) {
       if ((side == 1 ? left : right) == nullptr) continue;
-      while (ld_acquire_sys(mine + side) < e)
-        if (globaltimer_ns() - t0 > 20000000000ull) __trap();
+      while (ld_acquire_sys(mine + side) < e) {
+        if (globaltimer_ns() - t0 > kP2pTimeoutNs) {
+          atomicExch(mine + 4, 1ull);
+          break;
+        }
+      }
     }
   }
   __syncthreads();
@@ -381,13 +391,29 @@ struct P2pComm : Comm {
     rank0 = base->rank0;
     loc.resize(static_cast<size_t>(n_local));
     for (int k = 0; k < n_local; ++k) {
-      flag_mem.push_back(std::make_unique<DeviceBuf>(4));
-      cuda_check(cudaMemset(flag_mem.back()->p, 0, 4 * sizeof(double)), "memset");
+      flag_mem.push_back(std::make_unique<DeviceBuf>(kP2pFlagWords));
+      cuda_check(cudaMemset(flag_mem.back()->p, 0, kP2pFlagWords * sizeof(double)), "memset");
       loc[k].flags = flag_mem.back()->p;
     }
   }
-  ~P2pComm() override {
+  ~P2pComm() override { close_peers(); }
+  // Unmaps the neighbours' buffers (before this process frees its own).
+  void close_peers() {
     for (void* p : opened) cudaIpcCloseMemHandle(p);
+    opened.clear();
+  }
+  // Any neighbour wait of this process timed out since the last call?
+  bool timed_out(cudaStream_t s) {
+    bool any = false;
+    for (auto& L : loc) {
+      unsigned long long f = 0;
+      cuda_check(cudaMemcpyAsync(&f, reinterpret_cast<unsigned long long*>(L.flags) + 4, sizeof(f),
+                                 cudaMemcpyDeviceToHost, s),
+                 "p2p flag d2h");
+      cuda_check(cudaStreamSynchronize(s), "sync");
+      any = any || f != 0;
+    }
+    return any;
   }
   const char* name() const override { return "p2p"; }
   void exchange(const std::vector<double*>& v, const std::vector<int64_t>& b, int64_t nn, int depth,
@@ -502,6 +528,21 @@ struct stmg_dist {
     for (auto& kv : graphs) {
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
       if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+    }
+    // Peer-memory transport: no rank may free slab buffers a neighbour can still
+    // read.  Every rank first closes its mappings of the neighbours' buffers,
+    // then all ranks meet (a one-double all-reduce on the base communicator),
+    // and only then are the exported buffers freed.
+    if (auto* pc = dynamic_cast<stmgb::P2pComm*>(comm.get())) {
+      pc->close_peers();
+      if (!ranks.empty() && ranks.front().scalars) {
+        try {
+          std::vector<double*> v{ranks.front().scalars->p + 5};
+          pc->base->allreduce_sum(v, v, stream);
+          cudaStreamSynchronize(stream);
+        } catch (...) {
+        }
+      }
     }
     delete tail;
     ranks.clear();
@@ -832,8 +873,12 @@ double dist_fetch(stmg_dist* d, int slot) {
   return d->pinned[0];
 }
 
+// local = false: b and u are full-size global vectors (every process reads its
+// slab rows and their margins from them); local = true: b and u hold only this
+// process's rows [row_lo, row_hi) of level 0 (stmg_dist_info), so the caller's
+// memory scales as 1/W too, and the ghost rows are exchanged instead.
 void dist_solve(stmg_dist* d, const double* b, double* u, const stmg_solve_options& o,
-                stmg_solve_report* rep, double* history, int32_t cap) {
+                stmg_solve_report* rep, double* history, int32_t cap, bool local = false) {
   if (!b || !u) throw std::invalid_argument("mg_solve: vector size mismatch");
   if (o.nu < 0 || o.omega <= 0.0 || o.tol <= 0.0 || o.div_tol <= o.tol || o.max_cycles < 0)
     throw std::invalid_argument("mg_solve: invalid options");
@@ -843,7 +888,18 @@ void dist_solve(stmg_dist* d, const double* b, double* u, const stmg_solve_optio
   const auto t0 = std::chrono::steady_clock::now();
   const int64_t nn = d->nn(0);
   const bool b_dev = is_device_ptr(b), u_dev = is_device_ptr(u);
+  const int64_t row0 = d->ranks.front().views[0].n_lo;  // first local row (local mode)
   for (auto& R : d->ranks) {
+    if (local) {  // this rank's slab rows; ghosts follow by exchange
+      const LevelView& V = R.views[0];
+      const size_t src = static_cast<size_t>((V.n_lo - row0) * nn), dst = static_cast<size_t>(V.n_lo * nn);
+      const size_t bytes = sizeof(double) * static_cast<size_t>((V.n_hi - V.n_lo) * nn);
+      cuda_check(cudaMemcpyAsync(R.f[0]->p + dst, b + src, bytes,
+                                 b_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, d->stream), "b copy");
+      cuda_check(cudaMemcpyAsync(R.xa[0]->p + dst, u + src, bytes,
+                                 u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, d->stream), "u copy");
+      continue;
+    }
     // the allocated rows (slab + margins) of the global b and u
     const SlabBuf& F = *R.f[0];
     const size_t off = static_cast<size_t>(F.lo * nn), bytes = sizeof(double) * static_cast<size_t>(F.count());
@@ -851,6 +907,11 @@ void dist_solve(stmg_dist* d, const double* b, double* u, const stmg_solve_optio
                                b_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, d->stream), "b copy");
     cuda_check(cudaMemcpyAsync(R.xa[0]->first(), u + off, bytes,
                                u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, d->stream), "u copy");
+  }
+  if (local) {  // the right-hand side's ghost rows (the first norm pass exchanges u's)
+    std::vector<double*> F0;
+    for (auto& R : d->ranks) F0.push_back(R.f[0]->p);
+    d->comm->exchange(F0, d->plan.bounds[0], nn, 1, d->stream);
   }
   std::vector<double*> in, out;
   for (auto& R : d->ranks) {
@@ -911,11 +972,14 @@ void dist_solve(stmg_dist* d, const double* b, double* u, const stmg_solve_optio
     }
   }
   if (rep->cycles > 0) rep->factor = std::pow(history[nh - 1] / r0, 1.0 / rep->cycles);
+  if (auto* pc = dynamic_cast<P2pComm*>(d->comm.get()); pc && pc->timed_out(d->stream))
+    throw std::runtime_error("p2p exchange: a neighbour's epoch wait timed out (rank skew above 20 s)");
   // this process's slab rows of u (loopback: every rank's rows -> the full vector)
   for (auto& R : d->ranks) {
     const LevelView& V = R.views[0];
     const size_t off = static_cast<size_t>(V.n_lo * nn);
-    cuda_check(cudaMemcpyAsync(u + off, R.xa[0]->p + off, sizeof(double) * static_cast<size_t>((V.n_hi - V.n_lo) * nn),
+    const size_t dst = local ? static_cast<size_t>((V.n_lo - row0) * nn) : off;
+    cuda_check(cudaMemcpyAsync(u + dst, R.xa[0]->p + off, sizeof(double) * static_cast<size_t>((V.n_hi - V.n_lo) * nn),
                                u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, d->stream),
                "u copy back");
   }

@@ -2462,6 +2462,14 @@ int stmg_dist_mg_solve(stmg_dist* d, const double* b, double* u, const stmg_solv
   });
 }
 
+int stmg_dist_mg_solve_local(stmg_dist* d, const double* b_local, double* u_local, const stmg_solve_options* opts,
+                             stmg_solve_report* report, double* history, int32_t cap) {
+  return guarded([&] {
+    if (!d || !opts || !report) throw std::invalid_argument("mg_solve: null argument");
+    dist_solve(d, b_local, u_local, *opts, report, history, cap, true);
+  });
+}
+
 int stmg_dist_transport(const stmg_dist* d, char* name_out, int32_t cap) {
   return guarded([&] {
     if (!d || !name_out || cap < 1) throw std::invalid_argument("null handle or buffer");

@@ -185,67 +185,38 @@ __device__ __forceinline__ double prolong_row(const double* __restrict__ xc, int
   }
 }
 
-// Staged-row loaders.  operator() is the per-lane form (any lane subset);
-// warp_row() is called by all 32 lanes of a warp whose nodes wfirst-1 ..
-// wfirst+30 are all inside the grid (interior tiles).
-// Interior staging is split in two phases: warp_load issues every global load
-// of a row (all rows of a tile first, so the loads are in flight together),
-// warp_finish combines them (shuffles) once they are needed.
-struct PlainLoad {
-  const double* __restrict__ x;
-  int64_t nn;
-  __device__ __forceinline__ double operator()(int64_t n, int64_t i) const { return x[n * nn + i]; }
-  struct Raw {
-    double x;
-  };
-  __device__ __forceinline__ Raw warp_load(int64_t n, int64_t i, int64_t, int) const { return {x[n * nn + i]}; }
-  // invd: the lane's inverse diagonal (interior tiles: unmasked rows and nodes)
-  __device__ __forceinline__ double warp_finish(const Raw& r, int64_t, int64_t, int, double) const { return r.x; }
-};
-
-template <int DIR>
-struct ProlongLoad {
-  const double* __restrict__ x;
-  const double* __restrict__ xc;
-  int64_t nn, nnc;
-  __device__ __forceinline__ double operator()(int64_t n, int64_t i) const {
-    return x[n * nn + i] + prolong_row<DIR>(xc, nnc, n, i);
-  }
-  // x step: the warp's fine nodes need coarse nodes c0 .. c0+16, c0 = (wfirst-1)/2;
-  // lanes 0..17 load them once (coalesced) and every lane takes its one or two
-  // values by shuffle; even/odd rows are selected, not branched.  Same
-  // arithmetic as prolong_row.
-  struct Raw {
-    double x, v;
-  };
-  __device__ __forceinline__ Raw warp_load(int64_t n, int64_t i, int64_t wfirst, int lane) const {
-    Raw r;
-    r.x = x[n * nn + i];
-    if (DIR == 1) {
-      r.v = __ldg(xc + (n >> 1) * nnc + i);
-    } else {
-      const int64_t c0 = (wfirst - 1) >> 1;
-      r.v = (lane <= 17 && c0 + lane < nnc) ? __ldg(xc + n * nnc + c0 + lane) : 0.0;
-    }
-    return r;
-  }
-  __device__ __forceinline__ double warp_finish(const Raw& r, int64_t i, int64_t wfirst, int, double) const {
-    if (DIR == 1) return r.x + (0.0 + 1.0 * r.v);  // prolong_row<1>
-    const int64_t c0 = (wfirst - 1) >> 1;
-    const int k0 = (int)((i >> 1) - c0);
-    const double va = __shfl_sync(kFull, r.v, k0);      // xc[i/2] (even), xc[(i-1)/2] (odd)
-    const double vb = __shfl_sync(kFull, r.v, k0 + 1);  // xc[(i+1)/2] (odd)
-    const double pe = 0.0 + 1.0 * va;
-    const double po = (0.5 * va + 0.5 * vb) + 0.0;
-    return r.x + ((i & 1) == 0 ? pe : po);
-  }
-};
-
+// Staged-row loaders of the single-sweep chassis (dev_lean2).  operator()(n, i)
+// is the per-lane form (boundary tiles, any lane subset).  Interior tiles use
+// the three-phase form: lane() once per lane (64-bit row bases, hoisted out of
+// the row loop), load(l, r, nn32) for staged row r (32-bit element offsets
+// from those bases; every load of a tile is issued before the first use), and
+// finish() to combine (invd: the lane's inverse diagonal -- interior rows and
+// nodes are unmasked).
 // The first sweep from a zero iterate, S(0) = 0 + omega (f * inv_diag) (the
 // dev_sweep_from_zero / coarse_from_zero expression), recomputed from f where
 // the iterate is read instead of being stored by the parent's restriction and
 // read back: the coarse-level iterate after its first pre-smoothing sweep.
 __device__ __forceinline__ double zero_sweep(double fv, double id, double omega) { return 0.0 + omega * (fv * id); }
+
+struct PlainLoad {
+  const double* __restrict__ x;
+  int64_t nn;
+  __device__ __forceinline__ double operator()(int64_t n, int64_t i) const { return x[n * nn + i]; }
+  struct Lane {
+    const double* __restrict__ xb;
+  };
+  struct Raw {
+    double x;
+  };
+  // nbase: staged row 0; i: the lane's node
+  __device__ __forceinline__ Lane lane(int64_t nbase, int64_t i, int64_t, int) const {
+    return {opaque(x + (nbase * nn + i))};
+  }
+  __device__ __forceinline__ Raw load(const Lane& l, int r, uint32_t nn32) const {
+    return {__ldg(l.xb + (uint32_t)r * nn32)};
+  }
+  __device__ __forceinline__ double finish(const Raw& w, const Lane&, int64_t, double) const { return w.x; }
+};
 
 struct ZeroLoad {
   const double* __restrict__ f;
@@ -258,51 +229,84 @@ struct ZeroLoad {
   __device__ __forceinline__ double operator()(int64_t n, int64_t i) const {
     return zero_sweep(f[n * nn + i], id(n, i), omega);
   }
+  struct Lane {
+    const double* __restrict__ fb;
+  };
   struct Raw {
     double f;
   };
-  // interior tiles: n >= 1 and i >= 1, so no masked row and id = inv_diag[i]
-  __device__ __forceinline__ Raw warp_load(int64_t n, int64_t i, int64_t, int) const { return {f[n * nn + i]}; }
-  __device__ __forceinline__ double warp_finish(const Raw& r, int64_t, int64_t, int, double invd_i) const {
-    return zero_sweep(r.f, invd_i, omega);
+  __device__ __forceinline__ Lane lane(int64_t nbase, int64_t i, int64_t, int) const {
+    return {opaque(f + (nbase * nn + i))};
+  }
+  __device__ __forceinline__ Raw load(const Lane& l, int r, uint32_t nn32) const {
+    return {__ldg(l.fb + (uint32_t)r * nn32)};
+  }
+  __device__ __forceinline__ double finish(const Raw& w, const Lane&, int64_t, double invd_i) const {
+    return zero_sweep(w.f, invd_i, omega);
   }
 };
 
-// ProlongLoad with the fine iterate S(0) recomputed from f (nu = 1 coarse levels).
-template <int DIR>
-struct ProlongZeroLoad {
-  ZeroLoad z;
+// x + P xc at the staged rows (csr_spmv_add, proj/src/transfer.cpp:74-88), the
+// fine iterate x given by Base (PlainLoad, or ZeroLoad for nu = 1 coarse
+// levels).  x step (DIR 0): each lane reads its coarse values xc[i >> 1] and
+// xc[(i + 1) >> 1] directly (one or two distinct values, L1-resident across the
+// warp); causal t step (DIR 1): xc[n >> 1] at the same node.  The arithmetic is
+// prolong_row's: even i 0 + 1.0 a, odd i (0.5 a + 0.5 b) + 0.
+template <int DIR, class Base>
+struct ProlongOn {
+  Base base;
   const double* __restrict__ xc;
   int64_t nnc;
   __device__ __forceinline__ double operator()(int64_t n, int64_t i) const {
-    return z(n, i) + prolong_row<DIR>(xc, nnc, n, i);
+    return base(n, i) + prolong_row<DIR>(xc, nnc, n, i);
   }
-  struct Raw {
-    double f, v;
+  struct Lane {
+    typename Base::Lane b;
+    const double* __restrict__ cb;
+    uint32_t odd;  // DIR 0: i & 1; DIR 1: nbase & 1
   };
-  __device__ __forceinline__ Raw warp_load(int64_t n, int64_t i, int64_t wfirst, int lane) const {
-    Raw r;
-    r.f = z.f[n * z.nn + i];
-    if (DIR == 1) {
-      r.v = __ldg(xc + (n >> 1) * nnc + i);
+  struct Raw {
+    typename Base::Raw b;
+    double a, c;
+  };
+  __device__ __forceinline__ Lane lane(int64_t nbase, int64_t i, int64_t wfirst, int ln) const {
+    Lane l;
+    l.b = base.lane(nbase, i, wfirst, ln);
+    if (DIR == 0) {
+      l.cb = opaque(xc + (nbase * nnc + (i >> 1)));
+      l.odd = (uint32_t)(i & 1);
     } else {
-      const int64_t c0 = (wfirst - 1) >> 1;
-      r.v = (lane <= 17 && c0 + lane < nnc) ? __ldg(xc + n * nnc + c0 + lane) : 0.0;
+      l.cb = opaque(xc + ((nbase >> 1) * nnc + i));
+      l.odd = (uint32_t)(nbase & 1);
     }
-    return r;
+    return l;
   }
-  __device__ __forceinline__ double warp_finish(const Raw& r, int64_t i, int64_t wfirst, int, double invd_i) const {
-    const double x = zero_sweep(r.f, invd_i, z.omega);
-    if (DIR == 1) return x + (0.0 + 1.0 * r.v);  // prolong_row<1>
-    const int64_t c0 = (wfirst - 1) >> 1;
-    const int k0 = (int)((i >> 1) - c0);
-    const double va = __shfl_sync(kFull, r.v, k0);
-    const double vb = __shfl_sync(kFull, r.v, k0 + 1);
-    const double pe = 0.0 + 1.0 * va;
-    const double po = (0.5 * va + 0.5 * vb) + 0.0;
-    return x + ((i & 1) == 0 ? pe : po);
+  __device__ __forceinline__ Raw load(const Lane& l, int r, uint32_t nn32) const {
+    Raw w;
+    w.b = base.load(l.b, r, nn32);
+    const uint32_t nnc32 = (uint32_t)nnc;
+    if (DIR == 0) {
+      const double* p = l.cb + (uint32_t)r * nnc32;
+      w.a = __ldg(p);
+      w.c = __ldg(p + l.odd);
+    } else {
+      w.a = __ldg(l.cb + ((l.odd + (uint32_t)r) >> 1) * nnc32);
+      w.c = 0.0;
+    }
+    return w;
+  }
+  __device__ __forceinline__ double finish(const Raw& w, const Lane& l, int64_t i, double invd_i) const {
+    const double x = base.finish(w.b, l.b, i, invd_i);
+    if (DIR == 1) return x + (0.0 + 1.0 * w.a);  // prolong_row<1>
+    const double pe = 0.0 + 1.0 * w.a;
+    const double po = (0.5 * w.a + 0.5 * w.c) + 0.0;
+    return x + (l.odd ? po : pe);
   }
 };
+template <int DIR>
+using ProlongLoad = ProlongOn<DIR, PlainLoad>;
+template <int DIR>
+using ProlongZeroLoad = ProlongOn<DIR, ZeroLoad>;
 
 __device__ __forceinline__ double block_sum(double v) {
   __shared__ double warp_sums[32];
@@ -349,18 +353,21 @@ __device__ __forceinline__ double dev_lean2(const LevelView& L, const Ld& ld, co
   double xr[NT + 1], fv[NT];
   double acc = 0.0;
   if (rows_in && nodes_in) {
-    // every lane's node is inside the grid: lanes 0 / 31 load too (unused values)
+    // every lane's node is inside the grid: lanes 0 / 31 load too (unused values).
+    // 64-bit row bases once per lane, 32-bit element offsets per row.
     const bool computes = lane >= 1 && lane <= 30;
-    const double* fp = f + (n0 * nn + i);
+    const uint32_t nn32 = (uint32_t)nn;
+    const double* __restrict__ fp = opaque(f + (n0 * nn + i));
 #pragma unroll
-    for (int k = 0; k < NT; ++k) fv[k] = fp[k * nn];
+    for (int k = 0; k < NT; ++k) fv[k] = __ldg(fp + (uint32_t)k * nn32);
+    const typename Ld::Lane lc = ld.lane(nbase, i, wfirst, lane);
     typename Ld::Raw raw[NT + 1];
 #pragma unroll
-    for (int r = 0; r <= NT; ++r) raw[r] = ld.warp_load(nbase + r, i, wfirst, lane);
+    for (int r = 0; r <= NT; ++r) raw[r] = ld.load(lc, r, nn32);
     const Coefs c = load_coefs(L, i);
 #pragma unroll
-    for (int r = 0; r <= NT; ++r) xr[r] = ld.warp_finish(raw[r], i, wfirst, lane, c.invd);
-    double* yp = y + (n0 * nn + i);
+    for (int r = 0; r <= NT; ++r) xr[r] = ld.finish(raw[r], lc, i, c.invd);
+    double* __restrict__ yp = opaque(y + (n0 * nn + i));
     double pm = __shfl_up_sync(kFull, xr[0], 1);
     double pp = __shfl_down_sync(kFull, xr[0], 1);
 #pragma unroll
@@ -374,8 +381,8 @@ __device__ __forceinline__ double dev_lean2(const LevelView& L, const Ld& ld, co
       const double r = fv[k] - row;
       if (computes) {
         if (NORM) acc = acc + r * r;
-        if (MODE == kSweep) yp[k * nn] = x0 + omega * (r * c.invd);
-        else if (MODE == kResidual) yp[k * nn] = r;
+        if (MODE == kSweep) st_global(yp + (uint32_t)k * nn32, x0 + omega * (r * c.invd));
+        else if (MODE == kResidual) st_global(yp + (uint32_t)k * nn32, r);
       }
       pm = qm;
       pp = qp;
@@ -664,15 +671,17 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
   const bool nodes_in = base >= 2 && base + 29 <= F.n_el - 1;
   double xr[NT + 1], fv[NT];
   if (rows_in && nodes_in) {
-    const double* fp = f + (n0 * nn + i);
-    const double* xp = x + (nbase * nn + i);
+    // 64-bit row bases once per lane, 32-bit element offsets per row
+    const uint32_t nn32 = (uint32_t)nn, nnc32 = (uint32_t)nnc;
+    const double* __restrict__ fp = opaque(f + (n0 * nn + i));
 #pragma unroll
-    for (int k = 0; k < NT; ++k) fv[k] = fp[k * nn];
+    for (int k = 0; k < NT; ++k) fv[k] = __ldg(fp + (uint32_t)k * nn32);
     double fx = 0.0;  // ZX: the one staged level outside the f rows
-    if (ZX) fx = ADJ ? fp[NT * nn] : fp[-nn];
+    if (ZX) fx = ADJ ? __ldg(fp + (uint32_t)NT * nn32) : __ldg(opaque(f + (nbase * nn + i)));
     if (!ZX) {
+      const double* __restrict__ xp = opaque(x + (nbase * nn + i));
 #pragma unroll
-      for (int r = 0; r <= NT; ++r) xr[r] = xp[r * nn];
+      for (int r = 0; r <= NT; ++r) xr[r] = __ldg(xp + (uint32_t)r * nn32);
     }
     const Coefs c = load_coefs(F, i);
     if (ZX) {
@@ -683,12 +692,15 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
         xr[r] = zero_sweep(fr, c.invd, omega);
       }
     }
+    // Output lanes and their coarse node: x step, the lanes at even fine nodes
+    // i = 2I (odd lanes 3..29); t step, every computing lane (I = i).
+    const bool out = DIR == 0 ? ((lane & 1) && lane >= 3 && lane <= 29) : (lane >= 1 && lane <= 30);
+    const int64_t I = DIR == 0 ? (i >> 1) : i;
+    const int64_t crow = DIR == 0 ? n0 : (n0 >> 1);
+    double* __restrict__ fcb = opaque(fc + (crow * nnc + I));
+    double* __restrict__ xcb = xc0 != nullptr ? opaque(xc0 + (crow * nnc + I)) : nullptr;
     // coarse inverse diagonal at this lane's coarse node (first coarse sweep from zero)
-    double idc = 0.0;
-    if (xc0 != nullptr) {
-      const int64_t I = DIR == 0 ? base / 2 + lane : i;
-      if (DIR == 1 || (lane >= 1 && lane <= 14)) idc = __ldg(C.coef + kInvD * nnc + I);
-    }
+    const double idc = (xc0 != nullptr && out) ? __ldg(C.coef + kInvD * nnc + I) : 0.0;
     double pm = __shfl_up_sync(kFull, xr[0], 1), pp = __shfl_down_sync(kFull, xr[0], 1);
     double r_even = 0.0;
 #pragma unroll
@@ -698,23 +710,22 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
       const double r = fv[k] - (ADJ ? row_interior<true>(c, pm, xr[k], pp, qm, x1, qp)
                                     : row_interior<false>(c, qm, x1, qp, pm, xr[k], pp));
       if (DIR == 0) {
-        const int src = 2 * lane;
-        const double ra = __shfl_sync(kFull, r, src & 31);
-        const double rb = __shfl_sync(kFull, r, (src + 1) & 31);
-        const double rc = __shfl_sync(kFull, r, (src + 2) & 31);
+        // fine nodes 2I - 1, 2I, 2I + 1 are lanes l - 1, l, l + 1 of output lane l;
         // canonical ((0 + .5 ra) + (0 + rb)) + ((0 + .5 rc) + 0), folded (see row_interior)
-        if (lane >= 1 && lane <= 14) {
-          const double v = ((0.5 * ra + 1.0 * rb) + 0.5 * rc) + 0.0;
-          fc[(n0 + k) * nnc + base / 2 + lane] = v;
-          if (xc0 != nullptr) xc0[(n0 + k) * nnc + base / 2 + lane] = 0.0 + omega * (v * idc);
+        const double ra = __shfl_up_sync(kFull, r, 1);
+        const double rc = __shfl_down_sync(kFull, r, 1);
+        if (out) {
+          const double v = ((0.5 * ra + 1.0 * r) + 0.5 * rc) + 0.0;
+          st_global(fcb + (uint32_t)k * nnc32, v);
+          if (xc0 != nullptr) st_global(xcb + (uint32_t)k * nnc32, 0.0 + omega * (v * idc));
         }
       } else {
         if ((k & 1) == 0) {
           r_even = r;
-        } else if (lane >= 1 && lane <= 30) {
+        } else if (out) {
           const double v = (0.5 * r_even + 0.5 * r) + 0.0;
-          fc[((n0 + k) >> 1) * nnc + i] = v;
-          if (xc0 != nullptr) xc0[((n0 + k) >> 1) * nnc + i] = 0.0 + omega * (v * idc);
+          st_global(fcb + (uint32_t)(k >> 1) * nnc32, v);
+          if (xc0 != nullptr) st_global(xcb + (uint32_t)(k >> 1) * nnc32, 0.0 + omega * (v * idc));
         }
       }
       pm = qm;
@@ -1687,7 +1698,7 @@ int sweep_prolong_impl(const LevelView& L, const LevelView& C, const double* f, 
     const ProlongZeroLoad<DIR> ld{zero_load(L, f, omega), xc, C.nn};
     launch_pass<ADJ, kSweep, false>(L, ld, f, y, omega, nullptr, s);
   } else {
-    const ProlongLoad<DIR> ld{x, xc, L.nn, C.nn};
+    const ProlongLoad<DIR> ld{PlainLoad{x, L.nn}, xc, C.nn};
     launch_pass<ADJ, kSweep, false>(L, ld, f, y, omega, nullptr, s);
   }
   return check_launch();

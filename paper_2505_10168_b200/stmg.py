@@ -82,6 +82,7 @@ def _load():
         "stmg_synchronize": [vp],
         "stmg_hierarchy_set_tiling": [vp, i64, i64],
         "stmg_hierarchy_set_fusion": [vp, i32],
+        "stmg_objective_sensitivities": [vp, vp, vp, vp, vp, vp, i32],
         "stmg_level_fused": [vp, i32, i32, vp, vp, vp, vp, vp, f64, C.POINTER(f64)],
         "stmg_dist_partition": [i32, vp, vp, i32, i64, C.POINTER(i32), vp],
         "stmg_optimise": [vp, vp, i32, vp, vp, C.POINTER(i32), C.POINTER(f64), C.POINTER(i32),
@@ -92,6 +93,7 @@ def _load():
         "stmg_dist_info": [vp, C.POINTER(i32), C.POINTER(i64), C.POINTER(i64), C.POINTER(i32),
                            C.POINTER(i64)],
         "stmg_dist_mg_solve": [vp, vp, vp, vp, vp, vp, i32],
+        "stmg_dist_mg_solve_local": [vp, vp, vp, vp, vp, vp, i32],
         "stmg_dist_transport": [vp, C.c_char_p, i32],
     }
     for name, args in sig.items():
@@ -747,6 +749,20 @@ class OptimisationResult:
     design_history: Optional[np.ndarray] = None  # row i: the design evaluated at iteration i + 1
 
 
+def objective_sensitivities(geom: SpaceTimeGrid, mat, chi, u, lam, device: int = 0) -> np.ndarray:
+    """proj/src/optimisation.cpp:34-73 on the GPU (u, lam host arrays or device tensors)."""
+    n = (geom.n_el + 1) * (geom.n_t + 1)
+    if _numel(u) != n or _numel(lam) != n:
+        raise ValueError("objective_sensitivities: state size mismatch")
+    chi_a = _f64(chi.chi if hasattr(chi, "chi") else chi, geom.n_el)
+    sens = np.zeros(geom.n_el)
+    gc = geom._c()
+    m = MaterialPair.of(mat)._c()
+    _check(_lib.stmg_objective_sensitivities(C.byref(gc), C.byref(m), chi_a.ctypes.data, _ptr(u), _ptr(lam),
+                                             sens.ctypes.data, int(device)))
+    return sens
+
+
 def optimise(geom: SpaceTimeGrid, mat, opts: Optional[OptimisationOptions] = None,
              device: int = 0) -> OptimisationResult:
     o = opts or OptimisationOptions()
@@ -871,6 +887,22 @@ def mg_solve_dist(h: DistHierarchy, b, u, opts: Optional[SolveOptions] = None) -
                        [float(v) for v in hist[: rep.n_history]], bool(rep.absolute_norms),
                        rep.seconds, rep.device_seconds, rep.smoother_dof_updates, rep.kernel_launches)
 
+
+def mg_solve_dist_local(h: DistHierarchy, b_local, u_local, opts: Optional[SolveOptions] = None) -> SolveReport:
+    """Distributed solve on slab-local vectors: this process's level-0 rows
+    [h.row_lo, h.row_hi) only (stmg_dist_mg_solve_local); memory scales as 1/W."""
+    o = opts or SolveOptions()
+    n = (h.row_hi - h.row_lo) * (h.levels[0].n_el + 1)
+    if _numel(b_local) != n or _numel(u_local) != n:
+        raise ValueError("mg_solve: vector size mismatch")
+    hist = np.zeros(max(o.max_cycles, 0) + 1, np.float64)
+    rep = _SolveRep()
+    co = _SolveOpts(int(o.nu), float(o.omega), float(o.tol), float(o.div_tol), int(o.max_cycles))
+    _check(_lib.stmg_dist_mg_solve_local(h.handle, _ptr(b_local), _ptr(u_local), C.byref(co), C.byref(rep),
+                                         hist.ctypes.data, hist.size))
+    return SolveReport(SolveStatus(rep.status), rep.cycles, rep.factor,
+                       [float(v) for v in hist[: rep.n_history]], bool(rep.absolute_norms),
+                       rep.seconds, rep.device_seconds, rep.smoother_dof_updates, rep.kernel_launches)
 
 
 

@@ -50,6 +50,30 @@ def test_loopback_slabs_match_single_domain(S, port, name, world):
     assert np.allclose(r2.history, r1.history, rtol=1e-12, atol=0)
 
 
+@pytest.mark.parametrize("name,world", [("cfg1_mini", 2), ("cfg1_mini_adj", 4), ("cfg2_mini", 4)])
+def test_slab_local_vectors_match_full_vectors(S, port, name, world):
+    """stmg_dist_mg_solve_local: the caller holds only this process's level-0 rows
+    of b and u (loopback: all ranks' rows, [row_lo, row_hi)); the library exchanges
+    the right-hand side's ghost rows.  Bitwise the full-vector slab solve."""
+    import torch
+
+    cs = case(name)
+    g, path = grid_path(S, cs, port)
+    b = cs.rhs_vector(port)
+    opts = S.SolveOptions(nu=cs.nu, tol=cs.tol, max_cycles=cs.max_cycles)
+    dh = S.build_dist_hierarchy(g, cs.method, path, world, adjoint=cs.adjoint, chi=cs.chi, mat=cs.mat,
+                                min_slab=8)
+    u_full = np.zeros_like(b)
+    r_full = S.mg_solve_dist(dh, b, u_full, opts)
+    nn = cs.n_el + 1
+    rows = slice(dh.row_lo * nn, dh.row_hi * nn)
+    b_loc = torch.from_numpy(np.ascontiguousarray(b[rows])).cuda()
+    u_loc = torch.zeros_like(b_loc)
+    r_loc = S.mg_solve_dist_local(dh, b_loc, u_loc, opts)
+    assert r_loc.cycles == r_full.cycles and r_loc.history == r_full.history
+    assert np.array_equal(u_loc.cpu().numpy().view(np.uint64), u_full[rows].view(np.uint64))
+
+
 def test_partition_rules(S):
     # cfg1 path x,x,x,t,x,t,t,x,t: n_t per level 4096 x4, 2048 x2, 1024, 512 x2, 256
     nts = [4096, 4096, 4096, 4096, 2048, 2048, 1024, 512, 512, 256]

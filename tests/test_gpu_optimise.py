@@ -36,16 +36,72 @@ def test_optimise_matches_reference():
     assert abs(res.theta - float(gold["theta"])) <= 1e-9 * abs(float(gold["theta"]))
 
 
-def test_sensitivity_kernel_matches_reference_formula():
-    """objective_sensitivities (proj/src/optimisation.cpp:34-73) on random states."""
-    import torch
+def test_optimise_rejects_bad_options_like_the_reference():
+    """std::invalid_argument for the option checks of proj/src/optimisation.cpp:85-89."""
+    import torch  # noqa: F401
 
     from paper_2505_10168_b200 import stmg as S
 
-    # covered end to end by test_optimise_matches_reference; here check the
-    # optimiser rejects bad options like the reference (std::invalid_argument)
     geom = S.build_fine_grid(1.0, 1.0, 8, 8)
     with pytest.raises(ValueError):
         S.optimise(geom, (1e-3, 1, 1, 1, 3, 2), S.OptimisationOptions(volume_limit=0.0))
     with pytest.raises(ValueError):
         S.optimise(geom, (1e-3, 1, 1, 1, 3, 2), S.OptimisationOptions(max_iterations=0))
+
+
+@pytest.mark.parametrize("shape", [(64, 128), (100, 37), (4096, 512), (1, 3)])
+def test_sensitivity_kernel_matches_reference(ref, shape):
+    """k_sensitivities against the reference's own objective_sensitivities
+    (proj/src/optimisation.cpp:34-73, compiled in oracle/_ref), bit for bit, on
+    random states and designs (salted with zeros and the masked rows' values)."""
+    import torch
+
+    from paper_2505_10168_b200 import stmg as S
+
+    n_el, n_t = shape
+    rng = np.random.default_rng(n_el * 7 + n_t)
+    mat = (1e-3, 1.0, 1.0, 1.0, 3.0, 2.0)
+    chi = rng.uniform(0.0, 1.0, n_el)
+    chi[:: 5] = 1.0
+    chi[1:: 7] = 0.0
+    n = (n_el + 1) * (n_t + 1)
+    u, lam = rng.standard_normal(n), rng.standard_normal(n)
+    u[:: 11] = 0.0
+    want = ref.objective_sensitivities(1.0, 2.0, n_el, n_t, mat, chi, u, lam)
+    geom = S.build_fine_grid(1.0, 2.0, n_el, n_t)
+    got_host = S.objective_sensitivities(geom, mat, chi, u, lam)
+    got_dev = S.objective_sensitivities(geom, mat, chi, torch.from_numpy(u).cuda(), torch.from_numpy(lam).cuda())
+    assert np.array_equal(got_host.view(np.uint64), want.view(np.uint64))
+    assert np.array_equal(got_dev.view(np.uint64), want.view(np.uint64))
+
+
+@pytest.mark.slow
+def test_cfg4_configured_size_first_iterations():
+    """BASELINE config 4 at its configured size (4096 x 16384, CR, DesignIndependent,
+    6 levels, nu = 20, tol 1e-8, warm starts): the first design iterations against
+    the reference's own optimise() (tests/golden/cfg4_full.npz, made by
+    tests/golden/make_golden_cfg4.py): per-iteration primal / adjoint V-cycle
+    counts, statuses and paths, theta, volume and the final design."""
+    path = os.path.join(os.path.dirname(GOLD), "cfg4_full.npz")
+    if not os.path.exists(path):
+        pytest.skip("cfg4_full fixture not generated")
+    from paper_2505_10168_b200 import stmg as S
+    from tests.golden.make_golden_cfg4 import CFG4_FULL
+
+    gold = dict(np.load(path))
+    o = CFG4_FULL
+    its = int(gold["iterations"])
+    geom = S.build_fine_grid(o["L"], o["tT"], o["n_el"], o["n_t"])
+    opts = S.OptimisationOptions(method=o["method"], strategy=S.PlanStrategy(o["strategy"]), n_levels=o["n_levels"],
+                                 max_iterations=its, stable_iterations=o["stable_iterations"],
+                                 solve=S.SolveOptions(nu=o["nu"], tol=o["tol"]))
+    res = S.optimise(geom, o["mat"], opts)
+    rec = gold["records"]
+    assert res.iterations == rec.shape[0] == its
+    for i, h in enumerate(res.history):
+        assert (h["primal_cycles"], h["adjoint_cycles"]) == (int(rec[i, 6]), int(rec[i, 7])), i
+        assert (h["primal_status"], h["adjoint_status"]) == (int(rec[i, 4]), int(rec[i, 5])), i
+        assert abs(h["theta"] - rec[i, 0]) <= 1e-9 * abs(rec[i, 0]), i
+        assert abs(h["volume"] - rec[i, 1]) <= 1e-12, i
+        assert h["path"] == "x,x,x,x,t", h["path"]
+    assert np.max(np.abs(res.chi - gold["chi"])) <= 1e-9

@@ -14,6 +14,11 @@ on the GPU box's host cores at the configs' full sizes.
   proj/include/stmg/sparse.hpp:66-70) under the reference's stop rule
   (proj/src/multigrid.cpp:246-279): the same cycles and status (Diverged), the
   history within 1e-10 relative and the field within 1e-10 relative max-norm.
+  At 1.07e9 terms the reference's own 4-lane sequential norm order is itself
+  off by up to 6.6e-10 relative (profiles/round2_norm_order.txt: the GPU's
+  reported history equals the exactly summed residual norm to 2e-16), so the
+  oracle sums these residual norms pairwise (or_set_norm_mode); its iterates
+  do not depend on that.
 
 Host memory: up to ~75 GB for cfg2 (the oracle's level vectors plus b and both
 fields); the oracle uses every host core (OR_THREADS).
@@ -132,7 +137,11 @@ def test_cfg2_cfg3_full_size_vs_oracle(S, port, name):
     else:
         b = port.load_vector(cfg.L, cfg.t_T, cfg.n_el, cfg.n_t, cfg.source_kind, cfg.source_params)
     rep, u = gpu_solve(S, cfg, dirs, b, cfg.adjoint)
-    rep_o, u_o = oracle_solve(port, cfg, dirs, b, cfg.adjoint)
+    port.set_norm_mode(pairwise=True)
+    try:
+        rep_o, u_o = oracle_solve(port, cfg, dirs, b, cfg.adjoint)
+    finally:
+        port.set_norm_mode(pairwise=False)
     del b
     gc.collect()
     assert rep.cycles == rep_o.cycles and int(rep.status) == rep_o.status
