@@ -2274,6 +2274,16 @@ int stmg_level_fused(stmg_hierarchy* h, int32_t l, int32_t kind, const double* f
         if (norm2) *norm2 = sc[2];
         break;
       }
+      case STMG_FUSED_NORM_SWEEP: {
+        if (!x || !y) throw std::invalid_argument("level_fused: null x / y");
+        int64_t np = 0;
+        launch_check(launch_sweep(h->adjoint, L, f, x, y, omega, h->ws->partials->p, &np, h->stream), "norm sweep");
+        launch_check(launch_finalize_sum(h->ws->partials->p, np, h->ws->scalars->p + 2, h->stream), "finalize");
+        double sc[3];
+        fetch_scalars(h, 3, sc);
+        if (norm2) *norm2 = sc[2];
+        break;
+      }
       default:
         throw std::invalid_argument("level_fused: unknown kind");
     }

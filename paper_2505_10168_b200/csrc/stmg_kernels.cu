@@ -381,8 +381,8 @@ __device__ __forceinline__ double dev_lean2(const LevelView& L, const Ld& ld, co
       const double r = fv[k] - row;
       if (computes) {
         if (NORM) acc = acc + r * r;
-        if (MODE == kSweep) st_global(yp + (uint32_t)k * nn32, x0 + omega * (r * c.invd));
-        else if (MODE == kResidual) st_global(yp + (uint32_t)k * nn32, r);
+        if (MODE == kSweep) *(yp + (uint32_t)k * nn32) = x0 + omega * (r * c.invd);
+        else if (MODE == kResidual) *(yp + (uint32_t)k * nn32) = r;
       }
       pm = qm;
       pp = qp;
@@ -527,7 +527,7 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
       // lanes 2..29; row n0 + k is staged row k (J^T) / k + 2 (J)
       const double v = ADJ ? upd(y1[k], fv[k], row_interior<true>(c, am, y1[k], ap, bm, z1, bp))
                            : upd(z1, fv[k + 1], row_interior<false>(c, bm, z1, bp, am, y1[k], ap));
-      if (lane2) st_global(yb + o[ADJ ? k : k + 2], v);
+      if (lane2) *(yb + o[ADJ ? k : k + 2]) = v;
       am = bm;
       ap = bp;
     }
@@ -716,16 +716,16 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
         const double rc = __shfl_down_sync(kFull, r, 1);
         if (out) {
           const double v = ((0.5 * ra + 1.0 * r) + 0.5 * rc) + 0.0;
-          st_global(fcb + (uint32_t)k * nnc32, v);
-          if (xc0 != nullptr) st_global(xcb + (uint32_t)k * nnc32, 0.0 + omega * (v * idc));
+          *(fcb + (uint32_t)k * nnc32) = v;
+          if (xc0 != nullptr) *(xcb + (uint32_t)k * nnc32) = 0.0 + omega * (v * idc);
         }
       } else {
         if ((k & 1) == 0) {
           r_even = r;
         } else if (out) {
           const double v = (0.5 * r_even + 0.5 * r) + 0.0;
-          st_global(fcb + (uint32_t)(k >> 1) * nnc32, v);
-          if (xc0 != nullptr) st_global(xcb + (uint32_t)(k >> 1) * nnc32, 0.0 + omega * (v * idc));
+          *(fcb + (uint32_t)(k >> 1) * nnc32) = v;
+          if (xc0 != nullptr) *(xcb + (uint32_t)(k >> 1) * nnc32) = 0.0 + omega * (v * idc);
         }
       }
       pm = qm;
@@ -876,11 +876,16 @@ __device__ __forceinline__ double dev_down(const LevelView& F, const LevelView& 
 #pragma unroll
     for (int r = 0; r < NT + 1; ++r) fv[r] = __ldg(fb + o[ADJ ? r : r + 1]);  // f rows s1base + r
     const Coefs c = load_coefs(F, i);
-    double idc = 0.0;  // coarse inverse diagonal at this lane's coarse node (x_c0)
-    if (xc0 != nullptr) {
-      const int64_t I = DIR == 0 ? base / 2 + lane : i;
-      if (DIR == 1 || (lane >= 1 && lane <= 13)) idc = __ldg(C.coef + kInvD * nnc + I);
-    }
+    // output lanes and their coarse node: x step, even fine nodes i = 2I (odd lanes
+    // 3..27); t step, the owned lanes (I = i)
+    const bool out = DIR == 0 ? ((lane & 1) && lane >= 3 && lane <= 27) : owns;
+    const int64_t I = DIR == 0 ? (i >> 1) : i;
+    const int64_t crow = DIR == 0 ? n0 : (n0 >> 1);
+    const uint32_t nnc32 = (uint32_t)nnc;
+    double* __restrict__ fcb = opaque(fc + (crow * nnc + I));
+    double* __restrict__ xcb = xc0 != nullptr ? opaque(xc0 + (crow * nnc + I)) : nullptr;
+    // coarse inverse diagonal at this lane's coarse node (x_c0)
+    const double idc = (xc0 != nullptr && out) ? __ldg(C.coef + kInvD * nnc + I) : 0.0;
     // ---- stage 1: y1[r] = S(x) on row s1base + r; norm on the tile's own rows
     double pm = __shfl_up_sync(kFull, xs[0], 1), pp = __shfl_down_sync(kFull, xs[0], 1);
 #pragma unroll
@@ -899,7 +904,7 @@ __device__ __forceinline__ double dev_down(const LevelView& F, const LevelView& 
       const bool own_row = ADJ ? r < NT : r >= 1;  // row n0 .. n0 + NT - 1
       if (own_row && owns) {
         acc = acc + res * res;
-        st_global(yb + o[ADJ ? r : r + 1], y1[r]);
+        *(yb + o[ADJ ? r : r + 1]) = y1[r];
       }
       pm = qm;
       pp = qp;
@@ -914,22 +919,21 @@ __device__ __forceinline__ double dev_down(const LevelView& F, const LevelView& 
       const double r2 = ADJ ? fv[k] - row_interior<true>(c, am, y1[k], ap, bm, z1, bp)
                             : fv[k + 1] - row_interior<false>(c, bm, z1, bp, am, y1[k], ap);
       if (DIR == 0) {
-        const int src = 2 * lane;
-        const double ra = __shfl_sync(kFull, r2, src & 31);
-        const double rb = __shfl_sync(kFull, r2, (src + 1) & 31);
-        const double rc = __shfl_sync(kFull, r2, (src + 2) & 31);
-        if (lane >= 1 && lane <= 13) {
-          const double v = ((0.5 * ra + 1.0 * rb) + 0.5 * rc) + 0.0;
-          fc[(n0 + k) * nnc + base / 2 + lane] = v;
-          if (xc0 != nullptr) xc0[(n0 + k) * nnc + base / 2 + lane] = 0.0 + omega * (v * idc);
+        // output lanes (even fine node 2I: odd lanes 3..27) take lanes l - 1, l, l + 1
+        const double ra = __shfl_up_sync(kFull, r2, 1);
+        const double rc = __shfl_down_sync(kFull, r2, 1);
+        if (out) {
+          const double v = ((0.5 * ra + 1.0 * r2) + 0.5 * rc) + 0.0;
+          *(fcb + (uint32_t)k * nnc32) = v;
+          if (xc0 != nullptr) *(xcb + (uint32_t)k * nnc32) = 0.0 + omega * (v * idc);
         }
       } else {
         if ((k & 1) == 0) {
           r_even = r2;
-        } else if (owns) {
+        } else if (out) {
           const double v = (0.5 * r_even + 0.5 * r2) + 0.0;
-          fc[((n0 + k) >> 1) * nnc + i] = v;
-          if (xc0 != nullptr) xc0[((n0 + k) >> 1) * nnc + i] = 0.0 + omega * (v * idc);
+          *(fcb + (uint32_t)(k >> 1) * nnc32) = v;
+          if (xc0 != nullptr) *(xcb + (uint32_t)(k >> 1) * nnc32) = 0.0 + omega * (v * idc);
         }
       }
       am = bm;

@@ -571,7 +571,8 @@ class LevelHierarchy:
         """V-cycle fusions (stmg_hierarchy_set_fusion): bit-identical, traffic differs."""
         _check(_lib.stmg_hierarchy_set_fusion(self._h, int(flags)))
 
-    FUSED_ZERO_SWEEP, FUSED_ZERO_PAIR, FUSED_ZERO_RESTRICT, FUSED_ZERO_PROLONG_SWEEP, FUSED_FINE_DOWN = range(5)
+    (FUSED_ZERO_SWEEP, FUSED_ZERO_PAIR, FUSED_ZERO_RESTRICT, FUSED_ZERO_PROLONG_SWEEP, FUSED_FINE_DOWN,
+     FUSED_NORM_SWEEP) = range(6)
 
     def fused_kernel(self, l, kind, f, x=None, xc=None, y=None, fc=None, omega=0.5):
         """stmg_level_fused on device tensors; returns ||f - J x||^2 for FUSED_FINE_DOWN."""
