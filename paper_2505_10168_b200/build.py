@@ -41,34 +41,37 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str = OUT, defines=()) -> str:
+    """defines: extra -D flags (compile-time A/B builds into another `out`, profiles/ab_build.py)."""
+    if out == OUT and not defines and not force and not stale():
         return OUT
+    objdir = CSRC if out == OUT else os.path.dirname(out)
+    os.makedirs(objdir, exist_ok=True)
     objs = []
     log = []
     procs = []
     for src in SOURCES:  # the translation units compile in parallel
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [nvcc(), *NVCC_FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
         objs.append(obj)
     for src, p in procs:
-        out, err = p.communicate()
-        log.append(out + err)
+        so, se = p.communicate()
+        log.append(so + se)
         if p.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src}:\n{out}\n{err}")
-    tmp = OUT + ".tmp"
+            raise RuntimeError(f"nvcc failed for {src}:\n{so}\n{se}")
+    tmp = out + ".tmp"
     cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", tmp,
            "-lcudart_static", "-lpthread", "-ldl", "-lrt"]  # NCCL is dlopen'ed at run time
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, OUT)
-    with open(os.path.join(CSRC, "ptxas.log"), "w") as fh:
+    os.replace(tmp, out)
+    with open(os.path.join(objdir, "ptxas.log"), "w") as fh:
         fh.write("\n".join(log))
     if verbose:
         print("\n".join(log))
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
