@@ -259,6 +259,7 @@ int stmg_level_restrict_residual(stmg_hierarchy* h, int32_t level, const double*
  *   STMG_FUSED_ZERO_PROLONG_SWEEP  y = S(S(0) + P x_coarse)
  *   STMG_FUSED_FINE_DOWN           y = S(x), f_coarse = R (f - J y), *norm2 = ||f - J x||^2
  *   STMG_FUSED_NORM_SWEEP          y = S(x), *norm2 = ||f - J x||^2 (the solve loop's norm pass)
+ *   STMG_FUSED_PROLONG_SWEEP       y = S(x + P x_coarse) (the first post-smoothing sweep)
  * Unused pointers may be null. */
 enum {
   STMG_FUSED_ZERO_SWEEP = 0,
@@ -266,7 +267,8 @@ enum {
   STMG_FUSED_ZERO_RESTRICT = 2,
   STMG_FUSED_ZERO_PROLONG_SWEEP = 3,
   STMG_FUSED_FINE_DOWN = 4,
-  STMG_FUSED_NORM_SWEEP = 5
+  STMG_FUSED_NORM_SWEEP = 5,
+  STMG_FUSED_PROLONG_SWEEP = 6
 };
 int stmg_level_fused(stmg_hierarchy* h, int32_t level, int32_t kind, const double* f, const double* x,
                      const double* x_coarse, double* y, double* f_coarse, double omega, double* norm2);

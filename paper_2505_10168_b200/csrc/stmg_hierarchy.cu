@@ -2236,7 +2236,7 @@ int stmg_level_fused(stmg_hierarchy* h, int32_t l, int32_t kind, const double* f
     if (h->galerkin(l)) throw std::invalid_argument("level_fused: per-node levels only");
     if (!f) throw std::invalid_argument("level_fused: null f");
     const bool coarse_op = kind == STMG_FUSED_ZERO_RESTRICT || kind == STMG_FUSED_ZERO_PROLONG_SWEEP ||
-                           kind == STMG_FUSED_FINE_DOWN;
+                           kind == STMG_FUSED_FINE_DOWN || kind == STMG_FUSED_PROLONG_SWEEP;
     if (coarse_op && (l + 1 >= h->n_levels() || h->gen_xfer(l)))
       throw std::out_of_range("level_fused: no fused transfer to a coarser level");
     DeviceGuard dg(h->device);
@@ -2274,6 +2274,11 @@ int stmg_level_fused(stmg_hierarchy* h, int32_t l, int32_t kind, const double* f
         if (norm2) *norm2 = sc[2];
         break;
       }
+      case STMG_FUSED_PROLONG_SWEEP:
+        if (!x || !y || !xc) throw std::invalid_argument("level_fused: null x / y / x_coarse");
+        launch_check(launch_sweep_prolong(h->adjoint, L, h->views[l + 1], h->dirs[l], f, x, xc, y, omega, h->stream),
+                     "sweep_prolong");
+        break;
       case STMG_FUSED_NORM_SWEEP: {
         if (!x || !y) throw std::invalid_argument("level_fused: null x / y");
         int64_t np = 0;

@@ -572,7 +572,7 @@ class LevelHierarchy:
         _check(_lib.stmg_hierarchy_set_fusion(self._h, int(flags)))
 
     (FUSED_ZERO_SWEEP, FUSED_ZERO_PAIR, FUSED_ZERO_RESTRICT, FUSED_ZERO_PROLONG_SWEEP, FUSED_FINE_DOWN,
-     FUSED_NORM_SWEEP) = range(6)
+     FUSED_NORM_SWEEP, FUSED_PROLONG_SWEEP) = range(7)
 
     def fused_kernel(self, l, kind, f, x=None, xc=None, y=None, fc=None, omega=0.5):
         """stmg_level_fused on device tensors; returns ||f - J x||^2 for FUSED_FINE_DOWN."""

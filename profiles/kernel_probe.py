@@ -56,11 +56,12 @@ def main():
         "prolong_sweep_zero": lambda: h.fused_kernel(0, H.FUSED_ZERO_PROLONG_SWEEP, f, xc=xc, y=y),
         "down": lambda: h.fused_kernel(0, H.FUSED_FINE_DOWN, f, x=x, y=y, fc=fc),
         "norm_sweep": lambda: h.fused_kernel(0, H.FUSED_NORM_SWEEP, f, x=x, y=y),
+        "prolong_sweep": lambda: h.fused_kernel(0, H.FUSED_PROLONG_SWEEP, f, x=x, xc=xc, y=y),
         "pair_zero": lambda: h.fused_kernel(0, H.FUSED_ZERO_PAIR, f, y=y),
     }
     # algorithmic bytes per fine DOF (coarse vectors are half size: 4 B per fine DOF)
     bytes_per_dof = {"sweep": 24, "pair": 24, "restrict": 20, "restrict_zero": 12, "prolong_sweep_zero": 20,
-                     "down": 28, "norm_sweep": 24, "pair_zero": 16}
+                     "down": 28, "norm_sweep": 24, "pair_zero": 16, "prolong_sweep": 28}
     if not a.time:
         for fn in forms.values():
             fn()

@@ -65,6 +65,11 @@ def test_virtual_zero_kernels_bitwise(torch, S, port, name, omega):
                        omega=omega)
         want = hp.sweeps(l, f, hp.prolong_add(l, xc, x1), 1, omega)
         assert np.array_equal(bits(y), bits(want)), (l, "prolong_sweep")
+        x = special_values(rng, n)
+        h.fused_kernel(l, S.LevelHierarchy.FUSED_PROLONG_SWEEP, ft, x=torch.from_numpy(x).to(dev),
+                       xc=torch.from_numpy(xc).to(dev), y=y, omega=omega)
+        want = hp.sweeps(l, f, hp.prolong_add(l, xc, x), 1, omega)
+        assert np.array_equal(bits(y), bits(want)), (l, "stored prolong_sweep")
 
 
 @pytest.mark.parametrize("nu", [1, 2, 3])
