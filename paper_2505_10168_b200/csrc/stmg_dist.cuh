@@ -813,7 +813,7 @@ void dist_build(stmg_dist* d, int world, int rank, const void* nccl_id, int64_t 
     }
     R.fg = std::make_unique<DeviceBuf>(d->ndofs(Lg));
     R.xg = std::make_unique<DeviceBuf>(d->ndofs(Lg));
-    R.partials = std::make_unique<DeviceBuf>(max_partials);
+    R.partials = std::make_unique<DeviceBuf>(max_partials + kPartialsScratch);
     R.scalars = std::make_unique<DeviceBuf>(8);
     d->device_bytes += 8 * (2 * d->ndofs(Lg) + max_partials + 8);
   }

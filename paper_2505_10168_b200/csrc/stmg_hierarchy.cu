@@ -847,7 +847,7 @@ std::shared_ptr<Workspace> make_workspace(const stmg_hierarchy* h, int64_t* byte
     if (l == 0 && nl > 1)
       max_partials = std::max(max_partials, down_partials_needed(finest_tiles, h->views[1], h->dirs[0]));
   }
-  ws->partials = std::make_unique<DeviceBuf>(max_partials);
+  ws->partials = std::make_unique<DeviceBuf>(max_partials + kPartialsScratch);
   ws->scalars = std::make_unique<DeviceBuf>(8);
   const int m = h->coarsest.m;
   const int64_t scratch = std::max<int64_t>(
@@ -1232,7 +1232,7 @@ int64_t emit_norm(stmg_hierarchy* h, int nu, const double* f, const double* x, d
   launch_norm_pass(h, nu, f, x, y, omega, h->stream, &np);
   launch_check(launch_finalize_sum(h->ws->partials->p, np, h->ws->scalars->p + slot, h->stream),
                "finalize");
-  return 2;
+  return 1 + finalize_launches(np);
 }
 
 double fetch_scalars(stmg_hierarchy* h, int count, double* out) {
@@ -1281,7 +1281,7 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
   int64_t np = 0;
   launch_check(launch_sumsq(B, n, ws.partials->p, &np, h->stream), "sumsq");
   launch_check(launch_finalize_sum(ws.partials->p, np, ws.scalars->p + 0, h->stream), "finalize");
-  launches += 2;
+  launches += 1 + finalize_launches(np);
   const bool spec = speculative(h, o.nu);
   GraphEntry* g = nullptr;
   if (o.max_cycles > 0) g = &get_graph(h, o.nu, o.omega);
@@ -1325,7 +1325,10 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
     rep->cycles = ctl->cycles;
     rep->status = ctl->status;
     rep->smoother_dof_updates = per_cycle_updates * ctl->cycles;
-    launches += static_cast<int64_t>(ctl->cycles) * (g->kernels + 2);
+    // per cycle: the V-cycle graph, the norm pass and its fixed-order sum
+    const int64_t norm_np = fine_down(h, o.nu) ? down_partials_needed(h->views[0], h->views[1], h->dirs[0])
+                                                : sweep_partials_needed(h->views[0]);
+    launches += static_cast<int64_t>(ctl->cycles) * (g->kernels + 1 + finalize_launches(norm_np));
   } else {
     rep->status = STMG_MAX_CYCLES;
     for (int cycle = 1; cycle <= o.max_cycles; ++cycle) {

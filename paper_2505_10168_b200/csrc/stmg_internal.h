@@ -208,6 +208,11 @@ int launch_coarsest(bool adjoint, const CoarsestView& cv, const double* f, doubl
 // Q = A^pint_len (column-major m x m) into P by m parallel homogeneous marches,
 // then its squares Q^2, Q^4, ... into P + m^2, P + 2 m^2, ... (rounds matrices in all)
 int launch_coarsest_pint_prop(const CoarsestView& cv, double* P, int rounds, cudaStream_t s);
+// Doubles every partials buffer holds past its largest partial count (the first
+// stage of a two-stage sum of many partials writes there).
+constexpr int64_t kPartialsScratch = 1184;
+// Kernel launches launch_finalize_sum / launch_finalize_check issue for n partials.
+inline int finalize_launches(int64_t n) { return n > (int64_t{1} << 16) ? 2 : 1; }
 // Sum of n_partials doubles in a fixed order into *out (device scalar).
 int launch_finalize_sum(const double* partials, int64_t n, double* out, cudaStream_t s);
 // Sum of squares of x[0..n) into partials (fixed grid) then *out.

@@ -443,9 +443,10 @@ __global__ void __launch_bounds__(kMaxTW, MINB) k_lean2(LevelView L, Ld ld,
   double acc = 0.0;
   if (tt < ceil_div(L.n_hi - L.n_lo, NT))
     acc = dev_lean2<ADJ, MODE, NORM, NT>(L, ld, f, y, omega, blockIdx.x, tt, blockDim.x);
-  if (NORM) {
-    const double s = block_sum(acc);
-    if (threadIdx.x == 0) partials[tt * gridDim.x + blockIdx.x] = s;
+  if (NORM) {  // one partial per warp (no block barrier), fixed order
+    for (int o = 16; o > 0; o >>= 1) acc = acc + __shfl_xor_sync(kFull, acc, o);
+    if ((threadIdx.x & 31) == 0)
+      partials[(tt * gridDim.x + blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)] = acc;
   }
 }
 
@@ -621,6 +622,11 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
 // warps; on small levels the few blocks never fill the SMs and the spills of the
 // tighter register budget cost latency, so 3 is used there (launch sites).
 constexpr int64_t kMinB5Dofs = 200000;
+// Resident blocks the 8-level norm-pass sweep (NORM) is compiled for
+// (compile-time A/B switch, profiles/ab_build.py).
+#ifndef STMG_NORM_MINB8
+#define STMG_NORM_MINB8 3
+#endif
 template <int NT>
 constexpr int minb_for_nt() { return NT <= 2 ? 5 : NT <= 4 ? 4 : 3; }
 
@@ -1331,65 +1337,63 @@ __global__ void k_square(const double* __restrict__ A, double* __restrict__ C, i
 //   t_n = (dk_dx (u0 - u1)) (l0 - l1),   s_n = dc_dx6 (l0 (2 v0 + v1) + l1 (v0 + 2 v1)),
 // v = (u_n - u_{n-1}) / dt, masked DOFs (n == 0, node 0) read as zero, are
 // accumulated in the reference's order acc = ((acc + t_1) + s_1) + t_2 + ....
-// The terms are independent, the sums are a chain, so a block owns 32 elements
-// (one per lane) and kSensWarps warps: every warp computes the terms of
-// kSensLv consecutive levels from coalesced row loads (u and lambda at nodes e
-// and e + 1, the previous level's u kept in registers) into shared memory, then
-// warp 0 adds the tile's terms in level order.  ceil(n_el / 32) blocks stream
-// u and lambda once (config 4: 128 blocks x 16 warps over 1.07 GB).
-constexpr int kSensWarps = 16, kSensLv = 4, kSensTile = kSensWarps * kSensLv;
+// The terms are independent, the sums are a chain.  A block owns kSensE = 16
+// elements: warps 1..kSensWarps-1 compute the terms of a tile of kSensTile
+// levels (a half warp per level, 16 consecutive elements = one 128-byte row
+// segment of u and lambda at nodes e and e + 1) into one of two shared-memory
+// buffers, while warp 0 adds the previous tile's terms in level order (double
+// buffering: loads and the sequential chain overlap).  ceil(n_el / 16) blocks
+// stream u and lambda once (config 4: 256 blocks over 1.07 GB).
+constexpr int kSensE = 16, kSensWarps = 16, kSensLv = 3;
+constexpr int kSensTile = (kSensWarps - 1) * 2 * kSensLv;  // levels per tile (90; 46 KB of buffers)
 __global__ void __launch_bounds__(kSensWarps * 32) k_sensitivities(
     int64_t n_el, int64_t n_t, double dt, const double* __restrict__ dk_dx, const double* __restrict__ dc_dx6,
     const double* __restrict__ u, const double* __restrict__ lam, double* __restrict__ sens) {
   pdl_entry();
-  __shared__ double terms[2][kSensTile][32];
+  __shared__ double terms[2][2][kSensTile][kSensE];  // [buffer][t / s][level][element]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t e = (int64_t)blockIdx.x * 32 + lane;
+  const int el = lane & (kSensE - 1), half = lane >> 4;
+  const int64_t e = (int64_t)blockIdx.x * kSensE + el;
   const bool active = e < n_el;
   const bool lm = e == 0;  // node i = e is the Dirichlet node
   const int64_t nn = n_el + 1;
   const double kd = active ? dk_dx[e] : 0.0, cd = active ? dc_dx6[e] : 0.0;
+  const int64_t tiles = (n_t + kSensTile - 1) / kSensTile;
   double acc = 0.0;
-  for (int64_t base = 1; base <= n_t; base += kSensTile) {
-    const int64_t n0 = base + (int64_t)warp * kSensLv;
-    double U0[kSensLv], U1[kSensLv], L0[kSensLv], L1[kSensLv], P0 = 0.0, P1 = 0.0;
-    if (active && n0 <= n_t) {
-      if (n0 - 1 >= 1) {  // level n0 - 1 (level 0 is masked)
-        const int64_t r = (n0 - 1) * nn + e;
-        P0 = lm ? 0.0 : __ldg(u + r);
-        P1 = __ldg(u + r + 1);
-      }
+  for (int64_t t = 0; t <= tiles; ++t) {
+    if (warp > 0 && t < tiles && active) {  // terms of tile t into buffer t & 1
+      double(*T)[kSensTile][kSensE] = terms[t & 1];
 #pragma unroll
       for (int k = 0; k < kSensLv; ++k) {
-        const int64_t n = n0 + k <= n_t ? n0 + k : n_t;
+        const int j = ((warp - 1) * kSensLv + k) * 2 + half;  // level slot within the tile
+        const int64_t n = 1 + t * kSensTile + j;
+        if (n > n_t) continue;
         const int64_t r = n * nn + e;
-        U0[k] = lm ? 0.0 : __ldg(u + r);
-        U1[k] = __ldg(u + r + 1);
-        L0[k] = lm ? 0.0 : __ldg(lam + r);
-        L1[k] = __ldg(lam + r + 1);
-      }
-#pragma unroll
-      for (int k = 0; k < kSensLv; ++k) {
-        const double u0 = U0[k], u1 = U1[k], l0 = L0[k], l1 = L1[k];
-        const double v0 = (u0 - P0) / dt;
-        const double v1 = (u1 - P1) / dt;
-        terms[0][warp * kSensLv + k][lane] = (kd * (u0 - u1)) * (l0 - l1);
-        terms[1][warp * kSensLv + k][lane] = cd * (l0 * (2.0 * v0 + v1) + l1 * (v0 + 2.0 * v1));
-        P0 = u0;
-        P1 = u1;
+        const double u0 = lm ? 0.0 : __ldg(u + r), u1 = __ldg(u + r + 1);
+        const double l0 = lm ? 0.0 : __ldg(lam + r), l1 = __ldg(lam + r + 1);
+        double p0 = 0.0, p1 = 0.0;  // level n - 1 (level 0 is masked)
+        if (n >= 2) {
+          p0 = lm ? 0.0 : __ldg(u + r - nn);
+          p1 = __ldg(u + r - nn + 1);
+        }
+        const double v0 = (u0 - p0) / dt;
+        const double v1 = (u1 - p1) / dt;
+        T[0][j][el] = (kd * (u0 - u1)) * (l0 - l1);
+        T[1][j][el] = cd * (l0 * (2.0 * v0 + v1) + l1 * (v0 + 2.0 * v1));
       }
     }
-    __syncthreads();
-    if (warp == 0 && active) {
-      const int cnt = n_t - base + 1 < kSensTile ? (int)(n_t - base + 1) : kSensTile;
+    if (warp == 0 && t > 0 && half == 0 && active) {  // tile t - 1, in level order
+      double(*T)[kSensTile][kSensE] = terms[(t - 1) & 1];
+      const int64_t first = 1 + (t - 1) * kSensTile;
+      const int cnt = n_t - first + 1 < kSensTile ? (int)(n_t - first + 1) : kSensTile;
       for (int j = 0; j < cnt; ++j) {
-        acc = acc + terms[0][j][lane];
-        acc = acc + terms[1][j][lane];
+        acc = acc + T[0][j][el];
+        acc = acc + T[1][j][el];
       }
     }
     __syncthreads();
   }
-  if (warp == 0 && active) sens[e] = -acc;
+  if (warp == 0 && half == 0 && active) sens[e] = -acc;
 }
 
 __global__ void k_dot(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
@@ -1609,6 +1613,16 @@ __global__ void k_finalize_sum(const double* __restrict__ partials, int64_t n, d
   if (threadIdx.x == 0) *out = s;
 }
 
+// First stage of a two-stage fixed-order sum of many partials: block b adds
+// entries [b chunk, (b + 1) chunk) into out[b].
+__global__ void k_partials_stage(const double* __restrict__ partials, int64_t n, int64_t chunk, double* out) {
+  pdl_entry();
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t cnt = lo >= n ? 0 : (n - lo < chunk ? n - lo : chunk);
+  const double s = partials_sum(partials + lo, cnt);
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
 // k_finalize_sum into scalars[1], then the cycle bookkeeping (one launch less
 // per cycle of the device-side solve loop).
 __global__ void k_finalize_check(const double* __restrict__ partials, int64_t n, double* scalars,
@@ -1670,7 +1684,8 @@ void launch_pass(const LevelView& L, const Ld& ld, const double* f, double* y, d
   else if (lean_nt(L) == 4)
     pdl_launch(k_lean2<ADJ, MODE, NORM, 4, 4, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
   else
-    pdl_launch(k_lean2<ADJ, MODE, NORM, 8, 3, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
+    pdl_launch(k_lean2<ADJ, MODE, NORM, 8, NORM ? STMG_NORM_MINB8 : 3, Ld>, grd, blk, 0, s, L, ld, f, y, omega,
+               partials);
 }
 
 inline ZeroLoad zero_load(const LevelView& L, const double* f, double omega) {
@@ -1740,8 +1755,8 @@ int restrict_impl(const LevelView& F, const LevelView& C, const double* f, const
 }  // namespace
 
 int64_t sweep_partials_needed(const LevelView& L) {
-  const dim3 g = pass_grid(L, pass_block(L));
-  return (int64_t)g.x * g.y * g.z;
+  const dim3 b = pass_block(L), g = pass_grid(L, b);
+  return (int64_t)g.x * g.y * g.z * (b.x / 32);  // one per warp
 }
 
 int64_t sumsq_partials_needed(int64_t) { return kSumGrid; }
@@ -1974,23 +1989,40 @@ int kernels_init() {
   return static_cast<int>(e);
 }
 
+namespace {
+// More than this many partials are summed in two stages (kPartialsScratch blocks,
+// then one), through the scratch doubles every partials buffer has past its end.
+constexpr int64_t kOneStagePartials = int64_t{1} << 16;  // finalize_launches agrees
+const double* stage_partials(const double* partials, int64_t* n, cudaStream_t s) {
+  if (*n <= kOneStagePartials) return partials;
+  const int64_t chunk = ceil_div(*n, kPartialsScratch);
+  const unsigned blocks = (unsigned)ceil_div(*n, chunk);
+  double* scratch = const_cast<double*>(partials) + *n;
+  pdl_launch(k_partials_stage, blocks, 256, 0, s, partials, *n, chunk, scratch);
+  *n = blocks;
+  return scratch;
+}
+}  // namespace
+
 int launch_finalize_sum(const double* partials, int64_t n, double* out, cudaStream_t s) {
-  pdl_launch(k_finalize_sum, 1, 1024, 0, s, partials, n, out);
+  const double* p = stage_partials(partials, &n, s);
+  pdl_launch(k_finalize_sum, 1, 1024, 0, s, p, n, out);
   return check_launch();
 }
 
 int launch_finalize_check(const double* partials, int64_t n, double* scalars, SolveLoopCtl* ctl, double* hist,
                           cudaGraphConditionalHandle handle, cudaStream_t s) {
-  pdl_launch(k_finalize_check, 1, 1024, 0, s, partials, n, scalars, ctl, hist, handle);
+  const double* p = stage_partials(partials, &n, s);
+  pdl_launch(k_finalize_check, 1, 1024, 0, s, p, n, scalars, ctl, hist, handle);
   return check_launch();
 }
 
 int launch_sensitivities(int64_t n_el, int64_t n_t, double dt, const double* dk_dx,
                          const double* dc_dx6, const double* u, const double* lam, double* sens,
                          cudaStream_t s) {
-  // one block of kSensWarps warps per 32 elements
-  pdl_launch(k_sensitivities, (unsigned)((n_el + 31) / 32), kSensWarps * 32, 0, s, n_el, n_t, dt, dk_dx, dc_dx6, u,
-             lam, sens);
+  // one block of kSensWarps warps per kSensE elements
+  pdl_launch(k_sensitivities, (unsigned)((n_el + kSensE - 1) / kSensE), kSensWarps * 32, 0, s, n_el, n_t, dt, dk_dx,
+             dc_dx6, u, lam, sens);
   return check_launch();
 }
 

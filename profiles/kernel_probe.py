@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--time", action="store_true")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--tiles", type=int, default=0, help="force 4- or 2-level time tiles (0: default tiling)")
+    ap.add_argument("--only", default="", help="comma-separated subset of the forms")
     a = ap.parse_args()
     import torch
 
@@ -62,6 +63,8 @@ def main():
     # algorithmic bytes per fine DOF (coarse vectors are half size: 4 B per fine DOF)
     bytes_per_dof = {"sweep": 24, "pair": 24, "restrict": 20, "restrict_zero": 12, "prolong_sweep_zero": 20,
                      "down": 28, "norm_sweep": 24, "pair_zero": 16, "prolong_sweep": 28}
+    if a.only:
+        forms = {k: v for k, v in forms.items() if k in a.only.split(",")}
     if not a.time:
         for fn in forms.values():
             fn()
