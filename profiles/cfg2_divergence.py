@@ -55,21 +55,31 @@ def main():
     for gs in a.guards.split(","):
         M = base.n_el if gs == "full" else int(gs)
         if a.where == "gpu":
-            req = S.PlanRequest(n_levels=a.n_levels, strategy=S.PlanStrategy(base.strategy),
-                                reassembly=S.ReassemblyMethod(base.reassembly), min_elements=M)
-            try:
-                path = S.plan_coarsening(g, req)
-            except Exception as e:  # an impossible plan is a result too
-                print(json.dumps({"M": M, "error": str(e)}), flush=True)
+            path = None
+            for nl in range(a.n_levels, 1, -1):  # the deepest plan the guard allows
+                req = S.PlanRequest(n_levels=nl, strategy=S.PlanStrategy(base.strategy),
+                                    reassembly=S.ReassemblyMethod(base.reassembly), min_elements=M)
+                try:
+                    path = S.plan_coarsening(g, req)
+                    break
+                except Exception:
+                    continue
+            if path is None:
+                print(json.dumps({"M": M, "error": "no legal plan"}), flush=True)
                 continue
             dirs = [int(d) for d in path.dirs]
             h = S.build_hierarchy(g, base.method, path)
         else:
-            try:
-                dirs, _ = ref.plan(base.L, base.t_T, base.n_el, base.n_t, base.k, base.c, a.n_levels,
-                                   strategy=base.strategy, reassembly=base.reassembly, min_elements=M)
-            except Exception as e:
-                print(json.dumps({"M": M, "error": str(e)}), flush=True)
+            dirs = None
+            for nl in range(a.n_levels, 1, -1):  # the deepest plan the guard allows
+                try:
+                    dirs, _ = ref.plan(base.L, base.t_T, base.n_el, base.n_t, base.k, base.c, nl,
+                                       strategy=base.strategy, reassembly=base.reassembly, min_elements=M)
+                    break
+                except Exception:
+                    continue
+            if dirs is None:
+                print(json.dumps({"M": M, "error": "no legal plan"}), flush=True)
                 continue
             dirs = [int(d) for d in dirs]
             h = ref.hierarchy(base.L, base.t_T, base.n_el, base.n_t, base.k, base.c, dirs, method=base.method)
