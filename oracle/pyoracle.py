@@ -46,7 +46,7 @@ def build_ref() -> str | None:
     if os.path.isdir(REF_SRC):
         subprocess.check_call(["make", "-s", "-j8", "-C", HERE, "ref"])
         if os.path.exists(os.path.join(os.path.dirname(HERE), "paper_2505_10168_b200", "libstmg_b200.so")):
-            subprocess.check_call(["make", "-s", "-C", HERE, "dropin"])
+            subprocess.check_call(["make", "-s", "-j8", "-C", HERE, "dropin", "acceptance"])
     return REF_SO if os.path.exists(REF_SO) else None
 
 

@@ -136,10 +136,28 @@ class Subcase {
   std::vector<int> key_;
 };
 
-inline int run_all() {
+// Comma-separated name filters, as doctest's --test-case= / --test-case-exclude=
+// (substring match here, no wildcards).
+inline bool name_matches(const char* name, const std::string& list) {
+  std::size_t a = 0;
+  while (a <= list.size()) {
+    std::size_t b = list.find(',', a);
+    if (b == std::string::npos) b = list.size();
+    const std::string item = list.substr(a, b - a);
+    if (!item.empty() && std::strstr(name, item.c_str()) != nullptr) return true;
+    a = b + 1;
+  }
+  return false;
+}
+
+inline int run_all(const std::string& only = "", const std::string& exclude = "") {
   State& s = state();
   int failed_cases = 0;
+  std::size_t ran = 0;
   for (const TestCase& tc : s.tests) {
+    if (!only.empty() && !name_matches(tc.name, only)) continue;
+    if (!exclude.empty() && name_matches(tc.name, exclude)) continue;
+    ++ran;
     s.done.clear();
     s.current_failed = false;
     s.current_name = tc.name;
@@ -162,13 +180,16 @@ inline int run_all() {
         if (s.progress) s.rerun = true;
       }
     } while (s.rerun && ++passes < 10000);
-    if (s.current_failed) ++failed_cases;
+    if (s.current_failed) {
+      ++failed_cases;
+      std::fprintf(stderr, "[doctest-shim] FAILED test case: %s\n", tc.name);
+    }
   }
   std::fprintf(stderr,
-               "[doctest-shim] test cases: %zu | %zu passed | %d failed; assertions: %ld | %ld "
+               "[doctest-shim] test cases: %zu | %zu passed | %d failed | %zu skipped; assertions: %ld | %ld "
                "failed\n",
-               s.tests.size(), s.tests.size() - static_cast<std::size_t>(failed_cases),
-               failed_cases, s.assertions, s.failed_assertions);
+               ran, ran - static_cast<std::size_t>(failed_cases), failed_cases, s.tests.size() - ran,
+               s.assertions, s.failed_assertions);
   return failed_cases;
 }
 
@@ -246,5 +267,13 @@ inline int run_all() {
 #define MESSAGE(...) ((void)0)
 
 #ifdef DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
-int main() { return ::mini_doctest::run_all() ? 1 : 0; }
+int main(int argc, char** argv) {
+  std::string only, exclude;
+  for (int i = 1; i < argc; ++i) {
+    const std::string arg = argv[i];
+    if (arg.rfind("--test-case=", 0) == 0) only = arg.substr(12);
+    else if (arg.rfind("--test-case-exclude=", 0) == 0) exclude = arg.substr(20);
+  }
+  return ::mini_doctest::run_all(only, exclude) ? 1 : 0;
+}
 #endif
