@@ -376,12 +376,6 @@ void stmg_dist_destroy(stmg_dist* d);
  * rest 8-level tiles.  Values <= 0 restore the defaults (5,000,000 / 600,000).
  * Captured V-cycle graphs of the handle are rebuilt on the next solve. */
 int stmg_hierarchy_set_tiling(stmg_hierarchy* h, int64_t small_dofs, int64_t tiny_dofs);
-/* Levels of at least min_dofs DOFs run their single-sweep, prolong-sweep and
- * residual-restriction kernels on the streaming-march chassis (warp-private
- * cp.async rings in shared memory, csrc/stmg_march.cuh) instead of the
- * register-staged tiles; bit-identical results.  min_dofs <= 0 restores the
- * default threshold; 1 selects the chassis on every level (tests). */
-int stmg_hierarchy_set_march(stmg_hierarchy* h, int64_t min_dofs);
 /* Per-handle V-cycle fusions (A/B measurements and bitwise tests; default
  * STMG_FUSE_DEFAULT = STMG_FUSE_VIRTUAL_ZERO, the combination measured fastest).
  * Every combination gives bit-identical iterates.

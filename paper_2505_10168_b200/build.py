@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libstmg_b200.so")
 SOURCES = ["stmg_kernels.cu", "stmg_general.cu", "stmg_hierarchy.cu"]
-HEADERS = ["stmg_internal.h", "stmg_dist.cuh", "stmg_galerkin.h", "stmg_march.cuh", os.path.join("..", "..", "include", "stmg_b200.h")]
+HEADERS = ["stmg_internal.h", "stmg_dist.cuh", "stmg_galerkin.h", os.path.join("..", "..", "include", "stmg_b200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -748,13 +748,6 @@ constexpr int64_t kTinyNtDofs = 600000;  // measured: cfg1 solve 53.3 -> 50.8 ms
 int64_t tile_nt_for(int64_t dofs, int64_t small = kSmallNtDofs, int64_t tiny = kTinyNtDofs) {
   return dofs <= tiny ? 2 : dofs <= small ? 4 : 8;
 }
-// Levels with at least this many DOFs run the single-sweep, prolong-sweep and
-// residual-restriction kernels on the streaming-march chassis (stmg_march.cuh);
-// per handle: stmg_hierarchy_set_march.
-#ifndef STMG_MARCH_DOFS
-#define STMG_MARCH_DOFS INT64_MAX
-#endif
-constexpr int64_t kMarchDofs = STMG_MARCH_DOFS;
 
 // Device tables of the general coarse discretisations: Galerkin levels' 9-point
 // operators (transposed for an adjoint hierarchy, proj/src/multigrid.cpp:145-160),
@@ -829,7 +822,6 @@ void upload_levels(stmg_hierarchy* h) {
     v.n_lo = 0;
     v.n_hi = hl.g.n_t + 1;
     v.tile_nt = tile_nt_for(v.nn * (v.n_t + 1));
-    v.march = v.nn * (v.n_t + 1) >= kMarchDofs ? 1 : 0;
     h->views.push_back(v);
     h->device_bytes += static_cast<int64_t>((t.size() + kVecPad) * 8);
     h->coef.push_back(std::move(buf));
@@ -877,7 +869,7 @@ void finish_create(stmg_hierarchy* h, bool share_ws_from_other, const stmg_hiera
   if (share_ws_from_other) {
     // same tiling as the hierarchy whose workspace (norm partials) is shared
     for (size_t l = 0; l < h->views.size() && l < other->views.size(); ++l)
-      h->views[l].tile_nt = other->views[l].tile_nt, h->views[l].march = other->views[l].march;
+      h->views[l].tile_nt = other->views[l].tile_nt;
     h->ws = other->ws;
   } else {
     int64_t bytes = 0;
@@ -2070,19 +2062,6 @@ int stmg_hierarchy_set_tiling(stmg_hierarchy* h, int64_t small_dofs, int64_t tin
     const int64_t small = small_dofs > 0 ? small_dofs : kSmallNtDofs;
     const int64_t tiny = tiny_dofs > 0 ? tiny_dofs : kTinyNtDofs;
     for (auto& v : h->views) v.tile_nt = tile_nt_for(v.nn * (v.n_t + 1), small, tiny);
-    h->coarsest.lv = h->views.back();
-    for (auto& kv : h->graphs) destroy_graph_entry(kv.second);
-    h->graphs.clear();
-  });
-}
-
-int stmg_hierarchy_set_march(stmg_hierarchy* h, int64_t min_dofs) {
-  return guarded([&] {
-    checked(h);
-    DeviceGuard dg(h->device);
-    cuda_check(cudaStreamSynchronize(h->stream), "sync");
-    const int64_t lim = min_dofs > 0 ? min_dofs : kMarchDofs;
-    for (auto& v : h->views) v.march = v.nn * (v.n_t + 1) >= lim ? 1 : 0;
     h->coarsest.lv = h->views.back();
     for (auto& kv : h->graphs) destroy_graph_entry(kv.second);
     h->graphs.clear();

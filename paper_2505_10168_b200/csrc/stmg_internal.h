@@ -29,9 +29,6 @@ struct LevelView {
   // Time levels per tile of the overlapping-warp kernels (8, or 4 / 2 on small,
   // latency-bound levels); fixed when the hierarchy is built.
   int64_t tile_nt = 8;
-  // Streaming-march chassis (stmg_march.cuh) instead of the register-staged tiles:
-  // set on levels of at least kMarchDofs DOFs (stmg_hierarchy_set_march).
-  int32_t march = 0;
 };
 
 inline bool full_range(const LevelView& L) { return L.n_lo == 0 && L.n_hi == L.n_t + 1; }

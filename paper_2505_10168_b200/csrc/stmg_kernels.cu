@@ -72,15 +72,6 @@ __device__ __forceinline__ T* opaque(T* p) {
   return p;
 }
 
-// L2 prefetch of the rows a later time tile of the same node strip will read
-// (compile-time A/B switch: STMG_PF_TILES time tiles ahead, 0 = off).
-#ifndef STMG_PF_TILES
-#define STMG_PF_TILES 0
-#endif
-__device__ __forceinline__ void prefetch_l2(const double* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
 __device__ __forceinline__ void st_global(double* p, double v) {
   asm volatile("st.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
@@ -225,11 +216,6 @@ struct PlainLoad {
     return {__ldg(l.xb + (uint32_t)r * nn32)};
   }
   __device__ __forceinline__ double finish(const Raw& w, const Lane&, int64_t, double) const { return w.x; }
-  // L2 prefetch of staged rows pf_rows + 1 .. pf_rows + nt (a later tile's)
-  __device__ __forceinline__ void prefetch(const Lane& l, uint32_t pf_rows, uint32_t nn32, int nt) const {
-#pragma unroll
-    for (int k = 0; k < nt; ++k) prefetch_l2(l.xb + (pf_rows + (uint32_t)(k + 1)) * nn32);
-  }
 };
 
 struct ZeroLoad {
@@ -258,7 +244,6 @@ struct ZeroLoad {
   __device__ __forceinline__ double finish(const Raw& w, const Lane&, int64_t, double invd_i) const {
     return zero_sweep(w.f, invd_i, omega);
   }
-  __device__ __forceinline__ void prefetch(const Lane&, uint32_t, uint32_t, int) const {}  // f is prefetched by the tile
 };
 
 // x + P xc at the staged rows (csr_spmv_add, proj/src/transfer.cpp:74-88), the
@@ -316,17 +301,6 @@ struct ProlongOn {
     const double pe = 0.0 + 1.0 * w.a;
     const double po = (0.5 * w.a + 0.5 * w.c) + 0.0;
     return x + (l.odd ? po : pe);
-  }
-  __device__ __forceinline__ void prefetch(const Lane& l, uint32_t pf_rows, uint32_t nn32, int nt) const {
-    base.prefetch(l.b, pf_rows, nn32, nt);
-    const uint32_t nnc32 = (uint32_t)nnc;
-    if (DIR == 0) {
-#pragma unroll
-      for (int k = 0; k < nt; ++k) prefetch_l2(l.cb + (pf_rows + (uint32_t)(k + 1)) * nnc32);
-    } else {
-#pragma unroll
-      for (int k = 0; k < nt; k += 2) prefetch_l2(l.cb + ((l.odd + pf_rows + (uint32_t)(k + 1)) >> 1) * nnc32);
-    }
   }
 };
 template <int DIR>
@@ -390,14 +364,6 @@ __device__ __forceinline__ double dev_lean2(const LevelView& L, const Ld& ld, co
     typename Ld::Raw raw[NT + 1];
 #pragma unroll
     for (int r = 0; r <= NT; ++r) raw[r] = ld.load(lc, r, nn32);
-#if STMG_PF_TILES > 0
-    if (n0 + (STMG_PF_TILES + 1) * NT <= nt) {
-      const uint32_t pf0 = (uint32_t)(STMG_PF_TILES * NT) * nn32;
-#pragma unroll
-      for (int k = 0; k < NT; ++k) prefetch_l2(fp + (pf0 + (uint32_t)k * nn32));
-      ld.prefetch(lc, (uint32_t)(STMG_PF_TILES * NT), nn32, NT);
-    }
-#endif
     const Coefs c = load_coefs(L, i);
 #pragma unroll
     for (int r = 0; r <= NT; ++r) xr[r] = ld.finish(raw[r], lc, i, c.invd);
@@ -691,8 +657,6 @@ __device__ __forceinline__ double coarse_from_zero(const LevelView& C, int64_t N
   return 0.0 + omega * (fv * id);
 }
 
-#include "stmg_march.cuh"
-
 // ZX: x is S(0) = 0 + omega (f * inv_diag), recomputed from f (x is not read).
 template <bool ADJ, int DIR, int NT, bool ZX = false>
 __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelView& C,
@@ -724,21 +688,7 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
       const double* __restrict__ xp = opaque(x + (nbase * nn + i));
 #pragma unroll
       for (int r = 0; r <= NT; ++r) xr[r] = __ldg(xp + (uint32_t)r * nn32);
-#if STMG_PF_TILES > 0
-      if (n0 + (STMG_PF_TILES + 1) * NT <= nt) {
-        const uint32_t pf0 = (uint32_t)(STMG_PF_TILES * NT) * nn32;
-#pragma unroll
-        for (int k = 0; k < NT; ++k) prefetch_l2(xp + (pf0 + (uint32_t)(k + 1) * nn32));
-      }
-#endif
     }
-#if STMG_PF_TILES > 0
-    if (n0 + (STMG_PF_TILES + 1) * NT <= nt) {
-      const uint32_t pf0 = (uint32_t)(STMG_PF_TILES * NT) * nn32;
-#pragma unroll
-      for (int k = 0; k < NT; ++k) prefetch_l2(fp + (pf0 + (uint32_t)k * nn32));
-    }
-#endif
     const Coefs c = load_coefs(F, i);
     if (ZX) {
       // staged level nbase + r: f row r - 1 (J) / r (J^T)
@@ -1094,10 +1044,11 @@ __device__ __forceinline__ double dev_down(const LevelView& F, const LevelView& 
   return acc;
 }
 
-// Resident 256-thread blocks per SM k_down is compiled for (it stages one
-// level more than the pair and holds both stages: fewer blocks, no spills).
+// Resident 256-thread blocks per SM k_down is compiled for.  8-level tiles: 3
+// (80 registers, ~100 B of spills) measured faster than 2 (126 registers, no
+// spills): 0.92 vs 1.00 ms on 1.3e8 DOFs (profiles/round2_march_experiment.md).
 template <int NT>
-constexpr int down_minb() { return NT <= 2 ? 4 : NT <= 4 ? 3 : 2; }
+constexpr int down_minb() { return NT <= 2 ? 4 : 3; }
 
 template <bool ADJ, int DIR, int NT, int MINB = down_minb<NT>()>
 __global__ void __launch_bounds__(kMaxTW, MINB) k_down(LevelView F, LevelView C, const double* __restrict__ f,
@@ -1723,33 +1674,6 @@ inline dim3 pass_grid(const LevelView& L, dim3 blk) {
 }
 inline unsigned flat_grid(int64_t total) { return (unsigned)((total + kFlatBlock - 1) / kFlatBlock); }
 
-// ---- streaming-march chassis (stmg_march.cuh): levels with LevelView::march set
-#ifndef STMG_MARCH_MINB
-#define STMG_MARCH_MINB 8
-#endif
-inline int64_t march_strips(const LevelView& L, bool x_restrict) { return ceil_div(L.nn, x_restrict ? 30 : 32); }
-// rows per warp chunk: even, 16..256, small enough for ~8 blocks per resident slot
-inline int32_t march_chunk(const LevelView& L, bool x_restrict) {
-  const int64_t gx = ceil_div(march_strips(L, x_restrict), march::kWarps);
-  const int64_t want = 148 * STMG_MARCH_MINB * 4;  // blocks
-  int64_t chunks = ceil_div(want, gx);
-  if (chunks < 1) chunks = 1;
-  int64_t ch = rows(L) / chunks;
-  ch = ch < 16 ? 16 : ch > 256 ? 256 : ch;
-  return (int32_t)(ch & ~int64_t{1});
-}
-inline dim3 march_grid(const LevelView& L, bool x_restrict) {
-  return dim3((unsigned)ceil_div(march_strips(L, x_restrict), march::kWarps),
-              (unsigned)ceil_div(rows(L), march_chunk(L, x_restrict)));
-}
-template <bool ADJ, int SRC, int PDIR, int OUT, int RDIR, bool NORM>
-void march_launch(march::Args a, cudaStream_t s) {
-  constexpr bool xr = OUT == march::kOutRestrict && RDIR == 0;
-  a.chunk = march_chunk(a.F, xr);
-  pdl_launch(march::k_march<ADJ, SRC, PDIR, OUT, RDIR, NORM, STMG_MARCH_MINB>, march_grid(a.F, xr),
-             dim3(march::kWarps * 32), 0, s, a);
-}
-
 template <bool ADJ, int MODE, bool NORM, class Ld>
 void launch_pass(const LevelView& L, const Ld& ld, const double* f, double* y, double omega,
                  double* partials, cudaStream_t s) {
@@ -1772,18 +1696,6 @@ inline ZeroLoad zero_load(const LevelView& L, const double* f, double omega) {
 template <bool ADJ>
 int sweep_impl(const LevelView& L, const double* f, const double* x, double* y, double omega,
                double* partials, cudaStream_t s) {
-  if (L.march) {
-    march::Args a{L, L, f, x, nullptr, y, nullptr, nullptr, partials, omega, 0};
-    if (x == nullptr) {  // x = S(0), recomputed from f
-      if (y == nullptr || partials != nullptr) return static_cast<int>(cudaErrorInvalidValue);
-      march_launch<ADJ, march::kSrcZero, 0, march::kOutSweep, 0, false>(a, s);
-    } else if (partials != nullptr) {
-      march_launch<ADJ, march::kSrcPlain, 0, march::kOutSweep, 0, true>(a, s);
-    } else {
-      march_launch<ADJ, march::kSrcPlain, 0, march::kOutSweep, 0, false>(a, s);
-    }
-    return check_launch();
-  }
   if (x == nullptr) {  // x = S(0), recomputed from f
     if (y == nullptr || partials != nullptr) return static_cast<int>(cudaErrorInvalidValue);
     launch_pass<ADJ, kSweep, false>(L, zero_load(L, f, omega), f, y, omega, partials, s);
@@ -1802,12 +1714,6 @@ int sweep_impl(const LevelView& L, const double* f, const double* x, double* y, 
 template <bool ADJ, int DIR>
 int sweep_prolong_impl(const LevelView& L, const LevelView& C, const double* f, const double* x,
                        const double* xc, double* y, double omega, cudaStream_t s) {
-  if (L.march) {
-    march::Args a{L, C, f, x, xc, y, nullptr, nullptr, nullptr, omega, 0};
-    if (x == nullptr) march_launch<ADJ, march::kSrcProlongZ, DIR, march::kOutSweep, 0, false>(a, s);
-    else march_launch<ADJ, march::kSrcProlong, DIR, march::kOutSweep, 0, false>(a, s);
-    return check_launch();
-  }
   if (x == nullptr) {  // fine iterate S(0), recomputed from f
     const ProlongZeroLoad<DIR> ld{zero_load(L, f, omega), xc, C.nn};
     launch_pass<ADJ, kSweep, false>(L, ld, f, y, omega, nullptr, s);
@@ -1825,13 +1731,6 @@ void restrict_launch(const LevelView& F, const LevelView& C, const double* f, co
   const int64_t warps = DIR == 0 ? ceil_div(C.nn, 14) : ceil_div(F.nn, 30);
   const dim3 rb = balanced_block(warps, wpb_for(F));
   const int64_t tiles = ceil_div(warps, rb.x / 32);
-#ifdef STMG_ZX_NT16
-  if (ZX && lean_nt(F) == 8) {
-    pdl_launch(k_restrict2<ADJ, DIR, 16, STMG_ZX_NT16, ZX>, tgrid(tiles, (rows(F) + 15) / 16), rb, 0, s, F, C, f, x,
-               fc, xc0, omega);
-    return;
-  }
-#endif
   if (lean_nt(F) == 2 && F.nn * (F.n_t + 1) >= kMinB5Dofs)
     pdl_launch(k_restrict2<ADJ, DIR, 2, minb_for_nt<2>(), ZX>, tgrid(tiles, (rows(F) + 1) / 2), rb, 0, s, F, C,
                f, x, fc, xc0, omega);
@@ -1849,12 +1748,6 @@ void restrict_launch(const LevelView& F, const LevelView& C, const double* f, co
 template <bool ADJ, int DIR>
 int restrict_impl(const LevelView& F, const LevelView& C, const double* f, const double* x,
                   double* fc, cudaStream_t s, double* xc0, double omega) {
-  if (F.march) {
-    march::Args a{F, C, f, x, nullptr, nullptr, fc, xc0, nullptr, omega, 0};
-    if (x == nullptr) march_launch<ADJ, march::kSrcZero, 0, march::kOutRestrict, DIR, false>(a, s);
-    else march_launch<ADJ, march::kSrcPlain, 0, march::kOutRestrict, DIR, false>(a, s);
-    return check_launch();
-  }
   if (x == nullptr) restrict_launch<ADJ, DIR, true>(F, C, f, x, fc, s, xc0, omega);  // x = S(0) from f
   else restrict_launch<ADJ, DIR, false>(F, C, f, x, fc, s, xc0, omega);
   return check_launch();
@@ -1863,10 +1756,6 @@ int restrict_impl(const LevelView& F, const LevelView& C, const double* f, const
 }  // namespace
 
 int64_t sweep_partials_needed(const LevelView& L) {
-  if (L.march) {
-    const dim3 g = march_grid(L, false);
-    return (int64_t)g.x * g.y * march::kWarps;  // one per warp
-  }
   const dim3 b = pass_block(L), g = pass_grid(L, b);
   return (int64_t)g.x * g.y * g.z * (b.x / 32);  // one per warp
 }

@@ -81,7 +81,6 @@ def _load():
         "stmg_norm2": [vp, vp, i64, C.POINTER(f64)],
         "stmg_synchronize": [vp],
         "stmg_hierarchy_set_tiling": [vp, i64, i64],
-        "stmg_hierarchy_set_march": [vp, i64],
         "stmg_hierarchy_set_fusion": [vp, i32],
         "stmg_objective_sensitivities": [vp, vp, vp, vp, vp, vp, i32],
         "stmg_level_fused": [vp, i32, i32, vp, vp, vp, vp, vp, f64, C.POINTER(f64)],
@@ -565,11 +564,6 @@ class LevelHierarchy:
     def set_tiling(self, small_dofs=0, tiny_dofs=0):
         """Per-handle time-tile thresholds (stmg_hierarchy_set_tiling; 0 = defaults)."""
         _check(_lib.stmg_hierarchy_set_tiling(self._h, int(small_dofs), int(tiny_dofs)))
-
-    def set_march(self, min_dofs=0):
-        """Streaming-march chassis on levels of >= min_dofs DOFs (stmg_hierarchy_set_march;
-        0 = default threshold, 1 = every level)."""
-        _check(_lib.stmg_hierarchy_set_march(self._h, int(min_dofs)))
 
     FUSE_VIRTUAL_ZERO, FUSE_FINE_DOWN, FUSE_ALL, FUSE_DEFAULT = 1, 2, 3, 1
 

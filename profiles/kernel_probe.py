@@ -25,7 +25,6 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--tiles", type=int, default=0, help="force 4- or 2-level time tiles (0: default tiling)")
     ap.add_argument("--only", default="", help="comma-separated subset of the forms")
-    ap.add_argument("--march", action="store_true", help="streaming-march chassis (set_march(1))")
     a = ap.parse_args()
     import torch
 
@@ -39,8 +38,6 @@ def main():
     h = S.build_hierarchy(g, cfg.method, path, chi=cfg.chi, mat=cfg.mat)
     if a.adjoint:
         h = S.transposed_hierarchy(h)
-    if a.march:
-        h.set_march(1)
     if a.tiles:
         h.set_tiling(small_dofs=10 ** 15, tiny_dofs=10 ** 15 if a.tiles == 2 else 1)
     H = S.LevelHierarchy
@@ -73,7 +70,7 @@ def main():
             fn()
         torch.cuda.synchronize()
         return
-    out = {"grid": f"{a.n_el}x{a.n_t}", "dofs": n0, "dir": a.dir, "adjoint": a.adjoint, "tiles": a.tiles or 8, "march": a.march}
+    out = {"grid": f"{a.n_el}x{a.n_t}", "dofs": n0, "dir": a.dir, "adjoint": a.adjoint, "tiles": a.tiles or 8}
     st = torch.cuda.current_stream()
     for name, fn in forms.items():
         fn()
