@@ -222,6 +222,14 @@ int stmg_hierarchy_device_bytes(const stmg_hierarchy* h, int64_t* bytes);
  * history must hold history_cap >= opts->max_cycles + 1 doubles. */
 int stmg_mg_solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_options* opts,
                   stmg_solve_report* report, double* history, int32_t history_cap);
+/* The same with flags.  STMG_SOLVE_ZERO_GUESS: the initial iterate is zero and u is
+ * output only -- what every reference caller outside optimise()'s warm start passes
+ * (std::vector<double> u(n, 0.0): proj/tests/acceptance_main.cpp:70, proj/src/
+ * experiments.cpp).  u is then neither read nor uploaded (a host u saves one of the two
+ * host-to-device copies); the result equals stmg_mg_solve on a zeroed u bit for bit. */
+enum { STMG_SOLVE_ZERO_GUESS = 1 };
+int stmg_mg_solve_ex(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_options* opts, int32_t flags,
+                     stmg_solve_report* report, double* history, int32_t history_cap);
 
 /* Independent solves run concurrently (SURVEY.md §2.2 "data parallel over
  * independent solves", §8(f) item 4 "experiment sweeps as batched replicas"):

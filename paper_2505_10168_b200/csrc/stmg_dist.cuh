@@ -329,17 +329,19 @@ __global__ void k_p2p_signal(const unsigned long long* mine, unsigned long long*
                              unsigned long long* right_slot) {
   if (threadIdx.x == 0) p2p_post(mine, left_slot, right_slot);
 }
-// Exchange e = mine[0] + 1: (post, if POST: one rank per process), wait for both
-// neighbours' posts, copy; the last block to finish records epoch e.
+// One rank's exchange e = mine[0] + 1, run by the `nblk` blocks of that rank (this
+// block is `blk`): block 0 posts e to both neighbours (POST), every block waits for
+// both neighbours' posts, the blocks copy the ghost levels out of the neighbours'
+// vectors, and the last block to finish records epoch e.
 template <bool POST>
-__global__ void __launch_bounds__(256) k_p2p_pull(unsigned long long* mine, unsigned long long* left_slot,
+__device__ __forceinline__ void p2p_rank_exchange(unsigned long long* mine, unsigned long long* left_slot,
                                                   unsigned long long* right_slot, double* x,
                                                   const double* __restrict__ left,
-                                                  const double* __restrict__ right, int64_t lo,
-                                                  int64_t hi, int64_t depth, int64_t nn) {
+                                                  const double* __restrict__ right, int64_t lo, int64_t hi,
+                                                  int64_t depth, int64_t nn, unsigned blk, unsigned nblk) {
   const unsigned long long e = mine[0] + 1;  // mine[0] changes only after every block is done
   if (threadIdx.x == 0) {
-    if (POST && blockIdx.x == 0) p2p_post(mine, left_slot, right_slot);
+    if (POST && blk == 0) p2p_post(mine, left_slot, right_slot);
     // A neighbour later than the timeout (a stopped process, a replayed launch)
     // does not trap the context: the wait gives up, flags the failure in
     // mine[4] and the host turns it into STMG_ERUNTIME after the solve.
@@ -357,8 +359,7 @@ __global__ void __launch_bounds__(256) k_p2p_pull(unsigned long long* mine, unsi
   __syncthreads();
   const int64_t cnt = depth * nn;
   // leading ghosts [lo - depth, lo) from the left rank, trailing [hi, hi + depth) from the right
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < 2 * cnt;
-       k += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t k = (int64_t)blk * blockDim.x + threadIdx.x; k < 2 * cnt; k += (int64_t)nblk * blockDim.x) {
     const bool lead = k < cnt;
     const double* src = lead ? left : right;
     if (src == nullptr) continue;
@@ -367,11 +368,44 @@ __global__ void __launch_bounds__(256) k_p2p_pull(unsigned long long* mine, unsi
   }
   if (threadIdx.x == 0) {
     // every block has read e (it did so before its ticket), so the last one may advance the epoch
-    if (atomicAdd(mine + 3, 1ull) == gridDim.x - 1) {
+    if (atomicAdd(mine + 3, 1ull) == nblk - 1) {
       mine[3] = 0;
       mine[0] = e;
     }
   }
+}
+
+// One rank per process: the kernel of that rank (the neighbours' run in their processes).
+template <bool POST>
+__global__ void __launch_bounds__(256) k_p2p_pull(unsigned long long* mine, unsigned long long* left_slot,
+                                                  unsigned long long* right_slot, double* x,
+                                                  const double* __restrict__ left,
+                                                  const double* __restrict__ right, int64_t lo,
+                                                  int64_t hi, int64_t depth, int64_t nn) {
+  p2p_rank_exchange<POST>(mine, left_slot, right_slot, x, left, right, lo, hi, depth, nn, blockIdx.x, gridDim.x);
+}
+
+// Loopback (every rank in this process, on this GPU): ALL ranks' exchanges as one
+// COOPERATIVE grid, `bpr` blocks per rank, each rank running the cross-process
+// protocol unchanged -- its block 0 posts, its blocks spin on the neighbours'
+// posts.  The blocks of different ranks wait on one another, so they must be
+// co-resident: a cooperative launch guarantees that (separate launches or streams
+// do not, B200_PROFILING.md).  This is the posting / waiting / epoch code path of
+// a multi-GPU run, exercised with real races between ranks on one GPU.
+constexpr int kP2pMaxLocal = 16;
+struct P2pRankArgs {
+  unsigned long long *mine, *left_slot, *right_slot;
+  double* x;
+  const double *left, *right;
+  int64_t lo, hi;
+};
+struct P2pMultiArgs {
+  P2pRankArgs r[kP2pMaxLocal];
+};
+__global__ void __launch_bounds__(256) k_p2p_pull_multi(const P2pMultiArgs a, int bpr, int64_t depth, int64_t nn) {
+  const P2pRankArgs& r = a.r[blockIdx.x / bpr];
+  p2p_rank_exchange<true>(r.mine, r.left_slot, r.right_slot, r.x, r.left, r.right, r.lo, r.hi, depth, nn,
+                          blockIdx.x % bpr, (unsigned)bpr);
 }
 
 struct P2pComm : Comm {
@@ -385,6 +419,9 @@ struct P2pComm : Comm {
   std::vector<Local> loc;
   std::vector<std::unique_ptr<DeviceBuf>> flag_mem;
   std::vector<void*> opened;  // IPC mappings to close
+  // STMG_DIST_P2P=2: loopback with the pre-posted (signal, then pull) launches
+  // instead of the cooperative all-ranks grid
+  bool legacy_loopback = false;
   explicit P2pComm(std::unique_ptr<Comm> b) : base(std::move(b)) {
     world = base->world;
     n_local = base->n_local;
@@ -426,31 +463,52 @@ struct P2pComm : Comm {
       *rs = g < world - 1 ? reinterpret_cast<u64*>(loc[k].right_flags) + 1 : nullptr;
     };
     const bool loopback = n_local > 1;
-    if (loopback) {
-      for (int k = 0; k < n_local; ++k) {
-        u64 *ls, *rs;
-        slots(k, &ls, &rs);
-        k_p2p_signal<<<1, 32, 0, s>>>(reinterpret_cast<const u64*>(loc[k].flags), ls, rs);
-        launch_check(static_cast<int>(cudaGetLastError()), "p2p signal");
-      }
-    }
+    const int64_t cnt = 2 * nn * depth;
+    std::vector<P2pRankArgs> ra(static_cast<size_t>(n_local));
     for (int k = 0; k < n_local; ++k) {
       const int g = rank0 + k;
       Local& L = loc[k];
       const auto it = std::find(L.bufs.begin(), L.bufs.end(), v[k]);
       if (it == L.bufs.end()) throw std::runtime_error("p2p exchange: unregistered vector");
       const size_t j = static_cast<size_t>(it - L.bufs.begin());
-      const int64_t cnt = 2 * nn * depth;
-      const unsigned grid = static_cast<unsigned>(std::min<int64_t>((cnt + 255) / 256, 148));
       u64 *ls, *rs;
       slots(k, &ls, &rs);
-      const double* lp = g > 0 ? L.left[j] : nullptr;
-      const double* rp = g < world - 1 ? L.right[j] : nullptr;
-      u64* mine = reinterpret_cast<u64*>(L.flags);
+      ra[k] = {reinterpret_cast<u64*>(L.flags), ls, rs, v[k], g > 0 ? L.left[j] : nullptr,
+               g < world - 1 ? L.right[j] : nullptr, b[g], b[g + 1]};
+    }
+    if (loopback && n_local <= kP2pMaxLocal && !legacy_loopback) {
+      // one cooperative grid over all ranks (see k_p2p_pull_multi)
+      P2pMultiArgs ma{};
+      for (int k = 0; k < n_local; ++k) ma.r[k] = ra[k];
+      int bpr = static_cast<int>(std::min<int64_t>((cnt + 255) / 256, std::max(1, 148 / n_local)));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(static_cast<unsigned>(bpr * n_local));
+      cfg.blockDim = dim3(256);
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeCooperative;
+      attr[0].val.cooperative = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      launch_check(static_cast<int>(cudaLaunchKernelEx(&cfg, k_p2p_pull_multi, ma, bpr, static_cast<int64_t>(depth), nn)),
+                   "p2p pull (cooperative, all ranks)");
+      return;
+    }
+    if (loopback) {  // every rank posts, then every rank pulls (waits already satisfied)
+      for (int k = 0; k < n_local; ++k) {
+        k_p2p_signal<<<1, 32, 0, s>>>(ra[k].mine, ra[k].left_slot, ra[k].right_slot);
+        launch_check(static_cast<int>(cudaGetLastError()), "p2p signal");
+      }
+    }
+    for (int k = 0; k < n_local; ++k) {
+      const unsigned grid = static_cast<unsigned>(std::min<int64_t>((cnt + 255) / 256, 148));
+      const P2pRankArgs& r = ra[k];
       if (loopback)
-        k_p2p_pull<false><<<grid, 256, 0, s>>>(mine, ls, rs, v[k], lp, rp, b[g], b[g + 1], depth, nn);
+        k_p2p_pull<false><<<grid, 256, 0, s>>>(r.mine, r.left_slot, r.right_slot, r.x, r.left, r.right, r.lo, r.hi,
+                                               depth, nn);
       else
-        k_p2p_pull<true><<<grid, 256, 0, s>>>(mine, ls, rs, v[k], lp, rp, b[g], b[g + 1], depth, nn);
+        k_p2p_pull<true><<<grid, 256, 0, s>>>(r.mine, r.left_slot, r.right_slot, r.x, r.left, r.right, r.lo, r.hi,
+                                              depth, nn);
       launch_check(static_cast<int>(cudaGetLastError()), "p2p pull");
     }
   }
@@ -830,7 +888,10 @@ void dist_build(stmg_dist* d, int world, int rank, const void* nccl_id, int64_t 
   cuda_check(cudaStreamCreateWithFlags(&d->stream, cudaStreamDefault), "cudaStreamCreate");
   cuda_check(cudaStreamCreateWithFlags(&d->cap_stream, cudaStreamNonBlocking), "cudaStreamCreate");
   cuda_check(cudaMallocHost(&d->pinned, 8 * sizeof(double)), "cudaMallocHost");
-  if (const char* e = std::getenv("STMG_DIST_P2P"); e && std::atoi(e) != 0) enable_p2p(d);
+  if (const char* e = std::getenv("STMG_DIST_P2P"); e && std::atoi(e) != 0) {
+    enable_p2p(d);
+    if (std::atoi(e) == 2) static_cast<P2pComm*>(d->comm.get())->legacy_loopback = true;
+  }
   cuda_check(cudaDeviceSynchronize(), "sync");
 }
 

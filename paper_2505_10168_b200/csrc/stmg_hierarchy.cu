@@ -1245,9 +1245,13 @@ double fetch_scalars(stmg_hierarchy* h, int count, double* out) {
 }
 
 // mg_solve, proj/src/multigrid.cpp:212-279
+// flags & STMG_SOLVE_ZERO_GUESS: the initial iterate is zero and u is output only
+// (not read, not uploaded): the device iterate is cleared instead.
 void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_options& o,
-           stmg_solve_report* rep, double* history, int32_t cap) {
+           stmg_solve_report* rep, double* history, int32_t cap, int32_t flags = 0) {
   if (!b || !u) throw std::invalid_argument("mg_solve: vector size mismatch");
+  if (flags & ~STMG_SOLVE_ZERO_GUESS) throw std::invalid_argument("mg_solve: unknown flags");
+  const bool zero_guess = (flags & STMG_SOLVE_ZERO_GUESS) != 0;
   if (o.nu < 0 || o.omega <= 0.0 || o.tol <= 0.0 || o.div_tol <= o.tol || o.max_cycles < 0)
     throw std::invalid_argument("mg_solve: invalid options");
   if (!history || cap < o.max_cycles + 1)
@@ -1274,9 +1278,11 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
     cuda_check(cudaMemcpyAsync(ws.f[0]->p, b, bytes, b_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                                h->stream),
                "b copy");
-    cuda_check(cudaMemcpyAsync(X, u, bytes, u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream),
-               "u copy");
+    if (!zero_guess)
+      cuda_check(cudaMemcpyAsync(X, u, bytes, u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream),
+                 "u copy");
   }
+  if (zero_guess) cuda_check(cudaMemsetAsync(X, 0, bytes, h->stream), "u clear");
   int64_t launches = 0;
   int64_t np = 0;
   launch_check(launch_sumsq(B, n, ws.partials->p, &np, h->stream), "sumsq");
@@ -2096,6 +2102,15 @@ int stmg_mg_solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solv
     checked(h);
     if (!opts || !report) throw std::invalid_argument("mg_solve: null argument");
     solve(h, b, u, *opts, report, history, cap);
+  });
+}
+
+int stmg_mg_solve_ex(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_options* opts, int32_t flags,
+                     stmg_solve_report* report, double* history, int32_t cap) {
+  return guarded([&] {
+    checked(h);
+    if (!opts || !report) throw std::invalid_argument("mg_solve: null argument");
+    solve(h, b, u, *opts, report, history, cap, flags);
   });
 }
 

@@ -69,6 +69,7 @@ def _load():
         "stmg_hierarchy_set_profiling": [vp, i32],
         "stmg_hierarchy_profile": [vp, i32, i32, C.POINTER(i64), C.POINTER(f64)],
         "stmg_mg_solve": [vp, vp, vp, vp, vp, vp, i32],
+        "stmg_mg_solve_ex": [vp, vp, vp, vp, i32, vp, vp, i32],
         "stmg_mg_solve_batch": [i32, vp, vp, vp, vp, vp, vp, i32],
         "stmg_level_sweeps": [vp, i32, vp, vp, i32, f64],
         "stmg_level_residual": [vp, i32, vp, vp, vp],
@@ -656,11 +657,12 @@ def transposed_hierarchy(h: LevelHierarchy) -> LevelHierarchy:
     return LevelHierarchy(out, h.path, h.method, h.device, adjoint=not h.adjoint, parent=h)
 
 
-def mg_solve(h: LevelHierarchy, b, u, opts: Optional[SolveOptions] = None) -> SolveReport:
+def mg_solve(h: LevelHierarchy, b, u, opts: Optional[SolveOptions] = None, zero_guess: bool = False) -> SolveReport:
     """V-cycle solve of J u = b from the caller's u (warm start), u updated in place.
 
     b and u may be numpy arrays (host) or torch tensors (host, pinned or on the
-    hierarchy's GPU); proj/src/multigrid.cpp:212-279.
+    hierarchy's GPU); proj/src/multigrid.cpp:212-279.  zero_guess: start from zero, u is
+    output only (stmg_mg_solve_ex, STMG_SOLVE_ZERO_GUESS): a host u is not uploaded.
     """
     o = opts or SolveOptions()
     n = h.levels[0].n_dofs
@@ -669,8 +671,12 @@ def mg_solve(h: LevelHierarchy, b, u, opts: Optional[SolveOptions] = None) -> So
     hist = np.zeros(max(o.max_cycles, 0) + 1, np.float64)
     rep = _SolveRep()
     co = _SolveOpts(int(o.nu), float(o.omega), float(o.tol), float(o.div_tol), int(o.max_cycles))
-    _check(_lib.stmg_mg_solve(h.handle, _ptr(b), _ptr(u), C.byref(co), C.byref(rep), hist.ctypes.data,
-                              hist.size))
+    if zero_guess:
+        _check(_lib.stmg_mg_solve_ex(h.handle, _ptr(b), _ptr(u), C.byref(co), 1, C.byref(rep), hist.ctypes.data,
+                                     hist.size))
+    else:
+        _check(_lib.stmg_mg_solve(h.handle, _ptr(b), _ptr(u), C.byref(co), C.byref(rep), hist.ctypes.data,
+                                  hist.size))
     kt = {}
     if rep.fine_sweeps or rep.fine_restricts or rep.fine_prolong_sweeps or rep.fine_sweep_pairs:
         kt = {"fine_sweep": (rep.fine_sweeps, rep.fine_sweep_seconds),

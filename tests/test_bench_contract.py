@@ -47,8 +47,11 @@ def test_gpu_arm_contract():
     # size, tests/test_gpu_scale.py; the reference at reduced size, tests/golden/cfg2_mini.npz)
     assert d["cycles"] == 3 and d["status"] == "diverged"
     assert d["value"] > 0 and d["gpu_launches"] > 0
-    assert d["e2e"]["h2d_bytes_per_step"] == 16 * d["config"]["dofs"]
+    # headline e2e: b uploaded, u output only (zero initial guess flag); in/out u beside it
+    assert d["e2e"]["h2d_bytes_per_step"] == 8 * d["config"]["dofs"]
     assert d["e2e"]["d2h_bytes_per_step"] == 8 * d["config"]["dofs"]
+    assert d["e2e"]["inout_u"]["h2d_bytes_per_step"] == 16 * d["config"]["dofs"]
+    assert d["e2e"]["value"] > d["e2e"]["inout_u"]["value"] > 0
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.5
     assert "sm_mhz" in d["clocks"]

@@ -126,12 +126,17 @@ def test_slab_storage_scales_with_world(S):
     assert sizes[8] - sizes[2] < 0.15 * 6 * 3 * vec_bytes, sizes
 
 
+@pytest.mark.parametrize("mode", ["1", "2"])
 @pytest.mark.parametrize("name,world", [("cfg1_mini", 2), ("cfg1_mini_adj", 4), ("cfg4_mini", 8),
                                         ("cfg0_deep", 2)])
-def test_p2p_transport_loopback_matches_single_domain(S, port, monkeypatch, name, world):
-    """Peer-memory ghost pulls behind the neighbour epoch barrier
-    (STMG_DIST_P2P=1), all ranks in this process: bitwise the single-domain
-    iterate, through graph replays and repeated solves (epochs keep counting)."""
+def test_p2p_transport_loopback_matches_single_domain(S, port, monkeypatch, name, world, mode):
+    """Peer-memory ghost pulls behind the neighbour epoch barrier, all ranks in this
+    process: bitwise the single-domain iterate, through graph replays and repeated
+    solves (epochs keep counting).  STMG_DIST_P2P=1: every exchange is ONE cooperative
+    grid over all ranks, each rank running the cross-process protocol unchanged (its
+    block 0 posts, its blocks spin on the neighbours' posts), so the post / wait /
+    epoch path races between ranks on the hardware.  STMG_DIST_P2P=2: the pre-posted
+    form (all ranks signal, then all pull; the waits are already satisfied)."""
     cs = case(name)
     g, path = grid_path(S, cs, port)
     b = cs.rhs_vector(port)
@@ -141,7 +146,7 @@ def test_p2p_transport_loopback_matches_single_domain(S, port, monkeypatch, name
         h = S.transposed_hierarchy(h)
     u1 = np.zeros_like(b)
     r1 = S.mg_solve(h, b, u1, opts)
-    monkeypatch.setenv("STMG_DIST_P2P", "1")
+    monkeypatch.setenv("STMG_DIST_P2P", mode)
     dh = S.build_dist_hierarchy(g, cs.method, path, world, adjoint=cs.adjoint, chi=cs.chi, mat=cs.mat,
                                 min_slab=8)
     assert dh.transport == "p2p"

@@ -145,6 +145,36 @@ def test_solve_is_deterministic(torch, S, port):
     assert outs[0][1] == outs[1][1]
 
 
+@pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "cfg2_mini"])
+def test_zero_guess_flag_equals_a_zeroed_u(torch, S, port, name):
+    """stmg_mg_solve_ex with STMG_SOLVE_ZERO_GUESS: u is output only (garbage in, never
+    read); host and device vectors give the in/out solve from a zero vector bit for bit."""
+    cs = case(name)
+    h = gpu_hier(S, cs, port)
+    b = cs.rhs_vector(port)
+    opts = S.SolveOptions(nu=cs.nu, tol=cs.tol, max_cycles=cs.max_cycles)
+    u0 = np.zeros_like(b)
+    rep0 = S.mg_solve(h, b, u0, opts)
+    u1 = np.full_like(b, np.nan)
+    rep1 = S.mg_solve(h, b, u1, opts, zero_guess=True)
+    assert np.array_equal(bits(u1), bits(u0)) and rep1.history == rep0.history and rep1.cycles == rep0.cycles
+    bt = torch.from_numpy(b).cuda()
+    ut = torch.full_like(bt, float("nan"))
+    rep2 = S.mg_solve(h, bt, ut, opts, zero_guess=True)
+    assert np.array_equal(bits(ut), bits(u0)) and rep2.history == rep0.history
+    with pytest.raises(ValueError):
+        from paper_2505_10168_b200.stmg import _lib, _check, _ptr  # unknown flag bits are rejected
+        import ctypes as C
+
+        hist = np.zeros(opts.max_cycles + 1)
+        from paper_2505_10168_b200.stmg import _SolveOpts, _SolveRep
+
+        co = _SolveOpts(int(opts.nu), float(opts.omega), float(opts.tol), float(opts.div_tol), int(opts.max_cycles))
+        rep = _SolveRep()
+        _check(_lib.stmg_mg_solve_ex(h.handle, _ptr(b), _ptr(u1), C.byref(co), 6, C.byref(rep), hist.ctypes.data,
+                                     hist.size))
+
+
 def test_tiny_hand_values(torch, S, port):
     """proj/tests/test_assembly.cpp:133-144: T = 0.375, 0.46875, 0.4921875."""
     cs = case("tiny")
