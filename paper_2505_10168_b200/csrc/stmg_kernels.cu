@@ -17,6 +17,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 #include <algorithm>
 #include <cstdlib>
@@ -1347,7 +1348,11 @@ __global__ void k_square(const double* __restrict__ A, double* __restrict__ C, i
 // stream u and lambda once (config 4: 256 blocks over 1.07 GB).
 constexpr int kSensE = 16, kSensWarps = 16, kSensLv = 3;
 constexpr int kSensTile = (kSensWarps - 1) * 2 * kSensLv;  // levels per tile (90; 46 KB of buffers)
-__global__ void __launch_bounds__(kSensWarps * 32) k_sensitivities(
+// POW2: dt is a power of two, so a / dt and a * (1 / dt) are the same correctly
+// rounded number and the two divisions per level (~35 instructions each) become
+// multiplications (config 4: dt = 2^-14).
+template <bool POW2>
+__global__ void __launch_bounds__(kSensWarps * 32, 2) k_sensitivities(
     int64_t n_el, int64_t n_t, double dt, const double* __restrict__ dk_dx, const double* __restrict__ dc_dx6,
     const double* __restrict__ u, const double* __restrict__ lam, double* __restrict__ sens) {
   pdl_entry();
@@ -1360,6 +1365,7 @@ __global__ void __launch_bounds__(kSensWarps * 32) k_sensitivities(
   const int64_t nn = n_el + 1;
   const double kd = active ? dk_dx[e] : 0.0, cd = active ? dc_dx6[e] : 0.0;
   const int64_t tiles = (n_t + kSensTile - 1) / kSensTile;
+  const double inv_dt = 1.0 / dt;  // exact when POW2
   double acc = 0.0;
   for (int64_t t = 0; t <= tiles; ++t) {
     if (warp > 0 && t < tiles && active) {  // terms of tile t into buffer t & 1
@@ -1377,8 +1383,8 @@ __global__ void __launch_bounds__(kSensWarps * 32) k_sensitivities(
           p0 = lm ? 0.0 : __ldg(u + r - nn);
           p1 = __ldg(u + r - nn + 1);
         }
-        const double v0 = (u0 - p0) / dt;
-        const double v1 = (u1 - p1) / dt;
+        const double v0 = POW2 ? (u0 - p0) * inv_dt : (u0 - p0) / dt;
+        const double v1 = POW2 ? (u1 - p1) * inv_dt : (u1 - p1) / dt;
         T[0][j][el] = (kd * (u0 - u1)) * (l0 - l1);
         T[1][j][el] = cd * (l0 * (2.0 * v0 + v1) + l1 * (v0 + 2.0 * v1));
       }
@@ -2021,9 +2027,15 @@ int launch_finalize_check(const double* partials, int64_t n, double* scalars, So
 int launch_sensitivities(int64_t n_el, int64_t n_t, double dt, const double* dk_dx,
                          const double* dc_dx6, const double* u, const double* lam, double* sens,
                          cudaStream_t s) {
-  // one block of kSensWarps warps per kSensE elements
-  pdl_launch(k_sensitivities, (unsigned)((n_el + kSensE - 1) / kSensE), kSensWarps * 32, 0, s, n_el, n_t, dt, dk_dx,
-             dc_dx6, u, lam, sens);
+  // one block of kSensWarps warps per kSensE elements; dt a power of two (frexp
+  // mantissa 0.5, finite reciprocal): multiply by the exact 1 / dt instead of dividing
+  int ex = 0;
+  const bool pow2 = dt > 0.0 && std::frexp(dt, &ex) == 0.5 && std::isfinite(1.0 / dt);
+  const unsigned grid = (unsigned)((n_el + kSensE - 1) / kSensE);
+  if (pow2)
+    pdl_launch(k_sensitivities<true>, grid, kSensWarps * 32, 0, s, n_el, n_t, dt, dk_dx, dc_dx6, u, lam, sens);
+  else
+    pdl_launch(k_sensitivities<false>, grid, kSensWarps * 32, 0, s, n_el, n_t, dt, dk_dx, dc_dx6, u, lam, sens);
   return check_launch();
 }
 

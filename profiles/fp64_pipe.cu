@@ -70,6 +70,49 @@ double run(const char* name, int sms, double clock_hz, double dp_per_iter) {
   return per_clk;
 }
 
+// Dependent-issue latency: one chain per thread, one warp per SM.
+__global__ void k_latency(double* out, double b, int iters, int op, const double* tab) {
+  double v = b + threadIdx.x;
+  if (op == 0) {
+    for (int it = 0; it < iters; ++it) v = v + b;
+  } else if (op == 1) {
+    for (int it = 0; it < iters; ++it) v = v * b;
+  } else {
+    __shared__ double sm[1024];
+    for (int k = threadIdx.x; k < 1024; k += blockDim.x) sm[k] = tab[k];
+    __syncthreads();
+    for (int it = 0; it < iters; ++it) v = v + sm[(it * 32 + threadIdx.x) & 1023];  // LDS feeding the chain
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = v;
+}
+
+void latency(const char* name, int op, double clock_hz) {
+  double *out = nullptr, *tab = nullptr;
+  cudaMalloc(&out, sizeof(double) * 148 * 32);
+  cudaMalloc(&tab, sizeof(double) * 1024);
+  cudaMemset(tab, 0, sizeof(double) * 1024);
+  const int iters = 1 << 16;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k_latency<<<148, 32>>>(out, 1.0000001, iters, op, tab);
+  cudaDeviceSynchronize();
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0);
+    k_latency<<<148, 32>>>(out, 1.0000001, iters, op, tab);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  std::printf("{\"op\": \"%s\", \"ms\": %.4f, \"cycles_per_dependent_op_at_max_clock\": %.2f}\n", name, best,
+              best * 1e-3 * clock_hz / iters);
+  cudaFree(out);
+  cudaFree(tab);
+}
+
 int main() {
   cudaDeviceProp p;
   cudaGetDeviceProperties(&p, 0);
@@ -83,5 +126,8 @@ int main() {
   run<2>("dfma", p.multiProcessorCount, hz, 1);
   run<3>("dadd + 64-bit shfl per 4", p.multiProcessorCount, hz, 1);
   run<4>("dadd + imad per dadd", p.multiProcessorCount, hz, 1);
+  latency("dadd dependent chain", 0, hz);
+  latency("dmul dependent chain", 1, hz);
+  latency("lds + dadd dependent chain (unhoisted)", 2, hz);
   return 0;
 }
