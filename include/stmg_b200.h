@@ -376,6 +376,12 @@ int stmg_dist_mg_solve(stmg_dist* d, const double* b, double* u, const stmg_solv
 int stmg_dist_mg_solve_local(stmg_dist* d, const double* b_local, double* u_local, const stmg_solve_options* opts,
                              stmg_solve_report* report, double* history, int32_t history_cap);
 int stmg_dist_transport(const stmg_dist* d, char* name_out, int32_t cap);
+/* *yes = 1 when the last solve's cycle loop ran as ONE device graph (a conditional WHILE
+ * node around the distributed V-cycle, the all-reduced norm and the bookkeeping kernel;
+ * one launch and one read-back per solve), 0 for the host loop with a norm read-back per
+ * cycle.  Default: device loop when every rank is in this process (loopback); across
+ * processes (NCCL calls inside the loop body) opt in with STMG_DIST_DEVICE_LOOP=1. */
+int stmg_dist_loop_on_device(const stmg_dist* d, int32_t* yes);
 void stmg_dist_destroy(stmg_dist* d);
 
 /* Per-handle tiling of the stencil kernels (A/B measurements, tests of every

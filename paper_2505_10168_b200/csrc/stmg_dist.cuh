@@ -577,6 +577,11 @@ struct stmg_dist {
   double* pinned = nullptr;
   std::map<stmgb::GraphKey, stmgb::GraphEntry> graphs;
   int64_t device_bytes = 0;
+  // device-side cycle loop (dist_loop): SolveLoopCtl + history on the device, pinned mirror
+  std::unique_ptr<stmgb::DeviceBuf> loop;
+  double* loop_host = nullptr;
+  bool device_loop = false;
+  bool last_on_device = false;  // the last solve's cycle loop ran as the device graph
 
   ~stmg_dist() {
     int prev = 0;
@@ -586,7 +591,10 @@ struct stmg_dist {
     for (auto& kv : graphs) {
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
       if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+      if (kv.second.loop_exec) cudaGraphExecDestroy(kv.second.loop_exec);
+      if (kv.second.loop_graph) cudaGraphDestroy(kv.second.loop_graph);
     }
+    if (loop_host) cudaFreeHost(loop_host);
     // Peer-memory transport: no rank may free slab buffers a neighbour can still
     // read.  Every rank first closes its mappings of the neighbours' buffers,
     // then all ranks meet (a one-double all-reduce on the base communicator),
@@ -888,6 +896,13 @@ void dist_build(stmg_dist* d, int world, int rank, const void* nccl_id, int64_t 
   cuda_check(cudaStreamCreateWithFlags(&d->stream, cudaStreamDefault), "cudaStreamCreate");
   cuda_check(cudaStreamCreateWithFlags(&d->cap_stream, cudaStreamNonBlocking), "cudaStreamCreate");
   cuda_check(cudaMallocHost(&d->pinned, 8 * sizeof(double)), "cudaMallocHost");
+  d->loop = std::make_unique<DeviceBuf>(kLoopCtlDoubles + kLoopHistory + 1);
+  cuda_check(cudaMallocHost(&d->loop_host, sizeof(double) * (kLoopCtlDoubles + kLoopHistory + 1)), "cudaMallocHost");
+  // The cycle loop runs on the device (one conditional WHILE graph, dist_loop) when
+  // every rank is in this process (loopback).  Across processes the body holds NCCL
+  // calls; that form is opt-in (STMG_DIST_DEVICE_LOOP=1) until it has run at world > 1.
+  d->device_loop = nccl_id == nullptr;
+  if (const char* e = std::getenv("STMG_DIST_DEVICE_LOOP")) d->device_loop = std::atoi(e) != 0;
   if (const char* e = std::getenv("STMG_DIST_P2P"); e && std::atoi(e) != 0) {
     enable_p2p(d);
     if (std::atoi(e) == 2) static_cast<P2pComm*>(d->comm.get())->legacy_loopback = true;
@@ -911,20 +926,76 @@ GraphEntry& dist_graph(stmg_dist* d, int nu, double omega) {
 
 // residual-norm pass on level 0 of every local rank (optionally the speculative
 // first sweep), all-reduced into scalars[slot] of every rank
-void dist_norm(stmg_dist* d, bool spec, double omega, int slot) {
+void dist_norm(stmg_dist* d, bool spec, double omega, int slot, cudaStream_t s = nullptr) {
+  if (s == nullptr) s = d->stream;
   std::vector<double*> X, in, out;
   for (auto& R : d->ranks) X.push_back(R.xa[0]->p);
-  d->comm->exchange(X, d->plan.bounds[0], d->nn(0), 1, d->stream);
+  d->comm->exchange(X, d->plan.bounds[0], d->nn(0), 1, s);
   for (auto& R : d->ranks) {
     int64_t np = 0;
     launch_check(launch_sweep(d->adjoint, R.views[0], R.f[0]->p, R.xa[0]->p, spec ? R.xb[0]->p : nullptr,
-                              omega, R.partials->p, &np, d->stream),
+                              omega, R.partials->p, &np, s),
                  "dist norm sweep");
-    launch_check(launch_finalize_sum(R.partials->p, np, R.scalars->p + 4, d->stream), "finalize");
+    launch_check(launch_finalize_sum(R.partials->p, np, R.scalars->p + 4, s), "finalize");
     in.push_back(R.scalars->p + 4);
     out.push_back(R.scalars->p + slot);
   }
-  d->comm->allreduce_sum(in, out, d->stream);
+  d->comm->allreduce_sum(in, out, s);
+}
+
+// The whole cycle loop of the time-slab solve as one graph (as get_loop for one GPU):
+// a conditional WHILE node whose body is the distributed V-cycle (ghost exchanges,
+// the gathered tail), the all-reduced residual norm with the speculative first sweep,
+// and the bookkeeping kernel (history, status, loop condition) on this process's
+// first rank.  Every process sees the same all-reduced norm, so all of them leave the
+// loop after the same cycle and their collectives stay matched.  Returns nullptr
+// (host loop) when the graph cannot be built.
+cudaGraphExec_t dist_loop(stmg_dist* d, int nu, double omega) {
+  GraphEntry& e = dist_graph(d, nu, omega);
+  if (e.loop_tried) return e.loop_exec;
+  e.loop_tried = true;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ex = nullptr;
+  auto fail = [&] {
+    cudaGetLastError();
+    if (ex) cudaGraphExecDestroy(ex);
+    if (g) cudaGraphDestroy(g);
+    return static_cast<cudaGraphExec_t>(nullptr);
+  };
+  if (cudaGraphCreate(&g, 0) != cudaSuccess) return fail();
+  cudaGraphConditionalHandle handle;
+  if (cudaGraphConditionalHandleCreate(&handle, g, 1, cudaGraphCondAssignDefault) != cudaSuccess) return fail();
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = handle;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  if (cudaGraphAddNode(&node, g, nullptr, 0, &cp) != cudaSuccess) return fail();
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  cudaStream_t cs = d->cap_stream;
+  if (cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+    return fail();
+  bool ok = true;
+  try {
+    DistEmitter em{d, nu, omega, cs};
+    const bool spec = nu >= 1;
+    if (em.level(0, spec ? 1 : 0, spec ? 1 : 0, false) != 0)
+      throw std::logic_error("dist: level-0 iterate left the primary buffer");
+    dist_norm(d, spec, omega, 1, cs);
+    auto* ctl = reinterpret_cast<SolveLoopCtl*>(d->loop->p);
+    launch_check(launch_cycle_check(d->ranks[0].scalars->p, ctl, d->loop->p + kLoopCtlDoubles, handle, cs),
+                 "cycle check");
+  } catch (...) {
+    ok = false;
+  }
+  cudaGraph_t captured = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(cs, &captured);
+  if (!ok || ec != cudaSuccess) return fail();
+  if (cudaGraphInstantiate(&ex, g, 0) != cudaSuccess) return fail();
+  e.loop_graph = g;
+  e.loop_exec = ex;
+  return ex;
 }
 
 double dist_fetch(stmg_dist* d, int slot) {
@@ -1008,8 +1079,29 @@ void dist_solve(stmg_dist* d, const double* b, double* u, const stmg_solve_optio
   if (d->comm->is_root())
     for (int l = d->Lg(); l + 1 < d->L(); ++l) per_cycle += 2.0 * o.nu * static_cast<double>(d->ndofs(l));
   int64_t launches = 0;
+  cudaGraphExec_t loop = nullptr;
+  if (d->device_loop && r0 >= o.tol && o.max_cycles > 0 && o.max_cycles <= kLoopHistory)
+    loop = dist_loop(d, o.nu, o.omega);
+  d->last_on_device = loop != nullptr;
   if (r0 < o.tol) {
     rep->status = STMG_CONVERGED;
+  } else if (loop) {
+    // the whole cycle loop on the device: one launch, one read-back
+    auto* ctl = reinterpret_cast<SolveLoopCtl*>(d->loop_host);
+    *ctl = SolveLoopCtl{o.tol, o.div_tol, o.max_cycles, 0, STMG_MAX_CYCLES, 0};
+    cuda_check(cudaMemcpyAsync(d->loop->p, d->loop_host, sizeof(SolveLoopCtl), cudaMemcpyHostToDevice, d->stream),
+               "loop ctl");
+    cuda_check(cudaGraphLaunch(loop, d->stream), "loop graph launch");
+    cuda_check(cudaMemcpyAsync(d->loop_host, d->loop->p, sizeof(double) * (kLoopCtlDoubles + o.max_cycles + 1),
+                               cudaMemcpyDeviceToHost, d->stream),
+               "loop read-back");
+    cuda_check(cudaStreamSynchronize(d->stream), "sync");
+    const double* dh = d->loop_host + kLoopCtlDoubles;
+    for (int c = 1; c <= ctl->cycles; ++c) history[nh++] = dh[c];
+    rep->cycles = ctl->cycles;
+    rep->status = ctl->status;
+    rep->smoother_dof_updates = per_cycle * ctl->cycles;
+    launches = static_cast<int64_t>(ctl->cycles) * (g->kernels + 3 * static_cast<int64_t>(d->ranks.size()));
   } else {
     rep->status = STMG_MAX_CYCLES;
     for (int cycle = 1; cycle <= o.max_cycles; ++cycle) {

@@ -2510,6 +2510,13 @@ int stmg_dist_transport(const stmg_dist* d, char* name_out, int32_t cap) {
   });
 }
 
+int stmg_dist_loop_on_device(const stmg_dist* d, int32_t* yes) {
+  return guarded([&] {
+    if (!d || !yes) throw std::invalid_argument("null handle or argument");
+    *yes = d->last_on_device ? 1 : 0;
+  });
+}
+
 void stmg_dist_destroy(stmg_dist* d) { delete d; }
 
 int stmg_synchronize(stmg_hierarchy* h) {

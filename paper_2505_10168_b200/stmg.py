@@ -91,6 +91,7 @@ def _load():
         "stmg_dist_nccl_unique_id": [vp, i32],
         "stmg_dist_create": [vp, vp, vp, vp, vp, C.c_char_p, i32, vp, i32, i32, i32, vp, i32, i64,
                              C.POINTER(vp)],
+        "stmg_dist_loop_on_device": [vp, C.POINTER(i32)],
         "stmg_dist_info": [vp, C.POINTER(i32), C.POINTER(i64), C.POINTER(i64), C.POINTER(i32),
                            C.POINTER(i64)],
         "stmg_dist_mg_solve": [vp, vp, vp, vp, vp, vp, i32],
@@ -839,6 +840,13 @@ class DistHierarchy:
     @property
     def handle(self):
         return self._h
+
+    @property
+    def loop_on_device(self) -> bool:
+        """The last solve's cycle loop ran as one device graph (stmg_dist_loop_on_device)."""
+        v = C.c_int32(0)
+        _check(_lib.stmg_dist_loop_on_device(self._h, C.byref(v)))
+        return bool(v.value)
 
     @property
     def transport(self) -> str:

@@ -45,6 +45,7 @@ def test_loopback_slabs_match_single_domain(S, port, name, world):
     assert dh.n_distributed >= 1
     u2 = np.zeros_like(b)
     r2 = S.mg_solve_dist(dh, b, u2, opts)
+    assert dh.loop_on_device
     assert r2.cycles == r1.cycles and r2.status == r1.status
     assert np.array_equal(u1.view(np.uint64), u2.view(np.uint64))
     assert np.allclose(r2.history, r1.history, rtol=1e-12, atol=0)
@@ -179,3 +180,53 @@ def test_p2p_over_nccl_world1_gathers_handles_and_matches(S, port, monkeypatch):
     r2 = S.mg_solve_dist(dh, b, u2, opts)
     assert r2.cycles == r1.cycles
     assert np.array_equal(u1.view(np.uint64), u2.view(np.uint64))
+
+
+@pytest.mark.parametrize("name,world", [("cfg1_mini", 2), ("cfg1_mini_adj", 4), ("cfg2_mini", 4), ("cfg4_mini", 8)])
+def test_device_cycle_loop_equals_host_loop(S, port, monkeypatch, name, world):
+    """The time-slab solve's cycle loop as one conditional WHILE graph (dist_loop:
+    V-cycle with its ghost exchanges and gathered tail, all-reduced norm, bookkeeping
+    kernel; the default in loopback) against the host loop with a norm read-back per
+    cycle (STMG_DIST_DEVICE_LOOP=0): same cycles, status, history and iterate, bitwise;
+    also for a solve that stops at max_cycles and one that diverges (cfg2_mini)."""
+    cs = case(name)
+    g, path = grid_path(S, cs, port)
+    b = cs.rhs_vector(port)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("STMG_DIST_DEVICE_LOOP", mode)
+        dh = S.build_dist_hierarchy(g, cs.method, path, world, adjoint=cs.adjoint, chi=cs.chi, mat=cs.mat,
+                                    min_slab=8)
+        res = []
+        for max_cycles in (cs.max_cycles, 3):
+            u = np.zeros_like(b)
+            r = S.mg_solve_dist(dh, b, u, S.SolveOptions(nu=cs.nu, tol=cs.tol, max_cycles=max_cycles))
+            assert dh.loop_on_device == (mode == "1")
+            res.append((r, u))
+        out[mode] = res
+    for (r1, u1), (r0, u0) in zip(out["1"], out["0"]):
+        assert r1.cycles == r0.cycles and r1.status == r0.status
+        assert r1.history == r0.history
+        assert np.array_equal(u1.view(np.uint64), u0.view(np.uint64))
+
+
+def test_device_cycle_loop_with_nccl_in_the_body_world1(S, port, monkeypatch):
+    """STMG_DIST_DEVICE_LOOP=1 on a real NCCL communicator (world of one): the NCCL
+    all-reduce, gather and broadcast are captured INSIDE the conditional WHILE body.
+    Same result as the single-domain solve."""
+    cs = case("cfg1_mini")
+    g, path = grid_path(S, cs, port)
+    b = cs.rhs_vector(port)
+    opts = S.SolveOptions(nu=cs.nu, tol=cs.tol, max_cycles=cs.max_cycles)
+    h = S.build_hierarchy(g, cs.method, path)
+    u1 = np.zeros_like(b)
+    r1 = S.mg_solve(h, b, u1, opts)
+    monkeypatch.setenv("STMG_DIST_DEVICE_LOOP", "1")
+    dh = S.build_dist_hierarchy(g, cs.method, path, 1, rank=0, nccl_id=S.nccl_unique_id(), min_slab=8)
+    assert dh.transport == "nccl"
+    u2 = np.zeros_like(b)
+    r2 = S.mg_solve_dist(dh, b, u2, opts)
+    assert dh.loop_on_device
+    assert r2.cycles == r1.cycles and r2.status == r1.status
+    assert np.array_equal(u1.view(np.uint64), u2.view(np.uint64))
+    assert np.allclose(r2.history, r1.history, rtol=1e-12, atol=0)
