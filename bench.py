@@ -53,6 +53,7 @@ KERNEL_BYTES = {
     "fine_sweep_pair": 24,     # two sweeps in one pass: read u, f; write u''
     "fine_restrict": 20,       # read u, f; write f_c (half size: 4 B per fine DOF)
     "fine_prolong_sweep": 28,  # read u, f, x_c (4 B per fine DOF); write u'
+    "fine_up": 36,             # prolongation + post-sweep + norm + next pre-sweep: read u, f, x_c; write u', u''
 }
 KERNEL_NAMES = {
     "fine_norm_pass": "k_lean2<sweep, norm> (residual norm + speculative first sweep)",
@@ -60,6 +61,7 @@ KERNEL_NAMES = {
     "fine_sweep_pair": "k_lean2x2 (two fused Jacobi sweeps)",
     "fine_restrict": "k_restrict2 (residual + restriction)",
     "fine_prolong_sweep": "k_lean2<sweep, ProlongLoad> (prolongation + first post-sweep)",
+    "fine_up": "k_up (prolongation + post-sweep + residual norm + next cycle's first sweep)",
 }
 
 

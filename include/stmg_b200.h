@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define STMG_ABI_VERSION 2
+#define STMG_ABI_VERSION 3
 
 enum stmg_status_code {
   STMG_OK = 0,
@@ -112,6 +112,10 @@ typedef struct stmg_solve_report {
    * (+ the next cycle's level-0 restriction under STMG_FUSE_FINE_DOWN) */
   int64_t fine_norm_passes;
   double fine_norm_pass_seconds;
+  /* the level-0 up-pass closing each cycle under STMG_FUSE_FINE_UP: prolongation +
+   * post-sweep + residual norm + the next cycle's first sweep */
+  int64_t fine_ups;
+  double fine_up_seconds;
 } stmg_solve_report;
 
 typedef struct stmg_hierarchy stmg_hierarchy;
@@ -268,6 +272,8 @@ int stmg_level_restrict_residual(stmg_hierarchy* h, int32_t level, const double*
  *   STMG_FUSED_FINE_DOWN           y = S(x), f_coarse = R (f - J y), *norm2 = ||f - J x||^2
  *   STMG_FUSED_NORM_SWEEP          y = S(x), *norm2 = ||f - J x||^2 (the solve loop's norm pass)
  *   STMG_FUSED_PROLONG_SWEEP       y = S(x + P x_coarse) (the first post-smoothing sweep)
+ *   STMG_FUSED_FINE_UP             y = S(x + P x_coarse), f_coarse = S(y) (a FINE-level vector here:
+ *                                  the next cycle's speculative pre-sweep), *norm2 = ||f - J y||^2
  * Unused pointers may be null. */
 enum {
   STMG_FUSED_ZERO_SWEEP = 0,
@@ -276,7 +282,8 @@ enum {
   STMG_FUSED_ZERO_PROLONG_SWEEP = 3,
   STMG_FUSED_FINE_DOWN = 4,
   STMG_FUSED_NORM_SWEEP = 5,
-  STMG_FUSED_PROLONG_SWEEP = 6
+  STMG_FUSED_PROLONG_SWEEP = 6,
+  STMG_FUSED_FINE_UP = 7
 };
 int stmg_level_fused(stmg_hierarchy* h, int32_t level, int32_t kind, const double* f, const double* x,
                      const double* x_coarse, double* y, double* f_coarse, double omega, double* norm2);
@@ -391,14 +398,24 @@ void stmg_dist_destroy(stmg_dist* d);
  * Captured V-cycle graphs of the handle are rebuilt on the next solve. */
 int stmg_hierarchy_set_tiling(stmg_hierarchy* h, int64_t small_dofs, int64_t tiny_dofs);
 /* Per-handle V-cycle fusions (A/B measurements and bitwise tests; default
- * STMG_FUSE_DEFAULT = STMG_FUSE_VIRTUAL_ZERO, the combination measured fastest).
+ * STMG_FUSE_DEFAULT = STMG_FUSE_VIRTUAL_ZERO | STMG_FUSE_FINE_UP, the combination measured fastest).
  * Every combination gives bit-identical iterates.
  *   STMG_FUSE_VIRTUAL_ZERO: a coarse level's first sweep from zero is recomputed
  *     from f by the kernels that read it instead of being stored and re-read;
  *   STMG_FUSE_FINE_DOWN: for nu = 1, level 0's residual norm, pre-smoothing sweep
- *     and residual restriction run as one pass over memory.
+ *     and residual restriction run as one pass over memory;
+ *   STMG_FUSE_FINE_UP: for nu = 1, level 0's prolongation, post-smoothing sweep, the
+ *     residual norm closing the cycle and the next cycle's pre-smoothing sweep run as
+ *     one pass (36 B/DOF instead of 28 + 24; needs a third level-0 vector); takes
+ *     precedence over STMG_FUSE_FINE_DOWN.
  * Captured graphs of the handle are rebuilt on the next solve. */
-enum { STMG_FUSE_VIRTUAL_ZERO = 1, STMG_FUSE_FINE_DOWN = 2, STMG_FUSE_ALL = 3, STMG_FUSE_DEFAULT = 1 };
+enum {
+  STMG_FUSE_VIRTUAL_ZERO = 1,
+  STMG_FUSE_FINE_DOWN = 2,
+  STMG_FUSE_FINE_UP = 4,
+  STMG_FUSE_ALL = 7,
+  STMG_FUSE_DEFAULT = 5
+};
 int stmg_hierarchy_set_fusion(stmg_hierarchy* h, int32_t flags);
 
 #ifdef __cplusplus

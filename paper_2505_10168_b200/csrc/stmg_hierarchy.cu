@@ -383,6 +383,10 @@ struct Workspace {
   // device solve loop: SolveLoopCtl + history[kLoopHistory + 1], and a pinned mirror
   std::unique_ptr<DeviceBuf> loop;
   double* loop_host = nullptr;
+  // device-resident buffer pointers the fine up-pass kernels read (the speculative
+  // iterate alternates between two buffers from cycle to cycle): [0] in, [1] out
+  std::unique_ptr<DeviceBuf> ptrs;
+  std::unique_ptr<DeviceBuf> xz;  // third level-0 iterate buffer (fine up-pass), allocated on first use
   ~Workspace() {
     if (pinned) cudaFreeHost(pinned);
     if (loop_host) cudaFreeHost(loop_host);
@@ -411,11 +415,13 @@ constexpr size_t kMaxGraphs = 16;
 enum FusionFlags {
   kFuseVirtualZero = 1,  // coarse first sweep from zero recomputed from f where read
   kFuseFineDown = 2,     // level 0 (nu = 1): norm + sweep + residual restriction in one pass
-  kFuseAll = 3,
-  // measured (cfg2, profiles/round2_fusion_ab.txt): the virtual zero iterate pays,
-  // the fine down-pass does not (k_down is issue-bound: 1.06 ms vs 0.51 + 0.55 ms
-  // for the separate sweep and restriction on a 1.3e8-DOF level)
-  kFuseDefault = kFuseVirtualZero
+  kFuseFineUp = 4,       // level 0 (nu = 1): prolongation + post-sweep + norm + next pre-sweep in one pass
+  kFuseAll = 7,
+  // measured (cfg2): the virtual zero iterate pays (89 -> 85 ms), the fine up-pass pays
+  // (75.9 -> 72.4 ms; 69.4 with 128 registers), the fine down-pass does not (k_down:
+  // 0.92 ms vs 0.51 + 0.59 ms for the separate kernels on a 1.3e8-DOF level, but no
+  // gain in the power-capped solve)
+  kFuseDefault = kFuseVirtualZero | kFuseFineUp
 };
 
 enum TimedKind {
@@ -445,6 +451,8 @@ struct GraphEntry {
   cudaGraph_t loop_graph = nullptr;
   cudaGraphExec_t loop_exec = nullptr;
   bool loop_tried = false;
+  // fine up-pass: the graph ends before level 0's prolongation; level 1's result buffer
+  const double* up_xc = nullptr;
 };
 
 void destroy_graph_entry(GraphEntry& e) {
@@ -846,6 +854,7 @@ std::shared_ptr<Workspace> make_workspace(const stmg_hierarchy* h, int64_t* byte
     max_partials = std::max(max_partials, sweep_partials_needed(finest_tiles));
     if (l == 0 && nl > 1)
       max_partials = std::max(max_partials, down_partials_needed(finest_tiles, h->views[1], h->dirs[0]));
+    if (l + 1 < nl) max_partials = std::max(max_partials, up_partials_needed(finest_tiles));
   }
   ws->partials = std::make_unique<DeviceBuf>(max_partials + kPartialsScratch);
   ws->scalars = std::make_unique<DeviceBuf>(8);
@@ -855,6 +864,7 @@ std::shared_ptr<Workspace> make_workspace(const stmg_hierarchy* h, int64_t* byte
   ws->coarse_scratch = std::make_unique<DeviceBuf>(scratch);
   *bytes += 8 * (max_partials + 8 + scratch);
   cuda_check(cudaMallocHost(&ws->pinned, 8 * sizeof(double)), "cudaMallocHost");
+  ws->ptrs = std::make_unique<DeviceBuf>(8);
   ws->loop = std::make_unique<DeviceBuf>(kLoopCtlDoubles + kLoopHistory + 1);
   cuda_check(cudaMallocHost(&ws->loop_host, sizeof(double) * (kLoopCtlDoubles + kLoopHistory + 1)),
              "cudaMallocHost");
@@ -894,9 +904,19 @@ void finish_create(stmg_hierarchy* h, bool share_ws_from_other, const stmg_hiera
 
 // nu = 1 cycles whose level-0 residual restriction runs inside the norm pass
 // that closes the previous cycle (k_down: norm + sweep + restriction).
-bool fine_down(const stmg_hierarchy* h, int nu) {
-  return (h->fusion & kFuseFineDown) && nu == 1 && h->n_levels() >= 2 && !h->galerkin(0) && !h->gen_xfer(0);
+// nu = 1 cycles whose level-0 prolongation, post-sweep, closing residual norm and the
+// next cycle's speculative pre-sweep run as one pass (k_up); takes precedence over
+// the fine down-pass (both would own the norm pass).
+bool fine_up(const stmg_hierarchy* h, int nu) {
+  return (h->fusion & kFuseFineUp) && nu == 1 && h->n_levels() >= 2 && !h->galerkin(0) && !h->gen_xfer(0);
 }
+bool fine_down(const stmg_hierarchy* h, int nu) {
+  return (h->fusion & kFuseFineDown) && !fine_up(h, nu) && nu == 1 && h->n_levels() >= 2 && !h->galerkin(0) &&
+         !h->gen_xfer(0);
+}
+// device-resident pointer table of the fine up-pass: [0] the speculative iterate the
+// cycle reads (restriction, up-pass), [1] where the up-pass writes the next one
+inline double** up_ptrs(const stmg_hierarchy* h) { return reinterpret_cast<double**>(h->ws->ptrs->p); }
 
 // How level l + 1 gets its first sweep from zero: recomputed from f where it
 // is read (virt), written by level l's restriction (store), or neither (the
@@ -924,6 +944,10 @@ struct Emitter {
   // level 0's restriction was done by the norm pass closing the previous cycle
   // (fine_down); the V-cycle then starts at level 1
   bool down_done = false;
+  // fine up-pass: level 0 reads its iterate through the pointer table and the cycle
+  // graph ends after level 1 (the up-pass kernel follows it); up_xc: level 1's result
+  bool up_fused = false;
+  const double* up_xc = nullptr;
 
   template <class F>
   void timed_launch(int l, int kind, F&& launch) {
@@ -1054,7 +1078,7 @@ struct Emitter {
       timed_launch(l, kTimedRestrict, [&] {
         launch_check(launch_restrict_residual(h->adjoint, L, C, h->dirs[l], f, virt ? nullptr : buf(l, cur),
                                               h->ws->f[l + 1]->p, s, fuse_zero ? buf(l + 1, 0) : nullptr,
-                                              omega),
+                                              omega, l == 0 && up_fused ? up_ptrs(h) : nullptr),
                      "restrict");
       });
       ++kernels;
@@ -1071,6 +1095,11 @@ struct Emitter {
     }
     const int child = level(l + 1, 0, 0, true, fuse_zero, virt_zero);
     const double* xc = buf(l + 1, child);
+    if (l == 0 && up_fused) {  // the up-pass kernel (emit_up) prolongs, smooths and closes the cycle
+      if (!fused || virt || nu != 1) throw std::logic_error("fine up-pass on an unsupported level 0");
+      up_xc = xc;
+      return 0;
+    }
     int post = nu;
     if (virt && !fused) throw std::logic_error("virtual zero iterate on a level without fused transfers");
     if (!fused) {
@@ -1118,6 +1147,16 @@ void launch_norm_pass(stmg_hierarchy* h, int nu, const double* f, const double* 
   launch_check(launch_sweep(h->adjoint, h->views[0], f, x, y, omega, ws.partials->p, np, s), "norm sweep");
 }
 
+// Fine up-pass (k_up) closing a cycle: u = S(*P[0] + P x_c) into the primary buffer,
+// the next speculative iterate into *P[1], partials of ||f - J u||^2.
+void launch_up_pass(stmg_hierarchy* h, const double* xc, double omega, cudaStream_t s, int64_t* np) {
+  Workspace& ws = *h->ws;
+  double** P = up_ptrs(h);
+  launch_check(launch_up(h->adjoint, h->views[0], h->views[1], h->dirs[0], h->f_ptr(0), ws.xb[0]->p, xc, h->xa_ptr(0),
+                         P + 1, P, omega, ws.partials->p, np, s),
+               "prolong + sweep + norm + sweep");
+}
+
 GraphEntry& get_graph(stmg_hierarchy* h, int nu, double omega) {
   const GraphKey key{nu, omega, h->profiling, h->f_ptr(0), h->xa_ptr(0)};  // profiling: int mode, 0 = off
   auto it = h->graphs.find(key);
@@ -1130,6 +1169,7 @@ GraphEntry& get_graph(stmg_hierarchy* h, int nu, double omega) {
   GraphEntry e;
   Emitter em{h, nu, omega, h->cap_stream};
   em.down_done = fine_down(h, nu);
+  em.up_fused = fine_up(h, nu);
   if (h->profiling) {
     em.timed = &e.timed;
     em.prof_mode = h->profiling;
@@ -1140,6 +1180,7 @@ GraphEntry& get_graph(stmg_hierarchy* h, int nu, double omega) {
   cuda_check(cudaStreamEndCapture(h->cap_stream, &e.graph), "end capture");
   cuda_check(cudaGraphInstantiate(&e.exec, e.graph, 0), "graph instantiate");
   e.kernels = em.kernels;
+  e.up_xc = em.up_xc;
   return h->graphs.emplace(key, e).first->second;
 }
 
@@ -1179,16 +1220,19 @@ cudaGraphExec_t get_loop(stmg_hierarchy* h, int nu, double omega) {
   try {
     Emitter em{h, nu, omega, cs};
     em.down_done = fine_down(h, nu);
+    em.up_fused = fine_up(h, nu);
     const bool spec = h->n_levels() > 1 && nu >= 1;
     const int fin = em.level(0, spec ? 1 : 0, spec ? 1 : 0, false);
     if (fin != 0) throw std::logic_error("level-0 iterate left the primary buffer");
     Workspace& ws = *h->ws;
     int64_t np = 0;
-    launch_norm_pass(h, nu, h->f_ptr(0), h->xa_ptr(0), spec ? ws.xb[0]->p : nullptr, omega, cs, &np);
+    if (em.up_fused) launch_up_pass(h, em.up_xc, omega, cs, &np);
+    else launch_norm_pass(h, nu, h->f_ptr(0), h->xa_ptr(0), spec ? ws.xb[0]->p : nullptr, omega, cs, &np);
     auto* ctl = reinterpret_cast<SolveLoopCtl*>(ws.loop->p);
     launch_check(launch_finalize_check(ws.partials->p, np, ws.scalars->p, ctl, ws.loop->p + kLoopCtlDoubles,
                                        handle, cs),
                  "finalize + cycle check");
+    if (em.up_fused) launch_check(launch_swap_ptrs(up_ptrs(h), cs), "swap");
   } catch (...) {
     ok = false;
   }
@@ -1308,8 +1352,21 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
   rep->fine_sweep_pair_seconds = 0.0;
   rep->fine_norm_passes = 0;
   rep->fine_norm_pass_seconds = 0.0;
+  rep->fine_ups = 0;
+  rep->fine_up_seconds = 0.0;
   double per_cycle_updates = 0.0;
   for (int l = 0; l + 1 < h->n_levels(); ++l) per_cycle_updates += 2.0 * o.nu * static_cast<double>(h->ndofs(l));
+  const bool up = fine_up(h, o.nu) && o.max_cycles > 0;
+  if (up && r0 >= o.tol) {
+    // third level-0 buffer and the pointer table {speculative iterate in, out} = {Y, Z}
+    if (!ws.xz) {
+      ws.xz = std::make_unique<DeviceBuf>(n + kVecPad);
+      h->device_bytes += 8 * (n + kVecPad);
+    }
+    double* tab[2] = {Y, ws.xz->p};
+    std::memcpy(ws.pinned + 4, tab, sizeof(tab));
+    cuda_check(cudaMemcpyAsync(ws.ptrs->p, ws.pinned + 4, sizeof(tab), cudaMemcpyHostToDevice, h->stream), "ptrs");
+  }
   cudaGraphExec_t loop = nullptr;
   if (r0 >= o.tol && o.max_cycles > 0 && o.max_cycles <= kLoopHistory && !h->profiling)
     loop = get_loop(h, o.nu, o.omega);
@@ -1332,9 +1389,10 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
     rep->status = ctl->status;
     rep->smoother_dof_updates = per_cycle_updates * ctl->cycles;
     // per cycle: the V-cycle graph, the norm pass and its fixed-order sum
-    const int64_t norm_np = fine_down(h, o.nu) ? down_partials_needed(h->views[0], h->views[1], h->dirs[0])
-                                                : sweep_partials_needed(h->views[0]);
-    launches += static_cast<int64_t>(ctl->cycles) * (g->kernels + 1 + finalize_launches(norm_np));
+    const int64_t norm_np = up ? up_partials_needed(h->views[0])
+                               : fine_down(h, o.nu) ? down_partials_needed(h->views[0], h->views[1], h->dirs[0])
+                                                    : sweep_partials_needed(h->views[0]);
+    launches += static_cast<int64_t>(ctl->cycles) * (g->kernels + 1 + finalize_launches(norm_np) + (up ? 1 : 0));
   } else {
     rep->status = STMG_MAX_CYCLES;
     for (int cycle = 1; cycle <= o.max_cycles; ++cycle) {
@@ -1344,14 +1402,30 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
       if (g->final_buf != 0) throw std::logic_error("level-0 iterate left the primary buffer");
       const bool more = cycle < o.max_cycles;
       if (h->profiling) cuda_check(cudaEventRecord(h->norm_ev0, h->stream), "event");
-      launches += emit_norm(h, o.nu, B, X, spec && more ? Y : nullptr, o.omega, 1);
+      if (up) {
+        int64_t np = 0;
+        launch_up_pass(h, g->up_xc, o.omega, h->stream, &np);
+        launch_check(launch_finalize_sum(ws.partials->p, np, ws.scalars->p + 1, h->stream), "finalize");
+        launches += 1 + finalize_launches(np);
+      } else {
+        launches += emit_norm(h, o.nu, B, X, spec && more ? Y : nullptr, o.omega, 1);
+      }
       if (h->profiling) cuda_check(cudaEventRecord(h->norm_ev1, h->stream), "event");
+      if (up) {
+        launch_check(launch_swap_ptrs(up_ptrs(h), h->stream), "swap");
+        launches += 1;
+      }
       fetch_scalars(h, 2, sc);
-      if (h->profiling) {  // the norm pass (incl. its finalize launch)
+      if (h->profiling) {  // the pass closing the cycle (incl. its finalize launch)
         float ms = 0.f;
         cuda_check(cudaEventElapsedTime(&ms, h->norm_ev0, h->norm_ev1), "event elapsed");
-        rep->fine_norm_passes += 1;
-        rep->fine_norm_pass_seconds += ms * 1e-3;
+        if (up) {
+          rep->fine_ups += 1;
+          rep->fine_up_seconds += ms * 1e-3;
+        } else {
+          rep->fine_norm_passes += 1;
+          rep->fine_norm_pass_seconds += ms * 1e-3;
+        }
       }
       for (const TimedKernel& t : g->timed) {
         float ms = 0.f;
@@ -2254,7 +2328,8 @@ int stmg_level_fused(stmg_hierarchy* h, int32_t l, int32_t kind, const double* f
     if (h->galerkin(l)) throw std::invalid_argument("level_fused: per-node levels only");
     if (!f) throw std::invalid_argument("level_fused: null f");
     const bool coarse_op = kind == STMG_FUSED_ZERO_RESTRICT || kind == STMG_FUSED_ZERO_PROLONG_SWEEP ||
-                           kind == STMG_FUSED_FINE_DOWN || kind == STMG_FUSED_PROLONG_SWEEP;
+                           kind == STMG_FUSED_FINE_DOWN || kind == STMG_FUSED_PROLONG_SWEEP ||
+                           kind == STMG_FUSED_FINE_UP;
     if (coarse_op && (l + 1 >= h->n_levels() || h->gen_xfer(l)))
       throw std::out_of_range("level_fused: no fused transfer to a coarser level");
     DeviceGuard dg(h->device);
@@ -2297,6 +2372,23 @@ int stmg_level_fused(stmg_hierarchy* h, int32_t l, int32_t kind, const double* f
         launch_check(launch_sweep_prolong(h->adjoint, L, h->views[l + 1], h->dirs[l], f, x, xc, y, omega, h->stream),
                      "sweep_prolong");
         break;
+      case STMG_FUSED_FINE_UP: {
+        if (!x || !y || !xc || !fc || x == y || x == fc || y == fc)
+          throw std::invalid_argument("level_fused: fine up-pass needs distinct x, y and w (f_coarse)");
+        double* const wptr = fc;
+        cuda_check(cudaMemcpyAsync(h->ws->ptrs->p, &wptr, sizeof(wptr), cudaMemcpyHostToDevice, h->stream), "ptr");
+        cuda_check(cudaStreamSynchronize(h->stream), "sync");  // wptr is a stack variable
+        int64_t np = 0;
+        launch_check(launch_up(h->adjoint, L, h->views[l + 1], h->dirs[l], f, x, xc, y,
+                               reinterpret_cast<double* const*>(h->ws->ptrs->p), nullptr, omega, h->ws->partials->p,
+                               &np, h->stream),
+                     "up");
+        launch_check(launch_finalize_sum(h->ws->partials->p, np, h->ws->scalars->p + 2, h->stream), "finalize");
+        double sc[3];
+        fetch_scalars(h, 3, sc);
+        if (norm2) *norm2 = sc[2];
+        break;
+      }
       case STMG_FUSED_NORM_SWEEP: {
         if (!x || !y) throw std::invalid_argument("level_fused: null x / y");
         int64_t np = 0;

@@ -191,7 +191,9 @@ int launch_residual(bool adjoint, const LevelView& L, const double* f, const dou
 // launch_sweep_from_zero on fc).
 int launch_restrict_residual(bool adjoint, const LevelView& F, const LevelView& C, int dir,
                              const double* f, const double* x, double* fc, cudaStream_t s,
-                             double* xc0 = nullptr, double omega = 0.0);
+                             double* xc0 = nullptr, double omega = 0.0, const double* const* x_ind = nullptr);
+// p[0] <-> p[1] (device-resident buffer pointers of the fine up-pass)
+int launch_swap_ptrs(double** p, cudaStream_t s);
 // Level-0 down-pass of a V(1,1) cycle in one pass: block partials of
 // ||f - J x||^2, y = S(x), fc = R (f - J y) and, if xc0 != nullptr, the coarse
 // first sweep from zero (bitwise the separate sweep / restriction kernels).
@@ -199,6 +201,14 @@ int launch_down(bool adjoint, const LevelView& F, const LevelView& C, int dir, c
                 double* y, double* fc, double* xc0, double omega, double* partials, int64_t* n_partials,
                 cudaStream_t s);
 int64_t down_partials_needed(const LevelView& F, const LevelView& C, int dir);
+// Fine up-pass of a V(1,1) cycle in one pass (k_up): u_out = S(x + P xc) (the cycle's
+// result), *w_ind = S(u_out) (the next cycle's speculative pre-sweep), one partial per
+// warp of ||f - A u_out||^2.  x_ind: optional device-resident pointer to the input
+// iterate (read instead of x).  x, u_out and *w_ind are three distinct buffers.
+int launch_up(bool adjoint, const LevelView& L, const LevelView& C, int dir, const double* f, const double* x,
+              const double* xc, double* u_out, double* const* w_ind, const double* const* x_ind, double omega,
+              double* partials, int64_t* n_partials, cudaStream_t s);
+int64_t up_partials_needed(const LevelView& L);
 int launch_restrict(const LevelView& F, const LevelView& C, int dir, const double* r, double* fc,
                     cudaStream_t s);
 int launch_prolong_add(const LevelView& F, const LevelView& C, int dir, const double* xc, double* x,

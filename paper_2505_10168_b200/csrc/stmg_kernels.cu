@@ -618,6 +618,166 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
   }
 }
 
+// Fine up-pass of a V(1,1) cycle in one pass over memory (level 0, nu = 1): the
+// prolongation, the post-smoothing sweep, the residual norm that closes the cycle and
+// the speculative first sweep of the next cycle,
+//   v = x + P x_c               (proj/src/multigrid.cpp:202, staged, never stored)
+//   u = v + omega ((f - A v) inv_diag)    the cycle's result          -> u_out
+//   r = f - A u, sum r^2        (multigrid.cpp:246-249)               -> partial per warp
+//   w = u + omega (r inv_diag)  the next cycle's pre-smoothing sweep  -> w_out
+// i.e. the fused pair (dev_lean2x2) on the prolongated iterate with both sweeps stored
+// and the second residual's squares summed: 36 B/DOF instead of 28 (prolong-sweep) + 24
+// (norm pass).  u_out, w_out and x are three distinct buffers (every tile reads x rows
+// that other tiles own).  Values are the separate kernels' bit for bit; the norm's
+// summation order differs (deterministic).
+template <bool ADJ, int NT, class Ld>
+__device__ __forceinline__ double dev_up(const LevelView& L, const Ld& ld, const double* __restrict__ f,
+                                         double* __restrict__ u_out, double* __restrict__ w_out, double omega,
+                                         int64_t tile, int64_t ttile) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nn = L.nn, nt = L.n_t;
+  const int64_t node1 = tile * ((int64_t)(blockDim.x >> 5) * 28) + warp * 28 - 1;  // node of lane 1
+  if (node1 + 1 >= nn) return 0.0;  // no stored node in this warp (whole warp exits)
+  const int64_t i = node1 + lane - 1;  // node of this lane
+  const int64_t n0 = L.n_lo + ttile * NT;
+  const int64_t sbase = ADJ ? n0 : n0 - 2;   // staged rows (NT + 2)
+  const int64_t s1base = ADJ ? n0 : n0 - 1;  // sweep-1 rows (NT + 1)
+  const bool rows_in = (ADJ ? (n0 >= 1 && n0 + NT <= nt - 1) : (n0 >= 3 && n0 + NT - 1 <= nt)) &&
+                       n0 + NT - 1 < L.n_hi;
+  const bool nodes_in = node1 >= 2 && node1 + 29 <= L.n_el - 1;
+  double xs[NT + 2], fv[NT + 1], y1[NT + 1];
+  double acc = 0.0;
+  if (rows_in && nodes_in) {
+    const uint32_t nn32 = (uint32_t)nn;
+    const double* __restrict__ fb = opaque(f + (s1base * nn + i));
+#pragma unroll
+    for (int r = 0; r < NT + 1; ++r) fv[r] = __ldg(fb + (uint32_t)r * nn32);  // f rows s1base + r
+    const typename Ld::Lane lc = ld.lane(sbase, i, node1 - 1, lane);
+    typename Ld::Raw raw[NT + 2];
+#pragma unroll
+    for (int r = 0; r < NT + 2; ++r) raw[r] = ld.load(lc, r, nn32);
+    const Coefs c = load_coefs(L, i);
+#pragma unroll
+    for (int r = 0; r < NT + 2; ++r) xs[r] = ld.finish(raw[r], lc, i, c.invd);
+    double* __restrict__ ub = opaque(u_out + (s1base * nn + i));
+    double* __restrict__ wb = opaque(w_out + (n0 * nn + i));
+    const bool lane2 = lane >= 2 && lane <= 29;
+    double pm = __shfl_up_sync(kFull, xs[0], 1), pp = __shfl_down_sync(kFull, xs[0], 1);
+#pragma unroll
+    for (int r = 0; r <= NT; ++r) {
+      const double x1 = xs[r + 1];
+      const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
+      if (ADJ) y1[r] = xs[r] + omega * ((fv[r] - row_interior<true>(c, pm, xs[r], pp, qm, x1, qp)) * c.invd);
+      else y1[r] = x1 + omega * ((fv[r] - row_interior<false>(c, qm, x1, qp, pm, xs[r], pp)) * c.invd);
+      const bool own_row = ADJ ? r < NT : r >= 1;  // rows n0 .. n0 + NT - 1
+      if (own_row && lane2) *(ub + (uint32_t)r * nn32) = y1[r];
+      pm = qm;
+      pp = qp;
+    }
+    double am = __shfl_up_sync(kFull, y1[0], 1), ap = __shfl_down_sync(kFull, y1[0], 1);
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const double z1 = y1[k + 1];
+      const double bm = __shfl_up_sync(kFull, z1, 1), bp = __shfl_down_sync(kFull, z1, 1);
+      const double res = ADJ ? fv[k] - row_interior<true>(c, am, y1[k], ap, bm, z1, bp)
+                             : fv[k + 1] - row_interior<false>(c, bm, z1, bp, am, y1[k], ap);
+      const double x0 = ADJ ? y1[k] : z1;
+      if (lane2) {
+        acc = acc + res * res;
+        *(wb + (uint32_t)k * nn32) = x0 + omega * (res * c.invd);
+      }
+      am = bm;
+      ap = bp;
+    }
+    return acc;
+  }
+  // ---- general path (boundary tiles): per-row-class evaluation
+  const bool in_grid = i >= 0 && i < nn;
+  const bool lane1 = lane >= 1 && lane <= 30 && in_grid;
+  const bool lane2 = lane >= 2 && lane <= 29 && in_grid;
+#pragma unroll
+  for (int r = 0; r < NT + 2; ++r) {
+    const int64_t n = sbase + r;
+    xs[r] = (n >= 0 && n <= nt && in_grid) ? ld(n, i) : 0.0;
+  }
+#pragma unroll
+  for (int r = 0; r < NT + 1; ++r) {
+    const int64_t n = s1base + r;
+    fv[r] = (n >= 0 && n <= nt && lane1) ? f[n * nn + i] : 0.0;
+  }
+  Coefs c{};
+  if (lane1) c = load_coefs(L, i);
+  double pm = __shfl_up_sync(kFull, xs[0], 1), pp = __shfl_down_sync(kFull, xs[0], 1);
+#pragma unroll
+  for (int r = 0; r <= NT; ++r) {
+    const double x1 = xs[r + 1];
+    const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
+    const int64_t n = s1base + r;
+    double v = 0.0;
+    if (lane1 && n >= 0 && n <= nt) {
+      const double row = ADJ ? row_sum<true>(L, n, i, c, pm, xs[r], pp, qm, x1, qp)
+                             : row_sum<false>(L, n, i, c, qm, x1, qp, pm, xs[r], pp);
+      const double id = (n == 0 || i == 0) ? L.inv_w : c.invd;
+      v = (ADJ ? xs[r] : x1) + omega * ((fv[r] - row) * id);
+      if (lane2 && n >= n0 && n < n0 + NT && n < L.n_hi) u_out[n * nn + i] = v;
+    }
+    y1[r] = v;
+    pm = qm;
+    pp = qp;
+  }
+  double am = __shfl_up_sync(kFull, y1[0], 1), ap = __shfl_down_sync(kFull, y1[0], 1);
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    const double z1 = y1[k + 1];
+    const double bm = __shfl_up_sync(kFull, z1, 1), bp = __shfl_down_sync(kFull, z1, 1);
+    const int64_t n = n0 + k;
+    if (lane2 && n < L.n_hi) {
+      double row, x0, fval;
+      if (ADJ) {
+        row = row_sum<true>(L, n, i, c, am, y1[k], ap, bm, z1, bp);
+        x0 = y1[k];
+        fval = fv[k];
+      } else {
+        row = row_sum<false>(L, n, i, c, bm, z1, bp, am, y1[k], ap);
+        x0 = z1;
+        fval = fv[k + 1];
+      }
+      const double res = fval - row;
+      const double id = (n == 0 || i == 0) ? L.inv_w : c.invd;
+      acc = acc + res * res;
+      w_out[n * nn + i] = x0 + omega * (res * id);
+    }
+    am = bm;
+    ap = bp;
+  }
+  return acc;
+}
+
+// Resident 256-thread blocks per SM k_up is compiled for.  8-level tiles: 2 (up to 128
+// registers, no spills) measured faster than 3 (80 registers, ~100 B of spills): probe
+// 0.99 vs 1.05 ms on 1.3e8 DOFs, config-2 solve 69.4 vs 70.7 ms.
+template <int NT>
+constexpr int up_minb() { return NT <= 2 ? 4 : NT <= 4 ? 3 : 2; }
+
+// x_ind: optional device-resident pointer to the input iterate (overrides the
+// loader's x): the solve loop alternates the speculative iterate between two
+// buffers from cycle to cycle with the graph's kernel arguments fixed.
+template <bool ADJ, int NT, class Ld, int MINB = up_minb<NT>()>
+__global__ void __launch_bounds__(kMaxTW, MINB) k_up(LevelView L, Ld ld, const double* __restrict__ f,
+                                                     double* __restrict__ u_out, double* const* w_ind,
+                                                     const double* const* x_ind, double omega,
+                                                     double* __restrict__ partials) {
+  pdl_entry();
+  if (x_ind != nullptr) ld.base.x = *x_ind;
+  double* w_out = *w_ind;
+  const int64_t tt = (int64_t)blockIdx.z * gridDim.y + blockIdx.y;  // time tile
+  double acc = 0.0;
+  if (tt < ceil_div(L.n_hi - L.n_lo, NT)) acc = dev_up<ADJ, NT>(L, ld, f, u_out, w_out, omega, blockIdx.x, tt);
+  for (int o = 16; o > 0; o >>= 1) acc = acc + __shfl_xor_sync(kFull, acc, o);
+  if ((threadIdx.x & 31) == 0)
+    partials[(tt * gridDim.x + blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)] = acc;
+}
+
 // Resident blocks per SM the kernels are compiled for: 5 (48 registers) pays on
 // mid-sized levels, where the launch fills the GPU and latency is hidden by
 // warps; on small levels the few blocks never fill the SMs and the spills of the
@@ -817,11 +977,15 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
 }
 
 // omega: the coarse first sweep's (xc0) and, with ZX, the fine iterate's S(0).
+// x_ind: optional device-resident pointer to the iterate, read instead of x (the
+// fine up-pass alternates the speculative iterate between two buffers).
 template <bool ADJ, int DIR, int NT, int MINB = minb_for_nt<NT>(), bool ZX = false>
 __global__ void __launch_bounds__(kMaxTW, MINB) k_restrict2(LevelView F, LevelView C, const double* __restrict__ f,
-                                                         const double* __restrict__ x, double* __restrict__ fc,
-                                                         double* __restrict__ xc0, double omega) {
+                                                         const double* x, double* __restrict__ fc,
+                                                         double* __restrict__ xc0, double omega,
+                                                         const double* const* x_ind) {
   pdl_entry();
+  if (!ZX && x_ind != nullptr) x = *x_ind;
   const int64_t tt = (int64_t)blockIdx.z * gridDim.y + blockIdx.y;
   if (tt < ceil_div(F.n_hi - F.n_lo, NT))
     dev_restrict2<ADJ, DIR, NT, ZX>(F, C, f, x, fc, blockIdx.x, tt, blockDim.x, xc0, omega);
@@ -1732,30 +1896,30 @@ int sweep_prolong_impl(const LevelView& L, const LevelView& C, const double* f, 
 
 template <bool ADJ, int DIR, bool ZX>
 void restrict_launch(const LevelView& F, const LevelView& C, const double* f, const double* x,
-                     double* fc, cudaStream_t s, double* xc0, double omega) {
+                     double* fc, cudaStream_t s, double* xc0, double omega, const double* const* x_ind) {
   // DIR 0: warp w owns coarse nodes 14 w .. 14 w + 13; DIR 1: fine nodes 30 w ..
   const int64_t warps = DIR == 0 ? ceil_div(C.nn, 14) : ceil_div(F.nn, 30);
   const dim3 rb = balanced_block(warps, wpb_for(F));
   const int64_t tiles = ceil_div(warps, rb.x / 32);
   if (lean_nt(F) == 2 && F.nn * (F.n_t + 1) >= kMinB5Dofs)
     pdl_launch(k_restrict2<ADJ, DIR, 2, minb_for_nt<2>(), ZX>, tgrid(tiles, (rows(F) + 1) / 2), rb, 0, s, F, C,
-               f, x, fc, xc0, omega);
+               f, x, fc, xc0, omega, x_ind);
   else if (lean_nt(F) == 2)
     pdl_launch(k_restrict2<ADJ, DIR, 2, 3, ZX>, tgrid(tiles, (rows(F) + 1) / 2), rb, 0, s, F, C, f, x, fc, xc0,
-               omega);
+               omega, x_ind);
   else if (lean_nt(F) == 4)
     pdl_launch(k_restrict2<ADJ, DIR, 4, minb_for_nt<4>(), ZX>, tgrid(tiles, (rows(F) + 3) / 4), rb, 0, s, F, C,
-               f, x, fc, xc0, omega);
+               f, x, fc, xc0, omega, x_ind);
   else
     pdl_launch(k_restrict2<ADJ, DIR, 8, minb_for_nt<8>(), ZX>, tgrid(tiles, (rows(F) + 7) / 8), rb, 0, s, F, C,
-               f, x, fc, xc0, omega);
+               f, x, fc, xc0, omega, x_ind);
 }
 
 template <bool ADJ, int DIR>
 int restrict_impl(const LevelView& F, const LevelView& C, const double* f, const double* x,
-                  double* fc, cudaStream_t s, double* xc0, double omega) {
-  if (x == nullptr) restrict_launch<ADJ, DIR, true>(F, C, f, x, fc, s, xc0, omega);  // x = S(0) from f
-  else restrict_launch<ADJ, DIR, false>(F, C, f, x, fc, s, xc0, omega);
+                  double* fc, cudaStream_t s, double* xc0, double omega, const double* const* x_ind) {
+  if (x == nullptr) restrict_launch<ADJ, DIR, true>(F, C, f, x, fc, s, xc0, omega, nullptr);  // x = S(0) from f
+  else restrict_launch<ADJ, DIR, false>(F, C, f, x, fc, s, xc0, omega, x_ind);
   return check_launch();
 }
 
@@ -1851,6 +2015,48 @@ int launch_down(bool adjoint, const LevelView& F, const LevelView& C, int dir, c
   return check_launch();
 }
 
+namespace {
+inline dim3 up_block(const LevelView& L) { return balanced_block(ceil_div(L.nn, 28), wpb_for(L)); }
+inline dim3 up_grid(const LevelView& L, dim3 blk) {
+  const int64_t tiles = ceil_div(ceil_div(L.nn, 28), blk.x / 32);
+  return tgrid(tiles, ceil_div(rows(L), lean_nt(L)));
+}
+template <bool ADJ, int DIR>
+void up_launch(const LevelView& L, const LevelView& C, const double* f, const double* x, const double* xc,
+               double* u_out, double* const* w_ind, const double* const* x_ind, double omega, double* partials,
+               cudaStream_t s) {
+  const ProlongLoad<DIR> ld{PlainLoad{x, L.nn}, xc, C.nn};
+  const dim3 blk = up_block(L), grd = up_grid(L, blk);
+  if (lean_nt(L) == 2)
+    pdl_launch(k_up<ADJ, 2, ProlongLoad<DIR>>, grd, blk, 0, s, L, ld, f, u_out, w_ind, x_ind, omega, partials);
+  else if (lean_nt(L) == 4)
+    pdl_launch(k_up<ADJ, 4, ProlongLoad<DIR>>, grd, blk, 0, s, L, ld, f, u_out, w_ind, x_ind, omega, partials);
+  else
+    pdl_launch(k_up<ADJ, 8, ProlongLoad<DIR>>, grd, blk, 0, s, L, ld, f, u_out, w_ind, x_ind, omega, partials);
+}
+}  // namespace
+
+int64_t up_partials_needed(const LevelView& L) {
+  const dim3 b = up_block(L), g = up_grid(L, b);
+  return (int64_t)g.x * g.y * g.z * (b.x / 32);  // one per warp
+}
+
+// Fine up-pass (k_up): u_out = S(x + P xc), *w_ind = S(u_out), partials of ||f - A u_out||^2.
+// x_ind (optional): device-resident pointer to the input iterate, read instead of x.
+int launch_up(bool adjoint, const LevelView& L, const LevelView& C, int dir, const double* f, const double* x,
+              const double* xc, double* u_out, double* const* w_ind, const double* const* x_ind, double omega,
+              double* partials, int64_t* n_partials, cudaStream_t s) {
+  if (n_partials) *n_partials = up_partials_needed(L);
+  if (adjoint) {
+    if (dir == 0) up_launch<true, 0>(L, C, f, x, xc, u_out, w_ind, x_ind, omega, partials, s);
+    else up_launch<true, 1>(L, C, f, x, xc, u_out, w_ind, x_ind, omega, partials, s);
+  } else {
+    if (dir == 0) up_launch<false, 0>(L, C, f, x, xc, u_out, w_ind, x_ind, omega, partials, s);
+    else up_launch<false, 1>(L, C, f, x, xc, u_out, w_ind, x_ind, omega, partials, s);
+  }
+  return check_launch();
+}
+
 int launch_sweep_from_zero(const LevelView& L, const double* f, double* y, double omega,
                            cudaStream_t s) {
   const dim3 blk = march_block(L);
@@ -1881,12 +2087,28 @@ int launch_residual(bool adjoint, const LevelView& L, const double* f, const dou
 
 int launch_restrict_residual(bool adjoint, const LevelView& F, const LevelView& C, int dir,
                              const double* f, const double* x, double* fc, cudaStream_t s, double* xc0,
-                             double omega) {
+                             double omega, const double* const* x_ind) {
   if (adjoint)
-    return dir == 0 ? restrict_impl<true, 0>(F, C, f, x, fc, s, xc0, omega)
-                    : restrict_impl<true, 1>(F, C, f, x, fc, s, xc0, omega);
-  return dir == 0 ? restrict_impl<false, 0>(F, C, f, x, fc, s, xc0, omega)
-                  : restrict_impl<false, 1>(F, C, f, x, fc, s, xc0, omega);
+    return dir == 0 ? restrict_impl<true, 0>(F, C, f, x, fc, s, xc0, omega, x_ind)
+                    : restrict_impl<true, 1>(F, C, f, x, fc, s, xc0, omega, x_ind);
+  return dir == 0 ? restrict_impl<false, 0>(F, C, f, x, fc, s, xc0, omega, x_ind)
+                  : restrict_impl<false, 1>(F, C, f, x, fc, s, xc0, omega, x_ind);
+}
+
+namespace {
+__global__ void k_swap_ptrs(double** p) {
+  pdl_entry();
+  if (threadIdx.x == 0) {
+    double* t = p[0];
+    p[0] = p[1];
+    p[1] = t;
+  }
+}
+}  // namespace
+
+int launch_swap_ptrs(double** p, cudaStream_t s) {
+  pdl_launch(k_swap_ptrs, 1, 32, 0, s, p);
+  return check_launch();
 }
 
 int launch_restrict(const LevelView& F, const LevelView& C, int dir, const double* r, double* fc,

@@ -125,6 +125,15 @@ struct DirectSolver::Impl {
 
 namespace {
 
+// The structs passed across the C ABI (stmg_solve_report) are this header's: a library
+// built from another version must not be called.
+void check_abi() {
+  static const bool ok = stmg_abi_version() == STMG_ABI_VERSION;
+  if (!ok)
+    throw std::runtime_error("libstmg_b200.so has C ABI version " + std::to_string(stmg_abi_version()) +
+                             ", multigrid_b200.cpp was compiled for " + std::to_string(STMG_ABI_VERSION));
+}
+
 void check(int rc) {
   if (rc == STMG_OK) return;
   const std::string what = stmg_last_error();
@@ -257,6 +266,7 @@ std::vector<double> direct_solve(const SparseMatrix& m, std::span<const double> 
 LevelHierarchy build_hierarchy(const SpaceTimeGrid& fine, const RediscretisationMethod& method,
                                const CoarseningPath& path, const DesignField* chi, const MaterialPair* mat) {
   if (!fine.has_materials()) throw std::invalid_argument("build_hierarchy: fine grid has no materials");
+  check_abi();
   const bool track_chi = method.reassembly == ReassemblyMethod::D;
   if (track_chi && (chi == nullptr || mat == nullptr))
     throw std::invalid_argument("build_hierarchy: D reassembly needs the design field and materials");

@@ -42,6 +42,9 @@ class StmgCudaError(RuntimeError):
     pass
 
 
+ABI_VERSION = 3  # include/stmg_b200.h STMG_ABI_VERSION (stmg_solve_report layout)
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -51,6 +54,9 @@ def _load():
     i32, i64, f64, vp = C.c_int32, C.c_int64, C.c_double, C.c_void_p
     lib.stmg_last_error.restype = C.c_char_p
     lib.stmg_abi_version.restype = C.c_int
+    if lib.stmg_abi_version() != ABI_VERSION:  # struct layouts below are this version's
+        raise ImportError(f"{LIB_PATH} has C ABI version {lib.stmg_abi_version()}, this module needs "
+                          f"{ABI_VERSION}: rebuild with paper_2505_10168_b200/build.py")
     sig = {
         "stmg_apply_design": [vp, i64, vp, vp, vp],
         "stmg_load_vector": [vp, i32, vp, i32, vp],
@@ -175,7 +181,7 @@ class _SolveRep(C.Structure):
                 ("fine_restrict_seconds", C.c_double), ("fine_prolong_sweeps", C.c_int64),
                 ("fine_prolong_sweep_seconds", C.c_double), ("fine_sweep_pairs", C.c_int64),
                 ("fine_sweep_pair_seconds", C.c_double), ("fine_norm_passes", C.c_int64),
-                ("fine_norm_pass_seconds", C.c_double)]
+                ("fine_norm_pass_seconds", C.c_double), ("fine_ups", C.c_int64), ("fine_up_seconds", C.c_double)]
 
 
 # ---- enums ---------------------------------------------------------------------------
@@ -567,14 +573,14 @@ class LevelHierarchy:
         """Per-handle time-tile thresholds (stmg_hierarchy_set_tiling; 0 = defaults)."""
         _check(_lib.stmg_hierarchy_set_tiling(self._h, int(small_dofs), int(tiny_dofs)))
 
-    FUSE_VIRTUAL_ZERO, FUSE_FINE_DOWN, FUSE_ALL, FUSE_DEFAULT = 1, 2, 3, 1
+    FUSE_VIRTUAL_ZERO, FUSE_FINE_DOWN, FUSE_FINE_UP, FUSE_ALL, FUSE_DEFAULT = 1, 2, 4, 7, 5
 
-    def set_fusion(self, flags=1):
+    def set_fusion(self, flags=5):
         """V-cycle fusions (stmg_hierarchy_set_fusion): bit-identical, traffic differs."""
         _check(_lib.stmg_hierarchy_set_fusion(self._h, int(flags)))
 
     (FUSED_ZERO_SWEEP, FUSED_ZERO_PAIR, FUSED_ZERO_RESTRICT, FUSED_ZERO_PROLONG_SWEEP, FUSED_FINE_DOWN,
-     FUSED_NORM_SWEEP, FUSED_PROLONG_SWEEP) = range(7)
+     FUSED_NORM_SWEEP, FUSED_PROLONG_SWEEP, FUSED_FINE_UP) = range(8)
 
     def fused_kernel(self, l, kind, f, x=None, xc=None, y=None, fc=None, omega=0.5):
         """stmg_level_fused on device tensors; returns ||f - J x||^2 for FUSED_FINE_DOWN."""
@@ -684,7 +690,8 @@ def mg_solve(h: LevelHierarchy, b, u, opts: Optional[SolveOptions] = None, zero_
               "fine_sweep_pair": (rep.fine_sweep_pairs, rep.fine_sweep_pair_seconds),
               "fine_restrict": (rep.fine_restricts, rep.fine_restrict_seconds),
               "fine_prolong_sweep": (rep.fine_prolong_sweeps, rep.fine_prolong_sweep_seconds),
-              "fine_norm_pass": (rep.fine_norm_passes, rep.fine_norm_pass_seconds)}
+              "fine_norm_pass": (rep.fine_norm_passes, rep.fine_norm_pass_seconds),
+              "fine_up": (rep.fine_ups, rep.fine_up_seconds)}
     return SolveReport(SolveStatus(rep.status), rep.cycles, rep.factor,
                        [float(v) for v in hist[: rep.n_history]], bool(rep.absolute_norms),
                        rep.seconds, rep.device_seconds, rep.smoother_dof_updates, rep.kernel_launches,

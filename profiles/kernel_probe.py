@@ -48,6 +48,7 @@ def main():
     y = torch.empty_like(x)
     fc = torch.empty(n1, dtype=torch.float64, device=dev)
     xc = torch.randn(n1, dtype=torch.float64, device=dev)
+    w = torch.empty_like(x)
     torch.cuda.synchronize()
     forms = {
         "sweep": lambda: h.sweep_kernels(0, f, x, y, 1, False),
@@ -59,10 +60,11 @@ def main():
         "norm_sweep": lambda: h.fused_kernel(0, H.FUSED_NORM_SWEEP, f, x=x, y=y),
         "prolong_sweep": lambda: h.fused_kernel(0, H.FUSED_PROLONG_SWEEP, f, x=x, xc=xc, y=y),
         "pair_zero": lambda: h.fused_kernel(0, H.FUSED_ZERO_PAIR, f, y=y),
+        "up": lambda: h.fused_kernel(0, H.FUSED_FINE_UP, f, x=x, xc=xc, y=y, fc=w),
     }
     # algorithmic bytes per fine DOF (coarse vectors are half size: 4 B per fine DOF)
     bytes_per_dof = {"sweep": 24, "pair": 24, "restrict": 20, "restrict_zero": 12, "prolong_sweep_zero": 20,
-                     "down": 28, "norm_sweep": 24, "pair_zero": 16, "prolong_sweep": 28}
+                     "down": 28, "norm_sweep": 24, "pair_zero": 16, "prolong_sweep": 28, "up": 36}
     if a.only:
         forms = {k: v for k, v in forms.items() if k in a.only.split(",")}
     if not a.time:

@@ -19,13 +19,18 @@ KEYS = {  # demangled-name fragment -> bench.py kernel key
     "k_lean2x2<0, 8, 3, 0>": "fine_sweep_pair",
     "k_restrict2<0, 0, 8, 3, 0>": "fine_restrict",
     "k_lean2<0, 0, 0, 8, 3, unnamed>::ProlongOn<0, unnamed>::PlainLoad>>": "fine_prolong_sweep",
+    "k_up<0, 8, unnamed>::ProlongOn<0, unnamed>::PlainLoad>": "fine_up",
 }
 METRICS = "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum"
 
 
 def main():
+    path = os.path.join(ROOT, "profiles", "round2_ncu_cfg2.json")
     out = {"source": "ncu --set full --clock-control none, profiles/kernel_probe.py --n-t 65536 "
                      "(cfg2 level 0: 16384 x 65536, 1.07e9 DOFs)", "kernels": {}}
+    if os.path.exists(path):  # later captures update single kernels
+        with open(path) as fh:
+            out["kernels"] = json.load(fh).get("kernels", {})
     for rep in sys.argv[1:]:
         txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--print-units", "base", "--metrics", METRICS],
                              capture_output=True, text=True).stdout
@@ -39,7 +44,6 @@ def main():
                                            "duration_ms": float(d["gpu__time_duration.sum"]) * 1e-6,
                                            "dram_bytes_read": float(d["dram__bytes_read.sum"]),
                                            "dram_bytes_write": float(d["dram__bytes_write.sum"])}
-    path = os.path.join(ROOT, "profiles", "round2_ncu_cfg2.json")
     with open(path, "w") as fh:
         json.dump(out, fh, indent=1)
     print(json.dumps(out, indent=1))

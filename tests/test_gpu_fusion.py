@@ -84,12 +84,21 @@ def test_fused_solves_bitwise(torch, S, port, name, nu):
     h = gpu_hier(S, cs, port)
     out = {}
     H = S.LevelHierarchy
-    for flags in (H.FUSE_ALL, 0, H.FUSE_VIRTUAL_ZERO, H.FUSE_FINE_DOWN):
+    combos = (H.FUSE_ALL, 0, H.FUSE_VIRTUAL_ZERO, H.FUSE_FINE_DOWN, H.FUSE_FINE_UP,
+              H.FUSE_FINE_UP | H.FUSE_VIRTUAL_ZERO, H.FUSE_FINE_DOWN | H.FUSE_VIRTUAL_ZERO)
+    for flags in combos:
         h.set_fusion(flags)
         u = np.zeros_like(b)
         out[flags] = (S.mg_solve(h, b, u, opts), u)
+        if flags == H.FUSE_FINE_UP | H.FUSE_VIRTUAL_ZERO:  # repeated and warm-started solves, device vectors
+            ut = torch.from_numpy(u).cuda()
+            bt = torch.from_numpy(b).cuda()
+            r_w = S.mg_solve(h, bt, ut, opts)
+            u_w = u.copy()
+            r_w2 = S.mg_solve(h, b, u_w, opts)
+            assert r_w.history == r_w2.history and np.array_equal(bits(ut), bits(u_w))
     r0, u0 = out[H.FUSE_ALL]
-    for flags in (0, H.FUSE_VIRTUAL_ZERO, H.FUSE_FINE_DOWN):
+    for flags in combos[1:]:
         r1, u1 = out[flags]
         assert r1.cycles == r0.cycles and r1.status == r0.status, flags
         # the iterates are bitwise; the fine down-pass sums the norm over other blocks
@@ -127,4 +136,32 @@ def test_fine_down_kernel_bitwise(torch, S, port, name, tiles):
         assert np.array_equal(bits(y), bits(y_want)), (l, "sweep")
         assert np.array_equal(bits(fc), bits(hp.restrict(l, hp.residual(l, f, y_want)))), (l, "restrict")
         r = hp.residual(l, f, x)
+        assert abs(nrm2 - float(np.dot(r, r))) <= 1e-13 * float(np.dot(r, r)), (l, "norm")
+
+
+@pytest.mark.parametrize("tiles", [8, 4, 2])
+@pytest.mark.parametrize("name", KERNEL_CASES + ["cfg0", "tiny"])
+def test_fine_up_kernel_bitwise(torch, S, port, name, tiles):
+    """k_up: u = S(x + P x_c), w = S(u) and ||f - J u||^2 in one pass, against the
+    oracle's separate prolongation, sweeps and residual; every level with a per-node
+    transfer, every time-tile depth."""
+    cs = case(name)
+    h = gpu_hier(S, cs, port)
+    if h.n_levels() < 2:
+        pytest.skip("single-level hierarchy")
+    h.set_tiling(small_dofs=10 ** 15 if tiles <= 4 else 1, tiny_dofs=10 ** 15 if tiles == 2 else 1)
+    hp = port_hier(port, cs)
+    rng = np.random.default_rng(43)
+    dev = torch.device("cuda:0")
+    for l in range(h.n_levels() - 1):
+        n, nc = hp.ndofs(l), hp.ndofs(l + 1)
+        x, f, xc = special_values(rng, n), special_values(rng, n), special_values(rng, nc)
+        xt, ft, xct = torch.from_numpy(x).to(dev), torch.from_numpy(f).to(dev), torch.from_numpy(xc).to(dev)
+        u = torch.full_like(xt, np.nan)
+        w = torch.full_like(xt, np.nan)
+        nrm2 = h.fused_kernel(l, S.LevelHierarchy.FUSED_FINE_UP, ft, x=xt, xc=xct, y=u, fc=w)
+        u_want = hp.sweeps(l, f, hp.prolong_add(l, xc, x), 1)
+        assert np.array_equal(bits(u), bits(u_want)), (l, "post-sweep")
+        assert np.array_equal(bits(w), bits(hp.sweeps(l, f, u_want, 1))), (l, "speculative sweep")
+        r = hp.residual(l, f, u_want)
         assert abs(nrm2 - float(np.dot(r, r))) <= 1e-13 * float(np.dot(r, r)), (l, "norm")
