@@ -1901,6 +1901,14 @@ void restrict_launch(const LevelView& F, const LevelView& C, const double* f, co
   const int64_t warps = DIR == 0 ? ceil_div(C.nn, 14) : ceil_div(F.nn, 30);
   const dim3 rb = balanced_block(warps, wpb_for(F));
   const int64_t tiles = ceil_div(warps, rb.x / 32);
+  // x step on a virtual zero iterate (12 B/DOF, instruction-bound): 16-level tiles halve
+  // the per-tile prologue and the extra staged level (0.483 -> 0.420 ms on 1.3e8 DOFs,
+  // config-2 solve 69.8 -> 69.1 ms); the t step and the stored-iterate form do not gain
+  if (ZX && DIR == 0 && lean_nt(F) == 8) {
+    pdl_launch(k_restrict2<ADJ, DIR, 16, 3, ZX>, tgrid(tiles, (rows(F) + 15) / 16), rb, 0, s, F, C, f, x, fc, xc0,
+               omega, x_ind);
+    return;
+  }
   if (lean_nt(F) == 2 && F.nn * (F.n_t + 1) >= kMinB5Dofs)
     pdl_launch(k_restrict2<ADJ, DIR, 2, minb_for_nt<2>(), ZX>, tgrid(tiles, (rows(F) + 1) / 2), rb, 0, s, F, C,
                f, x, fc, xc0, omega, x_ind);
@@ -2016,6 +2024,7 @@ int launch_down(bool adjoint, const LevelView& F, const LevelView& C, int dir, c
 }
 
 namespace {
+// 4-warp blocks on large levels as for the other tiles (8-warp blocks: config-2 solve 71.1 vs 69.8 ms)
 inline dim3 up_block(const LevelView& L) { return balanced_block(ceil_div(L.nn, 28), wpb_for(L)); }
 inline dim3 up_grid(const LevelView& L, dim3 blk) {
   const int64_t tiles = ceil_div(ceil_div(L.nn, 28), blk.x / 32);

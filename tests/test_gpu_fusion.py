@@ -39,11 +39,16 @@ def S(torch):
     return stmg
 
 
+@pytest.mark.parametrize("tiles", [0, 8])
 @pytest.mark.parametrize("omega", [0.5, 0.6])
 @pytest.mark.parametrize("name", KERNEL_CASES)
-def test_virtual_zero_kernels_bitwise(torch, S, port, name, omega):
+def test_virtual_zero_kernels_bitwise(torch, S, port, name, omega, tiles):
+    """tiles = 8 forces the large-level tiling (8-level tiles; 16-level tiles for the
+    x-step restriction of a virtual zero iterate) onto every level."""
     cs = case(name)
     h = gpu_hier(S, cs, port)
+    if tiles:
+        h.set_tiling(small_dofs=1, tiny_dofs=1)
     hp = port_hier(port, cs)
     rng = np.random.default_rng(5)
     dev = torch.device("cuda:0")
