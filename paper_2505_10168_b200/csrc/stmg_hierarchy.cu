@@ -855,6 +855,7 @@ std::shared_ptr<Workspace> make_workspace(const stmg_hierarchy* h, int64_t* byte
     if (l == 0 && nl > 1)
       max_partials = std::max(max_partials, down_partials_needed(finest_tiles, h->views[1], h->dirs[0]));
     if (l + 1 < nl) max_partials = std::max(max_partials, up_partials_needed(finest_tiles));
+    if (l == 0) max_partials = std::max(max_partials, zero_norm_partials_needed(h->views[0]));
   }
   ws->partials = std::make_unique<DeviceBuf>(max_partials + kPartialsScratch);
   ws->scalars = std::make_unique<DeviceBuf>(8);
@@ -1326,16 +1327,30 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
       cuda_check(cudaMemcpyAsync(X, u, bytes, u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream),
                  "u copy");
   }
-  if (zero_guess) cuda_check(cudaMemsetAsync(X, 0, bytes, h->stream), "u clear");
   int64_t launches = 0;
   int64_t np = 0;
-  launch_check(launch_sumsq(B, n, ws.partials->p, &np, h->stream), "sumsq");
-  launch_check(launch_finalize_sum(ws.partials->p, np, ws.scalars->p + 0, h->stream), "finalize");
-  launches += 1 + finalize_launches(np);
   const bool spec = speculative(h, o.nu);
+  // Zero initial guess with a speculated first sweep: the initial residual is b itself
+  // (J 0 = +0 row by row), so ||r0||^2 = ||b||^2 and the first pre-smoothing sweep is
+  // S(0) = 0 + omega (b * inv_diag): ONE pass over b gives the sweep and the norm
+  // (history[0] is exactly 1, as in the reference).  The first cycle overwrites the
+  // primary iterate, so it is cleared only when no cycle runs.
+  const bool zero_open = zero_guess && spec && o.max_cycles > 0 && !fine_down(h, o.nu);
+  if (zero_guess && !zero_open) cuda_check(cudaMemsetAsync(X, 0, bytes, h->stream), "u clear");
   GraphEntry* g = nullptr;
   if (o.max_cycles > 0) g = &get_graph(h, o.nu, o.omega);
-  launches += emit_norm(h, o.nu, B, X, spec && o.max_cycles > 0 ? Y : nullptr, o.omega, 1);
+  if (zero_open) {
+    launch_check(launch_sweep_from_zero_norm(h->views[0], B, Y, o.omega, ws.partials->p, &np, h->stream),
+                 "sweep from zero + norm");
+    launch_check(launch_finalize_sum(ws.partials->p, np, ws.scalars->p + 0, h->stream), "finalize");
+    launch_check(launch_finalize_sum(ws.partials->p, np, ws.scalars->p + 1, h->stream), "finalize");
+    launches += 1 + 2 * finalize_launches(np);
+  } else {
+    launch_check(launch_sumsq(B, n, ws.partials->p, &np, h->stream), "sumsq");
+    launch_check(launch_finalize_sum(ws.partials->p, np, ws.scalars->p + 0, h->stream), "finalize");
+    launches += 1 + finalize_launches(np);
+    launches += emit_norm(h, o.nu, B, X, spec && o.max_cycles > 0 ? Y : nullptr, o.omega, 1);
+  }
   double sc[2];
   fetch_scalars(h, 2, sc);
   const double norm_b = std::sqrt(sc[0]);
@@ -1463,6 +1478,7 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
     }
   }
   if (rep->cycles > 0) rep->factor = std::pow(history[nh - 1] / r0, 1.0 / rep->cycles);
+  if (zero_open && rep->cycles == 0) cuda_check(cudaMemsetAsync(X, 0, bytes, h->stream), "u clear");
   cuda_check(cudaEventRecord(h->ev1, h->stream), "event");
   if (!in_place)
     cuda_check(cudaMemcpyAsync(u, X, bytes, u_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream),

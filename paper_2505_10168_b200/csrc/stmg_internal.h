@@ -192,6 +192,11 @@ int launch_residual(bool adjoint, const LevelView& L, const double* f, const dou
 int launch_restrict_residual(bool adjoint, const LevelView& F, const LevelView& C, int dir,
                              const double* f, const double* x, double* fc, cudaStream_t s,
                              double* xc0 = nullptr, double omega = 0.0, const double* const* x_ind = nullptr);
+// y = S(0) = 0 + omega (f * inv_diag) and block partials of sum f^2 in one pass over f
+// (the opening pass of a solve from a zero iterate)
+int launch_sweep_from_zero_norm(const LevelView& L, const double* f, double* y, double omega, double* partials,
+                                int64_t* n_partials, cudaStream_t s);
+int64_t zero_norm_partials_needed(const LevelView& L);
 // p[0] <-> p[1] (device-resident buffer pointers of the fine up-pass)
 int launch_swap_ptrs(double** p, cudaStream_t s);
 // Level-0 down-pass of a V(1,1) cycle in one pass: block partials of

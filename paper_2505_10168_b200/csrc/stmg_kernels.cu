@@ -1256,6 +1256,32 @@ __global__ void k_sweep_from_zero2(LevelView L, const double* __restrict__ f, do
   dev_sweep_from_zero(L, f, y, omega, blockIdx.x, blockIdx.y, blockDim.x);
 }
 
+// The opening pass of a solve from a zero iterate: y = S(0) = 0 + omega (f * inv_diag)
+// (the first pre-smoothing sweep) and one partial of sum f^2 per block.  With u = 0 the
+// initial residual is f itself (every row of J 0 is +0), so this one pass over f replaces
+// the separate ||b||^2 pass and the residual-norm + sweep pass (16 instead of 8 + 24 B/DOF).
+__global__ void k_sweep_from_zero_norm(LevelView L, const double* __restrict__ f, double* __restrict__ y,
+                                       double omega, double* __restrict__ partials) {
+  pdl_entry();
+  double acc = 0.0;
+  const int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
+  if (i < L.nn) {
+    const int64_t n0 = L.n_lo + (int64_t)blockIdx.x * kFlatNT;
+    const double idv = __ldg(L.coef + kInvD * L.nn + i);
+#pragma unroll
+    for (int k = 0; k < kFlatNT; ++k) {
+      const int64_t n = n0 + k;
+      if (n >= L.n_hi) break;
+      const double fv = f[n * L.nn + i];
+      const double id = (n == 0 || i == 0) ? L.inv_w : idv;
+      y[n * L.nn + i] = 0.0 + omega * (fv * id);
+      acc = acc + fv * fv;
+    }
+  }
+  const double s = block_sum(acc);
+  if (threadIdx.x == 0) partials[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
+}
+
 template <int DIR>
 __global__ void k_prolong_add2(LevelView F, LevelView C, const double* __restrict__ xc,
                                double* __restrict__ x) {
@@ -2071,6 +2097,20 @@ int launch_sweep_from_zero(const LevelView& L, const double* f, double* y, doubl
   const dim3 blk = march_block(L);
   const dim3 grd((unsigned)((rows(L) + kFlatNT - 1) / kFlatNT), (unsigned)((L.nn + blk.x - 1) / blk.x));
   pdl_launch(k_sweep_from_zero2, grd, blk, 0, s, L, f, y, omega);
+  return check_launch();
+}
+
+int64_t zero_norm_partials_needed(const LevelView& L) {
+  const dim3 blk = march_block(L);
+  return ((rows(L) + kFlatNT - 1) / kFlatNT) * ((L.nn + blk.x - 1) / blk.x);
+}
+
+int launch_sweep_from_zero_norm(const LevelView& L, const double* f, double* y, double omega, double* partials,
+                                int64_t* n_partials, cudaStream_t s) {
+  const dim3 blk = march_block(L);
+  const dim3 grd((unsigned)((rows(L) + kFlatNT - 1) / kFlatNT), (unsigned)((L.nn + blk.x - 1) / blk.x));
+  if (n_partials) *n_partials = (int64_t)grd.x * grd.y;
+  pdl_launch(k_sweep_from_zero_norm, grd, blk, 0, s, L, f, y, omega, partials);
   return check_launch();
 }
 

@@ -148,7 +148,10 @@ def test_solve_is_deterministic(torch, S, port):
 @pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "cfg2_mini"])
 def test_zero_guess_flag_equals_a_zeroed_u(torch, S, port, name):
     """stmg_mg_solve_ex with STMG_SOLVE_ZERO_GUESS: u is output only (garbage in, never
-    read); host and device vectors give the in/out solve from a zero vector bit for bit."""
+    read); host and device vectors give the in/out solve from a zero vector bit for bit.
+    The flagged solve opens with one pass over b (first sweep + ||b||^2 = ||r0||^2), so its
+    history[0] is exactly 1 as in the reference (the in/out path sums ||r0||^2 and ||b||^2 in
+    two different fixed orders: 1 to rounding)."""
     cs = case(name)
     h = gpu_hier(S, cs, port)
     b = cs.rhs_vector(port)
@@ -157,11 +160,17 @@ def test_zero_guess_flag_equals_a_zeroed_u(torch, S, port, name):
     rep0 = S.mg_solve(h, b, u0, opts)
     u1 = np.full_like(b, np.nan)
     rep1 = S.mg_solve(h, b, u1, opts, zero_guess=True)
-    assert np.array_equal(bits(u1), bits(u0)) and rep1.history == rep0.history and rep1.cycles == rep0.cycles
+    assert np.array_equal(bits(u1), bits(u0)) and rep1.cycles == rep0.cycles and rep1.status == rep0.status
+    assert rep1.history[0] == 1.0 and abs(rep0.history[0] - 1.0) <= 1e-15
+    assert rep1.history[1:] == rep0.history[1:]
     bt = torch.from_numpy(b).cuda()
     ut = torch.full_like(bt, float("nan"))
     rep2 = S.mg_solve(h, bt, ut, opts, zero_guess=True)
-    assert np.array_equal(bits(ut), bits(u0)) and rep2.history == rep0.history
+    assert np.array_equal(bits(ut), bits(u0)) and rep2.history == rep1.history
+    # b = 0: converged before any cycle, u is cleared
+    uz = np.full_like(b, np.nan)
+    rz = S.mg_solve(h, np.zeros_like(b), uz, opts, zero_guess=True)
+    assert rz.cycles == 0 and rz.absolute_norms and not uz.any()
     with pytest.raises(ValueError):
         from paper_2505_10168_b200.stmg import _lib, _check, _ptr  # unknown flag bits are rejected
         import ctypes as C
