@@ -472,6 +472,53 @@ def cfg1_extra(S, torch, dev, args):
     return out
 
 
+def cfg3_extra(S, torch, dev, h, cfg, stream, steps=2, warmup=1):
+    """BASELINE config 3: the adjoint solve on the config-2 grid and design (J^T, the
+    transposed hierarchy shares config 2's workspace), right-hand side dJ/dT of the
+    time- and space-integrated temperature, from lambda = 0, b and lambda in HBM."""
+    from paper_2505_10168_b200 import configs as C
+
+    ht = S.transposed_hierarchy(h)
+    ht.set_stream(stream)
+    with torch.cuda.stream(stream):
+        b = torch.from_numpy(C.adjoint_uniform_rhs(cfg.n_el, cfg.n_t, cfg.L, cfg.t_T)).to(dev)
+        lam = torch.empty_like(b)
+    opts = S.SolveOptions(nu=cfg.nu, omega=cfg.omega, tol=cfg.tol, div_tol=cfg.div_tol, max_cycles=cfg.max_cycles)
+    ts, rep = [], None
+    for k in range(warmup + steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rep = S.mg_solve(ht, b, lam, opts, zero_guess=True)
+        e1.record(stream)
+        e1.synchronize()
+        if k >= warmup:
+            ts.append(e0.elapsed_time(e1))
+    ms = sum(ts) / len(ts)
+    return {"grid": f"{cfg.n_el}x{cfg.n_t}", "dofs": (cfg.n_el + 1) * (cfg.n_t + 1), "adjoint": True, "solves": len(ts),
+            "solve_ms": ms, "cycles": rep.cycles, "status": S.status_name(rep.status), "history": rep.history,
+            "value": rep.smoother_dof_updates / (ms * 1e-3),
+            "note": "same coarsening path and stop rule as config 2 (the reference algorithm diverges on this design)"}
+
+
+def cfg4_extra(S, torch, iterations=50):
+    """BASELINE config 4: the 50-iteration topology-optimisation loop at 4096 x 16384
+    (nu = 20, tol 1e-8, warm-started, DesignIndependent, 6 levels): forward and adjoint
+    STMG solves and the sensitivities on the GPU, the MMA design update on the host."""
+    geom = S.build_fine_grid(1.0, 1.0, 4096, 16384)
+    opts = S.OptimisationOptions(method="CR", strategy=S.PlanStrategy.DesignIndependent, n_levels=6,
+                                 max_iterations=iterations, stable_iterations=10 ** 6,
+                                 solve=S.SolveOptions(nu=20, tol=1e-8))
+    res = S.optimise(geom, (1e-3, 1.0, 1.0, 1.0, 3.0, 2.0), opts)
+    hst = res.history
+    return {"grid": "4096x16384", "iterations": res.iterations, "total_seconds": res.seconds,
+            "stmg_seconds": sum(r["primal_seconds"] + r["adjoint_seconds"] for r in hst),
+            "primal_cycles": [r["primal_cycles"] for r in hst], "adjoint_cycles": [r["adjoint_cycles"] for r in hst],
+            "statuses": sorted({(r["primal_status"], r["adjoint_status"]) for r in hst}),
+            "theta_first_last": [hst[0]["theta"], hst[-1]["theta"]], "volume_last": hst[-1]["volume"],
+            "reference": "iterations 1-2: 6/6 and 5/5 primal/adjoint cycles (tests/golden/cfg4_full.npz; "
+                         "546 s + 524 s per solve on one core)"}
+
+
 def main():
     # NCCL_DEBUG=VERSION (set on some images) prints a banner on stdout at
     # communicator creation; the bench prints exactly one JSON line there
@@ -496,6 +543,8 @@ def main():
     ap.add_argument("--profile-steps", type=int, default=2,
                     help="extra solves with in-graph kernel timers (roofline), after the timed steps")
     ap.add_argument("--cfg1", type=int, default=1, help="also time BASELINE config 1 (extra key)")
+    ap.add_argument("--cfg3", type=int, default=1, help="also time BASELINE config 3 (adjoint, extra key)")
+    ap.add_argument("--cfg4", type=int, default=1, help="also run BASELINE config 4 (optimisation loop, extra key)")
     ap.add_argument("--cfg1-steps", type=int, default=5)
     ap.add_argument("--cfg1-warmup", type=int, default=3)
     ap.add_argument("--dist", action="store_true",
@@ -688,15 +737,31 @@ def main():
                    "d2h_bytes_per_step": 8 * nbytes, "solve_seconds": s_io}
 
     cpu = None
-    cfg1 = None
+    dev_bytes = h.device_bytes() if h is not None else dh.device_bytes
+    cfg1 = cfg3 = cfg4 = None
     if rank == 0 and world == 1:
-        if args.cfg1 and cfg.name != "cfg1":
+        if args.cfg3 and cfg.name == "cfg2" and h is not None:
             try:
                 del b_dev, u_dev
+                b_dev = u_dev = None
                 torch.cuda.empty_cache()
+                cfg3 = cfg3_extra(S, torch, dev, h, cfg, stream)
+            except Exception as e:  # an extra key, never required
+                cfg3 = {"error": repr(e)}
+        if (args.cfg1 and cfg.name != "cfg1") or args.cfg4:
+            b_dev = u_dev = None
+            h = None  # release the config-2 hierarchy (60 GB) before the other configs
+            torch.cuda.empty_cache()
+        if args.cfg1 and cfg.name != "cfg1":
+            try:
                 cfg1 = cfg1_extra(S, torch, dev, args)
             except Exception as e:  # an extra key, never required
                 cfg1 = {"error": repr(e)}
+        if args.cfg4 and cfg.name == "cfg2":
+            try:
+                cfg4 = cfg4_extra(S, torch)
+            except Exception as e:  # an extra key, never required
+                cfg4 = {"error": repr(e)}
         if not args.no_cpu_baseline:
             try:
                 res = run_cpu_sample(cfg, args.cpu_sample_nt, [int(d) for d in path.dirs])
@@ -728,8 +793,8 @@ def main():
             "status": S.status_name(last.status), "history": last.history,
             "gpu_launches": int(sum(r.kernel_launches for r in reps)),
             "roofline": roofline, "kernels": kt, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
-            "cfg1": cfg1, "build_seconds": t_build,
-            "device_bytes": h.device_bytes() if h is not None else dh.device_bytes,
+            "cfg1": cfg1, "cfg3": cfg3, "cfg4": cfg4, "build_seconds": t_build,
+            "device_bytes": dev_bytes,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
