@@ -380,11 +380,8 @@ __device__ __forceinline__ double dev_lean2(const LevelView& L, const Ld& ld, co
       const double row = ADJ ? row_interior<true>(c, pm, xr[k], pp, qm, x1, qp)
                              : row_interior<false>(c, qm, x1, qp, pm, xr[k], pp);
       const double r = fv[k] - row;
-      if (computes) {
-        if (NORM) acc = acc + r * r;
-        if (MODE == kSweep) *(yp + (uint32_t)k * nn32) = x0 + omega * (r * c.invd);
-        else if (MODE == kResidual) *(yp + (uint32_t)k * nn32) = r;
-      }
+      if (NORM) acc = acc + (computes ? r * r : 0.0);  // a select: keeps the row out of the store's branch
+      if (MODE != kNormOnly && computes) *(yp + (uint32_t)k * nn32) = MODE == kSweep ? x0 + omega * (r * c.invd) : r;
       pm = qm;
       pp = qp;
     }
@@ -669,7 +666,7 @@ __device__ __forceinline__ double dev_up(const LevelView& L, const Ld& ld, const
       const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
       if (ADJ) y1[r] = xs[r] + omega * ((fv[r] - row_interior<true>(c, pm, xs[r], pp, qm, x1, qp)) * c.invd);
       else y1[r] = x1 + omega * ((fv[r] - row_interior<false>(c, qm, x1, qp, pm, xs[r], pp)) * c.invd);
-      const bool own_row = ADJ ? r < NT : r >= 1;  // rows n0 .. n0 + NT - 1
+      const bool own_row = ADJ ? r < NT : r >= 1;  // rows n0 .. n0 + NT - 1 (compile-time per r)
       if (own_row && lane2) *(ub + (uint32_t)r * nn32) = y1[r];
       pm = qm;
       pp = qp;
@@ -682,10 +679,11 @@ __device__ __forceinline__ double dev_up(const LevelView& L, const Ld& ld, const
       const double res = ADJ ? fv[k] - row_interior<true>(c, am, y1[k], ap, bm, z1, bp)
                              : fv[k + 1] - row_interior<false>(c, bm, z1, bp, am, y1[k], ap);
       const double x0 = ADJ ? y1[k] : z1;
-      if (lane2) {
-        acc = acc + res * res;
-        *(wb + (uint32_t)k * nn32) = x0 + omega * (res * c.invd);
-      }
+      // the squared residual is summed by a select on every lane: the row evaluation then
+      // cannot be sunk into the divergent branch around the store (BSSY / BRA / BSYNC and
+      // a convergence check before the next shuffles, every row: 0.99 -> 0.93 ms)
+      acc = acc + (lane2 ? res * res : 0.0);
+      if (lane2) *(wb + (uint32_t)k * nn32) = x0 + omega * (res * c.invd);
       am = bm;
       ap = bp;
     }
@@ -881,18 +879,16 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
         // canonical ((0 + .5 ra) + (0 + rb)) + ((0 + .5 rc) + 0), folded (see row_interior)
         const double ra = __shfl_up_sync(kFull, r, 1);
         const double rc = __shfl_down_sync(kFull, r, 1);
-        if (out) {
-          const double v = ((0.5 * ra + 1.0 * r) + 0.5 * rc) + 0.0;
-          *(fcb + (uint32_t)k * nnc32) = v;
-          if (xc0 != nullptr) *(xcb + (uint32_t)k * nnc32) = 0.0 + omega * (v * idc);
-        }
+        const double v = ((0.5 * ra + 1.0 * r) + 0.5 * rc) + 0.0;
+        if (out) *(fcb + (uint32_t)k * nnc32) = v;
+        if (xc0 != nullptr && out) *(xcb + (uint32_t)k * nnc32) = 0.0 + omega * (v * idc);
       } else {
         if ((k & 1) == 0) {
           r_even = r;
-        } else if (out) {
+        } else {
           const double v = (0.5 * r_even + 0.5 * r) + 0.0;
-          *(fcb + (uint32_t)(k >> 1) * nnc32) = v;
-          if (xc0 != nullptr) *(xcb + (uint32_t)(k >> 1) * nnc32) = 0.0 + omega * (v * idc);
+          if (out) *(fcb + (uint32_t)(k >> 1) * nnc32) = v;
+          if (xc0 != nullptr && out) *(xcb + (uint32_t)(k >> 1) * nnc32) = 0.0 + omega * (v * idc);
         }
       }
       pm = qm;
