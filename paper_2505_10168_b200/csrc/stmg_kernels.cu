@@ -72,6 +72,24 @@ __device__ __forceinline__ T* opaque(T* p) {
   asm("mov.b64 %0, %0;" : "+l"(p));
   return p;
 }
+// A row stride, optionally hidden from the optimiser's uniformity analysis.  Known
+// uniform, k * stride is computed in 64-bit on the uniform datapath (UIMAD / USHF /
+// ULOP3 per access, then IADD3 + IADD3.X: ~6 instructions per access); as a per-thread
+// value it is one IMAD (shared by the row's accesses) and one IMAD.WIDE per access:
+// 12-19 % fewer instructions in the sweep and restriction tiles.  Measured per kernel
+// family (same box, 1.3e8 DOFs): x-step kernels and the t-step ZX restriction gain
+// 2-6 %, the t-step stored restriction and prolong-sweeps and k_up lose 3-12 %, so those
+// keep the uniform form.  Config-2 solve 65.5 -> 64.2 ms.
+template <bool OPAQUE>
+__device__ __forceinline__ uint32_t stride32(int64_t n) {
+  uint32_t v = (uint32_t)n;
+  if (OPAQUE) asm("mov.b32 %0, %0;" : "+r"(v));
+  return v;
+}
+template <class Ld>
+struct OpaqueStride {
+  static constexpr bool value = true;
+};
 
 __device__ __forceinline__ void st_global(double* p, double v) {
   asm volatile("st.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
@@ -285,7 +303,7 @@ struct ProlongOn {
   __device__ __forceinline__ Raw load(const Lane& l, int r, uint32_t nn32) const {
     Raw w;
     w.b = base.load(l.b, r, nn32);
-    const uint32_t nnc32 = (uint32_t)nnc;
+    const uint32_t nnc32 = stride32<DIR == 0>(nnc);
     if (DIR == 0) {
       const double* p = l.cb + (uint32_t)r * nnc32;
       w.a = __ldg(p);
@@ -303,6 +321,10 @@ struct ProlongOn {
     const double po = (0.5 * w.a + 0.5 * w.c) + 0.0;
     return x + (l.odd ? po : pe);
   }
+};
+template <class Base>
+struct OpaqueStride<ProlongOn<1, Base>> {  // t-step prolong-sweeps: uniform strides measured faster
+  static constexpr bool value = false;
 };
 template <int DIR>
 using ProlongLoad = ProlongOn<DIR, PlainLoad>;
@@ -357,7 +379,7 @@ __device__ __forceinline__ double dev_lean2(const LevelView& L, const Ld& ld, co
     // every lane's node is inside the grid: lanes 0 / 31 load too (unused values).
     // 64-bit row bases once per lane, 32-bit element offsets per row.
     const bool computes = lane >= 1 && lane <= 30;
-    const uint32_t nn32 = (uint32_t)nn;
+    const uint32_t nn32 = stride32<OpaqueStride<Ld>::value>(nn);
     const double* __restrict__ fp = opaque(f + (n0 * nn + i));
 #pragma unroll
     for (int k = 0; k < NT; ++k) fv[k] = __ldg(fp + (uint32_t)k * nn32);
@@ -483,7 +505,7 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
     const double* __restrict__ xb = opaque(x + rowbase);
     const double* __restrict__ fb = opaque(f + rowbase);
     double* __restrict__ yb = opaque(y + rowbase);
-    const uint32_t nn32 = (uint32_t)nn;
+    const uint32_t nn32 = stride32<false>(nn);
     uint32_t o[NT + 2];
     o[0] = (uint32_t)i;
 #pragma unroll
@@ -645,7 +667,7 @@ __device__ __forceinline__ double dev_up(const LevelView& L, const Ld& ld, const
   double xs[NT + 2], fv[NT + 1], y1[NT + 1];
   double acc = 0.0;
   if (rows_in && nodes_in) {
-    const uint32_t nn32 = (uint32_t)nn;
+    const uint32_t nn32 = stride32<false>(nn);
     const double* __restrict__ fb = opaque(f + (s1base * nn + i));
 #pragma unroll
     for (int r = 0; r < NT + 1; ++r) fv[r] = __ldg(fb + (uint32_t)r * nn32);  // f rows s1base + r
@@ -837,7 +859,7 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
   double xr[NT + 1], fv[NT];
   if (rows_in && nodes_in) {
     // 64-bit row bases once per lane, 32-bit element offsets per row
-    const uint32_t nn32 = (uint32_t)nn, nnc32 = (uint32_t)nnc;
+    const uint32_t nn32 = stride32<DIR == 0 || ZX>(nn), nnc32 = stride32<DIR == 0 || ZX>(nnc);
     const double* __restrict__ fp = opaque(f + (n0 * nn + i));
 #pragma unroll
     for (int k = 0; k < NT; ++k) fv[k] = __ldg(fp + (uint32_t)k * nn32);
@@ -1033,7 +1055,7 @@ __device__ __forceinline__ double dev_down(const LevelView& F, const LevelView& 
     const double* __restrict__ xb = opaque(x + rowbase);
     const double* __restrict__ fb = opaque(f + rowbase);
     double* __restrict__ yb = opaque(y + rowbase);
-    const uint32_t nn32 = (uint32_t)nn;
+    const uint32_t nn32 = stride32<false>(nn);
     uint32_t o[NT + 2];
     o[0] = (uint32_t)i;
 #pragma unroll
@@ -1048,7 +1070,7 @@ __device__ __forceinline__ double dev_down(const LevelView& F, const LevelView& 
     const bool out = DIR == 0 ? ((lane & 1) && lane >= 3 && lane <= 27) : owns;
     const int64_t I = DIR == 0 ? (i >> 1) : i;
     const int64_t crow = DIR == 0 ? n0 : (n0 >> 1);
-    const uint32_t nnc32 = (uint32_t)nnc;
+    const uint32_t nnc32 = stride32<false>(nnc);
     double* __restrict__ fcb = opaque(fc + (crow * nnc + I));
     double* __restrict__ xcb = xc0 != nullptr ? opaque(xc0 + (crow * nnc + I)) : nullptr;
     // coarse inverse diagonal at this lane's coarse node (x_c0)
