@@ -775,7 +775,8 @@ __device__ __forceinline__ double dev_up(const LevelView& L, const Ld& ld, const
 
 // Resident 256-thread blocks per SM k_up is compiled for.  8-level tiles: 2 (up to 128
 // registers, no spills) measured faster than 3 (80 registers, ~100 B of spills): probe
-// 0.99 vs 1.05 ms on 1.3e8 DOFs, config-2 solve 69.4 vs 70.7 ms.
+// 0.99 vs 1.05 ms on 1.3e8 DOFs, config-2 solve 69.4 vs 70.7 ms; register caps of 96 /
+// 104 (__maxnreg__) are slower still (1.00 / 1.09 vs 0.94 ms).
 template <int NT>
 constexpr int up_minb() { return NT <= 2 ? 4 : NT <= 4 ? 3 : 2; }
 
