@@ -1949,6 +1949,13 @@ void restrict_launch(const LevelView& F, const LevelView& C, const double* f, co
   // x step on a virtual zero iterate (12 B/DOF, instruction-bound): 16-level tiles halve
   // the per-tile prologue and the extra staged level (0.483 -> 0.420 ms on 1.3e8 DOFs,
   // config-2 solve 69.8 -> 69.1 ms); the t step and the stored-iterate form do not gain
+  // x step on a stored iterate: 16-level tiles with 2 resident blocks (no spills) 0.463 ->
+  // 0.442 ms on 1.3e8 DOFs (with 3 blocks / 80 registers: 0.530)
+  if (!ZX && DIR == 0 && lean_nt(F) == 8) {
+    pdl_launch(k_restrict2<ADJ, DIR, 16, 2, ZX>, tgrid(tiles, (rows(F) + 15) / 16), rb, 0, s, F, C, f, x, fc, xc0,
+               omega, x_ind);
+    return;
+  }
   if (ZX && DIR == 0 && lean_nt(F) == 8) {
     pdl_launch(k_restrict2<ADJ, DIR, 16, 3, ZX>, tgrid(tiles, (rows(F) + 15) / 16), rb, 0, s, F, C, f, x, fc, xc0,
                omega, x_ind);

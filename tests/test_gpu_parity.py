@@ -62,10 +62,15 @@ def special_values(rng, n):
     return v
 
 
+@pytest.mark.parametrize("tiles", [0, 8])
 @pytest.mark.parametrize("name", SMALL_CASES)
-def test_level_kernels_bitwise(torch, S, port, name):
+def test_level_kernels_bitwise(torch, S, port, name, tiles):
+    """tiles = 8 forces the large-level tiling (8-level tiles, 16-level tiles for the
+    x-step restrictions) onto every level of the small cases."""
     cs = case(name)
     h = gpu_hier(S, cs, port)
+    if tiles:
+        h.set_tiling(small_dofs=1, tiny_dofs=1)
     hp = port_hier(port, cs)
     assert h.n_levels() == hp.n_levels
     rng = np.random.default_rng(11)
