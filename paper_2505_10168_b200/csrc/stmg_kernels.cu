@@ -1889,6 +1889,18 @@ inline dim3 pass_grid(const LevelView& L, dim3 blk) {
 }
 inline unsigned flat_grid(int64_t total) { return (unsigned)((total + kFlatBlock - 1) / kFlatBlock); }
 
+// Resident blocks the 8-level single-sweep tiles are compiled for, by loader: 3 (80
+// registers); the x-step virtual-zero prolong-sweep 4 (64 registers: 0.577 -> 0.556 ms on
+// 1.3e8 DOFs; 2 blocks: 0.617).
+template <class Ld>
+struct Minb8 {
+  static constexpr int value = 3;
+};
+template <>
+struct Minb8<ProlongZeroLoad<0>> {
+  static constexpr int value = 4;
+};
+
 template <bool ADJ, int MODE, bool NORM, class Ld>
 void launch_pass(const LevelView& L, const Ld& ld, const double* f, double* y, double omega,
                  double* partials, cudaStream_t s) {
@@ -1900,8 +1912,8 @@ void launch_pass(const LevelView& L, const Ld& ld, const double* f, double* y, d
   else if (lean_nt(L) == 4)
     pdl_launch(k_lean2<ADJ, MODE, NORM, 4, 4, Ld>, grd, blk, 0, s, L, ld, f, y, omega, partials);
   else
-    pdl_launch(k_lean2<ADJ, MODE, NORM, 8, NORM ? STMG_NORM_MINB8 : 3, Ld>, grd, blk, 0, s, L, ld, f, y, omega,
-               partials);
+    pdl_launch(k_lean2<ADJ, MODE, NORM, 8, NORM ? STMG_NORM_MINB8 : Minb8<Ld>::value, Ld>, grd, blk, 0, s, L, ld, f, y,
+               omega, partials);
 }
 
 inline ZeroLoad zero_load(const LevelView& L, const double* f, double omega) {
