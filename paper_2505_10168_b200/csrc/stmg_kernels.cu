@@ -2104,7 +2104,7 @@ void up_launch(const LevelView& L, const LevelView& C, const double* f, const do
     pdl_launch(k_up<ADJ, 2, ProlongLoad<DIR>>, grd, blk, 0, s, L, ld, f, u_out, w_ind, x_ind, omega, partials);
   else if (lean_nt(L) == 4)
     pdl_launch(k_up<ADJ, 4, ProlongLoad<DIR>>, grd, blk, 0, s, L, ld, f, u_out, w_ind, x_ind, omega, partials);
-  else
+  else  // 8-level tiles: 6 / 10 levels measured slower (1.05 / 0.99 vs 0.94 ms on 1.3e8 DOFs)
     pdl_launch(k_up<ADJ, 8, ProlongLoad<DIR>>, grd, blk, 0, s, L, ld, f, u_out, w_ind, x_ind, omega, partials);
 }
 }  // namespace
