@@ -685,6 +685,14 @@ def main():
                                 "pass (24 B/DOF, 0.83): it moves 36 B/DOF instead of 52, is instruction-bound (ncu: "
                                 "54 % issue slots, 124 registers) and runs at the 1 kW power cap inside the solve; the "
                                 "timed span includes the fixed-order sum of its norm partials")
+        # all level-0 kernels together: algorithmic bytes of one cycle's level-0 passes over their time
+        l0 = [v for v in kt.values() if isinstance(v, dict)]
+        l0_bytes = sum(v["bytes_per_dof"] * n0 * v["launches"] for v in l0)
+        l0_secs = sum(v["total_ms"] for v in l0) * 1e-3
+        if l0_secs > 0:
+            roofline["level0"] = {"bytes_per_dof_per_cycle": sum(v["bytes_per_dof"] for v in l0),
+                                  "achieved": l0_bytes / l0_secs / 1e9, "frac": l0_bytes / l0_secs / 1e9 / hbm,
+                                  "kernels": sorted(k_ for k_, v in kt.items() if isinstance(v, dict))}
         kt["profiled_steps"] = len(prof_ms)
         kt["profiled_ms_per_step"] = sum(prof_ms) / len(prof_ms)
         kt["level0_share_of_step"] = sum(v["total_ms"] for v in kt.values() if isinstance(v, dict)) / max(
