@@ -400,10 +400,12 @@ struct GraphKey {
   int profiling;
   // level-0 vectors the graph reads and writes (the caller's b and u when they
   // are bound in place, else the workspace's)
-  const void* b;
-  const void* x;
+  const void* b = nullptr;
+  const void* x = nullptr;
+  // cycle 1 of a zero-guess solve whose level-0 restriction ran with the opening pass
+  int first = 0;
   bool operator<(const GraphKey& o) const {
-    return std::tie(nu, omega, profiling, b, x) < std::tie(o.nu, o.omega, o.profiling, o.b, o.x);
+    return std::tie(nu, omega, profiling, b, x, first) < std::tie(o.nu, o.omega, o.profiling, o.b, o.x, o.first);
   }
 };
 // Graphs kept per hierarchy; a solve with new bound pointers beyond this many
@@ -856,6 +858,8 @@ std::shared_ptr<Workspace> make_workspace(const stmg_hierarchy* h, int64_t* byte
       max_partials = std::max(max_partials, down_partials_needed(finest_tiles, h->views[1], h->dirs[0]));
     if (l + 1 < nl) max_partials = std::max(max_partials, up_partials_needed(finest_tiles));
     if (l == 0) max_partials = std::max(max_partials, zero_norm_partials_needed(h->views[0]));
+    if (l == 0 && nl > 1 && !h->galerkin(0) && !h->gen_xfer(0))
+      max_partials = std::max(max_partials, restrict_open_partials_needed(finest_tiles, h->views[1], h->dirs[0]));
   }
   ws->partials = std::make_unique<DeviceBuf>(max_partials + kPartialsScratch);
   ws->scalars = std::make_unique<DeviceBuf>(8);
@@ -1158,8 +1162,10 @@ void launch_up_pass(stmg_hierarchy* h, const double* xc, double omega, cudaStrea
                "prolong + sweep + norm + sweep");
 }
 
-GraphEntry& get_graph(stmg_hierarchy* h, int nu, double omega) {
-  const GraphKey key{nu, omega, h->profiling, h->f_ptr(0), h->xa_ptr(0)};  // profiling: int mode, 0 = off
+// first: the graph of cycle 1 after the opening restriction (launch_restrict_open): level 0's
+// restriction is already done, the cycle starts at level 1.
+GraphEntry& get_graph(stmg_hierarchy* h, int nu, double omega, bool first = false) {
+  const GraphKey key{nu, omega, h->profiling, h->f_ptr(0), h->xa_ptr(0), first ? 1 : 0};  // profiling: int mode
   auto it = h->graphs.find(key);
   if (it != h->graphs.end()) return it->second;
   if (h->graphs.size() >= kMaxGraphs) {
@@ -1169,7 +1175,7 @@ GraphEntry& get_graph(stmg_hierarchy* h, int nu, double omega) {
   Nvtx range("stmg::capture_v_cycle");
   GraphEntry e;
   Emitter em{h, nu, omega, h->cap_stream};
-  em.down_done = fine_down(h, nu);
+  em.down_done = first || fine_down(h, nu);
   em.up_fused = fine_up(h, nu);
   if (h->profiling) {
     em.timed = &e.timed;
@@ -1335,11 +1341,26 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
   // S(0) = 0 + omega (b * inv_diag): ONE pass over b gives the sweep and the norm
   // (history[0] is exactly 1, as in the reference).  The first cycle overwrites the
   // primary iterate, so it is cleared only when no cycle runs.
-  const bool zero_open = zero_guess && spec && o.max_cycles > 0 && !fine_down(h, o.nu);
+  // nu = 1 with fused level-0 transfers: cycle 1's level-0 restriction reads exactly S(0),
+  // so it runs inside the opening pass too (launch_restrict_open: 20 B/DOF for the sweep,
+  // the norm and level 1's right-hand side), and cycle 1 uses the graph that starts at level 1.
+  const bool open_r = zero_guess && spec && o.max_cycles > 0 && o.nu == 1 && h->n_levels() >= 2 &&
+                      !h->galerkin(0) && !h->gen_xfer(0);
+  const bool zero_open = zero_guess && spec && o.max_cycles > 0 && (open_r || !fine_down(h, o.nu));
   if (zero_guess && !zero_open) cuda_check(cudaMemsetAsync(X, 0, bytes, h->stream), "u clear");
   GraphEntry* g = nullptr;
+  GraphEntry* g1 = nullptr;  // cycle 1 after the opening restriction
   if (o.max_cycles > 0) g = &get_graph(h, o.nu, o.omega);
-  if (zero_open) {
+  if (open_r) g1 = &get_graph(h, o.nu, o.omega, true);
+  if (open_r) {
+    const ZeroMode zm = child_zero_mode(h, 0, o.nu);
+    launch_check(launch_restrict_open(h->adjoint, h->views[0], h->views[1], h->dirs[0], B, ws.f[1]->p,
+                                      zm.store ? ws.xa[1]->p : nullptr, Y, o.omega, ws.partials->p, &np, h->stream),
+                 "sweep from zero + norm + restriction");
+    launch_check(launch_finalize_sum(ws.partials->p, np, ws.scalars->p + 0, h->stream), "finalize");
+    launch_check(launch_finalize_sum(ws.partials->p, np, ws.scalars->p + 1, h->stream), "finalize");
+    launches += 1 + 2 * finalize_launches(np);
+  } else if (zero_open) {
     launch_check(launch_sweep_from_zero_norm(h->views[0], B, Y, o.omega, ws.partials->p, &np, h->stream),
                  "sweep from zero + norm");
     launch_check(launch_finalize_sum(ws.partials->p, np, ws.scalars->p + 0, h->stream), "finalize");
@@ -1383,98 +1404,113 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
     cuda_check(cudaMemcpyAsync(ws.ptrs->p, ws.pinned + 4, sizeof(tab), cudaMemcpyHostToDevice, h->stream), "ptrs");
   }
   cudaGraphExec_t loop = nullptr;
-  if (r0 >= o.tol && o.max_cycles > 0 && o.max_cycles <= kLoopHistory && !h->profiling)
+  if (r0 >= o.tol && o.max_cycles > (open_r ? 1 : 0) && o.max_cycles <= kLoopHistory && !h->profiling)
     loop = get_loop(h, o.nu, o.omega);
+  // One cycle launched from the host: the V-cycle graph gg, the pass that closes the
+  // cycle, a read-back of the norm and the reference's bookkeeping.  Returns true when
+  // the solve stops after it.
+  auto host_cycle = [&](GraphEntry* gg, int cycle) -> bool {
+    Nvtx cyc("stmg::v_cycle");
+    cuda_check(cudaGraphLaunch(gg->exec, h->stream), "graph launch");
+    launches += gg->kernels;
+    if (gg->final_buf != 0) throw std::logic_error("level-0 iterate left the primary buffer");
+    const bool more = cycle < o.max_cycles;
+    if (h->profiling) cuda_check(cudaEventRecord(h->norm_ev0, h->stream), "event");
+    if (up) {
+      int64_t npu = 0;
+      launch_up_pass(h, gg->up_xc, o.omega, h->stream, &npu);
+      launch_check(launch_finalize_sum(ws.partials->p, npu, ws.scalars->p + 1, h->stream), "finalize");
+      launches += 1 + finalize_launches(npu);
+    } else {
+      launches += emit_norm(h, o.nu, B, X, spec && more ? Y : nullptr, o.omega, 1);
+    }
+    if (h->profiling) cuda_check(cudaEventRecord(h->norm_ev1, h->stream), "event");
+    if (up) {
+      launch_check(launch_swap_ptrs(up_ptrs(h), h->stream), "swap");
+      launches += 1;
+    }
+    fetch_scalars(h, 2, sc);
+    if (h->profiling) {  // the pass closing the cycle (incl. its finalize launch)
+      float ms = 0.f;
+      cuda_check(cudaEventElapsedTime(&ms, h->norm_ev0, h->norm_ev1), "event elapsed");
+      if (up) {
+        rep->fine_ups += 1;
+        rep->fine_up_seconds += ms * 1e-3;
+      } else {
+        rep->fine_norm_passes += 1;
+        rep->fine_norm_pass_seconds += ms * 1e-3;
+      }
+    }
+    for (const TimedKernel& t : gg->timed) {
+      float ms = 0.f;
+      cuda_check(cudaEventElapsedTime(&ms, t.start, t.stop), "event elapsed");
+      if (h->prof.size() < h->host.size()) h->prof.resize(h->host.size());
+      h->prof[t.level][t.kind].first += 1;
+      h->prof[t.level][t.kind].second += ms * 1e-3;
+      if (t.level != 0) continue;
+      if (t.kind == kTimedSweep) {
+        rep->fine_sweeps += 1;
+        rep->fine_sweep_seconds += ms * 1e-3;
+      } else if (t.kind == kTimedSweep2) {
+        rep->fine_sweep_pairs += 1;
+        rep->fine_sweep_pair_seconds += ms * 1e-3;
+      } else if (t.kind == kTimedRestrict) {
+        rep->fine_restricts += 1;
+        rep->fine_restrict_seconds += ms * 1e-3;
+      } else if (t.kind == kTimedProlongSweep) {
+        rep->fine_prolong_sweeps += 1;
+        rep->fine_prolong_sweep_seconds += ms * 1e-3;
+      }
+    }
+    const double rn = std::sqrt(sc[1]) / denom;
+    history[nh++] = rn;
+    rep->cycles = cycle;
+    rep->smoother_dof_updates += per_cycle_updates;
+    if (rn < o.tol) {
+      rep->status = STMG_CONVERGED;
+      return true;
+    }
+    if (!std::isfinite(rn) || rn > o.div_tol) {
+      rep->status = STMG_DIVERGED;
+      return true;
+    }
+    return false;
+  };
   if (r0 < o.tol) {
     rep->status = STMG_CONVERGED;
-  } else if (loop) {
-    // the whole cycle loop on the device: one launch, one read-back
-    auto* ctl = reinterpret_cast<SolveLoopCtl*>(ws.loop_host);
-    *ctl = SolveLoopCtl{o.tol, o.div_tol, o.max_cycles, 0, STMG_MAX_CYCLES, 0};
-    cuda_check(cudaMemcpyAsync(ws.loop->p, ws.loop_host, sizeof(SolveLoopCtl), cudaMemcpyHostToDevice, h->stream),
-               "loop ctl");
-    cuda_check(cudaGraphLaunch(loop, h->stream), "loop graph launch");
-    cuda_check(cudaMemcpyAsync(ws.loop_host, ws.loop->p, sizeof(double) * (kLoopCtlDoubles + o.max_cycles + 1),
-                               cudaMemcpyDeviceToHost, h->stream),
-               "loop read-back");
-    cuda_check(cudaStreamSynchronize(h->stream), "stream sync");
-    const double* dh = ws.loop_host + kLoopCtlDoubles;
-    for (int c = 1; c <= ctl->cycles; ++c) history[nh++] = dh[c];
-    rep->cycles = ctl->cycles;
-    rep->status = ctl->status;
-    rep->smoother_dof_updates = per_cycle_updates * ctl->cycles;
-    // per cycle: the V-cycle graph, the norm pass and its fixed-order sum
-    const int64_t norm_np = up ? up_partials_needed(h->views[0])
-                               : fine_down(h, o.nu) ? down_partials_needed(h->views[0], h->views[1], h->dirs[0])
-                                                    : sweep_partials_needed(h->views[0]);
-    launches += static_cast<int64_t>(ctl->cycles) * (g->kernels + 1 + finalize_launches(norm_np) + (up ? 1 : 0));
   } else {
     rep->status = STMG_MAX_CYCLES;
-    for (int cycle = 1; cycle <= o.max_cycles; ++cycle) {
-      Nvtx cyc("stmg::v_cycle");
-      cuda_check(cudaGraphLaunch(g->exec, h->stream), "graph launch");
-      launches += g->kernels;
-      if (g->final_buf != 0) throw std::logic_error("level-0 iterate left the primary buffer");
-      const bool more = cycle < o.max_cycles;
-      if (h->profiling) cuda_check(cudaEventRecord(h->norm_ev0, h->stream), "event");
-      if (up) {
-        int64_t np = 0;
-        launch_up_pass(h, g->up_xc, o.omega, h->stream, &np);
-        launch_check(launch_finalize_sum(ws.partials->p, np, ws.scalars->p + 1, h->stream), "finalize");
-        launches += 1 + finalize_launches(np);
-      } else {
-        launches += emit_norm(h, o.nu, B, X, spec && more ? Y : nullptr, o.omega, 1);
-      }
-      if (h->profiling) cuda_check(cudaEventRecord(h->norm_ev1, h->stream), "event");
-      if (up) {
-        launch_check(launch_swap_ptrs(up_ptrs(h), h->stream), "swap");
-        launches += 1;
-      }
-      fetch_scalars(h, 2, sc);
-      if (h->profiling) {  // the pass closing the cycle (incl. its finalize launch)
-        float ms = 0.f;
-        cuda_check(cudaEventElapsedTime(&ms, h->norm_ev0, h->norm_ev1), "event elapsed");
-        if (up) {
-          rep->fine_ups += 1;
-          rep->fine_up_seconds += ms * 1e-3;
-        } else {
-          rep->fine_norm_passes += 1;
-          rep->fine_norm_pass_seconds += ms * 1e-3;
-        }
-      }
-      for (const TimedKernel& t : g->timed) {
-        float ms = 0.f;
-        cuda_check(cudaEventElapsedTime(&ms, t.start, t.stop), "event elapsed");
-        if (h->prof.size() < h->host.size()) h->prof.resize(h->host.size());
-        h->prof[t.level][t.kind].first += 1;
-        h->prof[t.level][t.kind].second += ms * 1e-3;
-        if (t.level != 0) continue;
-        if (t.kind == kTimedSweep) {
-          rep->fine_sweeps += 1;
-          rep->fine_sweep_seconds += ms * 1e-3;
-        } else if (t.kind == kTimedSweep2) {
-          rep->fine_sweep_pairs += 1;
-          rep->fine_sweep_pair_seconds += ms * 1e-3;
-        } else if (t.kind == kTimedRestrict) {
-          rep->fine_restricts += 1;
-          rep->fine_restrict_seconds += ms * 1e-3;
-        } else if (t.kind == kTimedProlongSweep) {
-          rep->fine_prolong_sweeps += 1;
-          rep->fine_prolong_sweep_seconds += ms * 1e-3;
-        }
-      }
-      const double rn = std::sqrt(sc[1]) / denom;
-      history[nh++] = rn;
-      rep->cycles = cycle;
-      rep->smoother_dof_updates += per_cycle_updates;
-      if (rn < o.tol) {
-        rep->status = STMG_CONVERGED;
-        break;
-      }
-      if (!std::isfinite(rn) || rn > o.div_tol) {
-        rep->status = STMG_DIVERGED;
-        break;
-      }
+    int done = 0;  // cycles run so far
+    bool stop = false;
+    if (open_r) {  // cycle 1: its level-0 restriction ran with the opening pass
+      stop = host_cycle(g1, 1);
+      done = 1;
+    }
+    if (!stop && done < o.max_cycles && loop) {
+      // the remaining cycle loop on the device: one launch, one read-back
+      auto* ctl = reinterpret_cast<SolveLoopCtl*>(ws.loop_host);
+      *ctl = SolveLoopCtl{o.tol, o.div_tol, o.max_cycles, done, STMG_MAX_CYCLES, 0};
+      cuda_check(cudaMemcpyAsync(ws.loop->p, ws.loop_host, sizeof(SolveLoopCtl), cudaMemcpyHostToDevice, h->stream),
+                 "loop ctl");
+      cuda_check(cudaGraphLaunch(loop, h->stream), "loop graph launch");
+      cuda_check(cudaMemcpyAsync(ws.loop_host, ws.loop->p, sizeof(double) * (kLoopCtlDoubles + o.max_cycles + 1),
+                                 cudaMemcpyDeviceToHost, h->stream),
+                 "loop read-back");
+      cuda_check(cudaStreamSynchronize(h->stream), "stream sync");
+      const double* dh = ws.loop_host + kLoopCtlDoubles;
+      for (int c = done + 1; c <= ctl->cycles; ++c) history[nh++] = dh[c];
+      const int ran = ctl->cycles - done;
+      rep->cycles = ctl->cycles;
+      rep->status = ctl->status;
+      rep->smoother_dof_updates += per_cycle_updates * ran;
+      // per cycle: the V-cycle graph, the pass closing the cycle and its fixed-order sum
+      const int64_t norm_np = up ? up_partials_needed(h->views[0])
+                                 : fine_down(h, o.nu) ? down_partials_needed(h->views[0], h->views[1], h->dirs[0])
+                                                      : sweep_partials_needed(h->views[0]);
+      launches += static_cast<int64_t>(ran) * (g->kernels + 1 + finalize_launches(norm_np) + (up ? 1 : 0));
+    } else if (!stop) {
+      for (int cycle = done + 1; cycle <= o.max_cycles; ++cycle)
+        if (host_cycle(g, cycle)) break;
     }
   }
   if (rep->cycles > 0) rep->factor = std::pow(history[nh - 1] / r0, 1.0 / rep->cycles);

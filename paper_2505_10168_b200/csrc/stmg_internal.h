@@ -197,6 +197,13 @@ int launch_restrict_residual(bool adjoint, const LevelView& F, const LevelView& 
 int launch_sweep_from_zero_norm(const LevelView& L, const double* f, double* y, double omega, double* partials,
                                 int64_t* n_partials, cudaStream_t s);
 int64_t zero_norm_partials_needed(const LevelView& L);
+// Opening pass of a zero-guess solve fused with cycle 1's level-0 restriction: y = S(0),
+// f_c = R (f - A S(0)) (x_c0: the stored coarse first sweep, or null), per-warp partials
+// of sum f^2 (20 B/DOF instead of 16 + 20).
+int launch_restrict_open(bool adjoint, const LevelView& F, const LevelView& C, int dir, const double* f, double* fc,
+                         double* xc0, double* y, double omega, double* partials, int64_t* n_partials,
+                         cudaStream_t s);
+int64_t restrict_open_partials_needed(const LevelView& F, const LevelView& C, int dir);
 // p[0] <-> p[1] (device-resident buffer pointers of the fine up-pass)
 int launch_swap_ptrs(double** p, cudaStream_t s);
 // Level-0 down-pass of a V(1,1) cycle in one pass: block partials of

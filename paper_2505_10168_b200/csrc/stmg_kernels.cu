@@ -840,17 +840,26 @@ __device__ __forceinline__ double coarse_from_zero(const LevelView& C, int64_t N
 }
 
 // ZX: x is S(0) = 0 + omega (f * inv_diag), recomputed from f (x is not read).
-template <bool ADJ, int DIR, int NT, bool ZX = false>
-__device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelView& C,
-                                              const double* __restrict__ f, const double* __restrict__ x,
-                                              double* __restrict__ fc, int64_t tile, int64_t ttile, int tw,
-                                              double* __restrict__ xc0 = nullptr, double omega = 0.0) {
-  if ((int)threadIdx.x >= tw) return;
+// OPEN (with ZX): the opening pass of a solve from a zero iterate rides along: the
+// owned entries of S(0) are stored to y_open and the thread's sum of f^2 over its owned
+// entries is returned (||b||^2 = ||r0||^2), so one pass over f gives the first sweep,
+// the norm and level 1's right-hand side.
+template <bool ADJ, int DIR, int NT, bool ZX = false, bool OPEN = false>
+__device__ __forceinline__ double dev_restrict2(const LevelView& F, const LevelView& C,
+                                                const double* __restrict__ f, const double* __restrict__ x,
+                                                double* __restrict__ fc, int64_t tile, int64_t ttile, int tw,
+                                                double* __restrict__ xc0 = nullptr, double omega = 0.0,
+                                                double* __restrict__ y_open = nullptr) {
+  static_assert(!OPEN || ZX, "the opening pass restricts the virtual zero iterate");
+  if ((int)threadIdx.x >= tw) return 0.0;
   constexpr int kAdv = DIR == 0 ? 28 : 30;  // nodes per warp
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t nn = F.nn, nt = F.n_t, nnc = C.nn;
   const int64_t base = tile * ((tw >> 5) * kAdv) + warp * kAdv + (DIR == 0 ? -2 : 0);
-  if (DIR == 0 ? (base / 2 + 1 >= nnc) : (base >= nn)) return;  // whole warp past the grid
+  if (DIR == 0 ? (base / 2 + 1 >= nnc) : (base >= nn)) return 0.0;  // whole warp past the grid
+  // fine nodes this warp owns (OPEN): x step 28 w .. 28 w + 27 = lanes 3..30; t step lanes 1..30
+  const bool owns = DIR == 0 ? (lane >= 3 && lane <= 30) : (lane >= 1 && lane <= 30);
+  double acc = 0.0;
   const int64_t i = base - 1 + lane;
   const int64_t n0 = F.n_lo + ttile * NT;
   const int64_t nbase = ADJ ? n0 : n0 - 1;
@@ -878,6 +887,14 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
       for (int r = 0; r <= NT; ++r) {
         const double fr = ADJ ? (r < NT ? fv[r] : fx) : (r == 0 ? fx : fv[r - 1]);
         xr[r] = zero_sweep(fr, c.invd, omega);
+      }
+    }
+    if (OPEN) {
+      double* __restrict__ yb = opaque(y_open + (n0 * nn + i));
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        acc = acc + (owns ? fv[k] * fv[k] : 0.0);
+        if (owns) *(yb + (uint32_t)k * nn32) = xr[ADJ ? k : k + 1];  // S(0) on row n0 + k
       }
     }
     // Output lanes and their coarse node: x step, the lanes at even fine nodes
@@ -917,7 +934,7 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
       pm = qm;
       pp = qp;
     }
-    return;
+    return acc;
   }
   const bool in_grid = i >= 0 && i < nn;
   const bool computes = lane >= 1 && lane <= 30 && in_grid;
@@ -952,6 +969,10 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
     if (n >= F.n_hi) break;
     const double x1 = xr[k + 1];
     const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
+    if (OPEN && owns && in_grid) {
+      acc = acc + fv[k] * fv[k];
+      y_open[n * nn + i] = xr[ADJ ? k : k + 1];  // S(0) on row n
+    }
     double r = 0.0;
     if (computes)
       r = fv[k] - (ADJ ? row_sum<true>(F, n, i, c, pm, xr[k], pp, qm, x1, qp)
@@ -993,6 +1014,7 @@ __device__ __forceinline__ void dev_restrict2(const LevelView& F, const LevelVie
     pm = qm;
     pp = qp;
   }
+  return acc;
 }
 
 // omega: the coarse first sweep's (xc0) and, with ZX, the fine iterate's S(0).
@@ -1008,6 +1030,24 @@ __global__ void __launch_bounds__(kMaxTW, MINB) k_restrict2(LevelView F, LevelVi
   const int64_t tt = (int64_t)blockIdx.z * gridDim.y + blockIdx.y;
   if (tt < ceil_div(F.n_hi - F.n_lo, NT))
     dev_restrict2<ADJ, DIR, NT, ZX>(F, C, f, x, fc, blockIdx.x, tt, blockDim.x, xc0, omega);
+}
+
+// The opening pass of a solve from a zero iterate fused with cycle 1's level-0
+// restriction: y = S(0) = 0 + omega (f * inv_diag), f_c = R (f - A S(0)), and one partial
+// per warp of sum f^2 (= ||b||^2 = ||r0||^2): 20 B/DOF instead of 16 (opening pass) + 20.
+template <bool ADJ, int DIR, int NT, int MINB>
+__global__ void __launch_bounds__(kMaxTW, MINB) k_restrict_open(LevelView F, LevelView C, const double* __restrict__ f,
+                                                             double* __restrict__ fc, double* __restrict__ xc0,
+                                                             double* __restrict__ y, double omega,
+                                                             double* __restrict__ partials) {
+  pdl_entry();
+  const int64_t tt = (int64_t)blockIdx.z * gridDim.y + blockIdx.y;
+  double acc = 0.0;
+  if (tt < ceil_div(F.n_hi - F.n_lo, NT))
+    acc = dev_restrict2<ADJ, DIR, NT, true, true>(F, C, f, nullptr, fc, blockIdx.x, tt, blockDim.x, xc0, omega, y);
+  for (int o = 16; o > 0; o >>= 1) acc = acc + __shfl_xor_sync(kFull, acc, o);
+  if ((threadIdx.x & 31) == 0)
+    partials[(tt * gridDim.x + blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)] = acc;
 }
 
 // Fine down-pass of a V(1,1) cycle in one pass over memory (level 0, nu = 1):
@@ -1987,6 +2027,32 @@ void restrict_launch(const LevelView& F, const LevelView& C, const double* f, co
                f, x, fc, xc0, omega, x_ind);
 }
 
+// grid of the opening restriction: the ZX restriction's, with 16-level tiles on large x-step levels
+template <int DIR>
+inline void restrict_open_geometry(const LevelView& F, const LevelView& C, dim3* blk, dim3* grd, int* nt) {
+  const int64_t warps = DIR == 0 ? ceil_div(C.nn, 14) : ceil_div(F.nn, 30);
+  *blk = balanced_block(warps, wpb_for(F));
+  const int64_t tiles = ceil_div(warps, blk->x / 32);
+  *nt = (DIR == 0 && lean_nt(F) == 8) ? 16 : lean_nt(F);
+  *grd = tgrid(tiles, ceil_div(rows(F), *nt));
+}
+template <bool ADJ, int DIR>
+void restrict_open_launch(const LevelView& F, const LevelView& C, const double* f, double* fc, double* xc0, double* y,
+                          double omega, double* partials, cudaStream_t s) {
+  dim3 blk, grd;
+  int nt = 0;
+  restrict_open_geometry<DIR>(F, C, &blk, &grd, &nt);
+  if (nt == 16) {
+    if (DIR == 0) pdl_launch(k_restrict_open<ADJ, 0, 16, 3>, grd, blk, 0, s, F, C, f, fc, xc0, y, omega, partials);
+  } else if (nt == 8) {
+    pdl_launch(k_restrict_open<ADJ, DIR, 8, 3>, grd, blk, 0, s, F, C, f, fc, xc0, y, omega, partials);
+  } else if (nt == 4) {
+    pdl_launch(k_restrict_open<ADJ, DIR, 4, 4>, grd, blk, 0, s, F, C, f, fc, xc0, y, omega, partials);
+  } else {
+    pdl_launch(k_restrict_open<ADJ, DIR, 2, 3>, grd, blk, 0, s, F, C, f, fc, xc0, y, omega, partials);
+  }
+}
+
 template <bool ADJ, int DIR>
 int restrict_impl(const LevelView& F, const LevelView& C, const double* f, const double* x,
                   double* fc, cudaStream_t s, double* xc0, double omega, const double* const* x_ind) {
@@ -2180,6 +2246,32 @@ int launch_restrict_residual(bool adjoint, const LevelView& F, const LevelView& 
                     : restrict_impl<true, 1>(F, C, f, x, fc, s, xc0, omega, x_ind);
   return dir == 0 ? restrict_impl<false, 0>(F, C, f, x, fc, s, xc0, omega, x_ind)
                   : restrict_impl<false, 1>(F, C, f, x, fc, s, xc0, omega, x_ind);
+}
+
+int64_t restrict_open_partials_needed(const LevelView& F, const LevelView& C, int dir) {
+  dim3 blk, grd;
+  int nt = 0;
+  if (dir == 0) restrict_open_geometry<0>(F, C, &blk, &grd, &nt);
+  else restrict_open_geometry<1>(F, C, &blk, &grd, &nt);
+  return (int64_t)grd.x * grd.y * grd.z * (blk.x / 32);
+}
+
+// Opening pass of a zero-guess solve fused with cycle 1's level-0 restriction
+// (k_restrict_open): y = S(0), f_c = R (f - A S(0)) (and the stored coarse first sweep
+// x_c0 when not null), one partial per warp of sum f^2.
+int launch_restrict_open(bool adjoint, const LevelView& F, const LevelView& C, int dir, const double* f, double* fc,
+                         double* xc0, double* y, double omega, double* partials, int64_t* n_partials,
+                         cudaStream_t s) {
+  if (dir == 1 && (F.tile_nt % 2 != 0 || (F.n_lo & 1) != 0)) return static_cast<int>(cudaErrorInvalidValue);
+  if (n_partials) *n_partials = restrict_open_partials_needed(F, C, dir);
+  if (adjoint) {
+    if (dir == 0) restrict_open_launch<true, 0>(F, C, f, fc, xc0, y, omega, partials, s);
+    else restrict_open_launch<true, 1>(F, C, f, fc, xc0, y, omega, partials, s);
+  } else {
+    if (dir == 0) restrict_open_launch<false, 0>(F, C, f, fc, xc0, y, omega, partials, s);
+    else restrict_open_launch<false, 1>(F, C, f, fc, xc0, y, omega, partials, s);
+  }
+  return check_launch();
 }
 
 namespace {

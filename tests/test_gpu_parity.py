@@ -150,8 +150,10 @@ def test_solve_is_deterministic(torch, S, port):
     assert outs[0][1] == outs[1][1]
 
 
-@pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "cfg2_mini"])
-def test_zero_guess_flag_equals_a_zeroed_u(torch, S, port, name):
+@pytest.mark.parametrize("nu", [0, 1, 2])
+@pytest.mark.parametrize("name", ["cfg0", "cfg1_mini", "cfg1_mini_adj", "cfg2_mini", "cfg3_mini", "time_first",
+                                  "cfgD", "tiny", "single_level"])
+def test_zero_guess_flag_equals_a_zeroed_u(torch, S, port, name, nu):
     """stmg_mg_solve_ex with STMG_SOLVE_ZERO_GUESS: u is output only (garbage in, never
     read); host and device vectors give the in/out solve from a zero vector bit for bit.
     The flagged solve opens with one pass over b (first sweep + ||b||^2 = ||r0||^2), so its
@@ -160,14 +162,28 @@ def test_zero_guess_flag_equals_a_zeroed_u(torch, S, port, name):
     cs = case(name)
     h = gpu_hier(S, cs, port)
     b = cs.rhs_vector(port)
-    opts = S.SolveOptions(nu=cs.nu, tol=cs.tol, max_cycles=cs.max_cycles)
+    # nu = 0: the case's own smoothing count; 1: the opening pass also runs cycle 1's level-0
+    # restriction (launch_restrict_open); 2: the plain one-pass opening
+    opts = S.SolveOptions(nu=nu or cs.nu, tol=cs.tol, max_cycles=min(cs.max_cycles, 30))
     u0 = np.zeros_like(b)
     rep0 = S.mg_solve(h, b, u0, opts)
     u1 = np.full_like(b, np.nan)
     rep1 = S.mg_solve(h, b, u1, opts, zero_guess=True)
     assert np.array_equal(bits(u1), bits(u0)) and rep1.cycles == rep0.cycles and rep1.status == rep0.status
-    assert rep1.history[0] == 1.0 and abs(rep0.history[0] - 1.0) <= 1e-15
+    assert abs(rep0.history[0] - 1.0) <= 1e-15 and abs(rep1.history[0] - 1.0) <= 1e-15
+    if h.n_levels() > 1:
+        assert rep1.history[0] == 1.0  # one pass gives ||b||^2 and ||r0||^2: exactly 1
     assert rep1.history[1:] == rep0.history[1:]
+    for flags in (0, S.LevelHierarchy.FUSE_FINE_DOWN, S.LevelHierarchy.FUSE_ALL):  # every fusion set, max_cycles 1 and 2
+        h.set_fusion(flags)
+        for mc in (1, 2):
+            o2 = S.SolveOptions(nu=opts.nu, tol=opts.tol, max_cycles=mc)
+            ua, ub = np.zeros_like(b), np.full_like(b, np.nan)
+            ra = S.mg_solve(h, b, ua, o2)
+            rb = S.mg_solve(h, b, ub, o2, zero_guess=True)
+            assert np.array_equal(bits(ua), bits(ub)) and ra.cycles == rb.cycles and ra.status == rb.status
+            assert ra.history[1:] == rb.history[1:]
+    h.set_fusion(S.LevelHierarchy.FUSE_DEFAULT)
     bt = torch.from_numpy(b).cuda()
     ut = torch.full_like(bt, float("nan"))
     rep2 = S.mg_solve(h, bt, ut, opts, zero_guess=True)
