@@ -1154,11 +1154,15 @@ void launch_norm_pass(stmg_hierarchy* h, int nu, const double* f, const double* 
 
 // Fine up-pass (k_up) closing a cycle: u = S(*P[0] + P x_c) into the primary buffer,
 // the next speculative iterate into *P[1], partials of ||f - J u||^2.
-void launch_up_pass(stmg_hierarchy* h, const double* xc, double omega, cudaStream_t s, int64_t* np) {
+// virtual_zero: the iterate read is S(0), recomputed from f (cycle 1 of a zero-guess solve:
+// the opening pass then does not store it).
+void launch_up_pass(stmg_hierarchy* h, const double* xc, double omega, cudaStream_t s, int64_t* np,
+                    bool virtual_zero = false) {
   Workspace& ws = *h->ws;
   double** P = up_ptrs(h);
-  launch_check(launch_up(h->adjoint, h->views[0], h->views[1], h->dirs[0], h->f_ptr(0), ws.xb[0]->p, xc, h->xa_ptr(0),
-                         P + 1, P, omega, ws.partials->p, np, s),
+  launch_check(launch_up(h->adjoint, h->views[0], h->views[1], h->dirs[0], h->f_ptr(0),
+                         virtual_zero ? nullptr : ws.xb[0]->p, xc, h->xa_ptr(0), P + 1, virtual_zero ? nullptr : P,
+                         omega, ws.partials->p, np, s),
                "prolong + sweep + norm + sweep");
 }
 
@@ -1354,8 +1358,10 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
   if (open_r) g1 = &get_graph(h, o.nu, o.omega, true);
   if (open_r) {
     const ZeroMode zm = child_zero_mode(h, 0, o.nu);
+    // with the fine up-pass, cycle 1 recomputes S(0) from b as well: it is not stored at all
     launch_check(launch_restrict_open(h->adjoint, h->views[0], h->views[1], h->dirs[0], B, ws.f[1]->p,
-                                      zm.store ? ws.xa[1]->p : nullptr, Y, o.omega, ws.partials->p, &np, h->stream),
+                                      zm.store ? ws.xa[1]->p : nullptr, fine_up(h, o.nu) ? nullptr : Y, o.omega,
+                                      ws.partials->p, &np, h->stream),
                  "sweep from zero + norm + restriction");
     launch_check(launch_finalize_sum(ws.partials->p, np, ws.scalars->p + 0, h->stream), "finalize");
     launch_check(launch_finalize_sum(ws.partials->p, np, ws.scalars->p + 1, h->stream), "finalize");
@@ -1418,7 +1424,7 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
     if (h->profiling) cuda_check(cudaEventRecord(h->norm_ev0, h->stream), "event");
     if (up) {
       int64_t npu = 0;
-      launch_up_pass(h, gg->up_xc, o.omega, h->stream, &npu);
+      launch_up_pass(h, gg->up_xc, o.omega, h->stream, &npu, open_r && cycle == 1);
       launch_check(launch_finalize_sum(ws.partials->p, npu, ws.scalars->p + 1, h->stream), "finalize");
       launches += 1 + finalize_launches(npu);
     } else {

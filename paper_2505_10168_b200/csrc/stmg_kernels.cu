@@ -783,13 +783,18 @@ constexpr int up_minb() { return NT <= 2 ? 4 : NT <= 4 ? 3 : 2; }
 // x_ind: optional device-resident pointer to the input iterate (overrides the
 // loader's x): the solve loop alternates the speculative iterate between two
 // buffers from cycle to cycle with the graph's kernel arguments fixed.
+template <int DIR>
+__device__ __forceinline__ void set_base_x(ProlongOn<DIR, PlainLoad>& ld, const double* x) { ld.base.x = x; }
+template <int DIR>
+__device__ __forceinline__ void set_base_x(ProlongOn<DIR, ZeroLoad>&, const double*) {}  // S(0) comes from f
+
 template <bool ADJ, int NT, class Ld, int MINB = up_minb<NT>()>
 __global__ void __launch_bounds__(kMaxTW, MINB) k_up(LevelView L, Ld ld, const double* __restrict__ f,
                                                      double* __restrict__ u_out, double* const* w_ind,
                                                      const double* const* x_ind, double omega,
                                                      double* __restrict__ partials) {
   pdl_entry();
-  if (x_ind != nullptr) ld.base.x = *x_ind;
+  if (x_ind != nullptr) set_base_x(ld, *x_ind);
   double* w_out = *w_ind;
   const int64_t tt = (int64_t)blockIdx.z * gridDim.y + blockIdx.y;  // time tile
   double acc = 0.0;
@@ -890,11 +895,11 @@ __device__ __forceinline__ double dev_restrict2(const LevelView& F, const LevelV
       }
     }
     if (OPEN) {
-      double* __restrict__ yb = opaque(y_open + (n0 * nn + i));
+      double* __restrict__ yb = y_open != nullptr ? opaque(y_open + (n0 * nn + i)) : nullptr;
 #pragma unroll
       for (int k = 0; k < NT; ++k) {
         acc = acc + (owns ? fv[k] * fv[k] : 0.0);
-        if (owns) *(yb + (uint32_t)k * nn32) = xr[ADJ ? k : k + 1];  // S(0) on row n0 + k
+        if (owns && y_open != nullptr) *(yb + (uint32_t)k * nn32) = xr[ADJ ? k : k + 1];  // S(0) on row n0 + k
       }
     }
     // Output lanes and their coarse node: x step, the lanes at even fine nodes
@@ -971,7 +976,7 @@ __device__ __forceinline__ double dev_restrict2(const LevelView& F, const LevelV
     const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
     if (OPEN && owns && in_grid) {
       acc = acc + fv[k] * fv[k];
-      y_open[n * nn + i] = xr[ADJ ? k : k + 1];  // S(0) on row n
+      if (y_open != nullptr) y_open[n * nn + i] = xr[ADJ ? k : k + 1];  // S(0) on row n
     }
     double r = 0.0;
     if (computes)
@@ -2164,8 +2169,18 @@ template <bool ADJ, int DIR>
 void up_launch(const LevelView& L, const LevelView& C, const double* f, const double* x, const double* xc,
                double* u_out, double* const* w_ind, const double* const* x_ind, double omega, double* partials,
                cudaStream_t s) {
-  const ProlongLoad<DIR> ld{PlainLoad{x, L.nn}, xc, C.nn};
   const dim3 blk = up_block(L), grd = up_grid(L, blk);
+  if (x == nullptr) {  // the iterate is S(0), recomputed from f (cycle 1 of a zero-guess solve)
+    const ProlongZeroLoad<DIR> lz{zero_load(L, f, omega), xc, C.nn};
+    if (lean_nt(L) == 2)
+      pdl_launch(k_up<ADJ, 2, ProlongZeroLoad<DIR>>, grd, blk, 0, s, L, lz, f, u_out, w_ind, x_ind, omega, partials);
+    else if (lean_nt(L) == 4)
+      pdl_launch(k_up<ADJ, 4, ProlongZeroLoad<DIR>>, grd, blk, 0, s, L, lz, f, u_out, w_ind, x_ind, omega, partials);
+    else
+      pdl_launch(k_up<ADJ, 8, ProlongZeroLoad<DIR>>, grd, blk, 0, s, L, lz, f, u_out, w_ind, x_ind, omega, partials);
+    return;
+  }
+  const ProlongLoad<DIR> ld{PlainLoad{x, L.nn}, xc, C.nn};
   if (lean_nt(L) == 2)
     pdl_launch(k_up<ADJ, 2, ProlongLoad<DIR>>, grd, blk, 0, s, L, ld, f, u_out, w_ind, x_ind, omega, partials);
   else if (lean_nt(L) == 4)
