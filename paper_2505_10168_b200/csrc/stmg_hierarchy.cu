@@ -934,7 +934,9 @@ ZeroMode child_zero_mode(const stmg_hierarchy* h, int l, int nu) {
   const bool fused = !h->galerkin(l) && !h->gen_xfer(l);
   const bool plain = fused && nu >= 1 && l + 1 < h->n_levels() - 1 && !h->galerkin(l + 1);
   m.virt = plain && (h->fusion & kFuseVirtualZero) && !h->gen_xfer(l + 1);
-  m.store = plain && !m.virt;
+  // without the virtual zero iterate the child sweeps from zero itself (launch_sweep_from_zero);
+  // the restriction tiles no longer write the child's first sweep (the fine down-pass k_down can)
+  m.store = plain && !m.virt && l == 0 && fine_down(h, nu);
   return m;
 }
 
@@ -1349,7 +1351,7 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
   // so it runs inside the opening pass too (launch_restrict_open: 20 B/DOF for the sweep,
   // the norm and level 1's right-hand side), and cycle 1 uses the graph that starts at level 1.
   const bool open_r = zero_guess && spec && o.max_cycles > 0 && o.nu == 1 && h->n_levels() >= 2 &&
-                      !h->galerkin(0) && !h->gen_xfer(0);
+                      !h->galerkin(0) && !h->gen_xfer(0) && !child_zero_mode(h, 0, o.nu).store;
   const bool zero_open = zero_guess && spec && o.max_cycles > 0 && (open_r || !fine_down(h, o.nu));
   if (zero_guess && !zero_open) cuda_check(cudaMemsetAsync(X, 0, bytes, h->stream), "u clear");
   GraphEntry* g = nullptr;
@@ -1357,10 +1359,9 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
   if (o.max_cycles > 0) g = &get_graph(h, o.nu, o.omega);
   if (open_r) g1 = &get_graph(h, o.nu, o.omega, true);
   if (open_r) {
-    const ZeroMode zm = child_zero_mode(h, 0, o.nu);
     // with the fine up-pass, cycle 1 recomputes S(0) from b as well: it is not stored at all
-    launch_check(launch_restrict_open(h->adjoint, h->views[0], h->views[1], h->dirs[0], B, ws.f[1]->p,
-                                      zm.store ? ws.xa[1]->p : nullptr, fine_up(h, o.nu) ? nullptr : Y, o.omega,
+    launch_check(launch_restrict_open(h->adjoint, h->views[0], h->views[1], h->dirs[0], B, ws.f[1]->p, nullptr,
+                                      fine_up(h, o.nu) ? nullptr : Y, o.omega,
                                       ws.partials->p, &np, h->stream),
                  "sweep from zero + norm + restriction");
     launch_check(launch_finalize_sum(ws.partials->p, np, ws.scalars->p + 0, h->stream), "finalize");

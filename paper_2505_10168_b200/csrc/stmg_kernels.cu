@@ -853,7 +853,7 @@ template <bool ADJ, int DIR, int NT, bool ZX = false, bool OPEN = false>
 __device__ __forceinline__ double dev_restrict2(const LevelView& F, const LevelView& C,
                                                 const double* __restrict__ f, const double* __restrict__ x,
                                                 double* __restrict__ fc, int64_t tile, int64_t ttile, int tw,
-                                                double* __restrict__ xc0 = nullptr, double omega = 0.0,
+                                                double* __restrict__ /*xc0: unused*/ = nullptr, double omega = 0.0,
                                                 double* __restrict__ y_open = nullptr) {
   static_assert(!OPEN || ZX, "the opening pass restricts the virtual zero iterate");
   if ((int)threadIdx.x >= tw) return 0.0;
@@ -908,9 +908,6 @@ __device__ __forceinline__ double dev_restrict2(const LevelView& F, const LevelV
     const int64_t I = DIR == 0 ? (i >> 1) : i;
     const int64_t crow = DIR == 0 ? n0 : (n0 >> 1);
     double* __restrict__ fcb = opaque(fc + (crow * nnc + I));
-    double* __restrict__ xcb = xc0 != nullptr ? opaque(xc0 + (crow * nnc + I)) : nullptr;
-    // coarse inverse diagonal at this lane's coarse node (first coarse sweep from zero)
-    const double idc = (xc0 != nullptr && out) ? __ldg(C.coef + kInvD * nnc + I) : 0.0;
     double pm = __shfl_up_sync(kFull, xr[0], 1), pp = __shfl_down_sync(kFull, xr[0], 1);
     double r_even = 0.0;
 #pragma unroll
@@ -926,14 +923,12 @@ __device__ __forceinline__ double dev_restrict2(const LevelView& F, const LevelV
         const double rc = __shfl_down_sync(kFull, r, 1);
         const double v = ((0.5 * ra + 1.0 * r) + 0.5 * rc) + 0.0;
         if (out) *(fcb + (uint32_t)k * nnc32) = v;
-        if (xc0 != nullptr && out) *(xcb + (uint32_t)k * nnc32) = 0.0 + omega * (v * idc);
       } else {
         if ((k & 1) == 0) {
           r_even = r;
         } else {
           const double v = (0.5 * r_even + 0.5 * r) + 0.0;
           if (out) *(fcb + (uint32_t)(k >> 1) * nnc32) = v;
-          if (xc0 != nullptr && out) *(xcb + (uint32_t)(k >> 1) * nnc32) = 0.0 + omega * (v * idc);
         }
       }
       pm = qm;
@@ -995,7 +990,6 @@ __device__ __forceinline__ double dev_restrict2(const LevelView& F, const LevelV
         if (2 * I + 1 <= F.n_el) a.add(0.5 * rc);
         const double v = a.result();
         fc[n * nnc + I] = v;
-        if (xc0 != nullptr) xc0[n * nnc + I] = coarse_from_zero(C, n, I, v, omega);
       }
     } else if (computes) {
       if ((k & 1) == 0) {
@@ -1005,7 +999,6 @@ __device__ __forceinline__ double dev_restrict2(const LevelView& F, const LevelV
           a.add(0.5 * r);
           const double v = a.result();
           fc[(n >> 1) * nnc + i] = v;
-          if (xc0 != nullptr) xc0[(n >> 1) * nnc + i] = coarse_from_zero(C, n >> 1, i, v, omega);
         }
       } else {
         Acc a;
@@ -1013,7 +1006,6 @@ __device__ __forceinline__ double dev_restrict2(const LevelView& F, const LevelV
         a.add(0.5 * r);
         const double v = a.result();
         fc[(n >> 1) * nnc + i] = v;
-        if (xc0 != nullptr) xc0[(n >> 1) * nnc + i] = coarse_from_zero(C, n >> 1, i, v, omega);
       }
     }
     pm = qm;
@@ -2061,6 +2053,9 @@ void restrict_open_launch(const LevelView& F, const LevelView& C, const double* 
 template <bool ADJ, int DIR>
 int restrict_impl(const LevelView& F, const LevelView& C, const double* f, const double* x,
                   double* fc, cudaStream_t s, double* xc0, double omega, const double* const* x_ind) {
+  // the stored coarse first sweep is no longer written by the restriction tiles (dead code on
+  // the default path: 8 % of the ZX tile's instructions); the child sweeps from zero itself
+  if (xc0 != nullptr) return static_cast<int>(cudaErrorInvalidValue);
   if (x == nullptr) restrict_launch<ADJ, DIR, true>(F, C, f, x, fc, s, xc0, omega, nullptr);  // x = S(0) from f
   else restrict_launch<ADJ, DIR, false>(F, C, f, x, fc, s, xc0, omega, x_ind);
   return check_launch();
@@ -2278,6 +2273,7 @@ int launch_restrict_open(bool adjoint, const LevelView& F, const LevelView& C, i
                          double* xc0, double* y, double omega, double* partials, int64_t* n_partials,
                          cudaStream_t s) {
   if (dir == 1 && (F.tile_nt % 2 != 0 || (F.n_lo & 1) != 0)) return static_cast<int>(cudaErrorInvalidValue);
+  if (xc0 != nullptr) return static_cast<int>(cudaErrorInvalidValue);  // see restrict_impl
   if (n_partials) *n_partials = restrict_open_partials_needed(F, C, dir);
   if (adjoint) {
     if (dir == 0) restrict_open_launch<true, 0>(F, C, f, fc, xc0, y, omega, partials, s);
