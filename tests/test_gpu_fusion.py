@@ -170,3 +170,32 @@ def test_fine_up_kernel_bitwise(torch, S, port, name, tiles):
         assert np.array_equal(bits(w), bits(hp.sweeps(l, f, u_want, 1))), (l, "speculative sweep")
         r = hp.residual(l, f, u_want)
         assert abs(nrm2 - float(np.dot(r, r))) <= 1e-13 * float(np.dot(r, r)), (l, "norm")
+
+
+def test_shared_workspace_alternating_forward_and_adjoint_solves(torch, S, port):
+    """A hierarchy and its transpose share the workspace (the third level-0 buffer and the
+    pointer table of the fine up-pass included): alternating nu = 1 solves on both, flagged
+    and in/out, give what fresh hierarchies give, bit for bit."""
+    cs = case("cfg1_mini")
+    b = cs.rhs_vector(port)
+    b2 = b[::-1].copy()
+    opts = S.SolveOptions(nu=1, tol=cs.tol, max_cycles=12)
+
+    def fresh(adj, rhs):
+        h = gpu_hier(S, cs, port)
+        if adj:
+            h = S.transposed_hierarchy(h)
+        u = np.zeros_like(rhs)
+        return S.mg_solve(h, rhs, u, opts), u
+
+    want = {(adj, k): fresh(adj, rhs) for adj in (False, True) for k, rhs in enumerate((b, b2))}
+    h = gpu_hier(S, cs, port)
+    ht = S.transposed_hierarchy(h)
+    for rnd in range(2):
+        for adj, hh in ((False, h), (True, ht)):
+            for k, rhs in enumerate((b, b2)):
+                u = np.full_like(rhs, np.nan) if rnd else np.zeros_like(rhs)
+                r = S.mg_solve(hh, rhs, u, opts, zero_guess=bool(rnd))
+                rw, uw = want[(adj, k)]
+                assert r.cycles == rw.cycles and r.status == rw.status and r.history[1:] == rw.history[1:]
+                assert np.array_equal(bits(u), bits(uw)), (rnd, adj, k)
