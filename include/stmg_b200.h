@@ -389,6 +389,11 @@ int stmg_dist_transport(const stmg_dist* d, char* name_out, int32_t cap);
  * cycle.  Default: device loop when every rank is in this process (loopback); across
  * processes (NCCL calls inside the loop body) opt in with STMG_DIST_DEVICE_LOOP=1. */
 int stmg_dist_loop_on_device(const stmg_dist* d, int32_t* yes);
+/* Passes captured in split form so far: with STMG_DIST_OVERLAP=<minimum slab DOFs> a level's
+ * ghost exchange runs on a forked side stream while every rank's kernel runs on the interior
+ * rows of its slab (no ghost level read); the first and last 16 rows follow after the join.
+ * Opt-in (its benefit needs more than one GPU to measure); results are bit-identical. */
+int stmg_dist_split_passes(const stmg_dist* d, int64_t* count);
 void stmg_dist_destroy(stmg_dist* d);
 
 /* Per-handle tiling of the stencil kernels (A/B measurements, tests of every

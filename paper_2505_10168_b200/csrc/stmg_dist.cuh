@@ -582,6 +582,12 @@ struct stmg_dist {
   double* loop_host = nullptr;
   bool device_loop = false;
   bool last_on_device = false;  // the last solve's cycle loop ran as the device graph
+  // Ghost exchanges overlapped with interior rows (STMG_DIST_OVERLAP = minimum slab DOFs
+  // of a level to split its passes; 0 = off): side stream and fork / join events
+  int64_t overlap_dofs = 0;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int64_t split_passes = 0;  // passes emitted in split form (tests)
 
   ~stmg_dist() {
     int prev = 0;
@@ -595,6 +601,9 @@ struct stmg_dist {
       if (kv.second.loop_graph) cudaGraphDestroy(kv.second.loop_graph);
     }
     if (loop_host) cudaFreeHost(loop_host);
+    if (side) cudaStreamDestroy(side);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     // Peer-memory transport: no rank may free slab buffers a neighbour can still
     // read.  Every rank first closes its mappings of the neighbours' buffers,
     // then all ranks meet (a one-double all-reduce on the base communicator),
@@ -644,17 +653,67 @@ struct DistEmitter {
     for (int k = 0; k < W(); ++k) v.push_back(buf(k, l, which));
     return v;
   }
-  void exchange(int l, int which, int depth = 1) {
-    d->comm->exchange(bufs(l, which), d->plan.bounds[l], d->nn(l), depth, s);
+  void exchange(int l, int which, int depth = 1, cudaStream_t on = nullptr) {
+    d->comm->exchange(bufs(l, which), d->plan.bounds[l], d->nn(l), depth, on ? on : s);
   }
-  void sweep_all(int l, int cur) {
-    exchange(l, cur);
-    for (int k = 0; k < W(); ++k) {
-      launch_check(launch_sweep(d->adjoint, d->ranks[k].views[l], d->ranks[k].f[l]->p, buf(k, l, cur),
-                                buf(k, l, 1 - cur), omega, nullptr, nullptr, s),
-                   "dist sweep");
-      ++kernels;
+
+  // One pass over level l on every local rank, fed by a ghost exchange.  Plain form:
+  // exchange, then each rank's kernel on its slab rows.  Split form (STMG_DIST_OVERLAP,
+  // levels whose slabs are large enough): the exchange runs on a forked side stream while
+  // each rank's kernel runs on the INTERIOR rows, whose tiles read no ghost level; after
+  // the join the first and last kEdge rows of each slab follow.  kEdge is a multiple of
+  // every tile depth and even, so the tiles and the t-restriction pairs are those of the
+  // unsplit launch; the kernels are pointwise in the rows, so the values are identical.
+  static constexpr int64_t kEdge = 16;
+  bool splits(int l) const {
+    if (d->overlap_dofs <= 0 || d->comm->world == 1) return false;
+    for (const RankState& R : d->ranks) {
+      const LevelView& V = R.views[l];
+      if (V.n_hi - V.n_lo < 4 * kEdge || (V.n_hi - V.n_lo) * V.nn < d->overlap_dofs) return false;
     }
+    return true;
+  }
+  template <class Exch, class Launch>
+  void pass(int l, Exch&& exch, Launch&& launch) {
+    if (!splits(l)) {
+      exch(s);
+      for (int k = 0; k < W(); ++k) launch(k, d->ranks[k].views[l]);
+      return;
+    }
+    ++d->split_passes;
+    cuda_check(cudaEventRecord(d->ev_fork, s), "fork");
+    cuda_check(cudaStreamWaitEvent(d->side, d->ev_fork, 0), "fork wait");
+    exch(d->side);
+    cuda_check(cudaEventRecord(d->ev_join, d->side), "join");
+    std::vector<std::pair<int64_t, int64_t>> inner(static_cast<size_t>(W()));
+    for (int k = 0; k < W(); ++k) {
+      LevelView V = d->ranks[k].views[l];
+      const int64_t lo = V.n_lo + kEdge, hi = (V.n_hi - kEdge) & ~int64_t{1};
+      inner[k] = {lo, hi};
+      V.n_lo = lo;
+      V.n_hi = hi;
+      launch(k, V);
+    }
+    cuda_check(cudaStreamWaitEvent(s, d->ev_join, 0), "join wait");
+    for (int k = 0; k < W(); ++k) {
+      LevelView V = d->ranks[k].views[l];
+      LevelView A = V, B = V;
+      A.n_hi = inner[k].first;
+      B.n_lo = inner[k].second;
+      launch(k, A);
+      launch(k, B);
+    }
+  }
+
+  void sweep_all(int l, int cur) {
+    pass(
+        l, [&](cudaStream_t on) { exchange(l, cur, 1, on); },
+        [&](int k, const LevelView& V) {
+          launch_check(launch_sweep(d->adjoint, V, d->ranks[k].f[l]->p, buf(k, l, cur), buf(k, l, 1 - cur), omega,
+                                    nullptr, nullptr, s),
+                       "dist sweep");
+          ++kernels;
+        });
   }
 
   // Returns the buffer index holding the level-l result on every rank (2 = the
@@ -710,15 +769,16 @@ struct DistEmitter {
     smooth_all(l, cur, pre);
     // residual + restriction into level l+1 (slab rows of l+1, or the rows this
     // rank contributes to the first gathered level)
-    exchange(l, cur);
-    for (int k = 0; k < W(); ++k) {
-      const LevelView C = l + 1 < Lg ? d->ranks[k].views[l + 1] : d->full_views[l + 1];
-      double* fc = l + 1 < Lg ? d->ranks[k].f[l + 1]->p : d->ranks[k].fg->p;
-      launch_check(launch_restrict_residual(d->adjoint, d->ranks[k].views[l], C, d->dirs[l],
-                                            d->ranks[k].f[l]->p, buf(k, l, cur), fc, s),
-                   "dist restrict");
-      ++kernels;
-    }
+    pass(
+        l, [&](cudaStream_t on) { exchange(l, cur, 1, on); },
+        [&](int k, const LevelView& V) {
+          const LevelView C = l + 1 < Lg ? d->ranks[k].views[l + 1] : d->full_views[l + 1];
+          double* fc = l + 1 < Lg ? d->ranks[k].f[l + 1]->p : d->ranks[k].fg->p;
+          launch_check(launch_restrict_residual(d->adjoint, V, C, d->dirs[l], d->ranks[k].f[l]->p, buf(k, l, cur), fc,
+                                                s),
+                       "dist restrict");
+          ++kernels;
+        });
     const int child = level(l + 1, 0, 0, true);
     if (child != 2) exchange(l + 1, child);  // coarse ghosts for the prolongation of ghost rows
     std::vector<const double*> xc;
@@ -751,13 +811,14 @@ struct DistEmitter {
   // exchange (one exchange per two sweeps), then a single sweep if count is odd.
   void smooth_all(int l, int& cur, int count) {
     for (; count >= 2; count -= 2) {
-      exchange(l, cur, 2);
-      for (int k = 0; k < W(); ++k) {
-        launch_check(launch_sweep2(d->adjoint, d->ranks[k].views[l], d->ranks[k].f[l]->p, buf(k, l, cur),
-                                   buf(k, l, 1 - cur), omega, s),
-                     "dist sweep2");
-        ++kernels;
-      }
+      pass(
+          l, [&](cudaStream_t on) { exchange(l, cur, 2, on); },
+          [&](int k, const LevelView& V) {
+            launch_check(launch_sweep2(d->adjoint, V, d->ranks[k].f[l]->p, buf(k, l, cur), buf(k, l, 1 - cur), omega,
+                                       s),
+                         "dist sweep2");
+            ++kernels;
+          });
       cur = 1 - cur;
     }
     if (count == 1) {
@@ -903,6 +964,12 @@ void dist_build(stmg_dist* d, int world, int rank, const void* nccl_id, int64_t 
   // calls; that form is opt-in (STMG_DIST_DEVICE_LOOP=1) until it has run at world > 1.
   d->device_loop = nccl_id == nullptr;
   if (const char* e = std::getenv("STMG_DIST_DEVICE_LOOP")) d->device_loop = std::atoi(e) != 0;
+  if (const char* e = std::getenv("STMG_DIST_OVERLAP")) d->overlap_dofs = std::atoll(e);
+  if (d->overlap_dofs > 0) {
+    cuda_check(cudaStreamCreateWithFlags(&d->side, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming), "cudaEventCreate");
+  }
   if (const char* e = std::getenv("STMG_DIST_P2P"); e && std::atoi(e) != 0) {
     enable_p2p(d);
     if (std::atoi(e) == 2) static_cast<P2pComm*>(d->comm.get())->legacy_loopback = true;

@@ -2661,6 +2661,13 @@ int stmg_dist_transport(const stmg_dist* d, char* name_out, int32_t cap) {
   });
 }
 
+int stmg_dist_split_passes(const stmg_dist* d, int64_t* count) {
+  return guarded([&] {
+    if (!d || !count) throw std::invalid_argument("null handle or argument");
+    *count = d->split_passes;
+  });
+}
+
 int stmg_dist_loop_on_device(const stmg_dist* d, int32_t* yes) {
   return guarded([&] {
     if (!d || !yes) throw std::invalid_argument("null handle or argument");

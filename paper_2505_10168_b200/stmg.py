@@ -98,6 +98,7 @@ def _load():
         "stmg_dist_create": [vp, vp, vp, vp, vp, C.c_char_p, i32, vp, i32, i32, i32, vp, i32, i64,
                              C.POINTER(vp)],
         "stmg_dist_loop_on_device": [vp, C.POINTER(i32)],
+        "stmg_dist_split_passes": [vp, C.POINTER(i64)],
         "stmg_dist_info": [vp, C.POINTER(i32), C.POINTER(i64), C.POINTER(i64), C.POINTER(i32),
                            C.POINTER(i64)],
         "stmg_dist_mg_solve": [vp, vp, vp, vp, vp, vp, i32],
@@ -847,6 +848,13 @@ class DistHierarchy:
     @property
     def handle(self):
         return self._h
+
+    @property
+    def split_passes(self) -> int:
+        """Passes captured with the ghost exchange overlapping interior rows (STMG_DIST_OVERLAP)."""
+        v = C.c_int64(0)
+        _check(_lib.stmg_dist_split_passes(self._h, C.byref(v)))
+        return int(v.value)
 
     @property
     def loop_on_device(self) -> bool:

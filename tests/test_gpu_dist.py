@@ -230,3 +230,32 @@ def test_device_cycle_loop_with_nccl_in_the_body_world1(S, port, monkeypatch):
     assert r2.cycles == r1.cycles and r2.status == r1.status
     assert np.array_equal(u1.view(np.uint64), u2.view(np.uint64))
     assert np.allclose(r2.history, r1.history, rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("p2p", ["0", "1"])
+@pytest.mark.parametrize("loop", ["1", "0"])
+@pytest.mark.parametrize("name,world", [("cfg1_mini", 2), ("cfg1_mini_adj", 2), ("cfg2_mini", 2), ("cfg4_mini", 2)])
+def test_overlapped_ghost_exchange_is_bitwise(S, port, monkeypatch, name, world, loop, p2p):
+    """STMG_DIST_OVERLAP: the ghost exchange of a pass runs on a forked side stream while
+    every rank's kernel runs on the interior rows of its slab; the first and last 16 rows
+    follow after the join (sweeps, fused pairs, restrictions; inside the captured V-cycle and
+    inside the device loop's conditional body).  Same iterate as the single-domain solve."""
+    cs = case(name)
+    g, path = grid_path(S, cs, port)
+    b = cs.rhs_vector(port)
+    opts = S.SolveOptions(nu=cs.nu, tol=cs.tol, max_cycles=min(cs.max_cycles, 20))
+    h = S.build_hierarchy(g, cs.method, path, chi=cs.chi, mat=cs.mat)
+    if cs.adjoint:
+        h = S.transposed_hierarchy(h)
+    u1 = np.zeros_like(b)
+    r1 = S.mg_solve(h, b, u1, opts)
+    monkeypatch.setenv("STMG_DIST_OVERLAP", "1")
+    monkeypatch.setenv("STMG_DIST_DEVICE_LOOP", loop)
+    monkeypatch.setenv("STMG_DIST_P2P", p2p)  # 1: the cooperative all-ranks pull kernel on the side stream
+    dh = S.build_dist_hierarchy(g, cs.method, path, world, adjoint=cs.adjoint, chi=cs.chi, mat=cs.mat, min_slab=8)
+    for _ in range(2):
+        u2 = np.zeros_like(b)
+        r2 = S.mg_solve_dist(dh, b, u2, opts)
+        assert r2.cycles == r1.cycles and r2.status == r1.status
+        assert np.array_equal(u1.view(np.uint64), u2.view(np.uint64))
+    assert dh.split_passes > 0 and dh.loop_on_device == (loop == "1")
