@@ -163,3 +163,14 @@ def test_dist_create_argument_errors_before_device_work():
     g.k, g.c = np.ones(8), np.ones(8)
     with pytest.raises(ValueError):  # time slabs take causal K/D/R only: rejected in the C layer, no device touched
         S.build_dist_hierarchy(g, "CP", S.CoarseningPath([S.CoarseningDirection(0)]), world=1, rank=0)
+
+
+def test_abi_version_matches_header():
+    """The ctypes struct layouts in stmg.py belong to one C ABI version: the header's."""
+    import re
+
+    from paper_2505_10168_b200 import stmg as S
+
+    hdr = open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "stmg_b200.h")).read()
+    v = int(re.search(r"#define STMG_ABI_VERSION (\d+)", hdr).group(1))
+    assert S.ABI_VERSION == v == S.abi_version()
