@@ -155,7 +155,11 @@ __device__ __forceinline__ double row_interior(const Coefs& c, double xm, double
 //   J^T row order: [W, D, E, NW, N, NE]  (same level first)
 // Masked columns (node 0 or time 0) and entries past the grid are absent
 // (proj/src/assembly.cpp:99-123; proj/src/sparse.cpp:74-96).
-template <bool ADJ>
+// EDGE: also short four-entry forms for node 1 / node n_el (see below); compiled into the
+// tiles of small levels only (time tiles of <= 4 levels), where the edge warps' blocks set
+// the pace; in the 8- and 16-level tiles the extra code costs registers (spills) and
+// measured slower.
+template <bool ADJ, bool EDGE = false>
 __device__ __forceinline__ double row_sum(const LevelView& L, int64_t n, int64_t i, const Coefs& c,
                                           double xm, double x0, double xp, double ym, double y0,
                                           double yp) {
@@ -166,6 +170,20 @@ __device__ __forceinline__ double row_sum(const LevelView& L, int64_t n, int64_t
   const bool has_p = i <= L.n_el - 1;
   const bool has_o = ADJ ? (n <= L.n_t - 1) : (n >= 2);
   if (has_m && has_p && has_o) return row_interior<ADJ>(c, xm, x0, xp, ym, y0, yp);
+  // Node 1 (no i - 1 entries) and node n_el (no i + 1 entries) on a row that has its coupled
+  // level: four entries, one per canonical lane, (s0 + s1) + (s2 + s3) with s = 0 + v, folded
+  // to a final + 0.0 as in row_interior.  These are the rows of the first and last warp of
+  // every interior time tile: without this short form they took the generic accumulator below
+  // (a data-dependent lane switch per entry) and made their block ~2x slower on narrow levels.
+  if (EDGE && has_o && has_m != has_p) {
+    if (!ADJ) {  // [SW, S, SE, W, D, E] without the missing side
+      if (has_p) return ((c.o0 * y0 + c.op * yp) + (c.c0 * x0 + c.cp * xp)) + 0.0;
+      return ((c.om * ym + c.o0 * y0) + (c.cm * xm + c.c0 * x0)) + 0.0;
+    }
+    // [W, D, E, NW, N, NE] without the missing side
+    if (has_p) return ((c.c0 * x0 + c.cp * xp) + (c.o0 * y0 + c.op * yp)) + 0.0;
+    return ((c.cm * xm + c.c0 * x0) + (c.om * ym + c.o0 * y0)) + 0.0;
+  }
   Acc a;
   if (!ADJ) {
     if (has_o) {
@@ -433,8 +451,8 @@ __device__ __forceinline__ double dev_lean2(const LevelView& L, const Ld& ld, co
     const double qm = __shfl_up_sync(kFull, x1, 1);
     const double qp = __shfl_down_sync(kFull, x1, 1);
     if (computes) {
-      const double row = ADJ ? row_sum<true>(L, n, i, c, pm, xr[k], pp, qm, x1, qp)
-                             : row_sum<false>(L, n, i, c, qm, x1, qp, pm, xr[k], pp);
+      const double row = ADJ ? row_sum<true, (NT <= 4)>(L, n, i, c, pm, xr[k], pp, qm, x1, qp)
+                             : row_sum<false, (NT <= 4)>(L, n, i, c, qm, x1, qp, pm, xr[k], pp);
       const double x0 = ADJ ? xr[k] : x1;
       const double r = fv[k] - row;
       if (NORM) acc = acc + r * r;
@@ -585,7 +603,7 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
       const int64_t n = s1base + r;
       double v = 0.0;
       if (lane1 && n <= nt) {
-        const double row = row_sum<true>(L, n, i, c, pm, xs[r], pp, qm, x1, qp);
+        const double row = row_sum<true, (NT <= 4)>(L, n, i, c, pm, xs[r], pp, qm, x1, qp);
         const double id = (n == 0 || i == 0) ? L.inv_w : c.invd;
         v = xs[r] + omega * ((fv[r] - row) * id);
       }
@@ -602,7 +620,7 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
       const int64_t n = s1base + r;
       double v = 0.0;
       if (lane1 && n >= 0 && n <= nt) {
-        const double row = row_sum<false>(L, n, i, c, qm, x1, qp, pm, xs[r], pp);
+        const double row = row_sum<false, (NT <= 4)>(L, n, i, c, qm, x1, qp, pm, xs[r], pp);
         const double id = (n == 0 || i == 0) ? L.inv_w : c.invd;
         v = x1 + omega * ((fv[r] - row) * id);
       }
@@ -621,11 +639,11 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
     if (lane2 && n < L.n_hi) {
       double row, x0, fval;
       if (ADJ) {  // row n = y1[k] level, coupled y1[k+1]
-        row = row_sum<true>(L, n, i, c, am, y1[k], ap, bm, z1, bp);
+        row = row_sum<true, (NT <= 4)>(L, n, i, c, am, y1[k], ap, bm, z1, bp);
         x0 = y1[k];
         fval = fv[k];
       } else {  // row n = y1[k+1] level, coupled y1[k]
-        row = row_sum<false>(L, n, i, c, bm, z1, bp, am, y1[k], ap);
+        row = row_sum<false, (NT <= 4)>(L, n, i, c, bm, z1, bp, am, y1[k], ap);
         x0 = z1;
         fval = fv[k + 1];
       }
@@ -735,8 +753,8 @@ __device__ __forceinline__ double dev_up(const LevelView& L, const Ld& ld, const
     const int64_t n = s1base + r;
     double v = 0.0;
     if (lane1 && n >= 0 && n <= nt) {
-      const double row = ADJ ? row_sum<true>(L, n, i, c, pm, xs[r], pp, qm, x1, qp)
-                             : row_sum<false>(L, n, i, c, qm, x1, qp, pm, xs[r], pp);
+      const double row = ADJ ? row_sum<true, (NT <= 4)>(L, n, i, c, pm, xs[r], pp, qm, x1, qp)
+                             : row_sum<false, (NT <= 4)>(L, n, i, c, qm, x1, qp, pm, xs[r], pp);
       const double id = (n == 0 || i == 0) ? L.inv_w : c.invd;
       v = (ADJ ? xs[r] : x1) + omega * ((fv[r] - row) * id);
       if (lane2 && n >= n0 && n < n0 + NT && n < L.n_hi) u_out[n * nn + i] = v;
@@ -754,11 +772,11 @@ __device__ __forceinline__ double dev_up(const LevelView& L, const Ld& ld, const
     if (lane2 && n < L.n_hi) {
       double row, x0, fval;
       if (ADJ) {
-        row = row_sum<true>(L, n, i, c, am, y1[k], ap, bm, z1, bp);
+        row = row_sum<true, (NT <= 4)>(L, n, i, c, am, y1[k], ap, bm, z1, bp);
         x0 = y1[k];
         fval = fv[k];
       } else {
-        row = row_sum<false>(L, n, i, c, bm, z1, bp, am, y1[k], ap);
+        row = row_sum<false, (NT <= 4)>(L, n, i, c, bm, z1, bp, am, y1[k], ap);
         x0 = z1;
         fval = fv[k + 1];
       }
@@ -975,8 +993,8 @@ __device__ __forceinline__ double dev_restrict2(const LevelView& F, const LevelV
     }
     double r = 0.0;
     if (computes)
-      r = fv[k] - (ADJ ? row_sum<true>(F, n, i, c, pm, xr[k], pp, qm, x1, qp)
-                       : row_sum<false>(F, n, i, c, qm, x1, qp, pm, xr[k], pp));
+      r = fv[k] - (ADJ ? row_sum<true, (NT <= 4)>(F, n, i, c, pm, xr[k], pp, qm, x1, qp)
+                       : row_sum<false, (NT <= 4)>(F, n, i, c, qm, x1, qp, pm, xr[k], pp));
     if (DIR == 0) {
       const int src = 2 * lane;
       const double ra = __shfl_sync(kFull, r, src & 31);
@@ -1194,10 +1212,10 @@ __device__ __forceinline__ double dev_down(const LevelView& F, const LevelView& 
     if (lane1 && n >= 0 && n <= nt) {
       double row, x0;
       if (ADJ) {
-        row = row_sum<true>(F, n, i, c, pm, xs[r], pp, qm, x1, qp);
+        row = row_sum<true, (NT <= 4)>(F, n, i, c, pm, xs[r], pp, qm, x1, qp);
         x0 = xs[r];
       } else {
-        row = row_sum<false>(F, n, i, c, qm, x1, qp, pm, xs[r], pp);
+        row = row_sum<false, (NT <= 4)>(F, n, i, c, qm, x1, qp, pm, xs[r], pp);
         x0 = x1;
       }
       const double res = fv[r] - row;
@@ -1223,8 +1241,8 @@ __device__ __forceinline__ double dev_down(const LevelView& F, const LevelView& 
     const double bm = __shfl_up_sync(kFull, z1, 1), bp = __shfl_down_sync(kFull, z1, 1);
     double r2 = 0.0;
     if (lane2)
-      r2 = ADJ ? fv[k] - row_sum<true>(F, n, i, c, am, y1[k], ap, bm, z1, bp)
-               : fv[k + 1] - row_sum<false>(F, n, i, c, bm, z1, bp, am, y1[k], ap);
+      r2 = ADJ ? fv[k] - row_sum<true, (NT <= 4)>(F, n, i, c, am, y1[k], ap, bm, z1, bp)
+               : fv[k + 1] - row_sum<false, (NT <= 4)>(F, n, i, c, bm, z1, bp, am, y1[k], ap);
     if (DIR == 0) {
       const int src = 2 * lane;
       const double ra = __shfl_sync(kFull, r2, src & 31);
