@@ -208,6 +208,49 @@ __device__ __forceinline__ double row_sum(const LevelView& L, int64_t n, int64_t
 }
 
 
+// Edge warps of an interior time tile (every row has its coupled level and is unmasked): the
+// warps holding node 0 / node 1 (first) and node n_el (last) run the interior tile body too,
+// with the lane's node clamped into the grid for addresses (out-of-grid lanes stage finite
+// duplicates that no stored lane couples to), and the three special rows re-evaluated in
+// their own canonical forms (row_sum's: node 0 masked, node 1 without i - 1, node n_el
+// without i + 1).  Without this the edge warps took the fully general tile body (64-bit
+// indexing, per-row masks, the lane-switching accumulator), ~5x an interior warp: 2 of 10
+// warps per row on a 257-node level, which made narrow levels ~2x slower per DOF than wide ones.
+struct EdgeLane {
+  int64_t ia;    // node used for addresses (clamped)
+  int cls;       // 0 interior row, 1 node 0, 2 node 1, 3 node n_el
+  bool in_grid;  // the lane's node exists
+};
+template <bool EDGE>
+__device__ __forceinline__ EdgeLane edge_lane(const LevelView& L, int64_t i) {
+  EdgeLane e{i, 0, true};
+  if (EDGE) {
+    e.ia = i < 0 ? 0 : (i > L.n_el ? L.n_el : i);
+    e.in_grid = e.ia == i;
+    e.cls = i == 0 ? 1 : (i == 1 ? 2 : (i == L.n_el ? 3 : 0));
+  }
+  return e;
+}
+// Needs n_el >= 2 (node 1 and node n_el distinct).
+template <bool ADJ, bool EDGE>
+__device__ __forceinline__ double row_tile(const LevelView& L, int cls, const Coefs& c, double xm, double x0,
+                                           double xp, double ym, double y0, double yp) {
+  double row = row_interior<ADJ>(c, xm, x0, xp, ym, y0, yp);
+  if (EDGE && cls != 0) {
+    if (cls == 1) {
+      row = 0.0 + L.w * x0;
+    } else if (!ADJ) {  // [SW, S, SE, W, D, E] without the missing side
+      row = cls == 2 ? ((c.o0 * y0 + c.op * yp) + (c.c0 * x0 + c.cp * xp)) + 0.0
+                     : ((c.om * ym + c.o0 * y0) + (c.cm * xm + c.c0 * x0)) + 0.0;
+    } else {  // [W, D, E, NW, N, NE] without the missing side
+      row = cls == 2 ? ((c.c0 * x0 + c.cp * xp) + (c.o0 * y0 + c.op * yp)) + 0.0
+                     : ((c.cm * xm + c.c0 * x0) + (c.om * ym + c.o0 * y0)) + 0.0;
+    }
+  }
+  return row;
+}
+
+
 // P x_c at fine DOF (n, i) (csr_spmv_add row, proj/src/transfer.cpp:74-88).
 template <int DIR>
 __device__ __forceinline__ double prolong_row(const double* __restrict__ xc, int64_t nnc, int64_t n,
@@ -393,22 +436,28 @@ __device__ __forceinline__ double dev_lean2(const LevelView& L, const Ld& ld, co
   const bool nodes_in = wfirst >= 2 && wfirst + 29 <= L.n_el - 1;
   double xr[NT + 1], fv[NT];
   double acc = 0.0;
-  if (rows_in && nodes_in) {
-    // every lane's node is inside the grid: lanes 0 / 31 load too (unused values).
+  // interior time tile: the predicate-free body; EDGE (std::true_type) for the warps that hold
+  // node 0 / 1 / n_el (see edge_lane)
+  auto body = [&](auto edge_tag) -> double {
+    constexpr bool EDGE = decltype(edge_tag)::value;
+    // every lane's (clamped) node is inside the grid: lanes 0 / 31 load too (unused values).
     // 64-bit row bases once per lane, 32-bit element offsets per row.
-    const bool computes = lane >= 1 && lane <= 30;
+    const EdgeLane e = edge_lane<EDGE>(L, i);
+    const int64_t ia = e.ia;
+    const bool computes = lane >= 1 && lane <= 30 && e.in_grid;
     const uint32_t nn32 = stride32<OpaqueStride<Ld>::value>(nn);
-    const double* __restrict__ fp = opaque(f + (n0 * nn + i));
+    const double* __restrict__ fp = opaque(f + (n0 * nn + ia));
 #pragma unroll
     for (int k = 0; k < NT; ++k) fv[k] = __ldg(fp + (uint32_t)k * nn32);
-    const typename Ld::Lane lc = ld.lane(nbase, i, wfirst, lane);
+    const typename Ld::Lane lc = ld.lane(nbase, ia, wfirst, lane);
     typename Ld::Raw raw[NT + 1];
 #pragma unroll
     for (int r = 0; r <= NT; ++r) raw[r] = ld.load(lc, r, nn32);
-    const Coefs c = load_coefs(L, i);
+    Coefs c = load_coefs(L, ia);
+    if (EDGE && e.cls == 1) c.invd = L.inv_w;
 #pragma unroll
-    for (int r = 0; r <= NT; ++r) xr[r] = ld.finish(raw[r], lc, i, c.invd);
-    double* __restrict__ yp = opaque(y + (n0 * nn + i));
+    for (int r = 0; r <= NT; ++r) xr[r] = ld.finish(raw[r], lc, ia, c.invd);
+    double* __restrict__ yp = opaque(y + (n0 * nn + ia));
     double pm = __shfl_up_sync(kFull, xr[0], 1);
     double pp = __shfl_down_sync(kFull, xr[0], 1);
 #pragma unroll
@@ -417,8 +466,8 @@ __device__ __forceinline__ double dev_lean2(const LevelView& L, const Ld& ld, co
       const double qm = __shfl_up_sync(kFull, x1, 1);
       const double qp = __shfl_down_sync(kFull, x1, 1);
       const double x0 = ADJ ? xr[k] : x1;
-      const double row = ADJ ? row_interior<true>(c, pm, xr[k], pp, qm, x1, qp)
-                             : row_interior<false>(c, qm, x1, qp, pm, xr[k], pp);
+      const double row = ADJ ? row_tile<true, EDGE>(L, e.cls, c, pm, xr[k], pp, qm, x1, qp)
+                             : row_tile<false, EDGE>(L, e.cls, c, qm, x1, qp, pm, xr[k], pp);
       const double r = fv[k] - row;
       if (NORM) acc = acc + (computes ? r * r : 0.0);  // a select: keeps the row out of the store's branch
       if (MODE != kNormOnly && computes) *(yp + (uint32_t)k * nn32) = MODE == kSweep ? x0 + omega * (r * c.invd) : r;
@@ -426,7 +475,9 @@ __device__ __forceinline__ double dev_lean2(const LevelView& L, const Ld& ld, co
       pp = qp;
     }
     return acc;
-  }
+  };
+  if (rows_in && nodes_in) return body(std::false_type{});
+  if (rows_in && L.n_el >= 2) return body(std::true_type{});
   const bool in_grid = i >= 0 && i < nn;
   const bool computes = lane >= 1 && lane <= 30 && in_grid;
 #pragma unroll
@@ -516,7 +567,10 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
                        n0 + NT - 1 < L.n_hi;
   const bool nodes_in = node1 >= 2 && node1 + 29 <= L.n_el - 1;
   double xs[NT + 2], fv[NT + 1], y1[NT + 1];
-  if (rows_in && nodes_in) {
+  // interior time tile; EDGE for the warps that hold node 0 / 1 / n_el (see edge_lane)
+  auto body = [&](auto edge_tag) {
+    constexpr bool EDGE = decltype(edge_tag)::value;
+    const EdgeLane e = edge_lane<EDGE>(L, i);
     // one 64-bit row base for x, f and y; 32-bit element offsets from it
     // (o[j] = node i on staged row sbase + j), so each access is one IMAD.WIDE
     const int64_t rowbase = sbase * nn;
@@ -525,7 +579,7 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
     double* __restrict__ yb = opaque(y + rowbase);
     const uint32_t nn32 = stride32<false>(nn);
     uint32_t o[NT + 2];
-    o[0] = (uint32_t)i;
+    o[0] = (uint32_t)e.ia;
 #pragma unroll
     for (int r = 1; r < NT + 2; ++r) o[r] = o[r - 1] + nn32;
     if (ZX) {
@@ -535,7 +589,8 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
       for (int r = 0; r < NT + 2; ++r) fs[r] = __ldg(fb + o[r]);
 #pragma unroll
       for (int r = 0; r < NT + 1; ++r) fv[r] = fs[ADJ ? r : r + 1];
-      const double idv = __ldg(L.coef + kInvD * nn + i);
+      double idv = __ldg(L.coef + kInvD * nn + e.ia);
+      if (EDGE && e.cls == 1) idv = L.inv_w;
 #pragma unroll
       for (int r = 0; r < NT + 2; ++r) xs[r] = zero_sweep(fs[r], idv, omega);
     } else {
@@ -544,19 +599,20 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
 #pragma unroll
       for (int r = 0; r < NT + 1; ++r) fv[r] = __ldg(fb + o[ADJ ? r : r + 1]);  // f rows s1base + r
     }
-    const Coefs c = load_coefs(L, i);
+    Coefs c = load_coefs(L, e.ia);
+    if (EDGE && e.cls == 1) c.invd = L.inv_w;
     auto upd = [&](double x0, double fval, double row) { return x0 + omega * ((fval - row) * c.invd); };
     double pm = __shfl_up_sync(kFull, xs[0], 1), pp = __shfl_down_sync(kFull, xs[0], 1);
 #pragma unroll
     for (int r = 0; r <= NT; ++r) {
       const double x1 = xs[r + 1];
       const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
-      if (ADJ) y1[r] = upd(xs[r], fv[r], row_interior<true>(c, pm, xs[r], pp, qm, x1, qp));
-      else y1[r] = upd(x1, fv[r], row_interior<false>(c, qm, x1, qp, pm, xs[r], pp));
+      if (ADJ) y1[r] = upd(xs[r], fv[r], row_tile<true, EDGE>(L, e.cls, c, pm, xs[r], pp, qm, x1, qp));
+      else y1[r] = upd(x1, fv[r], row_tile<false, EDGE>(L, e.cls, c, qm, x1, qp, pm, xs[r], pp));
       pm = qm;
       pp = qp;
     }
-    const bool lane2 = lane >= 2 && lane <= 29;
+    const bool lane2 = lane >= 2 && lane <= 29 && e.in_grid;
     double am = __shfl_up_sync(kFull, y1[0], 1), ap = __shfl_down_sync(kFull, y1[0], 1);
 #pragma unroll
     for (int k = 0; k < NT; ++k) {
@@ -564,14 +620,15 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
       const double bm = __shfl_up_sync(kFull, z1, 1), bp = __shfl_down_sync(kFull, z1, 1);
       // evaluated on every lane (no divergence around the shuffles); stored on
       // lanes 2..29; row n0 + k is staged row k (J^T) / k + 2 (J)
-      const double v = ADJ ? upd(y1[k], fv[k], row_interior<true>(c, am, y1[k], ap, bm, z1, bp))
-                           : upd(z1, fv[k + 1], row_interior<false>(c, bm, z1, bp, am, y1[k], ap));
+      const double v = ADJ ? upd(y1[k], fv[k], row_tile<true, EDGE>(L, e.cls, c, am, y1[k], ap, bm, z1, bp))
+                           : upd(z1, fv[k + 1], row_tile<false, EDGE>(L, e.cls, c, bm, z1, bp, am, y1[k], ap));
       if (lane2) *(yb + o[ADJ ? k : k + 2]) = v;
       am = bm;
       ap = bp;
     }
-    return;
-  }
+  };
+  if (rows_in && nodes_in) return body(std::false_type{});
+  if (rows_in && L.n_el >= 2) return body(std::true_type{});
   const bool in_grid = i >= 0 && i < nn;
   const bool lane1 = lane >= 1 && lane <= 30 && in_grid;
   const bool lane2 = lane >= 2 && lane <= 29 && in_grid;
@@ -890,20 +947,29 @@ __device__ __forceinline__ double dev_restrict2(const LevelView& F, const LevelV
                        n0 + NT - 1 < F.n_hi;
   const bool nodes_in = base >= 2 && base + 29 <= F.n_el - 1;
   double xr[NT + 1], fv[NT];
-  if (rows_in && nodes_in) {
+  // interior time tile; EDGE for the warps that hold node 0 / 1 / n_el (see edge_lane).  The
+  // x step's truncated coarse rows (I = 0 without 2I - 1, I = n_el / 2 without 2I + 1) are the
+  // interior form with the absent residual an exact zero: ((.5 0 + r) + .5 rc) + 0 is
+  // (0 + r) + (0 + .5 rc) up to the sign of a zero, which the final + 0 removes.
+  auto body = [&](auto edge_tag) -> double {
+    constexpr bool EDGE = decltype(edge_tag)::value;
+    const EdgeLane e = edge_lane<EDGE>(F, i);
+    const int64_t ia = e.ia;
+    const bool own = owns && e.in_grid;
     // 64-bit row bases once per lane, 32-bit element offsets per row
     const uint32_t nn32 = stride32<DIR == 0 || ZX>(nn), nnc32 = stride32<DIR == 0 || ZX>(nnc);
-    const double* __restrict__ fp = opaque(f + (n0 * nn + i));
+    const double* __restrict__ fp = opaque(f + (n0 * nn + ia));
 #pragma unroll
     for (int k = 0; k < NT; ++k) fv[k] = __ldg(fp + (uint32_t)k * nn32);
     double fx = 0.0;  // ZX: the one staged level outside the f rows
-    if (ZX) fx = ADJ ? __ldg(fp + (uint32_t)NT * nn32) : __ldg(opaque(f + (nbase * nn + i)));
+    if (ZX) fx = ADJ ? __ldg(fp + (uint32_t)NT * nn32) : __ldg(opaque(f + (nbase * nn + ia)));
     if (!ZX) {
-      const double* __restrict__ xp = opaque(x + (nbase * nn + i));
+      const double* __restrict__ xp = opaque(x + (nbase * nn + ia));
 #pragma unroll
       for (int r = 0; r <= NT; ++r) xr[r] = __ldg(xp + (uint32_t)r * nn32);
     }
-    const Coefs c = load_coefs(F, i);
+    Coefs c = load_coefs(F, ia);
+    if (EDGE && e.cls == 1) c.invd = F.inv_w;
     if (ZX) {
       // staged level nbase + r: f row r - 1 (J) / r (J^T)
 #pragma unroll
@@ -913,17 +979,17 @@ __device__ __forceinline__ double dev_restrict2(const LevelView& F, const LevelV
       }
     }
     if (OPEN) {
-      double* __restrict__ yb = y_open != nullptr ? opaque(y_open + (n0 * nn + i)) : nullptr;
+      double* __restrict__ yb = y_open != nullptr ? opaque(y_open + (n0 * nn + ia)) : nullptr;
 #pragma unroll
       for (int k = 0; k < NT; ++k) {
-        acc = acc + (owns ? fv[k] * fv[k] : 0.0);
-        if (owns && y_open != nullptr) *(yb + (uint32_t)k * nn32) = xr[ADJ ? k : k + 1];  // S(0) on row n0 + k
+        acc = acc + (own ? fv[k] * fv[k] : 0.0);
+        if (own && y_open != nullptr) *(yb + (uint32_t)k * nn32) = xr[ADJ ? k : k + 1];  // S(0) on row n0 + k
       }
     }
     // Output lanes and their coarse node: x step, the lanes at even fine nodes
     // i = 2I (odd lanes 3..29); t step, every computing lane (I = i).
-    const bool out = DIR == 0 ? ((lane & 1) && lane >= 3 && lane <= 29) : (lane >= 1 && lane <= 30);
-    const int64_t I = DIR == 0 ? (i >> 1) : i;
+    const bool out = (DIR == 0 ? ((lane & 1) && lane >= 3 && lane <= 29) : (lane >= 1 && lane <= 30)) && e.in_grid;
+    const int64_t I = DIR == 0 ? (ia >> 1) : ia;
     const int64_t crow = DIR == 0 ? n0 : (n0 >> 1);
     double* __restrict__ fcb = opaque(fc + (crow * nnc + I));
     double pm = __shfl_up_sync(kFull, xr[0], 1), pp = __shfl_down_sync(kFull, xr[0], 1);
@@ -932,9 +998,10 @@ __device__ __forceinline__ double dev_restrict2(const LevelView& F, const LevelV
     for (int k = 0; k < NT; ++k) {
       const double x1 = xr[k + 1];
       const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
-      const double r = fv[k] - (ADJ ? row_interior<true>(c, pm, xr[k], pp, qm, x1, qp)
-                                    : row_interior<false>(c, qm, x1, qp, pm, xr[k], pp));
+      double r = fv[k] - (ADJ ? row_tile<true, EDGE>(F, e.cls, c, pm, xr[k], pp, qm, x1, qp)
+                              : row_tile<false, EDGE>(F, e.cls, c, qm, x1, qp, pm, xr[k], pp));
       if (DIR == 0) {
+        if (EDGE && !e.in_grid) r = 0.0;  // the absent neighbour of a truncated coarse row
         // fine nodes 2I - 1, 2I, 2I + 1 are lanes l - 1, l, l + 1 of output lane l;
         // canonical ((0 + .5 ra) + (0 + rb)) + ((0 + .5 rc) + 0), folded (see row_interior)
         const double ra = __shfl_up_sync(kFull, r, 1);
@@ -953,7 +1020,9 @@ __device__ __forceinline__ double dev_restrict2(const LevelView& F, const LevelV
       pp = qp;
     }
     return acc;
-  }
+  };
+  if (rows_in && nodes_in) return body(std::false_type{});
+  if (rows_in && F.n_el >= 2 && (DIR == 1 || (F.n_el & 1) == 0)) return body(std::true_type{});
   const bool in_grid = i >= 0 && i < nn;
   const bool computes = lane >= 1 && lane <= 30 && in_grid;
 #pragma unroll
