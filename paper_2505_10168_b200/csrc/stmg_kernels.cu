@@ -741,28 +741,33 @@ __device__ __forceinline__ double dev_up(const LevelView& L, const Ld& ld, const
   const bool nodes_in = node1 >= 2 && node1 + 29 <= L.n_el - 1;
   double xs[NT + 2], fv[NT + 1], y1[NT + 1];
   double acc = 0.0;
-  if (rows_in && nodes_in) {
+  // interior time tile; EDGE for the warps that hold node 0 / 1 / n_el (see edge_lane)
+  auto body = [&](auto edge_tag) -> double {
+    constexpr bool EDGE = decltype(edge_tag)::value;
+    const EdgeLane e = edge_lane<EDGE>(L, i);
+    const int64_t ia = e.ia;
     const uint32_t nn32 = stride32<false>(nn);
-    const double* __restrict__ fb = opaque(f + (s1base * nn + i));
+    const double* __restrict__ fb = opaque(f + (s1base * nn + ia));
 #pragma unroll
     for (int r = 0; r < NT + 1; ++r) fv[r] = __ldg(fb + (uint32_t)r * nn32);  // f rows s1base + r
-    const typename Ld::Lane lc = ld.lane(sbase, i, node1 - 1, lane);
+    const typename Ld::Lane lc = ld.lane(sbase, ia, node1 - 1, lane);
     typename Ld::Raw raw[NT + 2];
 #pragma unroll
     for (int r = 0; r < NT + 2; ++r) raw[r] = ld.load(lc, r, nn32);
-    const Coefs c = load_coefs(L, i);
+    Coefs c = load_coefs(L, ia);
+    if (EDGE && e.cls == 1) c.invd = L.inv_w;
 #pragma unroll
-    for (int r = 0; r < NT + 2; ++r) xs[r] = ld.finish(raw[r], lc, i, c.invd);
-    double* __restrict__ ub = opaque(u_out + (s1base * nn + i));
-    double* __restrict__ wb = opaque(w_out + (n0 * nn + i));
-    const bool lane2 = lane >= 2 && lane <= 29;
+    for (int r = 0; r < NT + 2; ++r) xs[r] = ld.finish(raw[r], lc, ia, c.invd);
+    double* __restrict__ ub = opaque(u_out + (s1base * nn + ia));
+    double* __restrict__ wb = opaque(w_out + (n0 * nn + ia));
+    const bool lane2 = lane >= 2 && lane <= 29 && e.in_grid;
     double pm = __shfl_up_sync(kFull, xs[0], 1), pp = __shfl_down_sync(kFull, xs[0], 1);
 #pragma unroll
     for (int r = 0; r <= NT; ++r) {
       const double x1 = xs[r + 1];
       const double qm = __shfl_up_sync(kFull, x1, 1), qp = __shfl_down_sync(kFull, x1, 1);
-      if (ADJ) y1[r] = xs[r] + omega * ((fv[r] - row_interior<true>(c, pm, xs[r], pp, qm, x1, qp)) * c.invd);
-      else y1[r] = x1 + omega * ((fv[r] - row_interior<false>(c, qm, x1, qp, pm, xs[r], pp)) * c.invd);
+      if (ADJ) y1[r] = xs[r] + omega * ((fv[r] - row_tile<true, EDGE>(L, e.cls, c, pm, xs[r], pp, qm, x1, qp)) * c.invd);
+      else y1[r] = x1 + omega * ((fv[r] - row_tile<false, EDGE>(L, e.cls, c, qm, x1, qp, pm, xs[r], pp)) * c.invd);
       const bool own_row = ADJ ? r < NT : r >= 1;  // rows n0 .. n0 + NT - 1 (compile-time per r)
       if (own_row && lane2) *(ub + (uint32_t)r * nn32) = y1[r];
       pm = qm;
@@ -773,8 +778,8 @@ __device__ __forceinline__ double dev_up(const LevelView& L, const Ld& ld, const
     for (int k = 0; k < NT; ++k) {
       const double z1 = y1[k + 1];
       const double bm = __shfl_up_sync(kFull, z1, 1), bp = __shfl_down_sync(kFull, z1, 1);
-      const double res = ADJ ? fv[k] - row_interior<true>(c, am, y1[k], ap, bm, z1, bp)
-                             : fv[k + 1] - row_interior<false>(c, bm, z1, bp, am, y1[k], ap);
+      const double res = ADJ ? fv[k] - row_tile<true, EDGE>(L, e.cls, c, am, y1[k], ap, bm, z1, bp)
+                             : fv[k + 1] - row_tile<false, EDGE>(L, e.cls, c, bm, z1, bp, am, y1[k], ap);
       const double x0 = ADJ ? y1[k] : z1;
       // the squared residual is summed by a select on every lane: the row evaluation then
       // cannot be sunk into the divergent branch around the store (BSSY / BRA / BSYNC and
@@ -785,7 +790,9 @@ __device__ __forceinline__ double dev_up(const LevelView& L, const Ld& ld, const
       ap = bp;
     }
     return acc;
-  }
+  };
+  if (rows_in && nodes_in) return body(std::false_type{});
+  if (rows_in && L.n_el >= 2) return body(std::true_type{});
   // ---- general path (boundary tiles): per-row-class evaluation
   const bool in_grid = i >= 0 && i < nn;
   const bool lane1 = lane >= 1 && lane <= 30 && in_grid;
