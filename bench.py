@@ -15,8 +15,12 @@ after the same V-cycles (3 at full size).  A step is one such solve.
   stream, max over ranks.  Inputs exceed L2 (3 x 8.6 GB), so no flush is needed.
 * `e2e`: the same solve through the C ABI with pinned HOST b and u: h2d of b and d2h
   of u inside the timed region (stmg_mg_solve_ex with STMG_SOLVE_ZERO_GUESS: the
-  workload starts from u = 0, so u is output only); `e2e.inout_u` is the reference
-  signature's in/out u (u uploaded too).
+  workload starts from u = 0, so u is output only).  `e2e.value` is the throughput of a
+  stream of such solves on one hierarchy (stmg_mg_solve_stream: every step uploads its b
+  and downloads its u, step k's copies overlap its neighbours' solves; fill and drain
+  timed) -- the figure the reference arm's batch of concurrent CPU solves compares
+  with; `e2e.single` is one solve alone (upload + solve + download in sequence) and
+  `e2e.inout_u` the reference signature's in/out u (u uploaded too).
 * `roofline`: the level-0 kernel with the largest share of the profiled solves
   (in-graph CUDA events), algorithmic bytes per launch / its launch time.
 * `cpu_baseline`: the compiled reference (oracle/_ref) on one host core, on a
@@ -537,6 +541,8 @@ def main():
     ap.add_argument("--n-el", type=int, default=None)
     ap.add_argument("--n-t", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--e2e-stream-steps", type=int, default=8,
+                    help="solves in the streamed e2e measurement (0/1: skip; e2e.value is then the one-solve figure)")
     ap.add_argument("--cpu-sample-nt", type=int, default=512)
     ap.add_argument("--ref-cores", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -743,6 +749,32 @@ def main():
         else:
             e2e = {"value": v_io, "unit": UNIT, "h2d_bytes_per_step": 16 * nbytes,
                    "d2h_bytes_per_step": 8 * nbytes, "solve_seconds": s_io}
+        # A stream of solves through stmg_mg_solve_stream (one hierarchy, host vectors): every
+        # step still uploads its b and downloads its u, but step k's copies overlap its
+        # neighbours' solves.  This is the throughput figure the reference arm's batch of
+        # concurrent CPU solves compares with; the one-solve latency stays in e2e.single.
+        if h is not None and world == 1 and args.e2e_stream_steps > 1:
+            K = args.e2e_stream_steps
+            S.mg_solve_stream(h, [bh] * 2, [uh] * 2, opts, zero_guess=True)  # slots + graphs (untimed)
+            torch.cuda.synchronize(dev)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            e0.record(stream)
+            rs = S.mg_solve_stream(h, [bh] * K, [uh] * K, opts, zero_guess=True)
+            e1.record(stream)
+            e1.synchronize()
+            wall = time.perf_counter() - t0
+            ms = e0.elapsed_time(e1)
+            h.release_staging()
+            single = {k_: e2e[k_] for k_ in ("value", "solve_seconds")}
+            e2e.update({
+                "value": sum(r.smoother_dof_updates for r in rs) / (ms * 1e-3),
+                "solve_seconds": ms * 1e-3 / K, "wall_seconds_per_step": wall / K, "steps": K,
+                "mode": f"stream of {K} solves on one hierarchy (stmg_mg_solve_stream): each step uploads its b "
+                        "from pinned host memory and downloads its u; the copies of steps k - 1 / k + 1 overlap "
+                        "solve k (two device slots); pipeline fill and drain are inside the timed region",
+                "single": single})
 
     cpu = None
     dev_bytes = h.device_bytes() if h is not None else dh.device_bytes

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define STMG_ABI_VERSION 3
+#define STMG_ABI_VERSION 4
 
 enum stmg_status_code {
   STMG_OK = 0,
@@ -245,6 +245,23 @@ int stmg_mg_solve_ex(stmg_hierarchy* h, const double* b, double* u, const stmg_s
 int stmg_mg_solve_batch(int32_t count, stmg_hierarchy* const* hs, const double* const* bs, double* const* us,
                         const stmg_solve_options* opts, stmg_solve_report* reports, double* const* histories,
                         int32_t history_cap);
+
+/* A stream of solves on ONE hierarchy with HOST vectors (many right-hand sides on one
+ * operator: the load cases of an experiment sweep, proj/src/experiments.cpp, whose
+ * solves share the hierarchy).  Entry k is stmg_mg_solve_ex(h, bs[k], us[k], opts, flags,
+ * &reports[k], histories[k], history_cap), run in order, bit-identical results; the
+ * host<->device copies are software-pipelined over two device (b, u) slots: b_{k+1}
+ * (and u_{k+1} unless STMG_SOLVE_ZERO_GUESS) uploads and u_{k-1} downloads while solve k
+ * runs, so an entry costs max(upload, solve, download) instead of their sum (config 2 on
+ * PCIe 5: ~0.16 s instead of ~0.37 s).  The overlap needs page-locked host vectors
+ * (cudaHostAlloc / cudaHostRegister); pageable ones work but copy synchronously.  No
+ * b may alias a u.  The slots (4 level-0 vectors of device memory) are kept for the next
+ * call; stmg_hierarchy_release_staging frees them.  With count == 1 or any device
+ * pointer among the entries this is the plain sequence of stmg_mg_solve_ex calls. */
+int stmg_mg_solve_stream(stmg_hierarchy* h, int32_t count, const double* const* bs, double* const* us,
+                         const stmg_solve_options* opts, int32_t flags, stmg_solve_report* reports,
+                         double* const* histories, int32_t history_cap);
+int stmg_hierarchy_release_staging(stmg_hierarchy* h);
 
 /* ---- level kernels on device vectors (parity tests, profiling) ------------------- */
 /* `sweeps` damped-Jacobi sweeps in place (csr_residual + jacobi_update). */

@@ -387,6 +387,9 @@ struct Workspace {
   // iterate alternates between two buffers from cycle to cycle): [0] in, [1] out
   std::unique_ptr<DeviceBuf> ptrs;
   std::unique_ptr<DeviceBuf> xz;  // third level-0 iterate buffer (fine up-pass), allocated on first use
+  // stmg_mg_solve_stream: two (b, u) device slots, allocated on first use and kept (the cycle
+  // graphs are cached per bound pointer pair); stmg_hierarchy_release_staging frees them
+  std::unique_ptr<DeviceBuf> stage_b[2], stage_u[2];
   ~Workspace() {
     if (pinned) cudaFreeHost(pinned);
     if (loop_host) cudaFreeHost(loop_host);
@@ -2288,6 +2291,106 @@ int stmg_mg_solve_batch(int32_t count, stmg_hierarchy* const* hs, const double* 
         default: throw std::runtime_error(m);
       }
     }
+  });
+}
+
+namespace {
+struct StreamRaii {
+  cudaStream_t s = nullptr;
+  StreamRaii() { cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate"); }
+  ~StreamRaii() {
+    if (s) cudaStreamDestroy(s);
+  }
+};
+struct EventRaii {
+  cudaEvent_t e = nullptr;
+  EventRaii() { cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate"); }
+  ~EventRaii() {
+    if (e) cudaEventDestroy(e);
+  }
+};
+}  // namespace
+
+// A sequence of solves on one hierarchy with host vectors, software-pipelined over two
+// device (b, u) slots: while solve k runs on the hierarchy's stream, b_{k+1} (and u_{k+1}
+// for a warm start) uploads on a second stream and u_{k-1} downloads on a third, so a
+// stream of solves costs max(upload, solve, download) per entry instead of their sum.
+// Each solve binds its slot in place, i.e. it is exactly stmg_mg_solve_ex on device
+// vectors: the same kernels in the same order, bit-identical results.
+int stmg_mg_solve_stream(stmg_hierarchy* h, int32_t count, const double* const* bs, double* const* us,
+                         const stmg_solve_options* opts, int32_t flags, stmg_solve_report* reports,
+                         double* const* histories, int32_t history_cap) {
+  return guarded([&] {
+    checked(h);
+    if (count < 0 || !opts) throw std::invalid_argument("mg_solve_stream: bad arguments");
+    if (count == 0) return;
+    if (!bs || !us || !reports || !histories) throw std::invalid_argument("mg_solve_stream: null argument");
+    if (flags & ~STMG_SOLVE_ZERO_GUESS) throw std::invalid_argument("mg_solve_stream: unknown flags");
+    bool staged = count > 1;
+    for (int32_t k = 0; k < count; ++k) {
+      if (!bs[k] || !us[k] || !histories[k]) throw std::invalid_argument("mg_solve_stream: null entry");
+      int dev = -1;
+      if (is_device_ptr(bs[k], &dev) || is_device_ptr(us[k], &dev)) staged = false;  // nothing to overlap
+    }
+    if (!staged) {
+      for (int32_t k = 0; k < count; ++k) solve(h, bs[k], us[k], *opts, &reports[k], histories[k], history_cap, flags);
+      return;
+    }
+    Nvtx range("stmg::mg_solve_stream");
+    DeviceGuard dg(h->device);
+    Workspace& ws = *h->ws;
+    const int64_t n = h->ndofs(0);
+    const size_t bytes = sizeof(double) * static_cast<size_t>(n);
+    const bool zero_guess = (flags & STMG_SOLVE_ZERO_GUESS) != 0;
+    for (int s = 0; s < 2; ++s) {
+      if (!ws.stage_b[s]) ws.stage_b[s] = std::make_unique<DeviceBuf>(n);
+      if (!ws.stage_u[s]) ws.stage_u[s] = std::make_unique<DeviceBuf>(n);
+    }
+    StreamRaii up, down;
+    EventRaii ev_up[2], ev_down[2];
+    // upload entry k into slot k & 1: the slot's b was last read by solve k - 2 (finished:
+    // solves are host-synchronous); its u may still be downloading (ev_down)
+    auto upload = [&](int32_t k) {
+      const int s = k & 1;
+      if (!zero_guess) {
+        if (k >= 2) cuda_check(cudaStreamWaitEvent(up.s, ev_down[s].e, 0), "wait");
+        cuda_check(cudaMemcpyAsync(ws.stage_u[s]->p, us[k], bytes, cudaMemcpyHostToDevice, up.s), "u upload");
+      }
+      cuda_check(cudaMemcpyAsync(ws.stage_b[s]->p, bs[k], bytes, cudaMemcpyHostToDevice, up.s), "b upload");
+      cuda_check(cudaEventRecord(ev_up[s].e, up.s), "event");
+    };
+    try {
+      upload(0);
+      for (int32_t k = 0; k < count; ++k) {
+        const int s = k & 1;
+        if (k + 1 < count) upload(k + 1);
+        cuda_check(cudaStreamWaitEvent(h->stream, ev_up[s].e, 0), "wait");
+        if (k >= 2) cuda_check(cudaStreamWaitEvent(h->stream, ev_down[s].e, 0), "wait");  // u_{k-2} has left the slot
+        solve(h, ws.stage_b[s]->p, ws.stage_u[s]->p, *opts, &reports[k], histories[k], history_cap, flags);
+        // the solve returned after its stream drained: the slot's u is final
+        cuda_check(cudaMemcpyAsync(us[k], ws.stage_u[s]->p, bytes, cudaMemcpyDeviceToHost, down.s), "u download");
+        cuda_check(cudaEventRecord(ev_down[s].e, down.s), "event");
+      }
+      cuda_check(cudaStreamSynchronize(down.s), "stream sync");
+    } catch (...) {
+      cudaStreamSynchronize(up.s);  // no copy may outlive the caller's buffers
+      cudaStreamSynchronize(down.s);
+      throw;
+    }
+  });
+}
+
+int stmg_hierarchy_release_staging(stmg_hierarchy* h) {
+  return guarded([&] {
+    checked(h);
+    DeviceGuard dg(h->device);
+    cuda_check(cudaStreamSynchronize(h->stream), "stream sync");
+    for (int s = 0; s < 2; ++s) {
+      h->ws->stage_b[s].reset();
+      h->ws->stage_u[s].reset();
+    }
+    for (auto& kv : h->graphs) destroy_graph_entry(kv.second);  // cycle graphs bound to the freed slots
+    h->graphs.clear();
   });
 }
 

@@ -42,7 +42,7 @@ class StmgCudaError(RuntimeError):
     pass
 
 
-ABI_VERSION = 3  # include/stmg_b200.h STMG_ABI_VERSION (stmg_solve_report layout)
+ABI_VERSION = 4  # include/stmg_b200.h STMG_ABI_VERSION (stmg_solve_report layout)
 
 
 def _load():
@@ -77,6 +77,8 @@ def _load():
         "stmg_mg_solve": [vp, vp, vp, vp, vp, vp, i32],
         "stmg_mg_solve_ex": [vp, vp, vp, vp, i32, vp, vp, i32],
         "stmg_mg_solve_batch": [i32, vp, vp, vp, vp, vp, vp, i32],
+        "stmg_mg_solve_stream": [vp, i32, vp, vp, vp, i32, vp, vp, i32],
+        "stmg_hierarchy_release_staging": [vp],
         "stmg_level_sweeps": [vp, i32, vp, vp, i32, f64],
         "stmg_level_residual": [vp, i32, vp, vp, vp],
         "stmg_level_sweep_kernels": [vp, i32, vp, vp, vp, i32, i32, f64],
@@ -512,6 +514,10 @@ class LevelHierarchy:
         _check(_lib.stmg_hierarchy_device_bytes(self._h, C.byref(b)))
         return b.value
 
+    def release_staging(self) -> None:
+        """Free the device (b, u) slots mg_solve_stream keeps between calls."""
+        _check(_lib.stmg_hierarchy_release_staging(self._h))
+
     def level_coeffs(self, l: int) -> dict:
         nn = self.levels[l].n_el + 1
         arrs = [np.zeros(nn) for _ in range(7)]
@@ -720,6 +726,36 @@ def mg_solve_batch(hs: Sequence[LevelHierarchy], bs, us, opts: Optional[SolveOpt
     U = (C.c_void_p * max(k, 1))(*[_ptr(u) for u in us])
     P = (C.c_void_p * max(k, 1))(*[hist[i].ctypes.data for i in range(k)])
     _check(_lib.stmg_mg_solve_batch(k, H, B, U, C.byref(co), reps, P, cap))
+    out = []
+    for i in range(k):
+        r = reps[i]
+        out.append(SolveReport(SolveStatus(r.status), r.cycles, r.factor, [float(v) for v in hist[i, : r.n_history]],
+                               bool(r.absolute_norms), r.seconds, r.device_seconds, r.smoother_dof_updates,
+                               r.kernel_launches))
+    return out
+
+
+def mg_solve_stream(h: LevelHierarchy, bs, us, opts: Optional[SolveOptions] = None, zero_guess: bool = False) -> list:
+    """A stream of solves on one hierarchy with host vectors (stmg_mg_solve_stream):
+    entry k is mg_solve(h, bs[k], us[k], opts, zero_guess), in order, bit-identical; the
+    upload of entry k + 1 and the download of entry k - 1 overlap solve k (pinned host
+    vectors).  h.release_staging() frees the two device (b, u) slots it keeps."""
+    o = opts or SolveOptions()
+    k = len(bs)
+    if len(us) != k:
+        raise ValueError("mg_solve_stream: bs and us differ in length")
+    n = h.levels[0].n_dofs
+    for b, u in zip(bs, us):
+        if _numel(b) != n or _numel(u) != n:
+            raise ValueError("mg_solve_stream: vector size mismatch")
+    cap = max(o.max_cycles, 0) + 1
+    hist = np.zeros((max(k, 1), cap), np.float64)
+    reps = (_SolveRep * max(k, 1))()
+    co = _SolveOpts(int(o.nu), float(o.omega), float(o.tol), float(o.div_tol), int(o.max_cycles))
+    B = (C.c_void_p * max(k, 1))(*[_ptr(b) for b in bs])
+    U = (C.c_void_p * max(k, 1))(*[_ptr(u) for u in us])
+    P = (C.c_void_p * max(k, 1))(*[hist[i].ctypes.data for i in range(k)])
+    _check(_lib.stmg_mg_solve_stream(h.handle, k, B, U, C.byref(co), 1 if zero_guess else 0, reps, P, cap))
     out = []
     for i in range(k):
         r = reps[i]

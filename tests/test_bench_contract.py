@@ -52,6 +52,9 @@ def test_gpu_arm_contract():
     assert d["e2e"]["d2h_bytes_per_step"] == 8 * d["config"]["dofs"]
     assert d["e2e"]["inout_u"]["h2d_bytes_per_step"] == 16 * d["config"]["dofs"]
     assert d["e2e"]["value"] > d["e2e"]["inout_u"]["value"] > 0
+    # streamed e2e (copies overlap the neighbouring solves) with the one-solve figure beside it
+    assert d["e2e"]["steps"] >= 2 and "stmg_mg_solve_stream" in d["e2e"]["mode"]
+    assert d["e2e"]["value"] >= 0.9 * d["e2e"]["single"]["value"] > d["e2e"]["inout_u"]["value"]
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.5
     assert "sm_mhz" in d["clocks"]
