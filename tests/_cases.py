@@ -115,6 +115,14 @@ def case(name: str) -> Case:
                        adjoint=name.endswith("_adj"))
         cc.dirs = np.asarray([0, 0], np.int32)
         return cc
+    if name.startswith("edge_"):  # edge_<x|t>_<n_el>[_adj]: see EDGE_CASES
+        parts = name.split("_")
+        ne, adjoint = int(parts[2]), parts[-1] == "adj"
+        cc = _from_cfg(name, C.cfg2(n_el=ne, n_t=48, min_elements=0), n_levels=2, nu=2, adjoint=adjoint,
+                       method="CK")
+        cc.dirs = np.asarray([0 if parts[1] == "x" else 1], np.int32)
+        cc.max_cycles = 20
+        return cc
     if name in GENERAL:
         kind, ne, nt, method, dirs, adjoint, nu = GENERAL[name]
         if kind == "cfg1":
@@ -152,6 +160,15 @@ GENERAL = {
 }
 GENERAL_CASES = list(GENERAL)
 
+
+# Widths that put node n_el on every lane class of a row's last warp (warps advance 28 or
+# 30 nodes, 26 in the fused down-pass) and make the first warp also the last: the edge-warp
+# tile bodies (csrc/stmg_kernels.cu edge_lane / row_tile).  48 time steps give interior
+# 8-level time tiles; x steps need an even n_el, odd widths take the causal t step.
+EDGE_CASES = ([f"edge_x_{ne}" + ("_adj" if k % 2 else "") for k, ne in
+               enumerate([2, 4, 6, 26, 28, 30, 32, 54, 56, 58, 60, 62, 84, 86, 88, 90])] +
+              [f"edge_t_{ne}" + ("" if k % 2 else "_adj") for k, ne in
+               enumerate([2, 3, 5, 27, 29, 30, 31, 33, 55, 57, 59, 61, 85, 87, 89, 91])])
 
 SMALL_CASES = ["cfg0", "cfg0_deep", "cfg1_mini", "cfg1_mini_adj", "cfg2_mini", "cfg3_mini", "cfgD",
                "cfgK_contrast", "time_first", "space_first", "single_level", "tiny", "wide_short",

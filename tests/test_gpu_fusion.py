@@ -14,7 +14,7 @@ bit-identical to solves with every fusion off.
 import numpy as np
 import pytest
 
-from tests._cases import SMALL_CASES, case
+from tests._cases import EDGE_CASES, SMALL_CASES, case
 from tests.test_gpu_parity import bits, check_solve, gpu_hier, port_hier, special_values
 
 pytestmark = pytest.mark.gpu
@@ -41,7 +41,7 @@ def S(torch):
 
 @pytest.mark.parametrize("tiles", [0, 8])
 @pytest.mark.parametrize("omega", [0.5, 0.6])
-@pytest.mark.parametrize("name", KERNEL_CASES)
+@pytest.mark.parametrize("name", KERNEL_CASES + EDGE_CASES)
 def test_virtual_zero_kernels_bitwise(torch, S, port, name, omega, tiles):
     """tiles = 8 forces the large-level tiling (8-level tiles; 16-level tiles for the
     x-step restriction of a virtual zero iterate) onto every level."""
@@ -145,7 +145,7 @@ def test_fine_down_kernel_bitwise(torch, S, port, name, tiles):
 
 
 @pytest.mark.parametrize("tiles", [8, 4, 2])
-@pytest.mark.parametrize("name", KERNEL_CASES + ["cfg0", "tiny"])
+@pytest.mark.parametrize("name", KERNEL_CASES + ["cfg0", "tiny"] + EDGE_CASES)
 def test_fine_up_kernel_bitwise(torch, S, port, name, tiles):
     """k_up: u = S(x + P x_c), w = S(u) and ||f - J u||^2 in one pass, against the
     oracle's separate prolongation, sweeps and residual; every level with a per-node

@@ -8,7 +8,7 @@ floor of evaluating b - J u), and fields within 1e-10 relative max-norm.
 import numpy as np
 import pytest
 
-from tests._cases import SMALL_CASES, case
+from tests._cases import EDGE_CASES, SMALL_CASES, case
 
 pytestmark = pytest.mark.gpu
 
@@ -63,7 +63,7 @@ def special_values(rng, n):
 
 
 @pytest.mark.parametrize("tiles", [0, 8])
-@pytest.mark.parametrize("name", SMALL_CASES)
+@pytest.mark.parametrize("name", SMALL_CASES + EDGE_CASES)
 def test_level_kernels_bitwise(torch, S, port, name, tiles):
     """tiles = 8 forces the large-level tiling (8-level tiles, 16-level tiles for the
     x-step restrictions) onto every level of the small cases."""
@@ -295,7 +295,7 @@ def test_adjoint_shares_workspace_with_primal(torch, S, port):
         check_solve(rep, lam, *reversed(hp_adj.solve(c, nu=2, tol=1e-10, max_cycles=20)))
 
 
-@pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "wide_short", "cfg0_deep"])
+@pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "wide_short", "cfg0_deep"] + EDGE_CASES[::3])
 def test_sweep_kernel_forms_bitwise(torch, S, port, name):
     """Single-sweep and fused two-sweep kernels, launched back to back."""
     cs = case(name)
@@ -315,7 +315,7 @@ def test_sweep_kernel_forms_bitwise(torch, S, port, name):
 
 
 @pytest.mark.parametrize("tiles", [4, 2])
-@pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "time_first", "wide_short", "cfg0_deep"])
+@pytest.mark.parametrize("name", ["cfg1_mini", "cfg1_mini_adj", "time_first", "wide_short", "cfg0_deep"] + EDGE_CASES)
 def test_short_time_tiles_bitwise(torch, S, port, name, tiles):
     """4-level and 2-level time tiles (stmg_hierarchy_set_tiling), used on small
     latency-bound levels, on every level: kernels bit-identical to the oracle,
