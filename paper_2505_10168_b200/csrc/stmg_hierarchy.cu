@@ -1296,9 +1296,7 @@ int64_t emit_norm(stmg_hierarchy* h, int nu, const double* f, const double* x, d
 }
 
 double fetch_scalars(stmg_hierarchy* h, int count, double* out) {
-  cuda_check(cudaMemcpyAsync(h->ws->pinned, h->ws->scalars->p, sizeof(double) * count,
-                             cudaMemcpyDeviceToHost, h->stream),
-             "scalar d2h");
+  launch_check(launch_peek(h->ws->pinned, h->ws->scalars->p, count, h->stream), "scalar read-back");
   cuda_check(cudaStreamSynchronize(h->stream), "stream sync");
   for (int i = 0; i < count; ++i) out[i] = h->ws->pinned[i];
   return out[0];
@@ -1410,8 +1408,10 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
       h->device_bytes += 8 * (n + kVecPad);
     }
     double* tab[2] = {Y, ws.xz->p};
-    std::memcpy(ws.pinned + 4, tab, sizeof(tab));
-    cuda_check(cudaMemcpyAsync(ws.ptrs->p, ws.pinned + 4, sizeof(tab), cudaMemcpyHostToDevice, h->stream), "ptrs");
+    PokeWords w{};
+    static_assert(sizeof(tab) == 2 * sizeof(double), "pointer table travels as two words");
+    std::memcpy(w.v, tab, sizeof(tab));
+    launch_check(launch_poke(ws.ptrs->p, w, 2, h->stream), "ptrs");
   }
   cudaGraphExec_t loop = nullptr;
   if (r0 >= o.tol && o.max_cycles > (open_r ? 1 : 0) && o.max_cycles <= kLoopHistory && !h->profiling)
@@ -1500,12 +1500,14 @@ void solve(stmg_hierarchy* h, const double* b, double* u, const stmg_solve_optio
       // the remaining cycle loop on the device: one launch, one read-back
       auto* ctl = reinterpret_cast<SolveLoopCtl*>(ws.loop_host);
       *ctl = SolveLoopCtl{o.tol, o.div_tol, o.max_cycles, done, STMG_MAX_CYCLES, 0};
-      cuda_check(cudaMemcpyAsync(ws.loop->p, ws.loop_host, sizeof(SolveLoopCtl), cudaMemcpyHostToDevice, h->stream),
-                 "loop ctl");
+      PokeWords w{};
+      static_assert(sizeof(SolveLoopCtl) <= sizeof(w.v) && sizeof(SolveLoopCtl) % sizeof(double) == 0, "ctl words");
+      std::memcpy(w.v, ctl, sizeof(SolveLoopCtl));
+      launch_check(launch_poke(ws.loop->p, w, static_cast<int>(kLoopCtlDoubles), h->stream), "loop ctl");
       cuda_check(cudaGraphLaunch(loop, h->stream), "loop graph launch");
-      cuda_check(cudaMemcpyAsync(ws.loop_host, ws.loop->p, sizeof(double) * (kLoopCtlDoubles + o.max_cycles + 1),
-                                 cudaMemcpyDeviceToHost, h->stream),
-                 "loop read-back");
+      launch_check(launch_peek(ws.loop_host, ws.loop->p, static_cast<int>(kLoopCtlDoubles + o.max_cycles + 1),
+                               h->stream),
+                   "loop read-back");
       cuda_check(cudaStreamSynchronize(h->stream), "stream sync");
       const double* dh = ws.loop_host + kLoopCtlDoubles;
       for (int c = done + 1; c <= ctl->cycles; ++c) history[nh++] = dh[c];
@@ -2311,6 +2313,30 @@ struct EventRaii {
 };
 }  // namespace
 
+// The copy engines serve their queues one operation at a time, so any copy-engine operation
+// of the solve itself would wait behind a whole 8.6 GB vector of a neighbouring entry, and
+// the solve with it (measured with the solve's pointer table / loop control / read-back as
+// cudaMemcpyAsync: 0.27 s per entry, the solve started only after the next upload).  The
+// solve's small transfers are kernels now (launch_poke / launch_peek: 0.22 s per entry, the
+// PCIe duplex bound); the vectors still go in pieces so that other small copies on the
+// device (a caller's, another hierarchy's) are not held up either.  No bandwidth loss down to
+// 8 MiB pieces (profiles/pcie_duplex.cu), but very small pieces fill the stream's launch queue.
+size_t stream_chunk_bytes() {  // STMG_STREAM_CHUNK_MIB (0: whole vectors); default 64
+  static const size_t v = [] {
+    const char* e = std::getenv("STMG_STREAM_CHUNK_MIB");
+    const long mib = e ? std::atol(e) : 64;
+    return mib > 0 ? static_cast<size_t>(mib) << 20 : ~size_t(0);
+  }();
+  return v;
+}
+void copy_chunked(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s, const char* what) {
+  const size_t chunk = stream_chunk_bytes();
+  for (size_t o = 0; o < bytes; o += std::min(chunk, bytes - o))
+    cuda_check(cudaMemcpyAsync(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                               std::min(chunk, bytes - o), kind, s),
+               what);
+}
+
 // A sequence of solves on one hierarchy with host vectors, software-pipelined over two
 // device (b, u) slots: while solve k runs on the hierarchy's stream, b_{k+1} (and u_{k+1}
 // for a warm start) uploads on a second stream and u_{k-1} downloads on a third, so a
@@ -2354,9 +2380,9 @@ int stmg_mg_solve_stream(stmg_hierarchy* h, int32_t count, const double* const* 
       const int s = k & 1;
       if (!zero_guess) {
         if (k >= 2) cuda_check(cudaStreamWaitEvent(up.s, ev_down[s].e, 0), "wait");
-        cuda_check(cudaMemcpyAsync(ws.stage_u[s]->p, us[k], bytes, cudaMemcpyHostToDevice, up.s), "u upload");
+        copy_chunked(ws.stage_u[s]->p, us[k], bytes, cudaMemcpyHostToDevice, up.s, "u upload");
       }
-      cuda_check(cudaMemcpyAsync(ws.stage_b[s]->p, bs[k], bytes, cudaMemcpyHostToDevice, up.s), "b upload");
+      copy_chunked(ws.stage_b[s]->p, bs[k], bytes, cudaMemcpyHostToDevice, up.s, "b upload");
       cuda_check(cudaEventRecord(ev_up[s].e, up.s), "event");
     };
     try {
@@ -2368,7 +2394,7 @@ int stmg_mg_solve_stream(stmg_hierarchy* h, int32_t count, const double* const* 
         if (k >= 2) cuda_check(cudaStreamWaitEvent(h->stream, ev_down[s].e, 0), "wait");  // u_{k-2} has left the slot
         solve(h, ws.stage_b[s]->p, ws.stage_u[s]->p, *opts, &reports[k], histories[k], history_cap, flags);
         // the solve returned after its stream drained: the slot's u is final
-        cuda_check(cudaMemcpyAsync(us[k], ws.stage_u[s]->p, bytes, cudaMemcpyDeviceToHost, down.s), "u download");
+        copy_chunked(us[k], ws.stage_u[s]->p, bytes, cudaMemcpyDeviceToHost, down.s, "u download");
         cuda_check(cudaEventRecord(ev_down[s].e, down.s), "event");
       }
       cuda_check(cudaStreamSynchronize(down.s), "stream sync");

@@ -206,6 +206,14 @@ int launch_restrict_open(bool adjoint, const LevelView& F, const LevelView& C, i
 int64_t restrict_open_partials_needed(const LevelView& F, const LevelView& C, int dir);
 // p[0] <-> p[1] (device-resident buffer pointers of the fine up-pass)
 int launch_swap_ptrs(double** p, cudaStream_t s);
+// dst[0 .. count) = w.v[0 .. count) (values passed as kernel arguments, no copy engine)
+constexpr int kPokeWords = 8;
+struct PokeWords {
+  double v[kPokeWords];
+};
+int launch_poke(double* dst, const PokeWords& w, int count, cudaStream_t s);
+// host_dst[0 .. count) = src[0 .. count): host_dst is page-locked host memory, written by the device
+int launch_peek(double* host_dst, const double* src, int count, cudaStream_t s);
 // Level-0 down-pass of a V(1,1) cycle in one pass: block partials of
 // ||f - J x||^2, y = S(x), fc = R (f - J y) and, if xc0 != nullptr, the coarse
 // first sweep from zero (bitwise the separate sweep / restriction kernels).

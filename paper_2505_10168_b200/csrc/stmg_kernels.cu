@@ -2395,6 +2395,34 @@ int launch_swap_ptrs(double** p, cudaStream_t s) {
   return check_launch();
 }
 
+// Small host <-> device transfers of a solve as kernels instead of copy-engine
+// operations: values up travel as kernel arguments, values down are stored to page-locked
+// host memory (device-addressable under unified addressing).  A copy-engine operation
+// queues behind whatever large transfer another stream has in flight (the neighbouring
+// entries of stmg_mg_solve_stream), a kernel does not.
+namespace {
+__global__ void k_poke(double* dst, PokeWords w, int count) {
+  pdl_entry();
+  if ((int)threadIdx.x < count) dst[threadIdx.x] = w.v[threadIdx.x];
+}
+__global__ void k_peek(double* host_dst, const double* src, int count) {
+  pdl_entry();
+  for (int k = threadIdx.x; k < count; k += blockDim.x) host_dst[k] = src[k];
+  __threadfence_system();
+}
+}  // namespace
+
+int launch_poke(double* dst, const PokeWords& w, int count, cudaStream_t s) {
+  if (count < 0 || count > kPokeWords) return cudaErrorInvalidValue;
+  pdl_launch(k_poke, 1, 32, 0, s, dst, w, count);
+  return check_launch();
+}
+
+int launch_peek(double* host_dst, const double* src, int count, cudaStream_t s) {
+  pdl_launch(k_peek, 1, 256, 0, s, host_dst, src, count);
+  return check_launch();
+}
+
 int launch_restrict(const LevelView& F, const LevelView& C, int dir, const double* r, double* fc,
                     cudaStream_t s) {
   const int64_t total = C.nn * (C.n_t + 1);
