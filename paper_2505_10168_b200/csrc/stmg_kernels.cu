@@ -80,9 +80,20 @@ __device__ __forceinline__ T* opaque(T* p) {
 // family (same box, 1.3e8 DOFs): x-step kernels and the t-step ZX restriction gain
 // 2-6 %, the t-step stored restriction and prolong-sweeps and k_up lose 3-12 %, so those
 // keep the uniform form.  Config-2 solve 65.5 -> 64.2 ms.
+// Unsigned: k * stride wraps at 32 bits and is then scaled to bytes, which the compiler
+// emulates with 64-bit products and masks (~3.7 integer instructions per access in k_up).
+// Signed strides (-DSTMG_SIGNED_STRIDES: overflow undefined, free to widen) were measured
+// per kernel on 1.3e8 DOFs: sweep +1.3 %, ZX prolong-sweep +4 %, ZX restriction +1 %, but
+// pair -7 %, restriction -15 %, k_up -0.7 % -- the address code ptxas emits is erratic
+// either way; unsigned stays (profiles/round2_march_experiment.md).
+#ifdef STMG_SIGNED_STRIDES
+using stride_t = int32_t;
+#else
+using stride_t = uint32_t;
+#endif
 template <bool OPAQUE>
-__device__ __forceinline__ uint32_t stride32(int64_t n) {
-  uint32_t v = (uint32_t)n;
+__device__ __forceinline__ stride_t stride32(int64_t n) {
+  stride_t v = (stride_t)n;
   if (OPAQUE) asm("mov.b32 %0, %0;" : "+r"(v));
   return v;
 }
@@ -292,8 +303,8 @@ struct PlainLoad {
   __device__ __forceinline__ Lane lane(int64_t nbase, int64_t i, int64_t, int) const {
     return {opaque(x + (nbase * nn + i))};
   }
-  __device__ __forceinline__ Raw load(const Lane& l, int r, uint32_t nn32) const {
-    return {__ldg(l.xb + (uint32_t)r * nn32)};
+  __device__ __forceinline__ Raw load(const Lane& l, int r, stride_t nn32) const {
+    return {__ldg(l.xb + (stride_t)r * nn32)};
   }
   __device__ __forceinline__ double finish(const Raw& w, const Lane&, int64_t, double) const { return w.x; }
 };
@@ -318,8 +329,8 @@ struct ZeroLoad {
   __device__ __forceinline__ Lane lane(int64_t nbase, int64_t i, int64_t, int) const {
     return {opaque(f + (nbase * nn + i))};
   }
-  __device__ __forceinline__ Raw load(const Lane& l, int r, uint32_t nn32) const {
-    return {__ldg(l.fb + (uint32_t)r * nn32)};
+  __device__ __forceinline__ Raw load(const Lane& l, int r, stride_t nn32) const {
+    return {__ldg(l.fb + (stride_t)r * nn32)};
   }
   __device__ __forceinline__ double finish(const Raw& w, const Lane&, int64_t, double invd_i) const {
     return zero_sweep(w.f, invd_i, omega);
@@ -361,16 +372,16 @@ struct ProlongOn {
     }
     return l;
   }
-  __device__ __forceinline__ Raw load(const Lane& l, int r, uint32_t nn32) const {
+  __device__ __forceinline__ Raw load(const Lane& l, int r, stride_t nn32) const {
     Raw w;
     w.b = base.load(l.b, r, nn32);
-    const uint32_t nnc32 = stride32<DIR == 0>(nnc);
+    const stride_t nnc32 = stride32<DIR == 0>(nnc);
     if (DIR == 0) {
-      const double* p = l.cb + (uint32_t)r * nnc32;
+      const double* p = l.cb + (stride_t)r * nnc32;
       w.a = __ldg(p);
       w.c = __ldg(p + l.odd);
     } else {
-      w.a = __ldg(l.cb + ((l.odd + (uint32_t)r) >> 1) * nnc32);
+      w.a = __ldg(l.cb + (stride_t)((l.odd + (uint32_t)r) >> 1) * nnc32);
       w.c = 0.0;
     }
     return w;
@@ -445,10 +456,10 @@ __device__ __forceinline__ double dev_lean2(const LevelView& L, const Ld& ld, co
     const EdgeLane e = edge_lane<EDGE>(L, i);
     const int64_t ia = e.ia;
     const bool computes = lane >= 1 && lane <= 30 && e.in_grid;
-    const uint32_t nn32 = stride32<OpaqueStride<Ld>::value>(nn);
+    const stride_t nn32 = stride32<OpaqueStride<Ld>::value>(nn);
     const double* __restrict__ fp = opaque(f + (n0 * nn + ia));
 #pragma unroll
-    for (int k = 0; k < NT; ++k) fv[k] = __ldg(fp + (uint32_t)k * nn32);
+    for (int k = 0; k < NT; ++k) fv[k] = __ldg(fp + (stride_t)k * nn32);
     const typename Ld::Lane lc = ld.lane(nbase, ia, wfirst, lane);
     typename Ld::Raw raw[NT + 1];
 #pragma unroll
@@ -470,7 +481,7 @@ __device__ __forceinline__ double dev_lean2(const LevelView& L, const Ld& ld, co
                              : row_tile<false, EDGE>(L, e.cls, c, qm, x1, qp, pm, xr[k], pp);
       const double r = fv[k] - row;
       if (NORM) acc = acc + (computes ? r * r : 0.0);  // a select: keeps the row out of the store's branch
-      if (MODE != kNormOnly && computes) *(yp + (uint32_t)k * nn32) = MODE == kSweep ? x0 + omega * (r * c.invd) : r;
+      if (MODE != kNormOnly && computes) *(yp + (stride_t)k * nn32) = MODE == kSweep ? x0 + omega * (r * c.invd) : r;
       pm = qm;
       pp = qp;
     }
@@ -577,9 +588,9 @@ __device__ __forceinline__ void dev_lean2x2(const LevelView& L, const double* __
     const double* __restrict__ xb = opaque(x + rowbase);
     const double* __restrict__ fb = opaque(f + rowbase);
     double* __restrict__ yb = opaque(y + rowbase);
-    const uint32_t nn32 = stride32<false>(nn);
-    uint32_t o[NT + 2];
-    o[0] = (uint32_t)e.ia;
+    const stride_t nn32 = stride32<false>(nn);
+    stride_t o[NT + 2];
+    o[0] = (stride_t)e.ia;
 #pragma unroll
     for (int r = 1; r < NT + 2; ++r) o[r] = o[r - 1] + nn32;
     if (ZX) {
@@ -746,10 +757,10 @@ __device__ __forceinline__ double dev_up(const LevelView& L, const Ld& ld, const
     constexpr bool EDGE = decltype(edge_tag)::value;
     const EdgeLane e = edge_lane<EDGE>(L, i);
     const int64_t ia = e.ia;
-    const uint32_t nn32 = stride32<false>(nn);
+    const stride_t nn32 = stride32<false>(nn);
     const double* __restrict__ fb = opaque(f + (s1base * nn + ia));
 #pragma unroll
-    for (int r = 0; r < NT + 1; ++r) fv[r] = __ldg(fb + (uint32_t)r * nn32);  // f rows s1base + r
+    for (int r = 0; r < NT + 1; ++r) fv[r] = __ldg(fb + (stride_t)r * nn32);  // f rows s1base + r
     const typename Ld::Lane lc = ld.lane(sbase, ia, node1 - 1, lane);
     typename Ld::Raw raw[NT + 2];
 #pragma unroll
@@ -769,7 +780,7 @@ __device__ __forceinline__ double dev_up(const LevelView& L, const Ld& ld, const
       if (ADJ) y1[r] = xs[r] + omega * ((fv[r] - row_tile<true, EDGE>(L, e.cls, c, pm, xs[r], pp, qm, x1, qp)) * c.invd);
       else y1[r] = x1 + omega * ((fv[r] - row_tile<false, EDGE>(L, e.cls, c, qm, x1, qp, pm, xs[r], pp)) * c.invd);
       const bool own_row = ADJ ? r < NT : r >= 1;  // rows n0 .. n0 + NT - 1 (compile-time per r)
-      if (own_row && lane2) *(ub + (uint32_t)r * nn32) = y1[r];
+      if (own_row && lane2) *(ub + (stride_t)r * nn32) = y1[r];
       pm = qm;
       pp = qp;
     }
@@ -785,7 +796,7 @@ __device__ __forceinline__ double dev_up(const LevelView& L, const Ld& ld, const
       // cannot be sunk into the divergent branch around the store (BSSY / BRA / BSYNC and
       // a convergence check before the next shuffles, every row: 0.99 -> 0.93 ms)
       acc = acc + (lane2 ? res * res : 0.0);
-      if (lane2) *(wb + (uint32_t)k * nn32) = x0 + omega * (res * c.invd);
+      if (lane2) *(wb + (stride_t)k * nn32) = x0 + omega * (res * c.invd);
       am = bm;
       ap = bp;
     }
@@ -964,16 +975,16 @@ __device__ __forceinline__ double dev_restrict2(const LevelView& F, const LevelV
     const int64_t ia = e.ia;
     const bool own = owns && e.in_grid;
     // 64-bit row bases once per lane, 32-bit element offsets per row
-    const uint32_t nn32 = stride32<DIR == 0 || ZX>(nn), nnc32 = stride32<DIR == 0 || ZX>(nnc);
+    const stride_t nn32 = stride32<DIR == 0 || ZX>(nn), nnc32 = stride32<DIR == 0 || ZX>(nnc);
     const double* __restrict__ fp = opaque(f + (n0 * nn + ia));
 #pragma unroll
-    for (int k = 0; k < NT; ++k) fv[k] = __ldg(fp + (uint32_t)k * nn32);
+    for (int k = 0; k < NT; ++k) fv[k] = __ldg(fp + (stride_t)k * nn32);
     double fx = 0.0;  // ZX: the one staged level outside the f rows
-    if (ZX) fx = ADJ ? __ldg(fp + (uint32_t)NT * nn32) : __ldg(opaque(f + (nbase * nn + ia)));
+    if (ZX) fx = ADJ ? __ldg(fp + (stride_t)NT * nn32) : __ldg(opaque(f + (nbase * nn + ia)));
     if (!ZX) {
       const double* __restrict__ xp = opaque(x + (nbase * nn + ia));
 #pragma unroll
-      for (int r = 0; r <= NT; ++r) xr[r] = __ldg(xp + (uint32_t)r * nn32);
+      for (int r = 0; r <= NT; ++r) xr[r] = __ldg(xp + (stride_t)r * nn32);
     }
     Coefs c = load_coefs(F, ia);
     if (EDGE && e.cls == 1) c.invd = F.inv_w;
@@ -990,7 +1001,7 @@ __device__ __forceinline__ double dev_restrict2(const LevelView& F, const LevelV
 #pragma unroll
       for (int k = 0; k < NT; ++k) {
         acc = acc + (own ? fv[k] * fv[k] : 0.0);
-        if (own && y_open != nullptr) *(yb + (uint32_t)k * nn32) = xr[ADJ ? k : k + 1];  // S(0) on row n0 + k
+        if (own && y_open != nullptr) *(yb + (stride_t)k * nn32) = xr[ADJ ? k : k + 1];  // S(0) on row n0 + k
       }
     }
     // Output lanes and their coarse node: x step, the lanes at even fine nodes
@@ -1014,13 +1025,13 @@ __device__ __forceinline__ double dev_restrict2(const LevelView& F, const LevelV
         const double ra = __shfl_up_sync(kFull, r, 1);
         const double rc = __shfl_down_sync(kFull, r, 1);
         const double v = ((0.5 * ra + 1.0 * r) + 0.5 * rc) + 0.0;
-        if (out) *(fcb + (uint32_t)k * nnc32) = v;
+        if (out) *(fcb + (stride_t)k * nnc32) = v;
       } else {
         if ((k & 1) == 0) {
           r_even = r;
         } else {
           const double v = (0.5 * r_even + 0.5 * r) + 0.0;
-          if (out) *(fcb + (uint32_t)(k >> 1) * nnc32) = v;
+          if (out) *(fcb + (stride_t)(k >> 1) * nnc32) = v;
         }
       }
       pm = qm;
@@ -1187,9 +1198,9 @@ __device__ __forceinline__ double dev_down(const LevelView& F, const LevelView& 
     const double* __restrict__ xb = opaque(x + rowbase);
     const double* __restrict__ fb = opaque(f + rowbase);
     double* __restrict__ yb = opaque(y + rowbase);
-    const uint32_t nn32 = stride32<false>(nn);
-    uint32_t o[NT + 2];
-    o[0] = (uint32_t)i;
+    const stride_t nn32 = stride32<false>(nn);
+    stride_t o[NT + 2];
+    o[0] = (stride_t)i;
 #pragma unroll
     for (int r = 1; r < NT + 2; ++r) o[r] = o[r - 1] + nn32;
 #pragma unroll
@@ -1202,7 +1213,7 @@ __device__ __forceinline__ double dev_down(const LevelView& F, const LevelView& 
     const bool out = DIR == 0 ? ((lane & 1) && lane >= 3 && lane <= 27) : owns;
     const int64_t I = DIR == 0 ? (i >> 1) : i;
     const int64_t crow = DIR == 0 ? n0 : (n0 >> 1);
-    const uint32_t nnc32 = stride32<false>(nnc);
+    const stride_t nnc32 = stride32<false>(nnc);
     double* __restrict__ fcb = opaque(fc + (crow * nnc + I));
     double* __restrict__ xcb = xc0 != nullptr ? opaque(xc0 + (crow * nnc + I)) : nullptr;
     // coarse inverse diagonal at this lane's coarse node (x_c0)
@@ -1245,16 +1256,16 @@ __device__ __forceinline__ double dev_down(const LevelView& F, const LevelView& 
         const double rc = __shfl_down_sync(kFull, r2, 1);
         if (out) {
           const double v = ((0.5 * ra + 1.0 * r2) + 0.5 * rc) + 0.0;
-          *(fcb + (uint32_t)k * nnc32) = v;
-          if (xc0 != nullptr) *(xcb + (uint32_t)k * nnc32) = 0.0 + omega * (v * idc);
+          *(fcb + (stride_t)k * nnc32) = v;
+          if (xc0 != nullptr) *(xcb + (stride_t)k * nnc32) = 0.0 + omega * (v * idc);
         }
       } else {
         if ((k & 1) == 0) {
           r_even = r2;
         } else if (out) {
           const double v = (0.5 * r_even + 0.5 * r2) + 0.0;
-          *(fcb + (uint32_t)(k >> 1) * nnc32) = v;
-          if (xc0 != nullptr) *(xcb + (uint32_t)(k >> 1) * nnc32) = 0.0 + omega * (v * idc);
+          *(fcb + (stride_t)(k >> 1) * nnc32) = v;
+          if (xc0 != nullptr) *(xcb + (stride_t)(k >> 1) * nnc32) = 0.0 + omega * (v * idc);
         }
       }
       am = bm;
