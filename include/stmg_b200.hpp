@@ -118,24 +118,57 @@ class Hierarchy {
   std::shared_ptr<stmg_hierarchy> h_;
 };
 
-// mg_solve: b and u are host or device pointers; u is in/out (warm start).
-inline SolveReport mg_solve(const Hierarchy& h, std::span<const double> b, std::span<double> u,
-                            const SolveOptions& o = {}) {
-  if (b.size() != u.size()) throw std::invalid_argument("mg_solve: vector size mismatch");
-  const stmg_solve_options co{o.nu, o.omega, o.tol, o.div_tol, o.max_cycles};
-  stmg_solve_report r{};
-  std::vector<double> hist(static_cast<size_t>(o.max_cycles > 0 ? o.max_cycles : 0) + 1);
-  check(stmg_mg_solve(h.get(), b.data(), u.data(), &co, &r, hist.data(),
-                      static_cast<int32_t>(hist.size())));
+namespace detail {
+inline SolveReport to_report(const stmg_solve_report& r, const double* hist) {
   SolveReport out;
   out.status = static_cast<SolveStatus>(r.status);
   out.cycles = r.cycles;
   out.factor = r.factor;
-  out.history.assign(hist.begin(), hist.begin() + r.n_history);
+  out.history.assign(hist, hist + r.n_history);
   out.absolute_norms = r.absolute_norms != 0;
   out.seconds = r.seconds;
   out.device_seconds = r.device_seconds;
   out.smoother_dof_updates = r.smoother_dof_updates;
+  return out;
+}
+}  // namespace detail
+
+// mg_solve: b and u are host or device pointers; u is in/out (warm start).  zero_guess: start
+// from zero, u is output only (STMG_SOLVE_ZERO_GUESS; a host u is not uploaded).
+inline SolveReport mg_solve(const Hierarchy& h, std::span<const double> b, std::span<double> u,
+                            const SolveOptions& o = {}, bool zero_guess = false) {
+  if (b.size() != u.size()) throw std::invalid_argument("mg_solve: vector size mismatch");
+  const stmg_solve_options co{o.nu, o.omega, o.tol, o.div_tol, o.max_cycles};
+  stmg_solve_report r{};
+  std::vector<double> hist(static_cast<size_t>(o.max_cycles > 0 ? o.max_cycles : 0) + 1);
+  check(stmg_mg_solve_ex(h.get(), b.data(), u.data(), &co, zero_guess ? STMG_SOLVE_ZERO_GUESS : 0, &r, hist.data(),
+                         static_cast<int32_t>(hist.size())));
+  return detail::to_report(r, hist.data());
+}
+
+// A stream of solves on one hierarchy with host vectors (stmg_mg_solve_stream): entry k is
+// mg_solve(h, bs[k], us[k], o, zero_guess), in order, bit-identical; the upload of entry k + 1 and
+// the download of entry k - 1 overlap solve k when the vectors are page-locked.
+inline std::vector<SolveReport> mg_solve_stream(const Hierarchy& h, std::span<const std::span<const double>> bs,
+                                                std::span<const std::span<double>> us, const SolveOptions& o = {},
+                                                bool zero_guess = false) {
+  if (bs.size() != us.size()) throw std::invalid_argument("mg_solve_stream: bs and us differ in length");
+  const size_t k = bs.size(), cap = static_cast<size_t>(o.max_cycles > 0 ? o.max_cycles : 0) + 1;
+  std::vector<const double*> bp(k);
+  std::vector<double*> up(k), hp(k);
+  std::vector<double> hist(k * cap);
+  for (size_t i = 0; i < k; ++i) {
+    if (bs[i].size() != us[i].size()) throw std::invalid_argument("mg_solve_stream: vector size mismatch");
+    bp[i] = bs[i].data();
+    up[i] = us[i].data();
+    hp[i] = hist.data() + i * cap;
+  }
+  const stmg_solve_options co{o.nu, o.omega, o.tol, o.div_tol, o.max_cycles};
+  std::vector<stmg_solve_report> rs(k);
+  check(stmg_mg_solve_stream(h.get(), static_cast<int32_t>(k), bp.data(), up.data(), &co,
+                             zero_guess ? STMG_SOLVE_ZERO_GUESS : 0, rs.data(), hp.data(), static_cast<int32_t>(cap)));
+  std::vector<SolveReport> out;
+  for (size_t i = 0; i < k; ++i) out.push_back(detail::to_report(rs[i], hp[i]));
   return out;
 }
 
