@@ -115,6 +115,15 @@ def case(name: str) -> Case:
                        adjoint=name.endswith("_adj"))
         cc.dirs = np.asarray([0, 0], np.int32)
         return cc
+    if name.startswith("fixedw_"):  # fixedw_<n_el>[_adj]: see FIXEDW_CASES
+        parts = name.split("_")
+        ne, adjoint = int(parts[1]), parts[-1] == "adj"
+        dirs = [0, 0, 1] if ne <= 4096 else [0, 0]
+        cc = _from_cfg(name, C.cfg1(n_el=ne, n_t=48 if ne <= 4096 else 24), n_levels=len(dirs) + 1,
+                       nu=1, adjoint=adjoint, method="CR")
+        cc.dirs = np.asarray(dirs, np.int32)
+        cc.max_cycles = 6
+        return cc
     if name.startswith("edge_"):  # edge_<x|t>_<n_el>[_adj]: see EDGE_CASES
         parts = name.split("_")
         ne, adjoint = int(parts[2]), parts[-1] == "adj"
@@ -169,6 +178,11 @@ EDGE_CASES = ([f"edge_x_{ne}" + ("_adj" if k % 2 else "") for k, ne in
                enumerate([2, 4, 6, 26, 28, 30, 32, 54, 56, 58, 60, 62, 84, 86, 88, 90])] +
               [f"edge_t_{ne}" + ("" if k % 2 else "_adj") for k, ne in
                enumerate([2, 3, 5, 27, 29, 30, 31, 33, 55, 57, 59, 61, 85, 87, 89, 91])])
+
+# Level widths with compile-time instantiations of the x-step kernels (csrc/stmg_kernels.cu
+# dispatch_width: 16385, 8193, 4097, 2049 nodes): short grids of those widths, run with the
+# large-level tiling (tiles = 8) by the kernel tests.
+FIXEDW_CASES = ["fixedw_4096", "fixedw_4096_adj", "fixedw_16384", "fixedw_16384_adj"]
 
 SMALL_CASES = ["cfg0", "cfg0_deep", "cfg1_mini", "cfg1_mini_adj", "cfg2_mini", "cfg3_mini", "cfgD",
                "cfgK_contrast", "time_first", "space_first", "single_level", "tiny", "wide_short",

@@ -14,7 +14,7 @@ bit-identical to solves with every fusion off.
 import numpy as np
 import pytest
 
-from tests._cases import EDGE_CASES, SMALL_CASES, case
+from tests._cases import EDGE_CASES, FIXEDW_CASES, SMALL_CASES, case
 from tests.test_gpu_parity import bits, check_solve, gpu_hier, port_hier, special_values
 
 pytestmark = pytest.mark.gpu
@@ -41,7 +41,7 @@ def S(torch):
 
 @pytest.mark.parametrize("tiles", [0, 8])
 @pytest.mark.parametrize("omega", [0.5, 0.6])
-@pytest.mark.parametrize("name", KERNEL_CASES + EDGE_CASES)
+@pytest.mark.parametrize("name", KERNEL_CASES + EDGE_CASES + FIXEDW_CASES)
 def test_virtual_zero_kernels_bitwise(torch, S, port, name, omega, tiles):
     """tiles = 8 forces the large-level tiling (8-level tiles; 16-level tiles for the
     x-step restriction of a virtual zero iterate) onto every level."""
@@ -145,7 +145,7 @@ def test_fine_down_kernel_bitwise(torch, S, port, name, tiles):
 
 
 @pytest.mark.parametrize("tiles", [8, 4, 2])
-@pytest.mark.parametrize("name", KERNEL_CASES + ["cfg0", "tiny"] + EDGE_CASES)
+@pytest.mark.parametrize("name", KERNEL_CASES + ["cfg0", "tiny"] + EDGE_CASES + FIXEDW_CASES)
 def test_fine_up_kernel_bitwise(torch, S, port, name, tiles):
     """k_up: u = S(x + P x_c), w = S(u) and ||f - J u||^2 in one pass, against the
     oracle's separate prolongation, sweeps and residual; every level with a per-node
@@ -199,3 +199,34 @@ def test_shared_workspace_alternating_forward_and_adjoint_solves(torch, S, port)
                 rw, uw = want[(adj, k)]
                 assert r.cycles == rw.cycles and r.status == rw.status and r.history[1:] == rw.history[1:]
                 assert np.array_equal(bits(u), bits(uw)), (rnd, adj, k)
+
+
+@pytest.mark.parametrize("zero_guess", [False, True])
+@pytest.mark.parametrize("name", FIXEDW_CASES)
+def test_fixed_width_kernels_in_the_solve(torch, S, port, name, zero_guess):
+    """Levels of 16385 / 8193 / 4097 / 2049 nodes under the large-level tiling run the x-step
+    kernels instantiated for their width (dispatch_width); the same solve under the small-level
+    tiling runs the run-time-width kernels.  Same iterate bit for bit, same history to the
+    norm's summation order; the oracle's solve agrees to the rounding of the (very wide)
+    coarsest level's exact solve."""
+    cs = case(name)
+    b = cs.rhs_vector(port)
+    opts = S.SolveOptions(nu=cs.nu, tol=cs.tol, max_cycles=cs.max_cycles)
+    out = []
+    for big in (True, False):
+        h = gpu_hier(S, cs, port)
+        if big:
+            h.set_tiling(small_dofs=1, tiny_dofs=1)
+        u = np.zeros_like(b)
+        out.append((S.mg_solve(h, b, u, opts, zero_guess=zero_guess), u))
+    (r0, u0), (r1, u1) = out
+    assert r0.cycles == r1.cycles and r0.status == r1.status
+    np.testing.assert_allclose(r0.history, r1.history, rtol=1e-13, atol=0)
+    assert np.array_equal(bits(u0), bits(u1))
+    if cs.n_el > 4096:
+        return  # a 4097-node coarsest level: the two exact coarsest solvers differ by cond x eps ~ 1e-4 there
+    hp = port_hier(port, cs)
+    u_p, rep_p = hp.solve(b, nu=cs.nu, tol=cs.tol, max_cycles=cs.max_cycles)
+    assert r0.cycles == rep_p.cycles and int(r0.status) == rep_p.status
+    np.testing.assert_allclose(r0.history, rep_p.history, rtol=1e-7, atol=0)
+    assert np.max(np.abs(u0 - u_p)) <= 1e-7 * np.max(np.abs(u_p))

@@ -8,7 +8,7 @@ floor of evaluating b - J u), and fields within 1e-10 relative max-norm.
 import numpy as np
 import pytest
 
-from tests._cases import EDGE_CASES, SMALL_CASES, case
+from tests._cases import EDGE_CASES, FIXEDW_CASES, SMALL_CASES, case
 
 pytestmark = pytest.mark.gpu
 
@@ -63,7 +63,7 @@ def special_values(rng, n):
 
 
 @pytest.mark.parametrize("tiles", [0, 8])
-@pytest.mark.parametrize("name", SMALL_CASES + EDGE_CASES)
+@pytest.mark.parametrize("name", SMALL_CASES + EDGE_CASES + FIXEDW_CASES)
 def test_level_kernels_bitwise(torch, S, port, name, tiles):
     """tiles = 8 forces the large-level tiling (8-level tiles, 16-level tiles for the
     x-step restrictions) onto every level of the small cases."""
@@ -99,6 +99,8 @@ def test_level_kernels_bitwise(torch, S, port, name, tiles):
             xp = xt.clone()
             h.prolong_add(l, torch.from_numpy(xc).to(dev), xp)
             assert np.array_equal(bits(xp), bits(hp.prolong_add(l, xc, x))), f"prolong level {l}"
+    if name.startswith("fixedw_"):
+        return  # their coarsest levels are thousands of nodes wide: two exact solvers differ by cond x eps there
     # exact coarsest solve (PCR march vs Thomas march): rounding-level agreement
     nL = hp.ndofs(hp.n_levels - 1)
     f = rng.standard_normal(nL)
