@@ -2057,14 +2057,15 @@ inline unsigned flat_grid(int64_t total) { return (unsigned)((total + kFlatBlock
 
 // Compile-time level widths (fine_stride): fn(std::integral_constant<int, NNW>) with NNW the
 // level's nodes per time level when an instantiation exists for it, else 0 (run-time width).
-template <class Fn>
+// MINW: the smallest width instantiated for the caller's kernel (the level-0-only kernels skip 2049).
+template <int MINW = 2049, class Fn>
 inline void dispatch_width(const LevelView& F, const LevelView& C, Fn&& fn) {
-  const int64_t nn = C.nn == (F.nn + 1) / 2 ? F.nn : 0;  // an x step halves the elements
+  const int64_t nn = (C.nn == (F.nn + 1) / 2 && F.nn >= MINW) ? F.nn : 0;  // an x step halves the elements
   switch (nn) {
     case 16385: fn(std::integral_constant<int, 16385>{}); break;
     case 8193: fn(std::integral_constant<int, 8193>{}); break;
     case 4097: fn(std::integral_constant<int, 4097>{}); break;
-    case 2049: fn(std::integral_constant<int, 2049>{}); break;
+    case 2049: fn(std::integral_constant<int, MINW <= 2049 ? 2049 : 0>{}); break;
     default: fn(std::integral_constant<int, 0>{});
   }
 }
@@ -2193,7 +2194,7 @@ void restrict_open_launch(const LevelView& F, const LevelView& C, const double* 
   restrict_open_geometry<DIR>(F, C, &blk, &grd, &nt);
   if (nt == 16) {
     if (DIR == 0)
-      dispatch_width(F, C, [&](auto w) {
+      dispatch_width<4097>(F, C, [&](auto w) {
         pdl_launch(k_restrict_open<ADJ, 0, 16, 3, DIR == 0 ? decltype(w)::value : 0>, grd, blk, 0, s, F, C, f, fc, xc0,
                    y, omega, partials);
       });
@@ -2328,7 +2329,7 @@ void up_launch(const LevelView& L, const LevelView& C, const double* f, const do
     else if (lean_nt(L) == 4)
       pdl_launch(k_up<ADJ, 4, ProlongZeroLoad<DIR>>, grd, blk, 0, s, L, lz, f, u_out, w_ind, x_ind, omega, partials);
     else
-      dispatch_width(L, C, [&](auto w) {
+      dispatch_width<4097>(L, C, [&](auto w) {
         pdl_launch(k_up<ADJ, 8, ProlongZeroLoad<DIR>, up_minb<8>(), DIR == 0 ? decltype(w)::value : 0>, grd, blk, 0, s, L,
                    lz, f, u_out, w_ind, x_ind, omega, partials);
       });
@@ -2340,7 +2341,7 @@ void up_launch(const LevelView& L, const LevelView& C, const double* f, const do
   else if (lean_nt(L) == 4)
     pdl_launch(k_up<ADJ, 4, ProlongLoad<DIR>>, grd, blk, 0, s, L, ld, f, u_out, w_ind, x_ind, omega, partials);
   else  // 8-level tiles: 6 / 10 levels measured slower (1.05 / 0.99 vs 0.94 ms on 1.3e8 DOFs)
-    dispatch_width(L, C, [&](auto w) {
+    dispatch_width<4097>(L, C, [&](auto w) {
       pdl_launch(k_up<ADJ, 8, ProlongLoad<DIR>, up_minb<8>(), DIR == 0 ? decltype(w)::value : 0>, grd, blk, 0, s, L, ld,
                  f, u_out, w_ind, x_ind, omega, partials);
     });
