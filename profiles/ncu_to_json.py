@@ -13,15 +13,15 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KEYS = {  # demangled-name fragment -> bench.py kernel key
-    "k_lean2<0, 0, 1, 8, 3, unnamed>::PlainLoad>": "fine_norm_pass",
-    "k_lean2<0, 0, 0, 8, 3, unnamed>::PlainLoad>": "fine_sweep",
-    "k_lean2x2<0, 8, 3, 0>": "fine_sweep_pair",
-    "k_restrict2<0, 0, 8, 3, 0>": "fine_restrict",
-    "k_restrict2<0, 0, 16, 2, 0>": "fine_restrict",
-    "k_restrict2<0, 0, 16, 3, 1>": "zero_restrict",
-    "k_lean2<0, 0, 0, 8, 4, unnamed>::ProlongOn<0, unnamed>::ZeroLoad>>": "zero_prolong_sweep",
-    "k_lean2<0, 0, 0, 8, 3, unnamed>::ProlongOn<0, unnamed>::PlainLoad>>": "fine_prolong_sweep",
+KEYS = {  # demangled-name prefix -> bench.py kernel key (a trailing level-width parameter may follow)
+    "k_lean2<0, 0, 1, 8, 3, unnamed>::PlainLoad": "fine_norm_pass",
+    "k_lean2<0, 0, 0, 8, 3, unnamed>::PlainLoad": "fine_sweep",
+    "k_lean2x2<0, 8, 3, 0": "fine_sweep_pair",
+    "k_restrict2<0, 0, 8, 3, 0": "fine_restrict",
+    "k_restrict2<0, 0, 16, 2, 0": "fine_restrict",
+    "k_restrict2<0, 0, 16, 3, 1": "zero_restrict",
+    "k_lean2<0, 0, 0, 8, 4, unnamed>::ProlongOn<0, unnamed>::ZeroLoad>": "zero_prolong_sweep",
+    "k_lean2<0, 0, 0, 8, 3, unnamed>::ProlongOn<0, unnamed>::PlainLoad>": "fine_prolong_sweep",
     "k_up<0, 8, unnamed>::ProlongOn<0, unnamed>::PlainLoad>": "fine_up",
 }
 METRICS = "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum"
