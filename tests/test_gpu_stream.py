@@ -113,3 +113,27 @@ def test_stream_argument_errors(torch, S, port):
         S.mg_solve_stream(h, [b[:-1], b], [np.zeros_like(b), np.zeros_like(b)], S.SolveOptions())
     with pytest.raises(ValueError):  # the solve's own option checks apply to every entry
         S.mg_solve_stream(h, [b, b], [np.zeros_like(b), np.zeros_like(b)], S.SolveOptions(omega=-1.0))
+
+
+def test_stream_on_a_hierarchy_and_its_transpose_sharing_one_workspace(torch, S, port):
+    """The staging slots live in the workspace a hierarchy shares with its transpose: streams
+    on J and on J^T alternate over the same slots, with a release in between."""
+    cs = case("cfg1_mini")
+    h = build(S, cs, port)
+    ht = S.transposed_hierarchy(h)
+    bs = rhs_family(cs.rhs_vector(port), 3)
+    opts = S.SolveOptions(nu=1, tol=1e-10, max_cycles=8)
+    want = {}
+    for name, hh in (("J", h), ("JT", ht)):
+        want[name] = []
+        for b in bs:
+            u = np.zeros_like(b)
+            want[name].append((S.mg_solve(hh, b, u, opts, zero_guess=True), u))
+    pb = [torch.from_numpy(b).pin_memory() for b in bs]
+    for round_ in range(2):
+        for name, hh in (("J", h), ("JT", ht)):
+            pu = [torch.full((b.size,), float("nan"), dtype=torch.float64).pin_memory() for b in bs]
+            reps = S.mg_solve_stream(hh, pb, pu, opts, zero_guess=True)
+            for (r1, u1), r2, u2 in zip(want[name], reps, pu):
+                assert r1.history == r2.history and np.array_equal(u1, u2.numpy()), (round_, name)
+        h.release_staging()
