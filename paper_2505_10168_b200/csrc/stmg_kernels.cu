@@ -894,7 +894,12 @@ __device__ __forceinline__ double dev_up(const LevelView& L, const Ld& ld, const
 // 0.99 vs 1.05 ms on 1.3e8 DOFs, config-2 solve 69.4 vs 70.7 ms; register caps of 96 /
 // 104 (__maxnreg__) are slower still (1.00 / 1.09 vs 0.94 ms).
 template <int NT>
-constexpr int up_minb() { return NT <= 2 ? 4 : NT <= 4 ? 3 : 2; }
+// (with compile-time widths the 80-register build spills only ~50 B, but still measures
+// 0.881 vs 0.873 ms, config 2 60.6 vs 60.3 ms)
+#ifndef STMG_UP_MINB8
+#define STMG_UP_MINB8 2
+#endif
+constexpr int up_minb() { return NT <= 2 ? 4 : NT <= 4 ? 3 : STMG_UP_MINB8; }
 
 // x_ind: optional device-resident pointer to the input iterate (overrides the
 // loader's x): the solve loop alternates the speculative iterate between two
